@@ -1,0 +1,144 @@
+"""Seeded synthetic stand-ins for BASELINE.json's five configurations.
+
+The paper measured on a subset of SPE10, which is not in this container;
+the BASELINE configs are self-contained synthetic problems.
+Every array is generated from ``numpy.random.default_rng(seed)`` with the
+seeds below, and fed identically to the CPU oracle and to the GPU path.
+
+Unit convention: permeabilities are passed normalised by
+1e-13 m^2 (geometric mean 1), with gamma = 1 and the reference's default
+alpha, beta, phi; "one backward-Euler step" uses dt = 1 and p_prev = 0.
+
+Mapping of the restriction techniques:
+  config 1 -> base pattern          (Q = column pattern of A_cf^T)
+  config 2 -> static prototype "A"  (first technique, the config default)
+  config 3 -> dynamic (n_add=1, n_ent=4) (second technique)
+  configs 4/5 inherit config 2's static "A".
+Inner solves everywhere: IC(0)/ILU(0) (``no_fill=True``, drop tol 0; D5).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import assembly, mesh
+
+SEEDS = {1: 1001, 2: 1002, 3: 1003, 4: 1004, 5: 1002}
+
+
+@dataclass
+class CaseSpec:
+    name: str
+    system: object
+    precond: dict
+    rtol: float = 1e-8
+    restart: int = 50
+    max_it: int = 2000
+    meta: dict = field(default_factory=dict)
+
+
+def _inner():
+    return dict(face_drop_tol=0.0, schur_drop_tol=0.0, no_fill=True)
+
+
+def lognormal_aniso_field(n_cells, seed, sigma=2.0, kv_kh=0.1):
+    rng = np.random.default_rng(seed)
+    k = np.exp(rng.normal(0.0, sigma, size=n_cells))
+    return mesh.Conductivity.diagonal(k, k, kv_kh * k)
+
+
+def rotated_tensor_field(n_cells, seed, sigma=1.5):
+    """K = R diag(lambda) R^T, lambda_i = exp(N(0, sigma)), R a seeded proper
+    rotation (QR of a Gaussian matrix, signs fixed so det R = +1)."""
+    rng = np.random.default_rng(seed)
+    lam = np.exp(rng.normal(0.0, sigma, size=(n_cells, 3)))
+    Q, R = np.linalg.qr(rng.standard_normal((n_cells, 3, 3)))
+    Q = Q * np.sign(np.diagonal(R, axis1=1, axis2=2))[:, None, :]
+    flip = np.linalg.det(Q) < 0
+    Q[flip, :, 0] *= -1.0
+    K = np.einsum("nab,nb,ncb->nac", Q, lam, Q)
+    return mesh.Conductivity(0.5 * (K + K.transpose(0, 2, 1)))
+
+
+def config1(n=16):
+    g = mesh.box_grid(n, n, n, 1.0 / n, 1.0 / n, 1.0 / n)
+    fld = mesh.Conductivity.homogeneous(g.n_elems, 1.0)
+    bc = mesh.Boundaries(pressure_planes={"x-": 1.0, "x+": 0.0})
+    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=1.0,
+                          p_prev=np.zeros(g.n_elems))
+    return CaseSpec(f"config1-{n}^3-base", s, dict(pattern="base", **_inner()))
+
+
+def config2(n=64, seed=SEEDS[2], length=1000.0):
+    h = length / n
+    g = mesh.box_grid(n, n, n, h, h, h)
+    fld = lognormal_aniso_field(g.n_elems, seed)
+    bc = mesh.Boundaries(pressure_planes={"x-": 1.0, "x+": 0.0})
+    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=1.0,
+                          p_prev=np.zeros(g.n_elems))
+    return CaseSpec(f"config2-{n}^3-staticA", s,
+                    dict(pattern="static", prototype="A", **_inner()))
+
+
+def config3(n=128, seed=SEEDS[3]):
+    g = mesh.box_grid(n, n, n, 1.0 / n, 1.0 / n, 1.0 / n)
+    g = mesh.perturb_interior(g, 0.2, seed)
+    fld = rotated_tensor_field(g.n_elems, seed + 1)
+    bc = mesh.Boundaries(wells=[(0, 0, 1.0), (n - 1, n - 1, 0.0)])
+    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=1.0,
+                          p_prev=np.zeros(g.n_elems))
+    return CaseSpec(f"config3-{n}^3-dynamic14", s,
+                    dict(pattern="dynamic", n_add=1, n_ent=4, **_inner()))
+
+
+def channelised_field(nx, ny, nz, seed, sigma=2.5, kv_kh=0.1, n_channel_layers=None):
+    """Layered log-normal background plus high-K sinuous channels in the top
+    layers (k x 1e3 inside y0 + a sin(2 pi x / lambda + phi) bands)."""
+    rng = np.random.default_rng(seed)
+    mu = rng.normal(0.0, 1.5, size=nz)
+    lnk = mu[:, None, None] + rng.normal(0.0, sigma, size=(nz, ny, nx))
+    top = n_channel_layers if n_channel_layers is not None else max(1, nz // 2)
+    x = np.arange(nx)[None, :]
+    y = np.arange(ny)[:, None]
+    for k in range(nz - top, nz):
+        for _ in range(3):
+            y0 = rng.uniform(0, ny)
+            a = rng.uniform(0.05, 0.15) * ny
+            lam = rng.uniform(0.5, 1.5) * nx
+            ph = rng.uniform(0, 2 * np.pi)
+            width = rng.uniform(0.02, 0.05) * ny
+            band = np.abs(y - (y0 + a * np.sin(2 * np.pi * x / lam + ph))) < width
+            lnk[k][band] += np.log(1e3)
+    k = np.exp(lnk).ravel()
+    return mesh.Conductivity.diagonal(k, k, kv_kh * k)
+
+
+def config4(nx=60, ny=220, nz=85, seed=SEEDS[4], dt=0.1):
+    g = mesh.box_grid(nx, ny, nz, 6.1, 3.05, 0.61)
+    fld = channelised_field(nx, ny, nz, seed)
+    bc = mesh.Boundaries(wells=[(0, 0, 200.0), (nx - 1, 0, 200.0),
+                                (0, ny - 1, 200.0), (nx - 1, ny - 1, 200.0),
+                                (nx // 2, ny // 2, 100.0)])
+    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=dt,
+                          p_prev=np.full(g.n_elems, 140.0))
+    return CaseSpec(f"config4-{nx}x{ny}x{nz}-staticA-transient", s,
+                    dict(pattern="static", prototype="A", **_inner()),
+                    meta=dict(p_init=140.0, n_steps=10, dt0=dt, dt_max=5.0,
+                              dt_mult=1.1, dp_target=5.0))
+
+
+def config5(n=256, seed=SEEDS[5]):
+    c = config2(n=n, seed=seed)
+    c.name = f"config5-{n}^3-staticA"
+    return c
+
+
+def make(idx: int, **kw) -> CaseSpec:
+    return {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}[idx](**kw)
+
+
+def steady_equivalent(system):
+    return assembly.update_accumulation(system, math.inf)
