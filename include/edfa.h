@@ -1,0 +1,213 @@
+/*
+ * edfa.h -- C ABI of libedfa.so, the B200 (sm_100a) implementation of the
+ * EDFA block preconditioner and the Krylov solves it accelerates.
+ *
+ * The entry points replace the reference's hot-path Python API
+ * (hexflow 0.1.0, paths relative to /root/reference/pkg/src/hexflow):
+ *
+ *   edfa_csr_create / edfa_csr_export     scipy CSR blocks of BlockSystem
+ *                                         (assembly.py:135-183, sparse.py:28-34)
+ *   edfa_system_create                    BlockSystem.full_matrix (assembly.py:168-170)
+ *   edfa_pattern_static                   patterns.static_patterns (patterns.py:124-133)
+ *   edfa_stage1_build                     precond.build_stage1 (precond.py:204-261)
+ *   edfa_stage2_build                     precond.build_stage2 (precond.py:264-271)
+ *   edfa_precond_apply                    BlockLDUPreconditioner.apply (precond.py:311-320)
+ *   edfa_inner_apply                      InnerFactorization.apply (sparse.py:125-129)
+ *   edfa_restricted_solve                 precond.solve_restricted_row (precond.py:70-82)
+ *   edfa_grow_dynamic                     precond.grow_pattern_dynamic (precond.py:107-135)
+ *   edfa_spmv / edfa_system_spmv          sparse.spmv (sparse.py:37-42), A @ v (driver.py:135-139)
+ *   edfa_bicgstab                         krylov.bicgstab (krylov.py:40-115)
+ *   edfa_gmres                            GMRES(m) -- absent from the reference
+ *
+ * Conventions
+ *   - Every call is stream-ordered on the context's stream.  Calls that must
+ *     learn a data-dependent size (stage builds, exports of sizes) or a
+ *     convergence decision synchronise that stream; nothing else does.
+ *   - Vectors passed to apply/spmv/solve entry points are DEVICE pointers.
+ *     Matrix uploads/exports take a memory-space flag (host or device).
+ *   - Return value: EDFA_OK or an error code; edfa_last_error() returns the
+ *     message of the calling thread's last failure.  Error codes map onto the
+ *     reference's exceptions: VALUE -> ValueError, FACTORIZATION ->
+ *     FactorizationError (hx/errors.py:16), STATE -> RuntimeError.
+ *   - Indices are int32 (row pointers and column ids), values IEEE float64.
+ */
+#ifndef EDFA_H
+#define EDFA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EDFA_ABI_VERSION 1
+
+enum edfa_status {
+    EDFA_OK = 0,
+    EDFA_ERR_VALUE = 1,          /* invalid argument        -> ValueError          */
+    EDFA_ERR_FACTORIZATION = 2,  /* non-SPD restricted block -> FactorizationError  */
+    EDFA_ERR_STATE = 3,          /* apply before stage 2    -> RuntimeError        */
+    EDFA_ERR_CUDA = 4,           /* CUDA runtime failure                            */
+    EDFA_ERR_UNSUPPORTED = 5     /* option not implemented on this path            */
+};
+
+enum edfa_filtration {           /* precond.FILTRATION_MODES (precond.py:35) */
+    EDFA_FILT_NONE = 0,
+    EDFA_FILT_PRE = 1,
+    EDFA_FILT_POST_SCHUR = 2,
+    EDFA_FILT_POST_PRODUCT = 3
+};
+
+enum edfa_mem { EDFA_MEM_HOST = 0, EDFA_MEM_DEVICE = 1 };
+
+enum edfa_stage1_part {          /* Stage1 fields (precond.py:168-176) */
+    EDFA_S1_G = 0,               /* G~, cells x faces                          */
+    EDFA_S1_FT = 1,              /* F~^T, cells x faces (CSR of F~'s columns)  */
+    EDFA_S1_H = 2,               /* H~ = G~ A_ff F~, cells x cells             */
+    EDFA_S1_Q = 3,               /* restriction sets (values NULL)             */
+    EDFA_S1_L = 4,               /* IC factor L of -A_ff, explicit diagonal    */
+    EDFA_S1_F = 5                /* F~, faces x cells                          */
+};
+
+enum edfa_stage2_part {          /* Stage2 fields (precond.py:179-184) */
+    EDFA_S2_S = 0,               /* S~ = A_cc - H~                             */
+    EDFA_S2_L = 1,               /* unit lower ILU factor, explicit diagonal   */
+    EDFA_S2_U = 2                /* upper ILU factor, diagonal first           */
+};
+
+typedef struct edfa_ctx edfa_ctx;
+typedef struct edfa_csr edfa_csr;
+typedef struct edfa_system edfa_system;
+typedef struct edfa_stage1 edfa_stage1;
+typedef struct edfa_stage2 edfa_stage2;
+
+typedef struct edfa_dynamic {    /* precond.DynamicConfig (precond.py:38-67) */
+    int32_t n_add;
+    int32_t n_ent;
+    int32_t it_max;              /* <= 0 means "None" (sweep limit max(n_ent,1)) */
+} edfa_dynamic;
+
+typedef struct edfa_stage1_info {
+    int64_t nnz_G, nnz_FT, nnz_H, nnz_Q, nnz_L;
+    int32_t max_pattern;
+    int32_t pivot_shifts;        /* InnerFactorization.pivot_shifts of the IC */
+    int32_t trsv_levels;         /* dependency depth of L (and L^T)           */
+} edfa_stage1_info;
+
+typedef struct edfa_stage2_info {
+    int64_t nnz_S, nnz_L, nnz_U; /* L, U counted like the reference's CSR     */
+    int32_t pivot_shifts;
+    int32_t levels_L, levels_U;
+} edfa_stage2_info;
+
+typedef struct edfa_report {     /* krylov.SolveReport (krylov.py:15-37) */
+    int32_t n_it;
+    int32_t converged;
+    int32_t breakdown;
+    int32_t n_hist;              /* entries written to the history buffer      */
+    double final_relres;         /* ||b - A x|| / ||b|| recomputed at the end  */
+} edfa_report;
+
+/* ---- library / context ------------------------------------------------- */
+int         edfa_abi_version(void);
+const char* edfa_last_error(void);
+int edfa_ctx_create(int device, void* cuda_stream, edfa_ctx** out);
+int edfa_ctx_set_stream(edfa_ctx* ctx, void* cuda_stream);
+int edfa_ctx_sync(edfa_ctx* ctx);
+int edfa_ctx_destroy(edfa_ctx* ctx);
+/* Per-kernel CUDA-event timing with algorithmic byte counts (roofline). */
+int edfa_ctx_profile(edfa_ctx* ctx, int enable);
+/* JSON {"kernel": {"launches": n, "ms": t, "bytes": b}, ...}; returns needed length. */
+int64_t edfa_ctx_profile_report(edfa_ctx* ctx, char* buf, int64_t cap, int reset);
+/* Number of library kernel launches issued so far on this context. */
+int64_t edfa_ctx_launch_count(edfa_ctx* ctx);
+
+/* ---- matrices ---------------------------------------------------------- */
+int edfa_csr_create(edfa_ctx* ctx, int32_t n_rows, int32_t n_cols, int64_t nnz,
+                    const int32_t* indptr, const int32_t* indices, const double* data,
+                    int mem, edfa_csr** out);
+int edfa_csr_info(const edfa_csr* A, int32_t* n_rows, int32_t* n_cols, int64_t* nnz);
+int edfa_csr_export(edfa_ctx* ctx, const edfa_csr* A, int32_t* indptr, int32_t* indices,
+                    double* data, int mem);
+int edfa_csr_destroy(edfa_csr* A);
+
+/* ---- block system ------------------------------------------------------ */
+/* Borrows the four blocks (they must outlive the system); builds the
+ * monolithic [[A_ff, A_fc], [A_cf, A_cc]] operator on the device. */
+int edfa_system_create(edfa_ctx* ctx, const edfa_csr* A_ff, const edfa_csr* A_fc,
+                       const edfa_csr* A_cf, const edfa_csr* A_cc, edfa_system** out);
+/* update_accumulation: replace A_cc (face blocks untouched; assembly.py:314-333). */
+int edfa_system_set_cc(edfa_ctx* ctx, edfa_system* sys, const edfa_csr* A_cc);
+int edfa_system_destroy(edfa_system* sys);
+
+/* ---- restriction patterns ---------------------------------------------- */
+/* Static prototype 'A'..'E' (patterns.py:63-133).  elem_to_faces and
+ * neighbors are n_cells x 6 (global face ids / neighbour cell or -1);
+ * face_index maps global -> free face (-1 eliminated). */
+int edfa_pattern_static(edfa_ctx* ctx, int32_t n_cells, int32_t n_faces,
+                        const int32_t* elem_to_faces, const int32_t* neighbors,
+                        const int32_t* face_index, char prototype, int mem,
+                        edfa_csr** out);
+
+/* ---- EDFA stage 1 / stage 2 -------------------------------------------- */
+/* Exactly one of pattern (base/static sets as a CSR pattern over faces) or
+ * dyn must be non-NULL (precond.py:217-218). */
+int edfa_stage1_build(edfa_ctx* ctx, const edfa_system* sys, const edfa_csr* pattern,
+                      const edfa_dynamic* dyn, double tau_filt, int filtration,
+                      double face_drop_tol, int no_fill, edfa_stage1** out);
+int edfa_stage1_info_get(const edfa_stage1* s1, edfa_stage1_info* info);
+/* Materialises (lazily) and returns a borrowed handle to one part. */
+int edfa_stage1_part(edfa_ctx* ctx, edfa_stage1* s1, int part, const edfa_csr** out);
+int edfa_stage1_destroy(edfa_stage1* s1);
+
+int edfa_stage2_build(edfa_ctx* ctx, const edfa_csr* A_cc, const edfa_stage1* s1,
+                      double tau_filt, int filtration, double schur_drop_tol,
+                      int no_fill, edfa_stage2** out);
+int edfa_stage2_info_get(const edfa_stage2* s2, edfa_stage2_info* info);
+int edfa_stage2_part(edfa_ctx* ctx, edfa_stage2* s2, int part, const edfa_csr** out);
+int edfa_stage2_destroy(edfa_stage2* s2);
+
+/* ---- application and products (device vectors) ------------------------ */
+/* y = P^-1 r, block-triangular factored inverse; s2 == NULL -> EDFA_ERR_STATE. */
+int edfa_precond_apply(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1* s1,
+                       const edfa_stage2* s2, const double* r, double* y);
+/* which = 0: face inner (L L^T)^-1 of -A_ff;  which = 1: Schur inner (L U)^-1. */
+int edfa_inner_apply(edfa_ctx* ctx, const edfa_stage1* s1, const edfa_stage2* s2,
+                     int which, const double* r, double* y);
+/* y = alpha * A x + beta * y */
+int edfa_spmv(edfa_ctx* ctx, const edfa_csr* A, const double* x, double* y,
+              double alpha, double beta);
+int edfa_system_spmv(edfa_ctx* ctx, const edfa_system* sys, const double* x, double* y);
+
+/* ---- single-row kernels (precond.py:70-135), results on the host --------- */
+/* x (length |idx|) solving -A_ff[idx,idx] x = rhs[idx]; rhs_idx/rhs_val sparse. */
+int edfa_restricted_solve(edfa_ctx* ctx, const edfa_csr* A_ff, int32_t n_rhs,
+                          const int32_t* rhs_idx, const double* rhs_val, int32_t n_idx,
+                          const int32_t* idx, double* x_out);
+/* Grow one set from the rhs pattern; idx_out (cap entries) and x_out receive
+ * the final set / solution, *n_out its size. */
+int edfa_grow_dynamic(edfa_ctx* ctx, const edfa_csr* A_ff, int32_t n_rhs,
+                      const int32_t* rhs_idx, const double* rhs_val,
+                      const edfa_dynamic* dyn, int32_t cap, int32_t* idx_out,
+                      double* x_out, int32_t* n_out);
+
+/* ---- Krylov solves (device vectors b, x; host history buffer) ------------ */
+/* Right-preconditioned restarted GMRES(restart), x0 = 0, stop on the true
+ * residual ||b - A x|| / ||b|| <= rtol.  s1/s2 NULL -> unpreconditioned. */
+int edfa_gmres(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1* s1,
+               const edfa_stage2* s2, const double* b, double* x, double rtol,
+               int32_t restart, int32_t max_it, edfa_report* rep, double* hist,
+               int32_t hist_cap);
+/* Right-preconditioned Bi-CGStab exactly as krylov.bicgstab (krylov.py:40-115). */
+int edfa_bicgstab(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1* s1,
+                  const edfa_stage2* s2, const double* b, double* x, double rtol,
+                  int32_t max_it, edfa_report* rep, double* hist, int32_t hist_cap);
+
+/* ---- BLAS-1 helpers on device vectors (generic-callable Krylov paths) --- */
+int edfa_dot(edfa_ctx* ctx, int64_t n, const double* x, const double* y, double* out_host);
+int edfa_axpby(edfa_ctx* ctx, int64_t n, double a, const double* x, double b, double* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EDFA_H */

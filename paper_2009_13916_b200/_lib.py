@@ -1,0 +1,130 @@
+"""ctypes binding of libedfa.so (include/edfa.h).
+
+The shared library is built in-tree (``paper_2009_13916_b200/libedfa.so``) by
+``__graft_entry__.build()``.  Loading fails loudly when it is missing: there
+is no CPU or PyTorch fallback for any EDFA operation.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import pathlib
+
+from .errors import FactorizationError
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "libedfa.so"
+
+OK, ERR_VALUE, ERR_FACTORIZATION, ERR_STATE, ERR_CUDA, ERR_UNSUPPORTED = range(6)
+FILTRATION = {"none": 0, "pre": 1, "post-schur": 2, "post-product": 3}
+MEM_HOST, MEM_DEVICE = 0, 1
+S1_G, S1_FT, S1_H, S1_Q, S1_L, S1_F = range(6)
+S2_S, S2_L, S2_U = range(3)
+
+vp = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+f64 = C.c_double
+P_i32 = C.POINTER(C.c_int32)
+
+
+class Dynamic(C.Structure):
+    _fields_ = [("n_add", i32), ("n_ent", i32), ("it_max", i32)]
+
+
+class Stage1Info(C.Structure):
+    _fields_ = [("nnz_G", i64), ("nnz_FT", i64), ("nnz_H", i64), ("nnz_Q", i64), ("nnz_L", i64),
+                ("max_pattern", i32), ("pivot_shifts", i32), ("trsv_levels", i32)]
+
+
+class Stage2Info(C.Structure):
+    _fields_ = [("nnz_S", i64), ("nnz_L", i64), ("nnz_U", i64), ("pivot_shifts", i32),
+                ("levels_L", i32), ("levels_U", i32)]
+
+
+class Report(C.Structure):
+    _fields_ = [("n_it", i32), ("converged", i32), ("breakdown", i32), ("n_hist", i32),
+                ("final_relres", f64)]
+
+
+_SIGS = {
+    "edfa_abi_version": (i32, []),
+    "edfa_last_error": (C.c_char_p, []),
+    "edfa_ctx_create": (i32, [i32, vp, C.POINTER(vp)]),
+    "edfa_ctx_set_stream": (i32, [vp, vp]),
+    "edfa_ctx_sync": (i32, [vp]),
+    "edfa_ctx_destroy": (i32, [vp]),
+    "edfa_ctx_profile": (i32, [vp, i32]),
+    "edfa_ctx_profile_report": (i64, [vp, C.c_char_p, i64, i32]),
+    "edfa_ctx_launch_count": (i64, [vp]),
+    "edfa_csr_create": (i32, [vp, i32, i32, i64, vp, vp, vp, i32, C.POINTER(vp)]),
+    "edfa_csr_info": (i32, [vp, P_i32, P_i32, C.POINTER(i64)]),
+    "edfa_csr_export": (i32, [vp, vp, vp, vp, vp, i32]),
+    "edfa_csr_destroy": (i32, [vp]),
+    "edfa_system_create": (i32, [vp, vp, vp, vp, vp, C.POINTER(vp)]),
+    "edfa_system_set_cc": (i32, [vp, vp, vp]),
+    "edfa_system_destroy": (i32, [vp]),
+    "edfa_pattern_static": (i32, [vp, i32, i32, vp, vp, vp, C.c_char, i32, C.POINTER(vp)]),
+    "edfa_stage1_build": (i32, [vp, vp, vp, C.POINTER(Dynamic), f64, i32, f64, i32, C.POINTER(vp)]),
+    "edfa_stage1_info_get": (i32, [vp, C.POINTER(Stage1Info)]),
+    "edfa_stage1_part": (i32, [vp, vp, i32, C.POINTER(vp)]),
+    "edfa_stage1_destroy": (i32, [vp]),
+    "edfa_stage2_build": (i32, [vp, vp, vp, f64, i32, f64, i32, C.POINTER(vp)]),
+    "edfa_stage2_info_get": (i32, [vp, C.POINTER(Stage2Info)]),
+    "edfa_stage2_part": (i32, [vp, vp, i32, C.POINTER(vp)]),
+    "edfa_stage2_destroy": (i32, [vp]),
+    "edfa_precond_apply": (i32, [vp, vp, vp, vp, vp, vp]),
+    "edfa_inner_apply": (i32, [vp, vp, vp, i32, vp, vp]),
+    "edfa_spmv": (i32, [vp, vp, vp, vp, f64, f64]),
+    "edfa_system_spmv": (i32, [vp, vp, vp, vp]),
+    "edfa_restricted_solve": (i32, [vp, vp, i32, vp, vp, i32, vp, vp]),
+    "edfa_grow_dynamic": (i32, [vp, vp, i32, vp, vp, C.POINTER(Dynamic), i32, vp, vp, P_i32]),
+    "edfa_gmres": (i32, [vp, vp, vp, vp, vp, vp, f64, i32, i32, C.POINTER(Report), vp, i32]),
+    "edfa_bicgstab": (i32, [vp, vp, vp, vp, vp, vp, f64, i32, C.POINTER(Report), vp, i32]),
+    "edfa_dot": (i32, [vp, i64, vp, vp, C.POINTER(f64)]),
+    "edfa_axpby": (i32, [vp, i64, f64, vp, f64, vp]),
+}
+
+_lib = None
+
+
+class EdfaUnsupported(NotImplementedError):
+    """Option valid in the reference but not implemented on the GPU path."""
+
+
+def lib():
+    """Load libedfa.so once; raise (never fall back) if it is missing."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the EDFA path has no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        if L.edfa_abi_version() != 1:
+            raise RuntimeError("libedfa.so ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    msg = lib().edfa_last_error().decode(errors="replace")
+    if status == ERR_VALUE:
+        raise ValueError(msg)
+    if status == ERR_FACTORIZATION:
+        raise FactorizationError(msg)
+    if status == ERR_STATE:
+        raise RuntimeError(msg)
+    if status == ERR_UNSUPPORTED:
+        raise EdfaUnsupported(msg)
+    raise RuntimeError(f"libedfa CUDA failure: {msg}")
+
+
+def exported_symbols():
+    """Names declared in include/edfa.h (used by the ABI tests)."""
+    return sorted(_SIGS)

@@ -1,0 +1,421 @@
+// extern "C" entry points of libedfa.so (declared in include/edfa.h).
+#include <algorithm>
+#include <map>
+#include <vector>
+
+#include "dev_util.cuh"
+#include "edfa_internal.cuh"
+#include "objects.cuh"
+
+using namespace edfa;
+
+namespace {
+
+const Csr& M(const edfa_csr* h) {
+    require(h != nullptr, EDFA_ERR_VALUE, "matrix handle is NULL");
+    return h->m ? *h->m : h->own;
+}
+
+void upload(Ctx* c, void* dst, const void* src, size_t bytes, int mem) {
+    if (!bytes) return;
+    EDFA_CUDA(cudaMemcpyAsync(dst, src, bytes, mem == EDFA_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                              c->stream));
+}
+void download(Ctx* c, void* dst, const void* src, size_t bytes, int mem) {
+    if (!bytes) return;
+    EDFA_CUDA(cudaMemcpyAsync(dst, src, bytes, mem == EDFA_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                              c->stream));
+}
+
+// single-row helper matrices for the row-level entry points
+void host_row(Ctx* c, int32_t n_cols, const std::vector<int32_t>& idx, const std::vector<double>& val, Csr& out) {
+    out.n_rows = 1;
+    out.n_cols = n_cols;
+    out.nnz = (int64_t)idx.size();
+    int32_t ptr[2] = {0, (int32_t)idx.size()};
+    out.ptr.reset(c, 2);
+    EDFA_CUDA(cudaMemcpyAsync(out.ptr.p, ptr, sizeof ptr, cudaMemcpyHostToDevice, c->stream));
+    out.idx.reset(c, idx.size());
+    out.val.reset(c, idx.size());
+    if (!idx.empty()) {
+        EDFA_CUDA(cudaMemcpyAsync(out.idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, c->stream));
+        EDFA_CUDA(cudaMemcpyAsync(out.val.p, val.data(), val.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    }
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));   // host vectors go out of scope
+}
+
+// sort + unique keeping the LAST value of duplicates (numpy fancy assignment)
+void unique_last(int32_t n, const int32_t* idx, const double* val, std::vector<int32_t>& oi, std::vector<double>& ov) {
+    std::map<int32_t, double> m;
+    for (int32_t k = 0; k < n; ++k) m[idx[k]] = val ? val[k] : 0.0;
+    oi.clear();
+    ov.clear();
+    for (auto& kv : m) { oi.push_back(kv.first); ov.push_back(kv.second); }
+}
+
+}  // namespace
+
+extern "C" {
+
+// ---------------------------------------------------------------- matrices
+int edfa_csr_create(edfa_ctx* ctx, int32_t n_rows, int32_t n_cols, int64_t nnz, const int32_t* indptr,
+                    const int32_t* indices, const double* data, int mem, edfa_csr** out) {
+    API_BEGIN
+    require(ctx && out, EDFA_ERR_VALUE, "NULL argument");
+    require(n_rows >= 0 && n_cols >= 0 && nnz >= 0, EDFA_ERR_VALUE, "negative matrix size");
+    require(nnz <= INT32_MAX, EDFA_ERR_UNSUPPORTED, "more than 2^31-1 stored entries");
+    Ctx* c = &ctx->c;
+    auto* h = new edfa_csr();
+    h->ctx = c;
+    Csr& A = h->own;
+    A.n_rows = n_rows;
+    A.n_cols = n_cols;
+    A.nnz = nnz;
+    A.ptr.reset(c, (size_t)n_rows + 1);
+    upload(c, A.ptr.p, indptr, sizeof(int32_t) * (n_rows + 1), mem);
+    A.idx.reset(c, nnz);
+    upload(c, A.idx.p, indices, sizeof(int32_t) * nnz, mem);
+    if (data) {
+        A.val.reset(c, nnz);
+        upload(c, A.val.p, data, sizeof(double) * nnz, mem);
+    }
+    if (mem == EDFA_MEM_HOST) EDFA_CUDA(cudaStreamSynchronize(c->stream));   // pageable sources
+    *out = h;
+    API_END
+}
+
+int edfa_csr_info(const edfa_csr* A, int32_t* n_rows, int32_t* n_cols, int64_t* nnz) {
+    API_BEGIN
+    const Csr& m = M(A);
+    if (n_rows) *n_rows = m.n_rows;
+    if (n_cols) *n_cols = m.n_cols;
+    if (nnz) *nnz = m.nnz;
+    API_END
+}
+
+int edfa_csr_export(edfa_ctx* ctx, const edfa_csr* A, int32_t* indptr, int32_t* indices, double* data, int mem) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    const Csr& m = M(A);
+    if (indptr) download(c, indptr, m.ptr.p, sizeof(int32_t) * (m.n_rows + 1), mem);
+    if (indices) download(c, indices, m.idx.p, sizeof(int32_t) * m.nnz, mem);
+    if (data) {
+        require(m.val.p != nullptr || m.nnz == 0, EDFA_ERR_VALUE, "matrix has no values (pattern only)");
+        download(c, data, m.val.p, sizeof(double) * m.nnz, mem);
+    }
+    if (mem == EDFA_MEM_HOST) EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    API_END
+}
+
+int edfa_csr_destroy(edfa_csr* A) {
+    API_BEGIN
+    delete A;
+    API_END
+}
+
+// ---------------------------------------------------------------- system
+int edfa_system_create(edfa_ctx* ctx, const edfa_csr* A_ff, const edfa_csr* A_fc, const edfa_csr* A_cf,
+                       const edfa_csr* A_cc, edfa_system** out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    auto* s = new edfa_system();
+    try {
+        s->ctx = c;
+        s->A_ff = &M(A_ff);
+        s->A_fc = &M(A_fc);
+        s->A_cf = &M(A_cf);
+        s->A_cc = &M(A_cc);
+        require(s->A_ff->n_rows == s->A_ff->n_cols, EDFA_ERR_VALUE, "A_ff must be square");
+        require(s->A_cc->n_rows == s->A_cc->n_cols, EDFA_ERR_VALUE, "A_cc must be square");
+        block_merge(c, *s->A_ff, *s->A_fc, *s->A_cf, *s->A_cc, s->A);
+    } catch (...) {
+        delete s;
+        throw;
+    }
+    *out = s;
+    API_END
+}
+
+int edfa_system_set_cc(edfa_ctx* ctx, edfa_system* sys, const edfa_csr* A_cc) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    const Csr& cc = M(A_cc);
+    require(cc.n_rows == sys->A_cc->n_rows && cc.n_cols == sys->A_cc->n_cols, EDFA_ERR_VALUE, "A_cc shape changed");
+    sys->A_cc = &cc;
+    block_merge(c, *sys->A_ff, *sys->A_fc, *sys->A_cf, *sys->A_cc, sys->A);
+    API_END
+}
+
+int edfa_system_destroy(edfa_system* sys) {
+    API_BEGIN
+    delete sys;
+    API_END
+}
+
+// ---------------------------------------------------------------- patterns
+int edfa_pattern_static(edfa_ctx* ctx, int32_t n_cells, int32_t n_faces, const int32_t* elem_to_faces,
+                        const int32_t* neighbors, const int32_t* face_index, char prototype, int mem,
+                        edfa_csr** out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    require(n_cells >= 0 && n_faces >= 0, EDFA_ERR_VALUE, "negative sizes");
+    DevBuf<int32_t> e2f(c, (size_t)n_cells * 6), nbr(c, (size_t)n_cells * 6), fidx(c, std::max(n_faces, 1));
+    upload(c, e2f.p, elem_to_faces, sizeof(int32_t) * 6 * n_cells, mem);
+    upload(c, nbr.p, neighbors, sizeof(int32_t) * 6 * n_cells, mem);
+    upload(c, fidx.p, face_index, sizeof(int32_t) * n_faces, mem);
+    int32_t n_free = 0;
+    {
+        // number of free faces = max(face_index) + 1 (computed on the host side of the ABI)
+        std::vector<int32_t> h(n_faces);
+        if (mem == EDFA_MEM_HOST) std::copy(face_index, face_index + n_faces, h.begin());
+        else if (n_faces) EDFA_CUDA(cudaMemcpy(h.data(), face_index, 4 * (size_t)n_faces, cudaMemcpyDeviceToHost));
+        for (auto v : h) n_free = std::max(n_free, v + 1);
+    }
+    auto* h = new edfa_csr();
+    h->ctx = c;
+    try {
+        static_pattern(c, n_cells, n_free, e2f.p, nbr.p, fidx.p, prototype, h->own);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    API_END
+}
+
+// ---------------------------------------------------------------- stage 1 / 2
+int edfa_stage1_build(edfa_ctx* ctx, const edfa_system* sys, const edfa_csr* pattern, const edfa_dynamic* dyn,
+                      double tau_filt, int filtration, double face_drop_tol, int no_fill, edfa_stage1** out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    auto* s1 = new edfa_stage1();
+    s1->ctx = c;
+    try {
+        stage1_build(c, const_cast<edfa_system*>(sys), pattern ? &M(pattern) : nullptr, dyn, tau_filt, filtration,
+                     face_drop_tol, no_fill, s1);
+    } catch (...) {
+        delete s1;
+        throw;
+    }
+    *out = s1;
+    API_END
+}
+
+int edfa_stage1_info_get(const edfa_stage1* s1, edfa_stage1_info* info) {
+    API_BEGIN
+    info->nnz_G = s1->G.nnz;
+    info->nnz_FT = s1->FT.nnz;
+    info->nnz_H = s1->H.nnz;
+    info->nnz_Q = s1->Q.nnz;
+    info->nnz_L = s1->ic.Lpat.nnz + s1->ic.n;
+    info->max_pattern = s1->max_pattern;
+    info->pivot_shifts = s1->ic.shifts;
+    info->trsv_levels = std::max(s1->ic.fwd.n_levels, s1->ic.bwd.n_levels);
+    API_END
+}
+
+int edfa_stage1_part(edfa_ctx* ctx, edfa_stage1* s1, int part, const edfa_csr** out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    const Csr* m = nullptr;
+    switch (part) {
+        case EDFA_S1_G: m = &s1->G; break;
+        case EDFA_S1_FT: m = &s1->FT; break;
+        case EDFA_S1_H: m = &s1->H; break;
+        case EDFA_S1_Q: m = &s1->Q; break;
+        case EDFA_S1_L: ic_export(c, s1->ic); m = &s1->ic.export_L; break;
+        case EDFA_S1_F: m = &s1->F; break;
+        default: throw Error(EDFA_ERR_VALUE, "unknown stage-1 part");
+    }
+    s1->views[part].ctx = c;
+    s1->views[part].m = m;
+    *out = &s1->views[part];
+    API_END
+}
+
+int edfa_stage1_destroy(edfa_stage1* s1) {
+    API_BEGIN
+    delete s1;
+    API_END
+}
+
+int edfa_stage2_build(edfa_ctx* ctx, const edfa_csr* A_cc, const edfa_stage1* s1, double tau_filt, int filtration,
+                      double schur_drop_tol, int no_fill, edfa_stage2** out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    require(s1 != nullptr, EDFA_ERR_STATE, "stage 1 has not been built");
+    auto* s2 = new edfa_stage2();
+    s2->ctx = c;
+    try {
+        stage2_build(c, M(A_cc), s1, tau_filt, filtration, schur_drop_tol, no_fill, s2);
+    } catch (...) {
+        delete s2;
+        throw;
+    }
+    *out = s2;
+    API_END
+}
+
+int edfa_stage2_info_get(const edfa_stage2* s2, edfa_stage2_info* info) {
+    API_BEGIN
+    int64_t n = s2->ilu.n;
+    int64_t lower = s2->ilu.fwd.n_dep, upper = s2->ilu.bwd.n_dep;
+    info->nnz_S = s2->S.nnz;
+    info->nnz_L = lower + n;
+    info->nnz_U = upper + n;
+    info->pivot_shifts = s2->ilu.shifts;
+    info->levels_L = s2->ilu.fwd.n_levels;
+    info->levels_U = s2->ilu.bwd.n_levels;
+    API_END
+}
+
+int edfa_stage2_part(edfa_ctx* ctx, edfa_stage2* s2, int part, const edfa_csr** out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    const Csr* m = nullptr;
+    switch (part) {
+        case EDFA_S2_S: m = &s2->S; break;
+        case EDFA_S2_L: ilu_export(c, s2->ilu); m = &s2->ilu.export_L; break;
+        case EDFA_S2_U: ilu_export(c, s2->ilu); m = &s2->ilu.export_U; break;
+        default: throw Error(EDFA_ERR_VALUE, "unknown stage-2 part");
+    }
+    s2->views[part].ctx = c;
+    s2->views[part].m = m;
+    *out = &s2->views[part];
+    API_END
+}
+
+int edfa_stage2_destroy(edfa_stage2* s2) {
+    API_BEGIN
+    delete s2;
+    API_END
+}
+
+// ---------------------------------------------------------------- apply / products
+int edfa_precond_apply(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2,
+                       const double* r, double* y) {
+    API_BEGIN
+    require(s1 != nullptr, EDFA_ERR_STATE, "stage 1 has not been built");
+    require(s2 != nullptr, EDFA_ERR_STATE, "stage 2 has not been built; call refresh()");
+    apply_entry(&ctx->c, sys, s1, s2, r, y);
+    API_END
+}
+
+int edfa_inner_apply(edfa_ctx* ctx, const edfa_stage1* s1, const edfa_stage2* s2, int which, const double* r,
+                     double* y) {
+    API_BEGIN
+    require(which == 0 ? s1 != nullptr : s2 != nullptr, EDFA_ERR_STATE, "factorisation not built");
+    inner_apply(&ctx->c, s1, s2, which, r, y);
+    API_END
+}
+
+int edfa_spmv(edfa_ctx* ctx, const edfa_csr* A, const double* x, double* y, double alpha, double beta) {
+    API_BEGIN
+    const Csr& m = M(A);
+    spmv(&ctx->c, view(m), m.nnz, x, y, alpha, beta, "spmv");
+    API_END
+}
+
+int edfa_system_spmv(edfa_ctx* ctx, const edfa_system* sys, const double* x, double* y) {
+    API_BEGIN
+    spmv(&ctx->c, view(sys->A), sys->A.nnz, x, y, 1.0, 0.0, "spmv_A");
+    API_END
+}
+
+// ---------------------------------------------------------------- row-level kernels
+int edfa_restricted_solve(edfa_ctx* ctx, const edfa_csr* A_ff, int32_t n_rhs, const int32_t* rhs_idx,
+                          const double* rhs_val, int32_t n_idx, const int32_t* idx, double* x_out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    const Csr& A = M(A_ff);
+    std::vector<int32_t> ri, qi;
+    std::vector<double> rv, qv;
+    unique_last(n_rhs, rhs_idx, rhs_val, ri, rv);
+    unique_last(n_idx, idx, nullptr, qi, qv);
+    require((int32_t)qi.size() == n_idx, EDFA_ERR_VALUE, "idx must be unique");
+    for (auto v : qi) require(v >= 0 && v < A.n_rows, EDFA_ERR_VALUE, "row index out of range");
+    // rhs entries outside idx are dropped (hx/precond.py:88-92)
+    Csr acf, afct, pat;
+    host_row(c, A.n_cols, ri, rv, acf);
+    host_row(c, A.n_cols, {}, {}, afct);
+    host_row(c, A.n_cols, qi, qv, pat);
+    SetupInput in;
+    in.A = &A;
+    in.Acf = &acf;
+    in.AfcT = &afct;
+    in.pattern = &pat;
+    SetupOutput out;
+    setup_rows(c, in, out);
+    if (n_idx) download(c, x_out, out.g.p, sizeof(double) * n_idx, EDFA_MEM_HOST);
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    API_END
+}
+
+int edfa_grow_dynamic(edfa_ctx* ctx, const edfa_csr* A_ff, int32_t n_rhs, const int32_t* rhs_idx,
+                      const double* rhs_val, const edfa_dynamic* dyn, int32_t cap, int32_t* idx_out, double* x_out,
+                      int32_t* n_out) {
+    API_BEGIN
+    Ctx* c = &ctx->c;
+    const Csr& A = M(A_ff);
+    require(dyn && dyn->n_add >= 1 && dyn->n_ent >= 0, EDFA_ERR_VALUE, "invalid dynamic configuration");
+    std::vector<int32_t> ri;
+    std::vector<double> rv;
+    unique_last(n_rhs, rhs_idx, rhs_val, ri, rv);
+    for (auto v : ri) require(v >= 0 && v < A.n_rows, EDFA_ERR_VALUE, "row index out of range");
+    Csr acf, afct, AT;
+    host_row(c, A.n_cols, ri, rv, acf);
+    host_row(c, A.n_cols, {}, {}, afct);
+    transpose(c, A, AT);
+    SetupInput in;
+    in.A = &A;
+    in.AT = &AT;
+    in.Acf = &acf;
+    in.AfcT = &afct;
+    in.n_add = dyn->n_add;
+    in.n_ent = dyn->n_ent;
+    in.sweep_limit = dyn->it_max > 0 ? dyn->it_max : std::max(dyn->n_ent, 1);
+    SetupOutput out;
+    setup_rows(c, in, out);
+    int32_t s = 0;
+    download(c, &s, out.qsize.p, sizeof(int32_t), EDFA_MEM_HOST);
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    require(s <= cap, EDFA_ERR_VALUE, "output capacity too small");
+    download(c, idx_out, out.q.p, sizeof(int32_t) * s, EDFA_MEM_HOST);
+    download(c, x_out, out.g.p, sizeof(double) * s, EDFA_MEM_HOST);
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    *n_out = s;
+    API_END
+}
+
+// ---------------------------------------------------------------- Krylov
+int edfa_gmres(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b,
+               double* x, double rtol, int32_t restart, int32_t max_it, edfa_report* rep, double* hist,
+               int32_t hist_cap) {
+    API_BEGIN
+    require((s1 == nullptr) == (s2 == nullptr), EDFA_ERR_STATE, "stage 2 has not been built; call refresh()");
+    gmres(&ctx->c, sys, s1, s2, b, x, rtol, restart, max_it, rep, hist, hist_cap);
+    API_END
+}
+
+int edfa_bicgstab(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2,
+                  const double* b, double* x, double rtol, int32_t max_it, edfa_report* rep, double* hist,
+                  int32_t hist_cap) {
+    API_BEGIN
+    require((s1 == nullptr) == (s2 == nullptr), EDFA_ERR_STATE, "stage 2 has not been built; call refresh()");
+    bicgstab(&ctx->c, sys, s1, s2, b, x, rtol, max_it, rep, hist, hist_cap);
+    API_END
+}
+
+int edfa_dot(edfa_ctx* ctx, int64_t n, const double* x, const double* y, double* out_host) {
+    API_BEGIN
+    *out_host = dot_entry(&ctx->c, n, x, y);
+    API_END
+}
+
+int edfa_axpby(edfa_ctx* ctx, int64_t n, double a, const double* x, double b, double* y) {
+    API_BEGIN
+    axpby_entry(&ctx->c, n, a, x, b, y);
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+// Context: stream, stream-ordered allocator, scratch, per-kernel event timing.
+#include <algorithm>
+#include <cstring>
+
+#include "edfa_internal.cuh"
+
+namespace edfa {
+
+void* Ctx::alloc(size_t bytes) {
+    if (bytes == 0) return nullptr;
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(EDFA_ERR_CUDA, std::string("device allocation of ") + std::to_string(bytes) +
+                                       " bytes failed: " + cudaGetErrorString(e));
+    }
+    return p;
+}
+
+void Ctx::free(void* p) {
+    if (p) cudaFreeAsync(p, stream);
+}
+
+void* Ctx::cub_scratch(size_t bytes) {
+    if (bytes > cub_tmp_bytes) {
+        if (cub_tmp) free(cub_tmp);
+        cub_tmp_bytes = std::max(bytes, size_t(1) << 20);
+        cub_tmp = alloc(cub_tmp_bytes);
+    }
+    return cub_tmp;
+}
+
+cudaEvent_t Ctx::get_event() {
+    if (event_pool.empty()) {
+        cudaEvent_t e;
+        EDFA_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+}
+
+void Ctx::flush_profile() {
+    if (pending.empty()) return;
+    EDFA_CUDA(cudaStreamSynchronize(stream));
+    for (auto& r : pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.t0, r.t1);
+        auto it = std::find_if(acc.begin(), acc.end(), [&](const Acc& a) { return a.name == r.name; });
+        if (it == acc.end()) {
+            acc.push_back(Acc{r.name});
+            it = acc.end() - 1;
+        }
+        it->n += 1;
+        it->ms += ms;
+        it->bytes += r.bytes;
+        event_pool.push_back(r.t0);
+        event_pool.push_back(r.t1);
+    }
+    pending.clear();
+}
+
+}  // namespace edfa
+
+using namespace edfa;
+
+static thread_local std::string g_last_error;
+
+namespace edfa {
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+}  // namespace edfa
+
+
+extern "C" {
+
+int edfa_abi_version(void) { return EDFA_ABI_VERSION; }
+
+const char* edfa_last_error(void) { return g_last_error.c_str(); }
+
+int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
+    API_BEGIN
+    require(out != nullptr, EDFA_ERR_VALUE, "out is NULL");
+    EDFA_CUDA(cudaSetDevice(device));
+    auto* h = new edfa_ctx();
+    h->c.device = device;
+    h->c.stream = static_cast<cudaStream_t>(stream);
+    // keep freed memory in the stream-ordered pool between steps
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
+    h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));
+    EDFA_CUDA(cudaMallocHost(&h->c.h_pinned, 4096 * sizeof(double)));
+    *out = h;
+    API_END
+}
+
+int edfa_ctx_set_stream(edfa_ctx* ctx, void* stream) {
+    API_BEGIN
+    require(ctx, EDFA_ERR_VALUE, "ctx is NULL");
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    API_END
+}
+
+int edfa_ctx_sync(edfa_ctx* ctx) {
+    API_BEGIN
+    EDFA_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    API_END
+}
+
+int edfa_ctx_destroy(edfa_ctx* ctx) {
+    API_BEGIN
+    if (!ctx) return EDFA_OK;
+    Ctx& c = ctx->c;
+    cudaStreamSynchronize(c.stream);
+    c.flush_profile();
+    for (auto e : c.event_pool) cudaEventDestroy(e);
+    c.free(c.cub_tmp);
+    c.free(c.d_scalar_i);
+    c.free(c.d_scalar_d);
+    cudaFreeHost(c.h_pinned);
+    cudaStreamSynchronize(c.stream);
+    delete ctx;
+    API_END
+}
+
+int edfa_ctx_profile(edfa_ctx* ctx, int enable) {
+    API_BEGIN
+    ctx->c.flush_profile();
+    ctx->c.profiling = enable;
+    API_END
+}
+
+int64_t edfa_ctx_profile_report(edfa_ctx* ctx, char* buf, int64_t cap, int reset) {
+    try {
+        ctx->c.flush_profile();
+        std::string s = "{";
+        bool first = true;
+        for (auto& a : ctx->c.acc) {
+            char line[512];
+            snprintf(line, sizeof line, "%s\"%s\": {\"launches\": %lld, \"ms\": %.6f, \"bytes\": %.1f}",
+                     first ? "" : ", ", a.name.c_str(), (long long)a.n, a.ms, a.bytes);
+            s += line;
+            first = false;
+        }
+        s += "}";
+        if (buf && cap > 0) {
+            int64_t n = std::min<int64_t>(cap - 1, (int64_t)s.size());
+            memcpy(buf, s.data(), n);
+            buf[n] = 0;
+        }
+        if (reset) ctx->c.acc.clear();
+        return (int64_t)s.size() + 1;
+    } catch (const std::exception& e) {
+        edfa::set_error(EDFA_ERR_CUDA, e.what());
+        return -1;
+    }
+}
+
+int64_t edfa_ctx_launch_count(edfa_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,180 @@
+// Internal declarations shared by the libedfa translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/edfa.h"
+
+namespace edfa {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define EDFA_CUDA(call)                                                          \
+    do {                                                                         \
+        cudaError_t e_ = (call);                                                 \
+        if (e_ != cudaSuccess)                                                   \
+            throw ::edfa::Error(EDFA_ERR_CUDA, std::string(#call ": ") +         \
+                                                  cudaGetErrorString(e_));       \
+    } while (0)
+
+inline void require(bool ok, int code, const std::string& msg) {
+    if (!ok) throw Error(code, msg);
+}
+
+// ---------------------------------------------------------------- context
+struct ProfRec {
+    const char* name;
+    cudaEvent_t t0, t1;
+    double bytes;
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int profiling = 0;
+    int64_t launches = 0;
+    std::vector<ProfRec> pending;
+    std::vector<cudaEvent_t> event_pool;
+    struct Acc { std::string name; int64_t n = 0; double ms = 0, bytes = 0; };
+    std::vector<Acc> acc;
+    // scratch
+    void* cub_tmp = nullptr;
+    size_t cub_tmp_bytes = 0;
+    int* d_scalar_i = nullptr;     // small device int scratch (64 ints)
+    double* d_scalar_d = nullptr;  // small device double scratch (4096 doubles)
+    double* h_pinned = nullptr;    // pinned host scratch (4096 doubles)
+
+    void* alloc(size_t bytes);
+    void free(void* p);
+    void* cub_scratch(size_t bytes);
+    cudaEvent_t get_event();
+    void flush_profile();
+};
+
+// RAII guard for library-owned device allocations
+template <class T>
+struct DevBuf {
+    Ctx* ctx = nullptr;
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(Ctx* c, size_t count) { reset(c, count); }
+    void reset(Ctx* c, size_t count) {
+        release();
+        ctx = c;
+        n = count;
+        p = count ? static_cast<T*>(c->alloc(count * sizeof(T))) : nullptr;
+    }
+    void release() {
+        if (p && ctx) ctx->free(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); ctx = o.ctx; p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+};
+
+// Timed launch scope: records events around the enclosed launches when profiling.
+struct Prof {
+    Ctx* c;
+    const char* name;
+    double bytes;
+    cudaEvent_t e0 = nullptr;
+    Prof(Ctx* ctx, const char* nm, double b) : c(ctx), name(nm), bytes(b) {
+        c->launches++;
+        if (c->profiling) {
+            e0 = c->get_event();
+            cudaEventRecord(e0, c->stream);
+        }
+    }
+    ~Prof() {
+        if (c->profiling) {
+            cudaEvent_t e1 = c->get_event();
+            cudaEventRecord(e1, c->stream);
+            c->pending.push_back({name, e0, e1, bytes});
+        }
+    }
+};
+
+inline void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(EDFA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- CSR
+struct Csr {
+    int32_t n_rows = 0, n_cols = 0;
+    int64_t nnz = 0;
+    DevBuf<int32_t> ptr, idx;
+    DevBuf<double> val;   // may be empty for pattern-only matrices
+};
+
+// light view passed to kernels
+struct CsrV {
+    int32_t n_rows, n_cols;
+    const int32_t* __restrict__ ptr;
+    const int32_t* __restrict__ idx;
+    const double* __restrict__ val;
+};
+inline CsrV view(const Csr& A) {
+    return CsrV{A.n_rows, A.n_cols, A.ptr.p, A.idx.p, A.val.p};
+}
+
+constexpr int WARP = 32;
+constexpr int NUM_SMS_B200 = 148;
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- helpers (sparse_util.cu)
+// exclusive scan of int32 counts into int32 row pointers; returns total (syncs)
+int64_t scan_counts(Ctx* c, const int32_t* counts, int32_t* ptr_out, int32_t n);
+// CSR transpose (sorted rows in the output), values optional
+void transpose(Ctx* c, const Csr& A, Csr& AT);
+// monolithic block matrix [[A, B], [C, D]]
+void block_merge(Ctx* c, const Csr& A, const Csr& B, const Csr& C, const Csr& D, Csr& M);
+// y = alpha*A x + beta*y
+void spmv(Ctx* c, const CsrV& A, int64_t nnz, const double* x, double* y, double alpha, double beta,
+          const char* name = "spmv");
+// S = A - H (row-wise sorted merge, exact zeros dropped, optional row filter)
+void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S);
+// row filter (filter_rows, precond.py:138-157): drop |v| < tau*||row||_2 off-diagonal
+void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out);
+void copy_csr(Ctx* c, const Csr& A, Csr& out);
+void fill(Ctx* c, double* p, int64_t n, double v);
+void fill_bits(Ctx* c, double* p, int64_t n, unsigned long long bits);
+
+int set_error(int code, const std::string& msg);
+
+}  // namespace edfa
+
+#define API_BEGIN try {
+#define API_END                                                                      \
+    }                                                                                \
+    catch (const edfa::Error& e) { return edfa::set_error(e.code, e.what()); }       \
+    catch (const std::exception& e) { return edfa::set_error(EDFA_ERR_CUDA, e.what()); } \
+    return EDFA_OK;
+
+// ---------------------------------------------------------------- opaque handles
+struct edfa_ctx { edfa::Ctx c; };
+// owning handle (own) or borrowed view of a library-internal matrix (m)
+struct edfa_csr {
+    edfa::Ctx* ctx = nullptr;
+    edfa::Csr own;
+    const edfa::Csr* m = nullptr;
+};

@@ -1,0 +1,341 @@
+// K6/K7: IC(0) of -A_ff and ILU(0) of S~ (hx/sparse.py:141-282 with
+// no_fill=True, fill_tol=0), sync-free in dependency-level order.
+//
+// The arithmetic mirrors the reference operation for operation -- pivots in
+// increasing column order, multipliers a_ik / d_k, updates
+// w_j <- w_j - l_ik * u_kj without FMA contraction, the sign-preserving guard
+// |pivot| < 1e-12 * ||row||_inf -- so, given the same input matrix, the
+// factors are bit-identical to the reference's pure-Python factorisation.
+// Rows are processed in the forward triangular-solve plan's level order (the
+// factorisation DAG is the forward-solve DAG); a row publishes its pivot,
+// which doubles as the ready flag (sentinel-initialised), after its values.
+#include "dev_util.cuh"
+#include "edfa_internal.cuh"
+#include "objects.cuh"
+
+namespace edfa {
+namespace {
+
+constexpr double PIVOT_GUARD = 1e-12;
+
+// strictly lower (mode 0) / strictly upper (mode 1) part, values scaled
+template <bool FILL>
+__global__ void k_select(CsrV A, int mode, double scale, int32_t* __restrict__ cnt, const int32_t* __restrict__ Op,
+                         int32_t* __restrict__ Oi, double* __restrict__ Ov) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n_rows) return;
+    int n = 0, o = FILL ? Op[i] : 0;
+    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
+        int j = A.idx[e];
+        if (mode == 0 ? j < i : j > i) {
+            if (FILL) {
+                Oi[o + n] = j;
+                if (Ov) Ov[o + n] = A.val ? scale * A.val[e] : 0.0;
+            }
+            ++n;
+        }
+    }
+    if (!FILL) cnt[i] = n;
+}
+
+// diagonal (0 if not stored) and max |row| (1 for an empty row)
+__global__ void k_diag_scale(CsrV A, double sign, double* __restrict__ d, double* __restrict__ sc,
+                             int32_t* __restrict__ has) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n_rows) return;
+    double dv = 0.0, mx = 0.0;
+    int h = 0;
+    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
+        double v = A.val[e];
+        mx = fmax(mx, fabs(v));
+        if (A.idx[e] == i) { dv = sign * v; h = 1; }
+    }
+    d[i] = dv;
+    sc[i] = A.ptr[i + 1] > A.ptr[i] ? mx : 1.0;
+    if (has) has[i] = h;
+}
+
+__device__ double wait_pivot(const double* p, int* err) {
+    double v;
+    asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    long long spins = 0;
+    while (is_sentinel(v)) {
+        if (++spins > SPIN_LIMIT) { atomicExch(err, 3); return 1.0; }
+        asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    }
+    return v;
+}
+__device__ void publish_pivot(double* p, double v) {
+    asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// IC(0) of -A_ff: one thread per row, rows in forward-plan order.
+// L holds the strictly lower pattern (initialised with -A values); diag the
+// pivots (sentinel until published).
+__global__ void __launch_bounds__(256) k_ic0(const int* __restrict__ perm, int n_slices, const int32_t* __restrict__ Lp,
+                                             const int32_t* __restrict__ Li, double* __restrict__ Lv,
+                                             const double* __restrict__ aii, const double* __restrict__ scale,
+                                             double* __restrict__ diag, int* ticket, int* shifts, int* err) {
+    __shared__ int base[8];
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) base[wid] = atomicAdd(ticket, 1);
+    __syncwarp();
+    int s = base[wid];
+    if (s >= n_slices) return;
+    int i = perm[s * 32 + lane];
+    if (i < 0) return;
+    int lo = Lp[i], hi = Lp[i + 1];
+    // every dependency must be final before row i reads its L entries
+    for (int p = lo; p < hi; ++p) wait_pivot(diag + Li[p], err);
+    double d = aii[i];
+    for (int p = lo; p < hi; ++p) {
+        int k = Li[p];
+        double mult = __ddiv_rn(Lv[p], ld_cg(diag + k));
+        Lv[p] = mult;
+        for (int q = p + 1; q < hi; ++q) {
+            int j = Li[q];
+            int pos = bsearch(Li, Lp[j], Lp[j + 1], k);
+            if (pos >= 0) Lv[q] = sub_mul(Lv[q], mult, ld_cg(Lv + pos));
+        }
+        d = sub_mul(d, mult, mult);
+    }
+    double g = PIVOT_GUARD * scale[i];
+    if (d < g) {
+        d = g;
+        atomicAdd(shifts, 1);
+    }
+    __threadfence();
+    publish_pivot(diag + i, publishable(__dsqrt_rn(d)));
+}
+
+// ILU(0) of S: one warp per row, rows in forward-plan order.  LU starts as a
+// copy of S; on exit its strictly lower part holds the multipliers and its
+// strictly upper part U; pivots go to udiag (sentinel until published).
+template <int RMAX, int WPB = (RMAX >= 1024 ? 2 : 4)>
+__global__ void __launch_bounds__(128) k_ilu0(const int* __restrict__ perm, int n_slots, const int32_t* __restrict__ Sp,
+                                              const int32_t* __restrict__ Si, double* __restrict__ LU,
+                                              const double* __restrict__ scale, double* __restrict__ udiag,
+                                              int* ticket, int* shifts, int* err) {
+    __shared__ int s_cols[WPB][RMAX];
+    __shared__ double s_vals[WPB][RMAX];
+    __shared__ int base[WPB];
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* cols = s_cols[wid];
+    double* vals = s_vals[wid];
+    for (;;) {
+        if (lane == 0) base[wid] = atomicAdd(ticket, 1);
+        __syncwarp();
+        int slot = base[wid];
+        __syncwarp();
+        if (slot >= n_slots) return;
+        int i = perm[slot];
+        if (i < 0) continue;
+        int lo = Sp[i], n = Sp[i + 1] - lo;
+        if (n > RMAX) {
+            if (lane == 0) atomicExch(err, 4);
+            if (lane == 0) publish_pivot(udiag + i, 1.0);
+            continue;
+        }
+        for (int t = lane; t < n; t += 32) {
+            cols[t] = Si[lo + t];
+            vals[t] = LU[lo + t];
+        }
+        __syncwarp();
+        int nl = lower_bound(cols, 0, n, i);
+        for (int p = 0; p < nl; ++p) {
+            int k = cols[p];
+            double dk = wait_pivot(udiag + k, err);
+            double mult = __ddiv_rn(vals[p], dk);
+            __syncwarp();
+            if (lane == 0) vals[p] = mult;
+            int u0 = lower_bound(Si, Sp[k], Sp[k + 1], k + 1), u1 = Sp[k + 1];
+            for (int e = u0 + lane; e < u1; e += 32) {
+                int j = Si[e];
+                int slot_j = bsearch(cols, p + 1, n, j);
+                if (slot_j >= 0) vals[slot_j] = sub_mul(vals[slot_j], mult, ld_cg(LU + e));
+            }
+            __syncwarp();
+        }
+        int dslot = bsearch(cols, nl, n, i);
+        double piv = dslot >= 0 ? vals[dslot] : 0.0;
+        double g = PIVOT_GUARD * scale[i];
+        if (fabs(piv) < g) {
+            piv = piv >= 0.0 ? g : -g;
+            if (lane == 0) atomicAdd(shifts, 1);
+        }
+        for (int t = lane; t < n; t += 32) LU[lo + t] = vals[t];
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) publish_pivot(udiag + i, publishable(piv));
+        __syncwarp();
+    }
+}
+
+// exported CSRs in the reference layout: IC L with the diagonal last in each
+// row; ILU L = strict lower + unit diagonal (last); U = diagonal first + upper
+template <bool FILL>
+__global__ void k_export_tri(CsrV P, const double* __restrict__ diag, int mode, int32_t* __restrict__ cnt,
+                             const int32_t* __restrict__ Op, int32_t* __restrict__ Oi, double* __restrict__ Ov) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n_rows) return;
+    int n = 0, o = FILL ? Op[i] : 0;
+    auto put = [&](int j, double v) {
+        if (FILL) { Oi[o + n] = j; Ov[o + n] = v; }
+        ++n;
+    };
+    if (mode == 2) put(i, diag[i]);
+    for (int e = P.ptr[i]; e < P.ptr[i + 1]; ++e) {
+        int j = P.idx[e];
+        if (mode == 2 ? j > i : j < i) put(j, P.val[e]);
+    }
+    if (mode == 0) put(i, diag[i]);
+    if (mode == 1) put(i, 1.0);
+    if (!FILL) cnt[i] = n;
+}
+
+void select_part(Ctx* c, const Csr& A, int mode, double scale, bool values, Csr& out) {
+    int n = A.n_rows;
+    out.n_rows = n;
+    out.n_cols = A.n_cols;
+    out.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    if (n) {
+        Prof pr(c, "select", 8.0 * A.nnz);
+        k_select<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), mode, scale, cnt.p, nullptr, nullptr,
+                                                                nullptr);
+        check_launch("k_select");
+    }
+    out.nnz = scan_counts(c, cnt.p, out.ptr.p, n);
+    out.idx.reset(c, out.nnz);
+    if (values) out.val.reset(c, out.nnz);
+    else out.val.release();
+    if (n) {
+        Prof pr(c, "select", 8.0 * A.nnz + 12.0 * out.nnz);
+        k_select<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), mode, scale, nullptr, out.ptr.p, out.idx.p,
+                                                               values ? out.val.p : nullptr);
+        check_launch("k_select");
+    }
+}
+
+void export_tri(Ctx* c, const Csr& P, const double* diag, int mode, Csr& out) {
+    int n = P.n_rows;
+    out.n_rows = n;
+    out.n_cols = P.n_cols;
+    out.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    if (n) {
+        k_export_tri<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(P), diag, mode, cnt.p, nullptr, nullptr,
+                                                                    nullptr);
+        check_launch("k_export_tri");
+    }
+    out.nnz = scan_counts(c, cnt.p, out.ptr.p, n);
+    out.idx.reset(c, out.nnz);
+    out.val.reset(c, out.nnz);
+    if (n) {
+        k_export_tri<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(P), diag, mode, nullptr, out.ptr.p,
+                                                                   out.idx.p, out.val.p);
+        check_launch("k_export_tri");
+    }
+}
+
+int read_flags(Ctx* c, int* dev_shift, int* dev_err, int* shifts) {
+    int h[2];
+    EDFA_CUDA(cudaMemcpyAsync(&h[0], dev_shift, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(&h[1], dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    *shifts = h[0];
+    return h[1];
+}
+
+}  // namespace
+
+void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f) {
+    require(drop_tol == 0.0, EDFA_ERR_UNSUPPORTED,
+            "IC with a drop tolerance (face_drop_tol > 0) is not implemented on the GPU path; use 0 with no_fill");
+    const int n = A_ff.n_rows;
+    f.n = n;
+    select_part(c, A_ff, 0, -1.0, true, f.Lpat);
+    DevBuf<double> aii(c, std::max(n, 1)), sc(c, std::max(n, 1));
+    f.diag.reset(c, std::max(n, 1));
+    if (n) {
+        Prof pr(c, "ic0_prep", 12.0 * A_ff.nnz + 16.0 * n);
+        k_diag_scale<<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A_ff), -1.0, aii.p, sc.p, nullptr);
+        check_launch("k_diag_scale");
+    }
+    build_plan(c, f.Lpat, nullptr, false, false, f.fwd);
+    int* flags = c->d_scalar_i + 24;   // [ticket, shifts, err]
+    EDFA_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), c->stream));
+    if (n) {
+        fill_bits(c, f.diag.p, n, SENTINEL_BITS);
+        Prof pr(c, "ic0_factor", 24.0 * f.Lpat.nnz + 32.0 * n);
+        int n_slices = f.fwd.n_slots / 32;
+        k_ic0<<<ceil_div(n_slices, 8), 256, 0, c->stream>>>(f.fwd.perm.p, n_slices, f.Lpat.ptr.p, f.Lpat.idx.p,
+                                                            f.Lpat.val.p, aii.p, sc.p, f.diag.p, flags, flags + 1,
+                                                            flags + 2);
+        check_launch("k_ic0");
+    }
+    int err = read_flags(c, flags + 1, flags + 2, &f.shifts);
+    require(err == 0, EDFA_ERR_CUDA, "IC(0) factorisation did not complete (spin limit)");
+    plan_values(c, f.Lpat, f.diag.p, f.fwd);
+    Csr LT;
+    transpose(c, f.Lpat, LT);
+    build_plan(c, LT, f.diag.p, false, true, f.bwd);
+}
+
+void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f) {
+    require(drop_tol == 0.0, EDFA_ERR_UNSUPPORTED,
+            "ILU with a drop tolerance (schur_drop_tol > 0) is not implemented on the GPU path; use 0 with no_fill");
+    const int n = S.n_rows;
+    f.n = n;
+    copy_csr(c, S, f.LU);
+    DevBuf<double> dd(c, std::max(n, 1)), sc(c, std::max(n, 1));
+    f.udiag.reset(c, std::max(n, 1));
+    f.has_diag.reset(c, std::max(n, 1));
+    if (n) {
+        Prof pr(c, "ilu0_prep", 12.0 * S.nnz + 16.0 * n);
+        k_diag_scale<<<ceil_div(n, 128), 128, 0, c->stream>>>(view(S), 1.0, dd.p, sc.p, f.has_diag.p);
+        check_launch("k_diag_scale");
+    }
+    Csr Lpart;
+    select_part(c, S, 0, 1.0, false, Lpart);
+    build_plan(c, Lpart, nullptr, true, false, f.fwd);
+    int maxr = n ? max_row_nnz(c, S) : 0;
+    int* flags = c->d_scalar_i + 24;
+    EDFA_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), c->stream));
+    if (n) {
+        fill_bits(c, f.udiag.p, n, SENTINEL_BITS);
+        Prof pr(c, "ilu0_factor", 24.0 * S.nnz + 24.0 * n);
+        int blocks = std::min(ceil_div(f.fwd.n_slots, 4), NUM_SMS_B200 * 16);
+        if (maxr <= 64)
+            k_ilu0<64><<<blocks, 128, 0, c->stream>>>(f.fwd.perm.p, f.fwd.n_slots, f.LU.ptr.p, f.LU.idx.p,
+                                                      f.LU.val.p, sc.p, f.udiag.p, flags, flags + 1, flags + 2);
+        else if (maxr <= 256)
+            k_ilu0<256><<<blocks, 128, 0, c->stream>>>(f.fwd.perm.p, f.fwd.n_slots, f.LU.ptr.p, f.LU.idx.p,
+                                                       f.LU.val.p, sc.p, f.udiag.p, flags, flags + 1, flags + 2);
+        else
+            k_ilu0<1024><<<blocks, 64, 0, c->stream>>>(f.fwd.perm.p, f.fwd.n_slots, f.LU.ptr.p, f.LU.idx.p,
+                                                        f.LU.val.p, sc.p, f.udiag.p, flags, flags + 1, flags + 2);
+        check_launch("k_ilu0");
+    }
+    require(maxr <= 1024, EDFA_ERR_UNSUPPORTED, "Schur rows longer than 1024 entries are not supported");
+    int err = read_flags(c, flags + 1, flags + 2, &f.shifts);
+    require(err == 0, EDFA_ERR_CUDA, "ILU(0) factorisation did not complete");
+    Csr Lv, Uv;
+    select_part(c, f.LU, 0, 1.0, true, Lv);
+    plan_values(c, Lv, nullptr, f.fwd);
+    select_part(c, f.LU, 1, 1.0, true, Uv);
+    build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
+}
+
+void ic_export(Ctx* c, IcFactor& f) {
+    if (f.export_L.ptr.p) return;
+    export_tri(c, f.Lpat, f.diag.p, 0, f.export_L);
+}
+
+void ilu_export(Ctx* c, IluFactor& f) {
+    if (f.export_L.ptr.p) return;
+    export_tri(c, f.LU, f.udiag.p, 1, f.export_L);
+    export_tri(c, f.LU, f.udiag.p, 2, f.export_U);
+}
+
+}  // namespace edfa

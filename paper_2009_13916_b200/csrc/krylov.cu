@@ -1,0 +1,439 @@
+// K9-K11: EDFA application, right-preconditioned GMRES(m) and Bi-CGStab.
+//
+// apply  (hx/precond.py:311-320)
+//   t_f = -(L L^T)^-1 r_f            two level-ordered solves, sign folded in
+//   u_c = r_c - A_cf t_f             SpMV with beta = 1
+//   t_c = (L U)^-1 u_c               two level-ordered solves
+//   y_f = t_f + (L L^T)^-1 A_fc t_c  SpMV + two solves, "+ t_f" fused into the
+//                                    last solve's epilogue
+// GMRES: Arnoldi with classical Gram-Schmidt and DGKS selective
+// re-orthogonalisation (second pass only when ||w|| drops below ||w0||/sqrt2):
+// one fused multi-dot pass over V_0..V_j and one fused multi-axpy(+norm) pass
+// per iteration; block partial sums reduced in a fixed order (deterministic).
+// Givens rotations and the small triangular solve run on the host.
+#include <cmath>
+#include <vector>
+
+#include "dev_util.cuh"
+#include "edfa_internal.cuh"
+#include "objects.cuh"
+
+namespace edfa {
+namespace {
+
+constexpr int RED_BLOCKS = 2 * NUM_SMS_B200;   // fixed grid -> fixed reduction order
+constexpr int RED_THREADS = 256;
+constexpr int GROUP = 8;                      // vectors per multi-dot block row
+
+// partial[blk][k] = sum over the block's rows of V[k0+k] . w   (k < GROUP)
+__global__ void __launch_bounds__(RED_THREADS) k_multidot(const double* __restrict__ V, int64_t ldv, int nvec,
+                                                          const double* __restrict__ w, int64_t n,
+                                                          double* __restrict__ partial) {
+    int k0 = blockIdx.y * GROUP;
+    double acc[GROUP];
+#pragma unroll
+    for (int k = 0; k < GROUP; ++k) acc[k] = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double wi = w[i];
+#pragma unroll
+        for (int k = 0; k < GROUP; ++k)
+            if (k0 + k < nvec) {
+                acc[k] = fma(V[(int64_t)(k0 + k) * ldv + i], wi, acc[k]);
+            }
+    }
+    __shared__ double red[GROUP][RED_THREADS / 32];
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < GROUP; ++k) {
+        double v = warp_sum(acc[k]);
+        if (lane == 0) red[k][wid] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < GROUP && k0 + threadIdx.x < nvec) {
+        double s = 0.0;
+        for (int t = 0; t < RED_THREADS / 32; ++t) s += red[threadIdx.x][t];
+        partial[(int64_t)blockIdx.x * 64 + k0 + threadIdx.x] = s;
+    }
+}
+
+// out[k] = sum_blk partial[blk][k]   (fixed order)
+__global__ void k_reduce_partials(const double* __restrict__ partial, int nblk, int nvec, double* __restrict__ out) {
+    int k = blockIdx.x;
+    if (k >= nvec) return;
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblk; b += 32) s += partial[(int64_t)b * 64 + k];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) out[k] = s;
+}
+
+// w <- w - sum_{k<nv} h[k] V[k]   (or out = sum h[k] V[k] when w_in == NULL),
+// partial[blk] = block sum of out^2
+__global__ void __launch_bounds__(RED_THREADS) k_multiaxpy(const double* __restrict__ V, int64_t ldv, int nv,
+                                                           const double* __restrict__ h, double hscale,
+                                                           const double* w_in, double* out,
+                                                           int64_t n, double* __restrict__ partial) {
+    __shared__ double hs[64];
+    if (threadIdx.x < nv) hs[threadIdx.x] = h[threadIdx.x] * hscale;
+    __syncthreads();
+    double ss = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        int k = 0;
+        for (; k + 4 <= nv; k += 4) {
+            double a0 = V[(int64_t)k * ldv + i], a1 = V[(int64_t)(k + 1) * ldv + i];
+            double a2 = V[(int64_t)(k + 2) * ldv + i], a3 = V[(int64_t)(k + 3) * ldv + i];
+            acc = fma(hs[k], a0, acc);
+            acc = fma(hs[k + 1], a1, acc);
+            acc = fma(hs[k + 2], a2, acc);
+            acc = fma(hs[k + 3], a3, acc);
+        }
+        for (; k < nv; ++k) acc = fma(hs[k], V[(int64_t)k * ldv + i], acc);
+        double o = w_in ? w_in[i] - acc : acc;
+        out[i] = o;
+        ss = fma(o, o, ss);
+    }
+    __shared__ double red[RED_THREADS / 32];
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int t = 0; t < RED_THREADS / 32; ++t) s += red[t];
+        if (partial) partial[(int64_t)blockIdx.x * 64] = s;
+    }
+}
+
+__global__ void k_axpby(int64_t n, double a, const double* x, double b, double* y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = (b == 0.0) ? a * x[i] : fma(a, x[i], b * y[i]);
+}
+// z = x + a*(y - w*v)   (Bi-CGStab direction update, p = r + beta (p - omega v))
+__global__ void k_bicg_p(int64_t n, const double* __restrict__ r, double beta, double omega,
+                         const double* __restrict__ v, double* __restrict__ p) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = r[i] + beta * (p[i] - omega * v[i]);
+}
+__global__ void k_lincomb3(int64_t n, double a, const double* __restrict__ x, double b, const double* __restrict__ y,
+                           double* __restrict__ z) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        z[i] = z[i] + a * x[i] + b * y[i];
+}
+
+int grid_for(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>(RED_BLOCKS, (n + RED_THREADS - 1) / RED_THREADS)); }
+
+}  // namespace
+
+// ---------------------------------------------------------------- BLAS-1 (host-facing)
+struct Blas {
+    Ctx* c;
+    DevBuf<double> partial;  // RED_BLOCKS x 64
+    DevBuf<double> red;      // 64
+    explicit Blas(Ctx* ctx) : c(ctx), partial(ctx, (size_t)RED_BLOCKS * 64), red(ctx, 64) {}
+
+    // out_dev[k] = V_k . w for k < nvec
+    void multidot(const double* V, int64_t ldv, int nvec, const double* w, int64_t n, double* out_dev) {
+        if (nvec == 0) return;
+        dim3 grid(grid_for(n), (nvec + GROUP - 1) / GROUP);
+        Prof pr(c, "gs_multidot", 8.0 * n * (nvec + 1));
+        k_multidot<<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p);
+        k_reduce_partials<<<nvec, 32, 0, c->stream>>>(partial.p, grid.x, nvec, out_dev);
+        check_launch("multidot");
+    }
+    // out = w_in - V h  (or V h); returns nothing, norm^2 in red[0] when want_norm
+    void multiaxpy(const double* V, int64_t ldv, int nv, const double* h, double hscale, const double* w_in,
+                   double* out, int64_t n, double* norm2_dev) {
+        int g = grid_for(n);
+        Prof pr(c, "gs_multiaxpy", 8.0 * n * (nv + (w_in ? 2 : 1)));
+        k_multiaxpy<<<g, RED_THREADS, 0, c->stream>>>(V, ldv, nv, h, hscale, w_in, out, n,
+                                                       norm2_dev ? partial.p : nullptr);
+        if (norm2_dev) k_reduce_partials<<<1, 32, 0, c->stream>>>(partial.p, g, 1, norm2_dev);
+        check_launch("multiaxpy");
+    }
+    double dot(const double* x, const double* y, int64_t n) {
+        // x . y through the multidot path with V = x as a single vector
+        multidot(x, 0, 1, y, n, red.p);
+        double h;
+        EDFA_CUDA(cudaMemcpyAsync(&h, red.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        return h;
+    }
+    void axpby(int64_t n, double a, const double* x, double b, double* y) {
+        Prof pr(c, "axpby", 24.0 * n);
+        k_axpby<<<grid_for(n), RED_THREADS, 0, c->stream>>>(n, a, x, b, y);
+        check_launch("axpby");
+    }
+};
+
+// ---------------------------------------------------------------- apply
+struct ApplyWS {
+    DevBuf<double> a_f, t_f, u_c, c_c;
+};
+
+static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2,
+                          ApplyWS& ws, const double* r, double* y) {
+    const int nf = sys->A_ff->n_rows, nc = sys->A_cc->n_rows;
+    if (!ws.a_f.p && nf) {
+        ws.a_f.reset(c, nf);
+        ws.t_f.reset(c, nf);
+    }
+    if (!ws.u_c.p && nc) {
+        ws.u_c.reset(c, nc);
+        ws.c_c.reset(c, nc);
+    }
+    const double* r_f = r;
+    const double* r_c = r + nf;
+    double* y_f = y;
+    double* y_c = y + nf;
+    const IcFactor& ic = s1->ic;
+    const IluFactor& il = s2->ilu;
+    run_plan(c, ic.fwd, r_f, -1.0, ws.a_f.p, nullptr, nullptr, "trsv_ic_L");
+    run_plan(c, ic.bwd, ws.a_f.p, 1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_LT");
+    if (nc) {
+        EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
+        spmv(c, view(*sys->A_cf), sys->A_cf->nnz, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
+        run_plan(c, il.fwd, ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L");
+        run_plan(c, il.bwd, ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U");
+        spmv(c, view(*sys->A_fc), sys->A_fc->nnz, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
+    } else if (nf) {
+        EDFA_CUDA(cudaMemsetAsync(ws.a_f.p, 0, sizeof(double) * nf, c->stream));
+    }
+    if (nf) {
+        run_plan(c, ic.fwd, ws.a_f.p, 1.0, y_f, nullptr, nullptr, "trsv_ic_L");
+        // b and out2 alias row-wise only (thread r reads b[r] before writing out2[r])
+        run_plan(c, ic.bwd, y_f, 1.0, ws.a_f.p, ws.t_f.p, y_f, "trsv_ic_LT");
+    }
+}
+
+void inner_apply(Ctx* c, const edfa_stage1* s1, const edfa_stage2* s2, int which, const double* r, double* y) {
+    if (which == 0) {
+        const IcFactor& ic = s1->ic;
+        DevBuf<double> tmp(c, std::max(ic.n, 1));
+        run_plan(c, ic.fwd, r, 1.0, tmp.p, nullptr, nullptr, "trsv_ic_L");
+        run_plan(c, ic.bwd, tmp.p, 1.0, y, nullptr, nullptr, "trsv_ic_LT");
+    } else {
+        const IluFactor& il = s2->ilu;
+        DevBuf<double> tmp(c, std::max(il.n, 1));
+        run_plan(c, il.fwd, r, 1.0, tmp.p, nullptr, nullptr, "trsv_ilu_L");
+        run_plan(c, il.bwd, tmp.p, 1.0, y, nullptr, nullptr, "trsv_ilu_U");
+    }
+}
+
+// ---------------------------------------------------------------- solver plumbing
+struct Operator {
+    Ctx* c;
+    const edfa_system* sys;
+    const edfa_stage1* s1;
+    const edfa_stage2* s2;
+    ApplyWS ws;
+    int64_t n;
+    void A(const double* x, double* y) { spmv(c, view(sys->A), sys->A.nnz, x, y, 1.0, 0.0, "spmv_A"); }
+    void P(const double* x, double* y) {
+        if (s1 && s2) precond_apply(c, sys, s1, s2, ws, x, y);
+        else EDFA_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    }
+};
+
+static void check_trsv_error(Ctx* c) {
+    int e = 0;
+    EDFA_CUDA(cudaMemcpyAsync(&e, c->d_scalar_i + 8, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    if (e) {
+        EDFA_CUDA(cudaMemsetAsync(c->d_scalar_i + 8, 0, sizeof(int), c->stream));
+        throw Error(EDFA_ERR_CUDA, "triangular solve exceeded its spin limit (dependency never published)");
+    }
+}
+
+void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b, double* x,
+           double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap) {
+    require(rtol > 0.0, EDFA_ERR_VALUE, "tol must be positive");
+    require(m >= 1 && m <= 62, EDFA_ERR_VALUE, "restart must be in [1, 62]");
+    require(max_it >= 0, EDFA_ERR_VALUE, "max_it must be >= 0");
+    const int64_t n = (int64_t)sys->A.n_rows;
+    Operator op{c, sys, s1, s2, {}, n};
+    Blas bl(c);
+    *rep = edfa_report{0, 0, 0, 0, INFINITY};
+    auto push_hist = [&](double v) {
+        if (hist && rep->n_hist < hist_cap) hist[rep->n_hist] = v;
+        rep->n_hist++;
+    };
+    double bnorm = std::sqrt(bl.dot(b, b, n));
+    if (bnorm == 0.0) {
+        EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+        rep->converged = 1;
+        rep->final_relres = 0.0;
+        push_hist(0.0);
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    DevBuf<double> V(c, (size_t)(m + 1) * n), z(c, n), r(c, n), hd(c, 192);
+    double* hpin = c->h_pinned;
+    EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    double beta = bnorm;
+    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+    bool happy = false;
+    while (rep->n_it < max_it) {
+        bl.axpby(n, 1.0 / beta, r.p, 0.0, V.p);
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int k = 0;
+        for (int j = 0; j < m; ++j) {
+            double* vj = V.p + (int64_t)j * n;
+            double* w = V.p + (int64_t)(j + 1) * n;
+            op.P(vj, z.p);
+            op.A(z.p, w);
+            rep->n_it++;
+            // pass 1: h = V^T w and ||w||^2 (extra slot j+1 with V == NULL semantics -> w.w)
+            bl.multidot(V.p, n, j + 2, w, n, hd.p);             // slot j+1 = V_{j+1} . w = w.w
+            bl.multiaxpy(V.p, n, j + 1, hd.p, 1.0, w, w, n, hd.p + 64);
+            EDFA_CUDA(cudaMemcpyAsync(hpin, hd.p, sizeof(double) * 128, cudaMemcpyDeviceToHost, c->stream));
+            EDFA_CUDA(cudaStreamSynchronize(c->stream));
+            double w0 = std::sqrt(std::max(hpin[j + 1], 0.0));
+            double wn = std::sqrt(std::max(hpin[64], 0.0));
+            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hpin[i];
+            if (wn < 0.7071067811865476 * w0) {   // DGKS: second CGS pass
+                bl.multidot(V.p, n, j + 1, w, n, hd.p);
+                bl.multiaxpy(V.p, n, j + 1, hd.p, 1.0, w, w, n, hd.p + 64);
+                EDFA_CUDA(cudaMemcpyAsync(hpin, hd.p, sizeof(double) * 128, cudaMemcpyDeviceToHost, c->stream));
+                EDFA_CUDA(cudaStreamSynchronize(c->stream));
+                for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] += hpin[i];
+                wn = std::sqrt(std::max(hpin[64], 0.0));
+            }
+            H[(size_t)(j + 1) * m + j] = wn;
+            for (int i = 0; i < j; ++i) {
+                double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
+                H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
+                H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+            }
+            double den = std::hypot(H[(size_t)j * m + j], H[(size_t)(j + 1) * m + j]);
+            if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
+            else { cs[j] = H[(size_t)j * m + j] / den; sn[j] = H[(size_t)(j + 1) * m + j] / den; }
+            H[(size_t)j * m + j] = den;
+            H[(size_t)(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            double est = std::fabs(g[j + 1]) / bnorm;
+            push_hist(est);
+            k = j + 1;
+            if (wn == 0.0) { happy = true; break; }
+            bl.axpby(n, 1.0 / wn, w, 0.0, w);
+            if (est <= rtol || rep->n_it >= max_it) break;
+        }
+        for (int i = k - 1; i >= 0; --i) {   // back substitution H y = g
+            double s = g[i];
+            for (int t = i + 1; t < k; ++t) s -= H[(size_t)i * m + t] * y[t];
+            y[i] = H[(size_t)i * m + i] != 0.0 ? s / H[(size_t)i * m + i] : 0.0;
+        }
+        for (int i = 0; i < k; ++i) hpin[i] = y[i];
+        EDFA_CUDA(cudaMemcpyAsync(hd.p, hpin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
+        bl.multiaxpy(V.p, n, k, hd.p, 1.0, nullptr, r.p, n, nullptr);   // r <- V y (scratch)
+        op.P(r.p, z.p);
+        bl.axpby(n, 1.0, z.p, 1.0, x);
+        op.A(x, r.p);
+        bl.axpby(n, 1.0, b, -1.0, r.p);                                   // r = b - A x
+        beta = std::sqrt(bl.dot(r.p, r.p, n));
+        check_trsv_error(c);
+        if (beta / bnorm <= rtol) { rep->converged = 1; break; }
+        if (happy || beta == 0.0) { rep->breakdown = 1; break; }
+    }
+    rep->final_relres = beta / bnorm;
+    if (rep->n_it == 0) push_hist(beta / bnorm);
+}
+
+void bicgstab(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b,
+              double* x, double rtol, int max_it, edfa_report* rep, double* hist, int hist_cap) {
+    // operation-for-operation restatement of hx/krylov.py:40-115
+    require(rtol > 0.0, EDFA_ERR_VALUE, "tol must be positive");
+    const int64_t n = (int64_t)sys->A.n_rows;
+    Operator op{c, sys, s1, s2, {}, n};
+    Blas bl(c);
+    *rep = edfa_report{0, 0, 0, 0, INFINITY};
+    auto push_hist = [&](double v) {
+        if (hist && rep->n_hist < hist_cap) hist[rep->n_hist] = v;
+        rep->n_hist++;
+    };
+    double bnorm = std::sqrt(bl.dot(b, b, n));
+    EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+    if (bnorm == 0.0) {
+        rep->converged = 1;
+        rep->final_relres = 0.0;
+        push_hist(0.0);
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    DevBuf<double> r(c, n), rh(c, n), p(c, n), v(c, n), ph(c, n), s(c, n), sh(c, n), t(c, n);
+    EDFA_CUDA(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(rh.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    EDFA_CUDA(cudaMemsetAsync(p.p, 0, sizeof(double) * n, c->stream));
+    EDFA_CUDA(cudaMemsetAsync(v.p, 0, sizeof(double) * n, c->stream));
+    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    bool any_hist = false;
+    while (rep->n_it < max_it) {
+        double rho_new = bl.dot(rh.p, r.p, n);
+        if (rho_new == 0.0) { rep->breakdown = 1; break; }
+        double beta = (rho_new / rho) * (alpha / omega);
+        rho = rho_new;
+        {
+            Prof pr(c, "axpby", 32.0 * n);
+            k_bicg_p<<<grid_for(n), RED_THREADS, 0, c->stream>>>(n, r.p, beta, omega, v.p, p.p);
+            check_launch("k_bicg_p");
+        }
+        op.P(p.p, ph.p);
+        op.A(ph.p, v.p);
+        double den = bl.dot(rh.p, v.p, n);
+        if (den == 0.0) { rep->breakdown = 1; break; }
+        alpha = rho / den;
+        EDFA_CUDA(cudaMemcpyAsync(s.p, r.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+        bl.axpby(n, -alpha, v.p, 1.0, s.p);
+        rep->n_it++;
+        double snorm = std::sqrt(bl.dot(s.p, s.p, n));
+        if (snorm / bnorm <= rtol) {
+            bl.axpby(n, alpha, ph.p, 1.0, x);
+            push_hist(snorm / bnorm);
+            any_hist = true;
+            rep->converged = 1;
+            break;
+        }
+        op.P(s.p, sh.p);
+        op.A(sh.p, t.p);
+        double tt = bl.dot(t.p, t.p, n);
+        if (tt == 0.0) { rep->breakdown = 1; break; }
+        omega = bl.dot(t.p, s.p, n) / tt;
+        {
+            Prof pr(c, "axpby", 32.0 * n);
+            k_lincomb3<<<grid_for(n), RED_THREADS, 0, c->stream>>>(n, alpha, ph.p, omega, sh.p, x);
+            check_launch("k_lincomb3");
+        }
+        EDFA_CUDA(cudaMemcpyAsync(r.p, s.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+        bl.axpby(n, -omega, t.p, 1.0, r.p);
+        double rr = std::sqrt(bl.dot(r.p, r.p, n)) / bnorm;
+        push_hist(rr);
+        any_hist = true;
+        if (rr <= rtol) { rep->converged = 1; break; }
+        if (omega == 0.0) { rep->breakdown = 1; break; }
+    }
+    if (!any_hist) push_hist(std::sqrt(bl.dot(r.p, r.p, n)) / bnorm);
+    op.A(x, t.p);
+    bl.axpby(n, 1.0, b, -1.0, t.p);
+    rep->final_relres = std::sqrt(bl.dot(t.p, t.p, n)) / bnorm;
+    check_trsv_error(c);
+}
+
+// exported to capi.cu
+void apply_entry(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* r,
+                 double* y) {
+    ApplyWS ws;
+    precond_apply(c, sys, s1, s2, ws, r, y);
+    // workspace freed stream-ordered on return
+}
+double dot_entry(Ctx* c, int64_t n, const double* x, const double* y) {
+    Blas bl(c);
+    return bl.dot(x, y, n);
+}
+void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double* y) {
+    Blas bl(c);
+    bl.axpby(n, a, x, b, y);
+}
+
+}  // namespace edfa

@@ -1,0 +1,135 @@
+// Library objects behind the opaque C handles: system, stage 1, stage 2,
+// incomplete factors and their sync-free triangular-solve plans.
+#pragma once
+#include "edfa_internal.cuh"
+
+namespace edfa {
+
+// ---- stage-1 row kernel I/O (setup_rows.cu)
+struct SetupInput {
+    const Csr* A = nullptr;        // A_ff
+    const Csr* AT = nullptr;       // transpose of A_ff (dynamic), may be NULL -> A
+    const Csr* Acf = nullptr;
+    const Csr* AfcT = nullptr;     // A_fc^T (cells x faces)
+    const Csr* pattern = nullptr;  // static/base sets, NULL -> dynamic
+    int32_t n_add = 1, n_ent = 0, sweep_limit = 1;
+    double pre_tau = 0.0;
+};
+struct SetupOutput {
+    DevBuf<int32_t> slot_ptr, q, qsize, gcnt, fcnt;
+    DevBuf<double> g, f;
+    int64_t n_slots = 0;
+    int max_pattern = 0;
+};
+void setup_rows(Ctx* c, const SetupInput& in, SetupOutput& out);
+void compact_rows(Ctx* c, int32_t n, const DevBuf<int32_t>& slot_ptr, const int32_t* qsize, const int32_t* qidx,
+                  const double* vals, const DevBuf<int32_t>& cnt, int32_t n_cols, Csr& out);
+void pattern_compact(Ctx* c, int32_t n, const DevBuf<int32_t>& slot_ptr, const DevBuf<int32_t>& qsize,
+                     const DevBuf<int32_t>& q, int32_t n_cols, Csr& out);
+void static_pattern(Ctx* c, int32_t n_cells, int32_t n_free, const int32_t* e2f, const int32_t* nbr,
+                    const int32_t* fidx, char proto, Csr& out);
+int max_row_nnz(Ctx* c, const Csr& A);
+
+// ---- H~ = G~ A_ff F~ (product.cu)
+void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double post_tau, Csr& H);
+
+// ---- sync-free triangular solve plan (trsv.cu)
+// Rows are grouped by dependency level, each level padded to whole warps;
+// one thread per row; SELL-32 (column-major inside 32-row slices) so the
+// coefficient stream is fully coalesced.  Dependencies are polled on the
+// solution vector itself (sentinel-initialised), so there is no flag array.
+struct TriPlan {
+    int32_t n = 0;          // rows
+    int32_t n_slots = 0;    // padded thread count (multiple of 32)
+    int32_t n_levels = 0;
+    int64_t n_dep = 0;      // off-diagonal coefficients (algorithmic)
+    int64_t n_stored = 0;   // SELL entries incl. padding
+    bool unit = false;
+    DevBuf<int32_t> perm;       // slot -> row (-1 pad)
+    DevBuf<int64_t> slice_ptr;  // slice -> first SELL entry
+    DevBuf<int32_t> col;
+    DevBuf<double> val;
+    DevBuf<double> dinv;        // slot -> 1/diag (1 for unit)
+    DevBuf<int32_t> ticket;     // dynamic warp ticket
+};
+// deps: row i -> (j, coef) with x_i = (alpha*b_i - sum coef*x_j) * dinv_i;
+// reverse = deps point to higher rows (backward substitution).  diag may be
+// NULL (values loaded later with plan_values).
+void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& plan);
+void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& plan);
+// x = solve(b * alpha); if (add) out2 = x + add (fused epilogue)
+void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
+              const char* name);
+
+// ---- incomplete factors (factor.cu)
+struct IcFactor {               // IC of -A_ff (no fill)
+    int32_t n = 0;
+    Csr Lpat;                   // strictly lower part of -A_ff's pattern, values = L
+    DevBuf<double> diag;        // L_ii
+    int32_t shifts = 0;
+    TriPlan fwd, bwd;           // L y = b ; L^T x = y
+    Csr export_L;               // materialised on request
+};
+struct IluFactor {              // ILU of S (no fill)
+    int32_t n = 0;
+    Csr LU;                     // pattern of S; strict lower = multipliers, strict upper = U
+    DevBuf<double> udiag;
+    DevBuf<int32_t> has_diag;   // S stores its diagonal (for the exported nnz)
+    int32_t shifts = 0;
+    TriPlan fwd, bwd;
+    Csr export_L, export_U;
+};
+void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f);
+void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f);
+void ic_export(Ctx* c, IcFactor& f);
+void ilu_export(Ctx* c, IluFactor& f);
+
+}  // namespace edfa
+
+// ---- handle objects
+struct edfa_system {
+    edfa::Ctx* ctx;
+    const edfa::Csr* A_ff;
+    const edfa::Csr* A_fc;
+    const edfa::Csr* A_cf;
+    const edfa::Csr* A_cc;
+    edfa::Csr A;            // monolithic operator
+    edfa::Csr AfcT;         // A_fc^T, cells x faces (rows = f-rhs per cell)
+    edfa::Csr AffT;         // A_ff^T (columns of A_ff)
+    bool have_T = false;
+};
+
+struct edfa_stage1 {
+    edfa::Ctx* ctx;
+    edfa::Csr G, FT, H, Q;
+    edfa::Csr F;            // faces x cells
+    bool have_F = false;
+    edfa::IcFactor ic;
+    int32_t max_pattern = 0;
+    int32_t n_free = 0, n_cells = 0;
+    edfa_csr views[6];      // borrowed handles returned by edfa_stage1_part
+};
+
+struct edfa_stage2 {
+    edfa::Ctx* ctx;
+    edfa::Csr S;
+    edfa::IluFactor ilu;
+    edfa_csr views[3];
+};
+
+namespace edfa {
+void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynamic* dyn, double tau, int filt,
+                  double face_drop_tol, int no_fill, edfa_stage1* s1);
+void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, int filt, double schur_drop_tol,
+                  int no_fill, edfa_stage2* s2);
+void ensure_transposes(Ctx* c, edfa_system* sys, bool need_AffT);
+void apply_entry(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* r,
+                 double* y);
+void inner_apply(Ctx* c, const edfa_stage1* s1, const edfa_stage2* s2, int which, const double* r, double* y);
+void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b, double* x,
+           double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap);
+void bicgstab(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b,
+              double* x, double rtol, int max_it, edfa_report* rep, double* hist, int hist_cap);
+double dot_entry(Ctx* c, int64_t n, const double* x, const double* y);
+void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double* y);
+}  // namespace edfa

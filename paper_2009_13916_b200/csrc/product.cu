@@ -1,0 +1,254 @@
+// K3: H~ = G~ A_ff F~ (hx/precond.py:257) with the optional post-product
+// filtration fused into the epilogue (hx/precond.py:258-259, 138-157).
+//
+// Row-wise Gustavson, one warp per cell row m, two passes (count, fill):
+//   W_m = sum_{i in G_m, ascending} g_mi * A_ff[i, :]    (scipy csr_matmat order)
+//   H_m = sum_{k in W_m, ascending} W_mk * F~[k, :]
+// Both accumulators are shared-memory open-addressing tables; each
+// accumulation step adds the contributions of ONE source entry, whose target
+// columns are distinct, so lanes never collide and every sum is formed in a
+// fixed order (deterministic, bit-reproducible across runs).  Products are
+// not contracted into FMAs, as in the reference's compiled sparsetools.
+#include "dev_util.cuh"
+#include "edfa_internal.cuh"
+#include "objects.cuh"
+
+namespace edfa {
+namespace {
+
+constexpr int EMPTY = -1;
+
+__device__ __forceinline__ unsigned hslot(int key, int bits) { return ((unsigned)key * 2654435761u) >> (32 - bits); }
+
+// find-or-insert; returns slot or -1 when the table is full
+__device__ int h_insert(int* keys, int bits, int key) {
+    int mask = (1 << bits) - 1;
+    unsigned s = hslot(key, bits);
+    for (int t = 0; t <= mask; ++t) {
+        int cur = keys[s];
+        if (cur == key) return (int)s;
+        if (cur == EMPTY) {
+            int prev = atomicCAS(&keys[s], EMPTY, key);
+            if (prev == EMPTY || prev == key) return (int)s;
+        }
+        s = (s + 1) & mask;
+    }
+    return -1;
+}
+
+// compact (key, val) of a table into its front, sort by key; returns count
+__device__ int h_extract_sorted(int* keys, double* vals, int bits, int* tmpk, double* tmpv, int lane) {
+    int n_tab = 1 << bits;
+    int n = 0;
+    for (int i0 = 0; i0 < n_tab; i0 += 32) {
+        int i = i0 + lane;
+        bool live = keys[i] != EMPTY;
+        unsigned bal = __ballot_sync(0xffffffffu, live);
+        if (live) {
+            int p = n + __popc(bal & ((1u << lane) - 1));
+            tmpk[p] = keys[i];
+            tmpv[p] = vals[i];
+        }
+        n += __popc(bal);
+    }
+    __syncwarp();
+    int np2 = 32;
+    while (np2 < n) np2 <<= 1;
+    for (int i = n + lane; i < np2; i += 32) tmpk[i] = INT32_MAX;
+    __syncwarp();
+    for (int k = 2; k <= np2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < np2; i += 32) {
+                int l = i ^ j;
+                if (l > i) {
+                    int a = tmpk[i], b = tmpk[l];
+                    bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        tmpk[i] = b; tmpk[l] = a;
+                        double va = tmpv[i]; tmpv[i] = tmpv[l]; tmpv[l] = va;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    return n;
+}
+
+struct ProdArgs {
+    CsrV G, A, F;
+    int32_t n_rows;
+    const int32_t* rows;   // optional row list (overflow re-run)
+    int32_t n_list;
+    double tau;
+    int32_t* cnt;          // pass 1
+    const int32_t* Hp;     // pass 2
+    int32_t* Hi;
+    double* Hv;
+    int32_t* overflow;     // [count, rows...]
+};
+
+template <int BITS, bool FILL>
+__global__ void __launch_bounds__(256) k_product(ProdArgs a) {
+    constexpr int T = 1 << BITS;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // per warp: table keys/vals, sorted W (keys/vals), H table keys/vals
+    unsigned char* base = smem + (size_t)wid * T * (4 + 8) * 3;
+    double* tv = reinterpret_cast<double*>(base);
+    double* wv = tv + T;
+    double* hv = wv + T;
+    int* tk = reinterpret_cast<int*>(hv + T);
+    int* wk = tk + T;
+    int* hk = wk + T;
+    int n_items = a.rows ? a.n_list : a.n_rows;
+    for (int it = blockIdx.x * warps + wid; it < n_items; it += gridDim.x * warps) {
+        int m = a.rows ? a.rows[it] : it;
+        for (int i = lane; i < T; i += 32) { tk[i] = EMPTY; tv[i] = 0.0; hk[i] = EMPTY; hv[i] = 0.0; }
+        __syncwarp();
+        bool full = false;
+        // ---- W = g_m A_ff
+        int g0 = a.G.ptr[m], g1 = a.G.ptr[m + 1];
+        for (int t = g0; t < g1; ++t) {
+            int i = a.G.idx[t];
+            double g = a.G.val[t];
+            for (int e = a.A.ptr[i] + lane; e < a.A.ptr[i + 1]; e += 32) {
+                int s = h_insert(tk, BITS, a.A.idx[e]);
+                if (s < 0) full = true;
+                else tv[s] = add_mul(tv[s], g, a.A.val[e]);
+            }
+            __syncwarp();
+        }
+        full = __any_sync(0xffffffffu, full);
+        int nW = 0;
+        if (!full) nW = h_extract_sorted(tk, tv, BITS, wk, wv, lane);
+        // ---- H = W F
+        if (!full) {
+            for (int t = 0; t < nW; ++t) {
+                double w = wv[t];
+                if (w == 0.0) continue;          // scipy drops exact-zero sums of W
+                int k = wk[t];
+                for (int e = a.F.ptr[k] + lane; e < a.F.ptr[k + 1]; e += 32) {
+                    int s = h_insert(hk, BITS, a.F.idx[e]);
+                    if (s < 0) full = true;
+                    else hv[s] = add_mul(hv[s], w, a.F.val[e]);
+                }
+                __syncwarp();
+            }
+            full = __any_sync(0xffffffffu, full);
+        }
+        if (full) {
+            if (lane == 0) {
+                if (!FILL) a.cnt[m] = 0;
+                int p = atomicAdd(a.overflow, 1);
+                a.overflow[1 + p] = m;
+            }
+            __syncwarp();
+            continue;
+        }
+        int nH = h_extract_sorted(hk, hv, BITS, tk, tv, lane);   // sorted H row in (tk, tv)
+        double thr = 0.0;
+        if (a.tau > 0.0) {
+            double ss = 0.0;
+            for (int i = lane; i < nH; i += 32) ss += tv[i] * tv[i];
+            thr = a.tau * sqrt(warp_sum(ss));
+        }
+        int o = FILL ? a.Hp[m] : 0, n = 0;
+        for (int i0 = 0; i0 < nH; i0 += 32) {
+            int i = i0 + lane;
+            double v = i < nH ? tv[i] : 0.0;
+            int col = i < nH ? tk[i] : -1;
+            bool keep = i < nH && v != 0.0 && (col == m || !(fabs(v) < thr));
+            unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (FILL && keep) {
+                int p = o + n + __popc(bal & ((1u << lane) - 1));
+                a.Hi[p] = col;
+                a.Hv[p] = v;
+            }
+            n += __popc(bal);
+        }
+        if (!FILL && lane == 0) a.cnt[m] = n;
+        __syncwarp();
+    }
+}
+
+template <int BITS, bool FILL>
+void launch_product(Ctx* c, const ProdArgs& a) {
+    constexpr int T = 1 << BITS;
+    size_t pw = (size_t)T * 12 * 3;
+    int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / pw));
+    size_t sm = pw * warps;
+    auto kern = k_product<BITS, FILL>;
+    EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int items = a.rows ? a.n_list : a.n_rows;
+    int per_sm = std::max(1, (int)((227 * 1024) / sm));
+    int blocks = std::max(1, std::min(ceil_div(items, warps), NUM_SMS_B200 * per_sm * 4));
+    kern<<<blocks, warps * 32, sm, c->stream>>>(a);
+    check_launch("k_product");
+}
+
+template <bool FILL>
+void run_pass(Ctx* c, ProdArgs a, int32_t* ovf_dev, std::vector<int32_t>& ovf_rows, bool retry) {
+    int init = 0;
+    if (!retry) {
+        EDFA_CUDA(cudaMemcpyAsync(ovf_dev, &init, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        a.overflow = ovf_dev;
+        launch_product<8, FILL>(c, a);
+        int n_ovf = 0;
+        EDFA_CUDA(cudaMemcpyAsync(&n_ovf, ovf_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        ovf_rows.assign(n_ovf, 0);
+        if (n_ovf)
+            EDFA_CUDA(cudaMemcpyAsync(ovf_rows.data(), ovf_dev + 1, sizeof(int) * n_ovf, cudaMemcpyDeviceToHost,
+                                      c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    if (ovf_rows.empty()) return;
+    DevBuf<int32_t> rows(c, ovf_rows.size());
+    EDFA_CUDA(cudaMemcpyAsync(rows.p, ovf_rows.data(), sizeof(int) * ovf_rows.size(), cudaMemcpyHostToDevice,
+                              c->stream));
+    ProdArgs b = a;
+    b.rows = rows.p;
+    b.n_list = (int32_t)ovf_rows.size();
+    EDFA_CUDA(cudaMemcpyAsync(ovf_dev, &init, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    b.overflow = ovf_dev;
+    launch_product<12, FILL>(c, b);
+    int n2 = 0;
+    EDFA_CUDA(cudaMemcpyAsync(&n2, ovf_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    require(n2 == 0, EDFA_ERR_UNSUPPORTED, "H~ row exceeds 4096 distinct columns");
+}
+
+}  // namespace
+
+void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double post_tau, Csr& H) {
+    const int n = G.n_rows;
+    H.n_rows = n;
+    H.n_cols = F.n_cols;
+    H.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    DevBuf<int32_t> ovf(c, (size_t)n + 1);
+    ProdArgs a{};
+    a.G = view(G);
+    a.A = view(A);
+    a.F = view(F);
+    a.n_rows = n;
+    a.tau = post_tau;
+    a.cnt = cnt.p;
+    std::vector<int32_t> ovf_rows;
+    if (n) {
+        Prof pr(c, "product_count", 12.0 * (G.nnz + A.nnz + F.nnz));
+        run_pass<false>(c, a, ovf.p, ovf_rows, false);
+    }
+    H.nnz = scan_counts(c, cnt.p, H.ptr.p, n);
+    H.idx.reset(c, H.nnz);
+    H.val.reset(c, H.nnz);
+    if (n) {
+        a.Hp = H.ptr.p;
+        a.Hi = H.idx.p;
+        a.Hv = H.val.p;
+        Prof pr(c, "product_fill", 12.0 * (G.nnz + A.nnz + F.nnz + H.nnz));
+        run_pass<true>(c, a, ovf.p, ovf_rows, false);
+    }
+}
+
+}  // namespace edfa

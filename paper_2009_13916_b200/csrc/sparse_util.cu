@@ -1,0 +1,341 @@
+// Sparse plumbing kernels: scans, transpose, block merge, SpMV, S = A - H,
+// row filtration.  All HBM-bound integer/FP64 streaming work.
+#include <cub/cub.cuh>
+
+#include "dev_util.cuh"
+#include "edfa_internal.cuh"
+
+namespace edfa {
+
+namespace {
+
+__global__ void k_incl_to_ptr(const int64_t* __restrict__ incl, int32_t* __restrict__ ptr, int32_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i == 0) ptr[0] = 0;
+    if (i < n) ptr[i + 1] = (int32_t)incl[i];
+}
+
+struct ToI64 {
+    __host__ __device__ int64_t operator()(int32_t v) const { return (int64_t)v; }
+};
+
+__global__ void k_fill(double* p, int64_t n, double v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+__global__ void k_fill_bits(unsigned long long* p, int64_t n, unsigned long long v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+__global__ void k_row_of(const int32_t* __restrict__ ptr, int32_t n, int32_t* __restrict__ row_of) {
+    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= n) return;
+    for (int e = ptr[w] + lane; e < ptr[w + 1]; e += 32) row_of[e] = w;
+}
+__global__ void k_iota(int32_t* p, int64_t n) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = (int32_t)i;
+}
+__global__ void k_col_hist(const int32_t* __restrict__ idx, int64_t nnz, int32_t* __restrict__ cnt) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nnz) atomicAdd(&cnt[idx[i]], 1);
+}
+__global__ void k_gather_T(const int32_t* __restrict__ order, const int32_t* __restrict__ row_of,
+                           const double* __restrict__ val, int64_t nnz, int32_t* __restrict__ out_idx,
+                           double* __restrict__ out_val) {
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= nnz) return;
+    int32_t e = order[p];
+    out_idx[p] = row_of[e];
+    if (val) out_val[p] = val[e];
+}
+
+__global__ void k_merge_ptr(const int32_t* A, const int32_t* B, const int32_t* C, const int32_t* D, int32_t nA,
+                            int32_t nC, int32_t* M) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i <= nA) M[i] = A[i] + B[i];
+    else if (i <= nA + nC) {
+        int k = (int)(i - nA);
+        M[i] = A[nA] + B[nA] + C[k] + D[k];
+    }
+}
+__global__ void k_merge_fill(CsrV A, CsrV B, CsrV C, CsrV D, const int32_t* __restrict__ Mp,
+                             int32_t* __restrict__ Mi, double* __restrict__ Mv) {
+    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    int n = A.n_rows + C.n_rows;
+    if (w >= n) return;
+    const CsrV& L = w < A.n_rows ? A : C;
+    const CsrV& R = w < A.n_rows ? B : D;
+    int r = w < A.n_rows ? w : w - A.n_rows;
+    int off = A.n_cols;
+    int o = Mp[w];
+    int l0 = L.ptr[r], l1 = L.ptr[r + 1], r0 = R.ptr[r], r1 = R.ptr[r + 1];
+    for (int e = l0 + lane; e < l1; e += 32) {
+        Mi[o + e - l0] = L.idx[e];
+        Mv[o + e - l0] = L.val[e];
+    }
+    o += l1 - l0;
+    for (int e = r0 + lane; e < r1; e += 32) {
+        Mi[o + e - r0] = R.idx[e] + off;
+        Mv[o + e - r0] = R.val[e];
+    }
+}
+
+// vector-CSR SpMV: G lanes per row
+template <int G>
+__global__ void __launch_bounds__(256) k_spmv(CsrV A, const double* __restrict__ x, double* __restrict__ y,
+                                              double alpha, double beta) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int row = (int)(t / G);
+    int sub = (int)(t % G);
+    if (row >= A.n_rows) return;
+    int e0 = A.ptr[row], e1 = A.ptr[row + 1];
+    double s = 0.0;
+    for (int e = e0 + sub; e < e1; e += G) s = fma(A.val[e], __ldg(x + A.idx[e]), s);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+    if (sub == 0) y[row] = (beta == 0.0) ? alpha * s : fma(beta, y[row], alpha * s);
+}
+
+// S = A - H, thread per row, two passes (count / fill); tau > 0 -> filter_rows
+template <bool FILL>
+__global__ void k_sub(CsrV A, CsrV H, double tau, int32_t* __restrict__ cnt, const int32_t* __restrict__ Sp,
+                      int32_t* __restrict__ Si, double* __restrict__ Sv) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n_rows) return;
+    int a = A.ptr[i], a1 = A.ptr[i + 1], h = H.ptr[i], h1 = H.ptr[i + 1];
+    double thr = 0.0;
+    if (tau > 0.0) {
+        double ss = 0.0;
+        int p = a, q = h;
+        while (p < a1 || q < h1) {
+            int ca = p < a1 ? A.idx[p] : INT32_MAX, ch = q < h1 ? H.idx[q] : INT32_MAX;
+            double v;
+            if (ca == ch) v = A.val[p++] - H.val[q++];
+            else if (ca < ch) v = A.val[p++];
+            else v = 0.0 - H.val[q++];
+            ss += v * v;
+        }
+        thr = tau * sqrt(ss);
+    }
+    int o = FILL ? Sp[i] : 0, n = 0;
+    int p = a, q = h;
+    while (p < a1 || q < h1) {
+        int ca = p < a1 ? A.idx[p] : INT32_MAX, ch = q < h1 ? H.idx[q] : INT32_MAX;
+        double v;
+        int col;
+        if (ca == ch) { col = ca; v = A.val[p++] - H.val[q++]; }
+        else if (ca < ch) { col = ca; v = A.val[p++]; }
+        else { col = ch; v = 0.0 - H.val[q++]; }
+        bool keep = v != 0.0 && (col == i || !(fabs(v) < thr));
+        if (keep) {
+            if (FILL) { Si[o + n] = col; Sv[o + n] = v; }
+            ++n;
+        }
+    }
+    if (!FILL) cnt[i] = n;
+}
+
+template <bool FILL>
+__global__ void k_filter(CsrV A, double tau, int32_t* __restrict__ cnt, const int32_t* __restrict__ Sp,
+                         int32_t* __restrict__ Si, double* __restrict__ Sv) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n_rows) return;
+    int a = A.ptr[i], a1 = A.ptr[i + 1];
+    double ss = 0.0;
+    for (int p = a; p < a1; ++p) ss += A.val[p] * A.val[p];
+    double thr = tau * sqrt(ss);
+    int o = FILL ? Sp[i] : 0, n = 0;
+    for (int p = a; p < a1; ++p) {
+        double v = A.val[p];
+        int col = A.idx[p];
+        if (v != 0.0 && (col == i || !(fabs(v) < thr))) {
+            if (FILL) { Si[o + n] = col; Sv[o + n] = v; }
+            ++n;
+        }
+    }
+    if (!FILL) cnt[i] = n;
+}
+
+}  // namespace
+
+int64_t scan_counts(Ctx* c, const int32_t* counts, int32_t* ptr_out, int32_t n) {
+    if (n == 0) {
+        EDFA_CUDA(cudaMemsetAsync(ptr_out, 0, sizeof(int32_t), c->stream));
+        return 0;
+    }
+    DevBuf<int64_t> incl(c, n);
+    cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(counts, ToI64());
+    size_t bytes = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, bytes, it, incl.p, n, c->stream);
+    void* tmp = c->cub_scratch(bytes);
+    {
+        Prof pr(c, "scan", 12.0 * n);
+        EDFA_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, it, incl.p, n, c->stream));
+        k_incl_to_ptr<<<ceil_div(n, 256), 256, 0, c->stream>>>(incl.p, ptr_out, n);
+        check_launch("k_incl_to_ptr");
+    }
+    int64_t total = 0;
+    EDFA_CUDA(cudaMemcpyAsync(&total, incl.p + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    require(total <= INT32_MAX, EDFA_ERR_UNSUPPORTED, "matrix exceeds 2^31-1 stored entries");
+    return total;
+}
+
+void fill(Ctx* c, double* p, int64_t n, double v) {
+    if (n <= 0) return;
+    Prof pr(c, "fill", 8.0 * n);
+    int blocks = std::min<int64_t>(ceil_div(n, 256), NUM_SMS_B200 * 8);
+    k_fill<<<blocks, 256, 0, c->stream>>>(p, n, v);
+    check_launch("k_fill");
+}
+void fill_bits(Ctx* c, double* p, int64_t n, unsigned long long bits) {
+    if (n <= 0) return;
+    Prof pr(c, "fill", 8.0 * n);
+    int blocks = std::min<int64_t>(ceil_div(n, 256), NUM_SMS_B200 * 8);
+    k_fill_bits<<<blocks, 256, 0, c->stream>>>(reinterpret_cast<unsigned long long*>(p), n, bits);
+    check_launch("k_fill_bits");
+}
+
+void transpose(Ctx* c, const Csr& A, Csr& AT) {
+    AT.n_rows = A.n_cols;
+    AT.n_cols = A.n_rows;
+    AT.nnz = A.nnz;
+    AT.ptr.reset(c, (size_t)A.n_cols + 1);
+    AT.idx.reset(c, A.nnz);
+    if (A.val.p) AT.val.reset(c, A.nnz);
+    else AT.val.release();
+    DevBuf<int32_t> cnt(c, std::max<int32_t>(A.n_cols, 1));
+    EDFA_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * std::max<int32_t>(A.n_cols, 1), c->stream));
+    if (A.nnz == 0) {
+        EDFA_CUDA(cudaMemsetAsync(AT.ptr.p, 0, sizeof(int32_t) * (A.n_cols + 1), c->stream));
+        return;
+    }
+    DevBuf<int32_t> row_of(c, A.nnz), ids(c, A.nnz), keys_out(c, A.nnz), order(c, A.nnz);
+    {
+        Prof pr(c, "transpose", 24.0 * A.nnz + 8.0 * A.n_rows);
+        k_row_of<<<ceil_div((int64_t)A.n_rows * 32, 256), 256, 0, c->stream>>>(A.ptr.p, A.n_rows, row_of.p);
+        k_iota<<<ceil_div(A.nnz, 256), 256, 0, c->stream>>>(ids.p, A.nnz);
+        k_col_hist<<<ceil_div(A.nnz, 256), 256, 0, c->stream>>>(A.idx.p, A.nnz, cnt.p);
+        check_launch("transpose prep");
+    }
+    scan_counts(c, cnt.p, AT.ptr.p, A.n_cols);
+    int bits = 1;
+    while ((1ll << bits) < (int64_t)A.n_cols) ++bits;
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, A.idx.p, keys_out.p, ids.p, order.p, (int)A.nnz, 0, bits,
+                                    c->stream);
+    void* tmp = c->cub_scratch(bytes);
+    {
+        Prof pr(c, "transpose", 32.0 * A.nnz);
+        EDFA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, A.idx.p, keys_out.p, ids.p, order.p, (int)A.nnz, 0,
+                                                  bits, c->stream));
+        k_gather_T<<<ceil_div(A.nnz, 256), 256, 0, c->stream>>>(order.p, row_of.p, A.val.p, A.nnz, AT.idx.p,
+                                                                AT.val.p);
+        check_launch("k_gather_T");
+    }
+}
+
+void block_merge(Ctx* c, const Csr& A, const Csr& B, const Csr& C, const Csr& D, Csr& M) {
+    require(A.n_rows == B.n_rows && C.n_rows == D.n_rows && A.n_cols == C.n_cols && B.n_cols == D.n_cols,
+            EDFA_ERR_VALUE, "block shapes are inconsistent");
+    M.n_rows = A.n_rows + C.n_rows;
+    M.n_cols = A.n_cols + B.n_cols;
+    M.nnz = A.nnz + B.nnz + C.nnz + D.nnz;
+    require(M.nnz <= INT32_MAX, EDFA_ERR_UNSUPPORTED, "system exceeds 2^31-1 stored entries");
+    M.ptr.reset(c, (size_t)M.n_rows + 1);
+    M.idx.reset(c, M.nnz);
+    M.val.reset(c, M.nnz);
+    Prof pr(c, "block_merge", 24.0 * M.nnz);
+    k_merge_ptr<<<ceil_div(M.n_rows + 1, 256), 256, 0, c->stream>>>(A.ptr.p, B.ptr.p, C.ptr.p, D.ptr.p, A.n_rows,
+                                                                   C.n_rows, M.ptr.p);
+    k_merge_fill<<<ceil_div((int64_t)M.n_rows * 32, 256), 256, 0, c->stream>>>(view(A), view(B), view(C), view(D),
+                                                                              M.ptr.p, M.idx.p, M.val.p);
+    check_launch("block_merge");
+}
+
+void spmv(Ctx* c, const CsrV& A, int64_t nnz, const double* x, double* y, double alpha, double beta,
+          const char* name) {
+    if (A.n_rows == 0) return;
+    double avg = A.n_rows ? double(nnz) / A.n_rows : 0.0;
+    Prof pr(c, name, 12.0 * nnz + 4.0 * (A.n_rows + 1) + 8.0 * A.n_cols + 8.0 * A.n_rows * (beta != 0.0 ? 2 : 1));
+    auto launch = [&](auto kern, int G) {
+        int64_t threads = (int64_t)A.n_rows * G;
+        kern<<<ceil_div(threads, 256), 256, 0, c->stream>>>(A, x, y, alpha, beta);
+    };
+    if (avg <= 3.0) launch(k_spmv<1>, 1);
+    else if (avg <= 6.0) launch(k_spmv<2>, 2);
+    else if (avg <= 12.0) launch(k_spmv<4>, 4);
+    else if (avg <= 24.0) launch(k_spmv<8>, 8);
+    else if (avg <= 48.0) launch(k_spmv<16>, 16);
+    else launch(k_spmv<32>, 32);
+    check_launch("k_spmv");
+}
+
+void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S) {
+    require(A.n_rows == H.n_rows && A.n_cols == H.n_cols, EDFA_ERR_VALUE, "A_cc and H shapes differ");
+    int n = A.n_rows;
+    S.n_rows = n;
+    S.n_cols = A.n_cols;
+    S.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    if (n) {
+        Prof pr(c, "schur_sub", 12.0 * (A.nnz + H.nnz) + 8.0 * n);
+        k_sub<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), view(H), tau, cnt.p, nullptr, nullptr,
+                                                             nullptr);
+        check_launch("k_sub count");
+    }
+    S.nnz = scan_counts(c, cnt.p, S.ptr.p, n);
+    S.idx.reset(c, S.nnz);
+    S.val.reset(c, S.nnz);
+    if (n) {
+        Prof pr(c, "schur_sub", 12.0 * (A.nnz + H.nnz + S.nnz) + 8.0 * n);
+        k_sub<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), view(H), tau, nullptr, S.ptr.p, S.idx.p,
+                                                            S.val.p);
+        check_launch("k_sub fill");
+    }
+}
+
+void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out) {
+    int n = A.n_rows;
+    out.n_rows = n;
+    out.n_cols = A.n_cols;
+    out.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    if (n) {
+        Prof pr(c, "filter_rows", 12.0 * A.nnz);
+        k_filter<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), tau, cnt.p, nullptr, nullptr, nullptr);
+        check_launch("k_filter count");
+    }
+    out.nnz = scan_counts(c, cnt.p, out.ptr.p, n);
+    out.idx.reset(c, out.nnz);
+    out.val.reset(c, out.nnz);
+    if (n) {
+        Prof pr(c, "filter_rows", 12.0 * (A.nnz + out.nnz));
+        k_filter<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), tau, nullptr, out.ptr.p, out.idx.p,
+                                                               out.val.p);
+        check_launch("k_filter fill");
+    }
+}
+
+void copy_csr(Ctx* c, const Csr& A, Csr& out) {
+    out.n_rows = A.n_rows;
+    out.n_cols = A.n_cols;
+    out.nnz = A.nnz;
+    out.ptr.reset(c, (size_t)A.n_rows + 1);
+    out.idx.reset(c, A.nnz);
+    EDFA_CUDA(cudaMemcpyAsync(out.ptr.p, A.ptr.p, sizeof(int32_t) * (A.n_rows + 1), cudaMemcpyDeviceToDevice,
+                              c->stream));
+    if (A.nnz)
+        EDFA_CUDA(cudaMemcpyAsync(out.idx.p, A.idx.p, sizeof(int32_t) * A.nnz, cudaMemcpyDeviceToDevice,
+                                  c->stream));
+    if (A.val.p) {
+        out.val.reset(c, A.nnz);
+        if (A.nnz)
+            EDFA_CUDA(cudaMemcpyAsync(out.val.p, A.val.p, sizeof(double) * A.nnz, cudaMemcpyDeviceToDevice,
+                                      c->stream));
+    }
+}
+
+}  // namespace edfa

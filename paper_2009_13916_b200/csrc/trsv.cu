@@ -1,0 +1,261 @@
+// K8: sync-free, level-ordered triangular solves (InnerFactorization.apply,
+// hx/sparse.py:125-129) and the plan construction they need.
+//
+// Plan: dependency levels are computed once on the device (sync-free, one
+// thread per row); rows are sorted by level and each level is padded to whole
+// warps, so a warp never waits on itself; coefficients are stored SELL-32
+// (column-major inside 32-row slices) so every coefficient load is coalesced.
+// Solve: warps take slices in level order from an atomic ticket (deadlock-free
+// without relying on block scheduling order), each thread polls the solution
+// entries its row depends on -- the solution vector is sentinel-initialised,
+// so the value is its own ready flag -- and publishes its own entry.
+#include <cub/cub.cuh>
+
+#include "dev_util.cuh"
+#include "edfa_internal.cuh"
+#include "objects.cuh"
+
+namespace edfa {
+namespace {
+
+constexpr int LEVEL_UNSET = -1;
+
+// level[i] = 1 + max(level[j], j in deps(i)); rows visited in dependency order
+__global__ void k_levels(CsrV D, bool reverse, int* __restrict__ level, int* __restrict__ ticket,
+                         int* __restrict__ max_level, int* __restrict__ err) {
+    __shared__ int base[8];
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) base[wid] = atomicAdd(ticket, 1) * 32;
+    __syncwarp();
+    int t = base[wid] + lane;
+    if (t >= D.n_rows) return;
+    int i = reverse ? D.n_rows - 1 - t : t;
+    int lv = 0;
+    for (int e = D.ptr[i]; e < D.ptr[i + 1]; ++e) {
+        int j = D.idx[e];
+        int v = ld_relaxed_i(level + j);
+        long long spins = 0;
+        while (v == LEVEL_UNSET) {
+            if (++spins > SPIN_LIMIT) { atomicExch(err, 1); v = 0; break; }
+            v = ld_relaxed_i(level + j);
+        }
+        lv = max(lv, v + 1);
+    }
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(level + i), "r"(lv) : "memory");
+    atomicMax(max_level, lv);
+}
+
+__global__ void k_fill_int(int* p, int64_t n, int v) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+__global__ void k_iota_i(int* p, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = i;
+}
+__global__ void k_level_hist(const int* __restrict__ level, int n, int* __restrict__ cnt) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[level[i]], 1);
+}
+__global__ void k_pad_counts(const int* __restrict__ cnt, int nl, int* __restrict__ pcnt) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nl) pcnt[i] = (cnt[i] + 31) & ~31;
+}
+// perm[pstart[L] + (t - ustart[L])] = row
+__global__ void k_scatter_perm(const int* __restrict__ skeys, const int* __restrict__ srows, int n,
+                               const int* __restrict__ ustart, const int* __restrict__ pstart,
+                               int* __restrict__ perm) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int L = skeys[t];
+    perm[pstart[L] + (t - ustart[L])] = srows[t];
+}
+__global__ void k_slice_width(const int* __restrict__ perm, int n_slices, const int32_t* __restrict__ dptr,
+                              int64_t* __restrict__ wbytes) {
+    int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (s >= n_slices) return;
+    int r = perm[s * 32 + lane];
+    int len = r >= 0 ? dptr[r + 1] - dptr[r] : 0;
+    len = warp_max(len);
+    if (lane == 0) wbytes[s] = (int64_t)len * 32;
+}
+__global__ void k_fill_sell(const int* __restrict__ perm, int n_slices, CsrV D, const int64_t* __restrict__ sptr,
+                            int32_t* __restrict__ col, double* __restrict__ val, const double* __restrict__ diag,
+                            bool unit, double* __restrict__ dinv) {
+    int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (s >= n_slices) return;
+    int r = perm[s * 32 + lane];
+    int64_t b = sptr[s];
+    int w = (int)((sptr[s + 1] - b) / 32);
+    int e0 = r >= 0 ? D.ptr[r] : 0, len = r >= 0 ? D.ptr[r + 1] - e0 : 0;
+    for (int k = 0; k < w; ++k) {
+        bool live = k < len;
+        if (col) col[b + (int64_t)k * 32 + lane] = live ? D.idx[e0 + k] : -1;
+        if (val) val[b + (int64_t)k * 32 + lane] = live && D.val ? D.val[e0 + k] : 0.0;
+    }
+    if (dinv) dinv[s * 32 + lane] = (r < 0 || unit) ? 1.0 : 1.0 / diag[r];
+}
+
+struct SolveArgs {
+    const int* perm;
+    const int64_t* sptr;
+    const int32_t* col;
+    const double* val;
+    const double* dinv;
+    int n_slices;
+    const double* b;
+    double alpha;
+    double* x;
+    const double* add;
+    double* out2;
+    int* ticket;
+    int* err;
+};
+
+template <int U>
+__global__ void __launch_bounds__(256) k_trsv(SolveArgs a) {
+    __shared__ int base[8];
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) base[wid] = atomicAdd(a.ticket, 1);
+    __syncwarp();
+    int s = base[wid];
+    if (s >= a.n_slices) return;
+    int slot = s * 32 + lane;
+    int r = a.perm[slot];
+    if (r < 0) return;
+    int64_t b0 = a.sptr[s];
+    int w = (int)((a.sptr[s + 1] - b0) / 32);
+    double acc = a.alpha * __ldg(a.b + r);
+    const int32_t* cp = a.col + b0 + lane;
+    const double* vp = a.val + b0 + lane;
+    for (int k0 = 0; k0 < w; k0 += U) {
+        int c[U];
+        double v[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            bool in = k0 + u < w;
+            c[u] = in ? __ldg(cp + (int64_t)(k0 + u) * 32) : -1;
+            v[u] = in ? __ldg(vp + (int64_t)(k0 + u) * 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? ld_relaxed(a.x + c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (c[u] >= 0) {
+                long long spins = 0;
+                while (is_sentinel(xv[u])) {
+                    if (++spins > SPIN_LIMIT) { atomicExch(a.err, 2); xv[u] = 0.0; break; }
+                    xv[u] = ld_relaxed(a.x + c[u]);
+                }
+                acc = fma(-v[u], xv[u], acc);
+            }
+        }
+    }
+    double xr = publishable(acc * a.dinv[slot]);
+    st_relaxed(a.x + r, xr);
+    if (a.out2) a.out2[r] = xr + a.add[r];
+}
+
+}  // namespace
+
+// Build the level-ordered SELL plan for deps (pattern and, optionally, values).
+void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& p) {
+    const int n = deps.n_rows;
+    p.n = n;
+    p.unit = unit;
+    p.n_dep = deps.nnz;
+    p.ticket.reset(c, 1);
+    if (n == 0) {
+        p.n_slots = 0;
+        p.n_levels = 0;
+        p.perm.release();
+        p.slice_ptr.reset(c, 1);
+        EDFA_CUDA(cudaMemsetAsync(p.slice_ptr.p, 0, sizeof(int64_t), c->stream));
+        return;
+    }
+    DevBuf<int> level(c, n), rows(c, n), skeys(c, n), srows(c, n);
+    int* scal = c->d_scalar_i + 16;   // [ticket, max_level, err]
+    EDFA_CUDA(cudaMemsetAsync(scal, 0, 3 * sizeof(int), c->stream));
+    {
+        Prof pr(c, "trsv_levels", 4.0 * deps.nnz + 8.0 * n);
+        k_fill_int<<<ceil_div(n, 256), 256, 0, c->stream>>>(level.p, n, LEVEL_UNSET);
+        k_levels<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(deps), reverse, level.p, scal, scal + 1, scal + 2);
+        check_launch("k_levels");
+    }
+    int hs[3];
+    EDFA_CUDA(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    require(hs[2] == 0, EDFA_ERR_CUDA, "level computation did not converge (dependency cycle?)");
+    int nl = hs[1] + 1;
+    p.n_levels = nl;
+    // sort rows by level (stable: natural order inside a level)
+    k_iota_i<<<ceil_div(n, 256), 256, 0, c->stream>>>(rows.p, n);
+    int bits = 1;
+    while ((1 << bits) <= nl) ++bits;
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, level.p, skeys.p, rows.p, srows.p, n, 0, bits, c->stream);
+    EDFA_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_scratch(bytes), bytes, level.p, skeys.p, rows.p, srows.p, n, 0,
+                                              bits, c->stream));
+    DevBuf<int> cnt(c, nl), pcnt(c, nl), ustart(c, nl + 1), pstart(c, nl + 1);
+    EDFA_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int) * nl, c->stream));
+    k_level_hist<<<ceil_div(n, 256), 256, 0, c->stream>>>(level.p, n, cnt.p);
+    k_pad_counts<<<ceil_div(nl, 256), 256, 0, c->stream>>>(cnt.p, nl, pcnt.p);
+    check_launch("level hist");
+    scan_counts(c, cnt.p, ustart.p, nl);
+    int64_t slots = scan_counts(c, pcnt.p, pstart.p, nl);
+    p.n_slots = (int32_t)slots;
+    p.perm.reset(c, slots);
+    k_fill_int<<<ceil_div(slots, 256), 256, 0, c->stream>>>(p.perm.p, slots, -1);
+    k_scatter_perm<<<ceil_div(n, 256), 256, 0, c->stream>>>(skeys.p, srows.p, n, ustart.p, pstart.p, p.perm.p);
+    check_launch("k_scatter_perm");
+    int n_slices = (int)(slots / 32);
+    DevBuf<int64_t> wb(c, (size_t)n_slices + 1);
+    k_slice_width<<<ceil_div((int64_t)n_slices * 32, 256), 256, 0, c->stream>>>(p.perm.p, n_slices, deps.ptr.p,
+                                                                               wb.p);
+    check_launch("k_slice_width");
+    p.slice_ptr.reset(c, (size_t)n_slices + 1);
+    {
+        size_t b2 = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, b2, wb.p, p.slice_ptr.p, n_slices + 1, c->stream);
+        EDFA_CUDA(cudaMemsetAsync(wb.p + n_slices, 0, sizeof(int64_t), c->stream));
+        EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(b2), b2, wb.p, p.slice_ptr.p, n_slices + 1, c->stream));
+    }
+    int64_t stored = 0;
+    EDFA_CUDA(cudaMemcpyAsync(&stored, p.slice_ptr.p + n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    p.n_stored = stored;
+    p.col.reset(c, std::max<int64_t>(stored, 1));
+    p.val.reset(c, std::max<int64_t>(stored, 1));
+    p.dinv.reset(c, std::max<int64_t>(slots, 1));
+    Prof pr(c, "trsv_plan", 12.0 * stored + 8.0 * slots);
+    k_fill_sell<<<ceil_div((int64_t)n_slices * 32, 256), 256, 0, c->stream>>>(
+        p.perm.p, n_slices, view(deps), p.slice_ptr.p, p.col.p, deps.val.p ? p.val.p : nullptr, diag, unit,
+        diag || unit ? p.dinv.p : nullptr);
+    check_launch("k_fill_sell");
+}
+
+// (Re)load coefficient values and diagonal of an existing plan from deps.
+void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& p) {
+    int n_slices = p.n_slots / 32;
+    if (n_slices == 0) return;
+    Prof pr(c, "trsv_plan", 20.0 * p.n_stored);
+    k_fill_sell<<<ceil_div((int64_t)n_slices * 32, 256), 256, 0, c->stream>>>(
+        p.perm.p, n_slices, view(deps), p.slice_ptr.p, nullptr, p.val.p, diag, p.unit, p.dinv.p);
+    check_launch("k_fill_sell values");
+}
+
+void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
+              const char* name) {
+    if (p.n == 0) return;
+    fill_bits(c, x, p.n, SENTINEL_BITS);
+    EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
+    SolveArgs a{p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.n_slots / 32, b, alpha, x, add, out2,
+                p.ticket.p, c->d_scalar_i + 8};
+    double bytes = 12.0 * p.n_dep + 8.0 * p.n + 16.0 * p.n + (out2 ? 16.0 * p.n : 0.0);
+    Prof pr(c, name, bytes);
+    int n_slices = p.n_slots / 32;
+    k_trsv<4><<<ceil_div(n_slices, 8), 256, 0, c->stream>>>(a);
+    check_launch("k_trsv");
+}
+
+}  // namespace edfa

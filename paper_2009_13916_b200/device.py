@@ -1,0 +1,220 @@
+"""Device-resident matrices and block systems behind the drop-in API.
+
+PyTorch supplies the CUDA stream and the memory of vectors; matrices live in
+libedfa-owned device memory (stream-ordered pool) and are addressed through
+opaque handles.  Nothing here computes: every operation is a libedfa call.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib as L
+
+_CTX: dict[int, C.c_void_p] = {}
+
+
+def ctx(device: int | None = None) -> C.c_void_p:
+    """Context for a CUDA device, bound to torch's current stream."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("the EDFA path needs a CUDA device (there is no CPU fallback)")
+    dev = torch.cuda.current_device() if device is None else int(device)
+    lib = L.lib()
+    h = _CTX.get(dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    if h is None:
+        h = C.c_void_p()
+        with torch.cuda.device(dev):
+            L.check(lib.edfa_ctx_create(dev, C.c_void_p(stream), C.byref(h)))
+        _CTX[dev] = h
+    else:
+        L.check(lib.edfa_ctx_set_stream(h, C.c_void_p(stream)))
+    return h
+
+
+def dptr(t: torch.Tensor) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())
+
+
+def as_device_vector(v, n=None) -> torch.Tensor:
+    """float64 contiguous CUDA tensor (copies host arrays)."""
+    if isinstance(v, torch.Tensor):
+        t = v.to(device="cuda", dtype=torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.float64))).to("cuda")
+    t = t.contiguous()
+    if n is not None and t.numel() != n:
+        raise ValueError(f"shape mismatch: expected {n} entries, got {t.numel()}")
+    return t
+
+
+class DeviceCsr:
+    """A CSR matrix in libedfa device memory (int32 indices, float64 values)."""
+
+    def __init__(self, handle: C.c_void_p, owner: bool = True, keepalive=None):
+        self.handle = handle
+        self._owner = owner
+        self._keep = keepalive
+        r, c, z = C.c_int32(), C.c_int32(), C.c_int64()
+        L.check(L.lib().edfa_csr_info(handle, C.byref(r), C.byref(c), C.byref(z)))
+        self.shape = (r.value, c.value)
+        self.nnz = z.value
+
+    @classmethod
+    def from_scipy(cls, A) -> "DeviceCsr":
+        A = sp.csr_matrix(A)
+        if A.nnz >= 2 ** 31:
+            raise ValueError("matrix exceeds 2^31-1 stored entries")
+        ptr = np.ascontiguousarray(A.indptr, dtype=np.int32)
+        idx = np.ascontiguousarray(A.indices, dtype=np.int32)
+        val = np.ascontiguousarray(A.data, dtype=np.float64)
+        h = C.c_void_p()
+        L.check(L.lib().edfa_csr_create(ctx(), A.shape[0], A.shape[1], A.nnz,
+                                         ptr.ctypes.data_as(C.c_void_p), idx.ctypes.data_as(C.c_void_p),
+                                         val.ctypes.data_as(C.c_void_p), L.MEM_HOST, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_arrays(cls, shape, indptr, indices, data=None, device: bool = False) -> "DeviceCsr":
+        """Pattern-only when data is None.  Arrays are host numpy or CUDA tensors."""
+        h = C.c_void_p()
+        if device:
+            ptr = indptr.to(torch.int32).contiguous()
+            idx = indices.to(torch.int32).contiguous()
+            val = None if data is None else data.to(torch.float64).contiguous()
+            L.check(L.lib().edfa_csr_create(ctx(), shape[0], shape[1], idx.numel(), dptr(ptr), dptr(idx),
+                                             None if val is None else dptr(val), L.MEM_DEVICE, C.byref(h)))
+            torch.cuda.current_stream().synchronize()
+        else:
+            ptr = np.ascontiguousarray(indptr, dtype=np.int32)
+            idx = np.ascontiguousarray(indices, dtype=np.int32)
+            val = None if data is None else np.ascontiguousarray(data, dtype=np.float64)
+            L.check(L.lib().edfa_csr_create(ctx(), shape[0], shape[1], idx.size,
+                                             ptr.ctypes.data_as(C.c_void_p), idx.ctypes.data_as(C.c_void_p),
+                                             None if val is None else val.ctypes.data_as(C.c_void_p),
+                                             L.MEM_HOST, C.byref(h)))
+        return cls(h)
+
+    def arrays(self, values: bool = True):
+        n = self.shape[0]
+        ptr = np.empty(n + 1, dtype=np.int32)
+        idx = np.empty(self.nnz, dtype=np.int32)
+        val = np.empty(self.nnz, dtype=np.float64) if values else None
+        L.check(L.lib().edfa_csr_export(ctx(), self.handle, ptr.ctypes.data_as(C.c_void_p),
+                                         idx.ctypes.data_as(C.c_void_p),
+                                         None if val is None else val.ctypes.data_as(C.c_void_p), L.MEM_HOST))
+        return ptr, idx, val
+
+    def to_scipy(self) -> sp.csr_matrix:
+        ptr, idx, val = self.arrays(True)
+        return sp.csr_matrix((val, idx, ptr), shape=self.shape)
+
+    def matvec(self, x: torch.Tensor, y: torch.Tensor | None = None, alpha=1.0, beta=0.0) -> torch.Tensor:
+        x = as_device_vector(x, self.shape[1])
+        if y is None:
+            y = torch.empty(self.shape[0], dtype=torch.float64, device="cuda")
+        L.check(L.lib().edfa_spmv(ctx(), self.handle, dptr(x), dptr(y), alpha, beta))
+        return y
+
+    def __del__(self):
+        if self._owner and self.handle and L._lib is not None:
+            try:
+                L._lib.edfa_csr_destroy(self.handle)
+            except Exception:   # pragma: no cover - interpreter shutdown
+                pass
+            self.handle = None
+
+
+class DeviceSystem:
+    """The 2x2 block system on the device (hx/assembly.py:135-183 layout:
+    free faces first, then cells).  Keeps the host system for metadata."""
+
+    def __init__(self, A_ff: DeviceCsr, A_fc: DeviceCsr, A_cf: DeviceCsr, A_cc: DeviceCsr,
+                 rhs=None, host=None):
+        self.A_ff, self.A_fc, self.A_cf, self.A_cc = A_ff, A_fc, A_cf, A_cc
+        self.host = host
+        self.handle = C.c_void_p()
+        L.check(L.lib().edfa_system_create(ctx(), A_ff.handle, A_fc.handle, A_cf.handle, A_cc.handle,
+                                            C.byref(self.handle)))
+        self._rhs = None if rhs is None else as_device_vector(rhs, self.n_unknowns)
+        self._src = {}
+
+    @classmethod
+    def from_host(cls, system) -> "DeviceSystem":
+        """Upload a BlockSystem (scipy CSR blocks) -- hexflow's or this repo's."""
+        if isinstance(system, DeviceSystem):
+            return system
+        blocks = [DeviceCsr.from_scipy(getattr(system, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc")]
+        rhs = system.rhs() if hasattr(system, "rhs") else None
+        ds = cls(*blocks, rhs=rhs, host=system)
+        ds._src = {n: id(getattr(system, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc")}
+        return ds
+
+    def updated(self, system) -> "DeviceSystem":
+        """Device system for ``system`` reusing every block shared by identity
+        (update_accumulation replaces A_cc only, hx/assembly.py:314-333)."""
+        if isinstance(system, DeviceSystem):
+            return system
+        if self.host is None or any(id(getattr(system, n)) != self._src.get(n)
+                                    for n in ("A_ff", "A_fc", "A_cf")):
+            return DeviceSystem.from_host(system)
+        A_cc = self.A_cc if id(system.A_cc) == self._src.get("A_cc") else DeviceCsr.from_scipy(system.A_cc)
+        rhs = system.rhs() if hasattr(system, "rhs") else None
+        ds = DeviceSystem(self.A_ff, self.A_fc, self.A_cf, A_cc, rhs=rhs, host=system)
+        ds._src = dict(self._src, A_cc=id(system.A_cc))
+        return ds
+
+    @property
+    def n_free_faces(self) -> int:
+        return self.A_ff.shape[0]
+
+    @property
+    def n_cells(self) -> int:
+        return self.A_cc.shape[0]
+
+    @property
+    def n_unknowns(self) -> int:
+        return self.n_free_faces + self.n_cells
+
+    def rhs(self) -> torch.Tensor:
+        if self._rhs is None:
+            raise ValueError("system has no right-hand side")
+        return self._rhs
+
+    def spmv(self, x, y=None) -> torch.Tensor:
+        x = as_device_vector(x, self.n_unknowns)
+        if y is None:
+            y = torch.empty(self.n_unknowns, dtype=torch.float64, device="cuda")
+        L.check(L.lib().edfa_system_spmv(ctx(), self.handle, dptr(x), dptr(y)))
+        return y
+
+    __matmul__ = spmv
+
+    def __del__(self):
+        if getattr(self, "handle", None) and L._lib is not None:
+            try:
+                L._lib.edfa_system_destroy(self.handle)
+            except Exception:   # pragma: no cover
+                pass
+            self.handle = None
+
+
+class SystemOperator:
+    """``A_apply`` callable of the monolithic block operator on the device;
+    recognised by :func:`krylov.gmres`/`bicgstab` for the fused solver path."""
+
+    def __init__(self, system: DeviceSystem):
+        self.system = system
+
+    def __call__(self, v):
+        if isinstance(v, torch.Tensor):
+            return self.system.spmv(v)
+        return self.system.spmv(v).cpu().numpy()
+
+
+def system_operator(system) -> SystemOperator:
+    return SystemOperator(system if isinstance(system, DeviceSystem) else DeviceSystem.from_host(system))

@@ -1,0 +1,369 @@
+"""GPU parity: libedfa (through the drop-in API / C ABI) vs the reference.
+
+Gates (BASELINE.json north_star):
+  * restriction sets and the G~/F~ sparsity patterns bit-exact;
+  * G~/F~ values within 1e-10 relative per row (||d||_inf / ||row||_inf);
+  * H~/S~ patterns equal modulo |v| <= 1e-13 ||row||_2, values 1e-10;
+  * IC(0) of -A_ff bit-identical (same input, same operation order);
+  * preconditioner application within 1e-8 relative;
+  * GMRES iterations within +-2 of the oracle, final true relres <= rtol,
+    solution within 1e-7 relative.
+Golden files were produced by the unmodified reference (tests/golden/make_golden.py).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import GoldenSystem, g_csr, g_sets, golden, same_csr
+from oracle import edfa_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+ROW_TOL = 1e-10
+TINY = 1e-13
+
+
+@pytest.fixture(scope="module")
+def edfa(cuda):
+    import paper_2009_13916_b200 as E
+    from paper_2009_13916_b200 import _lib
+    _lib.lib()
+    return E
+
+
+def rowwise_rel(A, B):
+    """max over rows of ||A_i - B_i||_inf / ||B_i||_inf (same pattern)."""
+    A, B = A.tocsr(), B.tocsr()
+    worst = 0.0
+    D = abs(A - B).tocsr()
+    Bm = abs(B).tocsr()
+    dmax = np.zeros(B.shape[0])
+    bmax = np.zeros(B.shape[0])
+    for M, out in ((D, dmax), (Bm, bmax)):
+        for i in range(M.shape[0]):
+            lo, hi = M.indptr[i], M.indptr[i + 1]
+            if hi > lo:
+                out[i] = M.data[lo:hi].max()
+    nz = bmax > 0
+    if nz.any():
+        worst = float((dmax[nz] / bmax[nz]).max())
+    if (~nz).any():
+        worst = max(worst, float(dmax[~nz].max(initial=0.0)))
+    return worst
+
+
+def pattern_modulo_tiny(A, B, tol=TINY):
+    """Patterns equal after dropping |v| <= tol*||row||_2 from both."""
+    def strip(M):
+        M = M.tocsr().copy()
+        for i in range(M.shape[0]):
+            lo, hi = M.indptr[i], M.indptr[i + 1]
+            v = M.data[lo:hi]
+            nrm = np.linalg.norm(v)
+            v[np.abs(v) <= tol * nrm] = 0.0
+        M.eliminate_zeros()
+        return M
+    return same_csr(strip(A), strip(B))
+
+
+GOLD_NOFILL = [("small_wells", "base_nofill"), ("small_wells", "dyn14_nofill"),
+               ("small_wells", "dyn24_nofill"), ("small_wells", "dyn14_pre"),
+               ("small_wells", "dyn14_postprod"), ("small_wells", "dyn14_postschur"),
+               ("config1_n6", "base"), ("config2_n8", "staticA"), ("config2_n8", "staticB"),
+               ("config2_n8", "dyn14"), ("config3_n5", "dyn14"), ("config3_n5", "staticC")]
+
+
+def gpu_build(E, d, tag):
+    s = GoldenSystem(d)
+    kw = dict(no_fill=True)
+    s2kw = {}
+    if tag.startswith("dyn"):
+        dyn = E.DynamicConfig(int(tag[3]), int(tag[4]))
+        src = dict(dynamic=dyn)
+    else:
+        src = dict(patterns=_PS(g_sets(d, tag + "_Q")))
+    if tag == "dyn14_pre":
+        kw.update(tau_filt=1e-3, filtration="pre")
+    if tag == "dyn14_postprod":
+        kw.update(tau_filt=0.05, filtration="post-product")
+    if tag == "dyn14_postschur":
+        kw.update(tau_filt=0.05, filtration="post-schur")
+    pre = E.BlockLDUPreconditioner.build(s, **src, **kw)
+    return s, pre
+
+
+class _PS:
+    def __init__(self, sets):
+        self.sets = sets
+        self.provenance = "golden"
+
+
+@pytest.mark.parametrize("fname,tag", GOLD_NOFILL)
+def test_stage_artifacts_match_reference(edfa, fname, tag):
+    d = golden(fname)
+    s, pre = gpu_build(edfa, d, tag)
+    s1, s2 = pre.stage1, pre.stage2
+    # restriction sets (dynamic: grown on the GPU) -- bit-exact
+    used = s1.patterns.sets
+    ref_Q = g_sets(d, tag + "_Q")
+    assert len(used) == len(ref_Q)
+    assert all(np.array_equal(a, b) for a, b in zip(used, ref_Q))
+    for part, name in ((s1.G, "G"), (s1.F, "F")):
+        R = g_csr(d, f"{tag}_{name}")
+        assert same_csr(part, R), name
+        assert rowwise_rel(part, R) <= ROW_TOL, name
+    for part, name in ((s1.H, "H"), (s2.S, "S")):
+        R = g_csr(d, f"{tag}_{name}")
+        assert pattern_modulo_tiny(part, R), name
+        assert abs(part - R).max() <= ROW_TOL * abs(R).max(), name
+    L = s1.face_inner.L
+    R = g_csr(d, f"{tag}_Lff")
+    assert same_csr(L, R) and np.array_equal(L.data, R.data), "IC(0) must be bit-identical"
+    for part, name in ((s2.schur_inner.L, "LS"), (s2.schur_inner.U, "US")):
+        R = g_csr(d, f"{tag}_{name}")
+        assert same_csr(part, R), name
+        assert abs(part - R).max() <= 1e-9 * abs(R).max(), name
+    y = pre.apply(d[tag + "_apply_r"])
+    yr = d[tag + "_apply_y"]
+    assert np.abs(y - yr).max() <= 1e-8 * np.abs(yr).max()
+    assert pre.density == pytest.approx(float(d[tag + "_density"]), rel=0, abs=1e-12)
+
+
+@pytest.mark.parametrize("fname,tag", [("small_wells", "base_nofill"), ("config2_n8", "staticA"),
+                                       ("config3_n5", "dyn14")])
+def test_bicgstab_matches_reference_iterations(edfa, fname, tag):
+    d = golden(fname)
+    s, pre = gpu_build(edfa, d, tag)
+    ds = pre.device_system
+    x, rep = edfa.bicgstab(edfa.system_operator(ds), pre, s.rhs(), tol=1e-8)
+    n_ref = int(d[tag + "_bicg_nit"])
+    assert rep.converged
+    assert abs(rep.n_it - n_ref) <= 2
+    xr = d[tag + "_bicg_x"]
+    assert np.linalg.norm(x - xr) <= 1e-6 * np.linalg.norm(xr)
+    A = s.full_matrix()
+    assert np.linalg.norm(s.rhs() - A @ x) <= 10 * 1e-8 * np.linalg.norm(s.rhs())
+
+
+def _oracle_case(case):
+    s = case.system
+    p = case.precond
+    if p["pattern"] == "dynamic":
+        o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, dynamic=(p["n_add"], p["n_ent"], None), no_fill=True)
+    elif p["pattern"] == "static":
+        o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=O.static_sets(s.grid, s.face_index, p["prototype"]),
+                            no_fill=True)
+    else:
+        o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=O.base_sets(s.A_cf), no_fill=True)
+    o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
+    return o1, o2
+
+
+def _gpu_case(E, case):
+    s = case.system
+    p = case.precond
+    ds = E.DeviceSystem.from_host(s)
+    if p["pattern"] == "dynamic":
+        pre = E.BlockLDUPreconditioner.build(ds, dynamic=E.DynamicConfig(p["n_add"], p["n_ent"]), no_fill=True)
+    else:
+        pre = E.BlockLDUPreconditioner.build(ds, patterns=E.patterns_for(s, p["pattern"], p.get("prototype", "A")),
+                                             no_fill=True)
+    return ds, pre
+
+
+@pytest.mark.parametrize("idx,n", [(1, 8), (1, 12), (2, 8), (2, 12), (3, 6)])
+def test_gmres_matches_oracle(edfa, idx, n):
+    from paper_2009_13916_b200 import configs
+    case = configs.make(idx, n=n)
+    s = case.system
+    o1, o2 = _oracle_case(case)
+    A = s.full_matrix()
+    b = s.rhs()
+    xo, ro = O.gmres(lambda v: A @ v, lambda r: O.apply(o1, o2, s.A_fc, s.A_cf, r), b, tol=1e-8, restart=50)
+    ds, pre = _gpu_case(edfa, case)
+    assert all(np.array_equal(a, bb) for a, bb in zip(pre.stage1.patterns.sets, o1.sets))
+    x, rep = edfa.gmres(edfa.system_operator(ds), pre, b, tol=1e-8, restart=50)
+    assert ro.converged and rep.converged
+    assert abs(rep.n_it - ro.n_it) <= 2, (rep.n_it, ro.n_it)
+    assert rep.final_relres <= 1e-8
+    assert np.linalg.norm(b - A @ x) <= 1e-8 * np.linalg.norm(b) * 1.0001
+    assert np.linalg.norm(x - xo) <= 1e-7 * np.linalg.norm(xo)
+
+
+def test_static_patterns_on_device_match_oracle(edfa):
+    from paper_2009_13916_b200 import mesh
+    d = golden("protos")
+    g = mesh.box_grid(5, 5, 5, 1.0, 1.0, 1.0)
+    for p in "ABCDE":
+        mine = edfa.static_patterns(g, d["face_index"], p).sets
+        ref = g_sets(d, f"proto{p}")
+        assert all(np.array_equal(a, b) for a, b in zip(mine, ref)), p
+
+
+def test_static_prototype_sizes_interior(edfa):
+    from paper_2009_13916_b200 import mesh
+    g = mesh.box_grid(7, 7, 7, 1.0, 1.0, 1.0)
+    fidx = np.arange(g.n_faces)
+    m = g.elem_index(3, 3, 3)
+    sizes = {p: edfa.static_patterns(g, fidx, p).sizes()[m] for p in "ABCDE"}
+    assert sizes == {"A": 18, "B": 24, "C": 36, "D": 42, "E": 18}
+
+
+def test_determinism_bitwise(edfa):
+    """hx c10: repeated builds give bit-identical G, F, H (and S)."""
+    from paper_2009_13916_b200 import configs
+    case = configs.config3(n=5)
+    ds = edfa.DeviceSystem.from_host(case.system)
+    a = edfa.BlockLDUPreconditioner.build(ds, dynamic=edfa.DynamicConfig(2, 4), no_fill=True)
+    b = edfa.BlockLDUPreconditioner.build(ds, dynamic=edfa.DynamicConfig(2, 4), no_fill=True)
+    for x, y in ((a.stage1.G, b.stage1.G), (a.stage1.F, b.stage1.F), (a.stage1.H, b.stage1.H),
+                 (a.stage2.S, b.stage2.S)):
+        assert same_csr(x, y) and np.array_equal(x.data, y.data)
+
+
+def test_errors_and_state(edfa):
+    from paper_2009_13916_b200 import configs
+    s = configs.config1(n=3).system
+    with pytest.raises(ValueError):
+        edfa.build_stage1(s)
+    with pytest.raises(ValueError):
+        edfa.build_stage1(s, patterns=edfa.patterns_for(s, "base"), dynamic=edfa.DynamicConfig(1, 1))
+    with pytest.raises(ValueError):
+        edfa.build_stage1(s, patterns=edfa.patterns_for(s, "base"), filtration="bogus", no_fill=True)
+    with pytest.raises(ValueError):
+        edfa.DynamicConfig(n_add=0)
+    with pytest.raises(ValueError):
+        edfa.patterns_for(s, "nope")
+    s1 = edfa.build_stage1(s, patterns=edfa.patterns_for(s, "base"), no_fill=True)
+    pre = edfa.BlockLDUPreconditioner(s, s1)
+    with pytest.raises(RuntimeError):
+        pre.apply(np.zeros(s.n_unknowns))
+    with pytest.raises(ValueError):
+        edfa.gmres(lambda v: v, None, np.ones(3), tol=0.0)
+
+
+def test_non_spd_block_raises_factorization_error(edfa):
+    A = sp.csr_matrix(np.diag([1.0, -1.0]))    # -A indefinite
+    with pytest.raises(edfa.FactorizationError):
+        edfa.solve_restricted_row(A, np.ones(2), np.array([0, 1]))
+
+
+def test_restricted_solve_energy_minimality(edfa):
+    """hx c01 / test_precond.py:60-80 on the GPU kernel."""
+    rng = np.random.default_rng(101)
+    for _ in range(20):
+        n = int(rng.integers(6, 13))
+        M = rng.standard_normal((n, n))
+        Aspd = M @ M.T + n * np.eye(n)
+        s = int(rng.integers(2, n))
+        idx = np.sort(rng.choice(n, size=s, replace=False))
+        b = rng.standard_normal(n)
+        x = edfa.solve_restricted_row(sp.csr_matrix(-Aspd), b, idx)
+        res = b - Aspd @ x
+        assert np.abs(res[idx]).max() <= 1e-10 * np.linalg.norm(b)
+        assert np.all(x[np.setdiff1d(np.arange(n), idx)] == 0.0)
+
+
+def test_restricted_solve_zero_and_empty(edfa):
+    rng = np.random.default_rng(1)
+    M = rng.standard_normal((5, 5))
+    A = sp.csr_matrix(-(M @ M.T + 5 * np.eye(5)))
+    assert np.array_equal(edfa.solve_restricted_row(A, np.zeros(5), np.array([1, 3])), np.zeros(5))
+    assert np.array_equal(edfa.solve_restricted_row(A, rng.standard_normal(5), np.empty(0, int)), np.zeros(5))
+
+
+def test_grow_pattern_contracts(edfa):
+    from paper_2009_13916_b200 import configs
+    d = golden("small_wells")
+    s = GoldenSystem(d)
+    for m in (0, 7, 12):
+        lo, hi = s.A_cf.indptr[m], s.A_cf.indptr[m + 1]
+        ri, rv = s.A_cf.indices[lo:hi].astype(np.int64), s.A_cf.data[lo:hi]
+        idx0, _ = edfa.grow_pattern_dynamic(s.A_ff, ri, rv, edfa.DynamicConfig(1, 0))
+        assert np.array_equal(idx0, np.sort(ri))
+        idx, x = edfa.grow_pattern_dynamic(s.A_ff, ri, rv, edfa.DynamicConfig(2, 5))
+        oi, ox = O.grow_dynamic(s.A_ff, ri, rv, 2, 5)
+        assert np.array_equal(idx, oi)
+        assert np.abs(x - ox).max() <= 1e-10 * np.abs(ox).max()
+        assert ri.size <= idx.size <= ri.size + 5 and np.all(np.isin(ri, idx))
+    _ = configs
+
+
+def test_empty_patterns_give_cell_block(edfa):
+    from paper_2009_13916_b200 import configs
+    s = configs.config1(n=3).system
+    empty = _PS([np.empty(0, np.int64) for _ in range(s.n_cells)])
+    s1 = edfa.build_stage1(s, patterns=empty, no_fill=True)
+    assert s1.H.nnz == 0
+    s2 = edfa.build_stage2(s.A_cc, s1, no_fill=True)
+    assert np.allclose(s2.S.toarray(), s.A_cc.toarray())
+
+
+def test_full_patterns_exactness_limit(edfa):
+    """hx c02: full sets on 2x2x2 -> S~ equals the exact Schur complement."""
+    from paper_2009_13916_b200 import assembly, mesh
+    g = mesh.box_grid(2, 2, 2, 1.0, 1.0, 1.0)
+    rng = np.random.default_rng(5)
+    k = 10.0 ** rng.uniform(-4, 0, g.n_elems)
+    s = assembly.assemble(g, mesh.Conductivity.diagonal(k, k, k), mesh.RockProps(gamma=1.0),
+                          mesh.Boundaries(pressure_planes={"x-": 2.0, "x+": 1.0}), dt=math.inf)
+    full = _PS([np.arange(s.n_free_faces) for _ in range(s.n_cells)])
+    pre = edfa.BlockLDUPreconditioner.build(s, patterns=full, no_fill=True)
+    Aff = s.A_ff.toarray()
+    S = s.A_cc.toarray() - s.A_cf.toarray() @ np.linalg.solve(Aff, s.A_fc.toarray())
+    assert np.abs(pre.stage2.S.toarray() - S).max() <= 1e-10 * np.abs(S).max()
+
+
+def test_refresh_reuses_stage1(edfa):
+    """hx test_precond.py:242-252: only A_cc changes across time steps."""
+    from paper_2009_13916_b200 import assembly, configs
+    s = configs.config2(n=5).system
+    pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 2), no_fill=True)
+    s1 = pre.stage1
+    S_a = pre.stage2.S.toarray()
+    s_b = assembly.update_accumulation(s, 10.0, np.zeros(s.n_cells))
+    pre.refresh(s_b)
+    assert pre.stage1 is s1
+    diff = pre.stage2.S.toarray() - S_a
+    assert not np.allclose(diff, 0.0)
+    assert np.allclose(diff, np.diag(np.diag(diff)))
+
+
+def test_gmres_edge_cases(edfa):
+    from paper_2009_13916_b200 import configs
+    s = configs.config1(n=4).system
+    ds = edfa.DeviceSystem.from_host(s)
+    op = edfa.system_operator(ds)
+    x, rep = edfa.gmres(op, None, np.zeros(s.n_unknowns))
+    assert rep.converged and not np.any(x)
+    x, rep = edfa.gmres(op, None, s.rhs(), tol=1e-10, restart=30, max_it=3)
+    assert not rep.converged and rep.n_it == 3
+    # unpreconditioned fused GMRES still converges, true residual contract
+    x, rep = edfa.gmres(op, None, s.rhs(), tol=1e-9, restart=50, max_it=5000)
+    A = s.full_matrix()
+    assert rep.converged and np.linalg.norm(s.rhs() - A @ x) <= 1e-9 * np.linalg.norm(s.rhs())
+
+
+def test_generic_callables_path(edfa):
+    """hx usage: bicgstab(lambda v: A @ v, pre.apply, b) with host callables."""
+    d = golden("small_wells")
+    s, pre = gpu_build(edfa, d, "base_nofill")
+    A = s.full_matrix()
+    b = s.rhs()
+    x, rep = edfa.bicgstab(lambda v: A @ v, pre.apply, b, tol=1e-8)
+    assert rep.converged and abs(rep.n_it - int(d["base_nofill_bicg_nit"])) <= 2
+    x2, rep2 = edfa.gmres(lambda v: A @ v, pre.apply, b, tol=1e-8)
+    assert rep2.converged and np.linalg.norm(b - A @ x2) <= 1e-8 * np.linalg.norm(b) * 1.0001
+
+
+def test_fill_modes_are_reported_unsupported(edfa):
+    from paper_2009_13916_b200._lib import EdfaUnsupported
+    d = golden("small_wells")
+    s = GoldenSystem(d)
+    with pytest.raises(EdfaUnsupported):
+        edfa.BlockLDUPreconditioner.build(s, patterns=_PS(g_sets(d, "base_fill_Q")))
