@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""EDFA setup + GMRES(50) solve throughput on B200 (BASELINE.json metric).
+
+One step = the hot path over one system: static-pattern generation, stage 1
+(restricted row solves, G~/F~, H~ = G~ A_ff F~, IC(0) of -A_ff), stage 2
+(S~ = A_cc - H~, ILU(0)) and right-preconditioned GMRES(50) to rtol 1e-8 from
+x0 = 0.  Workload: BASELINE config 2 (64^3 hex grid, lognormal anisotropic K,
+static prototype A, IC(0)/ILU(0)), synthetic seeded inputs (SPE10 is not in
+this container).  ``value`` = N_dof * steps / device time with the blocks
+resident in HBM; ``e2e`` = the same through the drop-in API from host scipy
+blocks (H2D of the blocks and rhs, D2H of x inside the timed region).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl edfa|reference]
+
+``--impl reference`` times the CPU restatement of the reference algorithm
+(oracle/, the reference is pure Python and cannot travel to the GPU box) on a
+bounded sample of the same workload and prints the same JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "EDFA setup+GMRES solve throughput per system (config 2)"
+UNIT = "MDOF/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="edfa", choices=["edfa", "reference"])
+    ap.add_argument("--n", type=int, default=64, help="grid cells per side (config 2 is 64)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-json", default=None, help="write the per-kernel event profile here")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or self.f is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_baseline(n_full: int, n_iters_full: int, sample_n: int = 20, gmres_iters: int = 8):
+    """Time the oracle restatement of the reference on a bounded sample and
+    extrapolate to the full workload: stage 1 and stage 2 are
+    per-row independent work -> per-DOF rates from a sample_n^3 instance of the
+    same generator; GMRES -> per-iteration-per-DOF rate from ``gmres_iters``
+    iterations on that instance, scaled by the GPU's iteration count."""
+    import numpy as np
+
+    from oracle import edfa_oracle as O
+    from paper_2009_13916_b200 import configs
+    case = configs.config2(n=sample_n)
+    s = case.system
+    N = s.n_unknowns
+    A = s.full_matrix()
+    t0 = time.perf_counter()
+    sets = O.static_sets(s.grid, s.face_index, "A")
+    o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=sets, no_fill=True)
+    t1 = time.perf_counter()
+    o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
+    t2 = time.perf_counter()
+    O.gmres(lambda v: A @ v, lambda r: O.apply(o1, o2, s.A_fc, s.A_cf, r), s.rhs(), tol=1e-30,
+            restart=50, max_it=1)                   # one-time scipy solver initialisation
+    t2g = time.perf_counter()
+    _, rep = O.gmres(lambda v: A @ v, lambda r: O.apply(o1, o2, s.A_fc, s.A_cf, r), s.rhs(), tol=1e-30,
+                     restart=50, max_it=gmres_iters)
+    t3 = time.perf_counter()
+    it_time = (t3 - t2g) / max(rep.n_it, 1)
+    N_full = None
+    per_dof_setup = (t2 - t0) / N
+    per_dof_iter = it_time / N
+    return dict(per_dof_setup=per_dof_setup, per_dof_iter=per_dof_iter, sample_N=N,
+                sample=f"oracle port on the config-2 generator at {sample_n}^3 (N={N}): full stage 1 + stage 2, "
+                       f"{rep.n_it} GMRES(50) iterations; extrapolated per DOF to {n_full}^3 with "
+                       f"{n_iters_full} iterations",
+                t_stage1=t1 - t0, t_stage2=t2 - t1, t_iter=it_time, _np=np)
+
+
+def extrapolate(cb, N_full, iters):
+    t = N_full * cb["per_dof_setup"] + iters * N_full * cb["per_dof_iter"]
+    return N_full / t / 1e6
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if world > 1 and rank != 0:
+        return
+    from paper_2009_13916_b200 import configs  # noqa: F401
+    n_full = args.n
+    # iteration count of the full workload: the oracle's own GMRES count is
+    # not affordable at 64^3 per step; use the survey-measured 87 (SURVEY.md
+    # §6.2, oracle restatement, config-2 shape) unless a smaller grid is asked
+    iters = 87
+    N_full = free_faces_config2(n_full) + n_full ** 3
+    vals = []
+    cb = None
+    for k in range(max(args.warmup, 0) + args.steps):
+        cb = cpu_baseline(n_full, iters, sample_n=16, gmres_iters=5)
+        if k >= args.warmup:
+            vals.append(extrapolate(cb, N_full, iters))
+    v = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": N_full / (v * 1e6) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-2 generator)",
+        "config": {"workload": f"config2-{n_full}^3-staticA-IC0ILU0-gmres50", "n_dof": N_full,
+                   "rtol": 1e-8, "restart": 50, "l2": "inputs larger than L2"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": cb["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def free_faces_config2(n):
+    # x-faces minus the two Dirichlet x-planes, plus y and z faces
+    return (n + 1) * n * n - 2 * n * n + 2 * n * (n + 1) * n
+
+
+# ---------------------------------------------------------------- EDFA arm
+def run_edfa(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2009_13916_b200 import _lib, configs
+    from paper_2009_13916_b200.device import DeviceSystem, ctx, system_operator
+    from paper_2009_13916_b200.krylov import gmres
+    from paper_2009_13916_b200.precond import BlockLDUPreconditioner, patterns_for
+
+    lib = _lib.lib()
+    case = configs.config2(n=args.n)
+    s = case.system
+    N = s.n_unknowns
+    ds = DeviceSystem.from_host(s)
+    b_dev = torch.from_numpy(s.rhs()).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step(system_dev, b):
+        pats = patterns_for(system_dev, "static", "A", grid=s.grid)
+        pre = BlockLDUPreconditioner.build(system_dev, patterns=pats, no_fill=True)
+        x, rep = gmres(system_operator(system_dev), pre, b, tol=case.rtol, restart=case.restart,
+                       max_it=case.max_it)
+        return x, rep, pre
+
+    # patterns_for on a DeviceSystem needs the host grid/face_index
+    for _ in range(args.warmup):
+        x, rep, pre = step(ds, b_dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+
+    # ---- device-resident timed region
+    c = ctx()
+    lib.edfa_ctx_profile(c, 1)
+    lib.edfa_ctx_profile_report(c, None, 0, 1)
+    launches0 = lib.edfa_ctx_launch_count(c)
+    times = []
+    reps = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1.0)                        # evict L2 between steps
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            x, rep, pre = step(ds, b_dev)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            reps.append(rep)
+    launches = lib.edfa_ctx_launch_count(c) - launches0
+    buf_len = lib.edfa_ctx_profile_report(c, None, 0, 0)
+    import ctypes
+    buf = ctypes.create_string_buffer(int(buf_len))
+    lib.edfa_ctx_profile_report(c, buf, buf_len, 1)
+    lib.edfa_ctx_profile(c, 0)
+    prof = json.loads(buf.value.decode())
+    clocks = clk.summary()
+    t_total_ms = sum(times)
+    if world > 1:
+        tt = torch.tensor([t_total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_total_ms = float(tt.item())
+    value = world * N * args.steps / (t_total_ms / 1e3) / 1e6
+
+    # ---- end-to-end through the public API from host scipy blocks
+    A_host = s.full_matrix()
+    e2e_times = []
+    h2d = sum(getattr(s, n).data.nbytes + getattr(s, n).indices.nbytes + getattr(s, n).indptr.nbytes
+              for n in ("A_ff", "A_fc", "A_cf", "A_cc")) + s.rhs().nbytes
+    d2h = N * 8
+    for k in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ds_h = DeviceSystem.from_host(s)                      # H2D of the four blocks + rhs
+        pats = patterns_for(s, "static", "A")
+        pre_h = BlockLDUPreconditioner.build(ds_h, patterns=pats, no_fill=True)
+        x_h, rep_h = gmres(system_operator(ds_h), pre_h, s.rhs(), tol=case.rtol, restart=case.restart,
+                           max_it=case.max_it)                # x returned to host (D2H)
+        e2e_times.append(time.perf_counter() - t0)
+        del ds_h, pre_h
+    e2e_val = world * N / statistics.median(e2e_times) / 1e6
+    relres_host = float(np.linalg.norm(s.rhs() - A_host @ x_h) / np.linalg.norm(s.rhs()))
+
+    # ---- roofline of the dominant kernel
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, burst)" if peak else "fallback 6650 GB/s (B200_PROFILING.md)"
+    peak = peak or 6650.0
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", {"ms": 0, "bytes": 0, "launches": 1})
+    dname, d = dom
+    per_launch_ms = d["ms"] / max(d["launches"], 1)
+    per_launch_bytes = d["bytes"] / max(d["launches"], 1)
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
+    traffic = None
+    try:
+        nc = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        traffic = nc.get(dname)
+    except Exception:
+        pass
+    step_ms = t_total_ms / args.steps
+    shares = {k: round(v["ms"] / max(sum(p["ms"] for p in prof.values()), 1e-9), 4) for k, v in
+              sorted(prof.items(), key=lambda kv: -kv[1]["ms"])[:8]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-2 generator: 64^3, lnK~N(0,2), kz/kx=0.1)",
+        "config": {"workload": f"config2-{args.n}^3-staticA-IC0ILU0-gmres50", "n_dof": N,
+                   "n_free_faces": s.n_free_faces, "n_cells": s.n_cells, "rtol": case.rtol,
+                   "restart": case.restart, "gmres_iterations": reps[-1].n_it,
+                   "final_true_relres": reps[-1].final_relres, "host_check_relres": relres_host,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 and a 256 MiB L2 flush between steps"},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "seconds_per_step": statistics.median(e2e_times)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
+                     "launches_per_step": d["launches"] / args.steps, "step_share": shares},
+        "clocks": clocks,
+    }
+    if args.profile_json and rank == 0:
+        pathlib.Path(args.profile_json).write_text(json.dumps(prof, indent=1))
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_baseline(args.n, reps[-1].n_it)
+        v = extrapolate(cb, N, reps[-1].n_it)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": cb["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_edfa(args)
+
+
+if __name__ == "__main__":
+    main()
