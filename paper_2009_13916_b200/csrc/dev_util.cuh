@@ -58,6 +58,31 @@ __device__ __forceinline__ T warp_max(T v) {
     return v;
 }
 
+// Software grid barrier for cooperative (co-resident) persistent launches:
+// one arrival atomic per block, the last arriver bumps the generation.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+        __threadfence();
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            *count = 0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+        } else {
+            unsigned v;
+            unsigned ns = 8;
+            do {
+                __nanosleep(ns);
+                if (ns < 64) ns <<= 1;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
+            } while (v == g);
+        }
+    }
+    __syncthreads();
+}
+
 // position of key in sorted a[lo, hi) or -1
 __device__ __forceinline__ int bsearch(const int32_t* a, int lo, int hi, int key) {
     while (lo < hi) {

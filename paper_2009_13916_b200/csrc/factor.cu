@@ -1,14 +1,15 @@
 // K6/K7: IC(0) of -A_ff and ILU(0) of S~ (hx/sparse.py:141-282 with
-// no_fill=True, fill_tol=0), sync-free in dependency-level order.
+// no_fill=True, fill_tol=0) in dependency-level order.
 //
 // The arithmetic mirrors the reference operation for operation -- pivots in
 // increasing column order, multipliers a_ik / d_k, updates
 // w_j <- w_j - l_ik * u_kj without FMA contraction, the sign-preserving guard
 // |pivot| < 1e-12 * ||row||_inf -- so, given the same input matrix, the
 // factors are bit-identical to the reference's pure-Python factorisation.
-// Rows are processed in the forward triangular-solve plan's level order (the
-// factorisation DAG is the forward-solve DAG); a row publishes its pivot,
-// which doubles as the ready flag (sentinel-initialised), after its values.
+// Rows are processed level by level of the forward triangular-solve plan (the
+// factorisation DAG is the forward-solve DAG): chain-structured factors are
+// walked one chain per thread, everything else runs as a persistent
+// cooperative kernel with a software grid barrier between levels.
 #include "dev_util.cuh"
 #include "edfa_internal.cuh"
 #include "objects.cuh"
@@ -55,119 +56,104 @@ __global__ void k_diag_scale(CsrV A, double sign, double* __restrict__ d, double
     if (has) has[i] = h;
 }
 
-__device__ double wait_pivot(const double* p, int* err) {
-    double v;
-    asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-    long long spins = 0;
-    while (is_sentinel(v)) {
-        if (++spins > SPIN_LIMIT) { atomicExch(err, 3); return 1.0; }
-        asm volatile("ld.acquire.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-    }
-    return v;
-}
-__device__ void publish_pivot(double* p, double v) {
-    asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
+struct LevelArgs {
+    const int* perm;          // slot -> row (-1 padding)
+    const int* level_start;   // level -> first slice
+    int n_levels;
+    unsigned* bar;            // [count, generation]
+};
 
-// IC(0) of -A_ff: one thread per row, rows in forward-plan order.
-// L holds the strictly lower pattern (initialised with -A values); diag the
-// pivots (sentinel until published).
-__global__ void __launch_bounds__(256) k_ic0(const int* __restrict__ perm, int n_slices, const int32_t* __restrict__ Lp,
+// IC(0) of -A_ff, one thread per row; L holds the strictly lower pattern
+// initialised with -A values, diag receives L_ii.
+__global__ void __launch_bounds__(256) k_ic0(LevelArgs la, const int32_t* __restrict__ Lp,
                                              const int32_t* __restrict__ Li, double* __restrict__ Lv,
                                              const double* __restrict__ aii, const double* __restrict__ scale,
-                                             double* __restrict__ diag, int* ticket, int* shifts, int* err) {
-    __shared__ int base[8];
-    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) base[wid] = atomicAdd(ticket, 1);
-    __syncwarp();
-    int s = base[wid];
-    if (s >= n_slices) return;
-    int i = perm[s * 32 + lane];
-    if (i < 0) return;
-    int lo = Lp[i], hi = Lp[i + 1];
-    // every dependency must be final before row i reads its L entries
-    for (int p = lo; p < hi; ++p) wait_pivot(diag + Li[p], err);
-    double d = aii[i];
-    for (int p = lo; p < hi; ++p) {
-        int k = Li[p];
-        double mult = __ddiv_rn(Lv[p], ld_cg(diag + k));
-        Lv[p] = mult;
-        for (int q = p + 1; q < hi; ++q) {
-            int j = Li[q];
-            int pos = bsearch(Li, Lp[j], Lp[j + 1], k);
-            if (pos >= 0) Lv[q] = sub_mul(Lv[q], mult, ld_cg(Lv + pos));
+                                             double* __restrict__ diag, int* shifts) {
+    const int nthr = gridDim.x * blockDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int L = 0; L < la.n_levels; ++L) {
+        int t1 = la.level_start[L + 1] * 32;
+        for (int t = la.level_start[L] * 32 + tid; t < t1; t += nthr) {
+            int i = la.perm[t];
+            if (i < 0) continue;
+            int lo = Lp[i], hi = Lp[i + 1];
+            double d = aii[i];
+            for (int p = lo; p < hi; ++p) {
+                int k = Li[p];
+                double mult = __ddiv_rn(Lv[p], __ldcg(diag + k));
+                Lv[p] = mult;
+                for (int q = p + 1; q < hi; ++q) {
+                    int j = Li[q];
+                    int pos = bsearch(Li, Lp[j], Lp[j + 1], k);
+                    if (pos >= 0) Lv[q] = sub_mul(Lv[q], mult, __ldcg(Lv + pos));
+                }
+                d = sub_mul(d, mult, mult);
+            }
+            double g = PIVOT_GUARD * scale[i];
+            if (d < g) {
+                d = g;
+                atomicAdd(shifts, 1);
+            }
+            __stcg(diag + i, __dsqrt_rn(d));
         }
-        d = sub_mul(d, mult, mult);
+        if (L + 1 < la.n_levels) grid_barrier(la.bar, la.bar + 1, gridDim.x);
     }
-    double g = PIVOT_GUARD * scale[i];
-    if (d < g) {
-        d = g;
-        atomicAdd(shifts, 1);
-    }
-    __threadfence();
-    publish_pivot(diag + i, publishable(__dsqrt_rn(d)));
 }
 
-// ILU(0) of S: one warp per row, rows in forward-plan order.  LU starts as a
-// copy of S; on exit its strictly lower part holds the multipliers and its
-// strictly upper part U; pivots go to udiag (sentinel until published).
-template <int RMAX, int WPB = (RMAX >= 1024 ? 2 : 4)>
-__global__ void __launch_bounds__(128) k_ilu0(const int* __restrict__ perm, int n_slots, const int32_t* __restrict__ Sp,
+// ILU(0) of S, one warp per row.  LU starts as a copy of S; on exit its
+// strictly lower part holds the multipliers and its strictly upper part U;
+// pivots go to udiag.
+template <int RMAX>
+__global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __restrict__ Sp,
                                               const int32_t* __restrict__ Si, double* __restrict__ LU,
                                               const double* __restrict__ scale, double* __restrict__ udiag,
-                                              int* ticket, int* shifts, int* err) {
-    __shared__ int s_cols[WPB][RMAX];
-    __shared__ double s_vals[WPB][RMAX];
-    __shared__ int base[WPB];
-    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* cols = s_cols[wid];
-    double* vals = s_vals[wid];
-    for (;;) {
-        if (lane == 0) base[wid] = atomicAdd(ticket, 1);
-        __syncwarp();
-        int slot = base[wid];
-        __syncwarp();
-        if (slot >= n_slots) return;
-        int i = perm[slot];
-        if (i < 0) continue;
-        int lo = Sp[i], n = Sp[i + 1] - lo;
-        if (n > RMAX) {
-            if (lane == 0) atomicExch(err, 4);
-            if (lane == 0) publish_pivot(udiag + i, 1.0);
-            continue;
-        }
-        for (int t = lane; t < n; t += 32) {
-            cols[t] = Si[lo + t];
-            vals[t] = LU[lo + t];
-        }
-        __syncwarp();
-        int nl = lower_bound(cols, 0, n, i);
-        for (int p = 0; p < nl; ++p) {
-            int k = cols[p];
-            double dk = wait_pivot(udiag + k, err);
-            double mult = __ddiv_rn(vals[p], dk);
-            __syncwarp();
-            if (lane == 0) vals[p] = mult;
-            int u0 = lower_bound(Si, Sp[k], Sp[k + 1], k + 1), u1 = Sp[k + 1];
-            for (int e = u0 + lane; e < u1; e += 32) {
-                int j = Si[e];
-                int slot_j = bsearch(cols, p + 1, n, j);
-                if (slot_j >= 0) vals[slot_j] = sub_mul(vals[slot_j], mult, ld_cg(LU + e));
+                                              int* shifts, int* err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* cols = reinterpret_cast<int*>(smem) + wid * RMAX;
+    double* vals = reinterpret_cast<double*>(smem + sizeof(int) * RMAX * (blockDim.x >> 5)) + wid * RMAX;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int L = 0; L < la.n_levels; ++L) {
+        int t1 = la.level_start[L + 1] * 32;
+        for (int slot = la.level_start[L] * 32 + gw; slot < t1; slot += nw) {
+            int i = la.perm[slot];
+            if (i < 0) continue;
+            int lo = Sp[i], n = Sp[i + 1] - lo;
+            if (n > RMAX) {
+                if (lane == 0) atomicExch(err, 4);
+                continue;
+            }
+            for (int t = lane; t < n; t += 32) {
+                cols[t] = Si[lo + t];
+                vals[t] = LU[lo + t];
             }
             __syncwarp();
+            int nl = lower_bound(cols, 0, n, i);
+            for (int p = 0; p < nl; ++p) {
+                int k = cols[p];
+                double mult = __ddiv_rn(vals[p], __ldcg(udiag + k));
+                __syncwarp();
+                if (lane == 0) vals[p] = mult;
+                int u0 = lower_bound(Si, Sp[k], Sp[k + 1], k + 1), u1 = Sp[k + 1];
+                for (int e = u0 + lane; e < u1; e += 32) {
+                    int slot_j = bsearch(cols, p + 1, n, Si[e]);
+                    if (slot_j >= 0) vals[slot_j] = sub_mul(vals[slot_j], mult, __ldcg(LU + e));
+                }
+                __syncwarp();
+            }
+            int dslot = bsearch(cols, nl, n, i);
+            double piv = dslot >= 0 ? vals[dslot] : 0.0;
+            double g = PIVOT_GUARD * scale[i];
+            if (fabs(piv) < g) {
+                piv = piv >= 0.0 ? g : -g;
+                if (lane == 0) atomicAdd(shifts, 1);
+            }
+            for (int t = lane; t < n; t += 32) __stcg(LU + lo + t, vals[t]);
+            if (lane == 0) __stcg(udiag + i, piv);
+            __syncwarp();
         }
-        int dslot = bsearch(cols, nl, n, i);
-        double piv = dslot >= 0 ? vals[dslot] : 0.0;
-        double g = PIVOT_GUARD * scale[i];
-        if (fabs(piv) < g) {
-            piv = piv >= 0.0 ? g : -g;
-            if (lane == 0) atomicAdd(shifts, 1);
-        }
-        for (int t = lane; t < n; t += 32) LU[lo + t] = vals[t];
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) publish_pivot(udiag + i, publishable(piv));
-        __syncwarp();
+        if (L + 1 < la.n_levels) grid_barrier(la.bar, la.bar + 1, gridDim.x);
     }
 }
 
@@ -238,13 +224,19 @@ void export_tri(Ctx* c, const Csr& P, const double* diag, int mode, Csr& out) {
     }
 }
 
-int read_flags(Ctx* c, int* dev_shift, int* dev_err, int* shifts) {
+void read_flags(Ctx* c, const int* dev, int* shifts, int* err) {
     int h[2];
-    EDFA_CUDA(cudaMemcpyAsync(&h[0], dev_shift, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    EDFA_CUDA(cudaMemcpyAsync(&h[1], dev_err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(h, dev, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaStreamSynchronize(c->stream));
     *shifts = h[0];
-    return h[1];
+    *err = h[1];
+}
+
+template <class K>
+int coop_grid(K kern, int threads, size_t smem) {
+    int occ = 0;
+    EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+    return NUM_SMS_B200 * std::max(1, std::min(occ, 2));
 }
 
 }  // namespace
@@ -263,19 +255,27 @@ void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f) {
         check_launch("k_diag_scale");
     }
     build_plan(c, f.Lpat, nullptr, false, false, f.fwd);
-    int* flags = c->d_scalar_i + 24;   // [ticket, shifts, err]
-    EDFA_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), c->stream));
-    if (n) {
-        fill_bits(c, f.diag.p, n, SENTINEL_BITS);
+    int* flags = c->d_scalar_i + 24;   // [shifts, err]
+    EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+    if (n && f.fwd.is_chain) {
+        chain_ic0(c, f.fwd.chain, f.Lpat, aii.p, sc.p, f.diag.p, flags);
+    } else if (n) {
+        LevelArgs la{f.fwd.perm.p, f.fwd.level_start.p, f.fwd.n_levels, reinterpret_cast<unsigned*>(f.fwd.sync.p)};
         Prof pr(c, "ic0_factor", 24.0 * f.Lpat.nnz + 32.0 * n);
-        int n_slices = f.fwd.n_slots / 32;
-        k_ic0<<<ceil_div(n_slices, 8), 256, 0, c->stream>>>(f.fwd.perm.p, n_slices, f.Lpat.ptr.p, f.Lpat.idx.p,
-                                                            f.Lpat.val.p, aii.p, sc.p, f.diag.p, flags, flags + 1,
-                                                            flags + 2);
-        check_launch("k_ic0");
+        int grid = coop_grid(k_ic0, 256, 0);
+        const int32_t* Lp = f.Lpat.ptr.p;
+        const int32_t* Li = f.Lpat.idx.p;
+        double* Lv = f.Lpat.val.p;
+        const double* ap = aii.p;
+        const double* sp = sc.p;
+        double* dp = f.diag.p;
+        int* sh = flags;
+        void* args[] = {&la, &Lp, &Li, &Lv, &ap, &sp, &dp, &sh};
+        EDFA_CUDA(cudaLaunchCooperativeKernel((void*)k_ic0, dim3(grid), dim3(256), args, 0, c->stream));
     }
-    int err = read_flags(c, flags + 1, flags + 2, &f.shifts);
-    require(err == 0, EDFA_ERR_CUDA, "IC(0) factorisation did not complete (spin limit)");
+    int err = 0;
+    read_flags(c, flags, &f.shifts, &err);
+    require(err == 0, EDFA_ERR_CUDA, "IC(0) factorisation failed");
     plan_values(c, f.Lpat, f.diag.p, f.fwd);
     Csr LT;
     transpose(c, f.Lpat, LT);
@@ -298,28 +298,37 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f) {
     }
     Csr Lpart;
     select_part(c, S, 0, 1.0, false, Lpart);
-    build_plan(c, Lpart, nullptr, true, false, f.fwd);
+    build_plan(c, Lpart, nullptr, true, false, f.fwd, /*allow_chain=*/false);
     int maxr = n ? max_row_nnz(c, S) : 0;
-    int* flags = c->d_scalar_i + 24;
-    EDFA_CUDA(cudaMemsetAsync(flags, 0, 3 * sizeof(int), c->stream));
-    if (n) {
-        fill_bits(c, f.udiag.p, n, SENTINEL_BITS);
-        Prof pr(c, "ilu0_factor", 24.0 * S.nnz + 24.0 * n);
-        int blocks = std::min(ceil_div(f.fwd.n_slots, 4), NUM_SMS_B200 * 16);
-        if (maxr <= 64)
-            k_ilu0<64><<<blocks, 128, 0, c->stream>>>(f.fwd.perm.p, f.fwd.n_slots, f.LU.ptr.p, f.LU.idx.p,
-                                                      f.LU.val.p, sc.p, f.udiag.p, flags, flags + 1, flags + 2);
-        else if (maxr <= 256)
-            k_ilu0<256><<<blocks, 128, 0, c->stream>>>(f.fwd.perm.p, f.fwd.n_slots, f.LU.ptr.p, f.LU.idx.p,
-                                                       f.LU.val.p, sc.p, f.udiag.p, flags, flags + 1, flags + 2);
-        else
-            k_ilu0<1024><<<blocks, 64, 0, c->stream>>>(f.fwd.perm.p, f.fwd.n_slots, f.LU.ptr.p, f.LU.idx.p,
-                                                        f.LU.val.p, sc.p, f.udiag.p, flags, flags + 1, flags + 2);
-        check_launch("k_ilu0");
-    }
     require(maxr <= 1024, EDFA_ERR_UNSUPPORTED, "Schur rows longer than 1024 entries are not supported");
-    int err = read_flags(c, flags + 1, flags + 2, &f.shifts);
-    require(err == 0, EDFA_ERR_CUDA, "ILU(0) factorisation did not complete");
+    int* flags = c->d_scalar_i + 24;
+    EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+    if (n) {
+        const int32_t* Sp = f.LU.ptr.p;
+        const int32_t* Si = f.LU.idx.p;
+        double* LUv = f.LU.val.p;
+        const double* scp = sc.p;
+        double* ud = f.udiag.p;
+        int* sh = flags;
+        int* er = flags + 1;
+        Prof pr(c, "ilu0_factor", 24.0 * S.nnz + 24.0 * n);
+        LevelArgs la{f.fwd.perm.p, f.fwd.level_start.p, f.fwd.n_levels, reinterpret_cast<unsigned*>(f.fwd.sync.p)};
+        void* args[] = {&la, &Sp, &Si, &LUv, &scp, &ud, &sh, &er};
+        auto launch = [&](auto kern, int rmax) {
+            int threads = 256;
+            size_t smem = (size_t)rmax * (sizeof(int) + sizeof(double)) * (threads / 32);
+            if (smem > 48 * 1024)
+                EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int grid = coop_grid(kern, threads, smem);
+            EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(threads), args, smem, c->stream));
+        };
+        if (maxr <= 64) launch(k_ilu0<64>, 64);
+        else if (maxr <= 256) launch(k_ilu0<256>, 256);
+        else launch(k_ilu0<1024>, 1024);
+    }
+    int err = 0;
+    read_flags(c, flags, &f.shifts, &err);
+    require(err == 0, EDFA_ERR_CUDA, "ILU(0) factorisation failed");
     Csr Lv, Uv;
     select_part(c, f.LU, 0, 1.0, true, Lv);
     plan_values(c, Lv, nullptr, f.fwd);

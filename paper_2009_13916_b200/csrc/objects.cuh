@@ -38,7 +38,25 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
 // one thread per row; SELL-32 (column-major inside 32-row slices) so the
 // coefficient stream is fully coalesced.  Dependencies are polled on the
 // solution vector itself (sentinel-initialised), so there is no flag array.
+struct ChainPlan {              // disjoint-path DAGs (chain.cu)
+    int32_t n = 0, n_chains = 0;
+    int64_t n_stored = 0;
+    bool unit = false;
+    DevBuf<int64_t> gbase;      // group of 32 chains -> first stored step
+    DevBuf<int32_t> rows;       // SELL-32 over chains: row of step k of chain t
+    DevBuf<double> coef, dinv;  // dependency coefficient / inverse diagonal per step
+    DevBuf<int32_t> heads, succ;
+};
+bool build_chain(Ctx* c, const Csr& deps, const double* diag, bool unit, ChainPlan& cp);
+void chain_values(Ctx* c, const Csr& deps, const double* diag, ChainPlan& cp);
+void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add, double* out2,
+               const char* name);
+void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,
+               int* shifts);
+
 struct TriPlan {
+    bool is_chain = false;
+    ChainPlan chain;
     int32_t n = 0;          // rows
     int32_t n_slots = 0;    // padded thread count (multiple of 32)
     int32_t n_levels = 0;
@@ -50,12 +68,18 @@ struct TriPlan {
     DevBuf<int32_t> col;
     DevBuf<double> val;
     DevBuf<double> dinv;        // slot -> 1/diag (1 for unit)
-    DevBuf<int32_t> ticket;     // dynamic warp ticket
+    DevBuf<int32_t> slice_level;   // slice -> dependency level
+    DevBuf<int32_t> level_slices;  // level -> number of slices
+    DevBuf<int32_t> level_start;   // level -> first slice (n_levels + 1)
+    // [done[0..n_levels), ticket, finished]; self-resetting at kernel end
+    DevBuf<int32_t> sync;
+    DevBuf<int32_t> ticket;     // unused (kept for ABI of older plans)
 };
 // deps: row i -> (j, coef) with x_i = (alpha*b_i - sum coef*x_j) * dinv_i;
 // reverse = deps point to higher rows (backward substitution).  diag may be
 // NULL (values loaded later with plan_values).
-void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& plan);
+void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& plan,
+                bool allow_chain = true);
 void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& plan);
 // x = solve(b * alpha); if (add) out2 = x + add (fused epilogue)
 void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,

@@ -102,67 +102,208 @@ struct SolveArgs {
     const int32_t* col;
     const double* val;
     const double* dinv;
+    const int* slice_level;
+    const int* level_slices;
+    int* sync;            // done[n_levels], ticket, finished
+    int n_levels;
     int n_slices;
     const double* b;
     double alpha;
     double* x;
     const double* add;
     double* out2;
-    int* ticket;
     int* err;
 };
 
+__device__ __forceinline__ void wait_level(const int* done, int L, int need, int* err) {
+    // one lane per warp polls the per-level completion counter with backoff
+    if (L < 0) return;
+    unsigned ns = 16;
+    long long spins = 0;
+    while (ld_acquire(done + L) < need) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+        if (++spins > SPIN_LIMIT) { atomicExch(err, 2); return; }
+    }
+}
+
+// Level-counter synchronisation: a slice of level L starts once every slice
+// of level L-1 has finished; by induction all earlier levels are complete,
+// so dependencies are read without per-entry polling.  The last warp to
+// finish resets the counters for the next launch (no memset between solves).
 template <int U>
 __global__ void __launch_bounds__(256) k_trsv(SolveArgs a) {
     __shared__ int base[8];
     int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) base[wid] = atomicAdd(a.ticket, 1);
+    int* done = a.sync;
+    if (lane == 0) base[wid] = atomicAdd(a.sync + a.n_levels, 1);
     __syncwarp();
     int s = base[wid];
     if (s >= a.n_slices) return;
+    int L = a.slice_level[s];
+    if (lane == 0 && L > 0) wait_level(done, L - 1, a.level_slices[L - 1], a.err);
+    __syncwarp();
     int slot = s * 32 + lane;
     int r = a.perm[slot];
-    if (r < 0) return;
-    int64_t b0 = a.sptr[s];
-    int w = (int)((a.sptr[s + 1] - b0) / 32);
-    double acc = a.alpha * __ldg(a.b + r);
-    const int32_t* cp = a.col + b0 + lane;
-    const double* vp = a.val + b0 + lane;
-    for (int k0 = 0; k0 < w; k0 += U) {
-        int c[U];
-        double v[U], xv[U];
+    if (r >= 0) {
+        int64_t b0 = a.sptr[s];
+        int w = (int)((a.sptr[s + 1] - b0) / 32);
+        double acc = a.alpha * __ldg(a.b + r);
+        const int32_t* cp = a.col + b0 + lane;
+        const double* vp = a.val + b0 + lane;
+        for (int k0 = 0; k0 < w; k0 += U) {
+            int c[U];
+            double v[U], xv[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            bool in = k0 + u < w;
-            c[u] = in ? __ldg(cp + (int64_t)(k0 + u) * 32) : -1;
-            v[u] = in ? __ldg(vp + (int64_t)(k0 + u) * 32) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? ld_relaxed(a.x + c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (c[u] >= 0) {
-                long long spins = 0;
-                while (is_sentinel(xv[u])) {
-                    if (++spins > SPIN_LIMIT) { atomicExch(a.err, 2); xv[u] = 0.0; break; }
-                    xv[u] = ld_relaxed(a.x + c[u]);
-                }
-                acc = fma(-v[u], xv[u], acc);
+            for (int u = 0; u < U; ++u) {
+                bool in = k0 + u < w;
+                c[u] = in ? __ldg(cp + (int64_t)(k0 + u) * 32) : -1;
+                v[u] = in ? __ldg(vp + (int64_t)(k0 + u) * 32) : 0.0;
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u) xv[u] = c[u] >= 0 ? __ldcg(a.x + c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = fma(-v[u], xv[u], acc);
+        }
+        double xr = acc * a.dinv[slot];
+        __stcg(a.x + r, xr);
+        if (a.out2) a.out2[r] = xr + a.add[r];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        atomicAdd(done + L, 1);
+        int f = atomicAdd(a.sync + a.n_levels + 1, 1);
+        if (f == a.n_slices - 1) {           // last slice of the solve: reset
+            for (int l = 0; l < a.n_levels; ++l) done[l] = 0;
+            a.sync[a.n_levels] = 0;
+            a.sync[a.n_levels + 1] = 0;
+            __threadfence();
         }
     }
-    double xr = publishable(acc * a.dinv[slot]);
-    st_relaxed(a.x + r, xr);
-    if (a.out2) a.out2[r] = xr + a.add[r];
+}
+
+struct LsArgs {
+    const int* perm;
+    const int64_t* sptr;
+    const int32_t* col;
+    const double* val;
+    const double* dinv;
+    const int* level_start;
+    int n_levels;
+    unsigned* bar;        // [count, generation]
+    const double* b;
+    double alpha;
+    double* x;
+    const double* add;
+    double* out2;
+};
+
+// Level-synchronous persistent solve: all co-resident warps sweep the slices
+// of one level, then a software grid barrier; no per-entry polling.
+// Row data of one slot, prefetched before the grid barrier that precedes its
+// level: only the gather of already-final x entries remains on the critical path.
+template <int K>
+struct RowPre {
+    int r, w;
+    int64_t b0;
+    int c[K];
+    double v[K];
+    double bias, dinv;
+};
+
+template <int K>
+__device__ __forceinline__ void row_prefetch(const LsArgs& a, int s, int lane, RowPre<K>& p) {
+    int slot = s * 32 + lane;
+    p.r = a.perm[slot];
+    p.b0 = a.sptr[s];
+    p.w = (int)((a.sptr[s + 1] - p.b0) / 32);
+    const int32_t* cp = a.col + p.b0 + lane;
+    const double* vp = a.val + p.b0 + lane;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+        bool in = u < p.w;
+        p.c[u] = in ? __ldg(cp + (int64_t)u * 32) : -1;
+        p.v[u] = in ? __ldg(vp + (int64_t)u * 32) : 0.0;
+    }
+    p.bias = p.r >= 0 ? a.alpha * __ldg(a.b + p.r) : 0.0;
+    p.dinv = a.dinv[slot];
+}
+
+template <int K>
+__device__ __forceinline__ void row_finish(const LsArgs& a, int lane, const RowPre<K>& p) {
+    if (p.r < 0) return;
+    double xv[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) xv[u] = p.c[u] >= 0 ? __ldcg(a.x + p.c[u]) : 0.0;
+    double acc = p.bias;
+#pragma unroll
+    for (int u = 0; u < K; ++u) acc = fma(-p.v[u], xv[u], acc);
+    // rows wider than K (rare): remaining entries without prefetch
+    const int32_t* cp = a.col + p.b0 + lane;
+    const double* vp = a.val + p.b0 + lane;
+    for (int k = K; k < p.w; ++k) {
+        int c = __ldg(cp + (int64_t)k * 32);
+        if (c >= 0) acc = fma(-__ldg(vp + (int64_t)k * 32), __ldcg(a.x + c), acc);
+    }
+    double xr = acc * p.dinv;
+    __stcg(a.x + p.r, xr);
+    if (a.out2) a.out2[p.r] = xr + a.add[p.r];
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) k_trsv_ls(LsArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    RowPre<K> pre;
+    bool have = false;
+    {
+        int s = a.level_start[0] + gw;
+        if (a.n_levels > 0 && s < a.level_start[1]) { row_prefetch<K>(a, s, lane, pre); have = true; }
+    }
+    for (int L = 0; L < a.n_levels; ++L) {
+        int s0 = a.level_start[L], s1 = a.level_start[L + 1];
+        if (have) row_finish<K>(a, lane, pre);
+        for (int s = s0 + gw + nw; s < s1; s += nw) {   // levels wider than the grid
+            RowPre<K> q;
+            row_prefetch<K>(a, s, lane, q);
+            row_finish<K>(a, lane, q);
+        }
+        have = false;
+        if (L + 1 < a.n_levels) {
+            int s = s1 + gw;
+            if (s < a.level_start[L + 2]) { row_prefetch<K>(a, s, lane, pre); have = true; }
+            grid_barrier(a.bar, a.bar + 1, gridDim.x);
+        }
+    }
+}
+
+__global__ void k_slice_level(const int* __restrict__ pstart, int nl, int* __restrict__ slice_level,
+                              int* __restrict__ level_slices, int* __restrict__ level_start) {
+    int L = blockIdx.x * blockDim.x + threadIdx.x;
+    if (L >= nl) return;
+    int s0 = pstart[L] / 32, s1 = pstart[L + 1] / 32;
+    level_slices[L] = s1 - s0;
+    level_start[L] = s0;
+    if (L == nl - 1) level_start[nl] = s1;
+    for (int s = s0; s < s1; ++s) slice_level[s] = L;
 }
 
 }  // namespace
 
 // Build the level-ordered SELL plan for deps (pattern and, optionally, values).
-void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& p) {
+void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& p, bool allow_chain) {
     const int n = deps.n_rows;
     p.n = n;
     p.unit = unit;
+    p.is_chain = false;
+    if (allow_chain && n > 0 && build_chain(c, deps, diag, unit, p.chain)) {
+        p.is_chain = true;
+        p.n_dep = deps.nnz;
+        p.n_levels = 0;
+        return;
+    }
     p.n_dep = deps.nnz;
     p.ticket.reset(c, 1);
     if (n == 0) {
@@ -209,6 +350,14 @@ void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool rev
     k_scatter_perm<<<ceil_div(n, 256), 256, 0, c->stream>>>(skeys.p, srows.p, n, ustart.p, pstart.p, p.perm.p);
     check_launch("k_scatter_perm");
     int n_slices = (int)(slots / 32);
+    p.slice_level.reset(c, std::max(n_slices, 1));
+    p.level_slices.reset(c, nl);
+    p.level_start.reset(c, nl + 1);
+    k_slice_level<<<ceil_div(nl, 128), 128, 0, c->stream>>>(pstart.p, nl, p.slice_level.p, p.level_slices.p,
+                                                           p.level_start.p);
+    check_launch("k_slice_level");
+    p.sync.reset(c, (size_t)nl + 2);
+    EDFA_CUDA(cudaMemsetAsync(p.sync.p, 0, sizeof(int) * (nl + 2), c->stream));
     DevBuf<int64_t> wb(c, (size_t)n_slices + 1);
     k_slice_width<<<ceil_div((int64_t)n_slices * 32, 256), 256, 0, c->stream>>>(p.perm.p, n_slices, deps.ptr.p,
                                                                                wb.p);
@@ -236,6 +385,10 @@ void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool rev
 
 // (Re)load coefficient values and diagonal of an existing plan from deps.
 void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& p) {
+    if (p.is_chain) {
+        chain_values(c, deps, diag, p.chain);
+        return;
+    }
     int n_slices = p.n_slots / 32;
     if (n_slices == 0) return;
     Prof pr(c, "trsv_plan", 20.0 * p.n_stored);
@@ -247,14 +400,22 @@ void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& p) {
 void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name) {
     if (p.n == 0) return;
-    fill_bits(c, x, p.n, SENTINEL_BITS);
-    EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
-    SolveArgs a{p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.n_slots / 32, b, alpha, x, add, out2,
-                p.ticket.p, c->d_scalar_i + 8};
+    if (p.is_chain) {
+        run_chain(c, p.chain, b, alpha, x, add, out2, name);
+        return;
+    }
+    LsArgs a{p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.level_start.p, p.n_levels,
+             reinterpret_cast<unsigned*>(p.sync.p), b, alpha, x, add, out2};
     double bytes = 12.0 * p.n_dep + 8.0 * p.n + 16.0 * p.n + (out2 ? 16.0 * p.n : 0.0);
     Prof pr(c, name, bytes);
-    int n_slices = p.n_slots / 32;
-    k_trsv<4><<<ceil_div(n_slices, 8), 256, 0, c->stream>>>(a);
+    static int grid = 0;
+    if (!grid) {
+        int occ = 0;
+        EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv_ls<16>, 256, 0));
+        grid = NUM_SMS_B200 * std::max(1, std::min(occ, 2));
+    }
+    void* args[] = {&a};
+    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)k_trsv_ls<16>, dim3(grid), dim3(256), args, 0, c->stream));
     check_launch("k_trsv");
 }
 
