@@ -138,6 +138,10 @@ int edfa_system_create(edfa_ctx* ctx, const edfa_csr* A_ff, const edfa_csr* A_fc
                        const edfa_csr* A_cf, const edfa_csr* A_cc, edfa_system** out);
 /* update_accumulation: replace A_cc (face blocks untouched; assembly.py:314-333). */
 int edfa_system_set_cc(edfa_ctx* ctx, edfa_system* sys, const edfa_csr* A_cc);
+/* Optional hint: cells are the natural-order (x fastest) cells of an
+ * nx*ny*nz box (hx/grid.py:49-50).  Enables tile-DAG triangular solves of the
+ * Schur ILU; results do not depend on it. */
+int edfa_system_set_grid(edfa_system* sys, int32_t nx, int32_t ny, int32_t nz);
 int edfa_system_destroy(edfa_system* sys);
 
 /* ---- restriction patterns ---------------------------------------------- */

@@ -62,6 +62,7 @@ _SIGS = {
     "edfa_csr_destroy": (i32, [vp]),
     "edfa_system_create": (i32, [vp, vp, vp, vp, vp, C.POINTER(vp)]),
     "edfa_system_set_cc": (i32, [vp, vp, vp]),
+    "edfa_system_set_grid": (i32, [vp, i32, i32, i32]),
     "edfa_system_destroy": (i32, [vp]),
     "edfa_pattern_static": (i32, [vp, i32, i32, vp, vp, vp, C.c_char, i32, C.POINTER(vp)]),
     "edfa_stage1_build": (i32, [vp, vp, vp, C.POINTER(Dynamic), f64, i32, f64, i32, C.POINTER(vp)]),

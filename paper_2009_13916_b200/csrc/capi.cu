@@ -146,6 +146,16 @@ int edfa_system_set_cc(edfa_ctx* ctx, edfa_system* sys, const edfa_csr* A_cc) {
     API_END
 }
 
+int edfa_system_set_grid(edfa_system* sys, int32_t nx, int32_t ny, int32_t nz) {
+    API_BEGIN
+    require(sys != nullptr, EDFA_ERR_VALUE, "system is NULL");
+    require(nx >= 0 && ny >= 0 && nz >= 0, EDFA_ERR_VALUE, "negative grid dimensions");
+    sys->dims[0] = nx;
+    sys->dims[1] = ny;
+    sys->dims[2] = nz;
+    API_END
+}
+
 int edfa_system_destroy(edfa_system* sys) {
     API_BEGIN
     delete sys;

@@ -282,7 +282,7 @@ void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f) {
     build_plan(c, LT, f.diag.p, false, true, f.bwd);
 }
 
-void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f) {
+void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int* dims) {
     require(drop_tol == 0.0, EDFA_ERR_UNSUPPORTED,
             "ILU with a drop tolerance (schur_drop_tol > 0) is not implemented on the GPU path; use 0 with no_fill");
     const int n = S.n_rows;
@@ -331,9 +331,21 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f) {
     require(err == 0, EDFA_ERR_CUDA, "ILU(0) factorisation failed");
     Csr Lv, Uv;
     select_part(c, f.LU, 0, 1.0, true, Lv);
-    plan_values(c, Lv, nullptr, f.fwd);
     select_part(c, f.LU, 1, 1.0, true, Uv);
-    build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
+    // cell-grid factors: tile-DAG solves; otherwise level-synchronous plans
+    if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
+        f.fwd.is_tile = true;
+    } else {
+        plan_values(c, Lv, nullptr, f.fwd);
+    }
+    if (dims && build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile)) {
+        f.bwd.is_tile = true;
+        f.bwd.n = n;
+        f.bwd.n_dep = Uv.nnz;
+        f.bwd.n_levels = f.bwd.tile.n_tile_levels;
+    } else {
+        build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
+    }
 }
 
 void ic_export(Ctx* c, IcFactor& f) {

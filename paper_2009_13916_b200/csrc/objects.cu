@@ -54,6 +54,7 @@ void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynam
     ensure_transposes(c, sys, dyn != nullptr);
     s1->n_free = nf;
     s1->n_cells = nc;
+    for (int d = 0; d < 3; ++d) s1->dims[d] = sys->dims[d];
     SetupInput in;
     in.A = &Aff;
     in.AT = dyn ? &sys->AffT : nullptr;
@@ -90,7 +91,9 @@ void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, in
             "inner factorisations with fill-in (no_fill=False) are not implemented on the GPU path; "
             "pass no_fill=True for IC(0)/ILU(0)");
     csr_sub(c, A_cc, s1->H, filt == EDFA_FILT_POST_SCHUR ? tau : 0.0, s2->S);
-    ilu0_factor(c, s2->S, schur_drop_tol, s2->ilu);
+    const int* dims = (int64_t)s1->dims[0] * s1->dims[1] * s1->dims[2] == A_cc.n_rows && s1->dims[0] > 0
+                          ? s1->dims : nullptr;
+    ilu0_factor(c, s2->S, schur_drop_tol, s2->ilu, dims);
 }
 
 }  // namespace edfa

@@ -54,9 +54,28 @@ void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, doubl
 void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,
                int* shifts);
 
+struct TilePlan {               // tile-DAG solves of cell-indexed factors (tile.cu)
+    int32_t n = 0, n_tiles = 0, n_tile_levels = 0;
+    int32_t RC = 0, KD = 0, EC = 0;
+    int64_t n_dep = 0;
+    bool unit = false;
+    DevBuf<int32_t> hdr, row_id, ext_id, dptr, dsrc, up_cnt, up_ids, flags, ticket, order;
+    DevBuf<short> lev_ptr, dslot;
+    DevBuf<double> dcoef, dinv;
+    int32_t epoch = 0, ticket_base = 0;
+};
+// dims = {nx, ny, nz} of the cell grid (rows = cells in natural order) or NULL
+bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
+                     TilePlan& tp);
+void tile_values(Ctx* c, const Csr& D, const double* diag, TilePlan& tp);
+void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
+              const char* name);
+
 struct TriPlan {
     bool is_chain = false;
     ChainPlan chain;
+    bool is_tile = false;
+    TilePlan tile;
     int32_t n = 0;          // rows
     int32_t n_slots = 0;    // padded thread count (multiple of 32)
     int32_t n_levels = 0;
@@ -104,7 +123,7 @@ struct IluFactor {              // ILU of S (no fill)
     Csr export_L, export_U;
 };
 void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f);
-void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f);
+void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int* dims);
 void ic_export(Ctx* c, IcFactor& f);
 void ilu_export(Ctx* c, IluFactor& f);
 
@@ -121,6 +140,7 @@ struct edfa_system {
     edfa::Csr AfcT;         // A_fc^T, cells x faces (rows = f-rhs per cell)
     edfa::Csr AffT;         // A_ff^T (columns of A_ff)
     bool have_T = false;
+    int dims[3] = {0, 0, 0};   // cell grid (nx, ny, nz) when cells are a natural-order box
 };
 
 struct edfa_stage1 {
@@ -131,6 +151,7 @@ struct edfa_stage1 {
     edfa::IcFactor ic;
     int32_t max_pattern = 0;
     int32_t n_free = 0, n_cells = 0;
+    int dims[3] = {0, 0, 0};
     edfa_csr views[6];      // borrowed handles returned by edfa_stage1_part
 };
 

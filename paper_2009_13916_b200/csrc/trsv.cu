@@ -404,6 +404,10 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
         run_chain(c, p.chain, b, alpha, x, add, out2, name);
         return;
     }
+    if (p.is_tile) {   // epoch / ticket bookkeeping is per plan (serialised on the stream)
+        run_tile(c, const_cast<TilePlan&>(p.tile), b, alpha, x, add, out2, name);
+        return;
+    }
     LsArgs a{p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.level_start.p, p.n_levels,
              reinterpret_cast<unsigned*>(p.sync.p), b, alpha, x, add, out2};
     double bytes = 12.0 * p.n_dep + 8.0 * p.n + 16.0 * p.n + (out2 ? 16.0 * p.n : 0.0);

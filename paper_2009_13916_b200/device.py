@@ -142,6 +142,15 @@ class DeviceSystem:
                                             C.byref(self.handle)))
         self._rhs = None if rhs is None else as_device_vector(rhs, self.n_unknowns)
         self._src = {}
+        grid = getattr(host, "grid", None)
+        if grid is not None and all(hasattr(grid, a) for a in ("nx", "ny", "nz")) \
+                and grid.nx * grid.ny * grid.nz == self.n_cells:
+            self.set_grid(grid.nx, grid.ny, grid.nz)
+
+    def set_grid(self, nx: int, ny: int, nz: int) -> None:
+        """Declare cells as the natural-order cells of an nx*ny*nz box
+        (enables the tile-DAG Schur solves; numerics do not depend on it)."""
+        L.check(L.lib().edfa_system_set_grid(self.handle, int(nx), int(ny), int(nz)))
 
     @classmethod
     def from_host(cls, system) -> "DeviceSystem":
