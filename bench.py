@@ -213,7 +213,7 @@ def run_edfa(args):
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     def step(system_dev, b):
-        pats = patterns_for(system_dev, "static", "A", grid=s.grid)
+        pats = patterns_for(system_dev, "static", "A")
         pre = BlockLDUPreconditioner.build(system_dev, patterns=pats, no_fill=True)
         x, rep = gmres(system_operator(system_dev), pre, b, tol=case.rtol, restart=case.restart,
                        max_it=case.max_it)

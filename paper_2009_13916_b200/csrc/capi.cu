@@ -169,22 +169,27 @@ int edfa_pattern_static(edfa_ctx* ctx, int32_t n_cells, int32_t n_faces, const i
     API_BEGIN
     Ctx* c = &ctx->c;
     require(n_cells >= 0 && n_faces >= 0, EDFA_ERR_VALUE, "negative sizes");
-    DevBuf<int32_t> e2f(c, (size_t)n_cells * 6), nbr(c, (size_t)n_cells * 6), fidx(c, std::max(n_faces, 1));
-    upload(c, e2f.p, elem_to_faces, sizeof(int32_t) * 6 * n_cells, mem);
-    upload(c, nbr.p, neighbors, sizeof(int32_t) * 6 * n_cells, mem);
-    upload(c, fidx.p, face_index, sizeof(int32_t) * n_faces, mem);
+    DevBuf<int32_t> e2f, nbr, fidx;
+    const int32_t *pe2f = elem_to_faces, *pnbr = neighbors, *pfidx = face_index;
     int32_t n_free = 0;
-    {
-        // number of free faces = max(face_index) + 1 (computed on the host side of the ABI)
-        std::vector<int32_t> h(n_faces);
-        if (mem == EDFA_MEM_HOST) std::copy(face_index, face_index + n_faces, h.begin());
-        else if (n_faces) EDFA_CUDA(cudaMemcpy(h.data(), face_index, 4 * (size_t)n_faces, cudaMemcpyDeviceToHost));
-        for (auto v : h) n_free = std::max(n_free, v + 1);
+    if (mem == EDFA_MEM_HOST) {
+        e2f.reset(c, (size_t)n_cells * 6);
+        nbr.reset(c, (size_t)n_cells * 6);
+        fidx.reset(c, std::max(n_faces, 1));
+        upload(c, e2f.p, elem_to_faces, sizeof(int32_t) * 6 * n_cells, mem);
+        upload(c, nbr.p, neighbors, sizeof(int32_t) * 6 * n_cells, mem);
+        upload(c, fidx.p, face_index, sizeof(int32_t) * n_faces, mem);
+        pe2f = e2f.p;
+        pnbr = nbr.p;
+        pfidx = fidx.p;
+        for (int32_t k = 0; k < n_faces; ++k) n_free = std::max(n_free, face_index[k] + 1);
+    } else {
+        n_free = max_value_plus_one(c, face_index, n_faces);   // device reduction, 4-byte readback
     }
     auto* h = new edfa_csr();
     h->ctx = c;
     try {
-        static_pattern(c, n_cells, n_free, e2f.p, nbr.p, fidx.p, prototype, h->own);
+        static_pattern(c, n_cells, n_free, pe2f, pnbr, pfidx, prototype, h->own);
     } catch (...) {
         delete h;
         throw;

@@ -103,15 +103,35 @@ __global__ void __launch_bounds__(256) k_ic0(LevelArgs la, const int32_t* __rest
 // ILU(0) of S, one warp per row.  LU starts as a copy of S; on exit its
 // strictly lower part holds the multipliers and its strictly upper part U;
 // pivots go to udiag.
+__host__ __device__ constexpr size_t ilu0_warp_smem(int rmax) {
+    return ((size_t)(3 * rmax + 1024) * 8 + (size_t)(4 * rmax + 1 + 1024 + 2) * 4 + 15) & ~size_t(15);
+}
+
+// position of the first strictly-upper entry of every row
+__global__ void k_ustart(CsrV A, int32_t* __restrict__ us) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < A.n_rows) us[i] = lower_bound(A.idx, A.ptr[i], A.ptr[i + 1], i + 1);
+}
+
 template <int RMAX>
 __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __restrict__ Sp,
-                                              const int32_t* __restrict__ Si, double* __restrict__ LU,
-                                              const double* __restrict__ scale, double* __restrict__ udiag,
-                                              int* shifts, int* err) {
+                                              const int32_t* __restrict__ Si, const int32_t* __restrict__ ustart,
+                                              double* __restrict__ LU, const double* __restrict__ scale,
+                                              double* __restrict__ udiag, int* shifts, int* err) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int ECAP = 1024;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* cols = reinterpret_cast<int*>(smem) + wid * RMAX;
-    double* vals = reinterpret_cast<double*>(smem + sizeof(int) * RMAX * (blockDim.x >> 5)) + wid * RMAX;
+    // per-warp scratch: row, pivot metadata, staged U entries of a pivot chunk
+    unsigned char* base = smem + (size_t)wid * ilu0_warp_smem(RMAX);
+    double* vals = reinterpret_cast<double*>(base);
+    double* pdk = vals + RMAX;
+    double* eval = pdk + RMAX;
+    int* cols = reinterpret_cast<int*>(eval + ECAP);
+    int* pu0 = cols + RMAX;
+    int* pcnt = pu0 + RMAX;
+    int* poff = pcnt + RMAX;           // RMAX + 1
+    int* eslot = poff + RMAX + 1;      // ECAP
+    int* misc = eslot + ECAP;          // 2
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     for (int L = 0; L < la.n_levels; ++L) {
@@ -130,17 +150,79 @@ __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __res
             }
             __syncwarp();
             int nl = lower_bound(cols, 0, n, i);
-            for (int p = 0; p < nl; ++p) {
+            // every pivot row is final (earlier level): fetch its pivot and
+            // U-row extent in parallel
+            for (int p = lane; p < nl; p += 32) {
                 int k = cols[p];
-                double mult = __ddiv_rn(vals[p], __ldcg(udiag + k));
-                __syncwarp();
-                if (lane == 0) vals[p] = mult;
-                int u0 = lower_bound(Si, Sp[k], Sp[k + 1], k + 1), u1 = Sp[k + 1];
-                for (int e = u0 + lane; e < u1; e += 32) {
-                    int slot_j = bsearch(cols, p + 1, n, Si[e]);
-                    if (slot_j >= 0) vals[slot_j] = sub_mul(vals[slot_j], mult, __ldcg(LU + e));
+                pdk[p] = __ldcg(udiag + k);
+                int u0 = __ldg(ustart + k);
+                pu0[p] = u0;
+                pcnt[p] = Sp[k + 1] - u0;
+            }
+            __syncwarp();
+            for (int p0 = 0; p0 < nl;) {
+                if (lane == 0) {   // chunk of pivots whose U entries fit the staging buffer
+                    int acc = 0, p1 = p0;
+                    while (p1 < nl && (p1 == p0 || acc + pcnt[p1] <= ECAP)) {
+                        poff[p1 - p0] = acc;
+                        acc += pcnt[p1];
+                        ++p1;
+                    }
+                    poff[p1 - p0] = acc;
+                    misc[0] = p1;
+                    misc[1] = min(acc, ECAP);
                 }
                 __syncwarp();
+                const int p1 = misc[0], tot = misc[1];
+                // stage (target slot, u_kj) of every U entry of the chunk
+                for (int f0 = 0; f0 < tot; f0 += 32 * 4) {
+                    int e[4], q[4];
+                    double u[4];
+                    int32_t j[4];
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        int f = f0 + w * 32 + lane;
+                        q[w] = -1;
+                        if (f < tot) {
+                            int lo2 = 0, hi2 = p1 - p0;      // pivot owning flat entry f
+                            while (hi2 - lo2 > 1) {
+                                int mid = (lo2 + hi2) >> 1;
+                                if (poff[mid] <= f) lo2 = mid;
+                                else hi2 = mid;
+                            }
+                            q[w] = p0 + lo2;
+                            e[w] = pu0[q[w]] + (f - poff[lo2]);
+                        }
+                    }
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        if (q[w] >= 0) {
+                            j[w] = __ldg(Si + e[w]);
+                            u[w] = __ldcg(LU + e[w]);
+                        }
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        int f = f0 + w * 32 + lane;
+                        if (q[w] >= 0) {
+                            eslot[f] = bsearch(cols, q[w] + 1, n, j[w]);
+                            eval[f] = u[w];
+                        }
+                    }
+                }
+                __syncwarp();
+                // eliminate, pivots in increasing column order (reference IKJ order)
+                for (int p = p0; p < p1; ++p) {
+                    double mult = __ddiv_rn(vals[p], pdk[p]);
+                    __syncwarp();
+                    if (lane == 0) vals[p] = mult;
+                    const int off = poff[p - p0], cnt = min(pcnt[p], tot - off);
+                    for (int f = lane; f < cnt; f += 32) {
+                        int s = eslot[off + f];
+                        if (s >= 0) vals[s] = sub_mul(vals[s], mult, eval[off + f]);
+                    }
+                    __syncwarp();
+                }
+                p0 = p1;
             }
             int dslot = bsearch(cols, nl, n, i);
             double piv = dslot >= 0 ? vals[dslot] : 0.0;
@@ -304,8 +386,12 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
     int* flags = c->d_scalar_i + 24;
     EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
     if (n) {
+        DevBuf<int32_t> ust(c, n);
+        k_ustart<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(f.LU), ust.p);
+        check_launch("k_ustart");
         const int32_t* Sp = f.LU.ptr.p;
         const int32_t* Si = f.LU.idx.p;
+        const int32_t* Us = ust.p;
         double* LUv = f.LU.val.p;
         const double* scp = sc.p;
         double* ud = f.udiag.p;
@@ -313,10 +399,10 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         int* er = flags + 1;
         Prof pr(c, "ilu0_factor", 24.0 * S.nnz + 24.0 * n);
         LevelArgs la{f.fwd.perm.p, f.fwd.level_start.p, f.fwd.n_levels, reinterpret_cast<unsigned*>(f.fwd.sync.p)};
-        void* args[] = {&la, &Sp, &Si, &LUv, &scp, &ud, &sh, &er};
+        void* args[] = {&la, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
         auto launch = [&](auto kern, int rmax) {
-            int threads = 256;
-            size_t smem = (size_t)rmax * (sizeof(int) + sizeof(double)) * (threads / 32);
+            int threads = rmax >= 1024 ? 64 : 128;
+            size_t smem = ilu0_warp_smem(rmax) * (threads / 32);
             if (smem > 48 * 1024)
                 EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int grid = coop_grid(kern, threads, smem);

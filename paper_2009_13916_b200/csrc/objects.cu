@@ -16,6 +16,27 @@ __global__ void k_row_len_max(const int32_t* __restrict__ ptr, int n, int* __res
 }
 }  // namespace
 
+namespace {
+__global__ void k_max_plus_one(const int32_t* __restrict__ v, int n, int* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int x = i < n ? v[i] + 1 : 0;
+    x = warp_max(x);
+    if ((threadIdx.x & 31) == 0 && x > 0) atomicMax(out, x);
+}
+}  // namespace
+
+int max_value_plus_one(Ctx* c, const int32_t* v, int n) {
+    if (n <= 0) return 0;
+    int* d = c->d_scalar_i + 44;
+    EDFA_CUDA(cudaMemsetAsync(d, 0, sizeof(int), c->stream));
+    k_max_plus_one<<<ceil_div(n, 256), 256, 0, c->stream>>>(v, n, d);
+    check_launch("k_max_plus_one");
+    int h = 0;
+    EDFA_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    return h;
+}
+
 int max_row_nnz(Ctx* c, const Csr& A) {
     if (A.n_rows == 0) return 0;
     int* d = c->d_scalar_i + 40;

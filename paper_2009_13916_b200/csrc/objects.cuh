@@ -29,6 +29,7 @@ void pattern_compact(Ctx* c, int32_t n, const DevBuf<int32_t>& slot_ptr, const D
 void static_pattern(Ctx* c, int32_t n_cells, int32_t n_free, const int32_t* e2f, const int32_t* nbr,
                     const int32_t* fidx, char proto, Csr& out);
 int max_row_nnz(Ctx* c, const Csr& A);
+int max_value_plus_one(Ctx* c, const int32_t* v, int n);
 
 // ---- H~ = G~ A_ff F~ (product.cu)
 void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double post_tau, Csr& H);

@@ -19,6 +19,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "dev_util.cuh"
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
     if (threadIdx.x == 0) {
         for (int r = 0; r < n; ++r) cnt[lev[r] + 1]++;
         for (int l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
-        short* lp = b.lev_ptr + (size_t)t * (b.RC + 1);
+        short* lp = b.lev_ptr + (size_t)t * ((b.RC + 8) & ~7);
         for (int l = 0; l <= nlev; ++l) lp[l] = (short)cnt[l];
         for (int r = 0; r < n; ++r) {
             int p = cnt[lev[r]]++;
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
     }
     for (int q = threadIdx.x; q < ne; q += blockDim.x) b.ext_id[(size_t)t * b.EC + q] = ext[q];
     // per-row dependency counts -> local offsets (thread 0 scan; n <= RC)
-    int* dp = b.dptr + (size_t)t * (b.RC + 1);
+    int* dp = b.dptr + (size_t)t * ((b.RC + 4) & ~3);
     if (threadIdx.x == 0) {
         int acc = 0;
         for (int p = 0; p < n; ++p) {
@@ -306,70 +308,123 @@ struct TileSolve {
     const double* add;
     double* out2;
     int* err;
+    long long* dbg;        // optional per-tile phase timestamps (globaltimer ns)
 };
 
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned r16(unsigned b) { return (b + 15u) & ~15u; }
+// TMA bulk copy global -> shared, completion signalled on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mbar) {
+    if (bytes == 0) return;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mbar)) : "memory");
+}
+
 __global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
-    extern __shared__ __align__(16) unsigned char sm[];
+    extern __shared__ __align__(128) unsigned char sm[];
+    // 16-byte aligned sections (capacities padded on the host, see tile_smem_bytes)
     double* xs = reinterpret_cast<double*>(sm);                 // RC + EC
     double* cf = xs + a.RC + a.EC;                              // RC*KD
     double* di = cf + (size_t)a.RC * a.KD;                      // RC
-    short* sl = reinterpret_cast<short*>(di + a.RC);            // RC*KD
-    int* dp = reinterpret_cast<int*>(sl + (size_t)a.RC * a.KD + ((a.RC * a.KD) & 1));   // RC+1
-    short* lp = reinterpret_cast<short*>(dp + a.RC + 1);        // RC+1
-    __shared__ int s_tile;
+    int* rid = reinterpret_cast<int*>(di + a.RC);               // RC
+    int* dp = rid + a.RC;                                       // DPS = RC+1 rounded to 4
+    short* sl = reinterpret_cast<short*>(dp + ((a.RC + 4) & ~3));   // RC*KD
+    short* lp = sl + (size_t)a.RC * a.KD;                       // LPS = RC+1 rounded to 8
+    __shared__ int s_tile, s_hdr[4];
+    __shared__ __align__(8) uint64_t mbar;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&mbar)), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned phase = 0;
+    const int DPS = (a.RC + 4) & ~3, LPS = (a.RC + 8) & ~7;
     for (;;) {
         if (threadIdx.x == 0) {
             int k = atomicAdd(a.ticket, 1) - a.ticket_base;
-            s_tile = k < a.n_tiles ? a.order[k] : -1;
+            int t = k < a.n_tiles ? a.order[k] : -1;
+            s_tile = t;
+            if (t >= 0) {
+                const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
+                s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z; s_hdr[3] = h.w;
+                // 1. stage the tile's plan with TMA bulk copies (independent of
+                //    the solve, overlaps the upstream wait below)
+                unsigned b_cf = r16(8u * h.w), b_sl = r16(2u * h.w), b_dp = r16(4u * (h.x + 1));
+                unsigned b_lp = r16(2u * (h.z + 1)), b_di = r16(8u * h.x), b_ri = r16(4u * h.x);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(smem_addr(&mbar)), "r"(b_cf + b_sl + b_dp + b_lp + b_di + b_ri) : "memory");
+                bulk_g2s(cf, a.dcoef + (size_t)t * a.RC * a.KD, b_cf, &mbar);
+                bulk_g2s(sl, a.dslot + (size_t)t * a.RC * a.KD, b_sl, &mbar);
+                bulk_g2s(dp, a.dptr + (size_t)t * DPS, b_dp, &mbar);
+                bulk_g2s(lp, a.lev_ptr + (size_t)t * LPS, b_lp, &mbar);
+                bulk_g2s(di, a.dinv + (size_t)t * a.RC, b_di, &mbar);
+                bulk_g2s(rid, a.row_id + (size_t)t * a.RC, b_ri, &mbar);
+            }
         }
         __syncthreads();
         const int t = s_tile;
         if (t < 0) break;
-        const int* h = a.hdr + (size_t)t * 4;
-        const int n = h[0], ne = h[1], nlev = h[2], nd = h[3];
-        // 1. stage coefficients and the rhs (independent of the solve)
-        const size_t cbase = (size_t)t * a.RC * a.KD;
-        for (int q = threadIdx.x; q < nd; q += blockDim.x) {
-            cf[q] = __ldg(a.dcoef + cbase + q);
-            sl[q] = a.dslot[cbase + q];
-        }
-        for (int p = threadIdx.x; p <= n; p += blockDim.x) dp[p] = a.dptr[(size_t)t * (a.RC + 1) + p];
-        for (int l = threadIdx.x; l <= nlev; l += blockDim.x) lp[l] = a.lev_ptr[(size_t)t * (a.RC + 1) + l];
-        for (int p = threadIdx.x; p < n; p += blockDim.x) {
-            di[p] = a.dinv[(size_t)t * a.RC + p];
-            int row = a.row_id[(size_t)t * a.RC + p];
-            xs[p] = a.alpha * __ldg(a.b + row);       // rhs staged in the x slots
-        }
-        // 2. wait for upstream tiles
+        const int n = s_hdr[0], ne = s_hdr[1], nlev = s_hdr[2];
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 0] = gtimer();
+        // 2. wait for upstream tiles (relaxed polls: no L1 invalidation per poll)
         const int nu = a.up_cnt[t];
         if (threadIdx.x < nu) {
             const int* f = a.flags + a.up_ids[(size_t)t * 32 + threadIdx.x];
             unsigned ns = 8;
             long long spins = 0;
-            while (ld_acquire(f) != a.epoch) {
+            while (ld_relaxed_i(f) != a.epoch) {
                 __nanosleep(ns);
-                if (ns < 128) ns <<= 1;
+                if (ns < 64) ns <<= 1;
                 if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
             }
+            __threadfence();
+            if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
         }
+        // staged plan must have landed
+        {
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(smem_addr(&mbar)), "r"(phase) : "memory");
+            phase ^= 1u;
+        }
+        // rhs into the x slots
+        for (int p = threadIdx.x; p < n; p += blockDim.x) xs[p] = a.alpha * __ldg(a.b + rid[p]);
         __syncthreads();
         // 3. gather external dependencies
         for (int q = threadIdx.x; q < ne; q += blockDim.x)
             xs[a.RC + q] = __ldcg(a.x + a.ext_id[(size_t)t * a.EC + q]);
         __syncthreads();
-        // 4. local levels
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 2] = gtimer();
+        // 4. local levels: G lanes per row (shuffle-reduced), rows of a level
+        //    spread over the CTA
+        constexpr int G = 8;
+        const int grp = threadIdx.x / G, li = threadIdx.x % G, ngrp = blockDim.x / G;
         for (int l = 0; l < nlev; ++l) {
             int p1 = lp[l + 1];
-            for (int p = lp[l] + threadIdx.x; p < p1; p += blockDim.x) {
-                double acc = xs[p];
-                for (int q = dp[p]; q < dp[p + 1]; ++q) acc = fma(-cf[q], xs[sl[q]], acc);
-                xs[p] = acc * di[p];
+            for (int base = lp[l]; base < p1; base += ngrp) {   // warp-uniform trip count
+                const int p = base + grp;
+                const bool act = p < p1;
+                double acc = 0.0;
+                if (act)
+                    for (int q = dp[p] + li; q < dp[p + 1]; q += G) acc = fma(-cf[q], xs[sl[q]], acc);
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+                if (act && li == 0) xs[p] = (xs[p] + acc) * di[p];
             }
             __syncthreads();
         }
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 3] = gtimer();
         // 5. write back, publish
         for (int p = threadIdx.x; p < n; p += blockDim.x) {
-            int row = a.row_id[(size_t)t * a.RC + p];
+            int row = rid[p];
             double v = xs[p];
             __stcg(a.x + row, v);
             if (a.out2) a.out2[row] = v + a.add[row];
@@ -378,16 +433,19 @@ __global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
         __syncthreads();
         if (threadIdx.x == 0)
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.flags + t), "r"(a.epoch) : "memory");
+        if (a.dbg && threadIdx.x == 0) { a.dbg[t * 6 + 4] = gtimer(); a.dbg[t * 6 + 5] = blockIdx.x; }
     }
 }
 
 }  // namespace
 
+// smem layout of k_tile_solve: xs[RC+EC] cf[RC*KD] di[RC] rid[RC] dp[DPS] sl[RC*KD] lp[LPS]
+// (RC multiple of 8, KD and EC even -> every section starts 16-byte aligned)
 size_t tile_smem_bytes(const TilePlan& tp) {
     size_t rc = tp.RC, kd = tp.KD, ec = tp.EC;
-    size_t bytes = 8 * (rc + ec) + 8 * rc * kd + 8 * rc + 2 * rc * kd + ((rc * kd) & 1) * 2 + 4 * (rc + 1) +
-                   2 * (rc + 1);
-    return (bytes + 15) & ~size_t(15);
+    size_t dps = (rc + 4) & ~size_t(3), lps = (rc + 8) & ~size_t(7);
+    size_t bytes = 8 * (rc + ec) + 8 * rc * kd + 8 * rc + 4 * rc + 4 * dps + 2 * rc * kd + 2 * lps;
+    return (bytes + 127) & ~size_t(127);
 }
 
 bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
@@ -412,18 +470,19 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     const int nt = g.NX * g.NY * g.NZ;
     tp.n = n;
     tp.n_tiles = nt;
-    tp.RC = g.tx * g.ty * g.tz;
-    tp.KD = std::max(hf[1], 1);
-    tp.EC = std::min(tp.RC * tp.KD, 4 * tp.RC + 256);
+    tp.RC = (g.tx * g.ty * g.tz + 7) & ~7;           // per-tile capacities / strides
+    tp.KD = (std::max(hf[1], 1) + 1) & ~1;
+    tp.EC = (std::min(tp.RC * tp.KD, 4 * tp.RC + 256) + 1) & ~1;
     tp.unit = unit;
     tp.n_dep = D.nnz;
     size_t smem = tile_smem_bytes(tp);
     if (smem > 200 * 1024) return false;
+    const size_t dps = (tp.RC + 4) & ~3, lps = (tp.RC + 8) & ~7;
     tp.hdr.reset(c, (size_t)nt * 4);
-    tp.lev_ptr.reset(c, (size_t)nt * (tp.RC + 1));
+    tp.lev_ptr.reset(c, (size_t)nt * lps);
     tp.row_id.reset(c, (size_t)nt * tp.RC);
     tp.ext_id.reset(c, (size_t)nt * tp.EC);
-    tp.dptr.reset(c, (size_t)nt * (tp.RC + 1));
+    tp.dptr.reset(c, (size_t)nt * dps);
     tp.dslot.reset(c, (size_t)nt * tp.RC * tp.KD);
     tp.dsrc.reset(c, (size_t)nt * tp.RC * tp.KD);
     tp.dcoef.reset(c, (size_t)nt * tp.RC * tp.KD);
@@ -492,11 +551,29 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
     tp.epoch += 1;
     TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p, tp.ext_id.p,
                 tp.dptr.p, tp.dslot.p, tp.dcoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p, tp.flags.p, tp.ticket.p,
-                tp.epoch, tp.ticket_base, b, alpha, x, add, out2, c->d_scalar_i + 8};
+                tp.epoch, tp.ticket_base, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr};
+    static const char* dbg_path = getenv("EDFA_TILE_DEBUG");
+    DevBuf<long long> dbg;
+    if (dbg_path) {
+        dbg.reset(c, (size_t)tp.n_tiles * 6);
+        a.dbg = dbg.p;
+    }
     tp.ticket_base += tp.n_tiles + grid;   // every CTA takes exactly one failing ticket
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
     void* args[] = {&a};
     EDFA_CUDA(cudaLaunchCooperativeKernel((void*)k_tile_solve, dim3(grid), dim3(256), args, smem, c->stream));
+    if (dbg_path) {
+        std::vector<long long> h((size_t)tp.n_tiles * 6);
+        EDFA_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        FILE* f = fopen(dbg_path, "w");
+        if (f) {
+            for (int t = 0; t < tp.n_tiles; ++t)
+                fprintf(f, "%d %lld %lld %lld %lld %lld %lld\n", t, h[t * 6], h[t * 6 + 1], h[t * 6 + 2], h[t * 6 + 3],
+                        h[t * 6 + 4], h[t * 6 + 5]);
+            fclose(f);
+        }
+    }
 }
 
 }  // namespace edfa

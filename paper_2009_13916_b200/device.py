@@ -143,9 +143,17 @@ class DeviceSystem:
         self._rhs = None if rhs is None else as_device_vector(rhs, self.n_unknowns)
         self._src = {}
         grid = getattr(host, "grid", None)
+        self.topology = None
         if grid is not None and all(hasattr(grid, a) for a in ("nx", "ny", "nz")) \
                 and grid.nx * grid.ny * grid.nz == self.n_cells:
             self.set_grid(grid.nx, grid.ny, grid.nz)
+        if grid is not None and hasattr(host, "face_index"):
+            # cell->face map, neighbours and free-face index, resident with the
+            # blocks (inputs of the static-pattern kernel)
+            from .patterns import grid_topology
+            e2f, nbr = grid_topology(grid)
+            self.topology = tuple(torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to("cuda")
+                                  for a in (e2f, nbr, np.asarray(host.face_index)))
 
     def set_grid(self, nx: int, ny: int, nz: int) -> None:
         """Declare cells as the natural-order cells of an nx*ny*nz box

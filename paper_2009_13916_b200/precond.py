@@ -330,6 +330,9 @@ def patterns_for(system, kind: str, prototype: str = "A", grid=None) -> PatternS
             return base_pattern(system.A_cf)
         return base_pattern(system.A_cf)
     if kind == "static":
+        if isinstance(system, DeviceSystem) and grid is None and system.topology is not None:
+            from .patterns import static_patterns_device
+            return static_patterns_device(system.topology, prototype)
         host = system.host if isinstance(system, DeviceSystem) else system
         return static_patterns(grid or host.grid, host.face_index, prototype)
     raise ValueError(f"unknown pattern kind {kind!r}")
