@@ -132,6 +132,86 @@ __global__ void k_chain_ic0(const int* __restrict__ rows, const int64_t* __restr
     if (cnt) atomicAdd(shifts, cnt);
 }
 
+struct I64 {
+    __host__ __device__ int64_t operator()(int v) const { return (int64_t)v; }
+};
+
+// contiguous (chain-major) layout for the scan solver
+__global__ void k_chain_fill_contig(CsrV D, const int* __restrict__ succ, const int* __restrict__ heads, int n_chains,
+                                    const int64_t* __restrict__ cptr, int* __restrict__ rows, double* __restrict__ coef,
+                                    double* __restrict__ dinv, const double* __restrict__ diag, bool unit) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_chains) return;
+    int64_t p = cptr[t];
+    for (int r = heads[t]; r >= 0; r = succ[r], ++p) {
+        rows[p] = r;
+        int e = D.ptr[r];
+        coef[p] = (D.ptr[r + 1] > e && D.val) ? D.val[e] : 0.0;
+        dinv[p] = (unit || !diag) ? 1.0 : 1.0 / diag[r];
+    }
+}
+
+// One warp per chain: x_i = d_i (alpha b_i - c_i x_{i-1}) is an affine
+// recurrence x_i = a_i + m_i x_{i-1}; lanes compose their segment's maps,
+// a warp scan composes across lanes, then every lane replays its segment.
+// Depth log2(32) + E instead of the chain length.
+template <int E>
+__global__ void __launch_bounds__(256) k_chain_scan(const int64_t* __restrict__ cptr, const int* __restrict__ rows,
+                                                    const double* __restrict__ coef, const double* __restrict__ dinv,
+                                                    int n_chains, const double* __restrict__ b, double alpha,
+                                                    double* __restrict__ x, const double* __restrict__ add,
+                                                    double* __restrict__ out2) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= n_chains) return;
+    const int64_t s = cptr[w], e = cptr[w + 1];
+    double xin = 0.0;
+    for (int64_t c0 = s; c0 < e; c0 += 32 * E) {
+        int r[E];
+        double al[E], be[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            int64_t q = c0 + lane * E + j;
+            r[j] = q < e ? rows[q] : -1;
+            double d = q < e ? dinv[q] : 0.0, cf = q < e ? coef[q] : 0.0;
+            al[j] = d;
+            be[j] = -cf * d;
+        }
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            if (r[j] >= 0) al[j] = al[j] * (alpha * b[r[j]]);
+            else { al[j] = 0.0; be[j] = 1.0; }
+        }
+        double A = al[0], B = be[0];
+#pragma unroll
+        for (int j = 1; j < E; ++j) {
+            A = fma(be[j], A, al[j]);
+            B = be[j] * B;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            double Ap = __shfl_up_sync(0xffffffffu, A, off), Bp = __shfl_up_sync(0xffffffffu, B, off);
+            if (lane >= off) {
+                A = fma(B, Ap, A);
+                B = B * Bp;
+            }
+        }
+        double Ae = __shfl_up_sync(0xffffffffu, A, 1), Be = __shfl_up_sync(0xffffffffu, B, 1);
+        if (lane == 0) { Ae = 0.0; Be = 1.0; }
+        double xl = fma(Be, xin, Ae);
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            double v = fma(be[j], xl, al[j]);
+            if (r[j] >= 0) {
+                x[r[j]] = v;
+                if (out2) out2[r[j]] = v + add[r[j]];
+            }
+            xl = v;
+        }
+        double A31 = __shfl_sync(0xffffffffu, A, 31), B31 = __shfl_sync(0xffffffffu, B, 31);
+        xin = fma(B31, xin, A31);
+    }
+}
+
 }  // namespace
 
 // Try to build a chain plan for deps; returns false if deps is not chain-structured.
@@ -188,9 +268,24 @@ bool build_chain(Ctx* c, const Csr& deps, const double* diag, bool unit, ChainPl
     cp.dinv.reset(c, std::max<int64_t>(total, 1));
     cp.heads = std::move(heads_s);
     cp.succ = std::move(succ);
+    cp.cptr.reset(c, (size_t)nc + 1);
+    {
+        size_t bytes = 0;
+        cub::TransformInputIterator<int64_t, I64, const int*> it(lens_s.p, I64());
+        cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, cp.cptr.p, nc, c->stream);
+        EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(bytes), bytes, it, cp.cptr.p, nc, c->stream));
+        int64_t nn = n;
+        EDFA_CUDA(cudaMemcpyAsync(cp.cptr.p + nc, &nn, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    cp.crow.reset(c, n);
+    cp.ccoef.reset(c, n);
+    cp.cdinv.reset(c, n);
     Prof pr(c, "chain_plan", 24.0 * total);
     k_chain_fill<<<ceil_div(nc, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, nc, cp.gbase.p,
                                                            cp.rows.p, cp.coef.p, cp.dinv.p, diag, unit);
+    k_chain_fill_contig<<<ceil_div(nc, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, nc, cp.cptr.p,
+                                                                  cp.crow.p, cp.ccoef.p, cp.cdinv.p, diag, unit);
     check_launch("k_chain_fill");
     return true;
 }
@@ -200,15 +295,17 @@ void chain_values(Ctx* c, const Csr& deps, const double* diag, ChainPlan& cp) {
     k_chain_fill<<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, cp.n_chains,
                                                                     cp.gbase.p, cp.rows.p, cp.coef.p, cp.dinv.p,
                                                                     diag, cp.unit);
+    k_chain_fill_contig<<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(
+        view(deps), cp.succ.p, cp.heads.p, cp.n_chains, cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, diag, cp.unit);
     check_launch("k_chain_fill");
 }
 
 void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add, double* out2,
                const char* name) {
     Prof pr(c, name, 12.0 * cp.n + 24.0 * cp.n + (out2 ? 16.0 * cp.n : 0.0));
-    k_chain_solve<16><<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(cp.rows.p, cp.coef.p, cp.dinv.p, cp.gbase.p,
-                                                                       cp.n_chains, b, alpha, x, add, out2);
-    check_launch("k_chain_solve");
+    k_chain_scan<4><<<ceil_div((int64_t)cp.n_chains * 32, 256), 256, 0, c->stream>>>(
+        cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha, x, add, out2);
+    check_launch("k_chain_scan");
 }
 
 void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,

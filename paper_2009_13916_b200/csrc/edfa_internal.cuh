@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <ctime>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -108,6 +110,36 @@ struct Prof {
             cudaEvent_t e1 = c->get_event();
             cudaEventRecord(e1, c->stream);
             c->pending.push_back({name, e0, e1, bytes});
+        }
+    }
+};
+
+// Host-side phase timer (EDFA_PHASE_TIMING=1): synchronises the stream at
+// both ends and prints the phase's wall time -- diagnostics only.
+struct PhaseTimer {
+    Ctx* c;
+    const char* name;
+    double t0 = 0;
+    bool on;
+    static bool enabled() {
+        static const bool e = getenv("EDFA_PHASE_TIMING") != nullptr;
+        return e;
+    }
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    }
+    PhaseTimer(Ctx* ctx, const char* nm) : c(ctx), name(nm), on(enabled()) {
+        if (on) {
+            cudaStreamSynchronize(c->stream);
+            t0 = now();
+        }
+    }
+    ~PhaseTimer() {
+        if (on) {
+            cudaStreamSynchronize(c->stream);
+            fprintf(stderr, "[edfa phase] %-28s %9.3f ms\n", name, now() - t0);
         }
     }
 };

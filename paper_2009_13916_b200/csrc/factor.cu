@@ -379,8 +379,12 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         check_launch("k_diag_scale");
     }
     Csr Lpart;
-    select_part(c, S, 0, 1.0, false, Lpart);
-    build_plan(c, Lpart, nullptr, true, false, f.fwd, /*allow_chain=*/false);
+    {
+        PhaseTimer pt(c, "ilu0.level_plan");
+        select_part(c, S, 0, 1.0, false, Lpart);
+        build_plan(c, Lpart, nullptr, true, false, f.fwd, /*allow_chain=*/false);
+    }
+    PhaseTimer pt_fact(c, "ilu0.factor+plans");
     int maxr = n ? max_row_nnz(c, S) : 0;
     require(maxr <= 1024, EDFA_ERR_UNSUPPORTED, "Schur rows longer than 1024 entries are not supported");
     int* flags = c->d_scalar_i + 24;

@@ -89,17 +89,27 @@ void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynam
     }
     in.pre_tau = filt == EDFA_FILT_PRE ? tau : 0.0;
     SetupOutput out;
-    setup_rows(c, in, out);
+    {
+        PhaseTimer pt(c, "stage1.setup_rows");
+        setup_rows(c, in, out);
+    }
     s1->max_pattern = out.max_pattern;
     const int32_t* qsz = dyn ? out.qsize.p : nullptr;
     const int32_t* qidx = dyn ? out.q.p : pattern->idx.p;
-    compact_rows(c, nc, out.slot_ptr, qsz, qidx, out.g.p, out.gcnt, nf, s1->G);
-    compact_rows(c, nc, out.slot_ptr, qsz, qidx, out.f.p, out.fcnt, nf, s1->FT);
-    if (dyn) pattern_compact(c, nc, out.slot_ptr, out.qsize, out.q, nf, s1->Q);
-    else copy_csr(c, *pattern, s1->Q);
-    transpose(c, s1->FT, s1->F);
-    s1->have_F = true;
-    triple_product(c, s1->G, Aff, s1->F, filt == EDFA_FILT_POST_PRODUCT ? tau : 0.0, s1->H);
+    {
+        PhaseTimer pt(c, "stage1.compact+transpose");
+        compact_rows(c, nc, out.slot_ptr, qsz, qidx, out.g.p, out.gcnt, nf, s1->G);
+        compact_rows(c, nc, out.slot_ptr, qsz, qidx, out.f.p, out.fcnt, nf, s1->FT);
+        if (dyn) pattern_compact(c, nc, out.slot_ptr, out.qsize, out.q, nf, s1->Q);
+        else copy_csr(c, *pattern, s1->Q);
+        transpose(c, s1->FT, s1->F);
+        s1->have_F = true;
+    }
+    {
+        PhaseTimer pt(c, "stage1.product");
+        triple_product(c, s1->G, Aff, s1->F, filt == EDFA_FILT_POST_PRODUCT ? tau : 0.0, s1->H);
+    }
+    PhaseTimer pt(c, "stage1.ic0");
     ic0_factor(c, Aff, face_drop_tol, s1->ic);
 }
 
@@ -111,7 +121,11 @@ void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, in
     require(no_fill, EDFA_ERR_UNSUPPORTED,
             "inner factorisations with fill-in (no_fill=False) are not implemented on the GPU path; "
             "pass no_fill=True for IC(0)/ILU(0)");
-    csr_sub(c, A_cc, s1->H, filt == EDFA_FILT_POST_SCHUR ? tau : 0.0, s2->S);
+    {
+        PhaseTimer pt(c, "stage2.schur_sub");
+        csr_sub(c, A_cc, s1->H, filt == EDFA_FILT_POST_SCHUR ? tau : 0.0, s2->S);
+    }
+    PhaseTimer pt(c, "stage2.ilu0_total");
     const int* dims = (int64_t)s1->dims[0] * s1->dims[1] * s1->dims[2] == A_cc.n_rows && s1->dims[0] > 0
                           ? s1->dims : nullptr;
     ilu0_factor(c, s2->S, schur_drop_tol, s2->ilu, dims);

@@ -47,6 +47,9 @@ struct ChainPlan {              // disjoint-path DAGs (chain.cu)
     DevBuf<int32_t> rows;       // SELL-32 over chains: row of step k of chain t
     DevBuf<double> coef, dinv;  // dependency coefficient / inverse diagonal per step
     DevBuf<int32_t> heads, succ;
+    DevBuf<int64_t> cptr;       // chain-major layout for the warp-scan solver
+    DevBuf<int32_t> crow;
+    DevBuf<double> ccoef, cdinv;
 };
 bool build_chain(Ctx* c, const Csr& deps, const double* diag, bool unit, ChainPlan& cp);
 void chain_values(Ctx* c, const Csr& deps, const double* diag, ChainPlan& cp);
@@ -57,18 +60,17 @@ void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, 
 
 struct TilePlan {               // tile-DAG solves of cell-indexed factors (tile.cu)
     int32_t n = 0, n_tiles = 0, n_tile_levels = 0;
-    int32_t RC = 0, KD = 0, EC = 0;
+    int32_t RC = 0, KD = 0, EC = 0, LC = 0;   // rows / early deps / externals / levels per tile
     int64_t n_dep = 0;
     bool unit = false;
-    DevBuf<int32_t> hdr, row_id, ext_id, dptr, dsrc, up_cnt, up_ids, flags, ticket, order;
-    DevBuf<short> lev_ptr, dslot;
-    DevBuf<double> dcoef, dinv;
+    DevBuf<int32_t> hdr, row_id, ext_id, up_cnt, up_ids, flags, ticket, order;
+    DevBuf<short> lev_ptr, dslot, eslot;     // critical / early dependency slots
+    DevBuf<double> dcoef, ecoef, dinv;       // critical / early coefficients
     int32_t epoch = 0, ticket_base = 0;
 };
 // dims = {nx, ny, nz} of the cell grid (rows = cells in natural order) or NULL
 bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
                      TilePlan& tp);
-void tile_values(Ctx* c, const Csr& D, const double* diag, TilePlan& tp);
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name);
 

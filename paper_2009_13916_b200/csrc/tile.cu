@@ -8,14 +8,21 @@
 // DAG of depth ~ NX+NY+NZ instead of the row DAG's nx+ny+nz.
 //
 // One persistent CTA per SM takes tiles in tile-level order from a ticket:
-//   1. stage the tile's coefficients (slots, values, 1/diag, level bounds)
-//      from HBM into shared memory -- independent of the solve, so it runs
-//      before the upstream wait;
-//   2. wait for the upstream tiles' epoch flags (one poller per upstream);
-//   3. gather the external dependencies of the tile into shared memory;
-//   4. sweep the tile's local levels with __syncthreads between them, reading
-//      every dependency from shared memory;
-//   5. write the tile's solution to HBM and publish the tile's flag.
+//   1. stage the tile's plan (TMA bulk copies into shared memory) -- the plan
+//      is constant, so this overlaps the wait for upstream tiles;
+//   2. gather the tile's right-hand side, wait for the upstream tiles' epoch
+//      flags (one poller per upstream), gather the external dependencies;
+//   3. sweep the local levels.  The sweep is software-pipelined in two roles:
+//      "critical" lanes finish level k using only the dependencies on level
+//      k-1; "early" lanes fold every other dependency (earlier levels and
+//      externals, already final) of level k+1 into its partial sums.  Every
+//      lane's plan record for its next step is prefetched into registers, so
+//      a step's critical path is one shared-memory gather, a short FMA chain
+//      and a barrier;
+//   4. write the tile's solution to HBM and publish the tile's flag.
+//
+// Plan records are stored per level, column-major ([dep k][row r]) so the
+// lanes of a step read consecutive addresses.
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -30,6 +37,11 @@
 namespace edfa {
 namespace {
 
+constexpr int ROLE = 64;            // rows per level handled in one step
+constexpr int TILE_THREADS = 3 * ROLE;   // 2 warps critical (lane per row) + 4 warps early (2 lanes per row)
+constexpr int CK = 4;               // critical dependencies per row (axial stencils: <= 3)
+constexpr int EKMAX = 32;           // early dependencies per row
+
 struct Geo {
     int nx, ny, nz, tx, ty, tz, NX, NY, NZ;
     __host__ __device__ int tile_of(int e) const {
@@ -41,67 +53,68 @@ struct Geo {
         int ax = min(tx, nx - I * tx), ay = min(ty, ny - J * ty), az = min(tz, nz - K * tz);
         return ax * ay * az;
     }
-    // r-th cell (natural order inside the tile box) of tile t
     __host__ __device__ int tile_cell(int t, int r) const {
         int I = t % NX, J = (t / NX) % NY, K = t / (NX * NY);
         int ax = min(tx, nx - I * tx), ay = min(ty, ny - J * ty);
         int li = r % ax, lj = (r / ax) % ay, lk = r / (ax * ay);
         return (I * tx + li) + nx * ((J * ty + lj) + ny * (K * tz + lk));
     }
+    // box-local index of global cell j (j must lie in tile t)
+    __host__ __device__ int local_of(int t, int j) const {
+        int I = t % NX, J = (t / NX) % NY, K = t / (NX * NY);
+        int ax = min(tx, nx - I * tx), ay = min(ty, ny - J * ty);
+        int ji = j % nx - I * tx, jj = (j / nx) % ny - J * ty, jk = j / (nx * ny) - K * tz;
+        return ji + ax * (jj + ay * jk);
+    }
 };
 
-// every external dependency must lie in a tile before (forward) / after
-// (backward) the row's tile in natural tile order
 __global__ void k_tile_check(CsrV D, Geo g, bool reverse, int* __restrict__ bad, int* __restrict__ maxdeps) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= D.n_rows) return;
     int t = g.tile_of(i);
-    int len = D.ptr[i + 1] - D.ptr[i];
-    atomicMax(maxdeps, len);
+    atomicMax(maxdeps, D.ptr[i + 1] - D.ptr[i]);
     for (int e = D.ptr[i]; e < D.ptr[i + 1]; ++e) {
         int u = g.tile_of(D.idx[e]);
         if (reverse ? u < t : u > t) atomicExch(bad, 1);
     }
 }
 
-// Per-tile analysis: local levels, sort by level, external list, slot-mapped
-// dependencies.  One CTA per tile; fixed per-tile capacities:
-//   rows <= RC, deps <= RC*KD, externals <= EC.
 struct TileBuild {
     CsrV D;
     Geo g;
-    bool reverse;
-    int RC, KD, EC;
-    const double* diag;   // may be NULL (unit or values later)
+    int RC, EK, EC, LC;   // row / early-dep / external / level capacities per tile
+    const double* diag;   // may be NULL (unit)
     bool unit;
-    // outputs, tile-major with the fixed capacities
-    int* hdr;             // [n_rows, n_ext, n_lev, n_dep] per tile
-    short* lev_ptr;       // RC+1 per tile
+    int* hdr;             // [n_rows, n_ext, n_lev, 0] per tile
+    short* lev_ptr;       // LC per tile
     int* row_id;          // RC per tile (sorted by local level)
     int* ext_id;          // EC per tile
-    int* dptr;            // RC+1 per tile (local dep offsets)
-    short* dslot;         // RC*KD per tile
-    int* dsrc;            // RC*KD per tile: global CSR position of the dep (for value reloads)
-    double* dcoef;        // RC*KD per tile
+    short* cs;            // RC*CK per tile: critical dep slots, [lev_ptr*CK + k*R + r]
+    double* cc;           // RC*CK
+    short* es;            // RC*EK per tile: early dep slots, [lev_ptr*EK + k*R + r]
+    double* ec;           // RC*EK
     double* dinv;         // RC per tile
-    int* up_cnt;          // upstream tiles per tile (<= 26)
+    int* up_cnt;
     int* up_ids;          // 32 per tile
     int* err;
 };
 
-__global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
+__global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int t = blockIdx.x;
     const Geo& g = b.g;
     const int n = g.tile_rows(t);
-    int* cell = reinterpret_cast<int*>(sm);           // RC: tile row r -> global row (box order)
+    int* cell = reinterpret_cast<int*>(sm);           // RC
     int* lev = cell + b.RC;                           // RC
-    int* order = lev + b.RC;                          // RC: sorted position -> r
-    int* pos = order + b.RC;                          // RC: r -> sorted position
-    int* cnt = pos + b.RC;                            // RC+2 (level histogram)
+    int* order = lev + b.RC;                          // RC: sorted position -> box index
+    int* pos = order + b.RC;                          // RC: box index -> sorted position
+    int* cnt = pos + b.RC;                            // RC+2
     int* ext = cnt + b.RC + 2;                        // EC
     int* misc = ext + b.EC;                           // 8
+    int* hs = misc + 8;                               // HS
+    __shared__ int ups[32];
     if (threadIdx.x < 8) misc[threadIdx.x] = 0;
+    if (threadIdx.x < 32) ups[threadIdx.x] = -1;
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
         cell[r] = g.tile_cell(t, r);
         lev[r] = 0;
@@ -111,49 +124,40 @@ __global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
     for (int it = 0; it < b.RC + 1; ++it) {
         int changed = 0;
         for (int r = threadIdx.x; r < n; r += blockDim.x) {
-            int e0 = b.D.ptr[cell[r]], e1 = b.D.ptr[cell[r] + 1];
             int lv = 0;
-            for (int e = e0; e < e1; ++e) {
+            for (int e = b.D.ptr[cell[r]]; e < b.D.ptr[cell[r] + 1]; ++e) {
                 int j = b.D.idx[e];
-                if (g.tile_of(j) != t) continue;
-                // local index of j inside the box
-                int ji = j % g.nx - (t % g.NX) * g.tx;
-                int jj = (j / g.nx) % g.ny - ((t / g.NX) % g.NY) * g.ty;
-                int jk = j / (g.nx * g.ny) - (t / (g.NX * g.NY)) * g.tz;
-                int ax = min(g.tx, g.nx - (t % g.NX) * g.tx), ay = min(g.ty, g.ny - ((t / g.NX) % g.NY) * g.ty);
-                int rj = ji + ax * (jj + ay * jk);
-                lv = max(lv, lev[rj] + 1);
+                if (g.tile_of(j) == t) lv = max(lv, lev[g.local_of(t, j)] + 1);
             }
             if (lv != lev[r]) { lev[r] = lv; changed = 1; }
         }
-        changed = __syncthreads_or(changed);
-        if (!changed) break;
+        if (!__syncthreads_or(changed)) break;
     }
-    // counting sort by level (stable in box order)
     for (int l = threadIdx.x; l < b.RC + 2; l += blockDim.x) cnt[l] = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < n; r += blockDim.x) atomicMax(&misc[0], lev[r] + 1);
     __syncthreads();
-    int nlev = misc[0];
+    const int nlev = misc[0];
     if (threadIdx.x == 0) {
+        if (nlev + 1 > b.LC) atomicExch(b.err, 8);
         for (int r = 0; r < n; ++r) cnt[lev[r] + 1]++;
         for (int l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
-        short* lp = b.lev_ptr + (size_t)t * ((b.RC + 8) & ~7);
-        for (int l = 0; l <= nlev; ++l) lp[l] = (short)cnt[l];
+        short* lp = b.lev_ptr + (size_t)t * b.LC;
+        for (int l = 0; l <= nlev && l < b.LC; ++l) lp[l] = (short)cnt[l];
+        for (int l = 0; l < nlev; ++l)
+            if (cnt[l + 1] - cnt[l] > ROLE) atomicExch(b.err, 9);   // level wider than a role
         for (int r = 0; r < n; ++r) {
             int p = cnt[lev[r]]++;
             order[p] = r;
             pos[r] = p;
         }
+        // cnt[l] now holds the END of level l; rebuild starts in cnt via lp
+        for (int l = 0; l <= nlev && l < b.LC; ++l) cnt[l] = lp[l];
     }
-    __syncthreads();
-    // external dependency set: hash-set insert, compact, bitonic sort
-    int* hs = misc + 8;                 // HS = power of two >= 2*EC
+    // external dependency set: hash insert, compact, bitonic sort
     int HS = 1;
     while (HS < 2 * b.EC) HS <<= 1;
     for (int q = threadIdx.x; q < HS; q += blockDim.x) hs[q] = -1;
-    __shared__ int ups[32];
-    if (threadIdx.x < 32) ups[threadIdx.x] = -1;
     __syncthreads();
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
         int row = cell[r];
@@ -181,7 +185,6 @@ __global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
     const int ne = min(misc[1], b.EC);
     int np2 = 1;
     while (np2 < ne) np2 <<= 1;
-    // bitonic sort of ext[0, np2) (pad with INT_MAX; np2 <= EC rounded up fits in hs)
     int* srt = hs;
     for (int q = threadIdx.x; q < np2; q += blockDim.x) srt[q] = q < ne ? ext[q] : INT32_MAX;
     __syncthreads();
@@ -198,7 +201,6 @@ __global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
         }
     for (int q = threadIdx.x; q < ne; q += blockDim.x) ext[q] = srt[q];
     __syncthreads();
-    // upstream tiles (unique, <= 32)
     for (int q = threadIdx.x; q < ne; q += blockDim.x) {
         int u = g.tile_of(ext[q]);
         for (int z = 0; z < 32; ++z) {
@@ -216,34 +218,27 @@ __global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
         b.up_cnt[t] = nu;
     }
     for (int q = threadIdx.x; q < ne; q += blockDim.x) b.ext_id[(size_t)t * b.EC + q] = ext[q];
-    // per-row dependency counts -> local offsets (thread 0 scan; n <= RC)
-    int* dp = b.dptr + (size_t)t * ((b.RC + 4) & ~3);
-    if (threadIdx.x == 0) {
-        int acc = 0;
-        for (int p = 0; p < n; ++p) {
-            dp[p] = acc;
-            int row = cell[order[p]];
-            acc += b.D.ptr[row + 1] - b.D.ptr[row];
-        }
-        dp[n] = acc;
-        misc[2] = acc;
-    }
-    __syncthreads();
+    // records: critical deps = rows of the immediately preceding local level
+    const int ZSLOT = b.RC + b.EC;   // a shared-memory x slot that stays 0
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
-        int r = order[p], row = cell[r];
+        const int r = order[p], row = cell[r], lv = lev[r];
+        const int l0 = cnt[lv], R = cnt[lv + 1] - l0, rr = p - l0;
         b.row_id[(size_t)t * b.RC + p] = row;
-        double dv = (b.unit || !b.diag) ? 1.0 : 1.0 / b.diag[row];
-        b.dinv[(size_t)t * b.RC + p] = dv;
-        int o = dp[p];
-        for (int e = b.D.ptr[row]; e < b.D.ptr[row + 1]; ++e, ++o) {
+        b.dinv[(size_t)t * b.RC + p] = (b.unit || !b.diag) ? 1.0 : 1.0 / b.diag[row];
+        int nc = 0, nE = 0;
+        short* csb = b.cs + (size_t)t * b.RC * CK + (size_t)l0 * CK;
+        double* ccb = b.cc + (size_t)t * b.RC * CK + (size_t)l0 * CK;
+        short* esb = b.es + (size_t)t * b.RC * b.EK + (size_t)l0 * b.EK;
+        double* ecb = b.ec + (size_t)t * b.RC * b.EK + (size_t)l0 * b.EK;
+        for (int e = b.D.ptr[row]; e < b.D.ptr[row + 1]; ++e) {
             int j = b.D.idx[e];
+            double v = b.D.val ? b.D.val[e] : 0.0;
             int slot;
+            bool critical = false;
             if (g.tile_of(j) == t) {
-                int ji = j % g.nx - (t % g.NX) * g.tx;
-                int jj = (j / g.nx) % g.ny - ((t / g.NX) % g.NY) * g.ty;
-                int jk = j / (g.nx * g.ny) - (t / (g.NX * g.NY)) * g.tz;
-                int ax = min(g.tx, g.nx - (t % g.NX) * g.tx), ay = min(g.ty, g.ny - ((t / g.NX) % g.NY) * g.ty);
-                slot = pos[ji + ax * (jj + ay * jk)];
+                int rj = g.local_of(t, j);
+                slot = pos[rj];
+                critical = lev[rj] == lv - 1;
             } else {
                 int lo = 0, hi = ne;
                 while (lo < hi) {
@@ -253,53 +248,46 @@ __global__ void __launch_bounds__(512) k_tile_build(TileBuild b) {
                 }
                 slot = b.RC + lo;
             }
-            size_t q = (size_t)t * b.RC * b.KD + o;
-            b.dslot[q] = (short)slot;
-            b.dsrc[q] = e;
-            b.dcoef[q] = b.D.val ? b.D.val[e] : 0.0;
+            if (critical) {
+                if (nc >= CK) { atomicExch(b.err, 10); continue; }
+                csb[nc * R + rr] = (short)slot;
+                ccb[nc * R + rr] = v;
+                ++nc;
+            } else {
+                if (nE >= b.EK) { atomicExch(b.err, 11); continue; }
+                esb[nE * R + rr] = (short)slot;
+                ecb[nE * R + rr] = v;
+                ++nE;
+            }
         }
+        for (; nc < CK; ++nc) { csb[nc * R + rr] = (short)ZSLOT; ccb[nc * R + rr] = 0.0; }
+        for (; nE < b.EK; ++nE) { esb[nE * R + rr] = (short)ZSLOT; ecb[nE * R + rr] = 0.0; }
     }
     if (threadIdx.x == 0) {
         int* h = b.hdr + (size_t)t * 4;
         h[0] = n;
         h[1] = ne;
         h[2] = nlev;
-        h[3] = misc[2];
-    }
-}
-
-// reload coefficients / 1/diag from the CSR positions recorded at build time
-__global__ void k_tile_values(int n_tiles, int RC, int KD, const int* __restrict__ hdr, const int* __restrict__ dsrc,
-                              const double* __restrict__ val, double* __restrict__ dcoef,
-                              const int* __restrict__ row_id, const double* __restrict__ diag, bool unit,
-                              double* __restrict__ dinv) {
-    int t = blockIdx.x;
-    int n = hdr[t * 4], nd = hdr[t * 4 + 3];
-    for (int q = threadIdx.x; q < nd; q += blockDim.x) {
-        size_t o = (size_t)t * RC * KD + q;
-        dcoef[o] = val[dsrc[o]];
-    }
-    for (int p = threadIdx.x; p < n; p += blockDim.x) {
-        size_t o = (size_t)t * RC + p;
-        dinv[o] = (unit || !diag) ? 1.0 : 1.0 / diag[row_id[o]];
+        h[3] = 0;
     }
 }
 
 struct TileSolve {
-    int n_tiles, RC, KD, EC;
-    const int* order;      // ticket -> tile
+    int n_tiles, RC, EK, EC, LC;
+    const int* order;
     const int* hdr;
     const short* lev_ptr;
     const int* row_id;
     const int* ext_id;
-    const int* dptr;
-    const short* dslot;
-    const double* dcoef;
+    const short* cs;
+    const double* cc;
+    const short* es;
+    const double* ec;
     const double* dinv;
     const int* up_cnt;
     const int* up_ids;
-    int* flags;            // per tile: epoch of the last completed solve
-    int* ticket;           // [counter]
+    int* flags;
+    int* ticket;
     int epoch;
     int ticket_base;
     const double* b;
@@ -308,7 +296,7 @@ struct TileSolve {
     const double* add;
     double* out2;
     int* err;
-    long long* dbg;        // optional per-tile phase timestamps (globaltimer ns)
+    long long* dbg;
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -316,26 +304,72 @@ __device__ __forceinline__ long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
-
 __device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned r16(unsigned b) { return (b + 15u) & ~15u; }
-// TMA bulk copy global -> shared, completion signalled on an mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mbar) {
     if (bytes == 0) return;
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mbar)) : "memory");
 }
 
-__global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
+// per-lane step record: the row, its dependencies (slot, coefficient)
+template <int K>
+struct Rec {
+    int p;             // sorted row slot, -1 if the lane is idle in this step
+    short s[K];
+    double c[K];
+    double d;          // 1/diag (critical role)
+};
+
+template <int K>
+__device__ __forceinline__ void rec_load(Rec<K>& rc, const short* lp, int nlev, int lv, int lane, const short* S,
+                                         const double* C, const double* di) {
+    rc.p = -1;
+    if (lv < 0 || lv >= nlev) return;
+    const int l0 = lp[lv], R = lp[lv + 1] - l0;
+    if (lane >= R) return;
+    rc.p = l0 + lane;
+    const short* sb = S + (size_t)l0 * K + lane;
+    const double* cb = C + (size_t)l0 * K + lane;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        rc.s[k] = sb[k * R];
+        rc.c[k] = cb[k * R];
+    }
+    rc.d = di[rc.p];
+}
+
+// early record split over a lane pair: lane li of row r takes deps li, li+2, ...
+template <int KH>
+__device__ __forceinline__ void rec_load_pair(Rec<KH>& rc, const short* lp, int nlev, int lv, int r, int li,
+                                              const short* S, const double* C) {
+    rc.p = -1;
+    if (lv < 0 || lv >= nlev) return;
+    const int l0 = lp[lv], R = lp[lv + 1] - l0;
+    if (r >= R) return;
+    rc.p = l0 + r;
+    const short* sb = S + (size_t)l0 * (2 * KH) + r + li * R;
+    const double* cb = C + (size_t)l0 * (2 * KH) + r + li * R;
+#pragma unroll
+    for (int k = 0; k < KH; ++k) {
+        rc.s[k] = sb[2 * k * R];
+        rc.c[k] = cb[2 * k * R];
+    }
+}
+
+template <int EK>
+__global__ void __launch_bounds__(TILE_THREADS) k_tile_solve(TileSolve a) {
     extern __shared__ __align__(128) unsigned char sm[];
     // 16-byte aligned sections (capacities padded on the host, see tile_smem_bytes)
-    double* xs = reinterpret_cast<double*>(sm);                 // RC + EC
-    double* cf = xs + a.RC + a.EC;                              // RC*KD
-    double* di = cf + (size_t)a.RC * a.KD;                      // RC
-    int* rid = reinterpret_cast<int*>(di + a.RC);               // RC
-    int* dp = rid + a.RC;                                       // DPS = RC+1 rounded to 4
-    short* sl = reinterpret_cast<short*>(dp + ((a.RC + 4) & ~3));   // RC*KD
-    short* lp = sl + (size_t)a.RC * a.KD;                       // LPS = RC+1 rounded to 8
+    double* xs = reinterpret_cast<double*>(sm);                     // RC + EC + 2
+    double* cc = xs + a.RC + a.EC + 2;                              // RC*CK
+    double* ecf = cc + (size_t)a.RC * CK;                           // RC*EK
+    double* di = ecf + (size_t)a.RC * EK;                           // RC
+    int* rid = reinterpret_cast<int*>(di + a.RC);                   // RC
+    int* eid_s = rid + a.RC;                                        // EC (external row ids)
+    short* cs = reinterpret_cast<short*>(eid_s + a.EC);             // RC*CK
+    short* es = cs + (size_t)a.RC * CK;                             // RC*EK
+    short* lp = es + (size_t)a.RC * EK;                             // LC
     __shared__ int s_tile, s_hdr[4];
     __shared__ __align__(8) uint64_t mbar;
     if (threadIdx.x == 0) {
@@ -344,7 +378,10 @@ __global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
     }
     __syncthreads();
     unsigned phase = 0;
-    const int DPS = (a.RC + 4) & ~3, LPS = (a.RC + 8) & ~7;
+    const bool crit = threadIdx.x < ROLE;
+    const int lane = crit ? threadIdx.x : (threadIdx.x - ROLE) >> 1;   // row within the step
+    const int li = (threadIdx.x - ROLE) & 1;                            // early: half of the deps
+    constexpr int KH = EK / 2;
     for (;;) {
         if (threadIdx.x == 0) {
             int k = atomicAdd(a.ticket, 1) - a.ticket_base;
@@ -352,20 +389,23 @@ __global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
             s_tile = t;
             if (t >= 0) {
                 const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
-                s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z; s_hdr[3] = h.w;
-                // 1. stage the tile's plan with TMA bulk copies (independent of
-                //    the solve, overlaps the upstream wait below)
-                unsigned b_cf = r16(8u * h.w), b_sl = r16(2u * h.w), b_dp = r16(4u * (h.x + 1));
-                unsigned b_lp = r16(2u * (h.z + 1)), b_di = r16(8u * h.x), b_ri = r16(4u * h.x);
+                s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z;
+                const unsigned n = h.x;
+                unsigned b_cs = r16(2u * n * CK), b_cc = r16(8u * n * CK), b_es = r16(2u * n * EK),
+                         b_ec = r16(8u * n * EK), b_di = r16(8u * n), b_ri = r16(4u * n), b_lp = r16(2u * (h.z + 1));
+                unsigned b_ei = r16(4u * h.y);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                             ::"r"(smem_addr(&mbar)), "r"(b_cf + b_sl + b_dp + b_lp + b_di + b_ri) : "memory");
-                bulk_g2s(cf, a.dcoef + (size_t)t * a.RC * a.KD, b_cf, &mbar);
-                bulk_g2s(sl, a.dslot + (size_t)t * a.RC * a.KD, b_sl, &mbar);
-                bulk_g2s(dp, a.dptr + (size_t)t * DPS, b_dp, &mbar);
-                bulk_g2s(lp, a.lev_ptr + (size_t)t * LPS, b_lp, &mbar);
+                             ::"r"(smem_addr(&mbar)), "r"(b_cs + b_cc + b_es + b_ec + b_di + b_ri + b_lp + b_ei)
+                             : "memory");
+                bulk_g2s(eid_s, a.ext_id + (size_t)t * a.EC, b_ei, &mbar);
+                bulk_g2s(cs, a.cs + (size_t)t * a.RC * CK, b_cs, &mbar);
+                bulk_g2s(cc, a.cc + (size_t)t * a.RC * CK, b_cc, &mbar);
+                bulk_g2s(es, a.es + (size_t)t * a.RC * EK, b_es, &mbar);
+                bulk_g2s(ecf, a.ec + (size_t)t * a.RC * EK, b_ec, &mbar);
                 bulk_g2s(di, a.dinv + (size_t)t * a.RC, b_di, &mbar);
                 bulk_g2s(rid, a.row_id + (size_t)t * a.RC, b_ri, &mbar);
+                bulk_g2s(lp, a.lev_ptr + (size_t)t * a.LC, b_lp, &mbar);
             }
         }
         __syncthreads();
@@ -373,7 +413,34 @@ __global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
         if (t < 0) break;
         const int n = s_hdr[0], ne = s_hdr[1], nlev = s_hdr[2];
         if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 0] = gtimer();
-        // 2. wait for upstream tiles (relaxed polls: no L1 invalidation per poll)
+        {
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(smem_addr(&mbar)), "r"(phase) : "memory");
+            phase ^= 1u;
+        }
+        // right-hand side into the x slots (independent of upstream tiles)
+        for (int p0 = 0; p0 < n; p0 += 8 * TILE_THREADS) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                int p = p0 + u * TILE_THREADS + threadIdx.x;
+                v[u] = p < n ? __ldg(a.b + rid[p]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                int p = p0 + u * TILE_THREADS + threadIdx.x;
+                if (p < n) xs[p] = a.alpha * v[u];
+            }
+        }
+        if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
+        // first step records (plan constants) before waiting
+        Rec<CK> rcr;
+        Rec<KH> rer;
+        if (crit) rec_load<CK>(rcr, lp, nlev, 0, lane, cs, cc, di);
+        else rec_load_pair<KH>(rer, lp, nlev, 0, lane, li, es, ecf);
+        // wait for upstream tiles (relaxed polls: no L1 invalidation per poll)
         const int nu = a.up_cnt[t];
         if (threadIdx.x < nu) {
             const int* f = a.flags + a.up_ids[(size_t)t * 32 + threadIdx.x];
@@ -385,45 +452,70 @@ __global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
                 if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
             }
             __threadfence();
-            if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
         }
-        // staged plan must have landed
-        {
-            unsigned done = 0;
-            while (!done)
-                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                             : "=r"(done) : "r"(smem_addr(&mbar)), "r"(phase) : "memory");
-            phase ^= 1u;
-        }
-        // rhs into the x slots
-        for (int p = threadIdx.x; p < n; p += blockDim.x) xs[p] = a.alpha * __ldg(a.b + rid[p]);
         __syncthreads();
-        // 3. gather external dependencies
-        for (int q = threadIdx.x; q < ne; q += blockDim.x)
-            xs[a.RC + q] = __ldcg(a.x + a.ext_id[(size_t)t * a.EC + q]);
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
+        {
+            const int* eid = eid_s;
+            for (int q0 = 0; q0 < ne; q0 += 8 * TILE_THREADS) {
+                int id[8];
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    int q = q0 + u * TILE_THREADS + threadIdx.x;
+                    id[u] = q < ne ? eid[q] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = id[u] >= 0 ? __ldcg(a.x + id[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    int q = q0 + u * TILE_THREADS + threadIdx.x;
+                    if (q < ne) xs[a.RC + q] = v[u];
+                }
+            }
+        }
         __syncthreads();
         if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 2] = gtimer();
-        // 4. local levels: G lanes per row (shuffle-reduced), rows of a level
-        //    spread over the CTA
-        constexpr int G = 8;
-        const int grp = threadIdx.x / G, li = threadIdx.x % G, ngrp = blockDim.x / G;
-        for (int l = 0; l < nlev; ++l) {
-            int p1 = lp[l + 1];
-            for (int base = lp[l]; base < p1; base += ngrp) {   // warp-uniform trip count
-                const int p = base + grp;
-                const bool act = p < p1;
-                double acc = 0.0;
-                if (act)
-                    for (int q = dp[p] + li; q < dp[p + 1]; q += G) acc = fma(-cf[q], xs[sl[q]], acc);
+        const long long c_lev0 = clock64();
+        // pipelined level sweep: step k = critical(level k) || early(level k+1)
+        // step -1 only folds the early deps of level 0
+        // early half-sum of a lane pair; lane li == 0 folds it into the partial
+        auto early = [&]() {
+            double a2[2] = {0.0, 0.0};
+            if (rer.p >= 0) {
 #pragma unroll
-                for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
-                if (act && li == 0) xs[p] = (xs[p] + acc) * di[p];
+                for (int u = 0; u < KH; ++u) a2[u & 1] = fma(-rer.c[u], xs[rer.s[u]], a2[u & 1]);
+            }
+            double h = a2[0] + a2[1];
+            h += __shfl_xor_sync(0xffffffffu, h, 1);
+            if (rer.p >= 0 && li == 0) xs[rer.p] += h;
+        };
+        if (!crit) {
+            early();
+            rec_load_pair<KH>(rer, lp, nlev, 1, lane, li, es, ecf);
+        }
+        __syncthreads();
+        for (int k = 0; k < nlev; ++k) {
+            if (crit) {
+                if (rcr.p >= 0) {
+                    double x0 = xs[rcr.s[0]], x1 = xs[rcr.s[1]], x2 = xs[rcr.s[2]], x3 = xs[rcr.s[3]];
+                    double acc = xs[rcr.p];
+                    acc = fma(-rcr.c[0], x0, acc);
+                    acc = fma(-rcr.c[1], x1, acc);
+                    acc = fma(-rcr.c[2], x2, acc);
+                    acc = fma(-rcr.c[3], x3, acc);
+                    xs[rcr.p] = acc * rcr.d;
+                }
+                rec_load<CK>(rcr, lp, nlev, k + 1, lane, cs, cc, di);
+            } else {
+                early();
+                rec_load_pair<KH>(rer, lp, nlev, k + 2, lane, li, es, ecf);
             }
             __syncthreads();
         }
+        const long long c_lev1 = clock64();
         if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 3] = gtimer();
-        // 5. write back, publish
-        for (int p = threadIdx.x; p < n; p += blockDim.x) {
+        for (int p = threadIdx.x; p < n; p += TILE_THREADS) {
             int row = rid[p];
             double v = xs[p];
             __stcg(a.x + row, v);
@@ -433,18 +525,20 @@ __global__ void __launch_bounds__(512) k_tile_solve(TileSolve a) {
         __syncthreads();
         if (threadIdx.x == 0)
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.flags + t), "r"(a.epoch) : "memory");
-        if (a.dbg && threadIdx.x == 0) { a.dbg[t * 6 + 4] = gtimer(); a.dbg[t * 6 + 5] = blockIdx.x; }
+        if (a.dbg && threadIdx.x == 0) {
+            a.dbg[t * 6 + 4] = gtimer();
+            a.dbg[t * 6 + 5] = (c_lev1 - c_lev0) / (nlev + 1);
+        }
     }
 }
 
 }  // namespace
 
-// smem layout of k_tile_solve: xs[RC+EC] cf[RC*KD] di[RC] rid[RC] dp[DPS] sl[RC*KD] lp[LPS]
-// (RC multiple of 8, KD and EC even -> every section starts 16-byte aligned)
+// smem: xs[RC+EC+2] cc[RC*CK] ec[RC*EK] di[RC] rid[RC] cs[RC*CK] es[RC*EK] lp[LC]
 size_t tile_smem_bytes(const TilePlan& tp) {
-    size_t rc = tp.RC, kd = tp.KD, ec = tp.EC;
-    size_t dps = (rc + 4) & ~size_t(3), lps = (rc + 8) & ~size_t(7);
-    size_t bytes = 8 * (rc + ec) + 8 * rc * kd + 8 * rc + 4 * rc + 4 * dps + 2 * rc * kd + 2 * lps;
+    size_t rc = tp.RC, ek = tp.KD, ec = tp.EC, lc = tp.LC;
+    size_t bytes = 8 * (rc + ec + 2) + 8 * rc * CK + 8 * rc * ek + 8 * rc + 4 * rc + 4 * ec + 2 * rc * CK +
+                   2 * rc * ek + 2 * lc;
     return (bytes + 127) & ~size_t(127);
 }
 
@@ -466,26 +560,27 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     int hf[2];
     EDFA_CUDA(cudaMemcpyAsync(hf, fl, sizeof hf, cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    if (hf[0] || hf[1] > 64) return false;
+    if (hf[0] || hf[1] > EKMAX) return false;
     const int nt = g.NX * g.NY * g.NZ;
     tp.n = n;
     tp.n_tiles = nt;
-    tp.RC = (g.tx * g.ty * g.tz + 7) & ~7;           // per-tile capacities / strides
-    tp.KD = (std::max(hf[1], 1) + 1) & ~1;
-    tp.EC = (std::min(tp.RC * tp.KD, 4 * tp.RC + 256) + 1) & ~1;
+    tp.RC = (g.tx * g.ty * g.tz + 7) & ~7;
+    tp.KD = hf[1] <= 4 ? 4 : (hf[1] <= 8 ? 8 : (hf[1] <= 16 ? 16 : 32));   // early-dep capacity EK
+    tp.EC = (std::min(tp.RC * std::max(hf[1], 1), 4 * tp.RC + 256) + 7) & ~7;
+    tp.LC = ((g.tx + g.ty + g.tz) * 4 + 8 + 7) & ~7;    // generous bound on local levels + 1
+    if (tp.LC > tp.RC + 8) tp.LC = tp.RC + 8;
     tp.unit = unit;
     tp.n_dep = D.nnz;
     size_t smem = tile_smem_bytes(tp);
-    if (smem > 200 * 1024) return false;
-    const size_t dps = (tp.RC + 4) & ~3, lps = (tp.RC + 8) & ~7;
+    if (smem > 220 * 1024) return false;
     tp.hdr.reset(c, (size_t)nt * 4);
-    tp.lev_ptr.reset(c, (size_t)nt * lps);
+    tp.lev_ptr.reset(c, (size_t)nt * tp.LC);
     tp.row_id.reset(c, (size_t)nt * tp.RC);
     tp.ext_id.reset(c, (size_t)nt * tp.EC);
-    tp.dptr.reset(c, (size_t)nt * dps);
-    tp.dslot.reset(c, (size_t)nt * tp.RC * tp.KD);
-    tp.dsrc.reset(c, (size_t)nt * tp.RC * tp.KD);
-    tp.dcoef.reset(c, (size_t)nt * tp.RC * tp.KD);
+    tp.dslot.reset(c, (size_t)nt * tp.RC * CK);        // critical slots
+    tp.dcoef.reset(c, (size_t)nt * tp.RC * CK);        // critical coefficients
+    tp.eslot.reset(c, (size_t)nt * tp.RC * tp.KD);
+    tp.ecoef.reset(c, (size_t)nt * tp.RC * tp.KD);
     tp.dinv.reset(c, (size_t)nt * tp.RC);
     tp.up_cnt.reset(c, nt);
     tp.up_ids.reset(c, (size_t)nt * 32);
@@ -495,8 +590,8 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     EDFA_CUDA(cudaMemsetAsync(tp.ticket.p, 0, sizeof(int), c->stream));
     tp.epoch = 0;
     tp.ticket_base = 0;
-    TileBuild b{view(D), g, reverse, tp.RC, tp.KD, tp.EC, diag, unit, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
-                tp.ext_id.p, tp.dptr.p, tp.dslot.p, tp.dsrc.p, tp.dcoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
+    TileBuild b{view(D), g, tp.RC, tp.KD, tp.EC, tp.LC, diag, unit, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
+                tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
                 fl + 2};
     int HS = 1;
     while (HS < 2 * tp.EC) HS <<= 1;
@@ -510,12 +605,12 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     }
     int e = 0;
     EDFA_CUDA(cudaMemcpyAsync(&e, fl + 2, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    // tile schedule: level of the tile DAG (host, tiny), ticket order by (level, id)
     std::vector<int> upc(nt), upi((size_t)nt * 32);
     EDFA_CUDA(cudaMemcpyAsync(upc.data(), tp.up_cnt.p, sizeof(int) * nt, cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaMemcpyAsync(upi.data(), tp.up_ids.p, sizeof(int) * nt * 32, cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaStreamSynchronize(c->stream));
     if (e) return false;
+    // tile schedule: level of the tile DAG (host, tiny), ticket order by (level, id)
     std::vector<int> lvl(nt, 0), ord(nt);
     if (!reverse) {
         for (int t = 0; t < nt; ++t)
@@ -530,38 +625,45 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     tp.order.reset(c, nt);
     EDFA_CUDA(cudaMemcpyAsync(tp.order.p, ord.data(), sizeof(int) * nt, cudaMemcpyHostToDevice, c->stream));
     EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    if (smem > 48 * 1024)
-        EDFA_CUDA(cudaFuncSetAttribute(k_tile_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     return true;
 }
 
-void tile_values(Ctx* c, const Csr& D, const double* diag, TilePlan& tp) {
-    Prof pr(c, "tile_plan", 20.0 * D.nnz);
-    k_tile_values<<<tp.n_tiles, 256, 0, c->stream>>>(tp.n_tiles, tp.RC, tp.KD, tp.hdr.p, tp.dsrc.p, D.val.p,
-                                                     tp.dcoef.p, tp.row_id.p, diag, tp.unit, tp.dinv.p);
-    check_launch("k_tile_values");
+template <int EK>
+static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
+    auto kern = k_tile_solve<EK>;
+    EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TILE_THREADS, smem));
+    int grid = NUM_SMS_B200 * std::max(1, std::min(occ, 2));
+    a.ticket_base = tp.ticket_base;
+    tp.ticket_base += tp.n_tiles + grid;   // every CTA takes exactly one failing ticket
+    void* args[] = {&a};
+    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(TILE_THREADS), args, smem, c->stream));
 }
 
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name) {
     size_t smem = tile_smem_bytes(tp);
-    int occ = 0;
-    EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_solve, 256, smem));
-    int grid = NUM_SMS_B200 * std::max(1, std::min(occ, 2));
-    tp.epoch += 1;
-    TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p, tp.ext_id.p,
-                tp.dptr.p, tp.dslot.p, tp.dcoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p, tp.flags.p, tp.ticket.p,
-                tp.epoch, tp.ticket_base, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr};
+    // EDFA_TILE_NOWAIT (profiling only): every upstream flag already matches,
+    // so tiles run without waiting -- isolates per-tile processing cost
+    static const bool nowait = getenv("EDFA_TILE_NOWAIT") != nullptr;
+    if (!nowait) tp.epoch += 1;
+    TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.LC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
+                tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
+                tp.flags.p, tp.ticket.p, tp.epoch, 0, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr};
     static const char* dbg_path = getenv("EDFA_TILE_DEBUG");
     DevBuf<long long> dbg;
     if (dbg_path) {
         dbg.reset(c, (size_t)tp.n_tiles * 6);
         a.dbg = dbg.p;
     }
-    tp.ticket_base += tp.n_tiles + grid;   // every CTA takes exactly one failing ticket
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
-    void* args[] = {&a};
-    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)k_tile_solve, dim3(grid), dim3(256), args, smem, c->stream));
+    switch (tp.KD) {
+        case 4: launch_tile<4>(c, tp, a, smem); break;
+        case 8: launch_tile<8>(c, tp, a, smem); break;
+        case 16: launch_tile<16>(c, tp, a, smem); break;
+        default: launch_tile<32>(c, tp, a, smem); break;
+    }
     if (dbg_path) {
         std::vector<long long> h((size_t)tp.n_tiles * 6);
         EDFA_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
