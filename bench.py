@@ -219,17 +219,35 @@ def run_edfa(args):
                        max_it=case.max_it)
         return x, rep, pre
 
-    # patterns_for on a DeviceSystem needs the host grid/face_index
-    for _ in range(args.warmup):
+    import ctypes
+
+    def report(c, reset=1):
+        n = lib.edfa_ctx_profile_report(c, None, 0, 0)
+        buf = ctypes.create_string_buffer(int(n))
+        lib.edfa_ctx_profile_report(c, buf, n, reset)
+        return json.loads(buf.value.decode())
+
+    c = ctx()
+    for w in range(args.warmup):
+        last = w == args.warmup - 1
+        if last:   # full per-kernel event profile of one (untimed) step: shares + dominant kernel
+            lib.edfa_ctx_profile_filter(c, b"")
+            lib.edfa_ctx_profile(c, 1)
+            report(c)
         x, rep, pre = step(ds, b_dev)
+        if last:
+            prof_full = report(c)
+            lib.edfa_ctx_profile(c, 0)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
+    dom_name = max(prof_full.items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
 
-    # ---- device-resident timed region
-    c = ctx()
+    # ---- device-resident timed region; CUDA events bracket every launch of
+    # the dominant kernel only (cheap enough not to perturb the step)
+    lib.edfa_ctx_profile_filter(c, dom_name.encode())
     lib.edfa_ctx_profile(c, 1)
-    lib.edfa_ctx_profile_report(c, None, 0, 1)
+    report(c)
     launches0 = lib.edfa_ctx_launch_count(c)
     times = []
     reps = []
@@ -245,12 +263,9 @@ def run_edfa(args):
             times.append(e0.elapsed_time(e1))
             reps.append(rep)
     launches = lib.edfa_ctx_launch_count(c) - launches0
-    buf_len = lib.edfa_ctx_profile_report(c, None, 0, 0)
-    import ctypes
-    buf = ctypes.create_string_buffer(int(buf_len))
-    lib.edfa_ctx_profile_report(c, buf, buf_len, 1)
+    prof = report(c)
     lib.edfa_ctx_profile(c, 0)
-    prof = json.loads(buf.value.decode())
+    lib.edfa_ctx_profile_filter(c, b"")
     clocks = clk.summary()
     t_total_ms = sum(times)
     if world > 1:
@@ -299,8 +314,9 @@ def run_edfa(args):
     except Exception:
         pass
     step_ms = t_total_ms / args.steps
-    shares = {k: round(v["ms"] / max(sum(p["ms"] for p in prof.values()), 1e-9), 4) for k, v in
-              sorted(prof.items(), key=lambda kv: -kv[1]["ms"])[:8]}
+    tot_full = max(sum(p["ms"] for p in prof_full.values()), 1e-9)
+    shares = {k: round(v["ms"] / tot_full, 4) for k, v in sorted(prof_full.items(), key=lambda kv: -kv[1]["ms"])[:8]}
+    kernel_ms_per_step = tot_full
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -319,11 +335,14 @@ def run_edfa(args):
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
-                     "launches_per_step": d["launches"] / args.steps, "step_share": shares},
+                     "launches_per_step": d["launches"] / args.steps,
+                     "step_share_of_kernel_time": shares, "kernel_ms_per_step": kernel_ms_per_step,
+                     "shares_from": "per-kernel CUDA events of the last warm-up step (same workload)"},
         "clocks": clocks,
     }
     if args.profile_json and rank == 0:
-        pathlib.Path(args.profile_json).write_text(json.dumps(prof, indent=1))
+        pathlib.Path(args.profile_json).write_text(json.dumps({"timed_region": prof, "warmup_step": prof_full},
+                                                              indent=1))
     if rank == 0 and not args.no_cpu_baseline:
         cb = cpu_baseline(args.n, reps[-1].n_it)
         v = extrapolate(cb, N, reps[-1].n_it)

@@ -117,6 +117,8 @@ int edfa_ctx_sync(edfa_ctx* ctx);
 int edfa_ctx_destroy(edfa_ctx* ctx);
 /* Per-kernel CUDA-event timing with algorithmic byte counts (roofline). */
 int edfa_ctx_profile(edfa_ctx* ctx, int enable);
+/* Restrict event timing to kernels whose name starts with prefix ("" = all). */
+int edfa_ctx_profile_filter(edfa_ctx* ctx, const char* prefix);
 /* JSON {"kernel": {"launches": n, "ms": t, "bytes": b}, ...}; returns needed length. */
 int64_t edfa_ctx_profile_report(edfa_ctx* ctx, char* buf, int64_t cap, int reset);
 /* Number of library kernel launches issued so far on this context. */

@@ -54,6 +54,7 @@ _SIGS = {
     "edfa_ctx_sync": (i32, [vp]),
     "edfa_ctx_destroy": (i32, [vp]),
     "edfa_ctx_profile": (i32, [vp, i32]),
+    "edfa_ctx_profile_filter": (i32, [vp, C.c_char_p]),
     "edfa_ctx_profile_report": (i64, [vp, C.c_char_p, i64, i32]),
     "edfa_ctx_launch_count": (i64, [vp]),
     "edfa_csr_create": (i32, [vp, i32, i32, i64, vp, vp, vp, i32, C.POINTER(vp)]),

@@ -138,6 +138,13 @@ int edfa_ctx_profile(edfa_ctx* ctx, int enable) {
     API_END
 }
 
+int edfa_ctx_profile_filter(edfa_ctx* ctx, const char* prefix) {
+    API_BEGIN
+    ctx->c.flush_profile();
+    ctx->c.prof_prefix = prefix ? prefix : "";
+    API_END
+}
+
 int64_t edfa_ctx_profile_report(edfa_ctx* ctx, char* buf, int64_t cap, int reset) {
     try {
         ctx->c.flush_profile();

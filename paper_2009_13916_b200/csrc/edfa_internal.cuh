@@ -6,6 +6,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <ctime>
 #include <stdexcept>
 #include <string>
@@ -44,6 +45,7 @@ struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     int profiling = 0;
+    std::string prof_prefix;   // only kernels whose name starts with it are timed
     int64_t launches = 0;
     std::vector<ProfRec> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -98,15 +100,17 @@ struct Prof {
     const char* name;
     double bytes;
     cudaEvent_t e0 = nullptr;
+    bool on = false;
     Prof(Ctx* ctx, const char* nm, double b) : c(ctx), name(nm), bytes(b) {
         c->launches++;
-        if (c->profiling) {
+        on = c->profiling && (c->prof_prefix.empty() || strncmp(nm, c->prof_prefix.c_str(), c->prof_prefix.size()) == 0);
+        if (on) {
             e0 = c->get_event();
             cudaEventRecord(e0, c->stream);
         }
     }
     ~Prof() {
-        if (c->profiling) {
+        if (on) {
             cudaEvent_t e1 = c->get_event();
             cudaEventRecord(e1, c->stream);
             c->pending.push_back({name, e0, e1, bytes});

@@ -97,6 +97,8 @@ struct TileBuild {
     int* up_cnt;
     int* up_ids;          // 32 per tile
     int* err;
+    int* max_early;       // count-only pass: max early deps of a row (sizes EK)
+    bool count_only;
 };
 
 __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
@@ -132,6 +134,18 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
             if (lv != lev[r]) { lev[r] = lv; changed = 1; }
         }
         if (!__syncthreads_or(changed)) break;
+    }
+    if (b.count_only) {   // early deps = all but the intra-tile ones on the previous level
+        for (int r = threadIdx.x; r < n; r += blockDim.x) {
+            int ne_r = 0;
+            for (int e = b.D.ptr[cell[r]]; e < b.D.ptr[cell[r] + 1]; ++e) {
+                int j = b.D.idx[e];
+                bool critical = g.tile_of(j) == t && lev[g.local_of(t, j)] == lev[r] - 1;
+                ne_r += !critical;
+            }
+            atomicMax(b.max_early, ne_r);
+        }
+        return;
     }
     for (int l = threadIdx.x; l < b.RC + 2; l += blockDim.x) cnt[l] = 0;
     __syncthreads();
@@ -565,12 +579,41 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     tp.n = n;
     tp.n_tiles = nt;
     tp.RC = (g.tx * g.ty * g.tz + 7) & ~7;
-    tp.KD = hf[1] <= 4 ? 4 : (hf[1] <= 8 ? 8 : (hf[1] <= 16 ? 16 : 32));   // early-dep capacity EK
     tp.EC = (std::min(tp.RC * std::max(hf[1], 1), 4 * tp.RC + 256) + 7) & ~7;
     tp.LC = ((g.tx + g.ty + g.tz) * 4 + 8 + 7) & ~7;    // generous bound on local levels + 1
     if (tp.LC > tp.RC + 8) tp.LC = tp.RC + 8;
     tp.unit = unit;
     tp.n_dep = D.nnz;
+    int HS = 1;
+    while (HS < 2 * tp.EC) HS <<= 1;
+    size_t bsm = sizeof(int) * (5 * tp.RC + 2 + tp.EC + 8 + HS);
+    if (bsm > 48 * 1024)
+        EDFA_CUDA(cudaFuncSetAttribute(k_tile_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
+    {
+        // count pass: the early-dependency capacity EK is the exact maximum
+        // (rounded to the instantiated widths) so no padded work is staged
+        TileBuild cb{};
+        cb.D = view(D);
+        cb.g = g;
+        cb.RC = tp.RC;
+        cb.EC = tp.EC;
+        cb.LC = tp.LC;
+        cb.max_early = fl + 3;
+        cb.err = fl + 2;
+        cb.count_only = true;
+        EDFA_CUDA(cudaMemsetAsync(fl + 3, 0, sizeof(int), c->stream));
+        Prof pr(c, "tile_plan", 8.0 * D.nnz);
+        k_tile_build<<<nt, 256, bsm, c->stream>>>(cb);
+        check_launch("k_tile_build count");
+        int me = 0;
+        EDFA_CUDA(cudaMemcpyAsync(&me, fl + 3, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        const int widths[] = {4, 8, 12, 16, 24, 32};
+        tp.KD = 0;
+        for (int w : widths)
+            if (me <= w) { tp.KD = w; break; }
+        if (!tp.KD) return false;
+    }
     size_t smem = tile_smem_bytes(tp);
     if (smem > 220 * 1024) return false;
     tp.hdr.reset(c, (size_t)nt * 4);
@@ -592,14 +635,9 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     tp.ticket_base = 0;
     TileBuild b{view(D), g, tp.RC, tp.KD, tp.EC, tp.LC, diag, unit, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
-                fl + 2};
-    int HS = 1;
-    while (HS < 2 * tp.EC) HS <<= 1;
-    size_t bsm = sizeof(int) * (5 * tp.RC + 2 + tp.EC + 8 + HS);
+                fl + 2, fl + 3, false};
     {
         Prof pr(c, "tile_plan", 24.0 * D.nnz);
-        if (bsm > 48 * 1024)
-            EDFA_CUDA(cudaFuncSetAttribute(k_tile_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
         k_tile_build<<<nt, 256, bsm, c->stream>>>(b);
         check_launch("k_tile_build");
     }
@@ -661,7 +699,9 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
     switch (tp.KD) {
         case 4: launch_tile<4>(c, tp, a, smem); break;
         case 8: launch_tile<8>(c, tp, a, smem); break;
+        case 12: launch_tile<12>(c, tp, a, smem); break;
         case 16: launch_tile<16>(c, tp, a, smem); break;
+        case 24: launch_tile<24>(c, tp, a, smem); break;
         default: launch_tile<32>(c, tp, a, smem); break;
     }
     if (dbg_path) {
