@@ -10,7 +10,13 @@ this container).  ``value`` = N_dof * steps / device time with the blocks
 resident in HBM; ``e2e`` = the same through the drop-in API from host scipy
 blocks (H2D of the blocks and rhs, D2H of x inside the timed region).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl edfa|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl edfa|reference] [--slabs P]
+
+N = 1: the single-device solver on config 2.  N > 1 (torchrun, one process
+per GPU): weak scaling over z-slabs -- an n x n x (n N) grid of the config-2
+generator, one n^3 slab per GPU, block-Jacobi inner factors per slab, halo
+exchange and Krylov allreduces over NCCL (parallel.py).  ``--slabs P`` on one
+GPU runs P slabs in one process (the same per-slab device work, local halos).
 
 ``--impl reference`` times the CPU restatement of the reference algorithm
 (oracle/, the reference is pure Python and cannot travel to the GPU box) on a
@@ -47,6 +53,9 @@ def parse():
     ap.add_argument("--n", type=int, default=64, help="grid cells per side (config 2 is 64)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None, help="write the per-kernel event profile here")
+    ap.add_argument("--slabs", type=int, default=0,
+                    help="z-slab partitioned solver with this many slabs per process (default: 1 slab per "
+                         "GPU when N > 1, the single-device solver when N = 1)")
     return ap.parse_args()
 
 
@@ -354,10 +363,183 @@ def run_edfa(args):
         torch.distributed.destroy_process_group()
 
 
+# ---------------------------------------------------------------- slab-partitioned arm (N > 1)
+def run_slabs(args):
+    """Weak scaling over z-slabs (BASELINE config 5 method):
+    the global grid is n x n x (n * slabs), one n^3 slab per GPU, block-Jacobi
+    inner factors per slab, halo exchange + allreduce over NCCL."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    per_proc = max(args.slabs, 1)
+    parts = world * per_proc
+    from paper_2009_13916_b200 import _lib, configs, parallel
+    from paper_2009_13916_b200.device import ctx
+    lib = _lib.lib()
+    case = configs.config2(n=args.n, nz=args.n * parts)
+    s = case.system
+    N = s.n_unknowns
+    mine = [rank * per_proc + k for k in range(per_proc)]
+    halo = parallel.halo_layers("static", "A")
+    lays = parallel.build_layouts(s, parts, halo=halo, ranks=mine)
+    comm = (parallel.TorchComm([q // per_proc for q in range(parts)]) if world > 1
+            else parallel.LocalComm(parts))
+    my_lays = [lays[q] for q in mine]
+    solver = parallel.SlabSolver(my_lays, comm, kind="static", prototype="A")
+    if world > 1:
+        t = torch.zeros(1, device=dev)
+        torch.distributed.all_reduce(t)                # communicator up before the first P2P
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        solver.build()
+        return solver.solve(tol=case.rtol, restart=case.restart, max_it=case.max_it)
+
+    def report(c, reset=1):
+        n = lib.edfa_ctx_profile_report(c, None, 0, 0)
+        buf = ctypes.create_string_buffer(int(n))
+        lib.edfa_ctx_profile_report(c, buf, n, reset)
+        return json.loads(buf.value.decode())
+
+    c = ctx()
+    prof_full = {}
+    for w in range(args.warmup):
+        last = w == args.warmup - 1
+        if last:
+            lib.edfa_ctx_profile_filter(c, b"")
+            lib.edfa_ctx_profile(c, 1)
+            report(c)
+        xs, rep = step()
+        if last:
+            prof_full = report(c)
+            lib.edfa_ctx_profile(c, 0)
+    torch.cuda.synchronize()
+    dom_name = max(prof_full.items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
+    lib.edfa_ctx_profile_filter(c, dom_name.encode())
+    lib.edfa_ctx_profile(c, 1)
+    report(c)
+    launches0 = lib.edfa_ctx_launch_count(c)
+    times, reps = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            xs, rep = step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            reps.append(rep)
+    launches = lib.edfa_ctx_launch_count(c) - launches0
+    prof = report(c)
+    lib.edfa_ctx_profile(c, 0)
+    lib.edfa_ctx_profile_filter(c, b"")
+    clocks = clk.summary()
+    t_total_ms = sum(times)
+    if world > 1:
+        tt = torch.tensor([t_total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_total_ms = float(tt.item())
+    value = N * args.steps / (t_total_ms / 1e3) / 1e6
+    # true residual of the assembled global solution on the host (rank 0 gathers)
+    x_loc = [x.cpu().numpy() for x in xs]
+    relres_host = None
+    if world > 1:
+        gathered = [None] * world
+        torch.distributed.all_gather_object(gathered, x_loc)
+        x_all = [v for g in gathered for v in g]
+    else:
+        x_all = x_loc
+    if rank == 0:
+        x = parallel.scatter_solution(lays, x_all, s.n_free_faces, s.n_cells)
+        relres_host = float(np.linalg.norm(s.rhs() - s.full_matrix() @ x) / np.linalg.norm(s.rhs()))
+
+    # ---- end to end from host blocks: H2D of the slab's local blocks, build, solve, D2H of x
+    e2e_times = []
+    h2d = 0
+    for lay in my_lays:
+        b = lay.blocks
+        mats = [b["A_loc"], b["A_cf_loc"], b["A_fc_loc"], b["A_ff_own"], b["A_cc_own"]] + list(b["ext"].values())
+        h2d += sum(m.data.nbytes + m.indices.nbytes + m.indptr.nbytes for m in mats) + b["rhs"].nbytes
+        h2d += sum(a.nbytes for a in b["ext_topology"])
+    d2h = sum(l.n_own for l in my_lays) * 8
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        sv = parallel.SlabSolver(my_lays, comm, kind="static", prototype="A")
+        sv.build()
+        xs_h, _ = sv.solve(tol=case.rtol, restart=case.restart, max_it=case.max_it)
+        _ = [x.cpu().numpy() for x in xs_h]
+        dt = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([dt], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e_times.append(dt)
+        del sv
+    e2e_val = N / statistics.median(e2e_times) / 1e6
+
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs") or 6650.0
+    dname, d = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", {"ms": 0, "bytes": 0,
+                                                                                    "launches": 1})
+    per_launch_ms = d["ms"] / max(d["launches"], 1)
+    per_launch_bytes = d["bytes"] / max(d["launches"], 1)
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
+    tot_full = max(sum(p["ms"] for p in prof_full.values()), 1e-9)
+    shares = {k: round(v["ms"] / tot_full, 4) for k, v in sorted(prof_full.items(), key=lambda kv: -kv[1]["ms"])[:8]}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded config-2 generator stacked along z: {args.n}x{args.n}x{args.n * parts})",
+        "config": {"workload": f"config2-{args.n}^3-per-slab-z{parts}-staticA-IC0ILU0-gmres50",
+                   "n_dof": N, "slabs": parts, "slabs_per_gpu": per_proc, "halo_layers": halo,
+                   "gmres_iterations": reps[-1].n_it, "final_true_relres": reps[-1].final_relres,
+                   "host_check_relres": relres_host, "parallelism": f"zslab{parts}",
+                   "inner_factors": "block-Jacobi per slab (IC(0) of -A_ff, ILU(0) of S~)",
+                   "l2": "inputs larger than L2 and a 256 MiB L2 flush between steps"},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "seconds_per_step": statistics.median(e2e_times)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs, burst)",
+                     "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
+                     "step_share_of_kernel_time": shares},
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
+    _, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)
+    elif world > 1 or args.slabs > 0:
+        run_slabs(args)
     else:
         run_edfa(args)
 

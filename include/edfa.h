@@ -80,6 +80,7 @@ typedef struct edfa_csr edfa_csr;
 typedef struct edfa_system edfa_system;
 typedef struct edfa_stage1 edfa_stage1;
 typedef struct edfa_stage2 edfa_stage2;
+typedef struct edfa_factor edfa_factor;
 
 typedef struct edfa_dynamic {    /* precond.DynamicConfig (precond.py:38-67) */
     int32_t n_add;
@@ -212,6 +213,43 @@ int edfa_bicgstab(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1* s1,
 /* ---- BLAS-1 helpers on device vectors (generic-callable Krylov paths) --- */
 int edfa_dot(edfa_ctx* ctx, int64_t n, const double* x, const double* y, double* out_host);
 int edfa_axpby(edfa_ctx* ctx, int64_t n, double a, const double* x, double b, double* y);
+
+/* ---- z-slab (multi-GPU) building blocks, SURVEY.md §8(e) ------------------
+ * A rank computes stage-1 rows on its extended subsystem and keeps
+ * block-Jacobi inner factors of its own rows; parallel.py orchestrates. */
+/* out = A[rows, :] with column j kept as col_map[j] when col_map[j] >= 0
+ * (col_map must be increasing on the kept columns; device arrays). */
+int edfa_csr_submatrix(edfa_ctx* ctx, const edfa_csr* A, int32_t n_rows, const int32_t* rows,
+                       const int32_t* col_map, int32_t n_cols, edfa_csr** out);
+/* out = canonical(A - B) with the optional row filter (S~ = A_cc - H~,
+ * hx/precond.py:264-271; filter_rows 138-157 when tau > 0). */
+int edfa_csr_sub(edfa_ctx* ctx, const edfa_csr* A, const edfa_csr* B, double tau, edfa_csr** out);
+/* IC(0) of -A (ic_factorize(-A_ff, no_fill=True), hx/sparse.py:217-282). */
+int edfa_factor_ic0(edfa_ctx* ctx, const edfa_csr* A, double drop_tol, edfa_factor** out);
+/* ILU(0) of S (ilu_factorize(S, no_fill=True), hx/sparse.py:141-214); nx*ny*nz
+ * = n_rows enables the tile-DAG solves (cells in natural order), else 0s. */
+int edfa_factor_ilu0(edfa_ctx* ctx, const edfa_csr* S, double drop_tol, int32_t nx, int32_t ny,
+                     int32_t nz, edfa_factor** out);
+/* InnerFactorization.nnz_stored (hx/sparse.py:118-123), pivot shifts, levels. */
+int edfa_factor_info(const edfa_factor* f, int64_t* nnz_stored, int32_t* pivot_shifts,
+                     int32_t* levels_fwd, int32_t* levels_bwd);
+/* which = 0: L, 1: U (ILU only); borrowed handle. */
+int edfa_factor_part(edfa_ctx* ctx, edfa_factor* f, int which, const edfa_csr** out);
+/* y = alpha * (L L^T)^-1 r  or  alpha * (L U)^-1 r   (InnerFactorization.apply,
+ * hx/sparse.py:125-129). */
+int edfa_factor_solve(edfa_ctx* ctx, const edfa_factor* f, const double* r, double alpha, double* y);
+int edfa_factor_destroy(edfa_factor* f);
+/* Gram-Schmidt passes on device vectors (GMRES on distributed vectors):
+ * out_dev[k] = V_k . w (k < nvec <= 64, V_k = V + k*ldv);
+ * out = w_in - hscale * sum_k h_dev[k] V_k (out = hscale * V h when w_in is NULL),
+ * norm2_dev[0] = ||out||^2 when norm2_dev is not NULL. */
+int edfa_multidot(edfa_ctx* ctx, int64_t n, int32_t nvec, const double* V, int64_t ldv,
+                  const double* w, double* out_dev);
+int edfa_multiaxpy(edfa_ctx* ctx, int64_t n, int32_t nvec, const double* V, int64_t ldv,
+                   const double* h_dev, double hscale, const double* w_in, double* out,
+                   double* norm2_dev);
+/* out[i] = x[idx[i]]  (halo send buffers). */
+int edfa_gather(edfa_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* out);
 
 #ifdef __cplusplus
 }

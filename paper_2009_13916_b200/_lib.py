@@ -84,6 +84,17 @@ _SIGS = {
     "edfa_bicgstab": (i32, [vp, vp, vp, vp, vp, vp, f64, i32, C.POINTER(Report), vp, i32]),
     "edfa_dot": (i32, [vp, i64, vp, vp, C.POINTER(f64)]),
     "edfa_axpby": (i32, [vp, i64, f64, vp, f64, vp]),
+    "edfa_csr_submatrix": (i32, [vp, vp, i32, vp, vp, i32, C.POINTER(vp)]),
+    "edfa_csr_sub": (i32, [vp, vp, vp, f64, C.POINTER(vp)]),
+    "edfa_factor_ic0": (i32, [vp, vp, f64, C.POINTER(vp)]),
+    "edfa_factor_ilu0": (i32, [vp, vp, f64, i32, i32, i32, C.POINTER(vp)]),
+    "edfa_factor_info": (i32, [vp, C.POINTER(i64), P_i32, P_i32, P_i32]),
+    "edfa_factor_part": (i32, [vp, vp, i32, C.POINTER(vp)]),
+    "edfa_factor_solve": (i32, [vp, vp, vp, f64, vp]),
+    "edfa_factor_destroy": (i32, [vp]),
+    "edfa_multidot": (i32, [vp, i64, i32, vp, i64, vp, vp]),
+    "edfa_multiaxpy": (i32, [vp, i64, i32, vp, i64, vp, f64, vp, vp, vp]),
+    "edfa_gather": (i32, [vp, i64, vp, vp, vp]),
 }
 
 _lib = None

@@ -54,12 +54,12 @@ def element_ops(grid: HexGrid, field: Conductivity, gamma: float) -> ElementOps:
     pts, wts = gauss3()
     B = np.zeros((xyz.shape[0], 6, 6))
     for p, w in zip(pts, wts):
-        J = np.einsum("enc,nb->ecb", xyz, shape_grad(p))
+        J = np.matmul(xyz.transpose(0, 2, 1), shape_grad(p))          # (e, 3, 3)
         det = np.linalg.det(J)
         if np.any(det <= 0):
             raise ValueError("non-positive Jacobian")
-        M = np.einsum("ecb,fb->ecf", J, rt0_reference(p))
-        B += w * np.einsum("eaf,eab,ebg->efg", M, Kinv, M) / det[:, None, None]
+        M = np.matmul(J, rt0_reference(p).T)                          # (e, 3, 6)
+        B += np.matmul(M.transpose(0, 2, 1), np.matmul(Kinv, M)) * (w / det)[:, None, None]
     B *= gamma
     B = 0.5 * (B + B.transpose(0, 2, 1))
     Bi = np.linalg.inv(B)

@@ -72,14 +72,16 @@ def config1(n=16):
     return CaseSpec(f"config1-{n}^3-base", s, dict(pattern="base", **_inner()))
 
 
-def config2(n=64, seed=SEEDS[2], length=1000.0):
+def config2(n=64, seed=SEEDS[2], length=1000.0, nz=None):
+    """``nz`` > n stacks cubes along z (the weak-scaling grids of BASELINE
+    config 5: 64^3 per GPU grown along z so slabs stay z-slabs)."""
     h = length / n
-    g = mesh.box_grid(n, n, n, h, h, h)
+    g = mesh.box_grid(n, n, nz or n, h, h, h)
     fld = lognormal_aniso_field(g.n_elems, seed)
     bc = mesh.Boundaries(pressure_planes={"x-": 1.0, "x+": 0.0})
     s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=1.0,
                           p_prev=np.zeros(g.n_elems))
-    return CaseSpec(f"config2-{n}^3-staticA", s,
+    return CaseSpec(f"config2-{n}^3-staticA" if not nz or nz == n else f"config2-{n}x{n}x{nz}-staticA", s,
                     dict(pattern="static", prototype="A", **_inner()))
 
 

@@ -433,4 +433,158 @@ int edfa_axpby(edfa_ctx* ctx, int64_t n, double a, const double* x, double b, do
     API_END
 }
 
+// ---------------------------------------------------------------- slab (multi-GPU) building blocks
+int edfa_csr_submatrix(edfa_ctx* ctx, const edfa_csr* A, int32_t n_rows, const int32_t* rows, const int32_t* col_map,
+                       int32_t n_cols, edfa_csr** out) {
+    API_BEGIN
+    require(ctx && out && (n_rows == 0 || rows) && col_map, EDFA_ERR_VALUE, "NULL argument");
+    require(n_rows >= 0 && n_cols >= 0, EDFA_ERR_VALUE, "negative size");
+    auto* h = new edfa_csr();
+    h->ctx = &ctx->c;
+    try {
+        csr_submatrix(&ctx->c, M(A), rows, n_rows, col_map, n_cols, h->own);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    API_END
+}
+
+int edfa_csr_sub(edfa_ctx* ctx, const edfa_csr* A, const edfa_csr* B, double tau, edfa_csr** out) {
+    API_BEGIN
+    require(ctx && out, EDFA_ERR_VALUE, "NULL argument");
+    require(tau >= 0.0, EDFA_ERR_VALUE, "tau must be >= 0");
+    auto* h = new edfa_csr();
+    h->ctx = &ctx->c;
+    try {
+        csr_sub(&ctx->c, M(A), M(B), tau, h->own);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    API_END
+}
+
+int edfa_factor_ic0(edfa_ctx* ctx, const edfa_csr* A, double drop_tol, edfa_factor** out) {
+    API_BEGIN
+    require(ctx && out, EDFA_ERR_VALUE, "NULL argument");
+    require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
+    const Csr& a = M(A);
+    require(a.n_rows == a.n_cols, EDFA_ERR_VALUE, "IC needs a square matrix");
+    auto* f = new edfa_factor();
+    f->ctx = &ctx->c;
+    f->kind = 0;
+    try {
+        ic0_factor(&ctx->c, a, drop_tol, f->ic);
+    } catch (...) {
+        delete f;
+        throw;
+    }
+    *out = f;
+    API_END
+}
+
+int edfa_factor_ilu0(edfa_ctx* ctx, const edfa_csr* S, double drop_tol, int32_t nx, int32_t ny, int32_t nz,
+                     edfa_factor** out) {
+    API_BEGIN
+    require(ctx && out, EDFA_ERR_VALUE, "NULL argument");
+    require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
+    const Csr& s = M(S);
+    require(s.n_rows == s.n_cols, EDFA_ERR_VALUE, "ILU needs a square matrix");
+    int dims[3] = {nx, ny, nz};
+    const bool grid = nx > 0 && ny > 0 && nz > 0 && (int64_t)nx * ny * nz == s.n_rows;
+    auto* f = new edfa_factor();
+    f->ctx = &ctx->c;
+    f->kind = 1;
+    try {
+        ilu0_factor(&ctx->c, s, drop_tol, f->ilu, grid ? dims : nullptr);
+    } catch (...) {
+        delete f;
+        throw;
+    }
+    *out = f;
+    API_END
+}
+
+int edfa_factor_info(const edfa_factor* f, int64_t* nnz_stored, int32_t* pivot_shifts, int32_t* levels_fwd,
+                     int32_t* levels_bwd) {
+    API_BEGIN
+    require(f != nullptr, EDFA_ERR_VALUE, "factor handle is NULL");
+    const TriPlan& fw = f->kind == 0 ? f->ic.fwd : f->ilu.fwd;
+    const TriPlan& bw = f->kind == 0 ? f->ic.bwd : f->ilu.bwd;
+    // hx/sparse.py:118-123: IC stores 2 nnz(L) - n, ILU nnz(L) - n + nnz(U)
+    if (nnz_stored) {
+        if (f->kind == 0) *nnz_stored = 2 * (f->ic.Lpat.nnz + f->ic.n) - f->ic.n;
+        else *nnz_stored = f->ilu.fwd.n_dep + f->ilu.bwd.n_dep + f->ilu.n;
+    }
+    if (pivot_shifts) *pivot_shifts = f->kind == 0 ? f->ic.shifts : f->ilu.shifts;
+    if (levels_fwd) *levels_fwd = fw.n_levels;
+    if (levels_bwd) *levels_bwd = bw.n_levels;
+    API_END
+}
+
+int edfa_factor_part(edfa_ctx* ctx, edfa_factor* f, int which, const edfa_csr** out) {
+    API_BEGIN
+    require(ctx && f && out, EDFA_ERR_VALUE, "NULL argument");
+    require(which == 0 || (which == 1 && f->kind == 1), EDFA_ERR_VALUE, "unknown factor part");
+    Ctx* c = &ctx->c;
+    const Csr* m;
+    if (f->kind == 0) {
+        ic_export(c, f->ic);
+        m = &f->ic.export_L;
+    } else {
+        ilu_export(c, f->ilu);
+        m = which == 0 ? &f->ilu.export_L : &f->ilu.export_U;
+    }
+    f->views[which].ctx = c;
+    f->views[which].m = m;
+    *out = &f->views[which];
+    API_END
+}
+
+int edfa_factor_solve(edfa_ctx* ctx, const edfa_factor* f, const double* r, double alpha, double* y) {
+    API_BEGIN
+    require(ctx && f, EDFA_ERR_VALUE, "NULL argument");
+    Ctx* c = &ctx->c;
+    if (f->kind == 0) {
+        DevBuf<double> tmp(c, std::max(f->ic.n, 1));
+        run_plan(c, f->ic.fwd, r, alpha, tmp.p, nullptr, nullptr, "trsv_ic_L");
+        run_plan(c, f->ic.bwd, tmp.p, 1.0, y, nullptr, nullptr, "trsv_ic_LT");
+    } else {
+        DevBuf<double> tmp(c, std::max(f->ilu.n, 1));
+        run_plan(c, f->ilu.fwd, r, alpha, tmp.p, nullptr, nullptr, "trsv_ilu_L");
+        run_plan(c, f->ilu.bwd, tmp.p, 1.0, y, nullptr, nullptr, "trsv_ilu_U");
+    }
+    API_END
+}
+
+int edfa_factor_destroy(edfa_factor* f) {
+    API_BEGIN
+    delete f;
+    API_END
+}
+
+int edfa_multidot(edfa_ctx* ctx, int64_t n, int32_t nvec, const double* V, int64_t ldv, const double* w,
+                  double* out_dev) {
+    API_BEGIN
+    multidot_entry(&ctx->c, n, nvec, V, ldv, w, out_dev);
+    API_END
+}
+
+int edfa_multiaxpy(edfa_ctx* ctx, int64_t n, int32_t nvec, const double* V, int64_t ldv, const double* h_dev,
+                   double hscale, const double* w_in, double* out, double* norm2_dev) {
+    API_BEGIN
+    multiaxpy_entry(&ctx->c, n, nvec, V, ldv, h_dev, hscale, w_in, out, norm2_dev);
+    API_END
+}
+
+int edfa_gather(edfa_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* out) {
+    API_BEGIN
+    gather(&ctx->c, n, idx, x, out);
+    API_END
+}
+
 }  // extern "C"
+

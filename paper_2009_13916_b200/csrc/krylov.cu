@@ -21,11 +21,14 @@
 namespace edfa {
 namespace {
 
-constexpr int RED_BLOCKS = 2 * NUM_SMS_B200;   // fixed grid -> fixed reduction order
+constexpr int RED_BLOCKS = 3 * NUM_SMS_B200;   // fixed grid -> fixed reduction order
 constexpr int RED_THREADS = 256;
 constexpr int GROUP = 8;                      // vectors per multi-dot block row
 
-// partial[blk][k] = sum over the block's rows of V[k0+k] . w   (k < GROUP)
+// partial[blk][k] = sum over the block's rows of V[k0+k] . w   (k < GROUP).
+// VEC2: pairs of rows per thread with 16-byte loads (V rows and w 16-byte
+// aligned, ldv even); the odd tail row is taken by the scalar path.
+template <bool VEC2>
 __global__ void __launch_bounds__(RED_THREADS) k_multidot(const double* __restrict__ V, int64_t ldv, int nvec,
                                                           const double* __restrict__ w, int64_t n,
                                                           double* __restrict__ partial) {
@@ -33,13 +36,34 @@ __global__ void __launch_bounds__(RED_THREADS) k_multidot(const double* __restri
     double acc[GROUP];
 #pragma unroll
     for (int k = 0; k < GROUP; ++k) acc[k] = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double wi = w[i];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (VEC2) {
+        const int64_t n2 = n >> 1;
+        const double2* w2 = reinterpret_cast<const double2*>(w);
+        for (int64_t i = t0; i < n2; i += stride) {
+            double2 wi = w2[i];
+            double2 v[GROUP];
 #pragma unroll
-        for (int k = 0; k < GROUP; ++k)
-            if (k0 + k < nvec) {
-                acc[k] = fma(V[(int64_t)(k0 + k) * ldv + i], wi, acc[k]);
-            }
+            for (int k = 0; k < GROUP; ++k)
+                if (k0 + k < nvec) v[k] = reinterpret_cast<const double2*>(V + (int64_t)(k0 + k) * ldv)[i];
+#pragma unroll
+            for (int k = 0; k < GROUP; ++k)
+                if (k0 + k < nvec) acc[k] = fma(v[k].y, wi.y, fma(v[k].x, wi.x, acc[k]));
+        }
+        if ((n & 1) && t0 == 0) {
+            double wi = w[n - 1];
+#pragma unroll
+            for (int k = 0; k < GROUP; ++k)
+                if (k0 + k < nvec) acc[k] = fma(V[(int64_t)(k0 + k) * ldv + n - 1], wi, acc[k]);
+        }
+    } else {
+        for (int64_t i = t0; i < n; i += stride) {
+            double wi = w[i];
+#pragma unroll
+            for (int k = 0; k < GROUP; ++k)
+                if (k0 + k < nvec) acc[k] = fma(V[(int64_t)(k0 + k) * ldv + i], wi, acc[k]);
+        }
     }
     __shared__ double red[GROUP][RED_THREADS / 32];
     int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -67,8 +91,9 @@ __global__ void k_reduce_partials(const double* __restrict__ partial, int nblk, 
 }
 
 // w <- w - sum_{k<nv} h[k] V[k]   (or out = sum h[k] V[k] when w_in == NULL),
-// partial[blk] = block sum of out^2
-__global__ void __launch_bounds__(RED_THREADS) k_multiaxpy(const double* __restrict__ V, int64_t ldv, int nv,
+// partial[blk] = block sum of out^2.  VEC2 as in k_multidot.
+template <bool VEC2>
+__global__ void __launch_bounds__(RED_THREADS, 3) k_multiaxpy(const double* __restrict__ V, int64_t ldv, int nv,
                                                            const double* __restrict__ h, double hscale,
                                                            const double* w_in, double* out,
                                                            int64_t n, double* __restrict__ partial) {
@@ -76,21 +101,66 @@ __global__ void __launch_bounds__(RED_THREADS) k_multiaxpy(const double* __restr
     if (threadIdx.x < nv) hs[threadIdx.x] = h[threadIdx.x] * hscale;
     __syncthreads();
     double ss = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        int k = 0;
-        for (; k + 4 <= nv; k += 4) {
-            double a0 = V[(int64_t)k * ldv + i], a1 = V[(int64_t)(k + 1) * ldv + i];
-            double a2 = V[(int64_t)(k + 2) * ldv + i], a3 = V[(int64_t)(k + 3) * ldv + i];
-            acc = fma(hs[k], a0, acc);
-            acc = fma(hs[k + 1], a1, acc);
-            acc = fma(hs[k + 2], a2, acc);
-            acc = fma(hs[k + 3], a3, acc);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (VEC2) {
+        const int64_t n2 = n >> 1;
+        for (int64_t i = t0; i < n2; i += stride) {
+            double ax = 0.0, ay = 0.0;
+            int k = 0;
+            for (; k + 8 <= nv; k += 8) {
+                double2 a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] = reinterpret_cast<const double2*>(V + (int64_t)(k + u) * ldv)[i];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    ax = fma(hs[k + u], a[u].x, ax);
+                    ay = fma(hs[k + u], a[u].y, ay);
+                }
+            }
+            for (; k < nv; ++k) {
+                double2 a = reinterpret_cast<const double2*>(V + (int64_t)k * ldv)[i];
+                ax = fma(hs[k], a.x, ax);
+                ay = fma(hs[k], a.y, ay);
+            }
+            double2 o;
+            if (w_in) {
+                double2 wv = reinterpret_cast<const double2*>(w_in)[i];
+                o.x = wv.x - ax;
+                o.y = wv.y - ay;
+            } else {
+                o.x = ax;
+                o.y = ay;
+            }
+            reinterpret_cast<double2*>(out)[i] = o;
+            ss = fma(o.x, o.x, ss);
+            ss = fma(o.y, o.y, ss);
         }
-        for (; k < nv; ++k) acc = fma(hs[k], V[(int64_t)k * ldv + i], acc);
-        double o = w_in ? w_in[i] - acc : acc;
-        out[i] = o;
-        ss = fma(o, o, ss);
+        if ((n & 1) && t0 == 0) {
+            const int64_t i = n - 1;
+            double acc = 0.0;
+            for (int k = 0; k < nv; ++k) acc = fma(hs[k], V[(int64_t)k * ldv + i], acc);
+            double o = w_in ? w_in[i] - acc : acc;
+            out[i] = o;
+            ss = fma(o, o, ss);
+        }
+    } else {
+        for (int64_t i = t0; i < n; i += stride) {
+            double acc = 0.0;
+            int k = 0;
+            for (; k + 4 <= nv; k += 4) {
+                double a0 = V[(int64_t)k * ldv + i], a1 = V[(int64_t)(k + 1) * ldv + i];
+                double a2 = V[(int64_t)(k + 2) * ldv + i], a3 = V[(int64_t)(k + 3) * ldv + i];
+                acc = fma(hs[k], a0, acc);
+                acc = fma(hs[k + 1], a1, acc);
+                acc = fma(hs[k + 2], a2, acc);
+                acc = fma(hs[k + 3], a3, acc);
+            }
+            for (; k < nv; ++k) acc = fma(hs[k], V[(int64_t)k * ldv + i], acc);
+            double o = w_in ? w_in[i] - acc : acc;
+            out[i] = o;
+            ss = fma(o, o, ss);
+        }
     }
     __shared__ double red[RED_THREADS / 32];
     ss = warp_sum(ss);
@@ -102,6 +172,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_multiaxpy(const double* __restr
         if (partial) partial[(int64_t)blockIdx.x * 64] = s;
     }
 }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 __global__ void k_axpby(int64_t n, double a, const double* x, double b, double* y) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -135,7 +207,10 @@ struct Blas {
         if (nvec == 0) return;
         dim3 grid(grid_for(n), (nvec + GROUP - 1) / GROUP);
         Prof pr(c, "gs_multidot", 8.0 * n * (nvec + 1));
-        k_multidot<<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p);
+        if ((ldv % 2 == 0 || nvec == 1) && aligned16(V) && aligned16(w))
+            k_multidot<true><<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p);
+        else
+            k_multidot<false><<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p);
         k_reduce_partials<<<nvec, 32, 0, c->stream>>>(partial.p, grid.x, nvec, out_dev);
         check_launch("multidot");
     }
@@ -144,8 +219,13 @@ struct Blas {
                    double* out, int64_t n, double* norm2_dev) {
         int g = grid_for(n);
         Prof pr(c, "gs_multiaxpy", 8.0 * n * (nv + (w_in ? 2 : 1)));
-        k_multiaxpy<<<g, RED_THREADS, 0, c->stream>>>(V, ldv, nv, h, hscale, w_in, out, n,
-                                                       norm2_dev ? partial.p : nullptr);
+        const bool v2 = (ldv % 2 == 0 || nv <= 1) && aligned16(V) && aligned16(out) && (!w_in || aligned16(w_in));
+        if (v2)
+            k_multiaxpy<true><<<g, RED_THREADS, 0, c->stream>>>(V, ldv, nv, h, hscale, w_in, out, n,
+                                                                 norm2_dev ? partial.p : nullptr);
+        else
+            k_multiaxpy<false><<<g, RED_THREADS, 0, c->stream>>>(V, ldv, nv, h, hscale, w_in, out, n,
+                                                                  norm2_dev ? partial.p : nullptr);
         if (norm2_dev) k_reduce_partials<<<1, 32, 0, c->stream>>>(partial.p, g, 1, norm2_dev);
         check_launch("multiaxpy");
     }
@@ -430,6 +510,17 @@ void apply_entry(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const ed
 double dot_entry(Ctx* c, int64_t n, const double* x, const double* y) {
     Blas bl(c);
     return bl.dot(x, y, n);
+}
+void multidot_entry(Ctx* c, int64_t n, int nvec, const double* V, int64_t ldv, const double* w, double* out_dev) {
+    require(nvec >= 0 && nvec <= 64, EDFA_ERR_VALUE, "nvec must be in [0, 64]");
+    Blas bl(c);
+    bl.multidot(V, ldv, nvec, w, n, out_dev);
+}
+void multiaxpy_entry(Ctx* c, int64_t n, int nvec, const double* V, int64_t ldv, const double* h, double hscale,
+                     const double* w_in, double* out, double* norm2_dev) {
+    require(nvec >= 0 && nvec <= 64, EDFA_ERR_VALUE, "nvec must be in [0, 64]");
+    Blas bl(c);
+    bl.multiaxpy(V, ldv, nvec, h, hscale, w_in, out, n, norm2_dev);
 }
 void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double* y) {
     Blas bl(c);

@@ -165,6 +165,14 @@ struct edfa_stage2 {
     edfa_csr views[3];
 };
 
+struct edfa_factor {            // stand-alone IC(0) of -A / ILU(0) of S (slab.cu)
+    edfa::Ctx* ctx;
+    int kind = 0;               // 0 = IC (factor of -A), 1 = ILU
+    edfa::IcFactor ic;
+    edfa::IluFactor ilu;
+    edfa_csr views[2];
+};
+
 namespace edfa {
 void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynamic* dyn, double tau, int filt,
                   double face_drop_tol, int no_fill, edfa_stage1* s1);
@@ -179,5 +187,11 @@ void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_sta
 void bicgstab(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b,
               double* x, double rtol, int max_it, edfa_report* rep, double* hist, int hist_cap);
 double dot_entry(Ctx* c, int64_t n, const double* x, const double* y);
+void multidot_entry(Ctx* c, int64_t n, int nvec, const double* V, int64_t ldv, const double* w, double* out_dev);
+void multiaxpy_entry(Ctx* c, int64_t n, int nvec, const double* V, int64_t ldv, const double* h, double hscale,
+                     const double* w_in, double* out, double* norm2_dev);
+void csr_submatrix(Ctx* c, const Csr& A, const int32_t* rows, int32_t n_out, const int32_t* cmap, int32_t n_cols,
+                   Csr& out);
+void gather(Ctx* c, int64_t n, const int32_t* idx, const double* x, double* out);
 void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double* y);
 }  // namespace edfa

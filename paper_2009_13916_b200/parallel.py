@@ -1,0 +1,661 @@
+"""Z-slab partitioned EDFA + GMRES(m) over several GPUs.
+
+Partitioning (hx/grid.py:49-50, 100-129): cells are numbered i + nx(j + ny k)
+and every face family is k-slowest, so a slab of cell layers [k0, k1) is one
+contiguous cell range; a face belongs to the slab of its owner cell (the
+lower-indexed cell, ``face_to_elems[f, 0]``).  A rank keeps the rows of its
+own faces and cells; the local vector is ``[own faces | own cells]``.
+
+* Setup.  Stage-1 rows (restricted solves, G~, F~, H~) are independent per
+  cell.  Each rank computes them on its *extended* subsystem --
+  the slab plus ``halo`` cell layers on each side, a read-only copy of the
+  neighbours' rows -- so the rows of its own cells are exactly the global
+  ones.  It keeps the block-Jacobi inner factors
+      IC(0) of -A_ff[own, own],    ILU(0) of S~[own, own] = A_cc - H~ on own x own,
+  so no triangular solve crosses a slab boundary.
+* Apply (hx/precond.py:311-320) and SpMV exchange one layer of halo values
+  (faces for ``A_cf``, cells for ``A_fc``); Krylov dot products are summed
+  over ranks (NCCL allreduce over NVLink on the GPU path).
+
+The driver is written over *parts*: a process holds one part per GPU in
+production (``torch.distributed`` over NCCL), or several parts on one device
+when emulating k slabs (the halo copies are then local).  Nothing here
+computes on the host: parts do their arithmetic through libedfa.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib as L
+from .krylov import SolveReport
+
+# ---------------------------------------------------------------------------
+# host partition (integer bookkeeping only)
+
+PATTERN_REACH = {"base": 0, "A": 2, "B": 3, "C": 1, "D": 2, "E": 1}
+
+
+def halo_layers(kind: str, prototype: str = "A", dynamic=None) -> int:
+    """Cell layers of read-only halo that make the own rows of G~, F~ and
+    H~[own, own] exact: the pattern's reach in cells plus one (the faces of
+    a pattern need both of their cells for a complete A_ff row)."""
+    if dynamic is not None or kind == "dynamic":
+        n_ent = dynamic.n_ent if dynamic is not None else 4
+        return 2 + n_ent
+    if kind == "base":
+        return 1
+    return PATTERN_REACH[prototype] + 1
+
+
+def slab_bounds(nz: int, parts: int):
+    if parts < 1 or parts > nz:
+        raise ValueError(f"cannot cut {nz} cell layers into {parts} slabs")
+    return [(r * nz // parts, (r + 1) * nz // parts) for r in range(parts)]
+
+
+def _canon(A):
+    A = sp.csr_matrix(A)
+    A.sum_duplicates()
+    A.sort_indices()
+    return A
+
+
+@dataclass
+class SlabLayout:
+    """Rows, halo lists and local blocks of one slab (all numpy / scipy)."""
+
+    rank: int
+    size: int
+    k0: int
+    k1: int
+    e0: int
+    e1: int
+    nxyz: tuple
+    own_faces: np.ndarray          # free-face ids, sorted
+    own_cells: np.ndarray          # cell ids, contiguous
+    halo_faces: np.ndarray         # ordered by (owner rank, id)
+    halo_cells: np.ndarray
+    recv_faces: dict               # peer -> (start, stop) into halo_faces
+    recv_cells: dict
+    send_faces: dict = field(default_factory=dict)   # peer -> positions into own_faces
+    send_cells: dict = field(default_factory=dict)
+    ext_faces: np.ndarray = None
+    ext_cells: np.ndarray = None
+    blocks: dict = field(default_factory=dict)
+
+    @property
+    def n_faces(self) -> int:
+        return self.own_faces.size
+
+    @property
+    def n_cells(self) -> int:
+        return self.own_cells.size
+
+    @property
+    def n_own(self) -> int:
+        return self.n_faces + self.n_cells
+
+
+def _ordered_halo(ids, owner):
+    order = np.lexsort((ids, owner))
+    ids, owner = ids[order], owner[order]
+    recv = {}
+    for q in np.unique(owner):
+        w = np.flatnonzero(owner == q)
+        recv[int(q)] = (int(w[0]), int(w[-1]) + 1)
+    return ids, owner, recv
+
+
+def build_layouts(system, parts: int, halo: int, ranks=None):
+    """Slab layouts of a BlockSystem on an nx*ny*nz box (hexflow numbering).
+
+    ``ranks`` limits the (expensive) local block extraction to the listed
+    slabs; the halo lists of every slab are always computed (they define
+    what each slab sends)."""
+    grid = system.grid
+    nx, ny, nz = grid.nx, grid.ny, grid.nz
+    nxy = nx * ny
+    nf = system.n_free_faces
+    bounds = slab_bounds(nz, parts)
+    layer_part = np.empty(nz, dtype=np.int64)
+    for r, (a, b) in enumerate(bounds):
+        layer_part[a:b] = r
+    f2e = np.asarray(grid.face_to_elems)
+    free = np.asarray(system.free_faces)
+    face_part = layer_part[f2e[free, 0] // nxy]
+    cell_part = layer_part[np.arange(system.n_cells) // nxy]
+    A = _canon(system.full_matrix())
+    ranks = range(parts) if ranks is None else ranks
+    lays = []
+    for r, (k0, k1) in enumerate(bounds):
+        own_f = np.flatnonzero(face_part == r)
+        own_c = np.arange(k0 * nxy, k1 * nxy)
+        rows = np.concatenate([own_f, nf + own_c])
+        Ar = A[rows]
+        cols = np.unique(Ar.indices)
+        hf = cols[(cols < nf)]
+        hf = hf[face_part[hf] != r]
+        hc = cols[cols >= nf] - nf
+        hc = hc[cell_part[hc] != r]
+        hf, hf_own, recv_f = _ordered_halo(hf, face_part[hf])
+        hc, hc_own, recv_c = _ordered_halo(hc, cell_part[hc])
+        e0, e1 = max(0, k0 - halo), min(nz, k1 + halo)
+        lay = SlabLayout(r, parts, k0, k1, e0, e1, (nx, ny, nz), own_f, own_c, hf, hc, recv_f, recv_c)
+        if r in ranks:
+            _local_blocks(system, A, lay, nf, f2e, free, nxy)
+        lays.append(lay)
+    for q, lq in enumerate(lays):          # what slab q receives, slab r sends
+        for r, (a, b) in lq.recv_faces.items():
+            lays[r].send_faces[q] = np.searchsorted(lays[r].own_faces, lq.halo_faces[a:b])
+        for r, (a, b) in lq.recv_cells.items():
+            lays[r].send_cells[q] = np.searchsorted(lays[r].own_cells, lq.halo_cells[a:b])
+    return lays
+
+
+def _local_blocks(system, A, lay, nf, f2e, free, nxy):
+    """Local rows with local column numbering and the extended subsystem."""
+    nfo, nco = lay.n_faces, lay.n_cells
+    nhf, nhc = lay.halo_faces.size, lay.halo_cells.size
+    n_all = nf + system.n_cells
+    cmap = np.full(n_all, -1, dtype=np.int64)
+    cmap[lay.own_faces] = np.arange(nfo)
+    cmap[nf + lay.own_cells] = nfo + np.arange(nco)
+    cmap[lay.halo_faces] = nfo + nco + np.arange(nhf)
+    cmap[nf + lay.halo_cells] = nfo + nco + nhf + np.arange(nhc)
+    rows = np.concatenate([lay.own_faces, nf + lay.own_cells])
+
+    def remap(M, rows, cmap, n_cols):
+        M = M[rows]
+        c = cmap[M.indices]
+        if (c < 0).any():
+            raise AssertionError("halo lists miss a column of the local rows")
+        return _canon(sp.csr_matrix((M.data, c, M.indptr), shape=(M.shape[0], n_cols)))
+
+    b = lay.blocks
+    b["A_loc"] = remap(A, rows, cmap, nfo + nco + nhf + nhc)
+    fmap = np.full(nf, -1, dtype=np.int64)
+    fmap[lay.own_faces] = np.arange(nfo)
+    fmap[lay.halo_faces] = nfo + np.arange(nhf)
+    cmap_c = np.full(system.n_cells, -1, dtype=np.int64)
+    cmap_c[lay.own_cells] = np.arange(nco)
+    cmap_c[lay.halo_cells] = nco + np.arange(nhc)
+    b["A_cf_loc"] = remap(system.A_cf.tocsr(), lay.own_cells, fmap, nfo + nhf)
+    b["A_fc_loc"] = remap(system.A_fc.tocsr(), lay.own_faces, cmap_c, nco + nhc)
+    b["A_ff_own"] = _canon(system.A_ff.tocsr()[lay.own_faces][:, lay.own_faces])
+    b["A_cc_own"] = _canon(system.A_cc.tocsr()[lay.own_cells][:, lay.own_cells])
+    # extended subsystem: cells of layers [e0, e1) and every free face of theirs
+    ext_c = np.arange(lay.e0 * nxy, lay.e1 * nxy)
+    lay.ext_cells = ext_c
+    lo, hi = lay.e0 * nxy, lay.e1 * nxy
+    fe = f2e[free]
+    in_ext = ((fe[:, 0] >= lo) & (fe[:, 0] < hi)) | ((fe[:, 1] >= lo) & (fe[:, 1] < hi))
+    ext_f = np.flatnonzero(in_ext)
+    lay.ext_faces = ext_f
+    b["ext"] = {
+        "A_ff": _canon(system.A_ff.tocsr()[ext_f][:, ext_f]),
+        "A_fc": _canon(system.A_fc.tocsr()[ext_f][:, ext_c]),
+        "A_cf": _canon(system.A_cf.tocsr()[ext_c][:, ext_f]),
+        "A_cc": _canon(system.A_cc.tocsr()[ext_c][:, ext_c]),
+    }
+    b["own_cells_in_ext"] = lay.own_cells - lo
+    b["own_faces_in_ext"] = np.searchsorted(ext_f, lay.own_faces)
+    # topology of the extended box for the static-pattern kernel: ext cells'
+    # faces in a compact numbering, neighbours outside the box cut off
+    grid = system.grid
+    e2f = np.asarray(grid.elem_to_faces)[ext_c]
+    all_f, inv = np.unique(e2f, return_inverse=True)
+    e2f_loc = inv.reshape(e2f.shape)
+    fe_all = f2e[all_f]
+    nb = np.where(fe_all[inv.reshape(e2f.shape), 0] == ext_c[:, None],
+                  fe_all[inv.reshape(e2f.shape), 1], fe_all[inv.reshape(e2f.shape), 0])
+    nb = np.where((nb >= lo) & (nb < hi), nb - lo, -1)
+    fi = np.asarray(system.face_index)[all_f]
+    ext_pos = np.full(nf, -1, dtype=np.int64)
+    ext_pos[ext_f] = np.arange(ext_f.size)
+    fidx = np.where(fi >= 0, ext_pos[np.maximum(fi, 0)], -1)
+    b["ext_topology"] = (e2f_loc.astype(np.int32), nb.astype(np.int32), fidx.astype(np.int32))
+    b["rhs"] = np.concatenate([system.rhs_f[lay.own_faces], system.rhs_c[lay.own_cells]])
+
+
+def scatter_solution(layouts, xs, n_free_faces, n_cells):
+    """Global solution from the per-slab local vectors (host)."""
+    x = np.empty(n_free_faces + n_cells)
+    for lay, xl in zip(layouts, xs):
+        xl = xl.detach().cpu().numpy() if isinstance(xl, torch.Tensor) else np.asarray(xl)
+        x[lay.own_faces] = xl[:lay.n_faces]
+        x[n_free_faces + lay.own_cells] = xl[lay.n_faces:]
+    return x
+
+
+# ---------------------------------------------------------------------------
+# communication
+
+class LocalComm:
+    """Single process: every part is local, reductions are local sums."""
+
+    rank_of_part = None
+
+    def __init__(self, parts: int):
+        self.rank_of_part = [0] * parts
+        self.rank = 0
+
+    def allreduce_(self, t: torch.Tensor) -> None:
+        return None
+
+    def p2p(self, sends, recvs) -> None:
+        if sends or recvs:
+            raise RuntimeError("LocalComm has no remote peers")
+
+
+class TorchComm:
+    """torch.distributed process group (NCCL on GPUs, gloo on CPU); one or
+    more slabs per process, ``rank_of_part[s]`` = process holding slab s."""
+
+    def __init__(self, rank_of_part, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.rank_of_part = list(rank_of_part)
+
+    def allreduce_(self, t: torch.Tensor) -> None:
+        self.dist.all_reduce(t, group=self.group)
+
+    def p2p(self, sends, recvs) -> None:
+        """sends/recvs: lists of (peer process, tensor); matched in order."""
+        d = self.dist
+        ops = [d.P2POp(d.isend, t, peer, self.group) for peer, t in sends]
+        ops += [d.P2POp(d.irecv, t, peer, self.group) for peer, t in recvs]
+        if ops:
+            for req in d.batch_isend_irecv(ops):
+                req.wait()
+
+
+class HaloExchange:
+    """Moves own-entry values of each slab into its neighbours' halo slots."""
+
+    def __init__(self, parts, comm):
+        self.parts = parts                  # local parts (objects with .layout)
+        self.comm = comm
+        self.by_slab = {p.layout.rank: p for p in parts}
+
+    def run(self, kind: str, src, dst) -> None:
+        """kind 'f' or 'c'; src[i] own-entry vector, dst[i] halo vector of parts[i]."""
+        send_attr = "send_faces" if kind == "f" else "send_cells"
+        recv_attr = "recv_faces" if kind == "f" else "recv_cells"
+        rank_of = self.comm.rank_of_part
+        remote_s, remote_r = [], []
+        bufs = {}
+        for p, s in zip(self.parts, src):
+            for q in sorted(getattr(p.layout, send_attr)):
+                bufs[(p.layout.rank, q)] = p.gather(s, kind, q)
+        for p, d in zip(self.parts, dst):
+            for q, (a, b) in sorted(getattr(p.layout, recv_attr).items()):
+                if q in self.by_slab:
+                    d[a:b].copy_(bufs[(q, p.layout.rank)])
+                else:
+                    remote_r.append((rank_of[q], d[a:b]))
+        for (src_slab, q), buf in sorted(bufs.items()):
+            if q not in self.by_slab:
+                remote_s.append((rank_of[q], buf))
+        if remote_s or remote_r:
+            # matched in order: sends sorted by (source slab, target slab),
+            # receives by (local slab, source slab) -- the same sequence on
+            # both ends of every process pair
+            self.comm.p2p(remote_s, remote_r)
+
+
+# ---------------------------------------------------------------------------
+# device part
+
+class CudaSlab:
+    """One slab on the current CUDA device; every operation is a libedfa call."""
+
+    def __init__(self, layout: SlabLayout, *, kind="static", prototype="A", dynamic=None,
+                 tau_filt=0.0, filtration="none", face_drop_tol=0.0, schur_drop_tol=0.0, no_fill=True):
+        from .device import DeviceCsr, DeviceSystem, ctx
+        self.layout = layout
+        self.opts = dict(kind=kind, prototype=prototype, dynamic=dynamic, tau_filt=tau_filt,
+                         filtration=filtration, face_drop_tol=face_drop_tol, schur_drop_tol=schur_drop_tol,
+                         no_fill=no_fill)
+        self.lib = L.lib()
+        self.ctx = ctx()
+        b = layout.blocks
+        dev = torch.device("cuda", torch.cuda.current_device())
+        i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)  # noqa: E731
+        self.A_loc = DeviceCsr.from_scipy(b["A_loc"])
+        self.A_cf_loc = DeviceCsr.from_scipy(b["A_cf_loc"])
+        self.A_fc_loc = DeviceCsr.from_scipy(b["A_fc_loc"])
+        self.A_ff_own = DeviceCsr.from_scipy(b["A_ff_own"])
+        self.A_cc_own = DeviceCsr.from_scipy(b["A_cc_own"])
+        e = b["ext"]
+        self.ext = DeviceSystem(*(DeviceCsr.from_scipy(e[n]) for n in ("A_ff", "A_fc", "A_cf", "A_cc")))
+        self.ext.topology = tuple(i32(a) for a in b["ext_topology"])
+        self.own_in_ext = i32(b["own_cells_in_ext"])
+        cm = np.full(layout.ext_cells.size, -1, dtype=np.int32)
+        cm[b["own_cells_in_ext"]] = np.arange(layout.n_cells, dtype=np.int32)
+        self.cell_map = i32(cm)
+        self.send = {("f", q): i32(v) for q, v in layout.send_faces.items()}
+        self.send.update({("c", q): i32(v) for q, v in layout.send_cells.items()})
+        self.rhs = torch.from_numpy(b["rhs"]).to(dev)
+        nfo, nco = layout.n_faces, layout.n_cells
+        nhf, nhc = layout.halo_faces.size, layout.halo_cells.size
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.zext = torch.zeros(nfo + nco + nhf + nhc, **f64)      # [own | halo f | halo c]
+        self.tf_ext = torch.zeros(nfo + nhf, **f64)
+        self.yc_ext = torch.zeros(nco + nhc, **f64)
+        self.uc = torch.zeros(max(nco, 1), **f64)
+        self.af = torch.zeros(max(nfo, 1), **f64)
+        self.ic = self.ilu = None
+        self.s1 = None
+
+    # -- setup ------------------------------------------------------------
+    def build(self) -> None:
+        """Stage 1 on the extended subsystem, block-Jacobi stage 2 + factors."""
+        from .device import DeviceCsr
+        from .patterns import static_patterns_device
+        from .precond import build_stage1
+        o = self.opts
+        lib, c = self.lib, self.ctx
+        if o["dynamic"] is not None:
+            s1 = build_stage1(self.ext, dynamic=o["dynamic"], tau_filt=o["tau_filt"],
+                              filtration=o["filtration"], face_drop_tol=o["face_drop_tol"], no_fill=o["no_fill"])
+        else:
+            pats = (static_patterns_device(self.ext.topology, o["prototype"]) if o["kind"] == "static"
+                    else None)
+            if pats is None:
+                from .patterns import base_pattern
+                pats = base_pattern(self.ext.A_cf)
+            s1 = build_stage1(self.ext, patterns=pats, tau_filt=o["tau_filt"], filtration=o["filtration"],
+                              face_drop_tol=o["face_drop_tol"], no_fill=o["no_fill"])
+        self.s1 = s1
+        H = s1._part(L.S1_H)
+        lay = self.layout
+        h = C.c_void_p()
+        L.check(lib.edfa_csr_submatrix(c, H.handle, lay.n_cells, C.c_void_p(self.own_in_ext.data_ptr()),
+                                       C.c_void_p(self.cell_map.data_ptr()), lay.n_cells, C.byref(h)))
+        H_own = DeviceCsr(h)
+        tau = o["tau_filt"] if o["filtration"] == "post-schur" else 0.0
+        h = C.c_void_p()
+        L.check(lib.edfa_csr_sub(c, self.A_cc_own.handle, H_own.handle, tau, C.byref(h)))
+        self.S_own = DeviceCsr(h)
+        if not o["no_fill"]:
+            raise L.EdfaUnsupported("inner factorisations with fill-in are not implemented on the GPU path")
+        nx, ny, _ = lay.nxyz
+        self._free_factors()
+        f = C.c_void_p()
+        L.check(lib.edfa_factor_ilu0(c, self.S_own.handle, o["schur_drop_tol"], nx, ny, lay.k1 - lay.k0,
+                                     C.byref(f)))
+        self.ilu = f
+        f = C.c_void_p()
+        L.check(lib.edfa_factor_ic0(c, self.A_ff_own.handle, o["face_drop_tol"], C.byref(f)))
+        self.ic = f
+
+    def _free_factors(self):
+        for name in ("ic", "ilu"):
+            f = getattr(self, name, None)
+            if f:
+                L.check(self.lib.edfa_factor_destroy(f))
+                setattr(self, name, None)
+
+    def __del__(self):
+        try:
+            if L._lib is not None:
+                self._free_factors()
+        except Exception:   # pragma: no cover
+            pass
+
+    # -- vector kernels ----------------------------------------------------
+    def empty(self, *shape):
+        return torch.empty(*shape, dtype=torch.float64, device=self.rhs.device)
+
+    def gather(self, src, kind, q):
+        idx = self.send[(kind, q)]
+        out = self.empty(idx.numel())
+        L.check(self.lib.edfa_gather(self.ctx, idx.numel(), C.c_void_p(idx.data_ptr()),
+                                     C.c_void_p(src.data_ptr()), C.c_void_p(out.data_ptr())))
+        return out
+
+    def multidot(self, V, nvec, w, out):
+        n = self.layout.n_own
+        L.check(self.lib.edfa_multidot(self.ctx, n, nvec, C.c_void_p(V.data_ptr()), V.stride(0),
+                                       C.c_void_p(w.data_ptr()), C.c_void_p(out.data_ptr())))
+
+    def multiaxpy(self, V, nvec, h, w_in, out, norm2):
+        n = self.layout.n_own
+        L.check(self.lib.edfa_multiaxpy(self.ctx, n, nvec, C.c_void_p(V.data_ptr()), V.stride(0),
+                                        C.c_void_p(h.data_ptr()), 1.0,
+                                        None if w_in is None else C.c_void_p(w_in.data_ptr()),
+                                        C.c_void_p(out.data_ptr()),
+                                        None if norm2 is None else C.c_void_p(norm2.data_ptr())))
+
+    def axpby(self, a, x, b, y):
+        L.check(self.lib.edfa_axpby(self.ctx, y.numel(), a, C.c_void_p(x.data_ptr()), b,
+                                    C.c_void_p(y.data_ptr())))
+
+    def copy(self, src, dst):
+        self.axpby(1.0, src, 0.0, dst)
+
+    # -- operator pieces ---------------------------------------------------
+    def spmv_ext(self, y):
+        """y = A_loc zext (zext's own part and halo already in place)."""
+        L.check(self.lib.edfa_spmv(self.ctx, self.A_loc.handle, C.c_void_p(self.zext.data_ptr()),
+                                   C.c_void_p(y.data_ptr()), 1.0, 0.0))
+
+    def apply_faces(self, r):
+        """t_f = -(L L^T)^-1 r_f into tf_ext[:nfo]."""
+        nfo = self.layout.n_faces
+        if nfo:
+            L.check(self.lib.edfa_factor_solve(self.ctx, self.ic, C.c_void_p(r.data_ptr()), -1.0,
+                                               C.c_void_p(self.tf_ext.data_ptr())))
+
+    def apply_cells(self, r):
+        """y_c = (L U)^-1 (r_c - A_cf t_f) into yc_ext[:nco]."""
+        nfo, nco = self.layout.n_faces, self.layout.n_cells
+        if not nco:
+            return
+        rc = r[nfo:]
+        self.copy(rc, self.uc[:nco])
+        L.check(self.lib.edfa_spmv(self.ctx, self.A_cf_loc.handle, C.c_void_p(self.tf_ext.data_ptr()),
+                                   C.c_void_p(self.uc.data_ptr()), -1.0, 1.0))
+        L.check(self.lib.edfa_factor_solve(self.ctx, self.ilu, C.c_void_p(self.uc.data_ptr()), 1.0,
+                                           C.c_void_p(self.yc_ext.data_ptr())))
+
+    def apply_finish(self, y):
+        """y = [t_f + (L L^T)^-1 A_fc y_c ; y_c]."""
+        nfo, nco = self.layout.n_faces, self.layout.n_cells
+        if nfo:
+            L.check(self.lib.edfa_spmv(self.ctx, self.A_fc_loc.handle, C.c_void_p(self.yc_ext.data_ptr()),
+                                       C.c_void_p(self.af.data_ptr()), 1.0, 0.0))
+            L.check(self.lib.edfa_factor_solve(self.ctx, self.ic, C.c_void_p(self.af.data_ptr()), 1.0,
+                                               C.c_void_p(y.data_ptr())))
+            self.axpby(1.0, self.tf_ext[:nfo], 1.0, y[:nfo])
+        if nco:
+            self.copy(self.yc_ext[:nco], y[nfo:nfo + nco])
+
+
+# ---------------------------------------------------------------------------
+# distributed operator + GMRES
+
+class SlabOperator:
+    """The block operator and the EDFA preconditioner over a set of slabs."""
+
+    def __init__(self, parts, comm):
+        self.parts = parts
+        self.comm = comm
+        self.halo = HaloExchange(parts, comm)
+
+    def _own_views(self, vecs, kind):
+        out = []
+        for p, v in zip(self.parts, vecs):
+            nfo = p.layout.n_faces
+            out.append(v[:nfo] if kind == "f" else v[nfo:p.layout.n_own])
+        return out
+
+    def precond_into_zext(self, rs):
+        """zext[:n_own] = P^-1 r per part (two halo exchanges)."""
+        for p, r in zip(self.parts, rs):
+            p.apply_faces(r)
+        self.halo.run("f", [p.tf_ext[:p.layout.n_faces] for p in self.parts],
+                      [p.tf_ext[p.layout.n_faces:] for p in self.parts])
+        for p, r in zip(self.parts, rs):
+            p.apply_cells(r)
+        self.halo.run("c", [p.yc_ext[:p.layout.n_cells] for p in self.parts],
+                      [p.yc_ext[p.layout.n_cells:] for p in self.parts])
+        for p in self.parts:
+            p.apply_finish(p.zext[:p.layout.n_own])
+
+    def matvec_zext(self, ws):
+        """w = A zext per part (exchanges the halo of zext's own part)."""
+        self.halo.run("f", [p.zext[:p.layout.n_faces] for p in self.parts],
+                      [p.zext[p.layout.n_own:p.layout.n_own + p.layout.halo_faces.size] for p in self.parts])
+        self.halo.run("c", [p.zext[p.layout.n_faces:p.layout.n_own] for p in self.parts],
+                      [p.zext[p.layout.n_own + p.layout.halo_faces.size:] for p in self.parts])
+        for p, w in zip(self.parts, ws):
+            p.spmv_ext(w)
+
+    def allsum(self, partials):
+        t = partials[0]
+        if len(partials) > 1:
+            t = partials[0].clone()
+            for q in partials[1:]:
+                t += q.to(t.device)
+        self.comm.allreduce_(t)
+        return t
+
+
+def slab_gmres(op: SlabOperator, bs, tol=1e-8, restart=50, max_it=2000):
+    """Right-preconditioned restarted GMRES(m) on slab-distributed vectors.
+
+    The same algorithm as the single-device solver (krylov.cu): x0 = 0, CGS
+    Arnoldi with DGKS selective re-orthogonalisation (fused multi-dot +
+    multi-axpy per pass, dot products summed over slabs), Givens rotations on
+    the host, convergence confirmed on the true residual (hx/krylov.py
+    conventions).  Returns (list of local x, SolveReport)."""
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if not 1 <= restart <= 62:
+        raise ValueError("restart must be in [1, 62]")
+    parts = op.parts
+    m = restart
+    rep = SolveReport()
+    hd = [p.empty(192).zero_() for p in parts]
+
+    def global_dot(xs, ys):
+        for p, x, y, h in zip(parts, xs, ys, hd):
+            p.multidot(x.view(1, -1), 1, y, h[128:129])
+        return float(op.allsum([h[128:129] for h in hd]).item())
+
+    bnorm = math.sqrt(global_dot(bs, bs))
+    xs = [p.empty(p.layout.n_own).zero_() for p in parts]
+    if bnorm == 0.0:
+        rep.converged, rep.final_relres = True, 0.0
+        rep.relres_history.append(0.0)
+        return xs, rep
+    V = [p.empty(m + 1, p.layout.n_own) for p in parts]
+    rs = [b.clone() for b in bs]
+    beta = bnorm
+    happy = False
+    while rep.n_it < max_it:
+        for p, v, r in zip(parts, V, rs):
+            p.axpby(1.0 / beta, r, 0.0, v[0])
+        H = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        g[0] = beta
+        k = 0
+        for j in range(m):
+            op.precond_into_zext([v[j] for v in V])
+            op.matvec_zext([v[j + 1] for v in V])
+            rep.n_it += 1
+            ws = [v[j + 1] for v in V]
+            for p, v, w, h in zip(parts, V, ws, hd):
+                p.multidot(v, j + 2, w, h[:j + 2])
+            hsum = op.allsum([h[:j + 2] for h in hd])
+            for p, v, w, h in zip(parts, V, ws, hd):
+                p.multiaxpy(v, j + 1, hsum, w, w, h[64:65])
+            nsum = op.allsum([h[64:65] for h in hd])
+            host = torch.cat([hsum, nsum]).cpu().numpy()
+            w0 = math.sqrt(max(host[j + 1], 0.0))
+            wn = math.sqrt(max(host[j + 2], 0.0))
+            H[:j + 1, j] = host[:j + 1]
+            if wn < 0.7071067811865476 * w0:             # DGKS second pass
+                for p, v, w, h in zip(parts, V, ws, hd):
+                    p.multidot(v, j + 1, w, h[:j + 1])
+                hsum = op.allsum([h[:j + 1] for h in hd])
+                for p, v, w, h in zip(parts, V, ws, hd):
+                    p.multiaxpy(v, j + 1, hsum, w, w, h[64:65])
+                nsum = op.allsum([h[64:65] for h in hd])
+                host = torch.cat([hsum, nsum]).cpu().numpy()
+                H[:j + 1, j] += host[:j + 1]
+                wn = math.sqrt(max(host[j + 1], 0.0))
+            H[j + 1, j] = wn
+            for i in range(j):
+                a, c = H[i, j], H[i + 1, j]
+                H[i, j] = cs[i] * a + sn[i] * c
+                H[i + 1, j] = -sn[i] * a + cs[i] * c
+            den = math.hypot(H[j, j], H[j + 1, j])
+            cs[j], sn[j] = (1.0, 0.0) if den == 0.0 else (H[j, j] / den, H[j + 1, j] / den)
+            H[j, j], H[j + 1, j] = den, 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            est = abs(g[j + 1]) / bnorm
+            rep.relres_history.append(est)
+            k = j + 1
+            if wn == 0.0:
+                happy = True
+                break
+            for p, w in zip(parts, ws):
+                p.axpby(1.0 / wn, w, 0.0, w)
+            if est <= tol or rep.n_it >= max_it:
+                break
+        y = np.zeros(k)
+        for i in range(k - 1, -1, -1):
+            s = g[i] - H[i, i + 1:k] @ y[i + 1:k]
+            y[i] = s / H[i, i] if H[i, i] != 0.0 else 0.0
+        yd = [torch.from_numpy(y.copy()).to(h.device) for h in hd]
+        for p, v, r, yy in zip(parts, V, rs, yd):
+            p.multiaxpy(v, k, yy, None, r, None)                  # r <- V y (scratch)
+        op.precond_into_zext(rs)
+        for p, x in zip(parts, xs):
+            p.axpby(1.0, p.zext[:p.layout.n_own], 1.0, x)
+        for p, x in zip(parts, xs):
+            p.copy(x, p.zext[:p.layout.n_own])
+        op.matvec_zext(rs)
+        for p, r, b in zip(parts, rs, bs):
+            p.axpby(1.0, b, -1.0, r)                              # r = b - A x
+        beta = math.sqrt(global_dot(rs, rs))
+        if beta / bnorm <= tol:
+            rep.converged = True
+            break
+        if happy or beta == 0.0:
+            rep.breakdown = True
+            break
+    rep.final_relres = beta / bnorm
+    if rep.n_it == 0:
+        rep.relres_history.append(beta / bnorm)
+    return xs, rep
+
+
+class SlabSolver:
+    """Build + solve over the slabs this process holds (drop-in counterpart
+    of ``BlockLDUPreconditioner.build`` + ``gmres`` for a partitioned run)."""
+
+    def __init__(self, layouts, comm, **opts):
+        self.layouts = layouts
+        self.comm = comm
+        self.parts = [CudaSlab(lay, **opts) for lay in layouts]
+        self.op = SlabOperator(self.parts, comm)
+
+    def build(self):
+        for p in self.parts:
+            p.build()
+
+    def solve(self, tol=1e-8, restart=50, max_it=2000):
+        return slab_gmres(self.op, [p.rhs for p in self.parts], tol=tol, restart=restart, max_it=max_it)

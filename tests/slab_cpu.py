@@ -1,0 +1,130 @@
+"""CPU stand-in for one slab of the partitioned solver -- TEST INFRASTRUCTURE.
+
+It exposes the same part interface as ``parallel.CudaSlab`` with every
+operation done by the oracle / scipy on torch CPU tensors, so the multi-rank
+driver (``parallel.slab_gmres``, ``HaloExchange``, ``TorchComm``) can be
+exercised with the gloo backend on CPU.  The product path never uses it.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from oracle import edfa_oracle as O
+
+
+def ext_sets(layout, global_sets):
+    """Global restriction sets of the extended cells in ext face numbering
+    (faces outside the extended box dropped)."""
+    pos = np.full(int(max(layout.ext_faces.max(), max((s.max() for s in global_sets if s.size), default=0))) + 1,
+                  -1, dtype=np.int64)
+    pos[layout.ext_faces] = np.arange(layout.ext_faces.size)
+    out = []
+    for c in layout.ext_cells:
+        s = np.asarray(global_sets[c], dtype=np.int64)
+        m = pos[s]
+        out.append(np.sort(m[m >= 0]))
+    return out
+
+
+def ext_stage1(layout, global_sets=None, dynamic=None):
+    e = layout.blocks["ext"]
+    if dynamic is not None:
+        return O.build_stage1(e["A_ff"], e["A_fc"], e["A_cf"], dynamic=dynamic, no_fill=True)
+    return O.build_stage1(e["A_ff"], e["A_fc"], e["A_cf"], sets=ext_sets(layout, global_sets), no_fill=True)
+
+
+class CpuSlab:
+    def __init__(self, layout, global_sets=None, dynamic=None):
+        self.layout = lay = layout
+        b = lay.blocks
+        s1 = ext_stage1(lay, global_sets, dynamic)
+        own = b["own_cells_in_ext"]
+        H = s1.H.tocsr()[own][:, own]
+        self.S_own = O.canonical(b["A_cc_own"] - H)
+        self.ilu = O.ilu(self.S_own, 0.0, no_fill=True)
+        self.ic = O.ic(-b["A_ff_own"], 0.0, no_fill=True)
+        self.A_loc, self.A_cf_loc, self.A_fc_loc = b["A_loc"], b["A_cf_loc"], b["A_fc_loc"]
+        nfo, nco = lay.n_faces, lay.n_cells
+        nhf, nhc = lay.halo_faces.size, lay.halo_cells.size
+        self.zext = torch.zeros(nfo + nco + nhf + nhc, dtype=torch.float64)
+        self.tf_ext = torch.zeros(nfo + nhf, dtype=torch.float64)
+        self.yc_ext = torch.zeros(nco + nhc, dtype=torch.float64)
+        self.rhs = torch.from_numpy(b["rhs"].copy())
+
+    def empty(self, *shape):
+        return torch.empty(*shape, dtype=torch.float64)
+
+    def gather(self, src, kind, q):
+        idx = self.layout.send_faces[q] if kind == "f" else self.layout.send_cells[q]
+        return src[torch.from_numpy(idx)].clone()
+
+    def multidot(self, V, nvec, w, out):
+        out[:nvec] = torch.from_numpy(V[:nvec].numpy() @ w.numpy())
+
+    def multiaxpy(self, V, nvec, h, w_in, out, norm2):
+        acc = h[:nvec].numpy() @ V[:nvec].numpy()
+        o = acc if w_in is None else w_in.numpy() - acc
+        out.copy_(torch.from_numpy(o))
+        if norm2 is not None:
+            norm2[0] = float(o @ o)
+
+    def axpby(self, a, x, b, y):
+        y.copy_(a * x if b == 0.0 else a * x + b * y)
+
+    def copy(self, src, dst):
+        dst.copy_(src)
+
+    def spmv_ext(self, y):
+        y.copy_(torch.from_numpy(self.A_loc @ self.zext.numpy()))
+
+    def apply_faces(self, r):
+        nfo = self.layout.n_faces
+        self.tf_ext[:nfo] = torch.from_numpy(-self.ic.apply(r[:nfo].numpy()))
+
+    def apply_cells(self, r):
+        nfo, nco = self.layout.n_faces, self.layout.n_cells
+        u = r[nfo:nfo + nco].numpy() - self.A_cf_loc @ self.tf_ext.numpy()
+        self.yc_ext[:nco] = torch.from_numpy(self.ilu.apply(u))
+
+    def apply_finish(self, y):
+        nfo, nco = self.layout.n_faces, self.layout.n_cells
+        a = self.A_fc_loc @ self.yc_ext.numpy()
+        y[:nfo] = torch.from_numpy(self.tf_ext[:nfo].numpy() + self.ic.apply(a))
+        y[nfo:nfo + nco] = self.yc_ext[:nco]
+
+
+def block_jacobi_reference(system, layouts, global_sets=None, dynamic=None, tol=1e-8, restart=50):
+    """The oracle's EDFA with slab-block-diagonal inner factors (what the
+    partitioned solver computes), solved with the oracle's GMRES."""
+    A_ff, A_fc, A_cf, A_cc = (sp.csr_matrix(getattr(system, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc"))
+    if dynamic is not None:
+        s1 = O.build_stage1(A_ff, A_fc, A_cf, dynamic=dynamic, no_fill=True)
+    else:
+        s1 = O.build_stage1(A_ff, A_fc, A_cf, sets=global_sets, no_fill=True)
+    fpart = np.empty(A_ff.shape[0], dtype=np.int64)
+    cpart = np.empty(A_cc.shape[0], dtype=np.int64)
+    for lay in layouts:
+        fpart[lay.own_faces] = lay.rank
+        cpart[lay.own_cells] = lay.rank
+
+    def mask(M, p):
+        M = sp.coo_matrix(M)
+        keep = p[M.row] == p[M.col]
+        return O.canonical(sp.coo_matrix((M.data[keep], (M.row[keep], M.col[keep])), shape=M.shape))
+
+    S_bj = mask(O.canonical(A_cc - s1.H), cpart)
+    ilu = O.ilu(S_bj, 0.0, no_fill=True)
+    ic = O.ic(-mask(A_ff, fpart), 0.0, no_fill=True)
+    nf = A_ff.shape[0]
+
+    def P(r):
+        t_f = -ic.apply(r[:nf])
+        t_c = ilu.apply(r[nf:] - A_cf @ t_f)
+        return np.concatenate([t_f + ic.apply(A_fc @ t_c), t_c])
+
+    A = system.full_matrix()
+    x, rep = O.gmres(lambda v: A @ v, P, system.rhs(), tol=tol, restart=restart)
+    return x, rep, S_bj
