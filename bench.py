@@ -78,6 +78,8 @@ class ClockSampler:
         self.f = None
 
     def __enter__(self):
+        if os.environ.get("EDFA_BENCH_NO_CLOCKS"):
+            return self
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -214,6 +216,19 @@ def run_edfa(args):
     from paper_2009_13916_b200.precond import BlockLDUPreconditioner, patterns_for
 
     lib = _lib.lib()
+    diag = []
+    if os.environ.get("EDFA_BENCH_DIAG"):      # slow-call tracer (diagnostics only)
+        for _name in _lib._SIGS:
+            _fn = getattr(lib, _name)
+
+            def _w(*a, _fn=_fn, _name=_name):
+                t = time.perf_counter()
+                r = _fn(*a)
+                dt = time.perf_counter() - t
+                if dt > 0.03:
+                    diag.append((_name, round(dt * 1e3, 1)))
+                return r
+            setattr(lib, _name, _w)
     case = configs.config2(n=args.n)
     s = case.system
     N = s.n_unknowns
@@ -271,6 +286,9 @@ def run_edfa(args):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             reps.append(rep)
+            if diag:
+                print("diag step", len(times), times[-1], diag, file=sys.stderr, flush=True)
+                diag.clear()
     launches = lib.edfa_ctx_launch_count(c) - launches0
     prof = report(c)
     lib.edfa_ctx_profile(c, 0)
@@ -336,7 +354,7 @@ def run_edfa(args):
                    "n_free_faces": s.n_free_faces, "n_cells": s.n_cells, "rtol": case.rtol,
                    "restart": case.restart, "gmres_iterations": reps[-1].n_it,
                    "final_true_relres": reps[-1].final_relres, "host_check_relres": relres_host,
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": "single", "step_ms": [round(t, 3) for t in times],
                    "l2": "inputs larger than L2 and a 256 MiB L2 flush between steps"},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "seconds_per_step": statistics.median(e2e_times)},
@@ -441,6 +459,9 @@ def run_slabs(args):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             reps.append(rep)
+            if diag:
+                print("diag step", len(times), times[-1], diag, file=sys.stderr, flush=True)
+                diag.clear()
     launches = lib.edfa_ctx_launch_count(c) - launches0
     prof = report(c)
     lib.edfa_ctx_profile(c, 0)

@@ -6,20 +6,82 @@
 
 namespace edfa {
 
+double slow_log_ms() {
+    static const double v = [] {
+        const char* e = getenv("EDFA_SLOW_LOG");
+        return e ? atof(e) : 0.0;
+    }();
+    return v;
+}
+void slow_log(double ms, const char* what, const char* file, int line) {
+    fprintf(stderr, "[edfa slow] %8.2f ms  %s:%d  %s\n", ms, file, line, what);
+}
+
+namespace {
+constexpr size_t CACHE_LIMIT = size_t(48) << 30;   // trim when the idle cache exceeds this
+
+size_t round_block(size_t bytes) {
+    if (bytes <= (size_t(1) << 20)) return (bytes + 511) & ~size_t(511);
+    return (bytes + (size_t(1) << 20) - 1) & ~((size_t(1) << 20) - 1);
+}
+}  // namespace
+
+void Ctx::trim_cache() {
+    std::lock_guard<std::mutex> lk(alloc_mu);
+    if (free_blocks.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (auto& kv : free_blocks) {
+        block_size.erase(kv.second);
+        cudaFree(kv.second);
+    }
+    free_blocks.clear();
+    cached_bytes = 0;
+}
+
 void* Ctx::alloc(size_t bytes) {
     if (bytes == 0) return nullptr;
+    const size_t sz = round_block(bytes);
+    {
+        std::lock_guard<std::mutex> lk(alloc_mu);
+        auto it = free_blocks.lower_bound(sz);
+        if (it != free_blocks.end() && it->first <= sz + sz / 8 + (size_t(1) << 20)) {
+            void* p = it->second;
+            cached_bytes -= it->first;
+            free_blocks.erase(it);
+            return p;
+        }
+    }
     void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, (bytes + 255) & ~size_t(255), stream);
+    const double lim = slow_log_ms(), t0 = lim > 0 ? host_ms() : 0.0;
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e != cudaSuccess) {                 // give the cache back and retry once
+        cudaGetLastError();
+        trim_cache();
+        e = cudaMalloc(&p, sz);
+    }
+    if (lim > 0 && host_ms() - t0 > lim) slow_log(host_ms() - t0, "cudaMalloc", __FILE__, __LINE__);
     if (e != cudaSuccess) {
         cudaGetLastError();
         throw Error(EDFA_ERR_CUDA, std::string("device allocation of ") + std::to_string(bytes) +
                                        " bytes failed: " + cudaGetErrorString(e));
     }
+    std::lock_guard<std::mutex> lk(alloc_mu);
+    block_size[p] = sz;
     return p;
 }
 
 void Ctx::free(void* p) {
-    if (p) cudaFreeAsync(p, stream);
+    if (!p) return;
+    bool trim = false;
+    {
+        std::lock_guard<std::mutex> lk(alloc_mu);
+        auto it = block_size.find(p);
+        if (it == block_size.end()) return;   // not ours
+        free_blocks.emplace(it->second, p);   // reusable in stream order
+        cached_bytes += it->second;
+        trim = cached_bytes > CACHE_LIMIT;
+    }
+    if (trim) trim_cache();
 }
 
 void* Ctx::cub_scratch(size_t bytes) {
@@ -89,12 +151,6 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
     auto* h = new edfa_ctx();
     h->c.device = device;
     h->c.stream = static_cast<cudaStream_t>(stream);
-    // keep freed memory in the stream-ordered pool between steps
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
     h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
     h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));
     EDFA_CUDA(cudaMallocHost(&h->c.h_pinned, 4096 * sizeof(double)));
@@ -105,7 +161,12 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
 int edfa_ctx_set_stream(edfa_ctx* ctx, void* stream) {
     API_BEGIN
     require(ctx, EDFA_ERR_VALUE, "ctx is NULL");
-    ctx->c.stream = static_cast<cudaStream_t>(stream);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (s != ctx->c.stream) {
+        // cached blocks are recycled in the order of one stream: drain it first
+        EDFA_CUDA(cudaStreamSynchronize(ctx->c.stream));
+        ctx->c.stream = s;
+    }
     API_END
 }
 
@@ -127,6 +188,7 @@ int edfa_ctx_destroy(edfa_ctx* ctx) {
     c.free(c.d_scalar_d);
     cudaFreeHost(c.h_pinned);
     cudaStreamSynchronize(c.stream);
+    c.trim_cache();
     delete ctx;
     API_END
 }

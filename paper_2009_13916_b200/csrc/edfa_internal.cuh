@@ -1,5 +1,9 @@
 // Internal declarations shared by the libedfa translation units.
 #pragma once
+#include <chrono>
+#include <unordered_map>
+#include <mutex>
+#include <map>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,9 +26,23 @@ struct Error : std::runtime_error {
     Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
+// EDFA_SLOW_LOG=<ms>: report runtime calls that block the host longer than
+// that (diagnostics for host stalls inside the driver)
+double slow_log_ms();
+void slow_log(double ms, const char* what, const char* file, int line);
+inline double host_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 #define EDFA_CUDA(call)                                                          \
     do {                                                                         \
+        const double lim_ = ::edfa::slow_log_ms();                               \
+        const double t0_ = lim_ > 0 ? ::edfa::host_ms() : 0.0;                   \
         cudaError_t e_ = (call);                                                 \
+        if (lim_ > 0) {                                                          \
+            double dt_ = ::edfa::host_ms() - t0_;                                \
+            if (dt_ > lim_) ::edfa::slow_log(dt_, #call, __FILE__, __LINE__);    \
+        }                                                                        \
         if (e_ != cudaSuccess)                                                   \
             throw ::edfa::Error(EDFA_ERR_CUDA, std::string(#call ": ") +         \
                                                   cudaGetErrorString(e_));       \
@@ -57,9 +75,17 @@ struct Ctx {
     int* d_scalar_i = nullptr;     // small device int scratch (64 ints)
     double* d_scalar_d = nullptr;  // small device double scratch (4096 doubles)
     double* h_pinned = nullptr;    // pinned host scratch (4096 doubles)
+    // caching allocator: device blocks are recycled in stream order on this
+    // context's stream and only returned to the driver when the cache is
+    // trimmed (driver allocation calls can block the host for a long time)
+    std::multimap<size_t, void*> free_blocks;
+    std::unordered_map<void*, size_t> block_size;
+    size_t cached_bytes = 0;
+    std::mutex alloc_mu;
 
     void* alloc(size_t bytes);
     void free(void* p);
+    void trim_cache();             // synchronises the stream, releases cached blocks
     void* cub_scratch(size_t bytes);
     cudaEvent_t get_event();
     void flush_profile();

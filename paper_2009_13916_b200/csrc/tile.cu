@@ -26,6 +26,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -669,10 +671,26 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
 template <int EK>
 static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
     auto kern = k_tile_solve<EK>;
-    EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TILE_THREADS, smem));
-    int grid = NUM_SMS_B200 * std::max(1, std::min(occ, 2));
+    // attribute + occupancy once per (kernel, smem): these are driver calls,
+    // kept off the per-solve path
+    static std::mutex mu;
+    static std::map<size_t, int> grids;
+    static size_t smem_set = 0;
+    int grid;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = grids.find(smem);
+        if (it == grids.end()) {
+            if (smem > smem_set) {
+                EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                smem_set = smem;
+            }
+            int occ = 0;
+            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TILE_THREADS, smem));
+            it = grids.emplace(smem, NUM_SMS_B200 * std::max(1, std::min(occ, 2))).first;
+        }
+        grid = it->second;
+    }
     a.ticket_base = tp.ticket_base;
     tp.ticket_base += tp.n_tiles + grid;   // every CTA takes exactly one failing ticket
     void* args[] = {&a};

@@ -68,24 +68,28 @@ class InnerFactorization:
 
     def __init__(self, kind, owner, part_L, part_U, nnz_stored, shifts, levels):
         self.kind = kind
-        self._owner = owner          # Stage1 / Stage2 keeping the handle alive
+        # Stage1 / Stage2 keeping the handle alive.  The owner does not hold
+        # this object (it is made on access), so there is no reference cycle
+        # and device memory is released as soon as the stage is dropped.
+        self._owner = owner
         self._parts = (part_L, part_U)
         self._nnz_stored = nnz_stored
         self.pivot_shifts = shifts
         self.levels = levels
-        self._cache = {}
+        self._cache = owner._cache
 
     @property
     def nnz_stored(self) -> int:
         return self._nnz_stored
 
     def _export(self, which):
-        if which not in self._cache:
+        key = (self.kind, which)
+        if key not in self._cache:
             if self.kind == "ic" and which == 1:
-                self._cache[1] = self.L.T.tocsr()
+                self._cache[key] = self.L.T.tocsr()
             else:
-                self._cache[which] = self._owner._part(self._parts[which]).to_scipy()
-        return self._cache[which]
+                self._cache[key] = self._owner._part(self._parts[which]).to_scipy()
+        return self._cache[key]
 
     @property
     def L(self):
@@ -118,11 +122,13 @@ class Stage1:
         L.check(L.lib().edfa_stage1_info_get(handle, C.byref(info)))
         self.info = info
         self._cache = {}
-        n = system.n_free_faces
-        nL = info.nnz_L
-        self.face_inner = InnerFactorization("ic", self, L.S1_L, None, 2 * nL - n, info.pivot_shifts,
-                                             info.trsv_levels)
         self._sets = sets
+
+    @property
+    def face_inner(self) -> InnerFactorization:
+        n = self.system.n_free_faces
+        return InnerFactorization("ic", self, L.S1_L, None, 2 * self.info.nnz_L - n, self.info.pivot_shifts,
+                                  self.info.trsv_levels)
 
     def _part(self, which) -> DeviceCsr:
         h = C.c_void_p()
@@ -174,11 +180,14 @@ class Stage2:
         info = L.Stage2Info()
         L.check(L.lib().edfa_stage2_info_get(handle, C.byref(info)))
         self.info = info
-        n = stage1.system.n_cells
-        self.schur_inner = InnerFactorization("ilu", self, L.S2_L, L.S2_U,
-                                              info.nnz_L - n + info.nnz_U, info.pivot_shifts,
-                                              (info.levels_L, info.levels_U))
         self._cache = {}
+
+    @property
+    def schur_inner(self) -> InnerFactorization:
+        n = self.stage1.system.n_cells
+        i = self.info
+        return InnerFactorization("ilu", self, L.S2_L, L.S2_U, i.nnz_L - n + i.nnz_U, i.pivot_shifts,
+                                  (i.levels_L, i.levels_U))
 
     def _part(self, which) -> DeviceCsr:
         h = C.c_void_p()

@@ -407,3 +407,23 @@ def test_tile_solver_matches_level_solver(edfa, idx, n):
         r = np.random.default_rng(3).standard_normal(s.n_unknowns)
         ys.append(pre.apply(r))
     assert np.abs(ys[0] - ys[1]).max() <= 1e-12 * np.abs(ys[1]).max()
+
+
+def test_stages_freed_without_cycle_collection(edfa):
+    """Dropping a preconditioner releases its device objects at once (no
+    reference cycles), so repeated builds reuse the memory pool instead of
+    growing it."""
+    import gc
+    import weakref
+    from paper_2009_13916_b200 import configs
+    s = configs.config2(n=6).system
+    ds = edfa.DeviceSystem.from_host(s)
+    gc.disable()
+    try:
+        pre = edfa.BlockLDUPreconditioner.build(ds, patterns=edfa.patterns_for(ds, "static", "A"), no_fill=True)
+        _ = pre.stage1.face_inner.nnz_stored + pre.stage2.schur_inner.nnz_stored
+        r1, r2 = weakref.ref(pre.stage1), weakref.ref(pre.stage2)
+        del pre, _
+        assert r1() is None and r2() is None
+    finally:
+        gc.enable()
