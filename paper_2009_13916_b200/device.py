@@ -235,3 +235,32 @@ class SystemOperator:
 
 def system_operator(system) -> SystemOperator:
     return SystemOperator(system if isinstance(system, DeviceSystem) else DeviceSystem.from_host(system))
+
+
+def pinned_copy(system):
+    """Copy of a BlockSystem whose block arrays and right-hand side live in
+    page-locked host memory, so ``DeviceSystem.from_host`` uploads them by DMA
+    at full PCIe/C2C bandwidth (the staging a host application keeps between
+    time steps).  Grid/topology fields are shared, not copied."""
+    import dataclasses
+
+    def pin(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t.numpy()
+
+    def pin_csr(M):
+        M = sp.csr_matrix(M)
+        return sp.csr_matrix((pin(M.data), pin(M.indices.astype(np.int32, copy=False)),
+                              pin(M.indptr.astype(np.int32, copy=False))), shape=M.shape, copy=False)
+
+    repl = {n: pin_csr(getattr(system, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc")}
+    for n in ("rhs_f", "rhs_c"):
+        if hasattr(system, n):
+            repl[n] = pin(getattr(system, n))
+    if dataclasses.is_dataclass(system):
+        return dataclasses.replace(system, **repl)
+    import copy
+    out = copy.copy(system)
+    for k, v in repl.items():
+        setattr(out, k, v)
+    return out

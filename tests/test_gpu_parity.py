@@ -427,3 +427,19 @@ def test_stages_freed_without_cycle_collection(edfa):
         assert r1() is None and r2() is None
     finally:
         gc.enable()
+
+
+def test_pinned_copy_roundtrip(edfa):
+    from paper_2009_13916_b200 import configs
+    from paper_2009_13916_b200.device import pinned_copy
+    s = configs.config2(n=6).system
+    sp_ = pinned_copy(s)
+    for n in ("A_ff", "A_fc", "A_cf", "A_cc"):
+        assert same_csr(getattr(s, n), getattr(sp_, n))
+        assert np.array_equal(getattr(s, n).data, getattr(sp_, n).data)
+    assert np.array_equal(s.rhs(), sp_.rhs())
+    ds = edfa.DeviceSystem.from_host(sp_)
+    pre = edfa.BlockLDUPreconditioner.build(ds, patterns=edfa.patterns_for(ds, "static", "A"), no_fill=True)
+    x, rep = edfa.gmres(edfa.system_operator(ds), pre, sp_.rhs(), tol=1e-8)
+    assert rep.converged
+    assert np.linalg.norm(s.rhs() - s.full_matrix() @ x) <= 1e-8 * np.linalg.norm(s.rhs()) * 1.0001
