@@ -66,6 +66,8 @@ struct TilePlan {               // tile-DAG solves of cell-indexed factors (tile
     DevBuf<int32_t> hdr, row_id, ext_id, up_cnt, up_ids, flags, ticket, order;
     DevBuf<short> lev_ptr, dslot, eslot;     // critical / early dependency slots
     DevBuf<double> dcoef, ecoef, dinv;       // critical / early coefficients
+    DevBuf<short> xlev_ptr;                  // externals first needed below level l: [0, xlev_ptr[l])
+    DevBuf<unsigned char> req;               // [LC][32]: upstream levels needed before loading level l
     int32_t epoch = 0, ticket_base = 0;
 };
 // dims = {nx, ny, nz} of the cell grid (rows = cells in natural order) or NULL

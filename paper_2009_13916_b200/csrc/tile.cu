@@ -101,6 +101,9 @@ struct TileBuild {
     int* err;
     int* max_early;       // count-only pass: max early deps of a row (sizes EK)
     bool count_only;
+    int* glev;            // local level of every row (written by the count pass)
+    short* xlev_ptr;      // LC per tile: externals first needed below level l
+    unsigned char* req;   // LC*32 per tile: upstream progress needed to load externals < l+1
 };
 
 __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
@@ -138,6 +141,7 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
         if (!__syncthreads_or(changed)) break;
     }
     if (b.count_only) {   // early deps = all but the intra-tile ones on the previous level
+        for (int r = threadIdx.x; r < n; r += blockDim.x) b.glev[cell[r]] = lev[r];
         for (int r = threadIdx.x; r < n; r += blockDim.x) {
             int ne_r = 0;
             for (int e = b.D.ptr[cell[r]]; e < b.D.ptr[cell[r] + 1]; ++e) {
@@ -226,14 +230,79 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
         }
     }
     __syncthreads();
+    __shared__ int upl[32];   // compacted upstream list
     if (threadIdx.x == 0) {
         int nu = 0;
         int* up = b.up_ids + (size_t)t * 32;
         for (int z = 0; z < 32; ++z)
-            if (ups[z] >= 0) up[nu++] = ups[z];
+            if (ups[z] >= 0) { upl[nu] = ups[z]; up[nu++] = ups[z]; }
+        for (int z = nu; z < 32; ++z) upl[z] = -1;
         b.up_cnt[t] = nu;
     }
-    for (int q = threadIdx.x; q < ne; q += blockDim.x) b.ext_id[(size_t)t * b.EC + q] = ext[q];
+    // externals ordered by the first local level that needs them (pipelined
+    // loading); fn[q] = min level of a consumer row of ext[q]
+    int* fn = misc + 8 + HS;                          // EC
+    int* npos = fn + b.EC;                            // EC: id-sorted index -> need-sorted index
+    int* reqs = npos + b.EC;                          // LC*32
+    for (int q = threadIdx.x; q < ne; q += blockDim.x) fn[q] = INT32_MAX;
+    for (int q = threadIdx.x; q < b.LC * 32; q += blockDim.x) reqs[q] = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        int row = cell[r];
+        for (int e = b.D.ptr[row]; e < b.D.ptr[row + 1]; ++e) {
+            int j = b.D.idx[e];
+            if (g.tile_of(j) == t) continue;
+            int lo = 0, hi = ne;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (ext[mid] < j) lo = mid + 1;
+                else hi = mid;
+            }
+            atomicMin(&fn[lo], lev[r]);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < np2; q += blockDim.x) srt[q] = q < ne ? (fn[q] << 12) | q : INT32_MAX;
+    __syncthreads();
+    for (int k = 2; k <= np2; k <<= 1)
+        for (int jx = k >> 1; jx > 0; jx >>= 1) {
+            for (int q = threadIdx.x; q < np2; q += blockDim.x) {
+                int l = q ^ jx;
+                if (l > q) {
+                    int x0 = srt[q], x1 = srt[l];
+                    if ((x0 > x1) == ((q & k) == 0)) { srt[q] = x1; srt[l] = x0; }
+                }
+            }
+            __syncthreads();
+        }
+    for (int p = threadIdx.x; p < ne; p += blockDim.x) npos[srt[p] & 4095] = p;
+    __syncthreads();
+    for (int q = threadIdx.x; q < ne; q += blockDim.x) {
+        b.ext_id[(size_t)t * b.EC + npos[q]] = ext[q];
+        const int u = g.tile_of(ext[q]);
+        int ui = 0;
+        while (ui < 31 && upl[ui] != u) ++ui;
+        const int need = b.glev[ext[q]] + 1;
+        if (need > 255) atomicExch(b.err, 12);
+        if (fn[q] < b.LC) atomicMax(&reqs[fn[q] * 32 + ui], need);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {            // cumulative over levels, per upstream tile
+        int m = 0;
+        unsigned char* rq = b.req + (size_t)t * b.LC * 32;
+        for (int l = 0; l < b.LC; ++l) {
+            m = max(m, reqs[l * 32 + threadIdx.x]);
+            rq[l * 32 + threadIdx.x] = (unsigned char)m;
+        }
+    }
+    if (threadIdx.x == 0) {            // xlev_ptr[l] = #externals with fn < l
+        short* xl = b.xlev_ptr + (size_t)t * b.LC;
+        int q = 0;
+        for (int l = 0; l < b.LC; ++l) {
+            while (q < ne && (srt[q] >> 12) < l) ++q;
+            xl[l] = (short)q;
+        }
+    }
     // records: critical deps = rows of the immediately preceding local level
     const int ZSLOT = b.RC + b.EC;   // a shared-memory x slot that stays 0
     for (int p = threadIdx.x; p < n; p += blockDim.x) {
@@ -262,7 +331,7 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
                     if (ext[mid] < j) lo = mid + 1;
                     else hi = mid;
                 }
-                slot = b.RC + lo;
+                slot = b.RC + npos[lo];
             }
             if (critical) {
                 if (nc >= CK) { atomicExch(b.err, 10); continue; }
@@ -313,6 +382,9 @@ struct TileSolve {
     double* out2;
     int* err;
     long long* dbg;
+    const short* xlev_ptr;
+    const unsigned char* req;
+    int mode;             // EDFA_TILE_MODE experiment bits (diagnostics)
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -548,13 +620,238 @@ __global__ void __launch_bounds__(TILE_THREADS) k_tile_solve(TileSolve a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Pipelined tile solve: a tile starts as soon as its first levels' external
+// dependencies exist instead of after its upstream tiles have finished.
+//   * compute warps (6): the pipelined level sweep of k_tile_solve; critical
+//     lanes also store every finished row to HBM (x is SENTINEL-filled before
+//     the launch, so a stored value is its own "ready" flag);
+//   * loader warp: polls the external values in need order (relaxed loads,
+//     sentinel = not produced yet) and copies them into shared memory,
+//     publishing how many local levels have all their externals.
+// A downstream tile therefore runs a few levels behind its upstream tiles (a
+// wavefront): the critical path is ~ the row DAG depth plus one L2 round
+// trip per tile boundary, with no flag, fence or publisher on the way.
+constexpr int PIPE_THREADS = TILE_THREADS + 32;
+constexpr int LOADER_WARP = TILE_THREADS / 32;
+
+__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(TILE_THREADS) : "memory"); }
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_d(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return __longlong_as_double((long long)v);
+}
+
+template <int EK>
+__global__ void __launch_bounds__(PIPE_THREADS) k_tile_pipe(TileSolve a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    double* xs = reinterpret_cast<double*>(sm);                     // RC + EC + 2
+    double* cc = xs + a.RC + a.EC + 2;                              // RC*CK
+    double* ecf = cc + (size_t)a.RC * CK;                           // RC*EK
+    double* di = ecf + (size_t)a.RC * EK;                           // RC
+    int* rid = reinterpret_cast<int*>(di + a.RC);                   // RC
+    int* eid_s = rid + a.RC;                                        // EC (external row ids, need-sorted)
+    short* cs = reinterpret_cast<short*>(eid_s + a.EC);             // RC*CK
+    short* es = cs + (size_t)a.RC * CK;                             // RC*EK
+    short* lp = es + (size_t)a.RC * EK;                             // LC
+    short* xl = lp + a.LC;                                          // LC
+    __shared__ int s_tile, s_hdr[4], s_ready;
+    __shared__ __align__(8) uint64_t mbar;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&mbar)), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned phase = 0;
+    const int warp = threadIdx.x >> 5, lane32 = threadIdx.x & 31;
+    const bool crit = threadIdx.x < ROLE;
+    const int lane = crit ? threadIdx.x : (threadIdx.x - ROLE) >> 1;
+    const int li = (threadIdx.x - ROLE) & 1;
+    constexpr int KH = EK / 2;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            int k = atomicAdd(a.ticket, 1) - a.ticket_base;
+            int t = k < a.n_tiles ? a.order[k] : -1;
+            s_tile = t;
+            s_ready = 0;
+            if (t >= 0) {
+                const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
+                s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z;
+                const unsigned n = h.x;
+                unsigned b_cs = r16(2u * n * CK), b_cc = r16(8u * n * CK), b_es = r16(2u * n * EK),
+                         b_ec = r16(8u * n * EK), b_di = r16(8u * n), b_ri = r16(4u * n), b_lp = r16(2u * (h.z + 1));
+                unsigned b_ei = r16(4u * h.y), b_xl = r16(2u * (h.z + 1));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(smem_addr(&mbar)),
+                             "r"(b_cs + b_cc + b_es + b_ec + b_di + b_ri + b_lp + b_ei + b_xl)
+                             : "memory");
+                bulk_g2s(eid_s, a.ext_id + (size_t)t * a.EC, b_ei, &mbar);
+                bulk_g2s(cs, a.cs + (size_t)t * a.RC * CK, b_cs, &mbar);
+                bulk_g2s(cc, a.cc + (size_t)t * a.RC * CK, b_cc, &mbar);
+                bulk_g2s(es, a.es + (size_t)t * a.RC * EK, b_es, &mbar);
+                bulk_g2s(ecf, a.ec + (size_t)t * a.RC * EK, b_ec, &mbar);
+                bulk_g2s(di, a.dinv + (size_t)t * a.RC, b_di, &mbar);
+                bulk_g2s(rid, a.row_id + (size_t)t * a.RC, b_ri, &mbar);
+                bulk_g2s(lp, a.lev_ptr + (size_t)t * a.LC, b_lp, &mbar);
+                bulk_g2s(xl, a.xlev_ptr + (size_t)t * a.LC, b_xl, &mbar);
+            }
+        }
+        __syncthreads();
+        const int t = s_tile;
+        if (t < 0) break;
+        const int n = s_hdr[0], ne = s_hdr[1], nlev = s_hdr[2];
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 0] = gtimer();
+        {
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(smem_addr(&mbar)), "r"(phase) : "memory");
+            phase ^= 1u;
+        }
+        for (int p0 = 0; p0 < n; p0 += 8 * PIPE_THREADS) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                int p = p0 + u * PIPE_THREADS + threadIdx.x;
+                v[u] = p < n ? __ldg(a.b + rid[p]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                int p = p0 + u * PIPE_THREADS + threadIdx.x;
+                if (p < n) xs[p] = a.alpha * v[u];
+            }
+        }
+        if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
+        __syncthreads();
+        if (warp == LOADER_WARP) {
+            // ---- loader: externals in need order; q0 = first entry not yet seen.
+            // LW loads in flight per lane (one L2 round trip per LW*32 entries)
+            constexpr int LW = 16;
+            int q0 = 0, lv = 0;
+            long long spins = 0;
+            while (q0 < ne) {
+                const int qe = min(ne, q0 + LW * 32);
+                double v[LW];
+#pragma unroll
+                for (int u = 0; u < LW; ++u) {
+                    const int q = q0 + u * 32 + lane32;
+                    v[u] = q < qe ? ld_relaxed_d(a.x + eid_s[q]) : 0.0;
+                }
+                int adv = qe - q0;
+#pragma unroll
+                for (int u = 0; u < LW; ++u) {
+                    const int q = q0 + u * 32 + lane32;
+                    const bool ok = q >= qe || !is_sentinel(v[u]);
+                    if (q < qe && ok) xs[a.RC + q] = v[u];
+                    const unsigned miss = __ballot_sync(0xffffffffu, !ok);
+                    if (miss && adv == qe - q0) adv = u * 32 + __ffs(miss) - 1;
+                }
+                if (adv == 0) {
+                    __nanosleep(32);
+                    if (++spins > SPIN_LIMIT) { if (lane32 == 0) atomicExch(a.err, 7); break; }
+                    continue;
+                }
+                spins = 0;
+                q0 += adv;
+                while (lv < nlev && xl[lv + 1] <= q0) ++lv;   // levels [0, lv) have all externals
+                __syncwarp();
+                if (lane32 == 0) st_release_cta(&s_ready, lv);
+            }
+            if (lane32 == 0) st_release_cta(&s_ready, nlev);   // all loaded (or error path)
+        } else {
+            // ---- compute warps
+            auto wait_ready = [&](int m) {
+                if (threadIdx.x == 0) {
+                    m = min(m, nlev);
+                    long long spins = 0;
+                    while (ld_acquire_cta(&s_ready) < m)
+                        if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
+                }
+            };
+            Rec<CK> rcr;
+            Rec<KH> rer;
+            int rrow = 0;
+            if (crit) {
+                rec_load<CK>(rcr, lp, nlev, 0, lane, cs, cc, di);
+                if (rcr.p >= 0) rrow = rid[rcr.p];
+            } else {
+                rec_load_pair<KH>(rer, lp, nlev, 0, lane, li, es, ecf);
+            }
+            wait_ready(1);
+            bar_compute();
+            if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
+            auto early = [&]() {
+                double a2[2] = {0.0, 0.0};
+                if (rer.p >= 0) {
+#pragma unroll
+                    for (int u = 0; u < KH; ++u) a2[u & 1] = fma(-rer.c[u], xs[rer.s[u]], a2[u & 1]);
+                }
+                double h = a2[0] + a2[1];
+                h += __shfl_xor_sync(0xffffffffu, h, 1);
+                if (rer.p >= 0 && li == 0) xs[rer.p] += h;
+            };
+            if (!crit) {
+                early();
+                rec_load_pair<KH>(rer, lp, nlev, 1, lane, li, es, ecf);
+            }
+            wait_ready(2);
+            bar_compute();
+            const long long c_lev0 = clock64();
+            for (int k = 0; k < nlev; ++k) {
+                if (crit) {
+                    if (rcr.p >= 0) {
+                        double x0 = xs[rcr.s[0]], x1 = xs[rcr.s[1]], x2 = xs[rcr.s[2]], x3 = xs[rcr.s[3]];
+                        double acc = xs[rcr.p];
+                        acc = fma(-rcr.c[0], x0, acc);
+                        acc = fma(-rcr.c[1], x1, acc);
+                        acc = fma(-rcr.c[2], x2, acc);
+                        acc = fma(-rcr.c[3], x3, acc);
+                        const double v = acc * rcr.d;
+                        xs[rcr.p] = v;
+                        __stcg(a.x + rrow, publishable(v));
+                    }
+                    rec_load<CK>(rcr, lp, nlev, k + 1, lane, cs, cc, di);
+                    if (rcr.p >= 0) rrow = rid[rcr.p];
+                } else {
+                    early();
+                    rec_load_pair<KH>(rer, lp, nlev, k + 2, lane, li, es, ecf);
+                }
+                wait_ready(k + 3);
+                bar_compute();
+            }
+            const long long c_lev1 = clock64();
+            if (a.dbg && threadIdx.x == 0) {
+                a.dbg[t * 6 + 2] = gtimer();
+                a.dbg[t * 6 + 5] = (c_lev1 - c_lev0) / (nlev + 1);
+            }
+            if (a.out2)
+                for (int p = threadIdx.x; p < n; p += TILE_THREADS) {
+                    int row = rid[p];
+                    a.out2[row] = xs[p] + a.add[row];
+                }
+        }
+        __syncthreads();
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 3] = gtimer();
+    }
+}
+
 }  // namespace
 
 // smem: xs[RC+EC+2] cc[RC*CK] ec[RC*EK] di[RC] rid[RC] cs[RC*CK] es[RC*EK] lp[LC]
 size_t tile_smem_bytes(const TilePlan& tp) {
     size_t rc = tp.RC, ek = tp.KD, ec = tp.EC, lc = tp.LC;
     size_t bytes = 8 * (rc + ec + 2) + 8 * rc * CK + 8 * rc * ek + 8 * rc + 4 * rc + 4 * ec + 2 * rc * CK +
-                   2 * rc * ek + 2 * lc;
+                   2 * rc * ek + 2 * lc + 2 * lc;
     return (bytes + 127) & ~size_t(127);
 }
 
@@ -586,9 +883,11 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     if (tp.LC > tp.RC + 8) tp.LC = tp.RC + 8;
     tp.unit = unit;
     tp.n_dep = D.nnz;
+    if (tp.LC > 255) return false;                      // levels are stored as bytes in req
+    DevBuf<int32_t> glev(c, n);
     int HS = 1;
     while (HS < 2 * tp.EC) HS <<= 1;
-    size_t bsm = sizeof(int) * (5 * tp.RC + 2 + tp.EC + 8 + HS);
+    size_t bsm = sizeof(int) * (5 * tp.RC + 2 + tp.EC + 8 + HS + 2 * tp.EC + 32 * tp.LC);
     if (bsm > 48 * 1024)
         EDFA_CUDA(cudaFuncSetAttribute(k_tile_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
     {
@@ -603,6 +902,7 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
         cb.max_early = fl + 3;
         cb.err = fl + 2;
         cb.count_only = true;
+        cb.glev = glev.p;
         EDFA_CUDA(cudaMemsetAsync(fl + 3, 0, sizeof(int), c->stream));
         Prof pr(c, "tile_plan", 8.0 * D.nnz);
         k_tile_build<<<nt, 256, bsm, c->stream>>>(cb);
@@ -629,6 +929,8 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     tp.dinv.reset(c, (size_t)nt * tp.RC);
     tp.up_cnt.reset(c, nt);
     tp.up_ids.reset(c, (size_t)nt * 32);
+    tp.xlev_ptr.reset(c, (size_t)nt * tp.LC);
+    tp.req.reset(c, (size_t)nt * tp.LC * 32);
     tp.flags.reset(c, nt);
     tp.ticket.reset(c, 1);
     EDFA_CUDA(cudaMemsetAsync(tp.flags.p, 0, sizeof(int) * nt, c->stream));
@@ -637,7 +939,7 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     tp.ticket_base = 0;
     TileBuild b{view(D), g, tp.RC, tp.KD, tp.EC, tp.LC, diag, unit, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
-                fl + 2, fl + 3, false};
+                fl + 2, fl + 3, false, glev.p, tp.xlev_ptr.p, tp.req.p};
     {
         Prof pr(c, "tile_plan", 24.0 * D.nnz);
         k_tile_build<<<nt, 256, bsm, c->stream>>>(b);
@@ -670,7 +972,9 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
 
 template <int EK>
 static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
-    auto kern = k_tile_solve<EK>;
+    static const bool legacy = getenv("EDFA_TILE_LEGACY") != nullptr;
+    auto kern = legacy ? k_tile_solve<EK> : k_tile_pipe<EK>;
+    const int threads = legacy ? TILE_THREADS : PIPE_THREADS;
     // attribute + occupancy once per (kernel, smem): these are driver calls,
     // kept off the per-solve path
     static std::mutex mu;
@@ -686,15 +990,16 @@ static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
                 smem_set = smem;
             }
             int occ = 0;
-            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, TILE_THREADS, smem));
-            it = grids.emplace(smem, NUM_SMS_B200 * std::max(1, std::min(occ, 2))).first;
+            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            static const int occ_cap = getenv("EDFA_TILE_OCC") ? atoi(getenv("EDFA_TILE_OCC")) : 2;
+            it = grids.emplace(smem, NUM_SMS_B200 * std::max(1, std::min(occ, occ_cap))).first;
         }
         grid = it->second;
     }
     a.ticket_base = tp.ticket_base;
     tp.ticket_base += tp.n_tiles + grid;   // every CTA takes exactly one failing ticket
     void* args[] = {&a};
-    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(TILE_THREADS), args, smem, c->stream));
+    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(threads), args, smem, c->stream));
 }
 
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
@@ -704,15 +1009,24 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
     // so tiles run without waiting -- isolates per-tile processing cost
     static const bool nowait = getenv("EDFA_TILE_NOWAIT") != nullptr;
     if (!nowait) tp.epoch += 1;
+    if (tp.epoch >= (1 << 22)) {   // progress words hold epoch << 8: restart the epoch sequence
+        EDFA_CUDA(cudaMemsetAsync(tp.flags.p, 0, sizeof(int) * tp.n_tiles, c->stream));
+        tp.epoch = 1;
+    }
     TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.LC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
-                tp.flags.p, tp.ticket.p, tp.epoch, 0, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr};
+                tp.flags.p, tp.ticket.p, tp.epoch, 0, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr,
+                tp.xlev_ptr.p, tp.req.p, 0};
+    static const int tile_mode = getenv("EDFA_TILE_MODE") ? atoi(getenv("EDFA_TILE_MODE")) : 0;
+    a.mode = tile_mode;
     static const char* dbg_path = getenv("EDFA_TILE_DEBUG");
     DevBuf<long long> dbg;
     if (dbg_path) {
         dbg.reset(c, (size_t)tp.n_tiles * 6);
         a.dbg = dbg.p;
     }
+    static const bool legacy = getenv("EDFA_TILE_LEGACY") != nullptr;
+    if (!legacy) fill_bits(c, x, tp.n, SENTINEL_BITS);   // a row's value is its own ready flag
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
     switch (tp.KD) {
         case 4: launch_tile<4>(c, tp, a, smem); break;
