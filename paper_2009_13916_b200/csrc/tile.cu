@@ -774,8 +774,14 @@ __global__ void __launch_bounds__(PIPE_THREADS) k_tile_pipe(TileSolve a) {
                 if (threadIdx.x == 0) {
                     m = min(m, nlev);
                     long long spins = 0;
-                    while (ld_acquire_cta(&s_ready) < m)
-                        if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
+                    if (a.mode & 1) {
+                        while (*(volatile int*)&s_ready < m)
+                            if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
+                        __threadfence_block();
+                    } else {
+                        while (ld_acquire_cta(&s_ready) < m)
+                            if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
+                    }
                 }
             };
             Rec<CK> rcr;
@@ -818,7 +824,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) k_tile_pipe(TileSolve a) {
                         acc = fma(-rcr.c[3], x3, acc);
                         const double v = acc * rcr.d;
                         xs[rcr.p] = v;
-                        __stcg(a.x + rrow, publishable(v));
+                        if (!(a.mode & 2)) __stcg(a.x + rrow, publishable(v));
                     }
                     rec_load<CK>(rcr, lp, nlev, k + 1, lane, cs, cc, di);
                     if (rcr.p >= 0) rrow = rid[rcr.p];
@@ -1026,7 +1032,7 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
         a.dbg = dbg.p;
     }
     static const bool legacy = getenv("EDFA_TILE_LEGACY") != nullptr;
-    if (!legacy) fill_bits(c, x, tp.n, SENTINEL_BITS);   // a row's value is its own ready flag
+    if (!legacy && !nowait) fill_bits(c, x, tp.n, SENTINEL_BITS);   // a row's value is its own ready flag
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
     switch (tp.KD) {
         case 4: launch_tile<4>(c, tp, a, smem); break;

@@ -196,7 +196,7 @@ def _gpu_case(E, case):
     return ds, pre
 
 
-@pytest.mark.parametrize("idx,n", [(1, 8), (1, 12), (2, 8), (2, 12), (3, 6)])
+@pytest.mark.parametrize("idx,n", [(1, 8), (1, 12), (1, 16), (2, 8), (2, 12), (3, 6), (5, 10)])
 def test_gmres_matches_oracle(edfa, idx, n):
     from paper_2009_13916_b200 import configs
     case = configs.make(idx, n=n)
@@ -443,3 +443,29 @@ def test_pinned_copy_roundtrip(edfa):
     x, rep = edfa.gmres(edfa.system_operator(ds), pre, sp_.rhs(), tol=1e-8)
     assert rep.converged
     assert np.linalg.norm(s.rhs() - s.full_matrix() @ x) <= 1e-8 * np.linalg.norm(s.rhs()) * 1.0001
+
+
+def test_config4_transient_refresh_matches_oracle(edfa):
+    """Config 4 shape (layered channelised field, five-spot wells) on a small
+    box: stage 1 built once, stage 2 refreshed each time step after
+    update_accumulation (hx/assembly.py:314-333, hx/precond.py:301-309)."""
+    from paper_2009_13916_b200 import assembly, configs
+    case = configs.config4(nx=6, ny=10, nz=5)
+    s = case.system
+    dt, p_prev = case.meta["dt0"], np.full(s.n_cells, case.meta["p_init"])
+    sets = O.static_sets(s.grid, s.face_index, "A")
+    o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=sets, no_fill=True)
+    ds = edfa.DeviceSystem.from_host(s)
+    pre = edfa.BlockLDUPreconditioner.build(ds, patterns=edfa.patterns_for(ds, "static", "A"), no_fill=True)
+    for step in range(3):
+        s = assembly.update_accumulation(s, dt, p_prev=p_prev)
+        pre.refresh(s)
+        o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
+        A, b = s.full_matrix(), s.rhs()
+        xo, ro = O.gmres(lambda v: A @ v, lambda r: O.apply(o1, o2, s.A_fc, s.A_cf, r), b, tol=1e-8, restart=50)
+        x, rep = edfa.gmres(edfa.system_operator(pre.device_system), pre, b, tol=1e-8, restart=50)
+        assert rep.converged and abs(rep.n_it - ro.n_it) <= 2, (step, rep.n_it, ro.n_it)
+        assert np.linalg.norm(b - A @ x) <= 1e-8 * np.linalg.norm(b) * 1.0001
+        assert np.linalg.norm(x - xo) <= 1e-7 * np.linalg.norm(xo)
+        p_prev = x[s.n_free_faces:]
+        dt *= case.meta["dt_mult"]
