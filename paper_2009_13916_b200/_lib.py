@@ -8,11 +8,14 @@ is no CPU or PyTorch fallback for any EDFA operation.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import pathlib
 
 from .errors import FactorizationError
 
 LIB_PATH = pathlib.Path(__file__).resolve().parent / "libedfa.so"
+if os.environ.get("EDFA_LIB"):          # A/B experiments with an alternative build
+    LIB_PATH = pathlib.Path(os.environ["EDFA_LIB"]).resolve()
 
 OK, ERR_VALUE, ERR_FACTORIZATION, ERR_STATE, ERR_CUDA, ERR_UNSUPPORTED = range(6)
 FILTRATION = {"none": 0, "pre": 1, "post-schur": 2, "post-product": 3}
