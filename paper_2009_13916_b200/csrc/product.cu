@@ -85,9 +85,15 @@ struct ProdArgs {
     int32_t* Hi;
     double* Hv;
     int32_t* overflow;     // [count, rows...]
+    int32_t cap;           // PADDED: row capacity of the padded output
 };
 
-template <int BITS, bool FILL>
+// pass modes: COUNT (row lengths), FILL (into final CSR positions), PADDED
+// (single pass: rows of <= cap entries into a padded buffer + their lengths;
+// longer rows go to the overflow list like table overflows)
+enum { COUNT = 0, FILL = 1, PADDED = 2 };
+
+template <int BITS, int MODE>
 __global__ void __launch_bounds__(256) k_product(ProdArgs a) {
     constexpr int T = 1 << BITS;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -136,48 +142,53 @@ __global__ void __launch_bounds__(256) k_product(ProdArgs a) {
             }
             full = __any_sync(0xffffffffu, full);
         }
+        int nH = 0;
+        if (!full) {
+            nH = h_extract_sorted(hk, hv, BITS, tk, tv, lane);   // sorted H row in (tk, tv)
+            if (MODE == PADDED && nH > a.cap) full = true;       // (kept entries <= nH)
+        }
         if (full) {
             if (lane == 0) {
-                if (!FILL) a.cnt[m] = 0;
+                if (MODE != FILL) a.cnt[m] = 0;
                 int p = atomicAdd(a.overflow, 1);
                 a.overflow[1 + p] = m;
             }
             __syncwarp();
             continue;
         }
-        int nH = h_extract_sorted(hk, hv, BITS, tk, tv, lane);   // sorted H row in (tk, tv)
         double thr = 0.0;
         if (a.tau > 0.0) {
             double ss = 0.0;
             for (int i = lane; i < nH; i += 32) ss += tv[i] * tv[i];
             thr = a.tau * sqrt(warp_sum(ss));
         }
-        int o = FILL ? a.Hp[m] : 0, n = 0;
+        const long long o = MODE == FILL ? (long long)a.Hp[m] : MODE == PADDED ? (long long)m * a.cap : 0;
+        int n = 0;
         for (int i0 = 0; i0 < nH; i0 += 32) {
             int i = i0 + lane;
             double v = i < nH ? tv[i] : 0.0;
             int col = i < nH ? tk[i] : -1;
             bool keep = i < nH && v != 0.0 && (col == m || !(fabs(v) < thr));
             unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (FILL && keep) {
-                int p = o + n + __popc(bal & ((1u << lane) - 1));
+            if (MODE != COUNT && keep) {
+                const long long p = o + n + __popc(bal & ((1u << lane) - 1));
                 a.Hi[p] = col;
                 a.Hv[p] = v;
             }
             n += __popc(bal);
         }
-        if (!FILL && lane == 0) a.cnt[m] = n;
+        if (MODE != FILL && lane == 0) a.cnt[m] = n;
         __syncwarp();
     }
 }
 
-template <int BITS, bool FILL>
+template <int BITS, int MODE>
 void launch_product(Ctx* c, const ProdArgs& a) {
     constexpr int T = 1 << BITS;
     size_t pw = (size_t)T * 12 * 3;
     int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / pw));
     size_t sm = pw * warps;
-    auto kern = k_product<BITS, FILL>;
+    auto kern = k_product<BITS, MODE>;
     EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int items = a.rows ? a.n_list : a.n_rows;
     int per_sm = std::max(1, (int)((227 * 1024) / sm));
@@ -186,36 +197,30 @@ void launch_product(Ctx* c, const ProdArgs& a) {
     check_launch("k_product");
 }
 
-template <bool FILL>
-void run_pass(Ctx* c, ProdArgs a, int32_t* ovf_dev, std::vector<int32_t>& ovf_rows, bool retry) {
-    int init = 0;
-    if (!retry) {
-        EDFA_CUDA(cudaMemcpyAsync(ovf_dev, &init, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        a.overflow = ovf_dev;
-        launch_product<8, FILL>(c, a);
-        int n_ovf = 0;
-        EDFA_CUDA(cudaMemcpyAsync(&n_ovf, ovf_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-        EDFA_CUDA(cudaStreamSynchronize(c->stream));
-        ovf_rows.assign(n_ovf, 0);
-        if (n_ovf)
-            EDFA_CUDA(cudaMemcpyAsync(ovf_rows.data(), ovf_dev + 1, sizeof(int) * n_ovf, cudaMemcpyDeviceToHost,
-                                      c->stream));
+__global__ void k_unpad(const int32_t* __restrict__ cnt, const int32_t* __restrict__ Hp, int n, int cap,
+                        const int32_t* __restrict__ pi, const double* __restrict__ pv, int32_t* __restrict__ Hi,
+                        double* __restrict__ Hv) {
+    // one warp per row; rows of the overflow list have cnt 0 here
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const int c = cnt[w], o = Hp[w];
+    const size_t src = (size_t)w * cap;
+    for (int i = lane; i < c; i += 32) {
+        Hi[o + i] = pi[src + i];
+        Hv[o + i] = pv[src + i];
+    }
+}
+
+std::vector<int32_t> read_overflow(Ctx* c, int32_t* ovf_dev) {
+    int n_ovf = 0;
+    EDFA_CUDA(cudaMemcpyAsync(&n_ovf, ovf_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<int32_t> rows(n_ovf);
+    if (n_ovf) {
+        EDFA_CUDA(cudaMemcpyAsync(rows.data(), ovf_dev + 1, sizeof(int) * n_ovf, cudaMemcpyDeviceToHost, c->stream));
         EDFA_CUDA(cudaStreamSynchronize(c->stream));
     }
-    if (ovf_rows.empty()) return;
-    DevBuf<int32_t> rows(c, ovf_rows.size());
-    EDFA_CUDA(cudaMemcpyAsync(rows.p, ovf_rows.data(), sizeof(int) * ovf_rows.size(), cudaMemcpyHostToDevice,
-                              c->stream));
-    ProdArgs b = a;
-    b.rows = rows.p;
-    b.n_list = (int32_t)ovf_rows.size();
-    EDFA_CUDA(cudaMemcpyAsync(ovf_dev, &init, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    b.overflow = ovf_dev;
-    launch_product<12, FILL>(c, b);
-    int n2 = 0;
-    EDFA_CUDA(cudaMemcpyAsync(&n2, ovf_dev, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    require(n2 == 0, EDFA_ERR_UNSUPPORTED, "H~ row exceeds 4096 distinct columns");
+    return rows;
 }
 
 }  // namespace
@@ -234,20 +239,50 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
     a.n_rows = n;
     a.tau = post_tau;
     a.cnt = cnt.p;
+    a.overflow = ovf.p;
+    constexpr int CAP = 128;
+    a.cap = CAP;
+    DevBuf<int32_t> pi(c, (size_t)std::max(n, 1) * CAP);
+    DevBuf<double> pv(c, (size_t)std::max(n, 1) * CAP);
+    a.Hi = pi.p;
+    a.Hv = pv.p;
     std::vector<int32_t> ovf_rows;
     if (n) {
-        Prof pr(c, "product_count", 12.0 * (G.nnz + A.nnz + F.nnz));
-        run_pass<false>(c, a, ovf.p, ovf_rows, false);
+        // single pass into the padded buffer (256-slot tables)
+        Prof pr(c, "product", 12.0 * (G.nnz + A.nnz + F.nnz) + 12.0 * G.n_rows * 35);
+        EDFA_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c->stream));
+        launch_product<8, PADDED>(c, a);
+        ovf_rows = read_overflow(c, ovf.p);
+    }
+    DevBuf<int32_t> rows(c, std::max<size_t>(ovf_rows.size(), 1));
+    ProdArgs b = a;
+    if (!ovf_rows.empty()) {   // wide rows: count with 4096-slot tables
+        EDFA_CUDA(cudaMemcpyAsync(rows.p, ovf_rows.data(), sizeof(int) * ovf_rows.size(), cudaMemcpyHostToDevice,
+                                  c->stream));
+        b.rows = rows.p;
+        b.n_list = (int32_t)ovf_rows.size();
+        EDFA_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c->stream));
+        Prof pr(c, "product_wide", 12.0 * (G.nnz + A.nnz + F.nnz) * b.n_list / std::max(n, 1));
+        launch_product<12, COUNT>(c, b);
+        require(read_overflow(c, ovf.p).empty(), EDFA_ERR_UNSUPPORTED, "H~ row exceeds 4096 distinct columns");
     }
     H.nnz = scan_counts(c, cnt.p, H.ptr.p, n);
     H.idx.reset(c, H.nnz);
     H.val.reset(c, H.nnz);
     if (n) {
-        a.Hp = H.ptr.p;
-        a.Hi = H.idx.p;
-        a.Hv = H.val.p;
-        Prof pr(c, "product_fill", 12.0 * (G.nnz + A.nnz + F.nnz + H.nnz));
-        run_pass<true>(c, a, ovf.p, ovf_rows, false);
+        Prof pr(c, "product_unpad", 24.0 * H.nnz + 8.0 * n);
+        k_unpad<<<ceil_div((int64_t)n * 32, 256), 256, 0, c->stream>>>(cnt.p, H.ptr.p, n, CAP, pi.p, pv.p, H.idx.p,
+                                                                      H.val.p);
+        check_launch("k_unpad");
+    }
+    if (!ovf_rows.empty()) {
+        b.Hp = H.ptr.p;
+        b.Hi = H.idx.p;
+        b.Hv = H.val.p;
+        EDFA_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c->stream));
+        Prof pr(c, "product_wide", 12.0 * (G.nnz + A.nnz + F.nnz) * b.n_list / std::max(n, 1));
+        launch_product<12, FILL>(c, b);
+        require(read_overflow(c, ovf.p).empty(), EDFA_ERR_UNSUPPORTED, "H~ row exceeds 4096 distinct columns");
     }
 }
 
