@@ -101,6 +101,7 @@ struct TileBuild {
     int* err;
     int* max_early;       // count-only pass: max early deps of a row (sizes EK)
     bool count_only;
+    int MD;               // max dependencies of a row
     int* glev;            // local level of every row (written by the count pass)
     short* xlev_ptr;      // LC per tile: externals first needed below level l
     unsigned char* req;   // LC*32 per tile: upstream progress needed to load externals < l+1
@@ -127,32 +128,48 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
         lev[r] = 0;
     }
     __syncthreads();
-    // local levels by relaxation (converges in local-depth sweeps)
-    for (int it = 0; it < b.RC + 1; ++it) {
-        int changed = 0;
+    if (b.count_only) {
+        // intra-tile dependency lists (box indices, -1 = external), then local
+        // levels by relaxation over them (converges in local-depth sweeps);
+        // the fill pass reads the levels back from glev
+        short* dl = reinterpret_cast<short*>(order);      // RC*MD (reuses the fill-pass scratch)
         for (int r = threadIdx.x; r < n; r += blockDim.x) {
-            int lv = 0;
-            for (int e = b.D.ptr[cell[r]]; e < b.D.ptr[cell[r] + 1]; ++e) {
-                int j = b.D.idx[e];
-                if (g.tile_of(j) == t) lv = max(lv, lev[g.local_of(t, j)] + 1);
+            const int row = cell[r], e0 = b.D.ptr[row], e1 = b.D.ptr[row + 1];
+            for (int e = e0; e < e1; ++e) {
+                const int j = b.D.idx[e];
+                dl[r * b.MD + (e - e0)] = g.tile_of(j) == t ? (short)g.local_of(t, j) : (short)-1;
             }
-            if (lv != lev[r]) { lev[r] = lv; changed = 1; }
+            for (int e = e1 - e0; e < b.MD; ++e) dl[r * b.MD + e] = -2;
         }
-        if (!__syncthreads_or(changed)) break;
-    }
-    if (b.count_only) {   // early deps = all but the intra-tile ones on the previous level
-        for (int r = threadIdx.x; r < n; r += blockDim.x) b.glev[cell[r]] = lev[r];
+        __syncthreads();
+        for (int it = 0; it < b.RC + 1; ++it) {
+            int changed = 0;
+            for (int r = threadIdx.x; r < n; r += blockDim.x) {
+                int lv = 0;
+                for (int e = 0; e < b.MD; ++e) {
+                    const int q = dl[r * b.MD + e];
+                    if (q == -2) break;
+                    if (q >= 0) lv = max(lv, lev[q] + 1);
+                }
+                if (lv != lev[r]) { lev[r] = lv; changed = 1; }
+            }
+            if (!__syncthreads_or(changed)) break;
+        }
+        // early deps = all but the intra-tile ones on the previous level
         for (int r = threadIdx.x; r < n; r += blockDim.x) {
+            b.glev[cell[r]] = lev[r];
             int ne_r = 0;
-            for (int e = b.D.ptr[cell[r]]; e < b.D.ptr[cell[r] + 1]; ++e) {
-                int j = b.D.idx[e];
-                bool critical = g.tile_of(j) == t && lev[g.local_of(t, j)] == lev[r] - 1;
-                ne_r += !critical;
+            for (int e = 0; e < b.MD; ++e) {
+                const int q = dl[r * b.MD + e];
+                if (q == -2) break;
+                ne_r += !(q >= 0 && lev[q] == lev[r] - 1);
             }
             atomicMax(b.max_early, ne_r);
         }
         return;
     }
+    for (int r = threadIdx.x; r < n; r += blockDim.x) lev[r] = b.glev[cell[r]];
+    __syncthreads();
     for (int l = threadIdx.x; l < b.RC + 2; l += blockDim.x) cnt[l] = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < n; r += blockDim.x) atomicMax(&misc[0], lev[r] + 1);
@@ -894,6 +911,7 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     int HS = 1;
     while (HS < 2 * tp.EC) HS <<= 1;
     size_t bsm = sizeof(int) * (5 * tp.RC + 2 + tp.EC + 8 + HS + 2 * tp.EC + 32 * tp.LC);
+    bsm = std::max(bsm, sizeof(int) * 2 * tp.RC + sizeof(short) * (size_t)tp.RC * hf[1] + 64);
     if (bsm > 48 * 1024)
         EDFA_CUDA(cudaFuncSetAttribute(k_tile_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
     {
@@ -909,6 +927,7 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
         cb.err = fl + 2;
         cb.count_only = true;
         cb.glev = glev.p;
+        cb.MD = hf[1];
         EDFA_CUDA(cudaMemsetAsync(fl + 3, 0, sizeof(int), c->stream));
         Prof pr(c, "tile_plan", 8.0 * D.nnz);
         k_tile_build<<<nt, 256, bsm, c->stream>>>(cb);
@@ -945,7 +964,10 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     tp.ticket_base = 0;
     TileBuild b{view(D), g, tp.RC, tp.KD, tp.EC, tp.LC, diag, unit, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
-                fl + 2, fl + 3, false, glev.p, tp.xlev_ptr.p, tp.req.p};
+                fl + 2, fl + 3, false, hf[1]};
+    b.glev = glev.p;
+    b.xlev_ptr = tp.xlev_ptr.p;
+    b.req = tp.req.p;
     {
         Prof pr(c, "tile_plan", 24.0 * D.nnz);
         k_tile_build<<<nt, 256, bsm, c->stream>>>(b);
