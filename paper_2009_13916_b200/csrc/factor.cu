@@ -103,8 +103,11 @@ __global__ void __launch_bounds__(256) k_ic0(LevelArgs la, const int32_t* __rest
 // ILU(0) of S, one warp per row.  LU starts as a copy of S; on exit its
 // strictly lower part holds the multipliers and its strictly upper part U;
 // pivots go to udiag.
+// staged U entries per pivot chunk (the elimination chunks longer pivot sets)
+__host__ __device__ constexpr int ilu0_ecap(int rmax) { return rmax <= 64 ? 512 : 1024; }
 __host__ __device__ constexpr size_t ilu0_warp_smem(int rmax) {
-    return ((size_t)(3 * rmax + 1024) * 8 + (size_t)(4 * rmax + 1 + 1024 + 2) * 4 + 15) & ~size_t(15);
+    return ((size_t)(3 * rmax + ilu0_ecap(rmax)) * 8 + (size_t)(4 * rmax + 1 + ilu0_ecap(rmax) + 2) * 4 + 15) &
+           ~size_t(15);
 }
 
 // position of the first strictly-upper entry of every row
@@ -119,7 +122,8 @@ __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __res
                                               double* __restrict__ LU, const double* __restrict__ scale,
                                               double* __restrict__ udiag, int* shifts, int* err) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int ECAP = 1024;
+    constexpr int ECAP = ilu0_ecap(RMAX);
+    constexpr int SW = ECAP / 32 < 16 ? ECAP / 32 : 16;   // staged entries per lane per round trip
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // per-warp scratch: row, pivot metadata, staged U entries of a pivot chunk
     unsigned char* base = smem + (size_t)wid * ilu0_warp_smem(RMAX);
@@ -175,12 +179,12 @@ __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __res
                 __syncwarp();
                 const int p1 = misc[0], tot = misc[1];
                 // stage (target slot, u_kj) of every U entry of the chunk
-                for (int f0 = 0; f0 < tot; f0 += 32 * 4) {
-                    int e[4], q[4];
-                    double u[4];
-                    int32_t j[4];
+                for (int f0 = 0; f0 < tot; f0 += 32 * SW) {
+                    int e[SW], q[SW];
+                    double u[SW];
+                    int32_t j[SW];
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
+                    for (int w = 0; w < SW; ++w) {
                         int f = f0 + w * 32 + lane;
                         q[w] = -1;
                         if (f < tot) {
@@ -195,13 +199,13 @@ __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __res
                         }
                     }
 #pragma unroll
-                    for (int w = 0; w < 4; ++w)
+                    for (int w = 0; w < SW; ++w)
                         if (q[w] >= 0) {
                             j[w] = __ldg(Si + e[w]);
                             u[w] = __ldcg(LU + e[w]);
                         }
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
+                    for (int w = 0; w < SW; ++w) {
                         int f = f0 + w * 32 + lane;
                         if (q[w] >= 0) {
                             eslot[f] = bsearch(cols, q[w] + 1, n, j[w]);
@@ -315,10 +319,10 @@ void read_flags(Ctx* c, const int* dev, int* shifts, int* err) {
 }
 
 template <class K>
-int coop_grid(K kern, int threads, size_t smem) {
+int coop_grid(K kern, int threads, size_t smem, int cap = 2) {
     int occ = 0;
     EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-    return NUM_SMS_B200 * std::max(1, std::min(occ, 2));
+    return NUM_SMS_B200 * std::max(1, std::min(occ, cap));
 }
 
 }  // namespace
@@ -405,11 +409,11 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         LevelArgs la{f.fwd.perm.p, f.fwd.level_start.p, f.fwd.n_levels, reinterpret_cast<unsigned*>(f.fwd.sync.p)};
         void* args[] = {&la, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
         auto launch = [&](auto kern, int rmax) {
-            int threads = rmax >= 1024 ? 64 : 128;
+            int threads = rmax >= 1024 ? 64 : rmax <= 64 ? 256 : 128;
             size_t smem = ilu0_warp_smem(rmax) * (threads / 32);
             if (smem > 48 * 1024)
                 EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int grid = coop_grid(kern, threads, smem);
+            int grid = coop_grid(kern, threads, smem, 4);
             EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(threads), args, smem, c->stream));
         };
         if (maxr <= 64) launch(k_ilu0<64>, 64);

@@ -35,8 +35,11 @@ __global__ void k_levels(CsrV D, bool reverse, int* __restrict__ level, int* __r
         int j = D.idx[e];
         int v = ld_relaxed_i(level + j);
         long long spins = 0;
-        while (v == LEVEL_UNSET) {
+        unsigned ns = 32;
+        while (v == LEVEL_UNSET) {   // back off: thousands of pollers share the L2
             if (++spins > SPIN_LIMIT) { atomicExch(err, 1); v = 0; break; }
+            __nanosleep(ns);
+            if (ns < 512) ns <<= 1;
             v = ld_relaxed_i(level + j);
         }
         lv = max(lv, v + 1);

@@ -65,7 +65,7 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() 
     cpu1 = time.process_time()
     p = report()
     k = sum(v["ms"] for v in p.values())
-    top = sorted(p.items(), key=lambda kv: -kv[1]["ms"])[:3]
+    top = sorted(p.items(), key=lambda kv: -kv[1]["ms"])[:int(__import__("os").environ.get("TOPN", "3"))]
     slow, SLOW[:] = list(SLOW), []
     print(json.dumps(dict(slow=slow, setup_ms=round((t1 - t0) * 1e3, 1), gmres_ms=round((t2 - t1) * 1e3, 1),
                           kernel_ms=round(k, 1), cpu_ms=round((cpu1 - cpu0) * 1e3, 1),
