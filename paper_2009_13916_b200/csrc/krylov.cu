@@ -179,6 +179,13 @@ __global__ void k_axpby(int64_t n, double a, const double* x, double b, double* 
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = (b == 0.0) ? a * x[i] : fma(a, x[i], b * y[i]);
 }
+// w <- w / sqrt(nrm2[0])  (0 when the norm is 0: happy breakdown)
+__global__ void k_normalize(int64_t n, const double* __restrict__ nrm2, double* w) {
+    const double s2 = *nrm2;
+    const double inv = s2 > 0.0 ? 1.0 / sqrt(s2) : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        w[i] = w[i] * inv;
+}
 // z = x + a*(y - w*v)   (Bi-CGStab direction update, p = r + beta (p - omega v))
 __global__ void k_bicg_p(int64_t n, const double* __restrict__ r, double beta, double omega,
                          const double* __restrict__ v, double* __restrict__ p) {
@@ -236,6 +243,11 @@ struct Blas {
         EDFA_CUDA(cudaMemcpyAsync(&h, red.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         EDFA_CUDA(cudaStreamSynchronize(c->stream));
         return h;
+    }
+    void normalize(int64_t n, const double* nrm2_dev, double* w) {
+        Prof pr(c, "axpby", 16.0 * n);
+        k_normalize<<<grid_for(n), RED_THREADS, 0, c->stream>>>(n, nrm2_dev, w);
+        check_launch("normalize");
     }
     void axpby(int64_t n, double a, const double* x, double b, double* y) {
         Prof pr(c, "axpby", 24.0 * n);
@@ -325,6 +337,13 @@ static void check_trsv_error(Ctx* c) {
 
 void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b, double* x,
            double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap) {
+    // Arnoldi with classical Gram-Schmidt applied twice (CGS2): two fused
+    // multi-dot + multi-axpy(+norm) passes, normalisation by a device-side
+    // norm.  The host never waits inside a cycle for the step it just
+    // enqueued: it enqueues step j, then reads back step j-1's Hessenberg
+    // column (async copy + event), applies the Givens rotations and tests
+    // convergence.  When step j-1 converges, the already-enqueued step j is
+    // discarded (its vector is never used).
     require(rtol > 0.0, EDFA_ERR_VALUE, "tol must be positive");
     require(m >= 1 && m <= 62, EDFA_ERR_VALUE, "restart must be in [1, 62]");
     require(max_it >= 0, EDFA_ERR_VALUE, "max_it must be >= 0");
@@ -345,41 +364,47 @@ void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_sta
         EDFA_CUDA(cudaStreamSynchronize(c->stream));
         return;
     }
-    DevBuf<double> V(c, (size_t)(m + 1) * n), z(c, n), r(c, n), hd(c, 192);
-    double* hpin = c->h_pinned;
+    // per-step device slots (parity j & 1): [0, 64) pass-1 coefficients,
+    // [64, 128) pass-2 coefficients, 128 / 129 norms^2 after pass 1 / 2
+    DevBuf<double> V(c, (size_t)(m + 1) * n), z(c, n), r(c, n), hd(c, 2 * 192 + 64);
+    double* hpin = c->h_pinned;   // 2 x 192 host slots + 64 for y
+    cudaEvent_t ev[2] = {c->get_event(), c->get_event()};
     EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
     EDFA_CUDA(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
     double beta = bnorm;
     std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
     bool happy = false;
+    auto enqueue_step = [&](int j) {
+        double* vj = V.p + (int64_t)j * n;
+        double* w = V.p + (int64_t)(j + 1) * n;
+        double* h = hd.p + (j & 1) * 192;
+        op.P(vj, z.p);
+        op.A(z.p, w);
+        bl.multidot(V.p, n, j + 1, w, n, h);
+        bl.multiaxpy(V.p, n, j + 1, h, 1.0, w, w, n, h + 128);
+        bl.multidot(V.p, n, j + 1, w, n, h + 64);
+        bl.multiaxpy(V.p, n, j + 1, h + 64, 1.0, w, w, n, h + 129);
+        bl.normalize(n, h + 129, w);
+        EDFA_CUDA(cudaMemcpyAsync(hpin + (j & 1) * 192, h, sizeof(double) * 130, cudaMemcpyDeviceToHost,
+                                  c->stream));
+        EDFA_CUDA(cudaEventRecord(ev[j & 1], c->stream));
+    };
     while (rep->n_it < max_it) {
         bl.axpby(n, 1.0 / beta, r.p, 0.0, V.p);
         std::fill(H.begin(), H.end(), 0.0);
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = beta;
         int k = 0;
-        for (int j = 0; j < m; ++j) {
-            double* vj = V.p + (int64_t)j * n;
-            double* w = V.p + (int64_t)(j + 1) * n;
-            op.P(vj, z.p);
-            op.A(z.p, w);
+        int enq = 0;                       // steps enqueued in this cycle
+        const int budget = std::min(m, max_it - rep->n_it);
+        enqueue_step(enq++);
+        for (int j = 0; j < budget; ++j) {
+            if (enq < budget) enqueue_step(enq++);        // keep one step ahead
+            EDFA_CUDA(cudaEventSynchronize(ev[j & 1]));
+            const double* hp = hpin + (j & 1) * 192;
             rep->n_it++;
-            // pass 1: h = V^T w and ||w||^2 (extra slot j+1 with V == NULL semantics -> w.w)
-            bl.multidot(V.p, n, j + 2, w, n, hd.p);             // slot j+1 = V_{j+1} . w = w.w
-            bl.multiaxpy(V.p, n, j + 1, hd.p, 1.0, w, w, n, hd.p + 64);
-            EDFA_CUDA(cudaMemcpyAsync(hpin, hd.p, sizeof(double) * 128, cudaMemcpyDeviceToHost, c->stream));
-            EDFA_CUDA(cudaStreamSynchronize(c->stream));
-            double w0 = std::sqrt(std::max(hpin[j + 1], 0.0));
-            double wn = std::sqrt(std::max(hpin[64], 0.0));
-            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hpin[i];
-            if (wn < 0.7071067811865476 * w0) {   // DGKS: second CGS pass
-                bl.multidot(V.p, n, j + 1, w, n, hd.p);
-                bl.multiaxpy(V.p, n, j + 1, hd.p, 1.0, w, w, n, hd.p + 64);
-                EDFA_CUDA(cudaMemcpyAsync(hpin, hd.p, sizeof(double) * 128, cudaMemcpyDeviceToHost, c->stream));
-                EDFA_CUDA(cudaStreamSynchronize(c->stream));
-                for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] += hpin[i];
-                wn = std::sqrt(std::max(hpin[64], 0.0));
-            }
+            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hp[i] + hp[64 + i];
+            const double wn = std::sqrt(std::max(hp[129], 0.0));
             H[(size_t)(j + 1) * m + j] = wn;
             for (int i = 0; i < j; ++i) {
                 double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
@@ -397,17 +422,19 @@ void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_sta
             push_hist(est);
             k = j + 1;
             if (wn == 0.0) { happy = true; break; }
-            bl.axpby(n, 1.0 / wn, w, 0.0, w);
-            if (est <= rtol || rep->n_it >= max_it) break;
+            if (est <= rtol) break;
         }
+        // a speculatively enqueued step may still be running: everything below
+        // is stream-ordered after it and reads only V_0..V_{k-1}
         for (int i = k - 1; i >= 0; --i) {   // back substitution H y = g
-            double s = g[i];
-            for (int t = i + 1; t < k; ++t) s -= H[(size_t)i * m + t] * y[t];
-            y[i] = H[(size_t)i * m + i] != 0.0 ? s / H[(size_t)i * m + i] : 0.0;
+            double sacc = g[i];
+            for (int t = i + 1; t < k; ++t) sacc -= H[(size_t)i * m + t] * y[t];
+            y[i] = H[(size_t)i * m + i] != 0.0 ? sacc / H[(size_t)i * m + i] : 0.0;
         }
-        for (int i = 0; i < k; ++i) hpin[i] = y[i];
-        EDFA_CUDA(cudaMemcpyAsync(hd.p, hpin, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
-        bl.multiaxpy(V.p, n, k, hd.p, 1.0, nullptr, r.p, n, nullptr);   // r <- V y (scratch)
+        for (int i = 0; i < k; ++i) hpin[384 + i] = y[i];
+        double* yd = hd.p + 2 * 192;
+        EDFA_CUDA(cudaMemcpyAsync(yd, hpin + 384, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
+        bl.multiaxpy(V.p, n, k, yd, 1.0, nullptr, r.p, n, nullptr);   // r <- V y (scratch)
         op.P(r.p, z.p);
         bl.axpby(n, 1.0, z.p, 1.0, x);
         op.A(x, r.p);
@@ -417,6 +444,8 @@ void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_sta
         if (beta / bnorm <= rtol) { rep->converged = 1; break; }
         if (happy || beta == 0.0) { rep->breakdown = 1; break; }
     }
+    c->event_pool.push_back(ev[0]);
+    c->event_pool.push_back(ev[1]);
     rep->final_relres = beta / bnorm;
     if (rep->n_it == 0) push_hist(beta / bnorm);
 }
