@@ -41,7 +41,28 @@ ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "EDFA setup+GMRES solve throughput per system (config 2)"
+METRIC_OF = lambda k: METRIC.replace("config 2", f"config {k}")  # noqa: E731
 UNIT = "MDOF/s"
+
+
+DEFAULT_N = {1: 16, 2: 64, 3: 128, 4: None, 5: 256}
+
+
+def make_case(args):
+    from paper_2009_13916_b200 import configs
+    if args.config == 4:
+        return configs.config4() if args.n is None else configs.config4(nx=args.n, ny=args.n, nz=args.n)
+    return configs.make(args.config, n=args.n or DEFAULT_N[args.config])
+
+
+def build_pre(case, ds):
+    """Preconditioner of a BASELINE config through the drop-in API."""
+    from paper_2009_13916_b200.precond import BlockLDUPreconditioner, DynamicConfig, patterns_for
+    p = case.precond
+    if p["pattern"] == "dynamic":
+        return BlockLDUPreconditioner.build(ds, dynamic=DynamicConfig(p["n_add"], p["n_ent"]), no_fill=True)
+    pats = patterns_for(ds, p["pattern"], p.get("prototype", "A"))
+    return BlockLDUPreconditioner.build(ds, patterns=pats, no_fill=True)
 
 
 def parse():
@@ -50,7 +71,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="edfa", choices=["edfa", "reference"])
-    ap.add_argument("--n", type=int, default=64, help="grid cells per side (config 2 is 64)")
+    ap.add_argument("--n", type=int, default=None, help="grid cells per side (default: the config's size)")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE config (2 = the headline workload; others for evidence runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None, help="write the per-kernel event profile here")
     ap.add_argument("--slabs", type=int, default=0,
@@ -133,9 +156,10 @@ def cpu_baseline(n_full: int, n_iters_full: int, sample_n: int = 20, gmres_iters
     s = case.system
     N = s.n_unknowns
     A = s.full_matrix()
+    workers = max(1, os.cpu_count() or 1)
     t0 = time.perf_counter()
     sets = O.static_sets(s.grid, s.face_index, "A")
-    o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=sets, no_fill=True)
+    o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=sets, no_fill=True, n_workers=workers)
     t1 = time.perf_counter()
     o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
     t2 = time.perf_counter()
@@ -150,9 +174,11 @@ def cpu_baseline(n_full: int, n_iters_full: int, sample_n: int = 20, gmres_iters
     per_dof_setup = (t2 - t0) / N
     per_dof_iter = it_time / N
     return dict(per_dof_setup=per_dof_setup, per_dof_iter=per_dof_iter, sample_N=N,
-                sample=f"oracle port on the config-2 generator at {sample_n}^3 (N={N}): full stage 1 + stage 2, "
-                       f"{rep.n_it} GMRES(50) iterations; extrapolated per DOF to {n_full}^3 with "
-                       f"{n_iters_full} iterations",
+                sample=f"oracle port on the config-2 generator at {sample_n}^3 (N={N}): full stage 1 (per-cell "
+                       f"loop over {workers} processes, as the reference's n_workers fan-out) + stage 2 and "
+                       f"{rep.n_it} GMRES(50) iterations (scipy, single-threaded); extrapolated per DOF to "
+                       f"{n_full}^3 with {n_iters_full} iterations",
+                cores=workers,
                 t_stage1=t1 - t0, t_stage2=t2 - t1, t_iter=it_time, _np=np)
 
 
@@ -167,7 +193,7 @@ def run_reference(args):
     if world > 1 and rank != 0:
         return
     from paper_2009_13916_b200 import configs  # noqa: F401
-    n_full = args.n
+    n_full = args.n or 64
     # iteration count of the full workload: the oracle's own GMRES count is
     # not affordable at 64^3 per step; use the survey-measured 87 (SURVEY.md
     # §6.2, oracle restatement, config-2 shape) unless a smaller grid is asked
@@ -187,7 +213,7 @@ def run_reference(args):
         "data": "synthetic (seeded config-2 generator)",
         "config": {"workload": f"config2-{n_full}^3-staticA-IC0ILU0-gmres50", "n_dof": N_full,
                    "rtol": 1e-8, "restart": 50, "l2": "inputs larger than L2"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": cb["sample"]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "port", "sample": cb["sample"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -229,7 +255,9 @@ def run_edfa(args):
                     diag.append((_name, round(dt * 1e3, 1)))
                 return r
             setattr(lib, _name, _w)
-    case = configs.config2(n=args.n)
+    case = make_case(args)
+    if args.n is None:
+        args.n = DEFAULT_N[args.config] or 0
     s = case.system
     N = s.n_unknowns
     ds = DeviceSystem.from_host(s)
@@ -237,8 +265,7 @@ def run_edfa(args):
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     def step(system_dev, b):
-        pats = patterns_for(system_dev, "static", "A")
-        pre = BlockLDUPreconditioner.build(system_dev, patterns=pats, no_fill=True)
+        pre = build_pre(case, system_dev)
         x, rep = gmres(system_operator(system_dev), pre, b, tol=case.rtol, restart=case.restart,
                        max_it=case.max_it)
         return x, rep, pre
@@ -314,8 +341,7 @@ def run_edfa(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ds_h = DeviceSystem.from_host(s_pin)                  # H2D of the four blocks, rhs, topology
-        pats = patterns_for(ds_h, "static", "A")                # device topology uploaded with the blocks
-        pre_h = BlockLDUPreconditioner.build(ds_h, patterns=pats, no_fill=True)
+        pre_h = build_pre(case, ds_h)                          # patterns from the device topology
         x_h, rep_h = gmres(system_operator(ds_h), pre_h, s_pin.rhs(), tol=case.rtol, restart=case.restart,
                            max_it=case.max_it)                # x returned to host (D2H)
         e2e_times.append(time.perf_counter() - t0)
@@ -349,11 +375,13 @@ def run_edfa(args):
     kernel_ms_per_step = tot_full
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC_OF(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded config-2 generator: 64^3, lnK~N(0,2), kz/kx=0.1)",
-        "config": {"workload": f"config2-{args.n}^3-staticA-IC0ILU0-gmres50", "n_dof": N,
+        "data": ("synthetic (seeded config-2 generator: 64^3, lnK~N(0,2), kz/kx=0.1)" if args.config == 2
+                 else f"synthetic (seeded generator of BASELINE config {args.config}: {case.name})"),
+        "config": {"workload": (f"config2-{args.n}^3-staticA-IC0ILU0-gmres50" if args.config == 2
+                                else f"{case.name}-IC0ILU0-gmres50"), "n_dof": N,
                    "n_free_faces": s.n_free_faces, "n_cells": s.n_cells, "rtol": case.rtol,
                    "restart": case.restart, "gmres_iterations": reps[-1].n_it,
                    "final_true_relres": reps[-1].final_relres, "host_check_relres": relres_host,
@@ -373,10 +401,11 @@ def run_edfa(args):
     if args.profile_json and rank == 0:
         pathlib.Path(args.profile_json).write_text(json.dumps({"timed_region": prof, "warmup_step": prof_full},
                                                               indent=1))
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline and args.config == 2:
         cb = cpu_baseline(args.n, reps[-1].n_it)
         v = extrapolate(cb, N, reps[-1].n_it)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": cb["sample"]}
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "port",
+                                "sample": cb["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -406,6 +435,7 @@ def run_slabs(args):
     from paper_2009_13916_b200.device import ctx
     lib = _lib.lib()
     diag = []
+    args.n = args.n or 64
     case = configs.config2(n=args.n, nz=args.n * parts)
     s = case.system
     N = s.n_unknowns

@@ -387,22 +387,15 @@ class Stage2:
         self.S, self.schur_inner = S, schur_inner
 
 
-def build_stage1(A_ff, A_fc, A_cf, *, sets=None, dynamic=None, tau_filt=0.0,
-                 filtration="none", face_drop_tol=0.0, no_fill=False):
-    """hx/precond.py:187-261 (serial; the reference's worker fan-out merges in
-    cell order, so the serial result is the reference result for any
-    worker count).  ``dynamic`` = (n_add, n_ent, it_max) or None."""
-    if (sets is None) == (dynamic is None):
-        raise ValueError("give exactly one of patterns or dynamic")
-    if filtration not in FILTRATION_MODES:
-        raise ValueError(f"filtration must be one of {FILTRATION_MODES}")
-    A_ff, A_cf, A_fc = canonical(A_ff), canonical(A_cf), canonical(A_fc)
-    n_c, n_f = A_cf.shape[0], A_ff.shape[0]
-    A_csc = A_ff.tocsc()
-    A_fc_csc = A_fc.tocsc()
-    pre_tau = tau_filt if filtration == "pre" else 0.0
+_ROWS_CTX = {}
+
+
+def _stage1_rows(m0, m1):
+    """Per-cell loop of hx/precond.py:187-201 over cells [m0, m1)."""
+    A_ff, A_cf, A_csc, A_fc_csc, sets, dynamic, pre_tau = (_ROWS_CTX[k] for k in (
+        "A_ff", "A_cf", "A_csc", "A_fc_csc", "sets", "dynamic", "pre_tau"))
     rows, cols, gv, fv, sizes, used = [], [], [], [], [], []
-    for m in range(n_c):
+    for m in range(m0, m1):
         lo, hi = A_cf.indptr[m], A_cf.indptr[m + 1]
         gi, gval = A_cf.indices[lo:hi].astype(np.int64), A_cf.data[lo:hi]
         if dynamic is not None:
@@ -420,6 +413,33 @@ def build_stage1(A_ff, A_fc, A_cf, *, sets=None, dynamic=None, tau_filt=0.0,
         fv.append(filter_vector(f, pre_tau))
         sizes.append(idx.size)
         used.append(idx)
+    return rows, cols, gv, fv, sizes, used
+
+
+def build_stage1(A_ff, A_fc, A_cf, *, sets=None, dynamic=None, tau_filt=0.0,
+                 filtration="none", face_drop_tol=0.0, no_fill=False, n_workers=1):
+    """hx/precond.py:187-261.  The reference fans the per-cell loop out over
+    ``n_workers`` and merges in cell order (hx/precond.py:233-256), so the
+    result is the serial one for any worker count; here the workers are
+    processes (the reference's threads are GIL-bound).  ``dynamic`` =
+    (n_add, n_ent, it_max) or None."""
+    if (sets is None) == (dynamic is None):
+        raise ValueError("give exactly one of patterns or dynamic")
+    if filtration not in FILTRATION_MODES:
+        raise ValueError(f"filtration must be one of {FILTRATION_MODES}")
+    A_ff, A_cf, A_fc = canonical(A_ff), canonical(A_cf), canonical(A_fc)
+    n_c, n_f = A_cf.shape[0], A_ff.shape[0]
+    _ROWS_CTX.update(A_ff=A_ff, A_cf=A_cf, A_csc=A_ff.tocsc(), A_fc_csc=A_fc.tocsc(), sets=sets,
+                     dynamic=dynamic, pre_tau=tau_filt if filtration == "pre" else 0.0)
+    if n_workers > 1 and n_c > 1:
+        import multiprocessing as mp
+        cuts = np.linspace(0, n_c, n_workers + 1).astype(int)
+        with mp.get_context("fork").Pool(n_workers) as pool:
+            parts = pool.starmap(_stage1_rows, [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:])])
+    else:
+        parts = [_stage1_rows(0, n_c)]
+    _ROWS_CTX.clear()
+    rows, cols, gv, fv, sizes, used = ([x for p in parts for x in p[k]] for k in range(6))
     r = np.concatenate(rows) if rows else np.empty(0, np.int64)
     c = np.concatenate(cols) if cols else np.empty(0, np.int64)
     G = canonical(sp.coo_matrix((np.concatenate(gv) if gv else [], (r, c)), shape=(n_c, n_f)))
