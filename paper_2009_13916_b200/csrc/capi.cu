@@ -128,6 +128,9 @@ int edfa_system_create(edfa_ctx* ctx, const edfa_csr* A_ff, const edfa_csr* A_fc
         require(s->A_ff->n_rows == s->A_ff->n_cols, EDFA_ERR_VALUE, "A_ff must be square");
         require(s->A_cc->n_rows == s->A_cc->n_cols, EDFA_ERR_VALUE, "A_cc must be square");
         block_merge(c, *s->A_ff, *s->A_fc, *s->A_cf, *s->A_cc, s->A);
+        build_sell(c, s->A, s->sA);
+        build_sell(c, *s->A_cf, s->sAcf);
+        build_sell(c, *s->A_fc, s->sAfc);
     } catch (...) {
         delete s;
         throw;
@@ -143,6 +146,7 @@ int edfa_system_set_cc(edfa_ctx* ctx, edfa_system* sys, const edfa_csr* A_cc) {
     require(cc.n_rows == sys->A_cc->n_rows && cc.n_cols == sys->A_cc->n_cols, EDFA_ERR_VALUE, "A_cc shape changed");
     sys->A_cc = &cc;
     block_merge(c, *sys->A_ff, *sys->A_fc, *sys->A_cf, *sys->A_cc, sys->A);
+    build_sell(c, sys->A, sys->sA);
     API_END
 }
 
@@ -333,7 +337,7 @@ int edfa_spmv(edfa_ctx* ctx, const edfa_csr* A, const double* x, double* y, doub
 
 int edfa_system_spmv(edfa_ctx* ctx, const edfa_system* sys, const double* x, double* y) {
     API_BEGIN
-    spmv(&ctx->c, view(sys->A), sys->A.nnz, x, y, 1.0, 0.0, "spmv_A");
+    spmv_sell(&ctx->c, sys->sA, x, y, 1.0, 0.0, "spmv_A");
     API_END
 }
 

@@ -187,6 +187,16 @@ struct Csr {
     DevBuf<double> val;   // may be empty for pattern-only matrices
 };
 
+// SELL-32: slices of 32 consecutive rows, entries column-major inside a slice
+// (row r's k-th entry at slice_ptr[r/32] + 32*k + r%32), padded with zeros
+struct Sell {
+    int32_t n_rows = 0, n_cols = 0;
+    int64_t nnz = 0, stored = 0;
+    DevBuf<int64_t> slice_ptr;   // n_slices + 1
+    DevBuf<int32_t> col;
+    DevBuf<double> val;
+};
+
 // light view passed to kernels
 struct CsrV {
     int32_t n_rows, n_cols;
@@ -213,6 +223,8 @@ void block_merge(Ctx* c, const Csr& A, const Csr& B, const Csr& C, const Csr& D,
 // y = alpha*A x + beta*y
 void spmv(Ctx* c, const CsrV& A, int64_t nnz, const double* x, double* y, double alpha, double beta,
           const char* name = "spmv");
+void build_sell(Ctx* c, const Csr& A, Sell& S);
+void spmv_sell(Ctx* c, const Sell& A, const double* x, double* y, double alpha, double beta, const char* name);
 // S = A - H (row-wise sorted merge, exact zeros dropped, optional row filter)
 void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S);
 // row filter (filter_rows, precond.py:138-157): drop |v| < tau*||row||_2 off-diagonal

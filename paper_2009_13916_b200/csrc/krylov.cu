@@ -282,10 +282,10 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     run_plan(c, ic.bwd, ws.a_f.p, 1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_LT");
     if (nc) {
         EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
-        spmv(c, view(*sys->A_cf), sys->A_cf->nnz, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
+        spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
         run_plan(c, il.fwd, ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L");
         run_plan(c, il.bwd, ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U");
-        spmv(c, view(*sys->A_fc), sys->A_fc->nnz, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
+        spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
     } else if (nf) {
         EDFA_CUDA(cudaMemsetAsync(ws.a_f.p, 0, sizeof(double) * nf, c->stream));
     }
@@ -318,7 +318,7 @@ struct Operator {
     const edfa_stage2* s2;
     ApplyWS ws;
     int64_t n;
-    void A(const double* x, double* y) { spmv(c, view(sys->A), sys->A.nnz, x, y, 1.0, 0.0, "spmv_A"); }
+    void A(const double* x, double* y) { spmv_sell(c, sys->sA, x, y, 1.0, 0.0, "spmv_A"); }
     void P(const double* x, double* y) {
         if (s1 && s2) precond_apply(c, sys, s1, s2, ws, x, y);
         else EDFA_CUDA(cudaMemcpyAsync(y, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));

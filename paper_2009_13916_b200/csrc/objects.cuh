@@ -142,6 +142,7 @@ struct edfa_system {
     const edfa::Csr* A_cf;
     const edfa::Csr* A_cc;
     edfa::Csr A;            // monolithic operator
+    edfa::Sell sA, sAcf, sAfc;   // SELL-32 copies for the SpMVs of the solve
     edfa::Csr AfcT;         // A_fc^T, cells x faces (rows = f-rhs per cell)
     edfa::Csr AffT;         // A_ff^T (columns of A_ff)
     bool have_T = false;

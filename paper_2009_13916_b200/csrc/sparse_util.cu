@@ -98,6 +98,55 @@ __global__ void __launch_bounds__(256) k_spmv(CsrV A, const double* __restrict__
     if (sub == 0) y[row] = (beta == 0.0) ? alpha * s : fma(beta, y[row], alpha * s);
 }
 
+
+// ---------------------------------------------------------------- SELL-32
+__global__ void k_sell_width(const int32_t* __restrict__ ptr, int n, int64_t* __restrict__ w) {
+    const int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int r = s * 32 + lane;
+    int len = r < n ? ptr[r + 1] - ptr[r] : 0;
+    len = warp_max(len);
+    if (lane == 0 && s * 32 < n) w[s] = (int64_t)len * 32;
+}
+__global__ void k_sell_fill(CsrV A, const int64_t* __restrict__ sp, int32_t* __restrict__ col,
+                            double* __restrict__ val) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= A.n_rows) return;
+    const int s = r >> 5, lane = r & 31;
+    const int64_t base = sp[s] + lane, end = sp[s + 1];
+    const int e0 = A.ptr[r], e1 = A.ptr[r + 1];
+    int64_t q = base;
+    for (int e = e0; e < e1; ++e, q += 32) {
+        col[q] = A.idx[e];
+        val[q] = A.val[e];
+    }
+    for (; q < end; q += 32) {
+        col[q] = 0;
+        val[q] = 0.0;
+    }
+}
+// thread per row, sequential sum in column order (as CSR row order)
+__global__ void __launch_bounds__(256) k_spmv_sell(int n, const int64_t* __restrict__ sp,
+                                                   const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                   const double* __restrict__ x, double* __restrict__ y, double alpha,
+                                                   double beta) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int s = r >> 5, lane = r & 31;
+    const int64_t b = sp[s] + lane, e = sp[s + 1];
+    double acc = 0.0;
+    int64_t q = b;
+    for (; q + 3 * 32 < e; q += 4 * 32) {
+        const int c0 = col[q], c1 = col[q + 32], c2 = col[q + 64], c3 = col[q + 96];
+        const double v0 = val[q], v1 = val[q + 32], v2 = val[q + 64], v3 = val[q + 96];
+        acc = fma(v0, __ldg(x + c0), acc);
+        acc = fma(v1, __ldg(x + c1), acc);
+        acc = fma(v2, __ldg(x + c2), acc);
+        acc = fma(v3, __ldg(x + c3), acc);
+    }
+    for (; q < e; q += 32) acc = fma(val[q], __ldg(x + col[q]), acc);
+    y[r] = (beta == 0.0) ? alpha * acc : fma(beta, y[r], alpha * acc);
+}
+
 // S = A - H, thread per row, two passes (count / fill); tau > 0 -> filter_rows
 template <bool FILL>
 __global__ void k_sub(CsrV A, CsrV H, double tau, int32_t* __restrict__ cnt, const int32_t* __restrict__ Sp,
@@ -271,6 +320,43 @@ void spmv(Ctx* c, const CsrV& A, int64_t nnz, const double* x, double* y, double
     else if (avg <= 48.0) launch(k_spmv<16>, 16);
     else launch(k_spmv<32>, 32);
     check_launch("k_spmv");
+}
+
+
+void build_sell(Ctx* c, const Csr& A, Sell& S) {
+    const int n = A.n_rows;
+    S.n_rows = n;
+    S.n_cols = A.n_cols;
+    S.nnz = A.nnz;
+    const int ns = ceil_div(n, 32);
+    S.slice_ptr.reset(c, (size_t)ns + 1);
+    DevBuf<int64_t> w(c, (size_t)ns + 1);
+    EDFA_CUDA(cudaMemsetAsync(w.p, 0, sizeof(int64_t) * (ns + 1), c->stream));
+    if (n) {
+        Prof pr(c, "sell_build", 4.0 * n);
+        k_sell_width<<<ceil_div((int64_t)ns * 32, 256), 256, 0, c->stream>>>(A.ptr.p, n, w.p);
+        check_launch("k_sell_width");
+    }
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, w.p, S.slice_ptr.p, ns + 1, c->stream);
+    EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(bytes), bytes, w.p, S.slice_ptr.p, ns + 1, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(&S.stored, S.slice_ptr.p + ns, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    S.col.reset(c, std::max<int64_t>(S.stored, 1));
+    S.val.reset(c, std::max<int64_t>(S.stored, 1));
+    if (n) {
+        Prof pr(c, "sell_build", 24.0 * S.stored);
+        k_sell_fill<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(A), S.slice_ptr.p, S.col.p, S.val.p);
+        check_launch("k_sell_fill");
+    }
+}
+
+void spmv_sell(Ctx* c, const Sell& A, const double* x, double* y, double alpha, double beta, const char* name) {
+    if (A.n_rows == 0) return;
+    Prof pr(c, name, 12.0 * A.nnz + 4.0 * (A.n_rows + 1) + 8.0 * A.n_cols + 8.0 * A.n_rows * (beta != 0.0 ? 2 : 1));
+    k_spmv_sell<<<ceil_div(A.n_rows, 256), 256, 0, c->stream>>>(A.n_rows, A.slice_ptr.p, A.col.p, A.val.p, x, y,
+                                                               alpha, beta);
+    check_launch("k_spmv_sell");
 }
 
 void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S) {
