@@ -152,6 +152,7 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
     h->c.device = device;
     h->c.stream = static_cast<cudaStream_t>(stream);
     h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
+    EDFA_CUDA(cudaMemsetAsync(h->c.d_scalar_i, 0, 64 * sizeof(int), h->c.stream));   // [60]: reduction ticket
     h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));
     EDFA_CUDA(cudaMallocHost(&h->c.h_pinned, 4096 * sizeof(double)));
     *out = h;

@@ -25,13 +25,35 @@ constexpr int RED_BLOCKS = 3 * NUM_SMS_B200;   // fixed grid -> fixed reduction 
 constexpr int RED_THREADS = 256;
 constexpr int GROUP = 8;                      // vectors per multi-dot block row
 
+// The last block of a reduction kernel to finish (atomic ticket) sums the
+// per-block partials in a fixed order -- the same order as a separate
+// k_reduce_partials launch, so results are identical and deterministic.
+__device__ void last_block_reduce(const double* partial, int nblk, int nvec, double* out, unsigned* counter) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k = wid; k < nvec; k += nw) {
+        double s = 0.0;
+        for (int b = lane; b < nblk; b += 32) s += __ldcg(partial + (int64_t)b * 64 + k);
+        s = warp_sum(s);
+        if (lane == 0) out[k] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
 // partial[blk][k] = sum over the block's rows of V[k0+k] . w   (k < GROUP).
 // VEC2: pairs of rows per thread with 16-byte loads (V rows and w 16-byte
 // aligned, ldv even); the odd tail row is taken by the scalar path.
 template <bool VEC2>
 __global__ void __launch_bounds__(RED_THREADS) k_multidot(const double* __restrict__ V, int64_t ldv, int nvec,
                                                           const double* __restrict__ w, int64_t n,
-                                                          double* __restrict__ partial) {
+                                                          double* __restrict__ partial, double* __restrict__ out,
+                                                          unsigned* counter) {
     int k0 = blockIdx.y * GROUP;
     double acc[GROUP];
 #pragma unroll
@@ -78,6 +100,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_multidot(const double* __restri
         for (int t = 0; t < RED_THREADS / 32; ++t) s += red[threadIdx.x][t];
         partial[(int64_t)blockIdx.x * 64 + k0 + threadIdx.x] = s;
     }
+    last_block_reduce(partial, gridDim.x, nvec, out, counter);
 }
 
 // out[k] = sum_blk partial[blk][k]   (fixed order)
@@ -96,7 +119,8 @@ template <bool VEC2>
 __global__ void __launch_bounds__(RED_THREADS, 3) k_multiaxpy(const double* __restrict__ V, int64_t ldv, int nv,
                                                            const double* __restrict__ h, double hscale,
                                                            const double* w_in, double* out,
-                                                           int64_t n, double* __restrict__ partial) {
+                                                           int64_t n, double* __restrict__ partial,
+                                                           double* __restrict__ norm2, unsigned* counter) {
     __shared__ double hs[64];
     if (threadIdx.x < nv) hs[threadIdx.x] = h[threadIdx.x] * hscale;
     __syncthreads();
@@ -171,6 +195,7 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_multiaxpy(const double* __re
         for (int t = 0; t < RED_THREADS / 32; ++t) s += red[t];
         if (partial) partial[(int64_t)blockIdx.x * 64] = s;
     }
+    if (partial) last_block_reduce(partial, gridDim.x, 1, norm2, counter);
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -214,11 +239,11 @@ struct Blas {
         if (nvec == 0) return;
         dim3 grid(grid_for(n), (nvec + GROUP - 1) / GROUP);
         Prof pr(c, "gs_multidot", 8.0 * n * (nvec + 1));
+        unsigned* cnt = reinterpret_cast<unsigned*>(c->d_scalar_i + 60);
         if ((ldv % 2 == 0 || nvec == 1) && aligned16(V) && aligned16(w))
-            k_multidot<true><<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p);
+            k_multidot<true><<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p, out_dev, cnt);
         else
-            k_multidot<false><<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p);
-        k_reduce_partials<<<nvec, 32, 0, c->stream>>>(partial.p, grid.x, nvec, out_dev);
+            k_multidot<false><<<grid, RED_THREADS, 0, c->stream>>>(V, ldv, nvec, w, n, partial.p, out_dev, cnt);
         check_launch("multidot");
     }
     // out = w_in - V h  (or V h); returns nothing, norm^2 in red[0] when want_norm
@@ -227,13 +252,13 @@ struct Blas {
         int g = grid_for(n);
         Prof pr(c, "gs_multiaxpy", 8.0 * n * (nv + (w_in ? 2 : 1)));
         const bool v2 = (ldv % 2 == 0 || nv <= 1) && aligned16(V) && aligned16(out) && (!w_in || aligned16(w_in));
+        unsigned* cnt = reinterpret_cast<unsigned*>(c->d_scalar_i + 60);
         if (v2)
             k_multiaxpy<true><<<g, RED_THREADS, 0, c->stream>>>(V, ldv, nv, h, hscale, w_in, out, n,
-                                                                 norm2_dev ? partial.p : nullptr);
+                                                                 norm2_dev ? partial.p : nullptr, norm2_dev, cnt);
         else
             k_multiaxpy<false><<<g, RED_THREADS, 0, c->stream>>>(V, ldv, nv, h, hscale, w_in, out, n,
-                                                                  norm2_dev ? partial.p : nullptr);
-        if (norm2_dev) k_reduce_partials<<<1, 32, 0, c->stream>>>(partial.p, g, 1, norm2_dev);
+                                                                  norm2_dev ? partial.p : nullptr, norm2_dev, cnt);
         check_launch("multiaxpy");
     }
     double dot(const double* x, const double* y, int64_t n) {
