@@ -156,6 +156,18 @@ int edfa_pattern_static(edfa_ctx* ctx, int32_t n_cells, int32_t n_faces,
                         const int32_t* face_index, char prototype, int mem,
                         edfa_csr** out);
 
+/* Device-side topology for edfa_pattern_static (hexflow grid.py:100-129,
+ * what patterns.static_patterns derives per call on the host): narrows
+ * elem_to_faces (n_cells x 6) and face_index (n_faces; optional) to int32 and
+ * computes neighbors[e][s] = the other cell of face elem_to_faces[e][s] (-1 on
+ * the boundary) from face_to_elems (n_faces x 2).  All pointers are device
+ * memory; inputs are int32 or int64 (index_bytes 4 / 8). */
+int edfa_grid_topology(edfa_ctx* ctx, int32_t n_cells, int32_t n_faces,
+                       const void* elem_to_faces, const void* face_to_elems,
+                       const void* face_index, int index_bytes,
+                       int32_t* elem_to_faces_out, int32_t* neighbors_out,
+                       int32_t* face_index_out);
+
 /* ---- EDFA stage 1 / stage 2 -------------------------------------------- */
 /* Exactly one of pattern (base/static sets as a CSR pattern over faces) or
  * dyn must be non-NULL (precond.py:217-218). */

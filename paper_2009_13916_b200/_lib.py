@@ -69,6 +69,7 @@ _SIGS = {
     "edfa_system_set_grid": (i32, [vp, i32, i32, i32]),
     "edfa_system_destroy": (i32, [vp]),
     "edfa_pattern_static": (i32, [vp, i32, i32, vp, vp, vp, C.c_char, i32, C.POINTER(vp)]),
+    "edfa_grid_topology": (i32, [vp, i32, i32, vp, vp, vp, i32, vp, vp, vp]),
     "edfa_stage1_build": (i32, [vp, vp, vp, C.POINTER(Dynamic), f64, i32, f64, i32, C.POINTER(vp)]),
     "edfa_stage1_info_get": (i32, [vp, C.POINTER(Stage1Info)]),
     "edfa_stage1_part": (i32, [vp, vp, i32, C.POINTER(vp)]),

@@ -202,6 +202,17 @@ int edfa_pattern_static(edfa_ctx* ctx, int32_t n_cells, int32_t n_faces, const i
     API_END
 }
 
+int edfa_grid_topology(edfa_ctx* ctx, int32_t n_cells, int32_t n_faces, const void* elem_to_faces,
+                       const void* face_to_elems, const void* face_index, int index_bytes, int32_t* elem_to_faces_out,
+                       int32_t* neighbors_out, int32_t* face_index_out) {
+    API_BEGIN
+    require(n_cells >= 0 && n_faces >= 0, EDFA_ERR_VALUE, "negative sizes");
+    require(!face_index == !face_index_out, EDFA_ERR_VALUE, "face_index and face_index_out go together");
+    grid_topology(&ctx->c, n_cells, n_faces, elem_to_faces, face_to_elems, face_index, index_bytes,
+                  elem_to_faces_out, neighbors_out, face_index_out);
+    API_END
+}
+
 // ---------------------------------------------------------------- stage 1 / 2
 int edfa_stage1_build(edfa_ctx* ctx, const edfa_system* sys, const edfa_csr* pattern, const edfa_dynamic* dyn,
                       double tau_filt, int filtration, double face_drop_tol, int no_fill, edfa_stage1** out) {

@@ -10,6 +10,10 @@
 // factorisation DAG is the forward-solve DAG): chain-structured factors are
 // walked one chain per thread, everything else runs as a persistent
 // cooperative kernel with a software grid barrier between levels.
+#include <cub/cub.cuh>
+
+#include <cstdlib>
+
 #include "dev_util.cuh"
 #include "edfa_internal.cuh"
 #include "objects.cuh"
@@ -116,17 +120,16 @@ __global__ void k_ustart(CsrV A, int32_t* __restrict__ us) {
     if (i < A.n_rows) us[i] = lower_bound(A.idx, A.ptr[i], A.ptr[i + 1], i + 1);
 }
 
-template <int RMAX>
-__global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __restrict__ Sp,
-                                              const int32_t* __restrict__ Si, const int32_t* __restrict__ ustart,
-                                              double* __restrict__ LU, const double* __restrict__ scale,
-                                              double* __restrict__ udiag, int* shifts, int* err) {
-    extern __shared__ __align__(16) unsigned char smem[];
+// one row of the ILU(0): IKJ elimination against the (final) pivot rows.
+// SF: sync-free -- pivot rows are awaited through their published pivots
+// (udiag is SENTINEL-filled before the launch).
+template <int RMAX, bool SF>
+__device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, const int32_t* __restrict__ Si,
+                                         const int32_t* __restrict__ ustart, double* __restrict__ LU,
+                                         const double* __restrict__ scale, double* __restrict__ udiag, int* shifts,
+                                         int* err, unsigned char* base, int lane) {
     constexpr int ECAP = ilu0_ecap(RMAX);
     constexpr int SW = ECAP / 32 < 16 ? ECAP / 32 : 16;   // staged entries per lane per round trip
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per-warp scratch: row, pivot metadata, staged U entries of a pivot chunk
-    unsigned char* base = smem + (size_t)wid * ilu0_warp_smem(RMAX);
     double* vals = reinterpret_cast<double*>(base);
     double* pdk = vals + RMAX;
     double* eval = pdk + RMAX;
@@ -136,6 +139,131 @@ __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __res
     int* poff = pcnt + RMAX;           // RMAX + 1
     int* eslot = poff + RMAX + 1;      // ECAP
     int* misc = eslot + ECAP;          // 2
+    int lo = Sp[i], n = Sp[i + 1] - lo;
+    if (n > RMAX) {
+        if (lane == 0) atomicExch(err, 4);
+        if (SF && lane == 0) st_relaxed(udiag + i, 1.0);   // unblock dependants (the factor is discarded)
+        return;
+    }
+    for (int t = lane; t < n; t += 32) {
+        cols[t] = Si[lo + t];
+        vals[t] = LU[lo + t];
+    }
+    __syncwarp();
+    int nl = lower_bound(cols, 0, n, i);
+    // every pivot row is final (earlier level): fetch its pivot and
+    // U-row extent in parallel
+    for (int p = lane; p < nl; p += 32) {
+        int k = cols[p];
+        if (SF) {   // wait for pivot row k (its pivot is published last)
+            double d = ld_relaxed(udiag + k);
+            long long spins = 0;
+            while (is_sentinel(d)) {
+                if (++spins > SPIN_LIMIT) { atomicExch(err, 7); d = 1.0; break; }
+                __nanosleep(32);
+                d = ld_relaxed(udiag + k);
+            }
+            pdk[p] = d;
+        } else {
+            pdk[p] = __ldcg(udiag + k);
+        }
+        int u0 = __ldg(ustart + k);
+        pu0[p] = u0;
+        pcnt[p] = Sp[k + 1] - u0;
+    }
+    if (SF) __threadfence();   // pivot rows' U entries are read after their pivots were seen
+    __syncwarp();
+    for (int p0 = 0; p0 < nl;) {
+        if (lane == 0) {   // chunk of pivots whose U entries fit the staging buffer
+            int acc = 0, p1 = p0;
+            while (p1 < nl && (p1 == p0 || acc + pcnt[p1] <= ECAP)) {
+                poff[p1 - p0] = acc;
+                acc += pcnt[p1];
+                ++p1;
+            }
+            poff[p1 - p0] = acc;
+            misc[0] = p1;
+            misc[1] = min(acc, ECAP);
+        }
+        __syncwarp();
+        const int p1 = misc[0], tot = misc[1];
+        // stage (target slot, u_kj) of every U entry of the chunk
+        for (int f0 = 0; f0 < tot; f0 += 32 * SW) {
+            int e[SW], q[SW];
+            double u[SW];
+            int32_t j[SW];
+#pragma unroll
+            for (int w = 0; w < SW; ++w) {
+                int f = f0 + w * 32 + lane;
+                q[w] = -1;
+                if (f < tot) {
+                    int lo2 = 0, hi2 = p1 - p0;      // pivot owning flat entry f
+                    while (hi2 - lo2 > 1) {
+                        int mid = (lo2 + hi2) >> 1;
+                        if (poff[mid] <= f) lo2 = mid;
+                        else hi2 = mid;
+                    }
+                    q[w] = p0 + lo2;
+                    e[w] = pu0[q[w]] + (f - poff[lo2]);
+                }
+            }
+#pragma unroll
+            for (int w = 0; w < SW; ++w)
+                if (q[w] >= 0) {
+                    j[w] = __ldg(Si + e[w]);
+                    u[w] = __ldcg(LU + e[w]);
+                }
+#pragma unroll
+            for (int w = 0; w < SW; ++w) {
+                int f = f0 + w * 32 + lane;
+                if (q[w] >= 0) {
+                    eslot[f] = bsearch(cols, q[w] + 1, n, j[w]);
+                    eval[f] = u[w];
+                }
+            }
+        }
+        __syncwarp();
+        // eliminate, pivots in increasing column order (reference IKJ order)
+        for (int p = p0; p < p1; ++p) {
+            double mult = __ddiv_rn(vals[p], pdk[p]);
+            __syncwarp();
+            if (lane == 0) vals[p] = mult;
+            const int off = poff[p - p0], cnt = min(pcnt[p], tot - off);
+            for (int f = lane; f < cnt; f += 32) {
+                int s = eslot[off + f];
+                if (s >= 0) vals[s] = sub_mul(vals[s], mult, eval[off + f]);
+            }
+            __syncwarp();
+        }
+        p0 = p1;
+    }
+    int dslot = bsearch(cols, nl, n, i);
+    double piv = dslot >= 0 ? vals[dslot] : 0.0;
+    double g = PIVOT_GUARD * scale[i];
+    if (fabs(piv) < g) {
+        piv = piv >= 0.0 ? g : -g;
+        if (lane == 0) atomicAdd(shifts, 1);
+    }
+    for (int t = lane; t < n; t += 32) __stcg(LU + lo + t, vals[t]);
+    if (SF) {   // publish: row values, fence, then the pivot (the row's ready flag)
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_relaxed(udiag + i, publishable(piv));
+    } else if (lane == 0) {
+        __stcg(udiag + i, piv);
+    }
+    __syncwarp();
+}
+
+// level-synchronous: rows of one level per grid-barrier phase
+template <int RMAX>
+__global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __restrict__ Sp,
+                                              const int32_t* __restrict__ Si, const int32_t* __restrict__ ustart,
+                                              double* __restrict__ LU, const double* __restrict__ scale,
+                                              double* __restrict__ udiag, int* shifts, int* err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem + (size_t)wid * ilu0_warp_smem(RMAX);
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     for (int L = 0; L < la.n_levels; ++L) {
@@ -143,103 +271,52 @@ __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __res
         for (int slot = la.level_start[L] * 32 + gw; slot < t1; slot += nw) {
             int i = la.perm[slot];
             if (i < 0) continue;
-            int lo = Sp[i], n = Sp[i + 1] - lo;
-            if (n > RMAX) {
-                if (lane == 0) atomicExch(err, 4);
-                continue;
-            }
-            for (int t = lane; t < n; t += 32) {
-                cols[t] = Si[lo + t];
-                vals[t] = LU[lo + t];
-            }
-            __syncwarp();
-            int nl = lower_bound(cols, 0, n, i);
-            // every pivot row is final (earlier level): fetch its pivot and
-            // U-row extent in parallel
-            for (int p = lane; p < nl; p += 32) {
-                int k = cols[p];
-                pdk[p] = __ldcg(udiag + k);
-                int u0 = __ldg(ustart + k);
-                pu0[p] = u0;
-                pcnt[p] = Sp[k + 1] - u0;
-            }
-            __syncwarp();
-            for (int p0 = 0; p0 < nl;) {
-                if (lane == 0) {   // chunk of pivots whose U entries fit the staging buffer
-                    int acc = 0, p1 = p0;
-                    while (p1 < nl && (p1 == p0 || acc + pcnt[p1] <= ECAP)) {
-                        poff[p1 - p0] = acc;
-                        acc += pcnt[p1];
-                        ++p1;
-                    }
-                    poff[p1 - p0] = acc;
-                    misc[0] = p1;
-                    misc[1] = min(acc, ECAP);
-                }
-                __syncwarp();
-                const int p1 = misc[0], tot = misc[1];
-                // stage (target slot, u_kj) of every U entry of the chunk
-                for (int f0 = 0; f0 < tot; f0 += 32 * SW) {
-                    int e[SW], q[SW];
-                    double u[SW];
-                    int32_t j[SW];
-#pragma unroll
-                    for (int w = 0; w < SW; ++w) {
-                        int f = f0 + w * 32 + lane;
-                        q[w] = -1;
-                        if (f < tot) {
-                            int lo2 = 0, hi2 = p1 - p0;      // pivot owning flat entry f
-                            while (hi2 - lo2 > 1) {
-                                int mid = (lo2 + hi2) >> 1;
-                                if (poff[mid] <= f) lo2 = mid;
-                                else hi2 = mid;
-                            }
-                            q[w] = p0 + lo2;
-                            e[w] = pu0[q[w]] + (f - poff[lo2]);
-                        }
-                    }
-#pragma unroll
-                    for (int w = 0; w < SW; ++w)
-                        if (q[w] >= 0) {
-                            j[w] = __ldg(Si + e[w]);
-                            u[w] = __ldcg(LU + e[w]);
-                        }
-#pragma unroll
-                    for (int w = 0; w < SW; ++w) {
-                        int f = f0 + w * 32 + lane;
-                        if (q[w] >= 0) {
-                            eslot[f] = bsearch(cols, q[w] + 1, n, j[w]);
-                            eval[f] = u[w];
-                        }
-                    }
-                }
-                __syncwarp();
-                // eliminate, pivots in increasing column order (reference IKJ order)
-                for (int p = p0; p < p1; ++p) {
-                    double mult = __ddiv_rn(vals[p], pdk[p]);
-                    __syncwarp();
-                    if (lane == 0) vals[p] = mult;
-                    const int off = poff[p - p0], cnt = min(pcnt[p], tot - off);
-                    for (int f = lane; f < cnt; f += 32) {
-                        int s = eslot[off + f];
-                        if (s >= 0) vals[s] = sub_mul(vals[s], mult, eval[off + f]);
-                    }
-                    __syncwarp();
-                }
-                p0 = p1;
-            }
-            int dslot = bsearch(cols, nl, n, i);
-            double piv = dslot >= 0 ? vals[dslot] : 0.0;
-            double g = PIVOT_GUARD * scale[i];
-            if (fabs(piv) < g) {
-                piv = piv >= 0.0 ? g : -g;
-                if (lane == 0) atomicAdd(shifts, 1);
-            }
-            for (int t = lane; t < n; t += 32) __stcg(LU + lo + t, vals[t]);
-            if (lane == 0) __stcg(udiag + i, piv);
-            __syncwarp();
+            ilu0_row<RMAX, false>(i, Sp, Si, ustart, LU, scale, udiag, shifts, err, base, lane);
         }
         if (L + 1 < la.n_levels) grid_barrier(la.bar, la.bar + 1, gridDim.x);
+    }
+}
+
+// sync-free: warps take rows from a ticket in a topological order (every
+// dependency of ord[s] precedes it), so a warp only ever waits on rows held by
+// running warps -- no grid barrier, no level plan, a row starts as soon as its
+// own pivot rows are final
+template <int RMAX>
+__global__ void __launch_bounds__(256) k_ilu0_sf(const int* __restrict__ ord, int n_ord, int* ticket,
+                                                 const int32_t* __restrict__ Sp, const int32_t* __restrict__ Si,
+                                                 const int32_t* __restrict__ ustart, double* __restrict__ LU,
+                                                 const double* __restrict__ scale, double* __restrict__ udiag,
+                                                 int* shifts, int* err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem + (size_t)wid * ilu0_warp_smem(RMAX);
+    for (;;) {
+        int s = 0;
+        if (lane == 0) s = atomicAdd(ticket, 1);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= n_ord) break;
+        const int i = ord[s];
+        if (i < 0) continue;
+        ilu0_row<RMAX, true>(i, Sp, Si, ustart, LU, scale, udiag, shifts, err, base, lane);
+    }
+}
+
+// wavefront order of a cell grid: key = i + j + k (x fastest, hx/grid.py:49-50)
+__global__ void k_grid_keys(int n, int nx, int ny, int* __restrict__ key, int* __restrict__ row) {
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    key[e] = e % nx + (e / nx) % ny + e / (nx * ny);
+    row[e] = e;
+}
+// the order is topological iff every strictly-lower entry has key <= the row's
+__global__ void k_grid_order_check(CsrV A, int nx, int ny, int* __restrict__ bad) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n_rows) return;
+    const int ki = i % nx + (i / nx) % ny + i / (nx * ny);
+    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
+        const int j = A.idx[e];
+        if (j >= i) break;
+        if (j % nx + (j / nx) % ny + j / (nx * ny) > ki) { atomicExch(bad, 1); return; }
     }
 }
 
@@ -382,12 +459,42 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         k_diag_scale<<<ceil_div(n, 128), 128, 0, c->stream>>>(view(S), 1.0, dd.p, sc.p, f.has_diag.p);
         check_launch("k_diag_scale");
     }
+    // factorisation schedule: on a cell grid whose lower pattern only reaches
+    // back in i+j+k (true for the axial stencils of base/static patterns) the
+    // wavefront order (i+j+k, row) is topological and the sync-free kernel
+    // runs without a level plan; otherwise rows go level by level
+    const bool grid = dims && n > 0 && dims[0] > 0 && dims[1] > 0 && dims[2] > 0 &&
+                      (int64_t)dims[0] * dims[1] * dims[2] == n;
+    bool sync_free = false;
+    DevBuf<int> ord;
+    if (grid) {
+        PhaseTimer pt(c, "ilu0.wavefront_order");
+        int* bad = c->d_scalar_i + 28;
+        EDFA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+        k_grid_order_check<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(S), dims[0], dims[1], bad);
+        check_launch("k_grid_order_check");
+        DevBuf<int> key(c, n), row(c, n), skey(c, n);
+        ord.reset(c, n);
+        k_grid_keys<<<ceil_div(n, 256), 256, 0, c->stream>>>(n, dims[0], dims[1], key.p, row.p);
+        check_launch("k_grid_keys");
+        int bits = 1;
+        while ((1 << bits) <= dims[0] + dims[1] + dims[2]) ++bits;
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, skey.p, row.p, ord.p, n, 0, bits, c->stream);
+        EDFA_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_scratch(bytes), bytes, key.p, skey.p, row.p, ord.p, n, 0,
+                                                  bits, c->stream));
+        int hb = 0;
+        EDFA_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        sync_free = hb == 0 && !getenv("EDFA_ILU_LEVELS");
+    }
     Csr Lpart;
-    {
+    auto level_plan = [&]() {
         PhaseTimer pt(c, "ilu0.level_plan");
         select_part(c, S, 0, 1.0, false, Lpart);
         build_plan(c, Lpart, nullptr, true, false, f.fwd, /*allow_chain=*/false);
-    }
+    };
+    if (!sync_free) level_plan();
     PhaseTimer pt_fact(c, "ilu0.factor+plans");
     int maxr = n ? max_row_nnz(c, S) : 0;
     require(maxr <= 1024, EDFA_ERR_UNSUPPORTED, "Schur rows longer than 1024 entries are not supported");
@@ -405,20 +512,33 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         double* ud = f.udiag.p;
         int* sh = flags;
         int* er = flags + 1;
+        if (sync_free) fill_bits(c, ud, n, SENTINEL_BITS);   // a row's pivot is its ready flag
         Prof pr(c, "ilu0_factor", 24.0 * S.nnz + 24.0 * n);
         LevelArgs la{f.fwd.perm.p, f.fwd.level_start.p, f.fwd.n_levels, reinterpret_cast<unsigned*>(f.fwd.sync.p)};
+        const int* op = ord.p;
+        int n_ord = n;
+        int* tk = c->d_scalar_i + 29;
+        if (sync_free) EDFA_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), c->stream));
         void* args[] = {&la, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
-        auto launch = [&](auto kern, int rmax) {
+        void* args_sf[] = {&op, &n_ord, &tk, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
+        auto launch = [&](auto kern, auto kern_sf, int rmax) {
             int threads = rmax >= 1024 ? 64 : rmax <= 64 ? 256 : 128;
             size_t smem = ilu0_warp_smem(rmax) * (threads / 32);
+            void* k = sync_free ? (void*)kern_sf : (void*)kern;
             if (smem > 48 * 1024)
-                EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            int grid = coop_grid(kern, threads, smem, 4);
-            EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(threads), args, smem, c->stream));
+                EDFA_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            if (sync_free) {
+                // persistent warps, every resident slot filled (no co-residency requirement)
+                int grid = coop_grid(kern_sf, threads, smem, 8);
+                EDFA_CUDA(cudaLaunchKernel(k, dim3(grid), dim3(threads), args_sf, smem, c->stream));
+            } else {
+                int grid = coop_grid(kern, threads, smem, 4);
+                EDFA_CUDA(cudaLaunchCooperativeKernel(k, dim3(grid), dim3(threads), args, smem, c->stream));
+            }
         };
-        if (maxr <= 64) launch(k_ilu0<64>, 64);
-        else if (maxr <= 256) launch(k_ilu0<256>, 256);
-        else launch(k_ilu0<1024>, 1024);
+        if (maxr <= 64) launch(k_ilu0<64>, k_ilu0_sf<64>, 64);
+        else if (maxr <= 256) launch(k_ilu0<256>, k_ilu0_sf<256>, 256);
+        else launch(k_ilu0<1024>, k_ilu0_sf<1024>, 1024);
     }
     int err = 0;
     read_flags(c, flags, &f.shifts, &err);
@@ -429,7 +549,11 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
     // cell-grid factors: tile-DAG solves; otherwise level-synchronous plans
     if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
         f.fwd.is_tile = true;
+        f.fwd.n = n;
+        f.fwd.n_dep = Lv.nnz;
+        f.fwd.n_levels = f.fwd.tile.n_tile_levels;
     } else {
+        if (sync_free) level_plan();
         plan_values(c, Lv, nullptr, f.fwd);
     }
     if (dims && build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile)) {

@@ -28,6 +28,8 @@ void pattern_compact(Ctx* c, int32_t n, const DevBuf<int32_t>& slot_ptr, const D
                      const DevBuf<int32_t>& q, int32_t n_cols, Csr& out);
 void static_pattern(Ctx* c, int32_t n_cells, int32_t n_free, const int32_t* e2f, const int32_t* nbr,
                     const int32_t* fidx, char proto, Csr& out);
+void grid_topology(Ctx* c, int32_t n_cells, int32_t n_faces, const void* e2f, const void* f2e, const void* fidx,
+                   int index_bytes, int32_t* e2f_out, int32_t* nbr_out, int32_t* fidx_out);
 int max_row_nnz(Ctx* c, const Csr& A);
 int max_value_plus_one(Ctx* c, const int32_t* v, int n);
 

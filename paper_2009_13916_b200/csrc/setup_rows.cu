@@ -537,7 +537,42 @@ __global__ void k_copy_rows(int32_t n, const int32_t* __restrict__ sp, const int
     if (w >= n) return;
     for (int i = lane; i < sz[w]; i += 32) dst[dp[w] + i] = src[sp[w] + i];
 }
+// cell -> faces (narrowed to int32) and cell -> neighbour across each face
+// (hx/grid.py:100-129: face_to_elems[f] = (lower cell, upper cell or -1))
+template <typename I>
+__global__ void k_grid_topology(int32_t n_cells, int32_t n_faces, const I* __restrict__ e2f,
+                                const I* __restrict__ f2e, const I* __restrict__ fidx, int32_t* __restrict__ e2f_out,
+                                int32_t* __restrict__ nbr_out, int32_t* __restrict__ fidx_out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < (int64_t)n_cells * 6) {
+        const int32_t e = (int32_t)(t / 6);
+        const int32_t f = (int32_t)e2f[t];
+        const int32_t a = (int32_t)f2e[2 * (int64_t)f], b = (int32_t)f2e[2 * (int64_t)f + 1];
+        e2f_out[t] = f;
+        nbr_out[t] = a == e ? b : a;
+    }
+    if (fidx_out && t < n_faces) fidx_out[t] = (int32_t)fidx[t];
+}
+
 }  // namespace
+
+void grid_topology(Ctx* c, int32_t n_cells, int32_t n_faces, const void* e2f, const void* f2e, const void* fidx,
+                   int index_bytes, int32_t* e2f_out, int32_t* nbr_out, int32_t* fidx_out) {
+    require(index_bytes == 4 || index_bytes == 8, EDFA_ERR_VALUE, "index_bytes must be 4 or 8");
+    const int64_t work = std::max<int64_t>((int64_t)n_cells * 6, n_faces);
+    if (work == 0) return;
+    Prof pr(c, "grid_topology", (index_bytes + 12.0) * 6 * n_cells + (index_bytes + 4.0) * n_faces);
+    const int blocks = (int)ceil_div(work, (int64_t)256);
+    if (index_bytes == 8)
+        k_grid_topology<int64_t><<<blocks, 256, 0, c->stream>>>(
+            n_cells, n_faces, static_cast<const int64_t*>(e2f), static_cast<const int64_t*>(f2e),
+            static_cast<const int64_t*>(fidx), e2f_out, nbr_out, fidx ? fidx_out : nullptr);
+    else
+        k_grid_topology<int32_t><<<blocks, 256, 0, c->stream>>>(
+            n_cells, n_faces, static_cast<const int32_t*>(e2f), static_cast<const int32_t*>(f2e),
+            static_cast<const int32_t*>(fidx), e2f_out, nbr_out, fidx ? fidx_out : nullptr);
+    check_launch("k_grid_topology");
+}
 
 void copy_rows(Ctx* c, int32_t n, const int32_t* sp, const int32_t* sz, const int32_t* src, const int32_t* dp,
                int32_t* dst) {

@@ -134,7 +134,9 @@ class DeviceSystem:
     free faces first, then cells).  Keeps the host system for metadata."""
 
     def __init__(self, A_ff: DeviceCsr, A_fc: DeviceCsr, A_cf: DeviceCsr, A_cc: DeviceCsr,
-                 rhs=None, host=None):
+                 rhs=None, host=None, topology_src=None):
+        """``topology_src`` = (elem_to_faces, face_to_elems, face_index) of the
+        grid, host arrays or CUDA tensors (default: the host system's grid)."""
         self.A_ff, self.A_fc, self.A_cf, self.A_cc = A_ff, A_fc, A_cf, A_cc
         self.host = host
         self.handle = C.c_void_p()
@@ -147,13 +149,10 @@ class DeviceSystem:
         if grid is not None and all(hasattr(grid, a) for a in ("nx", "ny", "nz")) \
                 and grid.nx * grid.ny * grid.nz == self.n_cells:
             self.set_grid(grid.nx, grid.ny, grid.nz)
-        if grid is not None and hasattr(host, "face_index"):
-            # cell->face map, neighbours and free-face index, resident with the
-            # blocks (inputs of the static-pattern kernel)
-            from .patterns import grid_topology
-            e2f, nbr = grid_topology(grid)
-            self.topology = tuple(torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to("cuda")
-                                  for a in (e2f, nbr, np.asarray(host.face_index)))
+        if topology_src is not None:
+            self.topology = device_topology(*topology_src)
+        elif grid is not None and hasattr(host, "face_index") and hasattr(grid, "face_to_elems"):
+            self.topology = device_topology(grid.elem_to_faces, grid.face_to_elems, host.face_index)
 
     def set_grid(self, nx: int, ny: int, nz: int) -> None:
         """Declare cells as the natural-order cells of an nx*ny*nz box
@@ -220,6 +219,32 @@ class DeviceSystem:
             self.handle = None
 
 
+def _upload_index(a) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to("cuda").contiguous()
+    a = np.asarray(a)
+    if a.dtype not in (np.int32, np.int64):
+        a = a.astype(np.int64)
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=True)
+
+
+def device_topology(elem_to_faces, face_to_elems, face_index):
+    """(elem_to_faces, neighbours, face_index) as int32 CUDA tensors -- the
+    inputs of the static-pattern kernel.  The grid's own index arrays are
+    uploaded as they are (int32 or int64); narrowing and the neighbour map
+    (hx/grid.py:100-129) are computed on the device (edfa_grid_topology)."""
+    e2f_h, f2e_h, fidx_h = (_upload_index(a) for a in (elem_to_faces, face_to_elems, face_index))
+    if not (e2f_h.dtype == f2e_h.dtype == fidx_h.dtype):
+        e2f_h, f2e_h, fidx_h = (t.to(torch.int64) for t in (e2f_h, f2e_h, fidx_h))
+    n_cells, n_faces = int(e2f_h.shape[0]), int(fidx_h.numel())
+    e2f = torch.empty((n_cells, 6), dtype=torch.int32, device="cuda")
+    nbr = torch.empty((n_cells, 6), dtype=torch.int32, device="cuda")
+    fidx = torch.empty(n_faces, dtype=torch.int32, device="cuda")
+    L.check(L.lib().edfa_grid_topology(ctx(), n_cells, n_faces, dptr(e2f_h), dptr(f2e_h), dptr(fidx_h),
+                                       e2f_h.element_size(), dptr(e2f), dptr(nbr), dptr(fidx)))
+    return e2f, nbr, fidx
+
+
 class SystemOperator:
     """``A_apply`` callable of the monolithic block operator on the device;
     recognised by :func:`krylov.gmres`/`bicgstab` for the fused solver path."""
@@ -241,7 +266,7 @@ def pinned_copy(system):
     """Copy of a BlockSystem whose block arrays and right-hand side live in
     page-locked host memory, so ``DeviceSystem.from_host`` uploads them by DMA
     at full PCIe/C2C bandwidth (the staging a host application keeps between
-    time steps).  Grid/topology fields are shared, not copied."""
+    time steps), the grid's index arrays included."""
     import dataclasses
 
     def pin(a):
@@ -254,6 +279,12 @@ def pinned_copy(system):
                               pin(M.indptr.astype(np.int32, copy=False))), shape=M.shape, copy=False)
 
     repl = {n: pin_csr(getattr(system, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc")}
+    grid = getattr(system, "grid", None)
+    if grid is not None and dataclasses.is_dataclass(grid) and hasattr(grid, "face_to_elems"):
+        repl["grid"] = dataclasses.replace(grid, elem_to_faces=pin(grid.elem_to_faces),
+                                           face_to_elems=pin(grid.face_to_elems))
+    if hasattr(system, "face_index"):
+        repl["face_index"] = pin(system.face_index)
     for n in ("rhs_f", "rhs_c"):
         if hasattr(system, n):
             repl[n] = pin(getattr(system, n))
