@@ -12,6 +12,7 @@
 // per iteration; block partial sums reduced in a fixed order (deterministic).
 // Givens rotations and the small triangular solve run on the host.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "dev_util.cuh"
@@ -198,6 +199,293 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_multiaxpy(const double* __re
     if (partial) last_block_reduce(partial, gridDim.x, 1, norm2, counter);
 }
 
+// ---------------------------------------------------------------- DCGS2 Arnoldi step
+// One reduction per Arnoldi step (delayed classical Gram-Schmidt with
+// re-orthogonalisation; the re-orthogonalisation of u_j is folded into the
+// projection of the next Krylov vector).  Step j holds final q_0..q_{j-1}
+// (slots 0..j-1), u_j = A P q_{j-1} - Q_j h1 after ONE projection pass (slot
+// j, unnormalised) and w = A P u_j (slot j+1).
+//   dots:  [Q_j u]^T u = (a, alpha), [Q_j u]^T w = (b, beta)      (one pass)
+//   nu = sqrt(alpha - a.a),  q_j = (u - Q_j a) / nu
+//   H[:j, j-1] = h1 + a,  H[j, j-1] = nu                 (column j-1 final)
+//   A P q_j = (w - Q_{j+1} t) / nu with t = H[:j+1, :j] a  (Arnoldi relation)
+//   c = Q_{j+1}^T A P q_j,  u_{j+1} = A P q_j - Q_{j+1} c    (one pass)
+// so each step reads the basis twice (dots, update) instead of CGS2's four
+// times; in exact arithmetic the columns equal CGS2's.
+constexpr int D2_GROUP = 8;
+
+// dots of V_0..V_{nv-1} with u = V_{nv-1} and w = V_{nv}: grid (groups, ranges),
+// block-contiguous element ranges so the blocks sharing a range run together
+// and u, w come from L2 after the first group.  partial[r][0..63] = u-dots,
+// [64..127] = w-dots.
+template <bool VEC2>
+__global__ void __launch_bounds__(RED_THREADS) k_dots2(const double* __restrict__ V, int64_t ldv, int nv, int64_t n,
+                                                       int64_t range, double* __restrict__ partial,
+                                                       unsigned* counter, int j, int m, double* __restrict__ H,
+                                                       double* __restrict__ h1, double* __restrict__ coef,
+                                                       double* __restrict__ hcol) {
+    const int k0 = blockIdx.x * D2_GROUP;
+    const double* u = V + (int64_t)(nv - 1) * ldv;
+    const double* w = V + (int64_t)nv * ldv;
+    double au[D2_GROUP], aw[D2_GROUP];
+#pragma unroll
+    for (int k = 0; k < D2_GROUP; ++k) au[k] = aw[k] = 0.0;
+    const int64_t lo = blockIdx.y * range, hi = min(n, lo + range);
+    if (VEC2) {   // range is even, rows 16-byte aligned
+        const int64_t lo2 = lo >> 1, hi2 = hi >> 1;
+        for (int64_t i = lo2 + threadIdx.x; i < hi2; i += RED_THREADS) {
+            const double2 ui = reinterpret_cast<const double2*>(u)[i];
+            const double2 wi = reinterpret_cast<const double2*>(w)[i];
+            double2 v[D2_GROUP];
+#pragma unroll
+            for (int k = 0; k < D2_GROUP; ++k)
+                if (k0 + k < nv) v[k] = reinterpret_cast<const double2*>(V + (int64_t)(k0 + k) * ldv)[i];
+#pragma unroll
+            for (int k = 0; k < D2_GROUP; ++k)
+                if (k0 + k < nv) {
+                    au[k] = fma(v[k].y, ui.y, fma(v[k].x, ui.x, au[k]));
+                    aw[k] = fma(v[k].y, wi.y, fma(v[k].x, wi.x, aw[k]));
+                }
+        }
+        if ((hi & 1) && hi == n && threadIdx.x == 0) {
+            const int64_t i = n - 1;
+#pragma unroll
+            for (int k = 0; k < D2_GROUP; ++k)
+                if (k0 + k < nv) {
+                    const double vk = V[(int64_t)(k0 + k) * ldv + i];
+                    au[k] = fma(vk, u[i], au[k]);
+                    aw[k] = fma(vk, w[i], aw[k]);
+                }
+        }
+    } else {
+        for (int64_t i = lo + threadIdx.x; i < hi; i += RED_THREADS) {
+            const double ui = u[i], wi = w[i];
+#pragma unroll
+            for (int k = 0; k < D2_GROUP; ++k)
+                if (k0 + k < nv) {
+                    const double vk = V[(int64_t)(k0 + k) * ldv + i];
+                    au[k] = fma(vk, ui, au[k]);
+                    aw[k] = fma(vk, wi, aw[k]);
+                }
+        }
+    }
+    __shared__ double red[2 * D2_GROUP][RED_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < D2_GROUP; ++k) {
+        const double x = warp_sum(au[k]), y = warp_sum(aw[k]);
+        if (lane == 0) { red[k][wid] = x; red[D2_GROUP + k][wid] = y; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * D2_GROUP) {
+        const int k = threadIdx.x % D2_GROUP, side = threadIdx.x / D2_GROUP;
+        if (k0 + k < nv) {
+            double t = 0.0;
+            for (int q = 0; q < RED_THREADS / 32; ++q) t += red[threadIdx.x][q];
+            partial[(int64_t)blockIdx.y * 128 + side * 64 + k0 + k] = t;
+        }
+    }
+    // last block: fixed-order sum over ranges, then the step's coefficients
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // warp w sums partial rows w, w+8, ... (lanes over the 128 slots, coalesced),
+    // then the 8 warp sums are added in a fixed order: deterministic
+    __shared__ double dot[128];
+    __shared__ double wsum[RED_THREADS / 32][128];
+    {
+        const int nr = gridDim.y, nw = RED_THREADS / 32;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int b = wid;
+        for (; b + 3 * nw < nr; b += 4 * nw) {
+            double v[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[u][q] = __ldcg(partial + (int64_t)(b + u * nw) * 128 + q * 32 + lane);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] += v[u][q];
+        }
+        for (; b < nr; b += nw)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] += __ldcg(partial + (int64_t)b * 128 + q * 32 + lane);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) wsum[wid][q * 32 + lane] = acc[q];
+        __syncthreads();
+        if (threadIdx.x < 128) {
+            double t = 0.0;
+            for (int q = 0; q < nw; ++q) t += wsum[q][threadIdx.x];
+            dot[threadIdx.x] = t;
+        }
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    __syncthreads();
+    // coefficients (j = nv - 1):  coef[0..63] = q_j weights, [64..127] = u_{j+1}
+    // weights, coef[128..130] = (1/nu, 1/nu, -d_j/nu)
+    const int ld = m + 1, tid = threadIdx.x;
+    __shared__ double sa[64], st[64], sd[64], s_aa, s_ab, s_nu;
+    if (j == 0) {   // u_0 = q_0 is final: first projection only
+        if (tid == 0) {
+            const double c0 = dot[64];
+            h1[0] = c0;
+            coef[128] = 1.0;
+            coef[129] = 1.0;
+            coef[130] = -c0;
+        }
+        return;
+    }
+    if (tid < j) sa[tid] = dot[tid];
+    __syncthreads();
+    if (wid == 0) {
+        double aa = 0.0, ab = 0.0;
+        for (int i = lane; i < j; i += 32) {
+            aa = fma(sa[i], sa[i], aa);
+            ab = fma(sa[i], dot[64 + i], ab);
+        }
+        aa = warp_sum(aa);
+        ab = warp_sum(ab);
+        if (lane == 0) {
+            s_aa = aa;
+            s_ab = ab;
+            const double nu2 = dot[j] - aa;
+            s_nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+        }
+    }
+    __syncthreads();
+    const double nu = s_nu;
+    double* col = H + (int64_t)(j - 1) * ld;
+    if (tid < j) {
+        const double v = h1[tid] + sa[tid];
+        col[tid] = v;
+        hcol[tid] = v;
+    }
+    if (tid == j) { col[j] = nu; hcol[j] = nu; }
+    __syncthreads();
+    if (nu == 0.0) {   // happy breakdown: column j-1 ends the cycle
+        if (tid < 64) { coef[tid] = 0.0; coef[64 + tid] = 0.0; }
+        if (tid == 0) { coef[128] = 0.0; coef[129] = 0.0; coef[130] = 0.0; }
+        return;
+    }
+    const double inv = 1.0 / nu;
+    {   // t = H[:j+1, :j] a  (H[r, i] = 0 for r > i + 1): thread (r, quarter) loads
+        // its <= 16 entries at once, quarters summed in order
+        __shared__ double tq[4][64];
+        const int r = tid & 63, qt = tid >> 6;
+        double hv[16];
+        int ii[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int i = qt + 4 * u;
+            ii[u] = i;
+            hv[u] = (r <= j && i < j && i >= r - 1) ? H[(int64_t)i * ld + r] : 0.0;
+        }
+        double t = 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (ii[u] < j) t = fma(hv[u], sa[ii[u]], t);
+        tq[qt][r] = t;
+        __syncthreads();
+        if (tid <= j) st[tid] = ((tq[0][tid] + tq[1][tid]) + tq[2][tid]) + tq[3][tid];
+    }
+    __syncthreads();
+    if (tid <= j) {
+        const double c = tid < j ? (dot[64 + tid] - st[tid]) * inv
+                                 : ((dot[64 + j] - s_ab) * inv - st[j]) * inv;
+        sd[tid] = st[tid] * inv + c;
+        h1[tid] = c;
+    }
+    __syncthreads();
+    if (tid < j) {
+        coef[tid] = sa[tid] * inv;
+        coef[64 + tid] = sd[tid] - sd[j] * sa[tid] * inv;
+    }
+    if (tid == 0) {
+        coef[128] = inv;
+        coef[129] = inv;
+        coef[130] = -sd[j] * inv;
+    }
+}
+
+// slot j  <- q_j     = coef[128] u - sum_k coef[k] V_k          (j >= 1)
+// slot j+1 <- u_{j+1} = coef[129] w + coef[130] u - sum_k coef[64+k] V_k
+template <bool VEC2>
+__global__ void __launch_bounds__(RED_THREADS, 3) k_axpy2(double* __restrict__ V, int64_t ldv, int j, int64_t n,
+                                                          const double* __restrict__ coef) {
+    __shared__ double cq[64], cw[64], sc[3];
+    if (threadIdx.x < j) {
+        cq[threadIdx.x] = coef[threadIdx.x];
+        cw[threadIdx.x] = coef[64 + threadIdx.x];
+    }
+    if (threadIdx.x < 3) sc[threadIdx.x] = coef[128 + threadIdx.x];
+    __syncthreads();
+    double* u = V + (int64_t)j * ldv;
+    double* w = u + ldv;
+    const double su = sc[0], sw = sc[1], suw = sc[2];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (VEC2) {
+        const int64_t n2 = n >> 1;
+        for (int64_t i = t0; i < n2; i += stride) {
+            double qx = 0.0, qy = 0.0, ex = 0.0, ey = 0.0;
+            int k = 0;
+            for (; k + 8 <= j; k += 8) {
+                double2 a[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) a[t] = reinterpret_cast<const double2*>(V + (int64_t)(k + t) * ldv)[i];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    qx = fma(cq[k + t], a[t].x, qx);
+                    qy = fma(cq[k + t], a[t].y, qy);
+                    ex = fma(cw[k + t], a[t].x, ex);
+                    ey = fma(cw[k + t], a[t].y, ey);
+                }
+            }
+            for (; k < j; ++k) {
+                const double2 a = reinterpret_cast<const double2*>(V + (int64_t)k * ldv)[i];
+                qx = fma(cq[k], a.x, qx);
+                qy = fma(cq[k], a.y, qy);
+                ex = fma(cw[k], a.x, ex);
+                ey = fma(cw[k], a.y, ey);
+            }
+            const double2 uv = reinterpret_cast<const double2*>(u)[i];
+            const double2 wv = reinterpret_cast<const double2*>(w)[i];
+            if (j > 0) reinterpret_cast<double2*>(u)[i] = make_double2(su * uv.x - qx, su * uv.y - qy);
+            reinterpret_cast<double2*>(w)[i] =
+                make_double2(fma(sw, wv.x, suw * uv.x) - ex, fma(sw, wv.y, suw * uv.y) - ey);
+        }
+        if ((n & 1) && t0 == 0) {
+            const int64_t i = n - 1;
+            double q = 0.0, e = 0.0;
+            for (int k = 0; k < j; ++k) {
+                const double a = V[(int64_t)k * ldv + i];
+                q = fma(cq[k], a, q);
+                e = fma(cw[k], a, e);
+            }
+            const double uv = u[i], wv = w[i];
+            if (j > 0) u[i] = su * uv - q;
+            w[i] = fma(sw, wv, suw * uv) - e;
+        }
+    } else {
+        for (int64_t i = t0; i < n; i += stride) {
+            double q = 0.0, e = 0.0;
+            for (int k = 0; k < j; ++k) {
+                const double a = V[(int64_t)k * ldv + i];
+                q = fma(cq[k], a, q);
+                e = fma(cw[k], a, e);
+            }
+            const double uv = u[i], wv = w[i];
+            if (j > 0) u[i] = su * uv - q;
+            w[i] = fma(sw, wv, suw * uv) - e;
+        }
+    }
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 __global__ void k_axpby(int64_t n, double a, const double* x, double b, double* y) {
@@ -260,6 +548,39 @@ struct Blas {
             k_multiaxpy<false><<<g, RED_THREADS, 0, c->stream>>>(V, ldv, nv, h, hscale, w_in, out, n,
                                                                   norm2_dev ? partial.p : nullptr, norm2_dev, cnt);
         check_launch("multiaxpy");
+    }
+    // DCGS2 step j on basis V (ld n): dots + coefficients, then the update
+    void dcgs2_step(double* V, int64_t n, int j, int m, double* H, double* h1, double* coef, double* hcol,
+                    double* part2, int part2_rows) {
+        const int nv = j + 1;
+        const int groups = (nv + D2_GROUP - 1) / D2_GROUP;
+        int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((4 * NUM_SMS_B200) / groups, (n + 511) / 512));
+        ranges = std::max<int64_t>(ranges, std::min<int64_t>(NUM_SMS_B200, (n + 511) / 512));
+        ranges = std::min<int64_t>(ranges, part2_rows);
+        int64_t range = (n + ranges - 1) / ranges;
+        range = (range + 1) & ~int64_t(1);
+        ranges = (n + range - 1) / range;
+        unsigned* cnt = reinterpret_cast<unsigned*>(c->d_scalar_i + 60);
+        const bool v2 = n % 2 == 0 && aligned16(V);
+        {
+            Prof pr(c, "gs_dots2", 8.0 * n * (nv + 1));
+            dim3 grid(groups, (unsigned)ranges);
+            if (v2)
+                k_dots2<true><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, cnt, j, m, H, h1, coef,
+                                                                  hcol);
+            else
+                k_dots2<false><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, cnt, j, m, H, h1,
+                                                                   coef, hcol);
+            check_launch("dots2");
+        }
+        {
+            Prof pr(c, "gs_axpy2", 8.0 * n * (nv + 1) + 8.0 * n * (j > 0 ? 2 : 1));
+            if (v2)
+                k_axpy2<true><<<grid_for(n), RED_THREADS, 0, c->stream>>>(V, n, j, n, coef);
+            else
+                k_axpy2<false><<<grid_for(n), RED_THREADS, 0, c->stream>>>(V, n, j, n, coef);
+            check_launch("axpy2");
+        }
     }
     double dot(const double* x, const double* y, int64_t n) {
         // x . y through the multidot path with V = x as a single vector
@@ -360,8 +681,8 @@ static void check_trsv_error(Ctx* c) {
     }
 }
 
-void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b, double* x,
-           double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap) {
+static void gmres_cgs2(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b,
+                       double* x, double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap) {
     // Arnoldi with classical Gram-Schmidt applied twice (CGS2): two fused
     // multi-dot + multi-axpy(+norm) passes, normalisation by a device-side
     // norm.  The host never waits inside a cycle for the step it just
@@ -459,6 +780,127 @@ void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_sta
         for (int i = 0; i < k; ++i) hpin[384 + i] = y[i];
         double* yd = hd.p + 2 * 192;
         EDFA_CUDA(cudaMemcpyAsync(yd, hpin + 384, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
+        bl.multiaxpy(V.p, n, k, yd, 1.0, nullptr, r.p, n, nullptr);   // r <- V y (scratch)
+        op.P(r.p, z.p);
+        bl.axpby(n, 1.0, z.p, 1.0, x);
+        op.A(x, r.p);
+        bl.axpby(n, 1.0, b, -1.0, r.p);                                   // r = b - A x
+        beta = std::sqrt(bl.dot(r.p, r.p, n));
+        check_trsv_error(c);
+        if (beta / bnorm <= rtol) { rep->converged = 1; break; }
+        if (happy || beta == 0.0) { rep->breakdown = 1; break; }
+    }
+    c->event_pool.push_back(ev[0]);
+    c->event_pool.push_back(ev[1]);
+    rep->final_relres = beta / bnorm;
+    if (rep->n_it == 0) push_hist(beta / bnorm);
+}
+
+void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b, double* x,
+           double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap) {
+    // Right-preconditioned restarted GMRES(m), x0 = 0 (hx/krylov.py
+    // conventions), Arnoldi by DCGS2 (k_dots2 / k_axpy2: one
+    // reduction and two basis passes per step).  Step s applies A P to u_s and
+    // finalises Hessenberg column s-1 on the device; the host enqueues step
+    // s+1 before reading column s-1 back (pinned copy + event), applies the
+    // Givens rotations and tests the estimate, so the GPU never idles between
+    // steps.  Speculatively enqueued steps only touch slots above the ones the
+    // solution update reads.  Convergence is confirmed on the true residual.
+    if (getenv("EDFA_GMRES_CGS2")) {
+        gmres_cgs2(c, sys, s1, s2, b, x, rtol, m, max_it, rep, hist, hist_cap);
+        return;
+    }
+    require(rtol > 0.0, EDFA_ERR_VALUE, "tol must be positive");
+    require(m >= 1 && m <= 62, EDFA_ERR_VALUE, "restart must be in [1, 62]");
+    require(max_it >= 0, EDFA_ERR_VALUE, "max_it must be >= 0");
+    const int64_t n = (int64_t)sys->A.n_rows;
+    Operator op{c, sys, s1, s2, {}, n};
+    Blas bl(c);
+    *rep = edfa_report{0, 0, 0, 0, INFINITY};
+    auto push_hist = [&](double v) {
+        if (hist && rep->n_hist < hist_cap) hist[rep->n_hist] = v;
+        rep->n_hist++;
+    };
+    double bnorm = std::sqrt(bl.dot(b, b, n));
+    if (bnorm == 0.0) {
+        EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+        rep->converged = 1;
+        rep->final_relres = 0.0;
+        push_hist(0.0);
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    const int ld = m + 1;
+    const int part_rows = 4 * NUM_SMS_B200;
+    // device state: basis (m+2 slots), Hessenberg (unrotated, (m+1) x m col-major),
+    // first-pass coefficients, update coefficients, per-step column slots (parity s & 1)
+    DevBuf<double> V(c, (size_t)(m + 2) * n), z(c, n), r(c, n), Hd(c, (size_t)ld * m), h1(c, 64), coef(c, 192),
+        hcol(c, 2 * 64 + 64), part2(c, (size_t)part_rows * 128);
+    double* hpin = c->h_pinned;   // 2 x 64 host column slots + 64 for y
+    cudaEvent_t ev[2] = {c->get_event(), c->get_event()};
+    EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    double beta = bnorm;
+    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+    bool happy = false;
+    auto enqueue_step = [&](int st) {
+        double* us = V.p + (int64_t)st * n;
+        double* w = us + n;
+        op.P(us, z.p);
+        op.A(z.p, w);
+        double* hc = hcol.p + (st & 1) * 64;
+        bl.dcgs2_step(V.p, n, st, m, Hd.p, h1.p, coef.p, hc, part2.p, part_rows);
+        if (st >= 1) {
+            EDFA_CUDA(cudaMemcpyAsync(hpin + (st & 1) * 64, hc, sizeof(double) * (st + 1), cudaMemcpyDeviceToHost,
+                                      c->stream));
+            EDFA_CUDA(cudaEventRecord(ev[st & 1], c->stream));
+        }
+    };
+    while (rep->n_it < max_it) {
+        bl.axpby(n, 1.0 / beta, r.p, 0.0, V.p);
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int k = 0;
+        const int budget = std::min(m, max_it - rep->n_it);   // columns this cycle
+        int enq = 0;                                          // steps enqueued (step s finalises column s-1)
+        enqueue_step(enq++);
+        enqueue_step(enq++);
+        for (int j = 0; j < budget; ++j) {
+            if (enq <= budget) enqueue_step(enq++);            // keep one step ahead of the host
+            EDFA_CUDA(cudaEventSynchronize(ev[(j + 1) & 1]));
+            const double* hp = hpin + ((j + 1) & 1) * 64;
+            rep->n_it++;
+            for (int i = 0; i <= j + 1; ++i) H[(size_t)i * m + j] = hp[i];
+            const double wn = hp[j + 1];
+            for (int i = 0; i < j; ++i) {
+                double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
+                H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
+                H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
+            }
+            double den = std::hypot(H[(size_t)j * m + j], H[(size_t)(j + 1) * m + j]);
+            if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
+            else { cs[j] = H[(size_t)j * m + j] / den; sn[j] = H[(size_t)(j + 1) * m + j] / den; }
+            H[(size_t)j * m + j] = den;
+            H[(size_t)(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            double est = std::fabs(g[j + 1]) / bnorm;
+            push_hist(est);
+            k = j + 1;
+            if (wn == 0.0) { happy = true; break; }
+            if (est <= rtol) break;
+        }
+        // speculatively enqueued steps may still be running: everything below is
+        // stream-ordered after them and reads only slots 0..k-1, which they never write
+        for (int i = k - 1; i >= 0; --i) {   // back substitution H y = g
+            double sacc = g[i];
+            for (int t = i + 1; t < k; ++t) sacc -= H[(size_t)i * m + t] * y[t];
+            y[i] = H[(size_t)i * m + i] != 0.0 ? sacc / H[(size_t)i * m + i] : 0.0;
+        }
+        for (int i = 0; i < k; ++i) hpin[128 + i] = y[i];
+        double* yd = hcol.p + 128;
+        EDFA_CUDA(cudaMemcpyAsync(yd, hpin + 128, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
         bl.multiaxpy(V.p, n, k, yd, 1.0, nullptr, r.p, n, nullptr);   // r <- V y (scratch)
         op.P(r.p, z.p);
         bl.axpby(n, 1.0, z.p, 1.0, x);

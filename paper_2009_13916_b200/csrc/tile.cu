@@ -402,6 +402,7 @@ struct TileSolve {
     const short* xlev_ptr;
     const unsigned char* req;
     int mode;             // EDFA_TILE_MODE experiment bits (diagnostics)
+    long long* dbg2;      // per-group timestamps (diagnostics): [tile][64][5]
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -868,6 +869,304 @@ __global__ void __launch_bounds__(PIPE_THREADS) k_tile_pipe(TileSolve a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Dataflow tile solve: no per-level barrier.  Every x slot of the tile (its
+// rows and its externals) starts as the SENTINEL pattern in shared memory, so
+// a stored value is its own ready flag there too.
+//   * compute warps take the tile's 32-row groups (rows of one local level) in
+//     level order, round robin; a lane folds its row's early dependencies
+//     (older levels, externals) as soon as they are present, then its <= 3
+//     critical ones (previous level), stores x to shared memory and HBM;
+//   * the loader warp copies externals (HBM, polled in need order) into their
+//     shared slots as they appear.
+// A level therefore costs one shared-memory hand-off plus a short FMA chain
+// instead of a CTA barrier plus the slowest warp, and a downstream tile's row
+// starts as soon as its own externals exist.
+__device__ __forceinline__ double ld_vol_s(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
+__device__ __forceinline__ void st_vol_s(double* p, double v) { *reinterpret_cast<volatile double*>(p) = v; }
+#ifndef FLOW_SLEEP_NS
+#define FLOW_SLEEP_NS 16
+#endif
+__device__ __forceinline__ double poll_s(const double* p, int* err) {
+    double v = ld_vol_s(p);
+    if (is_sentinel(v)) {
+        long long spins = 0;
+        do {   // back off: spinning warps must not crowd the shared-memory pipe
+            if (++spins > SPIN_LIMIT) { atomicExch(err, 7); return 0.0; }
+            __nanosleep(FLOW_SLEEP_NS);
+            v = ld_vol_s(p);
+        } while (is_sentinel(v));
+    }
+    return v;
+}
+
+#ifndef FLOW_LW
+#define FLOW_LW 16         // loader: externals in flight per lane per polling round
+#endif
+#ifndef FLOW_LSLEEP
+#define FLOW_LSLEEP 20     // loader back-off (ns) when nothing new arrived
+#endif
+#ifndef FLOW_LAHEAD
+#define FLOW_LAHEAD 64     // loader window: need-levels polled past the first missing external
+#endif
+#ifndef FLOW_DIRECT
+#define FLOW_DIRECT 1      // compute lanes read missing externals from L2 themselves
+#endif
+#ifndef FLOW_STORE
+#define FLOW_STORE 0       // 0: st.global.cg, 1: st.relaxed.gpu, 2: st.cg + fence
+#endif
+#ifndef FLOW_POLL_CG
+#define FLOW_POLL_CG 0     // 1: poll with weak L2 loads (ld.global.cg) instead of ld.relaxed.gpu
+#endif
+__device__ __forceinline__ double flow_poll_g(const double* p) {
+    if (FLOW_POLL_CG) {
+        double v;
+        asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+        return v;
+    }
+    return ld_relaxed_d(p);
+}
+constexpr int FLOW_WARPS = 12;                      // compute warps (+1 loader)
+constexpr int FLOW_THREADS = (FLOW_WARPS + 1) * 32;
+__device__ __forceinline__ bool is_sent_hi(double v) {   // published values are never NaN-boxed like this
+    return __double2hiint(v) == (int)(SENTINEL_BITS >> 32);
+}
+
+template <int EK>
+__global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    double* xs = reinterpret_cast<double*>(sm);                     // RC + EC + 2
+    double* bsm = xs + a.RC + a.EC + 2;                             // RC (right-hand side)
+    double* cc = bsm + a.RC;                                        // RC*CK
+    double* ecf = cc + (size_t)a.RC * CK;                           // RC*EK
+    double* di = ecf + (size_t)a.RC * EK;                           // RC
+    int* rid = reinterpret_cast<int*>(di + a.RC);                   // RC
+    int* eid_s = rid + a.RC;                                        // EC (external row ids, need-sorted)
+    short* cs = reinterpret_cast<short*>(eid_s + a.EC);             // RC*CK
+    short* es = cs + (size_t)a.RC * CK;                             // RC*EK
+    short* lp = es + (size_t)a.RC * EK;                             // LC
+    short* xl = lp + a.LC;                                          // LC: externals needed below level l
+    __shared__ int s_tile, s_hdr[4];
+    __shared__ __align__(8) uint64_t mbar;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&mbar)), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned phase = 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double sent = __longlong_as_double((long long)SENTINEL_BITS);
+    for (;;) {
+        if (threadIdx.x == 0) {
+            int k = atomicAdd(a.ticket, 1) - a.ticket_base;
+            int t = k < a.n_tiles ? a.order[k] : -1;
+            s_tile = t;
+            if (t >= 0) {
+                const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
+                s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z;
+                const unsigned n = h.x;
+                unsigned b_cs = r16(2u * n * CK), b_cc = r16(8u * n * CK), b_es = r16(2u * n * EK),
+                         b_ec = r16(8u * n * EK), b_di = r16(8u * n), b_ri = r16(4u * n), b_lp = r16(2u * (h.z + 1));
+                unsigned b_ei = r16(4u * h.y), b_xl = r16(2u * (h.z + 1));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(smem_addr(&mbar)), "r"(b_cs + b_cc + b_es + b_ec + b_di + b_ri + b_lp + b_ei + b_xl)
+                             : "memory");
+                bulk_g2s(xl, a.xlev_ptr + (size_t)t * a.LC, b_xl, &mbar);
+                bulk_g2s(eid_s, a.ext_id + (size_t)t * a.EC, b_ei, &mbar);
+                bulk_g2s(cs, a.cs + (size_t)t * a.RC * CK, b_cs, &mbar);
+                bulk_g2s(cc, a.cc + (size_t)t * a.RC * CK, b_cc, &mbar);
+                bulk_g2s(es, a.es + (size_t)t * a.RC * EK, b_es, &mbar);
+                bulk_g2s(ecf, a.ec + (size_t)t * a.RC * EK, b_ec, &mbar);
+                bulk_g2s(di, a.dinv + (size_t)t * a.RC, b_di, &mbar);
+                bulk_g2s(rid, a.row_id + (size_t)t * a.RC, b_ri, &mbar);
+                bulk_g2s(lp, a.lev_ptr + (size_t)t * a.LC, b_lp, &mbar);
+            }
+        }
+        __syncthreads();
+        const int t = s_tile;
+        if (t < 0) break;
+        const int n = s_hdr[0], ne = s_hdr[1], nlev = s_hdr[2];
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 0] = gtimer();
+        for (int q = threadIdx.x; q < ne; q += FLOW_THREADS) xs[a.RC + q] = sent;
+        {
+            unsigned done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                             : "=r"(done) : "r"(smem_addr(&mbar)), "r"(phase) : "memory");
+            phase ^= 1u;
+        }
+        for (int p0 = 0; p0 < n; p0 += 8 * FLOW_THREADS) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                int p = p0 + u * FLOW_THREADS + threadIdx.x;
+                v[u] = p < n ? __ldg(a.b + rid[p]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                int p = p0 + u * FLOW_THREADS + threadIdx.x;
+                if (p < n) { bsm[p] = a.alpha * v[u]; xs[p] = sent; }
+            }
+        }
+        if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
+        __syncthreads();
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
+        if (warp == FLOW_WARPS) {
+            // externals in need order; q0 = first entry not yet present
+            constexpr int LW = FLOW_LW;
+            // the polling window stops FLOW_LAHEAD need-levels past the first
+            // missing external: no L2 traffic for values produced much later
+            int q0 = 0, lq = 0;
+            long long spins = 0;
+            while (q0 < ne) {
+                while (lq < nlev && xl[lq + 1] <= q0) ++lq;
+                const int qe = min(min(ne, q0 + LW * 32), (int)xl[min(lq + FLOW_LAHEAD, nlev)]);
+                double v[LW];
+#pragma unroll
+                for (int u = 0; u < LW; ++u) {
+                    const int q = q0 + u * 32 + lane;
+                    v[u] = q < qe ? flow_poll_g(a.x + eid_s[q]) : 0.0;
+                }
+                int adv = qe - q0;
+#pragma unroll
+                for (int u = 0; u < LW; ++u) {
+                    const int q = q0 + u * 32 + lane;
+                    const bool ok = q >= qe || !is_sentinel(v[u]);
+                    if (q < qe && ok) st_vol_s(xs + a.RC + q, v[u]);
+                    const unsigned miss = __ballot_sync(0xffffffffu, !ok);
+                    if (miss && adv == qe - q0) adv = u * 32 + __ffs(miss) - 1;
+                }
+                if (adv == 0) {
+                    if (FLOW_LSLEEP) __nanosleep(FLOW_LSLEEP);
+                    if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
+                    continue;
+                }
+                spins = 0;
+                q0 += adv;
+            }
+        } else {
+            // groups of 16 rows of one level; a lane pair per row splits the
+            // early dependencies (lane li takes li, li+2, ...).  The whole warp
+            // walks a group together (inactive lanes predicated, __syncwarp per
+            // group): lanes never run ahead into later groups, where they would
+            // spin on rows their own warp still has to produce.
+            constexpr int KH = EK / 2;
+            const int li = lane & 1;
+            int g = 0;
+            for (int lv = 0; lv < nlev; ++lv) {
+                const int l0 = lp[lv], R = lp[lv + 1] - l0;
+                for (int r0 = 0; r0 < R; r0 += 16, ++g) {
+                    if (g % FLOW_WARPS != warp) continue;
+                    const int r = r0 + (lane >> 1);
+                    const bool act = r < R;
+                    const int p = l0 + (act ? r : 0);
+                    const short zs = (short)(a.RC + a.EC);
+                    short es_[KH], cs_[CK];
+                    double ec_[KH], cc_[CK];
+#pragma unroll
+                    for (int u = 0; u < KH; ++u) {
+                        const int k = 2 * u + li;
+                        es_[u] = act ? es[(size_t)l0 * EK + k * R + r] : zs;
+                        ec_[u] = act ? ecf[(size_t)l0 * EK + k * R + r] : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < CK; ++k) {
+                        cs_[k] = act ? cs[(size_t)l0 * CK + k * R + r] : zs;
+                        cc_[k] = act ? cc[(size_t)l0 * CK + k * R + r] : 0.0;
+                    }
+                    long long c0 = a.dbg2 ? gtimer() : 0, c1 = 0, c2 = 0;
+                    const double d = di[p];
+                    const int row = rid[p];
+                    const double bv = bsm[p];
+                    // warp-uniform polling: one vote per round, no per-dependency branches
+                    double ev[KH];
+#pragma unroll
+                    for (int u = 0; u < KH; ++u) ev[u] = ld_vol_s(xs + es_[u]);
+                    {
+                        bool miss = false;
+#pragma unroll
+                        for (int u = 0; u < KH; ++u) miss |= is_sent_hi(ev[u]);
+                        long long spins = 0;
+                        while (__any_sync(0xffffffffu, miss)) {   // externals / older rows still on their way
+                            if (FLOW_SLEEP_NS) __nanosleep(FLOW_SLEEP_NS);
+                            miss = false;
+#pragma unroll
+                            for (int u = 0; u < KH; ++u) {
+                                if (is_sent_hi(ev[u])) {
+                                    // an external the loader has not copied yet is read from L2
+                                    // directly (one L2 hand-off instead of a loader round)
+                                    const int q = es_[u] - a.RC;
+                                    ev[u] = (FLOW_DIRECT && q >= 0 && q < ne) ? flow_poll_g(a.x + eid_s[q])
+                                                                              : ld_vol_s(xs + es_[u]);
+                                }
+                                miss |= is_sent_hi(ev[u]);
+                            }
+                            if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
+                        }
+                    }
+                    double h = 0.0;
+#pragma unroll
+                    for (int u = 0; u < KH; ++u) h = fma(-ec_[u], ev[u], h);
+                    h += __shfl_xor_sync(0xffffffffu, h, 1);   // same sum on both lanes
+                    double acc = bv + h;
+                    if (a.dbg2) c1 = gtimer();
+                    double cv[CK];
+#pragma unroll
+                    for (int k = 0; k < CK; ++k) cv[k] = ld_vol_s(xs + cs_[k]);
+                    {
+                        bool miss = false;
+#pragma unroll
+                        for (int k = 0; k < CK; ++k) miss |= is_sent_hi(cv[k]);
+                        long long spins = 0;
+                        while (__any_sync(0xffffffffu, miss)) {   // the previous level is being finished
+                            miss = false;
+#pragma unroll
+                            for (int k = 0; k < CK; ++k) {
+                                cv[k] = ld_vol_s(xs + cs_[k]);
+                                miss |= is_sent_hi(cv[k]);
+                            }
+                            if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
+                        }
+                    }
+                    if (a.dbg2) c2 = gtimer();
+#pragma unroll
+                    for (int k = 0; k < CK; ++k) acc = fma(-cc_[k], cv[k], acc);
+                    const double v = acc * d;
+                    if (act && li == 0) {
+                        st_vol_s(xs + p, v);
+                        if (FLOW_STORE == 1) {
+                            asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.x + row), "d"(publishable(v)) : "memory");
+                        } else if (FLOW_STORE == 3) {   // performed at L2 (no write buffering in the SM)
+                            atomicExch(reinterpret_cast<unsigned long long*>(a.x + row),
+                                       (unsigned long long)__double_as_longlong(publishable(v)));
+                        } else if (FLOW_STORE == 4) {
+                            asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(a.x + row), "d"(publishable(v)) : "memory");
+                        } else {
+                            __stcg(a.x + row, publishable(v));
+                        }
+                        if (FLOW_STORE == 2) __threadfence();
+                    }
+                    __syncwarp();
+                    if (a.dbg2 && lane == 0 && g < 64) {
+                        long long* q = a.dbg2 + ((size_t)t * 64 + g) * 5;
+                        q[0] = c0; q[1] = c1; q[2] = c2; q[3] = gtimer(); q[4] = lv;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 2] = gtimer();
+        if (a.out2)
+            for (int p = threadIdx.x; p < n; p += FLOW_THREADS) {
+                int row = rid[p];
+                a.out2[row] = xs[p] + a.add[row];
+            }
+        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 3] = gtimer();
+    }
+}
+
 }  // namespace
 
 // smem: xs[RC+EC+2] cc[RC*CK] ec[RC*EK] di[RC] rid[RC] cs[RC*CK] es[RC*EK] lp[LC]
@@ -876,6 +1175,10 @@ size_t tile_smem_bytes(const TilePlan& tp) {
     size_t bytes = 8 * (rc + ec + 2) + 8 * rc * CK + 8 * rc * ek + 8 * rc + 4 * rc + 4 * ec + 2 * rc * CK +
                    2 * rc * ek + 2 * lc + 2 * lc;
     return (bytes + 127) & ~size_t(127);
+}
+
+size_t tile_flow_smem_bytes(const TilePlan& tp) {
+    return (tile_smem_bytes(tp) + 8 * (size_t)tp.RC + 127) & ~size_t(127);
 }
 
 bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
@@ -941,7 +1244,7 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
             if (me <= w) { tp.KD = w; break; }
         if (!tp.KD) return false;
     }
-    size_t smem = tile_smem_bytes(tp);
+    size_t smem = tile_flow_smem_bytes(tp);
     if (smem > 220 * 1024) return false;
     tp.hdr.reset(c, (size_t)nt * 4);
     tp.lev_ptr.reset(c, (size_t)nt * tp.LC);
@@ -1000,9 +1303,12 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
 
 template <int EK>
 static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
-    static const bool legacy = getenv("EDFA_TILE_LEGACY") != nullptr;
-    auto kern = legacy ? k_tile_solve<EK> : k_tile_pipe<EK>;
-    const int threads = legacy ? TILE_THREADS : PIPE_THREADS;
+    // EDFA_TILE_KERNEL (A/B experiments only): legacy | pipe; default: dataflow
+    static const char* kv = getenv("EDFA_TILE_KERNEL");
+    static const int which = !kv ? 2 : (kv[0] == 'l' ? 0 : kv[0] == 'p' ? 1 : 2);
+    auto kern = which == 0 ? k_tile_solve<EK> : which == 1 ? k_tile_pipe<EK> : k_tile_flow<EK>;
+    const int threads = which == 0 ? TILE_THREADS : which == 1 ? PIPE_THREADS : FLOW_THREADS;
+    if (which == 2) smem = tile_flow_smem_bytes(tp);
     // attribute + occupancy once per (kernel, smem): these are driver calls,
     // kept off the per-solve path
     static std::mutex mu;
@@ -1044,16 +1350,23 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
     TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.LC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
                 tp.flags.p, tp.ticket.p, tp.epoch, 0, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr,
-                tp.xlev_ptr.p, tp.req.p, 0};
+                tp.xlev_ptr.p, tp.req.p, 0, nullptr};
     static const int tile_mode = getenv("EDFA_TILE_MODE") ? atoi(getenv("EDFA_TILE_MODE")) : 0;
     a.mode = tile_mode;
     static const char* dbg_path = getenv("EDFA_TILE_DEBUG");
-    DevBuf<long long> dbg;
+    static const char* dbg2_path = getenv("EDFA_TILE_DEBUG2");
+    DevBuf<long long> dbg, dbg2;
     if (dbg_path) {
         dbg.reset(c, (size_t)tp.n_tiles * 6);
         a.dbg = dbg.p;
     }
-    static const bool legacy = getenv("EDFA_TILE_LEGACY") != nullptr;
+    a.dbg2 = nullptr;
+    if (dbg2_path) {
+        dbg2.reset(c, (size_t)tp.n_tiles * 64 * 5);
+        EDFA_CUDA(cudaMemsetAsync(dbg2.p, 0, sizeof(long long) * tp.n_tiles * 64 * 5, c->stream));
+        a.dbg2 = dbg2.p;
+    }
+    static const bool legacy = getenv("EDFA_TILE_KERNEL") && getenv("EDFA_TILE_KERNEL")[0] == 'l';
     if (!legacy && !nowait) fill_bits(c, x, tp.n, SENTINEL_BITS);   // a row's value is its own ready flag
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
     switch (tp.KD) {
@@ -1063,6 +1376,20 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
         case 16: launch_tile<16>(c, tp, a, smem); break;
         case 24: launch_tile<24>(c, tp, a, smem); break;
         default: launch_tile<32>(c, tp, a, smem); break;
+    }
+    if (dbg2_path) {
+        std::vector<long long> h((size_t)tp.n_tiles * 64 * 5);
+        EDFA_CUDA(cudaMemcpyAsync(h.data(), dbg2.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        FILE* f = fopen(dbg2_path, "w");
+        if (f) {
+            for (int t = 0; t < tp.n_tiles; ++t)
+                for (int g = 0; g < 64; ++g) {
+                    const long long* q = &h[((size_t)t * 64 + g) * 5];
+                    if (q[0]) fprintf(f, "%d %d %lld %lld %lld %lld %lld\n", t, g, q[0], q[1], q[2], q[3], q[4]);
+                }
+            fclose(f);
+        }
     }
     if (dbg_path) {
         std::vector<long long> h((size_t)tp.n_tiles * 6);
