@@ -547,7 +547,14 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
     select_part(c, f.LU, 0, 1.0, true, Lv);
     select_part(c, f.LU, 1, 1.0, true, Uv);
     // cell-grid factors: tile-DAG solves; otherwise level-synchronous plans
-    if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
+    // cell-grid factors: pencil solves for axial stencils, tile-DAG solves for
+    // other grid-local stencils, otherwise level-ordered plans
+    if (dims && build_axial_plan(c, Lv, nullptr, true, false, dims, f.fwd.axial)) {
+        f.fwd.is_axial = true;
+        f.fwd.n = n;
+        f.fwd.n_dep = Lv.nnz;
+        f.fwd.n_levels = f.fwd.axial.nsteps;
+    } else if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
         f.fwd.is_tile = true;
         f.fwd.n = n;
         f.fwd.n_dep = Lv.nnz;
@@ -556,7 +563,12 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         if (sync_free) level_plan();
         plan_values(c, Lv, nullptr, f.fwd);
     }
-    if (dims && build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile)) {
+    if (dims && build_axial_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.axial)) {
+        f.bwd.is_axial = true;
+        f.bwd.n = n;
+        f.bwd.n_dep = Uv.nnz;
+        f.bwd.n_levels = f.bwd.axial.nsteps;
+    } else if (dims && build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile)) {
         f.bwd.is_tile = true;
         f.bwd.n = n;
         f.bwd.n_dep = Uv.nnz;

@@ -78,7 +78,23 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name);
 
+struct AxialPlan {              // pencil solves of axial-stencil cell factors (axial.cu)
+    int32_t n = 0, R = 0, NJ = 0, NK = 0, nsteps = 0;
+    int32_t dims[3] = {0, 0, 0};
+    bool reverse = false;
+    int64_t n_dep = 0;
+    DevBuf<double> coef;        // [block][step][3R+1][64]
+    DevBuf<int32_t> order, ticket;
+    int32_t ticket_base = 0;
+};
+bool build_axial_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
+                      AxialPlan& p);
+void run_axial(Ctx* c, AxialPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
+               const char* name);
+
 struct TriPlan {
+    bool is_axial = false;
+    AxialPlan axial;
     bool is_chain = false;
     ChainPlan chain;
     bool is_tile = false;

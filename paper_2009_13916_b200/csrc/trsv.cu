@@ -407,6 +407,10 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
         run_chain(c, p.chain, b, alpha, x, add, out2, name);
         return;
     }
+    if (p.is_axial) {
+        run_axial(c, const_cast<AxialPlan&>(p.axial), b, alpha, x, add, out2, name);
+        return;
+    }
     if (p.is_tile) {   // epoch / ticket bookkeeping is per plan (serialised on the stream)
         run_tile(c, const_cast<TilePlan&>(p.tile), b, alpha, x, add, out2, name);
         return;
