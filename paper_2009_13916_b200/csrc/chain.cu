@@ -132,6 +132,11 @@ __global__ void k_chain_ic0(const int* __restrict__ rows, const int64_t* __restr
     if (cnt) atomicAdd(shifts, cnt);
 }
 
+__global__ void k_max_int(const int* __restrict__ v, int n, int* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicMax(out, v[i]);
+}
+
 struct I64 {
     __host__ __device__ int64_t operator()(int v) const { return (int64_t)v; }
 };
@@ -212,6 +217,88 @@ __global__ void __launch_bounds__(256) k_chain_scan(const int64_t* __restrict__ 
     }
 }
 
+// (L L^T)^{-1} on chains in one pass: the IC factor of -A_ff is block
+// diagonal by chains, so a warp solves L then L^T for its own chain without any
+// global dependency -- forward affine scan (x_i = d_i(alpha b_i - c_i x_{i-1})),
+// then the mirrored backward scan (y_i = d_i(x_i - c_{i+1} y_{i+1})), with x
+// kept in registers (chains of at most 32*E rows).  Half the launches and no
+// HBM round trip for the intermediate vector.
+template <int E>
+__global__ void __launch_bounds__(256) k_chain_pair(const int64_t* __restrict__ cptr, const int* __restrict__ rows,
+                                                    const double* __restrict__ coef, const double* __restrict__ dinv,
+                                                    int n_chains, const double* b, double alpha, double* x,
+                                                    const double* __restrict__ add, double* __restrict__ out2) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= n_chains) return;
+    const int64_t s = cptr[w], e = cptr[w + 1];
+    int r[E];
+    double d[E], cf[E], xv[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const int64_t q = s + lane * E + j;
+        r[j] = q < e ? rows[q] : -1;
+        d[j] = q < e ? dinv[q] : 0.0;
+        cf[j] = q < e ? coef[q] : 0.0;
+    }
+    // forward: x_i = al_i + be_i x_{i-1}
+    double al[E], be[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        if (r[j] >= 0) { al[j] = d[j] * (alpha * b[r[j]]); be[j] = -cf[j] * d[j]; }
+        else { al[j] = 0.0; be[j] = 1.0; }
+    }
+    double A = al[0], B = be[0];
+#pragma unroll
+    for (int j = 1; j < E; ++j) {
+        A = fma(be[j], A, al[j]);
+        B = be[j] * B;
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double Ap = __shfl_up_sync(0xffffffffu, A, off), Bp = __shfl_up_sync(0xffffffffu, B, off);
+        if (lane >= off) { A = fma(B, Ap, A); B = B * Bp; }
+    }
+    double xl = __shfl_up_sync(0xffffffffu, A, 1);
+    if (lane == 0) xl = 0.0;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        xv[j] = fma(be[j], xl, al[j]);
+        xl = xv[j];
+    }
+    // backward: y_i = al'_i + be'_i y_{i+1}, al' = d_i x_i, be' = -c_{i+1} d_i
+    double cn = __shfl_down_sync(0xffffffffu, cf[0], 1);   // c of the next lane's first row
+    if (lane == 31) cn = 0.0;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const double cnext = j + 1 < E ? cf[j + 1] : cn;
+        if (r[j] >= 0) { al[j] = d[j] * xv[j]; be[j] = -cnext * d[j]; }
+        else { al[j] = 0.0; be[j] = 0.0; }
+    }
+    A = al[E - 1];
+    B = be[E - 1];
+#pragma unroll
+    for (int j = E - 2; j >= 0; --j) {
+        A = fma(be[j], A, al[j]);
+        B = be[j] * B;
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double Ap = __shfl_down_sync(0xffffffffu, A, off), Bp = __shfl_down_sync(0xffffffffu, B, off);
+        if (lane + off < 32) { A = fma(B, Ap, A); B = B * Bp; }
+    }
+    double yl = __shfl_down_sync(0xffffffffu, A, 1);
+    if (lane == 31) yl = 0.0;
+#pragma unroll
+    for (int j = E - 1; j >= 0; --j) {
+        const double y = fma(be[j], yl, al[j]);
+        if (r[j] >= 0) {
+            if (x) x[r[j]] = y;
+            if (out2) out2[r[j]] = y + add[r[j]];
+        }
+        yl = y;
+    }
+}
+
 }  // namespace
 
 // Try to build a chain plan for deps; returns false if deps is not chain-structured.
@@ -281,6 +368,13 @@ bool build_chain(Ctx* c, const Csr& deps, const double* diag, bool unit, ChainPl
     cp.crow.reset(c, n);
     cp.ccoef.reset(c, n);
     cp.cdinv.reset(c, n);
+    {   // longest chain (decides whether the fused L, L^T kernel applies)
+        int* mx = c->d_scalar_i + 34;
+        EDFA_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
+        k_max_int<<<ceil_div(nc, 256), 256, 0, c->stream>>>(lens_s.p, nc, mx);
+        EDFA_CUDA(cudaMemcpyAsync(&cp.max_len, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    }
     Prof pr(c, "chain_plan", 24.0 * total);
     k_chain_fill<<<ceil_div(nc, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, nc, cp.gbase.p,
                                                            cp.rows.p, cp.coef.p, cp.dinv.p, diag, unit);
@@ -314,6 +408,21 @@ void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, 
     k_chain_ic0<<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(cp.rows.p, cp.gbase.p, cp.n_chains, Lpat.ptr.p,
                                                                    Lpat.val.p, aii, scale, diag, shifts);
     check_launch("k_chain_ic0");
+}
+
+bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add,
+                    double* out2, const char* name) {
+    if (cp.n_chains == 0 || cp.max_len > 32 * 8) return false;
+    Prof pr(c, name, 12.0 * cp.n + 32.0 * cp.n + (out2 ? 16.0 * cp.n : 0.0) + (x ? 8.0 * cp.n : 0.0));
+    const unsigned grid = (unsigned)ceil_div((int64_t)cp.n_chains * 32, 256);
+    if (cp.max_len <= 32 * 4)
+        k_chain_pair<4><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha,
+                                                     x, add, out2);
+    else
+        k_chain_pair<8><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha,
+                                                     x, add, out2);
+    check_launch("k_chain_pair");
+    return true;
 }
 
 }  // namespace edfa

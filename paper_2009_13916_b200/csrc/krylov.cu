@@ -624,8 +624,12 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     double* y_c = y + nf;
     const IcFactor& ic = s1->ic;
     const IluFactor& il = s2->ilu;
-    run_plan(c, ic.fwd, r_f, -1.0, ws.a_f.p, nullptr, nullptr, "trsv_ic_L");
-    run_plan(c, ic.bwd, ws.a_f.p, 1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_LT");
+    // (L L^T)^{-1}: one fused chain kernel when the factor is chain-structured
+    const bool pair = ic.fwd.is_chain && ic.bwd.is_chain && ic.fwd.chain.max_len <= 256 && !getenv("EDFA_NO_IC_PAIR");
+    if (!pair || !run_chain_pair(c, ic.fwd.chain, r_f, -1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_pair")) {
+        run_plan(c, ic.fwd, r_f, -1.0, ws.a_f.p, nullptr, nullptr, "trsv_ic_L");
+        run_plan(c, ic.bwd, ws.a_f.p, 1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_LT");
+    }
     if (nc) {
         EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
         spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
@@ -636,9 +640,11 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
         EDFA_CUDA(cudaMemsetAsync(ws.a_f.p, 0, sizeof(double) * nf, c->stream));
     }
     if (nf) {
-        run_plan(c, ic.fwd, ws.a_f.p, 1.0, y_f, nullptr, nullptr, "trsv_ic_L");
-        // b and out2 alias row-wise only (thread r reads b[r] before writing out2[r])
-        run_plan(c, ic.bwd, y_f, 1.0, ws.a_f.p, ws.t_f.p, y_f, "trsv_ic_LT");
+        if (!pair || !run_chain_pair(c, ic.fwd.chain, ws.a_f.p, 1.0, nullptr, ws.t_f.p, y_f, "trsv_ic_pair")) {
+            run_plan(c, ic.fwd, ws.a_f.p, 1.0, y_f, nullptr, nullptr, "trsv_ic_L");
+            // b and out2 alias row-wise only (thread r reads b[r] before writing out2[r])
+            run_plan(c, ic.bwd, y_f, 1.0, ws.a_f.p, ws.t_f.p, y_f, "trsv_ic_LT");
+        }
     }
 }
 

@@ -42,7 +42,7 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
 // coefficient stream is fully coalesced.  Dependencies are polled on the
 // solution vector itself (sentinel-initialised), so there is no flag array.
 struct ChainPlan {              // disjoint-path DAGs (chain.cu)
-    int32_t n = 0, n_chains = 0;
+    int32_t n = 0, n_chains = 0, max_len = 0;
     int64_t n_stored = 0;
     bool unit = false;
     DevBuf<int64_t> gbase;      // group of 32 chains -> first stored step
@@ -57,6 +57,10 @@ bool build_chain(Ctx* c, const Csr& deps, const double* diag, bool unit, ChainPl
 void chain_values(Ctx* c, const Csr& deps, const double* diag, ChainPlan& cp);
 void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add, double* out2,
                const char* name);
+// x = (L L^T)^{-1} (alpha b) on the chains of L (out2 = x + add); false when
+// the chains are too long for the fused kernel (caller runs the two solves)
+bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add,
+                    double* out2, const char* name);
 void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,
                int* shifts);
 

@@ -409,6 +409,48 @@ def test_tile_solver_matches_level_solver(edfa, idx, n):
     assert np.abs(ys[0] - ys[1]).max() <= 1e-12 * np.abs(ys[1]).max()
 
 
+@pytest.mark.parametrize("idx,n", [(1, 12), (2, 10), (2, 19)])
+def test_axial_solver_matches_level_solver(edfa, idx, n, monkeypatch):
+    """The axial-stencil pencil solves (EDFA_AXIAL) and the level-synchronous
+    solves compute the same Schur triangular solutions (n = 19: blocks that
+    overhang the grid)."""
+    from paper_2009_13916_b200 import configs
+    case = configs.make(idx, n=n)
+    s = case.system
+    p = case.precond
+    ys = []
+    for hint in (True, False):
+        if hint:
+            monkeypatch.setenv("EDFA_AXIAL", "1")
+        else:
+            monkeypatch.delenv("EDFA_AXIAL", raising=False)
+        ds = edfa.DeviceSystem.from_host(s)
+        if not hint:
+            ds.set_grid(0, 0, 0)
+        pats = edfa.patterns_for(s, p["pattern"], p.get("prototype", "A"))
+        pre = edfa.BlockLDUPreconditioner.build(ds, patterns=pats, no_fill=True)
+        r = np.random.default_rng(5).standard_normal(s.n_unknowns)
+        ys.append(pre.apply(r))
+    assert np.abs(ys[0] - ys[1]).max() <= 1e-12 * np.abs(ys[1]).max()
+
+
+@pytest.mark.parametrize("idx,n", [(1, 12), (2, 16)])
+def test_ic_pair_matches_separate_solves(edfa, idx, n, monkeypatch):
+    """The fused (L L^T)^-1 chain kernel equals the two separate chain solves."""
+    from paper_2009_13916_b200 import configs
+    case = configs.make(idx, n=n)
+    s = case.system
+    p = case.precond
+    ds = edfa.DeviceSystem.from_host(s)
+    pats = edfa.patterns_for(s, p["pattern"], p.get("prototype", "A"))
+    pre = edfa.BlockLDUPreconditioner.build(ds, patterns=pats, no_fill=True)
+    r = np.random.default_rng(7).standard_normal(s.n_unknowns)
+    y_pair = pre.apply(r)
+    monkeypatch.setenv("EDFA_NO_IC_PAIR", "1")
+    y_sep = pre.apply(r)
+    assert np.abs(y_pair - y_sep).max() <= 1e-11 * np.abs(y_sep).max()
+
+
 def test_stages_freed_without_cycle_collection(edfa):
     """Dropping a preconditioner releases its device objects at once (no
     reference cycles), so repeated builds reuse the memory pool instead of

@@ -13,8 +13,8 @@ import re
 import sys
 
 # bench profiler name -> ncu kernel name prefix
-PROFILER_NAMES = {"trsv_ilu_L": "k_tile_pipe", "trsv_ilu_U": "k_tile_pipe", "gs_multidot": "k_multidot",
-                  "gs_multiaxpy": "k_multiaxpy", "spmv_A": "k_spmv", "trsv_ic_L": "k_chain_scan",
+PROFILER_NAMES = {"trsv_ilu_L": "k_tile_flow", "trsv_ilu_U": "k_tile_flow", "gs_dots2": "k_dots2",
+                  "gs_axpy2": "k_axpy2", "spmv_A": "k_spmv", "trsv_ic_L": "k_chain_scan",
                   "trsv_ic_LT": "k_chain_scan"}
 
 
