@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_multiaxpy(const double* __re
 // so each step reads the basis twice (dots, update) instead of CGS2's four
 // times; in exact arithmetic the columns equal CGS2's.
 constexpr int D2_GROUP = 8;
+#ifndef EDFA_DOTS2_WAVE
+#define EDFA_DOTS2_WAVE 2
+#endif
 
 // dots of V_0..V_{nv-1} with u = V_{nv-1} and w = V_{nv}: grid (groups, ranges),
 // block-contiguous element ranges so the blocks sharing a range run together
@@ -220,7 +223,7 @@ constexpr int D2_GROUP = 8;
 // [64..127] = w-dots.
 template <bool VEC2>
 __global__ void __launch_bounds__(RED_THREADS) k_dots2(const double* __restrict__ V, int64_t ldv, int nv, int64_t n,
-                                                       int64_t range, double* __restrict__ partial,
+                                                       int64_t range, double* __restrict__ partial, int pr,
                                                        unsigned* counter, int j, int m, double* __restrict__ H,
                                                        double* __restrict__ h1, double* __restrict__ coef,
                                                        double* __restrict__ hcol) {
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_dots2(const double* __restrict_
         if (k0 + k < nv) {
             double t = 0.0;
             for (int q = 0; q < RED_THREADS / 32; ++q) t += red[threadIdx.x][q];
-            partial[(int64_t)blockIdx.y * 128 + side * 64 + k0 + k] = t;
+            partial[(int64_t)(side * 64 + k0 + k) * pr + blockIdx.y] = t;   // slot-major
         }
     }
     // last block: fixed-order sum over ranges, then the step's coefficients
@@ -293,35 +296,25 @@ __global__ void __launch_bounds__(RED_THREADS) k_dots2(const double* __restrict_
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // warp w sums partial rows w, w+8, ... (lanes over the 128 slots, coalesced),
-    // then the 8 warp sums are added in a fixed order: deterministic
+    // warp w sums the needed slots w, w+8, ... over the ranges (slot-major
+    // partials: lanes read consecutive ranges), fixed order: deterministic
     __shared__ double dot[128];
-    __shared__ double wsum[RED_THREADS / 32][128];
     {
         const int nr = gridDim.y, nw = RED_THREADS / 32;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        int b = wid;
-        for (; b + 3 * nw < nr; b += 4 * nw) {
-            double v[4][4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) v[u][q] = __ldcg(partial + (int64_t)(b + u * nw) * 128 + q * 32 + lane);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] += v[u][q];
-        }
-        for (; b < nr; b += nw)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] += __ldcg(partial + (int64_t)b * 128 + q * 32 + lane);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) wsum[wid][q * 32 + lane] = acc[q];
-        __syncthreads();
-        if (threadIdx.x < 128) {
-            double t = 0.0;
-            for (int q = 0; q < nw; ++q) t += wsum[q][threadIdx.x];
-            dot[threadIdx.x] = t;
+        for (int q = wid; q < 2 * nv; q += nw) {
+            const int slot = q < nv ? q : 64 + (q - nv);
+            const double* col = partial + (int64_t)slot * pr;
+            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+            int b = lane;
+            for (; b + 96 < nr; b += 128) {
+                acc0 += __ldcg(col + b);
+                acc1 += __ldcg(col + b + 32);
+                acc2 += __ldcg(col + b + 64);
+                acc3 += __ldcg(col + b + 96);
+            }
+            for (; b < nr; b += 32) acc0 += __ldcg(col + b);
+            const double t = warp_sum((acc0 + acc1) + (acc2 + acc3));
+            if (lane == 0) dot[slot] = t;
         }
     }
     if (threadIdx.x == 0) *counter = 0u;
@@ -554,8 +547,9 @@ struct Blas {
                     double* part2, int part2_rows) {
         const int nv = j + 1;
         const int groups = (nv + D2_GROUP - 1) / D2_GROUP;
-        int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((4 * NUM_SMS_B200) / groups, (n + 511) / 512));
-        ranges = std::max<int64_t>(ranges, std::min<int64_t>(NUM_SMS_B200, (n + 511) / 512));
+        // one wave of resident blocks (2 per SM at 128 registers): no tail wave
+        int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((EDFA_DOTS2_WAVE * NUM_SMS_B200) / groups,
+                                                                (n + 511) / 512));
         ranges = std::min<int64_t>(ranges, part2_rows);
         int64_t range = (n + ranges - 1) / ranges;
         range = (range + 1) & ~int64_t(1);
@@ -566,11 +560,11 @@ struct Blas {
             Prof pr(c, "gs_dots2", 8.0 * n * (nv + 1));
             dim3 grid(groups, (unsigned)ranges);
             if (v2)
-                k_dots2<true><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, cnt, j, m, H, h1, coef,
-                                                                  hcol);
+                k_dots2<true><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, part2_rows, cnt, j, m, H,
+                                                                  h1, coef, hcol);
             else
-                k_dots2<false><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, cnt, j, m, H, h1,
-                                                                   coef, hcol);
+                k_dots2<false><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, part2_rows, cnt, j, m,
+                                                                   H, h1, coef, hcol);
             check_launch("dots2");
         }
         {
@@ -617,6 +611,7 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     if (!ws.u_c.p && nc) {
         ws.u_c.reset(c, nc);
         ws.c_c.reset(c, nc);
+        fill_bits(c, ws.c_c.p, nc, SENTINEL_BITS);   // kept SENTINEL between applies (tile path)
     }
     const double* r_f = r;
     const double* r_c = r + nf;
@@ -633,8 +628,18 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     if (nc) {
         EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
         spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
-        run_plan(c, il.fwd, ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L");
-        run_plan(c, il.bwd, ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U");
+        if (il.fwd.is_tile && il.bwd.is_tile && !getenv("EDFA_NO_FILL_FUSION")) {
+            // L writes c_c (SENTINEL since the last apply's U solve read it) and
+            // pre-fills y_c; U consumes c_c (resets it) and writes y_c
+            run_tile_ex(c, const_cast<TilePlan&>(il.fwd.tile), ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L",
+                        true, false, y_c);
+            run_tile_ex(c, const_cast<TilePlan&>(il.bwd.tile), ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U",
+                        true, true, nullptr);
+        } else {
+            run_plan(c, il.fwd, ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L");
+            run_plan(c, il.bwd, ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U");
+            if (il.fwd.is_tile) fill_bits(c, ws.c_c.p, nc, SENTINEL_BITS);   // restore the invariant
+        }
         spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
     } else if (nf) {
         EDFA_CUDA(cudaMemsetAsync(ws.a_f.p, 0, sizeof(double) * nf, c->stream));

@@ -81,6 +81,11 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
                      TilePlan& tp);
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name);
+// x_prefilled: x already holds SENTINEL; consume_b: b's rows are reset to
+// SENTINEL once read; pre_sent: a vector set to SENTINEL row by row (the next
+// solve's output) -- lets consecutive solves skip their fill kernels
+void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
+                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent);
 
 struct AxialPlan {              // pencil solves of axial-stencil cell factors (axial.cu)
     int32_t n = 0, R = 0, NJ = 0, NK = 0, nsteps = 0;

@@ -403,6 +403,8 @@ struct TileSolve {
     const unsigned char* req;
     int mode;             // EDFA_TILE_MODE experiment bits (diagnostics)
     long long* dbg2;      // per-group timestamps (diagnostics): [tile][64][5]
+    double* b_sent;       // flow kernel: == b, whose tile rows are reset to SENTINEL once read (or NULL)
+    double* pre_sent;     // flow kernel: another vector whose tile rows are set to SENTINEL (or NULL)
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -914,7 +916,7 @@ __device__ __forceinline__ double poll_s(const double* p, int* err) {
 #define FLOW_DIRECT 1      // compute lanes read missing externals from L2 themselves
 #endif
 #ifndef FLOW_STORE
-#define FLOW_STORE 0       // 0: st.global.cg, 1: st.relaxed.gpu, 2: st.cg + fence
+#define FLOW_STORE 5       // 0: st.global.cg, 1: st.relaxed.gpu, 2: st.cg + fence, 3: atom.exch, 4: st.release, 5: red.add at L2
 #endif
 #ifndef FLOW_POLL_CG
 #define FLOW_POLL_CG 0     // 1: poll with weak L2 loads (ld.global.cg) instead of ld.relaxed.gpu
@@ -1007,7 +1009,14 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 int p = p0 + u * FLOW_THREADS + threadIdx.x;
-                if (p < n) { bsm[p] = a.alpha * v[u]; xs[p] = sent; }
+                if (p < n) {
+                    bsm[p] = a.alpha * v[u];
+                    xs[p] = sent;
+                    // sentinel pre-fill of the next solves' outputs, row by row
+                    // (this tile is the only reader / writer of these rows)
+                    if (a.b_sent) a.b_sent[rid[p]] = sent;
+                    if (a.pre_sent) a.pre_sent[rid[p]] = sent;
+                }
             }
         }
         if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
@@ -1141,6 +1150,9 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                         } else if (FLOW_STORE == 3) {   // performed at L2 (no write buffering in the SM)
                             atomicExch(reinterpret_cast<unsigned long long*>(a.x + row),
                                        (unsigned long long)__double_as_longlong(publishable(v)));
+                        } else if (FLOW_STORE == 5) {   // fire-and-forget reduction at L2: SENTINEL + (v - SENTINEL)
+                            atomicAdd(reinterpret_cast<unsigned long long*>(a.x + row),
+                                      (unsigned long long)__double_as_longlong(publishable(v)) - SENTINEL_BITS);
                         } else if (FLOW_STORE == 4) {
                             asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(a.x + row), "d"(publishable(v)) : "memory");
                         } else {
@@ -1338,6 +1350,11 @@ static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
 
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name) {
+    run_tile_ex(c, tp, b, alpha, x, add, out2, name, false, false, nullptr);
+}
+
+void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
+                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent) {
     size_t smem = tile_smem_bytes(tp);
     // EDFA_TILE_NOWAIT (profiling only): every upstream flag already matches,
     // so tiles run without waiting -- isolates per-tile processing cost
@@ -1350,7 +1367,7 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
     TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.LC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
                 tp.flags.p, tp.ticket.p, tp.epoch, 0, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr,
-                tp.xlev_ptr.p, tp.req.p, 0, nullptr};
+                tp.xlev_ptr.p, tp.req.p, 0, nullptr, nullptr, nullptr};
     static const int tile_mode = getenv("EDFA_TILE_MODE") ? atoi(getenv("EDFA_TILE_MODE")) : 0;
     a.mode = tile_mode;
     static const char* dbg_path = getenv("EDFA_TILE_DEBUG");
@@ -1367,7 +1384,18 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
         a.dbg2 = dbg2.p;
     }
     static const bool legacy = getenv("EDFA_TILE_KERNEL") && getenv("EDFA_TILE_KERNEL")[0] == 'l';
-    if (!legacy && !nowait) fill_bits(c, x, tp.n, SENTINEL_BITS);   // a row's value is its own ready flag
+    const bool flow = !getenv("EDFA_TILE_KERNEL") || (getenv("EDFA_TILE_KERNEL")[0] != 'l' &&
+                                                     getenv("EDFA_TILE_KERNEL")[0] != 'p');
+    if (flow) {
+        a.b_sent = consume_b ? const_cast<double*>(b) : nullptr;
+        a.pre_sent = pre_sent;
+    } else {
+        x_prefilled = false;
+        if (consume_b) fill_bits(c, const_cast<double*>(b), tp.n, SENTINEL_BITS);
+        if (pre_sent) fill_bits(c, pre_sent, tp.n, SENTINEL_BITS);
+    }
+    // a row's value is its own ready flag
+    if (!legacy && !nowait && !x_prefilled) fill_bits(c, x, tp.n, SENTINEL_BITS);
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
     switch (tp.KD) {
         case 4: launch_tile<4>(c, tp, a, smem); break;
