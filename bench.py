@@ -6,9 +6,11 @@ One step = the hot path over one system: static-pattern generation, stage 1
 (S~ = A_cc - H~, ILU(0)) and right-preconditioned GMRES(50) to rtol 1e-8 from
 x0 = 0.  Workload: BASELINE config 2 (64^3 hex grid, lognormal anisotropic K,
 static prototype A, IC(0)/ILU(0)), synthetic seeded inputs (SPE10 is not in
-this container).  ``value`` = N_dof * steps / device time with the blocks
-resident in HBM; ``e2e`` = the same through the drop-in API from host scipy
-blocks (H2D of the blocks and rhs, D2H of x inside the timed region).
+this container).  ``value`` = N_dof * steps / device time with the blocks, rhs
+and grid index arrays resident in HBM (the step derives everything else:
+merged A, SELL copies, topology, patterns, stage 1/2, GMRES); ``e2e`` = the
+same through the drop-in API from page-locked host scipy blocks (H2D of the
+blocks, rhs and grid arrays, D2H of x inside the timed region).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl edfa|reference] [--slabs P]
 

@@ -12,7 +12,9 @@
 // cooperative kernel with a software grid barrier between levels.
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "dev_util.cuh"
 #include "edfa_internal.cuh"
@@ -127,7 +129,7 @@ template <int RMAX, bool SF>
 __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, const int32_t* __restrict__ Si,
                                          const int32_t* __restrict__ ustart, double* __restrict__ LU,
                                          const double* __restrict__ scale, double* __restrict__ udiag, int* shifts,
-                                         int* err, unsigned char* base, int lane) {
+                                         int* err, unsigned char* base, int lane, long long* dbg = nullptr) {
     constexpr int ECAP = ilu0_ecap(RMAX);
     constexpr int SW = ECAP / 32 < 16 ? ECAP / 32 : 16;   // staged entries per lane per round trip
     double* vals = reinterpret_cast<double*>(base);
@@ -173,6 +175,11 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
     }
     if (SF) __threadfence();   // pivot rows' U entries are read after their pivots were seen
     __syncwarp();
+    if (dbg && lane == 0) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        dbg[3 * (int64_t)i + 1] = t;
+    }
     for (int p0 = 0; p0 < nl;) {
         if (lane == 0) {   // chunk of pivots whose U entries fit the staging buffer
             int acc = 0, p1 = p0;
@@ -249,6 +256,11 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
         __threadfence();
         __syncwarp();
         if (lane == 0) st_relaxed(udiag + i, publishable(piv));
+        if (dbg && lane == 0) {
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            dbg[3 * (int64_t)i + 2] = t;
+        }
     } else if (lane == 0) {
         __stcg(udiag + i, piv);
     }
@@ -286,7 +298,7 @@ __global__ void __launch_bounds__(256) k_ilu0_sf(const int* __restrict__ ord, in
                                                  const int32_t* __restrict__ Sp, const int32_t* __restrict__ Si,
                                                  const int32_t* __restrict__ ustart, double* __restrict__ LU,
                                                  const double* __restrict__ scale, double* __restrict__ udiag,
-                                                 int* shifts, int* err) {
+                                                 int* shifts, int* err, long long* dbg) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* base = smem + (size_t)wid * ilu0_warp_smem(RMAX);
@@ -297,7 +309,12 @@ __global__ void __launch_bounds__(256) k_ilu0_sf(const int* __restrict__ ord, in
         if (s >= n_ord) break;
         const int i = ord[s];
         if (i < 0) continue;
-        ilu0_row<RMAX, true>(i, Sp, Si, ustart, LU, scale, udiag, shifts, err, base, lane);
+        if (dbg && lane == 0) {
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            dbg[3 * (int64_t)i] = t;
+        }
+        ilu0_row<RMAX, true>(i, Sp, Si, ustart, LU, scale, udiag, shifts, err, base, lane, dbg);
     }
 }
 
@@ -520,7 +537,14 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         int* tk = c->d_scalar_i + 29;
         if (sync_free) EDFA_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), c->stream));
         void* args[] = {&la, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
-        void* args_sf[] = {&op, &n_ord, &tk, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
+        static const char* dbg_path = getenv("EDFA_ILU_DEBUG");
+        DevBuf<long long> dbgb;
+        long long* dbgp = nullptr;
+        if (dbg_path && sync_free) {
+            dbgb.reset(c, (size_t)3 * n);
+            dbgp = dbgb.p;
+        }
+        void* args_sf[] = {&op, &n_ord, &tk, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er, &dbgp};
         auto launch = [&](auto kern, auto kern_sf, int rmax) {
             int threads = rmax >= 1024 ? 64 : rmax <= 64 ? 256 : 128;
             size_t smem = ilu0_warp_smem(rmax) * (threads / 32);
@@ -539,6 +563,16 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         if (maxr <= 64) launch(k_ilu0<64>, k_ilu0_sf<64>, 64);
         else if (maxr <= 256) launch(k_ilu0<256>, k_ilu0_sf<256>, 256);
         else launch(k_ilu0<1024>, k_ilu0_sf<1024>, 1024);
+        if (dbgp) {
+            std::vector<long long> h((size_t)3 * n);
+            EDFA_CUDA(cudaMemcpyAsync(h.data(), dbgp, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+            EDFA_CUDA(cudaStreamSynchronize(c->stream));
+            FILE* fp = fopen(dbg_path, "wb");
+            if (fp) {
+                fwrite(h.data(), 8, h.size(), fp);
+                fclose(fp);
+            }
+        }
     }
     int err = 0;
     read_flags(c, flags, &f.shifts, &err);
