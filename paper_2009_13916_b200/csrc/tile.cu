@@ -332,6 +332,14 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
         double* ccb = b.cc + (size_t)t * b.RC * CK + (size_t)l0 * CK;
         short* esb = b.es + (size_t)t * b.RC * b.EK + (size_t)l0 * b.EK;
         double* ecb = b.ec + (size_t)t * b.RC * b.EK + (size_t)l0 * b.EK;
+        // early deps ordered oldest first (largest wavefront distance |gl(row) -
+        // gl(dep)|, gl = i+j+k), padding in front: the dataflow solve folds them
+        // in this order, so only the last few can still be in flight
+        auto gl = [&](int e) { return e % g.nx + (e / g.nx) % g.ny + e / (g.nx * g.ny); };
+        const int glr = gl(row);
+        short e_slot[EKMAX];
+        double e_val[EKMAX];
+        int e_dist[EKMAX];
         for (int e = b.D.ptr[row]; e < b.D.ptr[row + 1]; ++e) {
             int j = b.D.idx[e];
             double v = b.D.val ? b.D.val[e] : 0.0;
@@ -356,14 +364,24 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
                 ccb[nc * R + rr] = v;
                 ++nc;
             } else {
-                if (nE >= b.EK) { atomicExch(b.err, 11); continue; }
-                esb[nE * R + rr] = (short)slot;
-                ecb[nE * R + rr] = v;
-                ++nE;
+                if (nE >= b.EK || nE >= EKMAX) { atomicExch(b.err, 11); continue; }
+                const int dist = abs(glr - gl(j));
+                int q = nE++;
+                while (q > 0 && e_dist[q - 1] < dist) {   // stable: descending distance
+                    e_dist[q] = e_dist[q - 1];
+                    e_slot[q] = e_slot[q - 1];
+                    e_val[q] = e_val[q - 1];
+                    --q;
+                }
+                e_dist[q] = dist;
+                e_slot[q] = (short)slot;
+                e_val[q] = v;
             }
         }
         for (; nc < CK; ++nc) { csb[nc * R + rr] = (short)ZSLOT; ccb[nc * R + rr] = 0.0; }
-        for (; nE < b.EK; ++nE) { esb[nE * R + rr] = (short)ZSLOT; ecb[nE * R + rr] = 0.0; }
+        const int pad = b.EK - nE;
+        for (int q = 0; q < pad; ++q) { esb[q * R + rr] = (short)ZSLOT; ecb[q * R + rr] = 0.0; }
+        for (int q = 0; q < nE; ++q) { esb[(pad + q) * R + rr] = e_slot[q]; ecb[(pad + q) * R + rr] = e_val[q]; }
     }
     if (threadIdx.x == 0) {
         int* h = b.hdr + (size_t)t * 4;
@@ -912,6 +930,9 @@ __device__ __forceinline__ double poll_s(const double* p, int* err) {
 #ifndef FLOW_LAHEAD
 #define FLOW_LAHEAD 64     // loader window: need-levels polled past the first missing external
 #endif
+#ifndef FLOW_LATE
+#define FLOW_LATE 0        // newest early deps per lane folded one by one (measured: 0 is best)
+#endif
 #ifndef FLOW_DIRECT
 #define FLOW_DIRECT 1      // compute lanes read missing externals from L2 themselves
 #endif
@@ -1089,27 +1110,28 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                     const double d = di[p];
                     const int row = rid[p];
                     const double bv = bsm[p];
-                    // warp-uniform polling: one vote per round, no per-dependency branches
+                    // early deps arrive oldest first (plan order): the older ones are
+                    // polled as one batch (one vote per round), the FLOW_LATE newest per
+                    // lane one at a time, so the fold runs up to the first missing one
                     double ev[KH];
 #pragma unroll
                     for (int u = 0; u < KH; ++u) ev[u] = ld_vol_s(xs + es_[u]);
+                    constexpr int NB = KH > FLOW_LATE ? KH - FLOW_LATE : 0;
+                    auto fetch = [&](int u) -> double {   // an external the loader has not copied yet comes from L2
+                        const int q = es_[u] - a.RC;
+                        return (FLOW_DIRECT && q >= 0 && q < ne) ? flow_poll_g(a.x + eid_s[q]) : ld_vol_s(xs + es_[u]);
+                    };
                     {
                         bool miss = false;
 #pragma unroll
-                        for (int u = 0; u < KH; ++u) miss |= is_sent_hi(ev[u]);
+                        for (int u = 0; u < NB; ++u) miss |= is_sent_hi(ev[u]);
                         long long spins = 0;
-                        while (__any_sync(0xffffffffu, miss)) {   // externals / older rows still on their way
+                        while (__any_sync(0xffffffffu, miss)) {
                             if (FLOW_SLEEP_NS) __nanosleep(FLOW_SLEEP_NS);
                             miss = false;
 #pragma unroll
-                            for (int u = 0; u < KH; ++u) {
-                                if (is_sent_hi(ev[u])) {
-                                    // an external the loader has not copied yet is read from L2
-                                    // directly (one L2 hand-off instead of a loader round)
-                                    const int q = es_[u] - a.RC;
-                                    ev[u] = (FLOW_DIRECT && q >= 0 && q < ne) ? flow_poll_g(a.x + eid_s[q])
-                                                                              : ld_vol_s(xs + es_[u]);
-                                }
+                            for (int u = 0; u < NB; ++u) {
+                                if (is_sent_hi(ev[u])) ev[u] = fetch(u);
                                 miss |= is_sent_hi(ev[u]);
                             }
                             if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
@@ -1117,7 +1139,16 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                     }
                     double h = 0.0;
 #pragma unroll
-                    for (int u = 0; u < KH; ++u) h = fma(-ec_[u], ev[u], h);
+                    for (int u = 0; u < NB; ++u) h = fma(-ec_[u], ev[u], h);
+#pragma unroll
+                    for (int u = NB; u < KH; ++u) {
+                        long long spins = 0;
+                        while (__any_sync(0xffffffffu, is_sent_hi(ev[u]))) {
+                            if (is_sent_hi(ev[u])) ev[u] = fetch(u);
+                            if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
+                        }
+                        h = fma(-ec_[u], ev[u], h);
+                    }
                     h += __shfl_xor_sync(0xffffffffu, h, 1);   // same sum on both lanes
                     double acc = bv + h;
                     if (a.dbg2) c1 = gtimer();
