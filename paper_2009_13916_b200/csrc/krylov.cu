@@ -625,27 +625,50 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
         run_plan(c, ic.fwd, r_f, -1.0, ws.a_f.p, nullptr, nullptr, "trsv_ic_L");
         run_plan(c, ic.bwd, ws.a_f.p, 1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_LT");
     }
+    const char* tk = getenv("EDFA_TILE_KERNEL");
+    const bool flow = !tk || (tk[0] != 'l' && tk[0] != 'p');
+    const bool fuse = nc && il.fwd.is_tile && il.bwd.is_tile && flow && !getenv("EDFA_NO_FILL_FUSION");
+    // fused SpMVs (A_cf t_f in the L solve's gather, A_fc y_c in the second IC pair)
+    // are opt-in: measured 2 ms/step slower on config 2 than the separate SELL SpMVs
+    // (the gathers sit on the solves' critical paths)
+    static const bool fuse_mv = getenv("EDFA_FUSE_SPMV") != nullptr;
     if (nc) {
-        EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
-        spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
-        if (il.fwd.is_tile && il.bwd.is_tile && !getenv("EDFA_NO_FILL_FUSION")) {
-            // L writes c_c (SENTINEL since the last apply's U solve read it) and
-            // pre-fills y_c; U consumes c_c (resets it) and writes y_c
+        if (fuse && !fuse_mv) {
+            EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
+            spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
             run_tile_ex(c, const_cast<TilePlan&>(il.fwd.tile), ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L",
                         true, false, y_c);
             run_tile_ex(c, const_cast<TilePlan&>(il.bwd.tile), ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U",
                         true, true, nullptr);
+        } else if (fuse) {
+            // L: rhs r_c - A_cf t_f formed in its gather (fused SpMV), writes c_c
+            // (SENTINEL since the last apply's U solve read it) and pre-fills y_c;
+            // U consumes c_c (resets it) and writes y_c
+            run_tile_ex(c, const_cast<TilePlan&>(il.fwd.tile), r_c, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L",
+                        true, false, y_c, sys->A_cf, ws.t_f.p);
+            run_tile_ex(c, const_cast<TilePlan&>(il.bwd.tile), ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U",
+                        true, true, nullptr);
         } else {
+            EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
+            spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
             run_plan(c, il.fwd, ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L");
             run_plan(c, il.bwd, ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U");
             if (il.fwd.is_tile) fill_bits(c, ws.c_c.p, nc, SENTINEL_BITS);   // restore the invariant
         }
-        spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
+        if (!pair || !fuse_mv) spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
     } else if (nf) {
         EDFA_CUDA(cudaMemsetAsync(ws.a_f.p, 0, sizeof(double) * nf, c->stream));
     }
     if (nf) {
-        if (!pair || !run_chain_pair(c, ic.fwd.chain, ws.a_f.p, 1.0, nullptr, ws.t_f.p, y_f, "trsv_ic_pair")) {
+        // second pair: its right-hand side A_fc y_c is formed in the chain kernel (fused SpMV)
+        bool done = false;
+        if (pair) {
+            if (nc && fuse_mv) done = run_chain_pair(c, ic.fwd.chain, nullptr, 1.0, nullptr, ws.t_f.p, y_f,
+                                                     "trsv_ic_pair", sys->A_fc, y_c);
+            else done = run_chain_pair(c, ic.fwd.chain, ws.a_f.p, 1.0, nullptr, ws.t_f.p, y_f, "trsv_ic_pair");
+            if (!done && nc && fuse_mv) spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
+        }
+        if (!done) {
             run_plan(c, ic.fwd, ws.a_f.p, 1.0, y_f, nullptr, nullptr, "trsv_ic_L");
             // b and out2 alias row-wise only (thread r reads b[r] before writing out2[r])
             run_plan(c, ic.bwd, y_f, 1.0, ws.a_f.p, ws.t_f.p, y_f, "trsv_ic_LT");

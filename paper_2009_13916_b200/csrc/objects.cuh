@@ -59,8 +59,9 @@ void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, doubl
                const char* name);
 // x = (L L^T)^{-1} (alpha b) on the chains of L (out2 = x + add); false when
 // the chains are too long for the fused kernel (caller runs the two solves)
+// fz (optional): b := fz x (a fused SpMV; rows of fz = rows of the factor), b itself is ignored
 bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add,
-                    double* out2, const char* name);
+                    double* out2, const char* name, const Csr* fz = nullptr, const double* fz_x = nullptr);
 void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,
                int* shifts);
 
@@ -84,8 +85,10 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
 // x_prefilled: x already holds SENTINEL; consume_b: b's rows are reset to
 // SENTINEL once read; pre_sent: a vector set to SENTINEL row by row (the next
 // solve's output) -- lets consecutive solves skip their fill kernels
+// fz (optional): the right-hand side becomes b - fz x (a fused SpMV; rows of fz = rows of the factor)
 void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
-                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent);
+                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent, const Csr* fz = nullptr,
+                 const double* fz_x = nullptr);
 
 struct AxialPlan {              // pencil solves of axial-stencil cell factors (axial.cu)
     int32_t n = 0, R = 0, NJ = 0, NK = 0, nsteps = 0;

@@ -422,6 +422,10 @@ struct TileSolve {
     int mode;             // EDFA_TILE_MODE experiment bits (diagnostics)
     long long* dbg2;      // per-group timestamps (diagnostics): [tile][64][5]
     double* b_sent;       // flow kernel: == b, whose tile rows are reset to SENTINEL once read (or NULL)
+    const int32_t* fz_ptr;   // flow kernel: fused right-hand side b - M x (CSR rows = this factor's rows) or NULL
+    const int32_t* fz_idx;
+    const double* fz_val;
+    const double* fz_x;
     double* pre_sent;     // flow kernel: another vector whose tile rows are set to SENTINEL (or NULL)
 };
 
@@ -1027,6 +1031,19 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                 int p = p0 + u * FLOW_THREADS + threadIdx.x;
                 v[u] = p < n ? __ldg(a.b + rid[p]) : 0.0;
             }
+            if (a.fz_ptr) {   // fused SpMV: b_row - M_row . x (same FMA order as k_spmv_sell)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    int p = p0 + u * FLOW_THREADS + threadIdx.x;
+                    if (p < n) {
+                        const int row = rid[p];
+                        double acc = 0.0;
+                        for (int e = a.fz_ptr[row]; e < a.fz_ptr[row + 1]; ++e)
+                            acc = fma(a.fz_val[e], __ldg(a.fz_x + a.fz_idx[e]), acc);
+                        v[u] = fma(1.0, v[u], -acc);
+                    }
+                }
+            }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 int p = p0 + u * FLOW_THREADS + threadIdx.x;
@@ -1381,11 +1398,12 @@ static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
 
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name) {
-    run_tile_ex(c, tp, b, alpha, x, add, out2, name, false, false, nullptr);
+    run_tile_ex(c, tp, b, alpha, x, add, out2, name, false, false, nullptr, nullptr, nullptr);
 }
 
 void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
-                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent) {
+                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent, const Csr* fz,
+                 const double* fz_x) {
     size_t smem = tile_smem_bytes(tp);
     // EDFA_TILE_NOWAIT (profiling only): every upstream flag already matches,
     // so tiles run without waiting -- isolates per-tile processing cost
@@ -1398,7 +1416,7 @@ void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x,
     TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.LC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
                 tp.flags.p, tp.ticket.p, tp.epoch, 0, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr,
-                tp.xlev_ptr.p, tp.req.p, 0, nullptr, nullptr, nullptr};
+                tp.xlev_ptr.p, tp.req.p, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     static const int tile_mode = getenv("EDFA_TILE_MODE") ? atoi(getenv("EDFA_TILE_MODE")) : 0;
     a.mode = tile_mode;
     static const char* dbg_path = getenv("EDFA_TILE_DEBUG");
@@ -1420,7 +1438,15 @@ void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x,
     if (flow) {
         a.b_sent = consume_b ? const_cast<double*>(b) : nullptr;
         a.pre_sent = pre_sent;
+        if (fz) {
+            require(!consume_b, EDFA_ERR_CUDA, "fused right-hand side and consumed b are exclusive");
+            a.fz_ptr = fz->ptr.p;
+            a.fz_idx = fz->idx.p;
+            a.fz_val = fz->val.p;
+            a.fz_x = fz_x;
+        }
     } else {
+        require(!fz, EDFA_ERR_CUDA, "fused right-hand side needs the dataflow tile kernel");
         x_prefilled = false;
         if (consume_b) fill_bits(c, const_cast<double*>(b), tp.n, SENTINEL_BITS);
         if (pre_sent) fill_bits(c, pre_sent, tp.n, SENTINEL_BITS);
