@@ -251,6 +251,24 @@ int edfa_factor_part(edfa_ctx* ctx, edfa_factor* f, int which, const edfa_csr** 
  * hx/sparse.py:125-129). */
 int edfa_factor_solve(edfa_ctx* ctx, const edfa_factor* f, const double* r, double alpha, double* y);
 int edfa_factor_destroy(edfa_factor* f);
+/* One DCGS2 Arnoldi step of a slab-distributed GMRES (the building blocks of
+ * edfa_gmres, for vectors whose dot products are summed across slabs/GPUs
+ * between the calls).  V holds q_0..q_{j-1}, u_j, w = A P u_j in rows
+ * 0..j+1 (leading dimension ldv >= n).
+ *   edfa_dcgs2_dots:   dots_dev[0..j] = [Q_j u_j]^T u_j, dots_dev[64..64+j] =
+ *                      [Q_j u_j]^T w (local sums, 128 doubles, unused slots 0)
+ *   edfa_dcgs2_coeffs: from the globally summed dots: Hessenberg column j-1
+ *                      into H_dev ((m+1) x m, column-major) and hcol_dev,
+ *                      first-pass coefficients h1_dev (64), update weights
+ *                      coef_dev (192)
+ *   edfa_dcgs2_update: row j <- q_j, row j+1 <- u_{j+1} (local) */
+int edfa_dcgs2_dots(edfa_ctx* ctx, int64_t n, int32_t j, const double* V, int64_t ldv,
+                    double* dots_dev);
+int edfa_dcgs2_coeffs(edfa_ctx* ctx, int32_t j, int32_t m, const double* dots_dev,
+                      double* H_dev, double* h1_dev, double* coef_dev, double* hcol_dev);
+int edfa_dcgs2_update(edfa_ctx* ctx, int64_t n, int32_t j, double* V, int64_t ldv,
+                      const double* coef_dev);
+
 /* Gram-Schmidt passes on device vectors (GMRES on distributed vectors):
  * out_dev[k] = V_k . w (k < nvec <= 64, V_k = V + k*ldv);
  * out = w_in - hscale * sum_k h_dev[k] V_k (out = hscale * V h when w_in is NULL),

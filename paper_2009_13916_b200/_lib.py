@@ -96,6 +96,9 @@ _SIGS = {
     "edfa_factor_part": (i32, [vp, vp, i32, C.POINTER(vp)]),
     "edfa_factor_solve": (i32, [vp, vp, vp, f64, vp]),
     "edfa_factor_destroy": (i32, [vp]),
+    "edfa_dcgs2_dots": (i32, [vp, i64, i32, vp, i64, vp]),
+    "edfa_dcgs2_coeffs": (i32, [vp, i32, i32, vp, vp, vp, vp, vp]),
+    "edfa_dcgs2_update": (i32, [vp, i64, i32, vp, i64, vp]),
     "edfa_multidot": (i32, [vp, i64, i32, vp, i64, vp, vp]),
     "edfa_multiaxpy": (i32, [vp, i64, i32, vp, i64, vp, f64, vp, vp, vp]),
     "edfa_gather": (i32, [vp, i64, vp, vp, vp]),

@@ -564,9 +564,13 @@ int edfa_factor_solve(edfa_ctx* ctx, const edfa_factor* f, const double* r, doub
     require(ctx && f, EDFA_ERR_VALUE, "NULL argument");
     Ctx* c = &ctx->c;
     if (f->kind == 0) {
-        DevBuf<double> tmp(c, std::max(f->ic.n, 1));
-        run_plan(c, f->ic.fwd, r, alpha, tmp.p, nullptr, nullptr, "trsv_ic_L");
-        run_plan(c, f->ic.bwd, tmp.p, 1.0, y, nullptr, nullptr, "trsv_ic_LT");
+        // chain-structured factor: (L L^T)^-1 in one fused kernel (no shared state: safe for concurrent calls)
+        if (!(f->ic.fwd.is_chain && f->ic.bwd.is_chain &&
+              run_chain_pair(c, f->ic.fwd.chain, r, alpha, y, nullptr, nullptr, "trsv_ic_pair"))) {
+            DevBuf<double> tmp(c, std::max(f->ic.n, 1));
+            run_plan(c, f->ic.fwd, r, alpha, tmp.p, nullptr, nullptr, "trsv_ic_L");
+            run_plan(c, f->ic.bwd, tmp.p, 1.0, y, nullptr, nullptr, "trsv_ic_LT");
+        }
     } else {
         DevBuf<double> tmp(c, std::max(f->ilu.n, 1));
         run_plan(c, f->ilu.fwd, r, alpha, tmp.p, nullptr, nullptr, "trsv_ilu_L");
@@ -578,6 +582,25 @@ int edfa_factor_solve(edfa_ctx* ctx, const edfa_factor* f, const double* r, doub
 int edfa_factor_destroy(edfa_factor* f) {
     API_BEGIN
     delete f;
+    API_END
+}
+
+int edfa_dcgs2_dots(edfa_ctx* ctx, int64_t n, int32_t j, const double* V, int64_t ldv, double* dots_dev) {
+    API_BEGIN
+    dcgs2_dots_entry(&ctx->c, n, j, V, ldv, dots_dev);
+    API_END
+}
+
+int edfa_dcgs2_coeffs(edfa_ctx* ctx, int32_t j, int32_t m, const double* dots_dev, double* H_dev, double* h1_dev,
+                      double* coef_dev, double* hcol_dev) {
+    API_BEGIN
+    dcgs2_coeffs_entry(&ctx->c, j, m, dots_dev, H_dev, h1_dev, coef_dev, hcol_dev);
+    API_END
+}
+
+int edfa_dcgs2_update(edfa_ctx* ctx, int64_t n, int32_t j, double* V, int64_t ldv, const double* coef_dev) {
+    API_BEGIN
+    dcgs2_update_entry(&ctx->c, n, j, V, ldv, coef_dev);
     API_END
 }
 

@@ -217,6 +217,107 @@ constexpr int D2_GROUP = 8;
 #define EDFA_DOTS2_WAVE 2
 #endif
 
+// DCGS2 step coefficients from the reduced dots (executed by one 256-thread block):
+// dot[0..j] = [Q_j u]^T u, dot[64..64+j] = [Q_j u]^T w.  Writes Hessenberg column
+// j-1 (H, hcol), the first-pass coefficients h1 of the next step and the update
+// weights coef: [0..63] q_j, [64..127] u_{j+1}, [128..130] = (1/nu, 1/nu, -d_j/nu).
+__device__ void dcgs2_coeffs_block(const double* dot, int j, int m, double* __restrict__ H, double* __restrict__ h1,
+                                   double* __restrict__ coef, double* __restrict__ hcol) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int ld = m + 1, tid = threadIdx.x;
+    __shared__ double sa[64], st[64], sd[64], s_aa, s_ab, s_nu;
+    if (j == 0) {   // u_0 = q_0 is final: first projection only
+        if (tid == 0) {
+            const double c0 = dot[64];
+            h1[0] = c0;
+            coef[128] = 1.0;
+            coef[129] = 1.0;
+            coef[130] = -c0;
+        }
+        return;
+    }
+    if (tid < j) sa[tid] = dot[tid];
+    __syncthreads();
+    if (wid == 0) {
+        double aa = 0.0, ab = 0.0;
+        for (int i = lane; i < j; i += 32) {
+            aa = fma(sa[i], sa[i], aa);
+            ab = fma(sa[i], dot[64 + i], ab);
+        }
+        aa = warp_sum(aa);
+        ab = warp_sum(ab);
+        if (lane == 0) {
+            s_aa = aa;
+            s_ab = ab;
+            const double nu2 = dot[j] - aa;
+            s_nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+        }
+    }
+    __syncthreads();
+    const double nu = s_nu;
+    double* col = H + (int64_t)(j - 1) * ld;
+    if (tid < j) {
+        const double v = h1[tid] + sa[tid];
+        col[tid] = v;
+        hcol[tid] = v;
+    }
+    if (tid == j) { col[j] = nu; hcol[j] = nu; }
+    __syncthreads();
+    if (nu == 0.0) {   // happy breakdown: column j-1 ends the cycle
+        if (tid < 64) { coef[tid] = 0.0; coef[64 + tid] = 0.0; }
+        if (tid == 0) { coef[128] = 0.0; coef[129] = 0.0; coef[130] = 0.0; }
+        return;
+    }
+    const double inv = 1.0 / nu;
+    {   // t = H[:j+1, :j] a  (H[r, i] = 0 for r > i + 1): thread (r, quarter) loads
+        // its <= 16 entries at once, quarters summed in order
+        __shared__ double tq[4][64];
+        const int r = tid & 63, qt = tid >> 6;
+        double hv[16];
+        int ii[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int i = qt + 4 * u;
+            ii[u] = i;
+            hv[u] = (r <= j && i < j && i >= r - 1) ? H[(int64_t)i * ld + r] : 0.0;
+        }
+        double t = 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+            if (ii[u] < j) t = fma(hv[u], sa[ii[u]], t);
+        tq[qt][r] = t;
+        __syncthreads();
+        if (tid <= j) st[tid] = ((tq[0][tid] + tq[1][tid]) + tq[2][tid]) + tq[3][tid];
+    }
+    __syncthreads();
+    if (tid <= j) {
+        const double c = tid < j ? (dot[64 + tid] - st[tid]) * inv
+                                 : ((dot[64 + j] - s_ab) * inv - st[j]) * inv;
+        sd[tid] = st[tid] * inv + c;
+        h1[tid] = c;
+    }
+    __syncthreads();
+    if (tid < j) {
+        coef[tid] = sa[tid] * inv;
+        coef[64 + tid] = sd[tid] - sd[j] * sa[tid] * inv;
+    }
+    if (tid == 0) {
+        coef[128] = inv;
+        coef[129] = inv;
+        coef[130] = -sd[j] * inv;
+    }
+}
+
+// standalone coefficient kernel (slab path: dots reduced across slabs in between)
+__global__ void __launch_bounds__(RED_THREADS) k_dcgs2_coeffs(const double* __restrict__ dots, int j, int m,
+                                                              double* __restrict__ H, double* __restrict__ h1,
+                                                              double* __restrict__ coef, double* __restrict__ hcol) {
+    __shared__ double dot[128];
+    if (threadIdx.x < 128) dot[threadIdx.x] = dots[threadIdx.x];
+    __syncthreads();
+    dcgs2_coeffs_block(dot, j, m, H, h1, coef, hcol);
+}
+
 // dots of V_0..V_{nv-1} with u = V_{nv-1} and w = V_{nv}: grid (groups, ranges),
 // block-contiguous element ranges so the blocks sharing a range run together
 // and u, w come from L2 after the first group.  partial[r][0..63] = u-dots,
@@ -319,90 +420,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_dots2(const double* __restrict_
     }
     if (threadIdx.x == 0) *counter = 0u;
     __syncthreads();
-    // coefficients (j = nv - 1):  coef[0..63] = q_j weights, [64..127] = u_{j+1}
-    // weights, coef[128..130] = (1/nu, 1/nu, -d_j/nu)
-    const int ld = m + 1, tid = threadIdx.x;
-    __shared__ double sa[64], st[64], sd[64], s_aa, s_ab, s_nu;
-    if (j == 0) {   // u_0 = q_0 is final: first projection only
-        if (tid == 0) {
-            const double c0 = dot[64];
-            h1[0] = c0;
-            coef[128] = 1.0;
-            coef[129] = 1.0;
-            coef[130] = -c0;
-        }
+    if (!coef) {   // dots only (slab-distributed solves reduce them across slabs first)
+        const int t = threadIdx.x;
+        if (t < 128) hcol[t] = (t < nv || (t >= 64 && t < 64 + nv)) ? dot[t] : 0.0;
         return;
     }
-    if (tid < j) sa[tid] = dot[tid];
-    __syncthreads();
-    if (wid == 0) {
-        double aa = 0.0, ab = 0.0;
-        for (int i = lane; i < j; i += 32) {
-            aa = fma(sa[i], sa[i], aa);
-            ab = fma(sa[i], dot[64 + i], ab);
-        }
-        aa = warp_sum(aa);
-        ab = warp_sum(ab);
-        if (lane == 0) {
-            s_aa = aa;
-            s_ab = ab;
-            const double nu2 = dot[j] - aa;
-            s_nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
-        }
-    }
-    __syncthreads();
-    const double nu = s_nu;
-    double* col = H + (int64_t)(j - 1) * ld;
-    if (tid < j) {
-        const double v = h1[tid] + sa[tid];
-        col[tid] = v;
-        hcol[tid] = v;
-    }
-    if (tid == j) { col[j] = nu; hcol[j] = nu; }
-    __syncthreads();
-    if (nu == 0.0) {   // happy breakdown: column j-1 ends the cycle
-        if (tid < 64) { coef[tid] = 0.0; coef[64 + tid] = 0.0; }
-        if (tid == 0) { coef[128] = 0.0; coef[129] = 0.0; coef[130] = 0.0; }
-        return;
-    }
-    const double inv = 1.0 / nu;
-    {   // t = H[:j+1, :j] a  (H[r, i] = 0 for r > i + 1): thread (r, quarter) loads
-        // its <= 16 entries at once, quarters summed in order
-        __shared__ double tq[4][64];
-        const int r = tid & 63, qt = tid >> 6;
-        double hv[16];
-        int ii[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            const int i = qt + 4 * u;
-            ii[u] = i;
-            hv[u] = (r <= j && i < j && i >= r - 1) ? H[(int64_t)i * ld + r] : 0.0;
-        }
-        double t = 0.0;
-#pragma unroll
-        for (int u = 0; u < 16; ++u)
-            if (ii[u] < j) t = fma(hv[u], sa[ii[u]], t);
-        tq[qt][r] = t;
-        __syncthreads();
-        if (tid <= j) st[tid] = ((tq[0][tid] + tq[1][tid]) + tq[2][tid]) + tq[3][tid];
-    }
-    __syncthreads();
-    if (tid <= j) {
-        const double c = tid < j ? (dot[64 + tid] - st[tid]) * inv
-                                 : ((dot[64 + j] - s_ab) * inv - st[j]) * inv;
-        sd[tid] = st[tid] * inv + c;
-        h1[tid] = c;
-    }
-    __syncthreads();
-    if (tid < j) {
-        coef[tid] = sa[tid] * inv;
-        coef[64 + tid] = sd[tid] - sd[j] * sa[tid] * inv;
-    }
-    if (tid == 0) {
-        coef[128] = inv;
-        coef[129] = inv;
-        coef[130] = -sd[j] * inv;
-    }
+    dcgs2_coeffs_block(dot, j, m, H, h1, coef, hcol);
 }
 
 // slot j  <- q_j     = coef[128] u - sum_k coef[k] V_k          (j >= 1)
@@ -575,6 +598,42 @@ struct Blas {
                 k_axpy2<false><<<grid_for(n), RED_THREADS, 0, c->stream>>>(V, n, j, n, coef);
             check_launch("axpy2");
         }
+    }
+    // split DCGS2 step for slab-distributed vectors (ld = ldv)
+    void dcgs2_dots(const double* V, int64_t ldv, int64_t n, int j, double* dots_out, double* part2, int part2_rows) {
+        const int nv = j + 1;
+        const int groups = (nv + D2_GROUP - 1) / D2_GROUP;
+        int64_t ranges = std::max<int64_t>(1, std::min<int64_t>((EDFA_DOTS2_WAVE * NUM_SMS_B200) / groups,
+                                                                (n + 511) / 512));
+        ranges = std::min<int64_t>(ranges, part2_rows);
+        int64_t range = (n + ranges - 1) / ranges;
+        range = (range + 1) & ~int64_t(1);
+        ranges = (n + range - 1) / range;
+        unsigned* cnt = reinterpret_cast<unsigned*>(c->d_scalar_i + 60);
+        const bool v2 = n % 2 == 0 && ldv % 2 == 0 && aligned16(V);
+        Prof pr(c, "gs_dots2", 8.0 * n * (nv + 1));
+        dim3 grid(groups, (unsigned)ranges);
+        double* Vm = const_cast<double*>(V);
+        if (v2)
+            k_dots2<true><<<grid, RED_THREADS, 0, c->stream>>>(Vm, ldv, nv, n, range, part2, part2_rows, cnt, j, 0,
+                                                              nullptr, nullptr, nullptr, dots_out);
+        else
+            k_dots2<false><<<grid, RED_THREADS, 0, c->stream>>>(Vm, ldv, nv, n, range, part2, part2_rows, cnt, j, 0,
+                                                               nullptr, nullptr, nullptr, dots_out);
+        check_launch("dots2");
+    }
+    void dcgs2_coeffs(const double* dots, int j, int m, double* H, double* h1, double* coef, double* hcol) {
+        k_dcgs2_coeffs<<<1, RED_THREADS, 0, c->stream>>>(dots, j, m, H, h1, coef, hcol);
+        check_launch("dcgs2_coeffs");
+    }
+    void dcgs2_update(double* V, int64_t ldv, int64_t n, int j, const double* coef) {
+        const bool v2 = n % 2 == 0 && ldv % 2 == 0 && aligned16(V);
+        Prof pr(c, "gs_axpy2", 8.0 * n * (j + 2) + 8.0 * n * (j > 0 ? 2 : 1));
+        if (v2)
+            k_axpy2<true><<<grid_for(n), RED_THREADS, 0, c->stream>>>(V, ldv, j, n, coef);
+        else
+            k_axpy2<false><<<grid_for(n), RED_THREADS, 0, c->stream>>>(V, ldv, j, n, coef);
+        check_launch("axpy2");
     }
     double dot(const double* x, const double* y, int64_t n) {
         // x . y through the multidot path with V = x as a single vector
@@ -1051,6 +1110,24 @@ void multiaxpy_entry(Ctx* c, int64_t n, int nvec, const double* V, int64_t ldv, 
     require(nvec >= 0 && nvec <= 64, EDFA_ERR_VALUE, "nvec must be in [0, 64]");
     Blas bl(c);
     bl.multiaxpy(V, ldv, nvec, h, hscale, w_in, out, n, norm2_dev);
+}
+void dcgs2_dots_entry(Ctx* c, int64_t n, int j, const double* V, int64_t ldv, double* dots_out) {
+    require(j >= 0 && j <= 62, EDFA_ERR_VALUE, "j must be in [0, 62]");
+    require(ldv >= n, EDFA_ERR_VALUE, "ldv must be >= n");
+    Blas bl(c);
+    DevBuf<double> part2(c, (size_t)4 * NUM_SMS_B200 * 128);
+    bl.dcgs2_dots(V, ldv, n, j, dots_out, part2.p, 4 * NUM_SMS_B200);
+}
+void dcgs2_coeffs_entry(Ctx* c, int j, int m, const double* dots, double* H, double* h1, double* coef, double* hcol) {
+    require(j >= 0 && j <= m && m >= 1 && m <= 62, EDFA_ERR_VALUE, "need 0 <= j <= m <= 62");
+    Blas bl(c);
+    bl.dcgs2_coeffs(dots, j, m, H, h1, coef, hcol);
+}
+void dcgs2_update_entry(Ctx* c, int64_t n, int j, double* V, int64_t ldv, const double* coef) {
+    require(j >= 0 && j <= 62, EDFA_ERR_VALUE, "j must be in [0, 62]");
+    require(ldv >= n, EDFA_ERR_VALUE, "ldv must be >= n");
+    Blas bl(c);
+    bl.dcgs2_update(V, ldv, n, j, coef);
 }
 void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double* y) {
     Blas bl(c);

@@ -227,4 +227,7 @@ void csr_submatrix(Ctx* c, const Csr& A, const int32_t* rows, int32_t n_out, con
                    Csr& out);
 void gather(Ctx* c, int64_t n, const int32_t* idx, const double* x, double* out);
 void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double* y);
+void dcgs2_dots_entry(Ctx* c, int64_t n, int j, const double* V, int64_t ldv, double* dots_out);
+void dcgs2_coeffs_entry(Ctx* c, int j, int m, const double* dots, double* H, double* h1, double* coef, double* hcol);
+void dcgs2_update_entry(Ctx* c, int64_t n, int j, double* V, int64_t ldv, const double* coef);
 }  // namespace edfa

@@ -440,6 +440,29 @@ class CudaSlab:
         L.check(self.lib.edfa_axpby(self.ctx, y.numel(), a, C.c_void_p(x.data_ptr()), b,
                                     C.c_void_p(y.data_ptr())))
 
+    # DCGS2 building blocks (krylov.cu): local dots, coefficients from the summed
+    # dots, local two-output update
+    def dcgs2_dots(self, V, j, out):
+        L.check(self.lib.edfa_dcgs2_dots(self.ctx, self.layout.n_own, j, C.c_void_p(V.data_ptr()), V.stride(0),
+                                         C.c_void_p(out.data_ptr())))
+
+    def dcgs2_coeffs(self, j, m, dots, H, h1, coef, hcol):
+        L.check(self.lib.edfa_dcgs2_coeffs(self.ctx, j, m, C.c_void_p(dots.data_ptr()), C.c_void_p(H.data_ptr()),
+                                           C.c_void_p(h1.data_ptr()), C.c_void_p(coef.data_ptr()),
+                                           C.c_void_p(hcol.data_ptr())))
+
+    def dcgs2_update(self, V, j, coef):
+        L.check(self.lib.edfa_dcgs2_update(self.ctx, self.layout.n_own, j, C.c_void_p(V.data_ptr()), V.stride(0),
+                                           C.c_void_p(coef.data_ptr())))
+
+    def fetch(self, t):
+        """Asynchronous device->host copy of t; returns a callable giving the array."""
+        host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        host.copy_(t, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return lambda: (ev.synchronize(), host.numpy())[1]
+
     def copy(self, src, dst):
         self.axpby(1.0, src, 0.0, dst)
 
@@ -534,11 +557,14 @@ class SlabOperator:
 def slab_gmres(op: SlabOperator, bs, tol=1e-8, restart=50, max_it=2000):
     """Right-preconditioned restarted GMRES(m) on slab-distributed vectors.
 
-    The same algorithm as the single-device solver (krylov.cu): x0 = 0, CGS
-    Arnoldi with DGKS selective re-orthogonalisation (fused multi-dot +
-    multi-axpy per pass, dot products summed over slabs), Givens rotations on
-    the host, convergence confirmed on the true residual (hx/krylov.py
-    conventions).  Returns (list of local x, SolveReport)."""
+    The same algorithm as the single-device solver (krylov.cu gmres): x0 = 0,
+    DCGS2 Arnoldi -- per step one local dot kernel, ONE all-reduce of the
+    2(j+1) dot products over the slabs (NCCL over NVLink between GPUs), the
+    coefficient kernel on the summed dots and one local two-output update --
+    and the host one step behind the devices (it reads Hessenberg column j-1
+    while step j+1 is queued), Givens rotations on the host, convergence
+    confirmed on the true residual (hx/krylov.py conventions).
+    Returns (list of local x, SolveReport)."""
     if tol <= 0:
         raise ValueError("tol must be positive")
     if not 1 <= restart <= 62:
@@ -559,10 +585,30 @@ def slab_gmres(op: SlabOperator, bs, tol=1e-8, restart=50, max_it=2000):
         rep.converged, rep.final_relres = True, 0.0
         rep.relres_history.append(0.0)
         return xs, rep
-    V = [p.empty(m + 1, p.layout.n_own) for p in parts]
+    V = [p.empty(m + 2, p.layout.n_own) for p in parts]
+    Hd = [p.empty(m, m + 1).zero_() for p in parts]        # unrotated Hessenberg, column i = row i
+    h1 = [p.empty(64).zero_() for p in parts]
+    coef = [p.empty(192).zero_() for p in parts]
+    dots = [p.empty(128).zero_() for p in parts]
+    hcol = [p.empty(2, 64).zero_() for p in parts]
     rs = [b.clone() for b in bs]
     beta = bnorm
     happy = False
+    pending = {}
+
+    def enqueue_step(st):
+        op.precond_into_zext([v[st] for v in V])
+        op.matvec_zext([v[st + 1] for v in V])
+        for p, v, d in zip(parts, V, dots):
+            p.dcgs2_dots(v, st, d)
+        dsum = op.allsum(dots)
+        for i, p in enumerate(parts):
+            p.dcgs2_coeffs(st, m, dsum.to(dots[i].device), Hd[i], h1[i], coef[i], hcol[i][st & 1])
+        for p, v, cf in zip(parts, V, coef):
+            p.dcgs2_update(v, st, cf)
+        if st >= 1:
+            pending[st] = parts[0].fetch(hcol[0][st & 1][:st + 1])
+
     while rep.n_it < max_it:
         for p, v, r in zip(parts, V, rs):
             p.axpby(1.0 / beta, r, 0.0, v[0])
@@ -570,32 +616,21 @@ def slab_gmres(op: SlabOperator, bs, tol=1e-8, restart=50, max_it=2000):
         cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
         g[0] = beta
         k = 0
-        for j in range(m):
-            op.precond_into_zext([v[j] for v in V])
-            op.matvec_zext([v[j + 1] for v in V])
+        budget = min(m, max_it - rep.n_it)     # columns this cycle (step s finalises column s-1)
+        enq = 0
+        pending.clear()
+        enqueue_step(enq)
+        enq += 1
+        enqueue_step(enq)
+        enq += 1
+        for j in range(budget):
+            if enq <= budget:
+                enqueue_step(enq)              # keep one step ahead of the host
+                enq += 1
+            col = pending.pop(j + 1)()
             rep.n_it += 1
-            ws = [v[j + 1] for v in V]
-            for p, v, w, h in zip(parts, V, ws, hd):
-                p.multidot(v, j + 2, w, h[:j + 2])
-            hsum = op.allsum([h[:j + 2] for h in hd])
-            for p, v, w, h in zip(parts, V, ws, hd):
-                p.multiaxpy(v, j + 1, hsum, w, w, h[64:65])
-            nsum = op.allsum([h[64:65] for h in hd])
-            host = torch.cat([hsum, nsum]).cpu().numpy()
-            w0 = math.sqrt(max(host[j + 1], 0.0))
-            wn = math.sqrt(max(host[j + 2], 0.0))
-            H[:j + 1, j] = host[:j + 1]
-            if wn < 0.7071067811865476 * w0:             # DGKS second pass
-                for p, v, w, h in zip(parts, V, ws, hd):
-                    p.multidot(v, j + 1, w, h[:j + 1])
-                hsum = op.allsum([h[:j + 1] for h in hd])
-                for p, v, w, h in zip(parts, V, ws, hd):
-                    p.multiaxpy(v, j + 1, hsum, w, w, h[64:65])
-                nsum = op.allsum([h[64:65] for h in hd])
-                host = torch.cat([hsum, nsum]).cpu().numpy()
-                H[:j + 1, j] += host[:j + 1]
-                wn = math.sqrt(max(host[j + 1], 0.0))
-            H[j + 1, j] = wn
+            H[:j + 2, j] = col[:j + 2]
+            wn = col[j + 1]
             for i in range(j):
                 a, c = H[i, j], H[i + 1, j]
                 H[i, j] = cs[i] * a + sn[i] * c
@@ -611,10 +646,9 @@ def slab_gmres(op: SlabOperator, bs, tol=1e-8, restart=50, max_it=2000):
             if wn == 0.0:
                 happy = True
                 break
-            for p, w in zip(parts, ws):
-                p.axpby(1.0 / wn, w, 0.0, w)
-            if est <= tol or rep.n_it >= max_it:
+            if est <= tol:
                 break
+        # queued speculative steps only write rows >= k + 1
         y = np.zeros(k)
         for i in range(k - 1, -1, -1):
             s = g[i] - H[i, i + 1:k] @ y[i + 1:k]

@@ -8,6 +8,8 @@ exercised with the gloo backend on CPU.  The product path never uses it.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -73,6 +75,57 @@ class CpuSlab:
 
     def axpby(self, a, x, b, y):
         y.copy_(a * x if b == 0.0 else a * x + b * y)
+
+    # DCGS2 building blocks: numpy restatement of krylov.cu's k_dots2 /
+    # dcgs2_coeffs_block / k_axpy2 (the coefficient algebra is the product's)
+    def dcgs2_dots(self, V, j, out):
+        Vn = V.numpy()
+        out.zero_()
+        out[:j + 1] = torch.from_numpy(Vn[:j + 1] @ Vn[j])
+        out[64:65 + j] = torch.from_numpy(Vn[:j + 1] @ Vn[j + 1])
+
+    def dcgs2_coeffs(self, j, m, dots, H, h1, coef, hcol):
+        d = dots.numpy()
+        Hn = H.numpy()            # (m, m+1): row i = Hessenberg column i
+        if j == 0:
+            h1[0] = d[64]
+            coef[128], coef[129], coef[130] = 1.0, 1.0, -d[64]
+            return
+        a = d[:j].copy()
+        aa, ab = a @ a, a @ d[64:64 + j]
+        nu2 = d[j] - aa
+        nu = math.sqrt(nu2) if nu2 > 0.0 else 0.0
+        colv = h1.numpy()[:j] + a
+        Hn[j - 1, :j] = colv
+        Hn[j - 1, j] = nu
+        hcol[:j] = torch.from_numpy(colv)
+        hcol[j] = nu
+        if nu == 0.0:
+            coef.zero_()
+            return
+        inv = 1.0 / nu
+        t = np.array([sum(Hn[i, r] * a[i] for i in range(max(0, r - 1), j)) for r in range(j + 1)])
+        c = np.empty(j + 1)
+        c[:j] = (d[64:64 + j] - t[:j]) * inv
+        c[j] = ((d[64 + j] - ab) * inv - t[j]) * inv
+        dd = t * inv + c
+        h1[:j + 1] = torch.from_numpy(c)
+        coef[:j] = torch.from_numpy(a * inv)
+        coef[64:64 + j] = torch.from_numpy(dd[:j] - dd[j] * a * inv)
+        coef[128], coef[129], coef[130] = inv, inv, -dd[j] * inv
+
+    def dcgs2_update(self, V, j, coef):
+        Vn, cf = V.numpy(), coef.numpy()
+        u, w = Vn[j].copy(), Vn[j + 1].copy()
+        q = cf[128] * u - cf[:j] @ Vn[:j]
+        wt = cf[129] * w + cf[130] * u - cf[64:64 + j] @ Vn[:j]
+        if j > 0:
+            Vn[j] = q
+        Vn[j + 1] = wt
+
+    def fetch(self, t):
+        a = t.numpy().copy()
+        return lambda: a
 
     def copy(self, src, dst):
         dst.copy_(src)
