@@ -407,6 +407,8 @@ def run_edfa(args):
                      "shares_from": "per-kernel CUDA events of the last warm-up step (same workload)"},
         "clocks": clocks,
     }
+    if rank == 0 and "inputs" in case.meta:
+        line["assembly"] = assembly_leg(case, c, lib, report, N)
     if args.profile_json and rank == 0:
         pathlib.Path(args.profile_json).write_text(json.dumps({"timed_region": prof, "warmup_step": prof_full},
                                                               indent=1))
@@ -420,6 +422,43 @@ def run_edfa(args):
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+def assembly_leg(case, c, lib, report, N):
+    """The device assembly of the same system (the
+    producer of the path's blocks): hexflow's assemble through
+    device_assembly.assemble_device -- grid arrays and tensors uploaded from
+    host numpy, blocks left in HBM -- against the host numpy assembly."""
+    import torch
+
+    from paper_2009_13916_b200 import device_assembly as DA
+    g, fld, props, bc, dt, p0 = case.meta["inputs"]
+    DA.assemble_device(g, fld, props, bc, dt, p0)
+    torch.cuda.synchronize()
+    lib.edfa_ctx_profile_filter(c, b"asm_")
+    lib.edfa_ctx_profile(c, 1)
+    report(c)
+    ts = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d = DA.assemble_device(g, fld, props, bc, dt, p0)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        del d
+    prof = report(c)
+    lib.edfa_ctx_profile(c, 0)
+    lib.edfa_ctx_profile_filter(c, b"")
+    kms = sum(v["ms"] for v in prof.values()) / 3
+    kbytes = sum(v["bytes"] for v in prof.values()) / 3
+    t = statistics.median(ts)
+    host = case.meta.get("host_assembly_s")
+    return {"seconds": t, "mdof_s": N / t / 1e6, "kernel_ms": kms,
+            "kernel_gbs": kbytes / (kms / 1e3) / 1e9 if kms > 0 else None,
+            "kernels": {k: round(v["ms"] / 3, 4) for k, v in prof.items()},
+            "host_numpy_seconds": host, "speedup_vs_host_numpy": host / t if host else None,
+            "scope": "assemble_device: H2D of grid/tensor arrays + element operators + block rows + "
+                     "Dirichlet elimination + accumulation (hx/assembly.py:186-333)"}
 
 
 # ---------------------------------------------------------------- slab-partitioned arm (N > 1)

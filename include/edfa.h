@@ -18,6 +18,9 @@
  *   edfa_spmv / edfa_system_spmv          sparse.spmv (sparse.py:37-42), A @ v (driver.py:135-139)
  *   edfa_bicgstab                         krylov.bicgstab (krylov.py:40-115)
  *   edfa_gmres                            GMRES(m) -- absent from the reference
+ *   edfa_assemble                         assembly.assemble (assembly.py:186-311), the
+ *                                         producer of the path's blocks
+ *   edfa_update_accumulation              assembly.update_accumulation (assembly.py:314-333)
  *
  * Conventions
  *   - Every call is stream-ordered on the context's stream.  Calls that must
@@ -280,6 +283,55 @@ int edfa_multiaxpy(edfa_ctx* ctx, int64_t n, int32_t nvec, const double* V, int6
                    double* norm2_dev);
 /* out[i] = x[idx[i]]  (halo send buffers). */
 int edfa_gather(edfa_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* out);
+
+/* ---- RT0 MHFE / FV assembly --------------------------
+ * Device arrays of a hexahedral grid in hexflow's numbering (hx/grid.py:22-65):
+ * cells x-fastest, faces grouped by family and k-slowest, local slots
+ * (-x,+x,-y,+y,-z,+z), face_to_elems[f][0] = owner (lower-indexed cell). */
+typedef struct edfa_hex_grid {
+    int32_t n_cells, n_faces, n_nodes;
+    const double*  node_coords;      /* [n_nodes][3]                          */
+    const int32_t* elem_to_nodes;    /* [n_cells][8], hx/refelem.py:13-16     */
+    const int32_t* elem_to_faces;    /* [n_cells][6]                          */
+    const int32_t* face_to_elems;    /* [n_faces][2], -1 on the hull          */
+    const int32_t* face_local;       /* [n_faces][2], -1 on the hull          */
+    const double*  face_area;        /* [n_faces]                             */
+} edfa_hex_grid;
+
+typedef struct edfa_assembly_in {
+    const double* K;                 /* [n_cells][3][3] conductivity tensors   */
+    double gamma;                    /* FluidRockProps.gamma                   */
+    const int8_t* face_bc;           /* [n_faces] 0 none, 1 pressure, 2 flux   */
+    const double* face_value;        /* [n_faces] prescribed pressure / flux   */
+    const double* source;            /* [n_cells] or NULL (zero source)        */
+    const double* storage;           /* [n_cells] storage coefficient or NULL  */
+    double storage_scalar;           /* used when storage is NULL              */
+} edfa_assembly_in;
+
+typedef struct edfa_assembly_out {   /* caller-allocated device arrays         */
+    int32_t* face_index;             /* [n_faces] free numbering, -1 = Dirichlet */
+    double*  rhs_f;                  /* [n_faces] capacity; first n_free used  */
+    double*  rhs_c_base;             /* [n_cells]                              */
+    double*  elem_volume;            /* [n_cells] 2x2x2 Gauss volumes          */
+    double*  accumulation;           /* [n_cells] volume * storage             */
+    double*  binv;                   /* [36][n_cells] Binv (SoA) or NULL       */
+    double*  row_sums;               /* [6][n_cells] or NULL                   */
+    double*  diag;                   /* [6][n_cells] or NULL                   */
+    int32_t  n_free;                 /* out: number of free faces              */
+    int32_t  bad_element;            /* out: first inverted element or -1      */
+} edfa_assembly_out;
+
+/* Steady blocks A_ff, A_fc, A_cf, A_cc_steady (canonical CSR, free faces
+ * first) and rhs of assemble(..., dt=inf).  An inverted element or a
+ * non-SPD elemental matrix -> EDFA_ERR_VALUE (GeometryError/AssemblyError). */
+int edfa_assemble(edfa_ctx* ctx, const edfa_hex_grid* grid, const edfa_assembly_in* in,
+                  edfa_assembly_out* out, edfa_csr** A_ff, edfa_csr** A_fc, edfa_csr** A_cf,
+                  edfa_csr** A_cc_steady);
+/* A_cc = canonical(A_cc_steady + diag(acc/dt)), rhs_c = rhs_c_base + acc*p_prev/dt
+ * (p_prev NULL = zeros; dt = +inf returns the steady pair). */
+int edfa_update_accumulation(edfa_ctx* ctx, const edfa_csr* A_cc_steady, const double* accumulation,
+                             const double* rhs_c_base, const double* p_prev, double dt,
+                             edfa_csr** A_cc, double* rhs_c);
 
 #ifdef __cplusplus
 }

@@ -49,6 +49,23 @@ class Report(C.Structure):
                 ("final_relres", f64)]
 
 
+class HexGridDesc(C.Structure):
+    _fields_ = [("n_cells", i32), ("n_faces", i32), ("n_nodes", i32), ("node_coords", vp),
+                ("elem_to_nodes", vp), ("elem_to_faces", vp), ("face_to_elems", vp), ("face_local", vp),
+                ("face_area", vp)]
+
+
+class AssemblyIn(C.Structure):
+    _fields_ = [("K", vp), ("gamma", f64), ("face_bc", vp), ("face_value", vp), ("source", vp),
+                ("storage", vp), ("storage_scalar", f64)]
+
+
+class AssemblyOut(C.Structure):
+    _fields_ = [("face_index", vp), ("rhs_f", vp), ("rhs_c_base", vp), ("elem_volume", vp),
+                ("accumulation", vp), ("binv", vp), ("row_sums", vp), ("diag", vp), ("n_free", i32),
+                ("bad_element", i32)]
+
+
 _SIGS = {
     "edfa_abi_version": (i32, []),
     "edfa_last_error": (C.c_char_p, []),
@@ -102,6 +119,9 @@ _SIGS = {
     "edfa_multidot": (i32, [vp, i64, i32, vp, i64, vp, vp]),
     "edfa_multiaxpy": (i32, [vp, i64, i32, vp, i64, vp, f64, vp, vp, vp]),
     "edfa_gather": (i32, [vp, i64, vp, vp, vp]),
+    "edfa_assemble": (i32, [vp, C.POINTER(HexGridDesc), C.POINTER(AssemblyIn), C.POINTER(AssemblyOut),
+                            C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+    "edfa_update_accumulation": (i32, [vp, vp, vp, vp, vp, f64, C.POINTER(vp), vp]),
 }
 
 _lib = None

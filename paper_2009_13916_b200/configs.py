@@ -20,6 +20,7 @@ Inner solves everywhere: IC(0)/ILU(0) (``no_fill=True``, drop tol 0; D5).
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -38,6 +39,14 @@ class CaseSpec:
     restart: int = 50
     max_it: int = 2000
     meta: dict = field(default_factory=dict)
+
+
+def _assemble(g, fld, props, bc, dt, p_prev):
+    """Host assembly plus the inputs it was built from (kept so the device
+    assembly, device_assembly.assemble_device, can rebuild the same system)."""
+    t = time.perf_counter()
+    s = assembly.assemble(g, fld, props, bc, dt=dt, p_prev=p_prev)
+    return s, dict(inputs=(g, fld, props, bc, dt, p_prev), host_assembly_s=time.perf_counter() - t)
 
 
 def _inner():
@@ -67,9 +76,8 @@ def config1(n=16):
     g = mesh.box_grid(n, n, n, 1.0 / n, 1.0 / n, 1.0 / n)
     fld = mesh.Conductivity.homogeneous(g.n_elems, 1.0)
     bc = mesh.Boundaries(pressure_planes={"x-": 1.0, "x+": 0.0})
-    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=1.0,
-                          p_prev=np.zeros(g.n_elems))
-    return CaseSpec(f"config1-{n}^3-base", s, dict(pattern="base", **_inner()))
+    s, meta = _assemble(g, fld, mesh.RockProps(gamma=1.0), bc, 1.0, np.zeros(g.n_elems))
+    return CaseSpec(f"config1-{n}^3-base", s, dict(pattern="base", **_inner()), meta=meta)
 
 
 def config2(n=64, seed=SEEDS[2], length=1000.0, nz=None):
@@ -79,10 +87,9 @@ def config2(n=64, seed=SEEDS[2], length=1000.0, nz=None):
     g = mesh.box_grid(n, n, nz or n, h, h, h)
     fld = lognormal_aniso_field(g.n_elems, seed)
     bc = mesh.Boundaries(pressure_planes={"x-": 1.0, "x+": 0.0})
-    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=1.0,
-                          p_prev=np.zeros(g.n_elems))
+    s, meta = _assemble(g, fld, mesh.RockProps(gamma=1.0), bc, 1.0, np.zeros(g.n_elems))
     return CaseSpec(f"config2-{n}^3-staticA" if not nz or nz == n else f"config2-{n}x{n}x{nz}-staticA", s,
-                    dict(pattern="static", prototype="A", **_inner()))
+                    dict(pattern="static", prototype="A", **_inner()), meta=meta)
 
 
 def config3(n=128, seed=SEEDS[3]):
@@ -90,10 +97,9 @@ def config3(n=128, seed=SEEDS[3]):
     g = mesh.perturb_interior(g, 0.2, seed)
     fld = rotated_tensor_field(g.n_elems, seed + 1)
     bc = mesh.Boundaries(wells=[(0, 0, 1.0), (n - 1, n - 1, 0.0)])
-    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=1.0,
-                          p_prev=np.zeros(g.n_elems))
+    s, meta = _assemble(g, fld, mesh.RockProps(gamma=1.0), bc, 1.0, np.zeros(g.n_elems))
     return CaseSpec(f"config3-{n}^3-dynamic14", s,
-                    dict(pattern="dynamic", n_add=1, n_ent=4, **_inner()))
+                    dict(pattern="dynamic", n_add=1, n_ent=4, **_inner()), meta=meta)
 
 
 def channelised_field(nx, ny, nz, seed, sigma=2.5, kv_kh=0.1, n_channel_layers=None):
@@ -124,11 +130,10 @@ def config4(nx=60, ny=220, nz=85, seed=SEEDS[4], dt=0.1):
     bc = mesh.Boundaries(wells=[(0, 0, 200.0), (nx - 1, 0, 200.0),
                                 (0, ny - 1, 200.0), (nx - 1, ny - 1, 200.0),
                                 (nx // 2, ny // 2, 100.0)])
-    s = assembly.assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt=dt,
-                          p_prev=np.full(g.n_elems, 140.0))
+    s, meta = _assemble(g, fld, mesh.RockProps(gamma=1.0), bc, dt, np.full(g.n_elems, 140.0))
     return CaseSpec(f"config4-{nx}x{ny}x{nz}-staticA-transient", s,
                     dict(pattern="static", prototype="A", **_inner()),
-                    meta=dict(p_init=140.0, n_steps=10, dt0=dt, dt_max=5.0,
+                    meta=dict(meta, p_init=140.0, n_steps=10, dt0=dt, dt_max=5.0,
                               dt_mult=1.1, dp_target=5.0))
 
 

@@ -624,5 +624,44 @@ int edfa_gather(edfa_ctx* ctx, int64_t n, const int32_t* idx, const double* x, d
     API_END
 }
 
+int edfa_assemble(edfa_ctx* ctx, const edfa_hex_grid* grid, const edfa_assembly_in* in, edfa_assembly_out* out,
+                  edfa_csr** A_ff, edfa_csr** A_fc, edfa_csr** A_cf, edfa_csr** A_cc_steady) {
+    API_BEGIN
+    require(ctx && grid && in && out && A_ff && A_fc && A_cf && A_cc_steady, EDFA_ERR_VALUE, "NULL argument");
+    edfa_csr* h[4];
+    for (auto& x : h) {
+        x = new edfa_csr();
+        x->ctx = &ctx->c;
+    }
+    try {
+        assemble(&ctx->c, *grid, *in, *out, h[0]->own, h[1]->own, h[2]->own, h[3]->own);
+    } catch (...) {
+        for (auto* x : h) delete x;
+        throw;
+    }
+    *A_ff = h[0];
+    *A_fc = h[1];
+    *A_cf = h[2];
+    *A_cc_steady = h[3];
+    API_END
+}
+
+int edfa_update_accumulation(edfa_ctx* ctx, const edfa_csr* A_cc_steady, const double* accumulation,
+                             const double* rhs_c_base, const double* p_prev, double dt, edfa_csr** A_cc,
+                             double* rhs_c) {
+    API_BEGIN
+    require(ctx && A_cc_steady && accumulation && rhs_c_base && A_cc && rhs_c, EDFA_ERR_VALUE, "NULL argument");
+    auto* h = new edfa_csr();
+    h->ctx = &ctx->c;
+    try {
+        update_accumulation(&ctx->c, M(A_cc_steady), accumulation, rhs_c_base, p_prev, dt, h->own, rhs_c);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *A_cc = h;
+    API_END
+}
+
 }  // extern "C"
 

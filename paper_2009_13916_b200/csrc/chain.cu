@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(128) k_chain_solve(const int* __restrict__ row
 // L_ii = sqrt(d) -- the same IEEE operations as the general k_ic0.
 __global__ void k_chain_ic0(const int* __restrict__ rows, const int64_t* __restrict__ gbase, int n_chains,
                             const int32_t* __restrict__ Lp, double* __restrict__ Lv, const double* __restrict__ aii,
-                            const double* __restrict__ scale, double* __restrict__ diag, int* shifts) {
+                            const double* __restrict__ scale, double* __restrict__ diag, int* shifts,
+                            double fill_tol) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_chains) return;
     int64_t p = gbase[t >> 5] + (t & 31), end = gbase[(t >> 5) + 1];
@@ -116,7 +117,9 @@ __global__ void k_chain_ic0(const int* __restrict__ rows, const int64_t* __restr
         if (i < 0) break;
         double d = aii[i];
         int lo = Lp[i];
-        if (Lp[i + 1] > lo) {
+        if (Lp[i + 1] > lo && fabs(Lv[lo]) < fill_tol * scale[i]) {
+            Lv[lo] = 0.0;   // dropped (hx/sparse.py:255-256)
+        } else if (Lp[i + 1] > lo) {
             double mult = __ddiv_rn(Lv[lo], dprev);
             Lv[lo] = mult;
             d = sub_mul(d, mult, mult);
@@ -412,10 +415,10 @@ void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, doubl
 }
 
 void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,
-               int* shifts) {
+               int* shifts, double fill_tol) {
     Prof pr(c, "ic0_factor", 40.0 * cp.n);
     k_chain_ic0<<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(cp.rows.p, cp.gbase.p, cp.n_chains, Lpat.ptr.p,
-                                                                   Lpat.val.p, aii, scale, diag, shifts);
+                                                                   Lpat.val.p, aii, scale, diag, shifts, fill_tol);
     check_launch("k_chain_ic0");
 }
 

@@ -74,7 +74,7 @@ struct LevelArgs {
 __global__ void __launch_bounds__(256) k_ic0(LevelArgs la, const int32_t* __restrict__ Lp,
                                              const int32_t* __restrict__ Li, double* __restrict__ Lv,
                                              const double* __restrict__ aii, const double* __restrict__ scale,
-                                             double* __restrict__ diag, int* shifts) {
+                                             double* __restrict__ diag, int* shifts, double fill_tol) {
     const int nthr = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     for (int L = 0; L < la.n_levels; ++L) {
@@ -84,8 +84,13 @@ __global__ void __launch_bounds__(256) k_ic0(LevelArgs la, const int32_t* __rest
             if (i < 0) continue;
             int lo = Lp[i], hi = Lp[i + 1];
             double d = aii[i];
+            const double tau = fill_tol * scale[i];
             for (int p = lo; p < hi; ++p) {
                 int k = Li[p];
+                if (fabs(Lv[p]) < tau) {   // dropped on the unscaled working value
+                    Lv[p] = 0.0;
+                    continue;
+                }
                 double mult = __ddiv_rn(Lv[p], __ldcg(diag + k));
                 Lv[p] = mult;
                 for (int q = p + 1; q < hi; ++q) {
@@ -421,9 +426,10 @@ int coop_grid(K kern, int threads, size_t smem, int cap = 2) {
 
 }  // namespace
 
-void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f) {
-    require(drop_tol == 0.0, EDFA_ERR_UNSUPPORTED,
-            "IC with a drop tolerance (face_drop_tol > 0) is not implemented on the GPU path; use 0 with no_fill");
+void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels);
+
+void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f, bool no_fill) {
+    require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
     const int n = A_ff.n_rows;
     f.n = n;
     select_part(c, A_ff, 0, -1.0, true, f.Lpat);
@@ -435,10 +441,22 @@ void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f) {
         check_launch("k_diag_scale");
     }
     build_plan(c, f.Lpat, nullptr, false, false, f.fwd);
+    // a chain-structured (disjoint paths) pattern has no fill-in, so IC(tau)
+    // with fill equals the pattern-restricted factorisation there
+    if (!no_fill && n && !f.fwd.is_chain) {
+        ict_factor(c, A_ff, -1.0, drop_tol, f);
+        f.fwd = TriPlan();
+        build_plan(c, f.Lpat, f.diag.p, false, false, f.fwd);
+        plan_values(c, f.Lpat, f.diag.p, f.fwd);
+        Csr LT;
+        transpose(c, f.Lpat, LT);
+        build_plan(c, LT, f.diag.p, false, true, f.bwd);
+        return;
+    }
     int* flags = c->d_scalar_i + 24;   // [shifts, err]
     EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
     if (n && f.fwd.is_chain) {
-        chain_ic0(c, f.fwd.chain, f.Lpat, aii.p, sc.p, f.diag.p, flags);
+        chain_ic0(c, f.fwd.chain, f.Lpat, aii.p, sc.p, f.diag.p, flags, drop_tol);
     } else if (n) {
         LevelArgs la{f.fwd.perm.p, f.fwd.level_start.p, f.fwd.n_levels, reinterpret_cast<unsigned*>(f.fwd.sync.p)};
         Prof pr(c, "ic0_factor", 24.0 * f.Lpat.nnz + 32.0 * n);
@@ -450,21 +468,31 @@ void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f) {
         const double* sp = sc.p;
         double* dp = f.diag.p;
         int* sh = flags;
-        void* args[] = {&la, &Lp, &Li, &Lv, &ap, &sp, &dp, &sh};
+        double ft = drop_tol;
+        void* args[] = {&la, &Lp, &Li, &Lv, &ap, &sp, &dp, &sh, &ft};
         EDFA_CUDA(cudaLaunchCooperativeKernel((void*)k_ic0, dim3(grid), dim3(256), args, 0, c->stream));
     }
     int err = 0;
     read_flags(c, flags, &f.shifts, &err);
     require(err == 0, EDFA_ERR_CUDA, "IC(0) factorisation failed");
+    if (drop_tol > 0.0) {   // dropped entries (exact zeros: kept ones satisfy |w| >= tau > 0) leave the factor
+        drop_zeros(c, f.Lpat);
+        f.fwd = TriPlan();
+        build_plan(c, f.Lpat, f.diag.p, false, false, f.fwd);
+    }
     plan_values(c, f.Lpat, f.diag.p, f.fwd);
     Csr LT;
     transpose(c, f.Lpat, LT);
     build_plan(c, LT, f.diag.p, false, true, f.bwd);
 }
 
-void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int* dims) {
-    require(drop_tol == 0.0, EDFA_ERR_UNSUPPORTED,
-            "ILU with a drop tolerance (schur_drop_tol > 0) is not implemented on the GPU path; use 0 with no_fill");
+void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int* dims, bool no_fill) {
+    require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
+    if (drop_tol > 0.0 || !no_fill) {   // threshold ILU (ilut.cu), then the same solve plans
+        ilut_factor(c, S, drop_tol, no_fill, f);
+        ilu_plans(c, f, dims, false);
+        return;
+    }
     const int n = S.n_rows;
     f.n = n;
     copy_csr(c, S, f.LU);
@@ -577,6 +605,13 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
     int err = 0;
     read_flags(c, flags, &f.shifts, &err);
     require(err == 0, EDFA_ERR_CUDA, "ILU(0) factorisation failed");
+    ilu_plans(c, f, dims, !sync_free);
+}
+
+// triangular-solve plans of an ILU factor (f.LU strict parts + f.udiag);
+// have_fwd_levels: f.fwd already holds the level plan of L's pattern
+void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
+    const int n = f.n;
     Csr Lv, Uv;
     select_part(c, f.LU, 0, 1.0, true, Lv);
     select_part(c, f.LU, 1, 1.0, true, Uv);
@@ -594,7 +629,7 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         f.fwd.n_dep = Lv.nnz;
         f.fwd.n_levels = f.fwd.tile.n_tile_levels;
     } else {
-        if (sync_free) level_plan();
+        if (!have_fwd_levels) build_plan(c, Lv, nullptr, true, false, f.fwd, /*allow_chain=*/false);
         plan_values(c, Lv, nullptr, f.fwd);
     }
     if (dims && build_axial_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.axial)) {

@@ -1,0 +1,559 @@
+// Threshold incomplete factorisations with fill-in:
+// ilu_factorize / ic_factorize of hx/sparse.py:141-282 with fill_tol > 0
+// and/or no_fill=False -- the reference CLI's default inner solves
+// (face_drop_tol = schur_drop_tol = 1e-3, no_fill = False, hx/config.py:79-83).
+//
+// The working row of the reference (a dict plus a heap of pending lower
+// columns) becomes an open-addressing hash table in the warp's shared memory:
+//   * pivots are taken in increasing column order by a warp-wide min search
+//     over the table (the heap), popped entries become tombstones;
+//   * the drop test is applied to the unscaled working value, the multiplier
+//     is a_ik / u_kk, updates w_j <- w_j - l_ik u_kj run without FMA
+//     contraction, new fill enters as -(l_ik u_kj); with no_fill only entries
+//     already in the row are updated -- operation for operation the
+//     reference's arithmetic, so factors and drop decisions are bit-identical;
+//   * the U part keeps |v| >= tau, sorted; the pivot guard is the reference's
+//     sign-preserving 1e-12 ||row||_inf shift.
+// ILU(tau): sync-free -- warps take rows in natural order from a ticket and
+// wait only on their pivot rows' published pivots (a row's U part depends on
+// nothing else), so independent rows overlap as in the ILU(0) kernel.
+// IC(tau) with fill: row i needs column k of L restricted to rows < i for
+// every pivot k, and which rows hold column k is only known once they are
+// factored; the kernel therefore walks the rows in order on one warp and
+// appends every finished row to per-column lists (the reference's ``cols``).
+// Rows are written to padded per-row slots and compacted to CSR afterwards.
+#include <climits>
+
+#include "dev_util.cuh"
+#include "edfa_internal.cuh"
+#include "objects.cuh"
+
+namespace edfa {
+namespace {
+
+constexpr double PIVOT_GUARD = 1e-12;   // hx/sparse.py:24-25
+constexpr int HBITS = 10;
+constexpr int HSZ = 1 << HBITS;         // working-row hash slots per warp
+constexpr int HMAX = HSZ * 3 / 4;       // load limit -> EDFA_ERR_UNSUPPORTED
+constexpr int EMPTY = -1, TOMB = -2;
+constexpr int ERR_OVERFLOW = 1, ERR_SPIN = 2;
+
+struct Table {
+    int* keys;      // [HSZ]
+    double* vals;   // [HSZ]
+    int* ckey;      // [cap] compacted U candidates
+    double* cval;   // [cap]
+    int* misc;      // [4]: inserted count
+};
+
+__host__ __device__ constexpr size_t warp_bytes(int cap) {
+    return ((size_t)HSZ * 12 + (size_t)cap * 12 + 16 + 15) & ~size_t(15);
+}
+
+__device__ __forceinline__ Table table_at(unsigned char* base, int cap) {
+    Table t;
+    t.vals = reinterpret_cast<double*>(base);
+    t.cval = t.vals + HSZ;
+    t.keys = reinterpret_cast<int*>(t.cval + cap);
+    t.ckey = t.keys + HSZ;
+    t.misc = t.ckey + cap;
+    return t;
+}
+
+__device__ __forceinline__ unsigned hslot(int j) { return ((unsigned)j * 2654435761u) >> (32 - HBITS); }
+
+// slot of key j, or -1
+__device__ __forceinline__ int hfind(const Table& t, int j) {
+    unsigned s = hslot(j);
+    for (int p = 0; p < HSZ; ++p, s = (s + 1) & (HSZ - 1)) {
+        const int k = t.keys[s];
+        if (k == j) return (int)s;
+        if (k == EMPTY) return -1;
+    }
+    return -1;
+}
+
+// slot of key j, inserting it when absent (*fresh = true); -1 when full.
+// Keys inserted concurrently by the lanes of one warp are distinct.
+__device__ __forceinline__ int hinsert(const Table& t, int j, bool* fresh) {
+    unsigned s = hslot(j);
+    for (int p = 0; p < HSZ; ++p, s = (s + 1) & (HSZ - 1)) {
+        int k = t.keys[s];
+        if (k == j) { *fresh = false; return (int)s; }
+        if (k == EMPTY) {
+            k = atomicCAS(t.keys + s, EMPTY, j);
+            if (k == EMPTY) { *fresh = true; return (int)s; }
+            if (k == j) { *fresh = false; return (int)s; }
+        }
+    }
+    return -1;
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// next pivot: smallest live key in (last, lim); returns (key << 32 | slot) or ~0
+__device__ __forceinline__ unsigned long long next_pivot(const Table& t, int last, int lim, int lane) {
+    unsigned long long best = ~0ull;
+    for (int s = lane; s < HSZ; s += 32) {
+        const int k = t.keys[s];
+        if (k > last && k < lim) {
+            unsigned long long v = ((unsigned long long)(unsigned)k << 32) | (unsigned)s;
+            best = v < best ? v : best;
+        }
+    }
+    return warp_min_u64(best);
+}
+
+__device__ __forceinline__ void clear_table(const Table& t, int lane) {
+    for (int s = lane; s < HSZ; s += 32) t.keys[s] = EMPTY;
+    if (lane == 0) t.misc[0] = 0;
+    __syncwarp();
+}
+
+// Compact the row's live keys with key > i (and |v| >= tau) into ckey/cval and
+// write them sorted to out_col/out_val; returns the count (> cap: overflow).
+__device__ __forceinline__ int emit_sorted_upper(const Table& t, int i, double tau, int cap, int lane,
+                                                 int32_t* __restrict__ out_col, double* __restrict__ out_val) {
+    int m = 0;
+    for (int s0 = 0; s0 < HSZ; s0 += 32) {
+        const int s = s0 + lane;
+        const int k = t.keys[s];
+        const bool take = k > i && !(fabs(t.vals[s]) < tau);
+        const unsigned b = __ballot_sync(0xffffffffu, take);
+        const int pos = m + __popc(b & ((1u << lane) - 1));
+        if (take && pos < cap) {
+            t.ckey[pos] = k;
+            t.cval[pos] = t.vals[s];
+        }
+        m += __popc(b);
+    }
+    __syncwarp();
+    if (m > cap) return m;
+    for (int a = lane; a < m; a += 32) {
+        const int k = t.ckey[a];
+        int r = 0;
+        for (int b = 0; b < m; ++b) r += t.ckey[b] < k;
+        out_col[r] = k;
+        out_val[r] = t.cval[a];
+    }
+    return m;
+}
+
+// ILU(tau): one warp per row, rows from a ticket in natural order.
+template <bool NO_FILL>
+__global__ void __launch_bounds__(128) k_ilut(int n, int* ticket, CsrV S, const double* __restrict__ scale,
+                                              double fill_tol, int cap, int* __restrict__ Lcnt,
+                                              int32_t* __restrict__ Lcol, double* __restrict__ Lval,
+                                              int* __restrict__ Ucnt, int32_t* __restrict__ Ucol,
+                                              double* __restrict__ Uval, double* __restrict__ udiag, int* shifts,
+                                              int* err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Table t = table_at(smem + (size_t)wid * warp_bytes(cap), cap);
+    for (;;) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(ticket, 1);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= n) break;
+        clear_table(t, lane);
+        const int lo = S.ptr[i], hi = S.ptr[i + 1];
+        const double norm = scale[i];
+        const double tau = fill_tol * norm;
+        bool bad = hi - lo > HMAX;
+        if (!bad) {
+            for (int e = lo + lane; e < hi; e += 32) {
+                bool fresh;
+                const int s = hinsert(t, S.idx[e], &fresh);
+                t.vals[s] = S.val[e];
+            }
+            if (lane == 0) t.misc[0] = hi - lo;
+        }
+        __syncwarp();
+        const int64_t o = (int64_t)i * cap;
+        int nl = 0, last = -1;
+        while (!bad) {
+            const unsigned long long best = next_pivot(t, last, i, lane);
+            if (best == ~0ull) break;
+            const int k = (int)(best >> 32), s = (int)(best & 0xffffffffu);
+            const double a = t.vals[s];
+            __syncwarp();
+            if (lane == 0) t.keys[s] = TOMB;   // row.pop(k)
+            last = k;
+            if (fabs(a) < tau) {               // dropped: no multiplier, no update
+                __syncwarp();
+                continue;
+            }
+            double d = 0.0;
+            if (lane == 0) {
+                d = ld_relaxed(udiag + k);
+                long long spins = 0;
+                while (is_sentinel(d)) {
+                    if (++spins > SPIN_LIMIT) { atomicExch(err, ERR_SPIN); d = 1.0; break; }
+                    __nanosleep(32);
+                    d = ld_relaxed(udiag + k);
+                }
+            }
+            d = __shfl_sync(0xffffffffu, d, 0);
+            __threadfence();                   // pivot row k's U part is read after its pivot was seen
+            const double lik = __ddiv_rn(a, d);
+            const int cu = __ldcg(Ucnt + k);
+            const int64_t ok = (int64_t)k * cap;
+            int added = 0;
+            for (int q = lane; q < cu; q += 32) {
+                const int j = __ldcg(Ucol + ok + q);
+                const double u = __ldcg(Uval + ok + q);
+                if (NO_FILL) {
+                    const int sj = hfind(t, j);
+                    if (sj >= 0) t.vals[sj] = sub_mul(t.vals[sj], lik, u);
+                } else {
+                    bool fresh = false;
+                    const int sj = hinsert(t, j, &fresh);
+                    if (sj < 0) { bad = true; continue; }
+                    if (fresh) {
+                        t.vals[sj] = -__dmul_rn(lik, u);
+                        ++added;
+                    } else {
+                        t.vals[sj] = sub_mul(t.vals[sj], lik, u);
+                    }
+                }
+            }
+            added = warp_sum(added);
+            bad = __any_sync(0xffffffffu, bad);
+            if (lane == 0) {
+                if (nl < cap) {
+                    Lcol[o + nl] = k;
+                    Lval[o + nl] = lik;
+                }
+                t.misc[0] += added;
+            }
+            ++nl;
+            __syncwarp();
+            if (nl > cap || t.misc[0] > HMAX) bad = true;
+        }
+        double piv = 0.0;
+        int nu = 0;
+        if (!bad) {
+            const int sd = hfind(t, i);          // row.pop(i, 0.0)
+            piv = sd >= 0 ? t.vals[sd] : 0.0;
+            const double g = PIVOT_GUARD * norm;
+            if (fabs(piv) < g) {
+                piv = piv >= 0.0 ? g : -g;
+                if (lane == 0) atomicAdd(shifts, 1);
+            }
+            nu = emit_sorted_upper(t, i, tau, cap, lane, Ucol + o, Uval + o);
+            if (nu > cap) bad = true;
+        }
+        if (bad) {
+            if (lane == 0) atomicExch(err, ERR_OVERFLOW);
+            nl = nu = 0;
+            piv = 1.0;                           // unblock dependants; the factor is discarded
+        }
+        if (lane == 0) {
+            Lcnt[i] = nl;
+            Ucnt[i] = nu;
+        }
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_relaxed(udiag + i, publishable(piv));
+    }
+}
+
+// IC(tau) with fill of sign*A, rows in order on one warp; finished rows are
+// appended to per-column lists (row, L_ik) -- hx/sparse.py:217-282.
+__global__ void __launch_bounds__(32) k_ict(int n, CsrV A, double sign, const double* __restrict__ scale,
+                                            double fill_tol, int cap, int capc, int* __restrict__ Lcnt,
+                                            int32_t* __restrict__ Lcol, double* __restrict__ Lval,
+                                            double* __restrict__ diag, int* __restrict__ Ccnt,
+                                            int32_t* __restrict__ Crow, double* __restrict__ Cval, int* shifts,
+                                            int* err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const Table t = table_at(smem, cap);
+    int nshift = 0;
+    for (int i = 0; i < n; ++i) {
+        clear_table(t, lane);
+        const int lo = A.ptr[i], hi = A.ptr[i + 1];
+        const double norm = scale[i];
+        const double tau = fill_tol * norm;
+        bool bad = hi - lo > HMAX;
+        double dii = 0.0;                       // row.get(i, 0.0)
+        if (!bad) {
+            for (int e = lo + lane; e < hi; e += 32) {
+                const int j = A.idx[e];
+                if (j < i) {
+                    bool fresh;
+                    const int s = hinsert(t, j, &fresh);
+                    t.vals[s] = sign * A.val[e];
+                } else if (j == i) {
+                    dii = sign * A.val[e];
+                }
+            }
+            dii = warp_sum(dii);                 // at most one lane holds the diagonal
+            if (lane == 0) t.misc[0] = hi - lo;
+        }
+        __syncwarp();
+        const int64_t o = (int64_t)i * cap;
+        int nl = 0, last = -1;
+        while (!bad) {
+            const unsigned long long best = next_pivot(t, last, i, lane);
+            if (best == ~0ull) break;
+            const int k = (int)(best >> 32), s = (int)(best & 0xffffffffu);
+            const double w = t.vals[s];
+            __syncwarp();
+            if (lane == 0) t.keys[s] = TOMB;
+            last = k;
+            if (fabs(w) < tau) {
+                __syncwarp();
+                continue;
+            }
+            const double lik = __ddiv_rn(w, diag[k]);   // diagonal of row k is stored last
+            const int cc = Ccnt[k];
+            const int64_t ok = (int64_t)k * capc;
+            int added = 0;
+            for (int q = lane; q < cc && q < capc; q += 32) {
+                const int j = Crow[ok + q];
+                if (j <= k || j >= i) continue;
+                const double ljk = Cval[ok + q];
+                bool fresh = false;
+                const int sj = hinsert(t, j, &fresh);
+                if (sj < 0) { bad = true; continue; }
+                if (fresh) {
+                    t.vals[sj] = -__dmul_rn(lik, ljk);
+                    ++added;
+                } else {
+                    t.vals[sj] = sub_mul(t.vals[sj], lik, ljk);
+                }
+            }
+            added = warp_sum(added);
+            bad = __any_sync(0xffffffffu, bad);
+            dii = sub_mul(dii, lik, lik);
+            if (lane == 0) {
+                if (nl < cap) {
+                    Lcol[o + nl] = k;
+                    Lval[o + nl] = lik;
+                }
+                t.misc[0] += added;
+            }
+            ++nl;
+            __syncwarp();
+            if (nl > cap || t.misc[0] > HMAX) bad = true;
+        }
+        double d = dii;
+        if (bad) {
+            if (lane == 0) atomicExch(err, ERR_OVERFLOW);
+            nl = 0;
+            d = 1.0;
+        } else if (d < PIVOT_GUARD * norm) {
+            d = PIVOT_GUARD * norm;
+            ++nshift;
+        }
+        // the row's entries join their columns' lists (cols[j].append((i, v)))
+        __syncwarp();
+        if (lane == 0) {
+            for (int q = 0; q < nl; ++q) {
+                const int k = Lcol[o + q];
+                const int pos = Ccnt[k];
+                if (pos < capc) {
+                    Crow[(int64_t)k * capc + pos] = i;
+                    Cval[(int64_t)k * capc + pos] = Lval[o + q];
+                } else {
+                    atomicExch(err, ERR_OVERFLOW);
+                }
+                Ccnt[k] = pos + 1;
+            }
+            Lcnt[i] = nl;
+            diag[i] = __dsqrt_rn(d);
+        }
+        __syncwarp();
+    }
+    if (lane == 0 && nshift) atomicAdd(shifts, nshift);
+}
+
+// padded rows -> CSR (row = [first part | second part], both already sorted)
+template <bool FILL>
+__global__ void k_pad_to_csr(int n, int cap, const int* __restrict__ c1, const int32_t* __restrict__ col1,
+                             const double* __restrict__ val1, const int* __restrict__ c2,
+                             const int32_t* __restrict__ col2, const double* __restrict__ val2,
+                             int32_t* __restrict__ cnt, const int32_t* __restrict__ ptr, int32_t* __restrict__ idx,
+                             double* __restrict__ val) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int a = c1[i], b = c2 ? c2[i] : 0;
+    if (!FILL) {
+        cnt[i] = a + b;
+        return;
+    }
+    const int64_t o = (int64_t)i * cap;
+    int p = ptr[i];
+    for (int q = 0; q < a; ++q, ++p) {
+        idx[p] = col1[o + q];
+        val[p] = val1[o + q];
+    }
+    for (int q = 0; q < b; ++q, ++p) {
+        idx[p] = col2[o + q];
+        val[p] = val2[o + q];
+    }
+}
+
+__global__ void k_row_scale(CsrV A, double* __restrict__ sc) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n_rows) return;
+    double mx = 0.0;
+    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) mx = fmax(mx, fabs(A.val[e]));
+    sc[i] = A.ptr[i + 1] > A.ptr[i] ? mx : 1.0;
+}
+
+void pad_to_csr(Ctx* c, int n, int n_cols, int cap, const int* c1, const int32_t* col1, const double* val1,
+                const int* c2, const int32_t* col2, const double* val2, Csr& out) {
+    out.n_rows = n;
+    out.n_cols = n_cols;
+    out.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    if (n) {
+        k_pad_to_csr<false><<<ceil_div(n, 256), 256, 0, c->stream>>>(n, cap, c1, col1, val1, c2, col2, val2, cnt.p,
+                                                                    nullptr, nullptr, nullptr);
+        check_launch("k_pad_to_csr");
+    }
+    out.nnz = scan_counts(c, cnt.p, out.ptr.p, n);
+    out.idx.reset(c, out.nnz);
+    out.val.reset(c, out.nnz);
+    if (n) {
+        Prof pr(c, "ilut_compact", 24.0 * out.nnz);
+        k_pad_to_csr<true><<<ceil_div(n, 256), 256, 0, c->stream>>>(n, cap, c1, col1, val1, c2, col2, val2, nullptr,
+                                                                   out.ptr.p, out.idx.p, out.val.p);
+        check_launch("k_pad_to_csr");
+    }
+}
+
+template <bool FILL>
+__global__ void k_nonzero(CsrV A, int32_t* __restrict__ cnt, const int32_t* __restrict__ ptr,
+                          int32_t* __restrict__ idx, double* __restrict__ val) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= A.n_rows) return;
+    int o = FILL ? ptr[i] : 0, m = 0;
+    for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
+        if (A.val[e] == 0.0) continue;
+        if (FILL) {
+            idx[o + m] = A.idx[e];
+            val[o + m] = A.val[e];
+        }
+        ++m;
+    }
+    if (!FILL) cnt[i] = m;
+}
+
+int row_cap(Ctx* c, const Csr& A, double fill_tol, bool no_fill) {
+    // output slots per row: the longest input row with room for fill, capped
+    // by what the working table can hold; complete factorisations (no drop
+    // tolerance) of small matrices get whole rows
+    const int maxr = A.n_rows ? max_row_nnz(c, A) : 0;
+    int cap = 64;
+    while (cap < 4 * maxr && cap < 512) cap *= 2;
+    if (!no_fill && fill_tol == 0.0) cap = std::max(cap, std::min(A.n_rows, 512));
+    return cap;
+}
+
+}  // namespace
+
+void drop_zeros(Ctx* c, Csr& A) {
+    const int n = A.n_rows;
+    Csr out;
+    out.n_rows = n;
+    out.n_cols = A.n_cols;
+    out.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    if (n) {
+        k_nonzero<false><<<ceil_div(n, 256), 256, 0, c->stream>>>(view(A), cnt.p, nullptr, nullptr, nullptr);
+        check_launch("k_nonzero");
+    }
+    out.nnz = scan_counts(c, cnt.p, out.ptr.p, n);
+    out.idx.reset(c, out.nnz);
+    out.val.reset(c, out.nnz);
+    if (n) {
+        k_nonzero<true><<<ceil_div(n, 256), 256, 0, c->stream>>>(view(A), nullptr, out.ptr.p, out.idx.p, out.val.p);
+        check_launch("k_nonzero");
+    }
+    A = std::move(out);
+}
+
+void ilut_factor(Ctx* c, const Csr& S, double fill_tol, bool no_fill, IluFactor& f) {
+    const int n = S.n_rows;
+    f.n = n;
+    const int cap = row_cap(c, S, fill_tol, no_fill);
+    DevBuf<double> sc(c, std::max(n, 1));
+    DevBuf<int> lc(c, std::max(n, 1)), uc(c, std::max(n, 1));
+    DevBuf<int32_t> lcol(c, (size_t)std::max(n, 1) * cap), ucol(c, (size_t)std::max(n, 1) * cap);
+    DevBuf<double> lval(c, (size_t)std::max(n, 1) * cap), uval(c, (size_t)std::max(n, 1) * cap);
+    f.udiag.reset(c, std::max(n, 1));
+    f.has_diag.reset(c, std::max(n, 1));
+    int* flags = c->d_scalar_i + 24;   // [shifts, err]
+    EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+    if (n) {
+        k_row_scale<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(S), sc.p);
+        check_launch("k_row_scale");
+        fill_bits(c, f.udiag.p, n, SENTINEL_BITS);
+        int* tk = c->d_scalar_i + 29;
+        EDFA_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), c->stream));
+        const int threads = 128;
+        const size_t smem = warp_bytes(cap) * (threads / 32);
+        auto kern = no_fill ? k_ilut<true> : k_ilut<false>;
+        EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int occ = 0;
+        EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+        const int grid = NUM_SMS_B200 * std::max(1, occ);
+        Prof pr(c, "ilut_factor", 24.0 * S.nnz + 24.0 * n);
+        kern<<<grid, threads, smem, c->stream>>>(n, tk, view(S), sc.p, fill_tol, cap, lc.p, lcol.p, lval.p, uc.p,
+                                                 ucol.p, uval.p, f.udiag.p, flags, flags + 1);
+        check_launch("k_ilut");
+    }
+    int h[2];
+    EDFA_CUDA(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    f.shifts = h[0];
+    require(h[1] != ERR_SPIN, EDFA_ERR_CUDA, "ILU(tau) factorisation stalled");
+    require(h[1] == 0, EDFA_ERR_UNSUPPORTED,
+            "ILU(tau) fill exceeds " + std::to_string(cap) + " entries per factor row (use a larger drop tolerance)");
+    pad_to_csr(c, n, n, cap, lc.p, lcol.p, lval.p, uc.p, ucol.p, uval.p, f.LU);
+    if (n) EDFA_CUDA(cudaMemsetAsync(f.has_diag.p, 0, sizeof(int32_t) * n, c->stream));
+}
+
+void ict_factor(Ctx* c, const Csr& A, double sign, double fill_tol, IcFactor& f) {
+    const int n = A.n_rows;
+    f.n = n;
+    const int cap = row_cap(c, A, fill_tol, false);
+    const int capc = std::max(2 * cap, fill_tol == 0.0 ? std::min(n, 512) : 0);
+    DevBuf<double> sc(c, std::max(n, 1));
+    DevBuf<int> lc(c, std::max(n, 1)), cc(c, std::max(n, 1));
+    DevBuf<int32_t> lcol(c, (size_t)std::max(n, 1) * cap), crow(c, (size_t)std::max(n, 1) * capc);
+    DevBuf<double> lval(c, (size_t)std::max(n, 1) * cap), cval(c, (size_t)std::max(n, 1) * capc);
+    f.diag.reset(c, std::max(n, 1));
+    int* flags = c->d_scalar_i + 24;
+    EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+    if (n) {
+        EDFA_CUDA(cudaMemsetAsync(cc.p, 0, sizeof(int) * n, c->stream));
+        k_row_scale<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(A), sc.p);
+        check_launch("k_row_scale");
+        const size_t smem = warp_bytes(cap);
+        EDFA_CUDA(cudaFuncSetAttribute(k_ict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        Prof pr(c, "ict_factor", 12.0 * A.nnz + 16.0 * n);
+        k_ict<<<1, 32, smem, c->stream>>>(n, view(A), sign, sc.p, fill_tol, cap, capc, lc.p, lcol.p, lval.p, f.diag.p,
+                                          cc.p, crow.p, cval.p, flags, flags + 1);
+        check_launch("k_ict");
+    }
+    int h[2];
+    EDFA_CUDA(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    f.shifts = h[0];
+    require(h[1] == 0, EDFA_ERR_UNSUPPORTED,
+            "IC(tau) fill exceeds " + std::to_string(cap) + " entries per factor row (use a larger drop tolerance)");
+    pad_to_csr(c, n, n, cap, lc.p, lcol.p, lval.p, nullptr, nullptr, nullptr, f.Lpat);
+}
+
+}  // namespace edfa

@@ -60,9 +60,6 @@ void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynam
     require(filt >= EDFA_FILT_NONE && filt <= EDFA_FILT_POST_PRODUCT, EDFA_ERR_VALUE,
             "filtration must be one of ('none', 'pre', 'post-schur', 'post-product')");
     require(face_drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
-    require(no_fill, EDFA_ERR_UNSUPPORTED,
-            "inner factorisations with fill-in (no_fill=False) are not implemented on the GPU path; "
-            "pass no_fill=True for IC(0)/ILU(0)");
     const Csr& Aff = *sys->A_ff;
     const int nf = Aff.n_rows, nc = sys->A_cf->n_rows;
     if (pattern) {
@@ -110,7 +107,7 @@ void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynam
         triple_product(c, s1->G, Aff, s1->F, filt == EDFA_FILT_POST_PRODUCT ? tau : 0.0, s1->H);
     }
     PhaseTimer pt(c, "stage1.ic0");
-    ic0_factor(c, Aff, face_drop_tol, s1->ic);
+    ic0_factor(c, Aff, face_drop_tol, s1->ic, no_fill != 0);
 }
 
 void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, int filt, double schur_drop_tol,
@@ -118,9 +115,6 @@ void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, in
     require(filt >= EDFA_FILT_NONE && filt <= EDFA_FILT_POST_PRODUCT, EDFA_ERR_VALUE,
             "filtration must be one of ('none', 'pre', 'post-schur', 'post-product')");
     require(schur_drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
-    require(no_fill, EDFA_ERR_UNSUPPORTED,
-            "inner factorisations with fill-in (no_fill=False) are not implemented on the GPU path; "
-            "pass no_fill=True for IC(0)/ILU(0)");
     {
         PhaseTimer pt(c, "stage2.schur_sub");
         csr_sub(c, A_cc, s1->H, filt == EDFA_FILT_POST_SCHUR ? tau : 0.0, s2->S);
@@ -128,7 +122,7 @@ void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, in
     PhaseTimer pt(c, "stage2.ilu0_total");
     const int* dims = (int64_t)s1->dims[0] * s1->dims[1] * s1->dims[2] == A_cc.n_rows && s1->dims[0] > 0
                           ? s1->dims : nullptr;
-    ilu0_factor(c, s2->S, schur_drop_tol, s2->ilu, dims);
+    ilu0_factor(c, s2->S, schur_drop_tol, s2->ilu, dims, no_fill != 0);
 }
 
 }  // namespace edfa

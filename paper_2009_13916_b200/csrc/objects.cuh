@@ -63,7 +63,7 @@ void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, doubl
 bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add,
                     double* out2, const char* name, const Csr* fz = nullptr, const double* fz_x = nullptr);
 void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,
-               int* shifts);
+               int* shifts, double fill_tol = 0.0);
 
 struct TilePlan {               // tile-DAG solves of cell-indexed factors (tile.cu)
     int32_t n = 0, n_tiles = 0, n_tile_levels = 0;
@@ -157,8 +157,14 @@ struct IluFactor {              // ILU of S (no fill)
     TriPlan fwd, bwd;
     Csr export_L, export_U;
 };
-void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f);
-void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int* dims);
+// IC of -A_ff / ILU of S with the reference's drop tolerance; no_fill = False
+// admits fill-in (threshold factorisations, ilut.cu)
+void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f, bool no_fill = true);
+void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int* dims, bool no_fill = true);
+// threshold kernels (ilut.cu): f.LU / f.Lpat compact, pivots, shifts
+void ilut_factor(Ctx* c, const Csr& S, double fill_tol, bool no_fill, IluFactor& f);
+void ict_factor(Ctx* c, const Csr& A, double sign, double fill_tol, IcFactor& f);
+void drop_zeros(Ctx* c, Csr& A);
 void ic_export(Ctx* c, IcFactor& f);
 void ilu_export(Ctx* c, IluFactor& f);
 
@@ -230,4 +236,9 @@ void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double*
 void dcgs2_dots_entry(Ctx* c, int64_t n, int j, const double* V, int64_t ldv, double* dots_out);
 void dcgs2_coeffs_entry(Ctx* c, int j, int m, const double* dots, double* H, double* h1, double* coef, double* hcol);
 void dcgs2_update_entry(Ctx* c, int64_t n, int j, double* V, int64_t ldv, const double* coef);
+// RT0 MHFE / FV assembly (assembly.cu)
+void assemble(Ctx* c, const edfa_hex_grid& g, const edfa_assembly_in& in, edfa_assembly_out& out, Csr& A_ff,
+              Csr& A_fc, Csr& A_cf, Csr& A_cc);
+void update_accumulation(Ctx* c, const Csr& A_cc_steady, const double* acc, const double* rhs_c_base,
+                         const double* p_prev, double dt, Csr& A_cc, double* rhs_c);
 }  // namespace edfa

@@ -75,3 +75,30 @@ def test_csr_info_rejects_null():
     n = ctypes.c_int32()
     st = lib.edfa_csr_info(None, ctypes.byref(n), ctypes.byref(n), None)
     assert st == _lib.ERR_VALUE
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """ctypes mirrors of the header's structs have the C sizes and offsets."""
+    import shutil
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc unavailable")
+    structs = {"edfa_hex_grid": _lib.HexGridDesc, "edfa_assembly_in": _lib.AssemblyIn,
+               "edfa_assembly_out": _lib.AssemblyOut, "edfa_report": _lib.Report,
+               "edfa_stage1_info": _lib.Stage1Info, "edfa_stage2_info": _lib.Stage2Info,
+               "edfa_dynamic": _lib.Dynamic}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void) {"]
+    for cname, cls in structs.items():
+        lines.append(f'printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
+    got = dict(line.rsplit(" ", 1) for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                                check=True).stdout.splitlines())
+    for cname, cls in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for fname, _ in cls._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(cls, fname).offset, f"{cname}.{fname}"

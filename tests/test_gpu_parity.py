@@ -381,14 +381,6 @@ def test_generic_callables_path(edfa):
     assert rep2.converged and np.linalg.norm(b - A @ x2) <= 1e-8 * np.linalg.norm(b) * 1.0001
 
 
-def test_fill_modes_are_reported_unsupported(edfa):
-    from paper_2009_13916_b200._lib import EdfaUnsupported
-    d = golden("small_wells")
-    s = GoldenSystem(d)
-    with pytest.raises(EdfaUnsupported):
-        edfa.BlockLDUPreconditioner.build(s, patterns=_PS(g_sets(d, "base_fill_Q")))
-
-
 @pytest.mark.parametrize("idx,n", [(1, 12), (2, 10), (2, 16)])
 def test_tile_solver_matches_level_solver(edfa, idx, n):
     """The tile-DAG Schur solves (grid hint) and the level-synchronous solves
