@@ -57,14 +57,32 @@ def make_case(args):
     return configs.make(args.config, n=args.n or DEFAULT_N[args.config])
 
 
+INNER = {}   # --drop-tol / --fill override the config's inner-solve options
+
+
+def inner_opts(case):
+    p = case.precond
+    o = dict(face_drop_tol=p.get("face_drop_tol", 0.0), schur_drop_tol=p.get("schur_drop_tol", 0.0),
+             no_fill=p.get("no_fill", True))
+    o.update(INNER)
+    return o
+
+
 def build_pre(case, ds):
     """Preconditioner of a BASELINE config through the drop-in API."""
     from paper_2009_13916_b200.precond import BlockLDUPreconditioner, DynamicConfig, patterns_for
     p = case.precond
     if p["pattern"] == "dynamic":
-        return BlockLDUPreconditioner.build(ds, dynamic=DynamicConfig(p["n_add"], p["n_ent"]), no_fill=True)
+        return BlockLDUPreconditioner.build(ds, dynamic=DynamicConfig(p["n_add"], p["n_ent"]), **inner_opts(case))
     pats = patterns_for(ds, p["pattern"], p.get("prototype", "A"))
-    return BlockLDUPreconditioner.build(ds, patterns=pats, no_fill=True)
+    return BlockLDUPreconditioner.build(ds, patterns=pats, **inner_opts(case))
+
+
+def inner_tag(case):
+    o = inner_opts(case)
+    if o["no_fill"] and not o["face_drop_tol"] and not o["schur_drop_tol"]:
+        return "IC0ILU0"
+    return f"ICILU(tau={o['face_drop_tol']:g},{'nofill' if o['no_fill'] else 'fill'})"
 
 
 def parse():
@@ -77,6 +95,9 @@ def parse():
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
                     help="BASELINE config (2 = the headline workload; others for evidence runs)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--drop-tol", type=float, default=0.0,
+                    help="face_drop_tol = schur_drop_tol (evidence runs of the threshold inner solves)")
+    ap.add_argument("--fill", action="store_true", help="no_fill=False (threshold factorisations with fill)")
     ap.add_argument("--profile-json", default=None, help="write the per-kernel event profile here")
     ap.add_argument("--slabs", type=int, default=0,
                     help="z-slab partitioned solver with this many slabs per process (default: 1 slab per "
@@ -389,8 +410,8 @@ def run_edfa(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": ("synthetic (seeded config-2 generator: 64^3, lnK~N(0,2), kz/kx=0.1)" if args.config == 2
                  else f"synthetic (seeded generator of BASELINE config {args.config}: {case.name})"),
-        "config": {"workload": (f"config2-{args.n}^3-staticA-IC0ILU0-gmres50" if args.config == 2
-                                else f"{case.name}-IC0ILU0-gmres50"), "n_dof": N,
+        "config": {"workload": (f"config2-{args.n}^3-staticA-{inner_tag(case)}-gmres50" if args.config == 2
+                                else f"{case.name}-{inner_tag(case)}-gmres50"), "n_dof": N,
                    "n_free_faces": s.n_free_faces, "n_cells": s.n_cells, "rtol": case.rtol,
                    "restart": case.restart, "gmres_iterations": reps[-1].n_it,
                    "final_true_relres": reps[-1].final_relres, "host_check_relres": relres_host,
@@ -638,6 +659,8 @@ def run_slabs(args):
 
 def main():
     args = parse()
+    if args.drop_tol > 0 or args.fill:
+        INNER.update(face_drop_tol=args.drop_tol, schur_drop_tol=args.drop_tol, no_fill=not args.fill)
     _, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)

@@ -245,6 +245,13 @@ int edfa_factor_ic0(edfa_ctx* ctx, const edfa_csr* A, double drop_tol, edfa_fact
  * = n_rows enables the tile-DAG solves (cells in natural order), else 0s. */
 int edfa_factor_ilu0(edfa_ctx* ctx, const edfa_csr* S, double drop_tol, int32_t nx, int32_t ny,
                      int32_t nz, edfa_factor** out);
+/* General forms: ic_factorize(-A, drop_tol, no_fill) / ilu_factorize(S,
+ * drop_tol, no_fill) (hx/sparse.py:141-282) -- no_fill = 0 admits fill-in
+ * (threshold factorisations); rows outgrowing the working table ->
+ * EDFA_ERR_UNSUPPORTED. */
+int edfa_factor_ic(edfa_ctx* ctx, const edfa_csr* A, double drop_tol, int no_fill, edfa_factor** out);
+int edfa_factor_ilu(edfa_ctx* ctx, const edfa_csr* S, double drop_tol, int no_fill, int32_t nx, int32_t ny,
+                    int32_t nz, edfa_factor** out);
 /* InnerFactorization.nnz_stored (hx/sparse.py:118-123), pivot shifts, levels. */
 int edfa_factor_info(const edfa_factor* f, int64_t* nnz_stored, int32_t* pivot_shifts,
                      int32_t* levels_fwd, int32_t* levels_bwd);

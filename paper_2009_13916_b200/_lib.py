@@ -109,6 +109,8 @@ _SIGS = {
     "edfa_csr_sub": (i32, [vp, vp, vp, f64, C.POINTER(vp)]),
     "edfa_factor_ic0": (i32, [vp, vp, f64, C.POINTER(vp)]),
     "edfa_factor_ilu0": (i32, [vp, vp, f64, i32, i32, i32, C.POINTER(vp)]),
+    "edfa_factor_ic": (i32, [vp, vp, f64, i32, C.POINTER(vp)]),
+    "edfa_factor_ilu": (i32, [vp, vp, f64, i32, i32, i32, i32, C.POINTER(vp)]),
     "edfa_factor_info": (i32, [vp, C.POINTER(i64), P_i32, P_i32, P_i32]),
     "edfa_factor_part": (i32, [vp, vp, i32, C.POINTER(vp)]),
     "edfa_factor_solve": (i32, [vp, vp, vp, f64, vp]),

@@ -523,6 +523,47 @@ int edfa_factor_ilu0(edfa_ctx* ctx, const edfa_csr* S, double drop_tol, int32_t 
     API_END
 }
 
+int edfa_factor_ic(edfa_ctx* ctx, const edfa_csr* A, double drop_tol, int no_fill, edfa_factor** out) {
+    API_BEGIN
+    require(ctx && out, EDFA_ERR_VALUE, "NULL argument");
+    require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
+    const Csr& a = M(A);
+    require(a.n_rows == a.n_cols, EDFA_ERR_VALUE, "IC needs a square matrix");
+    auto* f = new edfa_factor();
+    f->ctx = &ctx->c;
+    f->kind = 0;
+    try {
+        ic0_factor(&ctx->c, a, drop_tol, f->ic, no_fill != 0);
+    } catch (...) {
+        delete f;
+        throw;
+    }
+    *out = f;
+    API_END
+}
+
+int edfa_factor_ilu(edfa_ctx* ctx, const edfa_csr* S, double drop_tol, int no_fill, int32_t nx, int32_t ny,
+                    int32_t nz, edfa_factor** out) {
+    API_BEGIN
+    require(ctx && out, EDFA_ERR_VALUE, "NULL argument");
+    require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
+    const Csr& s = M(S);
+    require(s.n_rows == s.n_cols, EDFA_ERR_VALUE, "ILU needs a square matrix");
+    int dims[3] = {nx, ny, nz};
+    const bool grid = nx > 0 && ny > 0 && nz > 0 && (int64_t)nx * ny * nz == s.n_rows;
+    auto* f = new edfa_factor();
+    f->ctx = &ctx->c;
+    f->kind = 1;
+    try {
+        ilu0_factor(&ctx->c, s, drop_tol, f->ilu, grid ? dims : nullptr, no_fill != 0);
+    } catch (...) {
+        delete f;
+        throw;
+    }
+    *out = f;
+    API_END
+}
+
 int edfa_factor_info(const edfa_factor* f, int64_t* nnz_stored, int32_t* pivot_shifts, int32_t* levels_fwd,
                      int32_t* levels_bwd) {
     API_BEGIN

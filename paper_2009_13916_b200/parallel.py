@@ -386,16 +386,15 @@ class CudaSlab:
         h = C.c_void_p()
         L.check(lib.edfa_csr_sub(c, self.A_cc_own.handle, H_own.handle, tau, C.byref(h)))
         self.S_own = DeviceCsr(h)
-        if not o["no_fill"]:
-            raise L.EdfaUnsupported("inner factorisations with fill-in are not implemented on the GPU path")
         nx, ny, _ = lay.nxyz
         self._free_factors()
+        nf = int(bool(o["no_fill"]))
         f = C.c_void_p()
-        L.check(lib.edfa_factor_ilu0(c, self.S_own.handle, o["schur_drop_tol"], nx, ny, lay.k1 - lay.k0,
-                                     C.byref(f)))
+        L.check(lib.edfa_factor_ilu(c, self.S_own.handle, o["schur_drop_tol"], nf, nx, ny, lay.k1 - lay.k0,
+                                    C.byref(f)))
         self.ilu = f
         f = C.c_void_p()
-        L.check(lib.edfa_factor_ic0(c, self.A_ff_own.handle, o["face_drop_tol"], C.byref(f)))
+        L.check(lib.edfa_factor_ic(c, self.A_ff_own.handle, o["face_drop_tol"], nf, C.byref(f)))
         self.ic = f
 
     def _free_factors(self):

@@ -131,7 +131,21 @@ def test_gmres_with_threshold_inner_solves(edfa, idx, n, kind):
 def test_threshold_overflow_is_reported(edfa):
     """A complete factorisation whose rows outgrow the working table fails
     loudly (EdfaUnsupported), never silently approximates."""
-    from paper_2009_13916_b200._lib import EdfaUnsupported
-    s = _case(3, 9).system
-    with pytest.raises(EdfaUnsupported):
-        _build(edfa, s, "static", face_drop_tol=0.0, schur_drop_tol=0.0, no_fill=False)
+    import ctypes as C
+
+    import scipy.sparse as sp
+
+    from paper_2009_13916_b200 import _lib as L
+    from paper_2009_13916_b200.device import DeviceCsr, ctx
+    n = 600
+    rng = np.random.default_rng(0)
+    M = rng.standard_normal((n, n)) + n * np.eye(n)      # dense: row n-1 has n-1 multipliers
+    A = DeviceCsr.from_scipy(sp.csr_matrix(M))
+    f = C.c_void_p()
+    with pytest.raises(L.EdfaUnsupported):
+        L.check(L.lib().edfa_factor_ilu(ctx(), A.handle, 0.0, 0, 0, 0, 0, C.byref(f)))
+    # the same matrix with a drop tolerance that keeps rows short factorises
+    B = sp.csr_matrix(np.where(np.abs(M) > 2.5, M, 0.0))
+    Bd = DeviceCsr.from_scipy(B)
+    L.check(L.lib().edfa_factor_ilu(ctx(), Bd.handle, 0.5, 0, 0, 0, 0, C.byref(f)))
+    L.lib().edfa_factor_destroy(f)
