@@ -456,7 +456,7 @@ int row_cap(Ctx* c, const Csr& A, double fill_tol, bool no_fill) {
     const int maxr = A.n_rows ? max_row_nnz(c, A) : 0;
     int cap = 64;
     while (cap < 4 * maxr && cap < 512) cap *= 2;
-    if (!no_fill && fill_tol == 0.0) cap = std::max(cap, std::min(A.n_rows, 512));
+    if (!no_fill) cap = std::max(cap, std::min(A.n_rows, 512));   // fill: whole table's worth
     return cap;
 }
 
