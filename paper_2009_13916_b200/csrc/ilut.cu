@@ -22,6 +22,8 @@
 // factored; the kernel therefore walks the rows in order on one warp and
 // appends every finished row to per-column lists (the reference's ``cols``).
 // Rows are written to padded per-row slots and compacted to CSR afterwards.
+#include <cub/cub.cuh>
+
 #include <climits>
 
 #include "dev_util.cuh"
@@ -146,45 +148,105 @@ __device__ __forceinline__ int emit_sorted_upper(const Table& t, int i, double t
     return m;
 }
 
-// ILU(tau): one warp per row, rows from a ticket in natural order.
-template <bool NO_FILL>
+// ---- ILU(tau): working table of 2^HB slots per warp, rows to a shared pool
+template <int HB>
+struct HTab {
+    static constexpr int N = 1 << HB;
+    static constexpr int MAX = N * 3 / 4;
+    int* keys;
+    double* vals;
+    __device__ __forceinline__ unsigned slot(int j) const { return ((unsigned)j * 2654435761u) >> (32 - HB); }
+    __device__ __forceinline__ int find(int j) const {
+        unsigned s = slot(j);
+        for (int p = 0; p < N; ++p, s = (s + 1) & (N - 1)) {
+            const int k = keys[s];
+            if (k == j) return (int)s;
+            if (k == EMPTY) return -1;
+        }
+        return -1;
+    }
+    __device__ __forceinline__ int insert(int j, bool* fresh) const {
+        unsigned s = slot(j);
+        for (int p = 0; p < N; ++p, s = (s + 1) & (N - 1)) {
+            int k = keys[s];
+            if (k == j) { *fresh = false; return (int)s; }
+            if (k == EMPTY) {
+                k = atomicCAS(keys + s, EMPTY, j);
+                if (k == EMPTY) { *fresh = true; return (int)s; }
+                if (k == j) { *fresh = false; return (int)s; }
+            }
+        }
+        return -1;
+    }
+    __device__ __forceinline__ unsigned long long next_pivot(int last, int lim, int lane) const {
+        unsigned long long best = ~0ull;
+        for (int s = lane; s < N; s += 32) {
+            const int k = keys[s];
+            if (k > last && k < lim) {
+                unsigned long long v = ((unsigned long long)(unsigned)k << 32) | (unsigned)s;
+                best = v < best ? v : best;
+            }
+        }
+        return warp_min_u64(best);
+    }
+};
+
+struct IlutOut {
+    int* Lcnt;              // per row: multipliers
+    int* Ucnt;              // per row: kept U entries (unsorted in the pool)
+    int64_t* off;           // per row: first pool slot (L part, then U part)
+    int32_t* pcol;          // pool
+    double* pval;
+    unsigned long long* pool_used;
+    int64_t pool_cap;
+    int32_t* scol;          // per-warp L staging (MAX entries per warp)
+    double* sval;
+};
+
+// One warp per row, rows from a ticket in natural order (topological: every
+// pivot row precedes the row); a row waits only on its pivot rows' published
+// pivots and reads their U parts from the pool in L2.
+template <bool NO_FILL, int HB>
 __global__ void __launch_bounds__(128) k_ilut(int n, int* ticket, CsrV S, const double* __restrict__ scale,
-                                              double fill_tol, int cap, int* __restrict__ Lcnt,
-                                              int32_t* __restrict__ Lcol, double* __restrict__ Lval,
-                                              int* __restrict__ Ucnt, int32_t* __restrict__ Ucol,
-                                              double* __restrict__ Uval, double* __restrict__ udiag, int* shifts,
-                                              int* err) {
+                                              double fill_tol, IlutOut out, double* __restrict__ udiag,
+                                              int* shifts, int* err) {
+    using T = HTab<HB>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Table t = table_at(smem + (size_t)wid * warp_bytes(cap), cap);
+    T t;
+    t.vals = reinterpret_cast<double*>(smem + (size_t)wid * T::N * 12);
+    t.keys = reinterpret_cast<int*>(t.vals + T::N);
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int32_t* scol = out.scol + gw * T::MAX;
+    double* sval = out.sval + gw * T::MAX;
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(ticket, 1);
         i = __shfl_sync(0xffffffffu, i, 0);
         if (i >= n) break;
-        clear_table(t, lane);
+        for (int q = lane; q < T::N; q += 32) t.keys[q] = EMPTY;
+        __syncwarp();
         const int lo = S.ptr[i], hi = S.ptr[i + 1];
         const double norm = scale[i];
         const double tau = fill_tol * norm;
-        bool bad = hi - lo > HMAX;
+        int live = hi - lo;                     // keys ever inserted (tombstones included)
+        bool bad = live > T::MAX;
         if (!bad) {
             for (int e = lo + lane; e < hi; e += 32) {
                 bool fresh;
-                const int s = hinsert(t, S.idx[e], &fresh);
-                t.vals[s] = S.val[e];
+                const int q = t.insert(S.idx[e], &fresh);
+                t.vals[q] = S.val[e];
             }
-            if (lane == 0) t.misc[0] = hi - lo;
         }
         __syncwarp();
-        const int64_t o = (int64_t)i * cap;
         int nl = 0, last = -1;
         while (!bad) {
-            const unsigned long long best = next_pivot(t, last, i, lane);
+            const unsigned long long best = t.next_pivot(last, i, lane);
             if (best == ~0ull) break;
-            const int k = (int)(best >> 32), s = (int)(best & 0xffffffffu);
-            const double a = t.vals[s];
+            const int k = (int)(best >> 32), q = (int)(best & 0xffffffffu);
+            const double a = t.vals[q];
             __syncwarp();
-            if (lane == 0) t.keys[s] = TOMB;   // row.pop(k)
+            if (lane == 0) t.keys[q] = TOMB;   // row.pop(k)
             last = k;
             if (fabs(a) < tau) {               // dropped: no multiplier, no update
                 __syncwarp();
@@ -203,18 +265,18 @@ __global__ void __launch_bounds__(128) k_ilut(int n, int* ticket, CsrV S, const 
             d = __shfl_sync(0xffffffffu, d, 0);
             __threadfence();                   // pivot row k's U part is read after its pivot was seen
             const double lik = __ddiv_rn(a, d);
-            const int cu = __ldcg(Ucnt + k);
-            const int64_t ok = (int64_t)k * cap;
+            const int cu = __ldcg(out.Ucnt + k);
+            const int64_t ok = __ldcg(out.off + k) + __ldcg(out.Lcnt + k);
             int added = 0;
-            for (int q = lane; q < cu; q += 32) {
-                const int j = __ldcg(Ucol + ok + q);
-                const double u = __ldcg(Uval + ok + q);
+            for (int r = lane; r < cu; r += 32) {
+                const int j = __ldcg(out.pcol + ok + r);
+                const double u = __ldcg(out.pval + ok + r);
                 if (NO_FILL) {
-                    const int sj = hfind(t, j);
+                    const int sj = t.find(j);
                     if (sj >= 0) t.vals[sj] = sub_mul(t.vals[sj], lik, u);
                 } else {
                     bool fresh = false;
-                    const int sj = hinsert(t, j, &fresh);
+                    const int sj = t.insert(j, &fresh);
                     if (sj < 0) { bad = true; continue; }
                     if (fresh) {
                         t.vals[sj] = -__dmul_rn(lik, u);
@@ -224,40 +286,66 @@ __global__ void __launch_bounds__(128) k_ilut(int n, int* ticket, CsrV S, const 
                     }
                 }
             }
-            added = warp_sum(added);
-            bad = __any_sync(0xffffffffu, bad);
+            live += warp_sum(added);
+            bad = __any_sync(0xffffffffu, bad) || live > T::MAX;
             if (lane == 0) {
-                if (nl < cap) {
-                    Lcol[o + nl] = k;
-                    Lval[o + nl] = lik;
-                }
-                t.misc[0] += added;
+                scol[nl] = k;
+                sval[nl] = lik;
             }
             ++nl;
             __syncwarp();
-            if (nl > cap || t.misc[0] > HMAX) bad = true;
         }
         double piv = 0.0;
         int nu = 0;
         if (!bad) {
-            const int sd = hfind(t, i);          // row.pop(i, 0.0)
+            const int sd = t.find(i);          // row.pop(i, 0.0)
             piv = sd >= 0 ? t.vals[sd] : 0.0;
             const double g = PIVOT_GUARD * norm;
             if (fabs(piv) < g) {
                 piv = piv >= 0.0 ? g : -g;
                 if (lane == 0) atomicAdd(shifts, 1);
             }
-            nu = emit_sorted_upper(t, i, tau, cap, lane, Ucol + o, Uval + o);
-            if (nu > cap) bad = true;
+            for (int q = lane; q < T::N; q += 32) {
+                const int k = t.keys[q];
+                nu += k > i && !(fabs(t.vals[q]) < tau);
+            }
+            nu = warp_sum(nu);
         }
-        if (bad) {
+        int64_t base = 0;
+        if (!bad && lane == 0) {
+            base = (int64_t)atomicAdd(out.pool_used, (unsigned long long)(nl + nu));
+            if (base + nl + nu > out.pool_cap) bad = true;
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        bad = __shfl_sync(0xffffffffu, bad, 0);
+        if (!bad) {
+            __syncwarp();
+            for (int r = lane; r < nl; r += 32) {
+                out.pcol[base + r] = scol[r];
+                out.pval[base + r] = sval[r];
+            }
+            int m = nl;
+            for (int q0 = 0; q0 < T::N; q0 += 32) {   // U part in table order (sorted at compaction)
+                const int q = q0 + lane;
+                const int k = t.keys[q];
+                const bool take = k > i && !(fabs(t.vals[q]) < tau);
+                const unsigned bal = __ballot_sync(0xffffffffu, take);
+                if (take) {
+                    const int64_t pos = base + m + __popc(bal & ((1u << lane) - 1));
+                    out.pcol[pos] = k;
+                    out.pval[pos] = t.vals[q];
+                }
+                m += __popc(bal);
+            }
+        } else {
             if (lane == 0) atomicExch(err, ERR_OVERFLOW);
             nl = nu = 0;
             piv = 1.0;                           // unblock dependants; the factor is discarded
         }
         if (lane == 0) {
-            Lcnt[i] = nl;
-            Ucnt[i] = nu;
+            out.off[i] = base;
+            out.Lcnt[i] = nl;
+            out.Ucnt[i] = nu;
         }
         __threadfence();
         __syncwarp();
@@ -462,6 +550,58 @@ int row_cap(Ctx* c, const Csr& A, double fill_tol, bool no_fill) {
 
 }  // namespace
 
+namespace {
+template <bool FILL>
+__global__ void k_pool_rows(int n, const int* __restrict__ lc, const int* __restrict__ uc,
+                            const int64_t* __restrict__ off, const int32_t* __restrict__ pcol,
+                            const double* __restrict__ pval, int32_t* __restrict__ cnt, const int32_t* __restrict__ ptr,
+                            int32_t* __restrict__ idx, double* __restrict__ val) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int m = lc[i] + uc[i];
+    if (!FILL) {
+        cnt[i] = m;
+        return;
+    }
+    const int64_t o = off[i];
+    const int p = ptr[i];
+    for (int q = 0; q < m; ++q) {
+        idx[p + q] = pcol[o + q];
+        val[p + q] = pval[o + q];
+    }
+}
+}  // namespace
+
+// pooled rows (L part in pop order, U part unsorted) -> canonical CSR rows
+void pool_to_csr(Ctx* c, int n, const int* lc, const int* uc, const int64_t* off, const int32_t* pcol,
+                 const double* pval, Csr& out) {
+    out.n_rows = out.n_cols = n;
+    out.ptr.reset(c, (size_t)n + 1);
+    DevBuf<int32_t> cnt(c, std::max(n, 1));
+    if (n) {
+        k_pool_rows<false><<<ceil_div(n, 256), 256, 0, c->stream>>>(n, lc, uc, off, pcol, pval, cnt.p, nullptr,
+                                                                   nullptr, nullptr);
+        check_launch("k_pool_rows");
+    }
+    out.nnz = scan_counts(c, cnt.p, out.ptr.p, n);
+    DevBuf<int32_t> idx(c, std::max<int64_t>(out.nnz, 1));
+    DevBuf<double> val(c, std::max<int64_t>(out.nnz, 1));
+    out.idx.reset(c, std::max<int64_t>(out.nnz, 1));
+    out.val.reset(c, std::max<int64_t>(out.nnz, 1));
+    if (n && out.nnz) {
+        Prof pr(c, "ilut_compact", 48.0 * out.nnz);
+        k_pool_rows<true><<<ceil_div(n, 256), 256, 0, c->stream>>>(n, lc, uc, off, pcol, pval, nullptr, out.ptr.p,
+                                                                  idx.p, val.p);
+        check_launch("k_pool_rows");
+        size_t bytes = 0;
+        cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, idx.p, out.idx.p, val.p, out.val.p, (int)out.nnz, n,
+                                            out.ptr.p, out.ptr.p + 1, c->stream);
+        EDFA_CUDA(cub::DeviceSegmentedSort::SortPairs(c->cub_scratch(bytes), bytes, idx.p, out.idx.p, val.p,
+                                                      out.val.p, (int)out.nnz, n, out.ptr.p, out.ptr.p + 1,
+                                                      c->stream));
+    }
+}
+
 void drop_zeros(Ctx* c, Csr& A) {
     const int n = A.n_rows;
     Csr out;
@@ -486,41 +626,65 @@ void drop_zeros(Ctx* c, Csr& A) {
 void ilut_factor(Ctx* c, const Csr& S, double fill_tol, bool no_fill, IluFactor& f) {
     const int n = S.n_rows;
     f.n = n;
-    const int cap = row_cap(c, S, fill_tol, no_fill);
     DevBuf<double> sc(c, std::max(n, 1));
     DevBuf<int> lc(c, std::max(n, 1)), uc(c, std::max(n, 1));
-    DevBuf<int32_t> lcol(c, (size_t)std::max(n, 1) * cap), ucol(c, (size_t)std::max(n, 1) * cap);
-    DevBuf<double> lval(c, (size_t)std::max(n, 1) * cap), uval(c, (size_t)std::max(n, 1) * cap);
+    DevBuf<int64_t> off(c, std::max(n, 1));
     f.udiag.reset(c, std::max(n, 1));
     f.has_diag.reset(c, std::max(n, 1));
     int* flags = c->d_scalar_i + 24;   // [shifts, err]
-    EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+    unsigned long long* used = reinterpret_cast<unsigned long long*>(c->d_scalar_i + 56);
+    // pool: no_fill rows are at most S's rows; with fill start at 4x and grow on overflow
+    int64_t pool_cap = no_fill ? S.nnz + 1 : 4 * S.nnz + 64 * (int64_t)n;
+    int hb = 10;
     if (n) {
         k_row_scale<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(S), sc.p);
         check_launch("k_row_scale");
-        fill_bits(c, f.udiag.p, n, SENTINEL_BITS);
-        int* tk = c->d_scalar_i + 29;
-        EDFA_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), c->stream));
-        const int threads = 128;
-        const size_t smem = warp_bytes(cap) * (threads / 32);
-        auto kern = no_fill ? k_ilut<true> : k_ilut<false>;
-        EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        int occ = 0;
-        EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-        const int grid = NUM_SMS_B200 * std::max(1, occ);
-        Prof pr(c, "ilut_factor", 24.0 * S.nnz + 24.0 * n);
-        kern<<<grid, threads, smem, c->stream>>>(n, tk, view(S), sc.p, fill_tol, cap, lc.p, lcol.p, lval.p, uc.p,
-                                                 ucol.p, uval.p, f.udiag.p, flags, flags + 1);
-        check_launch("k_ilut");
     }
-    int h[2];
-    EDFA_CUDA(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, c->stream));
-    EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    f.shifts = h[0];
-    require(h[1] != ERR_SPIN, EDFA_ERR_CUDA, "ILU(tau) factorisation stalled");
-    require(h[1] == 0, EDFA_ERR_UNSUPPORTED,
-            "ILU(tau) fill exceeds " + std::to_string(cap) + " entries per factor row (use a larger drop tolerance)");
-    pad_to_csr(c, n, n, cap, lc.p, lcol.p, lval.p, uc.p, ucol.p, uval.p, f.LU);
+    for (int attempt = 0;; ++attempt) {
+        DevBuf<int32_t> pcol(c, (size_t)std::max<int64_t>(pool_cap, 1));
+        DevBuf<double> pval(c, (size_t)std::max<int64_t>(pool_cap, 1));
+        EDFA_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+        EDFA_CUDA(cudaMemsetAsync(used, 0, sizeof(unsigned long long), c->stream));
+        if (n) {
+            fill_bits(c, f.udiag.p, n, SENTINEL_BITS);
+            int* tk = c->d_scalar_i + 29;
+            EDFA_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), c->stream));
+            const int threads = 128;
+            auto kern = hb == 10 ? (no_fill ? k_ilut<true, 10> : k_ilut<false, 10>)
+                                 : (no_fill ? k_ilut<true, 12> : k_ilut<false, 12>);
+            const size_t smem = (size_t)(1 << hb) * 12 * (threads / 32);
+            EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            int occ = 0;
+            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+            const int grid = NUM_SMS_B200 * std::max(1, occ);
+            const int64_t warps = (int64_t)grid * (threads / 32);
+            const int hmax = (1 << hb) * 3 / 4;
+            DevBuf<int32_t> scol(c, (size_t)warps * hmax);
+            DevBuf<double> sval(c, (size_t)warps * hmax);
+            IlutOut o{lc.p, uc.p, off.p, pcol.p, pval.p, used, pool_cap, scol.p, sval.p};
+            Prof pr(c, "ilut_factor", 24.0 * S.nnz + 24.0 * n);
+            kern<<<grid, threads, smem, c->stream>>>(n, tk, view(S), sc.p, fill_tol, o, f.udiag.p, flags, flags + 1);
+            check_launch("k_ilut");
+        }
+        int h[2];
+        unsigned long long hu = 0;
+        EDFA_CUDA(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaMemcpyAsync(&hu, used, sizeof hu, cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        require(h[1] != ERR_SPIN, EDFA_ERR_CUDA, "ILU(tau) factorisation stalled");
+        if (h[1] == 0) {
+            f.shifts = h[0];
+            pool_to_csr(c, n, lc.p, uc.p, off.p, pcol.p, pval.p, f.LU);
+            break;
+        }
+        // overflow: a row outgrew the working table (-> 4096 slots) or the pool (-> larger pool)
+        const bool pool_full = (int64_t)hu > pool_cap;
+        require(attempt < 4 && (pool_full || hb == 10), EDFA_ERR_UNSUPPORTED,
+                "ILU(tau) fill exceeds " + std::to_string((1 << hb) * 3 / 4) +
+                    " entries per working row (use a larger drop tolerance)");
+        if (pool_full) pool_cap = std::max<int64_t>(2 * pool_cap, (int64_t)hu + n);
+        else hb = 12;
+    }
     if (n) EDFA_CUDA(cudaMemsetAsync(f.has_diag.p, 0, sizeof(int32_t) * n, c->stream));
 }
 

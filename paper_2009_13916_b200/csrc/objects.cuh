@@ -116,6 +116,7 @@ struct TriPlan {
     int32_t n_levels = 0;
     int64_t n_dep = 0;      // off-diagonal coefficients (algorithmic)
     int64_t n_stored = 0;   // SELL entries incl. padding
+    int32_t max_w = 0;      // widest slice (entries per row); > 16 -> warp-per-row sync-free solve
     bool unit = false;
     DevBuf<int32_t> perm;       // slot -> row (-1 pad)
     DevBuf<int64_t> slice_ptr;  // slice -> first SELL entry

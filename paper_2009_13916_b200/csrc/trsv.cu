@@ -82,6 +82,11 @@ __global__ void k_slice_width(const int* __restrict__ perm, int n_slices, const 
     len = warp_max(len);
     if (lane == 0) wbytes[s] = (int64_t)len * 32;
 }
+__global__ void k_max_width(const int64_t* __restrict__ sptr, int n_slices, int* __restrict__ out) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n_slices) atomicMax(out, (int)((sptr[s + 1] - sptr[s]) / 32));
+}
+
 __global__ void k_fill_sell(const int* __restrict__ perm, int n_slices, CsrV D, const int64_t* __restrict__ sptr,
                             int32_t* __restrict__ col, double* __restrict__ val, const double* __restrict__ diag,
                             bool unit, double* __restrict__ dinv) {
@@ -373,9 +378,16 @@ void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool rev
         EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(b2), b2, wb.p, p.slice_ptr.p, n_slices + 1, c->stream));
     }
     int64_t stored = 0;
+    int* mw = c->d_scalar_i + 19;
+    EDFA_CUDA(cudaMemsetAsync(mw, 0, sizeof(int), c->stream));
+    k_max_width<<<ceil_div(n_slices, 256), 256, 0, c->stream>>>(p.slice_ptr.p, n_slices, mw);
+    check_launch("k_max_width");
+    int hmw = 0;
     EDFA_CUDA(cudaMemcpyAsync(&stored, p.slice_ptr.p + n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(&hmw, mw, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaStreamSynchronize(c->stream));
     p.n_stored = stored;
+    p.max_w = hmw;
     p.col.reset(c, std::max<int64_t>(stored, 1));
     p.val.reset(c, std::max<int64_t>(stored, 1));
     p.dinv.reset(c, std::max<int64_t>(slots, 1));
@@ -400,6 +412,52 @@ void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& p) {
     check_launch("k_fill_sell values");
 }
 
+// Sync-free solve for plans with wide rows (e.g. the Schur factors of dynamic
+// patterns on distorted grids, ~70 dependencies per row): one warp per row,
+// rows taken from a ticket in level order (topological, so a warp only waits
+// on rows held by running warps), lanes gather the row's dependencies in
+// parallel and poll each one on the solution vector itself (SENTINEL-filled:
+// a stored value is its own ready flag), a warp reduction, one store.  No
+// grid barrier per level; the hand-off is one L2 round trip.
+__global__ void __launch_bounds__(256) k_trsv_wsf(const int* __restrict__ perm, const int64_t* __restrict__ sptr,
+                                                  const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ dinv, int n_slots, int* ticket,
+                                                  const double* __restrict__ b, double alpha, double* x,
+                                                  const double* __restrict__ add, double* __restrict__ out2,
+                                                  int* err) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(ticket, 1);
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (slot >= n_slots) break;
+        const int r = perm[slot];
+        if (r < 0) continue;
+        const int s = slot >> 5, rr = slot & 31;
+        const int64_t b0 = sptr[s];
+        const int w = (int)((sptr[s + 1] - b0) / 32);
+        double acc = 0.0;
+        for (int k = lane; k < w; k += 32) {
+            const int cidx = __ldg(col + b0 + 32 * (int64_t)k + rr);
+            if (cidx < 0) continue;
+            const double v = __ldg(val + b0 + 32 * (int64_t)k + rr);
+            double xv = ld_relaxed(x + cidx);
+            long long spins = 0;
+            while (is_sentinel(xv)) {
+                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv = 0.0; break; }
+                xv = ld_relaxed(x + cidx);
+            }
+            acc = fma(-v, xv, acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) {
+            const double xr = (alpha * __ldg(b + r) + acc) * dinv[slot];
+            st_relaxed(x + r, publishable(xr));
+            if (out2) out2[r] = xr + add[r];
+        }
+    }
+}
+
 void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name) {
     if (p.n == 0) return;
@@ -413,6 +471,22 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
     }
     if (p.is_tile) {   // epoch / ticket bookkeeping is per plan (serialised on the stream)
         run_tile(c, const_cast<TilePlan&>(p.tile), b, alpha, x, add, out2, name);
+        return;
+    }
+    if (p.max_w > 16 && x != b && !getenv("EDFA_TRSV_LEVELS")) {
+        fill_bits(c, x, p.n, SENTINEL_BITS);
+        EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
+        int* err = c->d_scalar_i + 52;
+        Prof pr(c, name, 12.0 * p.n_dep + 8.0 * p.n + 16.0 * p.n + (out2 ? 16.0 * p.n : 0.0));
+        static int grid_sf = 0;
+        if (!grid_sf) {
+            int occ = 0;
+            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv_wsf, 256, 0));
+            grid_sf = NUM_SMS_B200 * std::max(1, occ);
+        }
+        k_trsv_wsf<<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.n_slots,
+                                                   p.ticket.p, b, alpha, x, add, out2, err);
+        check_launch("k_trsv_wsf");
         return;
     }
     LsArgs a{p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.level_start.p, p.n_levels,

@@ -503,3 +503,24 @@ def test_config4_transient_refresh_matches_oracle(edfa):
         assert np.linalg.norm(x - xo) <= 1e-7 * np.linalg.norm(xo)
         p_prev = x[s.n_free_faces:]
         dt *= case.meta["dt_mult"]
+
+
+@pytest.mark.parametrize("idx,n,dyn", [(3, 7, True), (3, 6, False)])
+def test_wide_row_syncfree_solver_matches_level_solver(edfa, idx, n, dyn, monkeypatch):
+    """Schur factors with wide rows (dynamic / distorted patterns) use the
+    warp-per-row sync-free solve; it computes the level solver's triangular
+    solutions (up to the order of the row sums)."""
+    from paper_2009_13916_b200 import configs
+    s = configs.make(idx, n=n).system
+    ys = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("EDFA_TRSV_LEVELS", env)
+        if dyn:
+            pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
+        else:
+            pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, "static", "C"), no_fill=True)
+        r = np.random.default_rng(11).standard_normal(s.n_unknowns)
+        ys.append((pre.apply(r), pre.stage2.schur_inner.apply(r[s.n_free_faces:])))
+    for a, b in zip(ys[0], ys[1]):
+        assert np.abs(a - b).max() <= 1e-11 * np.abs(b).max()
