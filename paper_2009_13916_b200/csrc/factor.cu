@@ -539,7 +539,13 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         select_part(c, S, 0, 1.0, false, Lpart);
         build_plan(c, Lpart, nullptr, true, false, f.fwd, /*allow_chain=*/false);
     };
-    if (!sync_free) level_plan();
+    const bool have_levels = !sync_free;
+    if (!sync_free) {
+        level_plan();
+        // rows in level order are topological too: run the sync-free kernel on
+        // that order (no grid barrier per level) unless levels are requested
+        sync_free = !getenv("EDFA_ILU_LEVELS");
+    }
     PhaseTimer pt_fact(c, "ilu0.factor+plans");
     int maxr = n ? max_row_nnz(c, S) : 0;
     require(maxr <= 1024, EDFA_ERR_UNSUPPORTED, "Schur rows longer than 1024 entries are not supported");
@@ -560,8 +566,8 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         if (sync_free) fill_bits(c, ud, n, SENTINEL_BITS);   // a row's pivot is its ready flag
         Prof pr(c, "ilu0_factor", 24.0 * S.nnz + 24.0 * n);
         LevelArgs la{f.fwd.perm.p, f.fwd.level_start.p, f.fwd.n_levels, reinterpret_cast<unsigned*>(f.fwd.sync.p)};
-        const int* op = ord.p;
-        int n_ord = n;
+        const int* op = have_levels ? f.fwd.perm.p : ord.p;
+        int n_ord = have_levels ? f.fwd.n_slots : n;
         int* tk = c->d_scalar_i + 29;
         if (sync_free) EDFA_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), c->stream));
         void* args[] = {&la, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
@@ -605,7 +611,7 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
     int err = 0;
     read_flags(c, flags, &f.shifts, &err);
     require(err == 0, EDFA_ERR_CUDA, "ILU(0) factorisation failed");
-    ilu_plans(c, f, dims, !sync_free);
+    ilu_plans(c, f, dims, have_levels);
 }
 
 // triangular-solve plans of an ILU factor (f.LU strict parts + f.udiag);

@@ -524,3 +524,19 @@ def test_wide_row_syncfree_solver_matches_level_solver(edfa, idx, n, dyn, monkey
         ys.append((pre.apply(r), pre.stage2.schur_inner.apply(r[s.n_free_faces:])))
     for a, b in zip(ys[0], ys[1]):
         assert np.abs(a - b).max() <= 1e-11 * np.abs(b).max()
+
+
+def test_syncfree_ilu0_on_level_order_is_bitwise_level_synchronous(edfa, monkeypatch):
+    """Stencils whose wavefront order is not topological (dynamic patterns on
+    distorted grids) factor sync-free in level order; the factors equal the
+    level-synchronous kernel's bit for bit (same operations per row)."""
+    from paper_2009_13916_b200 import configs
+    s = configs.make(3, n=6).system
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("EDFA_ILU_LEVELS", env)
+        pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
+        out.append((pre.stage2.schur_inner.L, pre.stage2.schur_inner.U))
+    for a, b in zip(out[0], out[1]):
+        assert same_csr(a, b) and np.array_equal(a.data, b.data)
