@@ -452,7 +452,10 @@ __global__ void __launch_bounds__(256) k_trsv_wsf(const int* __restrict__ perm, 
         acc = warp_sum(acc);
         if (lane == 0) {
             const double xr = (alpha * __ldg(b + r) + acc) * dinv[slot];
-            st_relaxed(x + r, publishable(xr));
+            // fire-and-forget reduction performed at L2 (SENTINEL + (x - SENTINEL)):
+            // visible to the polling warps sooner than a buffered store
+            atomicAdd(reinterpret_cast<unsigned long long*>(x + r),
+                      (unsigned long long)__double_as_longlong(publishable(xr)) - SENTINEL_BITS);
             if (out2) out2[r] = xr + add[r];
         }
     }
@@ -473,7 +476,8 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
         run_tile(c, const_cast<TilePlan&>(p.tile), b, alpha, x, add, out2, name);
         return;
     }
-    if (p.max_w > 16 && x != b && !getenv("EDFA_TRSV_LEVELS")) {
+    static const bool force_sf = getenv("EDFA_TRSV_WSF") != nullptr;
+    if ((p.max_w > 16 || force_sf) && x != b && !getenv("EDFA_TRSV_LEVELS")) {
         fill_bits(c, x, p.n, SENTINEL_BITS);
         EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
         int* err = c->d_scalar_i + 52;

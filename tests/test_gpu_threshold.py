@@ -137,13 +137,17 @@ def test_threshold_overflow_is_reported(edfa):
 
     from paper_2009_13916_b200 import _lib as L
     from paper_2009_13916_b200.device import DeviceCsr, ctx
-    n = 600
-    rng = np.random.default_rng(0)
-    M = rng.standard_normal((n, n)) + n * np.eye(n)      # dense: row n-1 has n-1 multipliers
+    n = 4000                                              # arrow: the last row holds n entries
+    M = sp.lil_matrix((n, n))
+    M.setdiag(4.0)
+    M[n - 1, :] = 1.0
+    M[n - 1, n - 1] = 4.0 * n
     A = DeviceCsr.from_scipy(sp.csr_matrix(M))
     f = C.c_void_p()
     with pytest.raises(L.EdfaUnsupported):
         L.check(L.lib().edfa_factor_ilu(ctx(), A.handle, 0.0, 0, 0, 0, 0, C.byref(f)))
+    rng = np.random.default_rng(0)
+    M = rng.standard_normal((600, 600)) + 600 * np.eye(600)
     # the same matrix with a drop tolerance that keeps rows short factorises
     B = sp.csr_matrix(np.where(np.abs(M) > 2.5, M, 0.0))
     Bd = DeviceCsr.from_scipy(B)
