@@ -477,7 +477,10 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
         return;
     }
     static const bool force_sf = getenv("EDFA_TRSV_WSF") != nullptr;
-    if ((p.max_w > 16 || force_sf) && x != b && !getenv("EDFA_TRSV_LEVELS")) {
+    // wide rows, or levels narrow enough that a grid barrier per level costs
+    // more than the rows: sync-free warp-per-row solve
+    const bool sf = p.max_w > 16 || (int64_t)p.n < 16384ll * std::max(p.n_levels, 1) || force_sf;
+    if (sf && x != b && !getenv("EDFA_TRSV_LEVELS")) {
         fill_bits(c, x, p.n, SENTINEL_BITS);
         EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
         int* err = c->d_scalar_i + 52;
