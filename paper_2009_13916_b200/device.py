@@ -121,7 +121,7 @@ class DeviceCsr:
         return y
 
     def __del__(self):
-        if self._owner and self.handle and L._lib is not None:
+        if self._owner and self.handle and getattr(L, "_lib", None) is not None:
             try:
                 L._lib.edfa_csr_destroy(self.handle)
             except Exception:   # pragma: no cover - interpreter shutdown
@@ -211,7 +211,7 @@ class DeviceSystem:
     __matmul__ = spmv
 
     def __del__(self):
-        if getattr(self, "handle", None) and L._lib is not None:
+        if getattr(self, "handle", None) and getattr(L, "_lib", None) is not None:
             try:
                 L._lib.edfa_system_destroy(self.handle)
             except Exception:   # pragma: no cover

@@ -163,7 +163,7 @@ class Stage1:
         return PatternSet(device=self._part(L.S1_Q), provenance="used")
 
     def __del__(self):
-        if getattr(self, "handle", None) and L._lib is not None:
+        if getattr(self, "handle", None) and getattr(L, "_lib", None) is not None:
             try:
                 L._lib.edfa_stage1_destroy(self.handle)
             except Exception:   # pragma: no cover
@@ -201,7 +201,7 @@ class Stage2:
         return self._cache["S"]
 
     def __del__(self):
-        if getattr(self, "handle", None) and L._lib is not None:
+        if getattr(self, "handle", None) and getattr(L, "_lib", None) is not None:
             try:
                 L._lib.edfa_stage2_destroy(self.handle)
             except Exception:   # pragma: no cover
