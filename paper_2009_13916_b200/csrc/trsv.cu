@@ -461,6 +461,56 @@ __global__ void __launch_bounds__(256) k_trsv_wsf(const int* __restrict__ perm, 
     }
 }
 
+// Sync-free solve for narrow rows: one warp per 32-row slice (rows of one
+// level), slices from a ticket in level order, a thread per row polls its
+// dependencies on the SENTINEL-filled solution vector.  Coefficient loads are
+// coalesced (SELL-32) and issued before the polls; the row arithmetic is the
+// level solver's (bias first, entries in stored order) so the results are
+// bitwise those of k_trsv_ls.
+template <int K>
+__global__ void __launch_bounds__(256) k_trsv_tsf(const int* __restrict__ perm, const int64_t* __restrict__ sptr,
+                                                  const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                  const double* __restrict__ dinv, int n_slices, int* ticket,
+                                                  const double* __restrict__ b, double alpha, double* x,
+                                                  const double* __restrict__ add, double* __restrict__ out2,
+                                                  int* err) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        int s = 0;
+        if (lane == 0) s = atomicAdd(ticket, 1);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        if (s >= n_slices) break;
+        const int r = perm[s * 32 + lane];
+        const int64_t b0 = sptr[s];
+        const int w = (int)((sptr[s + 1] - b0) / 32);
+        if (r < 0) continue;
+        int cc[K];
+        double vv[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            const bool in = u < w;
+            cc[u] = in ? __ldg(col + b0 + (int64_t)u * 32 + lane) : -1;
+            vv[u] = in ? __ldg(val + b0 + (int64_t)u * 32 + lane) : 0.0;
+        }
+        double acc = alpha * __ldg(b + r);
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            if (cc[u] < 0) continue;
+            double xv = ld_relaxed(x + cc[u]);
+            long long spins = 0;
+            while (is_sentinel(xv)) {
+                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv = 0.0; break; }
+                xv = ld_relaxed(x + cc[u]);
+            }
+            acc = fma(-vv[u], xv, acc);
+        }
+        const double xr = acc * dinv[s * 32 + lane];
+        atomicAdd(reinterpret_cast<unsigned long long*>(x + r),
+                  (unsigned long long)__double_as_longlong(publishable(xr)) - SENTINEL_BITS);
+        if (out2) out2[r] = xr + add[r];
+    }
+}
+
 void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name) {
     if (p.n == 0) return;
@@ -491,9 +541,15 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
             EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv_wsf, 256, 0));
             grid_sf = NUM_SMS_B200 * std::max(1, occ);
         }
-        k_trsv_wsf<<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.n_slots,
-                                                   p.ticket.p, b, alpha, x, add, out2, err);
-        check_launch("k_trsv_wsf");
+        if (p.max_w > 16 || getenv("EDFA_TRSV_WARP_ROWS")) {
+            k_trsv_wsf<<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p,
+                                                       p.n_slots, p.ticket.p, b, alpha, x, add, out2, err);
+            check_launch("k_trsv_wsf");
+        } else {
+            k_trsv_tsf<16><<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p,
+                                                           p.n_slots / 32, p.ticket.p, b, alpha, x, add, out2, err);
+            check_launch("k_trsv_tsf");
+        }
         return;
     }
     LsArgs a{p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p, p.level_start.p, p.n_levels,

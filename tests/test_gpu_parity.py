@@ -540,3 +540,19 @@ def test_syncfree_ilu0_on_level_order_is_bitwise_level_synchronous(edfa, monkeyp
         out.append((pre.stage2.schur_inner.L, pre.stage2.schur_inner.U))
     for a, b in zip(out[0], out[1]):
         assert same_csr(a, b) and np.array_equal(a.data, b.data)
+
+
+def test_narrow_row_syncfree_solver_is_bitwise_level_solver(edfa, monkeypatch):
+    """Level plans with narrow rows (IC of -A_ff on a distorted grid) run the
+    thread-per-row sync-free solve: same arithmetic order as the
+    level-synchronous kernel, so the solutions agree bit for bit."""
+    from paper_2009_13916_b200 import configs
+    s = configs.make(3, n=7).system
+    r = np.random.default_rng(5).standard_normal(s.n_free_faces)
+    ys = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("EDFA_TRSV_LEVELS", env)
+        pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, "static", "A"), no_fill=True)
+        ys.append(pre.stage1.face_inner.apply(r))
+    assert np.array_equal(ys[0], ys[1])
