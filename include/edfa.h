@@ -21,6 +21,8 @@
  *   edfa_assemble                         assembly.assemble (assembly.py:186-311), the
  *                                         producer of the path's blocks
  *   edfa_update_accumulation              assembly.update_accumulation (assembly.py:314-333)
+ *   edfa_face_fluxes / edfa_cfl           assembly.recover_face_fluxes (assembly.py:334-356),
+ *                                         driver.cfl (driver.py:67-71)
  *
  * Conventions
  *   - Every call is stream-ordered on the context's stream.  Calls that must
@@ -334,6 +336,20 @@ typedef struct edfa_assembly_out {   /* caller-allocated device arrays         *
 int edfa_assemble(edfa_ctx* ctx, const edfa_hex_grid* grid, const edfa_assembly_in* in,
                   edfa_assembly_out* out, edfa_csr** A_ff, edfa_csr** A_fc, edfa_csr** A_cf,
                   edfa_csr** A_cc_steady);
+/* After the solve (hx/assembly.py:334-356): per-face fluxes q_out[n_faces],
+ * positive out of the owner -- strong two-sided flux on interior faces, the
+ * owner's one-sided flux on the hull.  face_value holds the prescribed
+ * pressures of Dirichlet faces (face_index < 0); binv/row_sums/diag as
+ * written by edfa_assemble. */
+int edfa_face_fluxes(edfa_ctx* ctx, const edfa_hex_grid* grid, const int32_t* face_index,
+                     const double* face_value, const double* binv, const double* row_sums,
+                     const double* diag, const double* pi_reduced, const double* p, double* q_out);
+/* cfl (hx/driver.py:67-71): chi_out[e] = outflow rate * dt / (volume * porosity)
+ * (chi_out may be NULL); max_out (HOST, 2 doubles) = [max chi, max |p_new - p_old|]
+ * (the step controller's dp_max, hx/driver.py:215; p_new/p_old may be NULL). */
+int edfa_cfl(edfa_ctx* ctx, const edfa_hex_grid* grid, const double* q, const double* elem_volume,
+             const double* porosity, double porosity_scalar, double dt, const double* p_new,
+             const double* p_old, double* chi_out, double* max_out);
 /* A_cc = canonical(A_cc_steady + diag(acc/dt)), rhs_c = rhs_c_base + acc*p_prev/dt
  * (p_prev NULL = zeros; dt = +inf returns the steady pair). */
 int edfa_update_accumulation(edfa_ctx* ctx, const edfa_csr* A_cc_steady, const double* accumulation,

@@ -632,3 +632,65 @@ def gmres(A_apply, P_apply, b, tol=1e-8, restart=50, max_it=2000):
             break
     rep.final_relres = np.linalg.norm(b - A_apply(x)) / bn
     return x, rep
+
+
+# ---------------------------------------------------------------------------
+# Transient-loop pieces after the solve: flux recovery,
+# CFL numbers, mass-balance residuals, pressure-driven step control.
+
+def face_pressures(n_faces, free_faces, dirichlet_faces, dirichlet_values, pi_reduced):
+    """Full per-face pressures with prescribed values inserted (hx/assembly.py:178-183)."""
+    out = np.empty(n_faces)
+    out[free_faces] = pi_reduced
+    out[dirichlet_faces] = dirichlet_values
+    return out
+
+
+def recover_face_fluxes(e2f, f2e, floc, Binv, row_sums, diag, pi_full, p):
+    """Per-face flux, positive out of the owner: interior faces the strong
+    two-sided expression, hull faces the owner's one-sided flux
+    (hx/assembly.py:334-356)."""
+    pi_local = pi_full[e2f]
+    q_one = row_sums * p[:, None] - np.einsum("eij,ej->ei", Binv, pi_local)
+    lam = q_one + diag * pi_local
+    owner, nbr = f2e[:, 0], f2e[:, 1]
+    lo, ln = floc[:, 0], floc[:, 1]
+    q = q_one[owner, lo].copy()
+    it = np.flatnonzero(nbr >= 0)
+    d_o = diag[owner[it], lo[it]]
+    d_n = diag[nbr[it], ln[it]]
+    q[it] = (d_n * lam[owner[it], lo[it]] - d_o * lam[nbr[it], ln[it]]) / (d_o + d_n)
+    return q
+
+
+def element_outflows(e2f, f2e, q):
+    """Signed flux out of each element through its faces (hx/assembly.py:359-363)."""
+    sign = np.where(f2e[e2f, 0] == np.arange(e2f.shape[0])[:, None], 1.0, -1.0)
+    return sign * q[e2f]
+
+
+def cfl(e2f, f2e, q, elem_volume, porosity, dt):
+    """chi = outflow rate * dt / pore volume per element (hx/driver.py:67-71)."""
+    out = element_outflows(e2f, f2e, q)
+    rate = np.where(out > 0, out, 0.0).sum(axis=1)
+    return rate * dt / (elem_volume * porosity)
+
+
+def balance_residuals(e2f, f2e, q, elem_volume, accumulation, dt, p, p_prev=None, source=None):
+    """Relative per-cell mass-balance residual (hx/assembly.py:367-387)."""
+    signed = element_outflows(e2f, f2e, q)
+    net = signed.sum(axis=1)
+    gross = np.abs(signed).sum(axis=1)
+    src = np.zeros(e2f.shape[0]) if source is None else elem_volume * source
+    if math.isinf(dt):
+        acc = np.zeros(e2f.shape[0])
+    else:
+        acc = accumulation * (p - (np.zeros(e2f.shape[0]) if p_prev is None else p_prev)) / dt
+    scale = np.maximum(gross + np.abs(acc) + np.abs(src), np.abs(q).max() + 1e-300)
+    return np.abs(acc + net - src) / scale
+
+
+def next_dt(dt, dt_max, dt_mult, dp_target, dp_max):
+    """Pressure-change driven step (hx/driver.py:50-53)."""
+    ratio = dt_mult if dp_max <= 0 else min(dt_mult, dp_target / dp_max)
+    return min(dt * ratio, dt_max)

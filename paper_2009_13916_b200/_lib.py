@@ -124,6 +124,8 @@ _SIGS = {
     "edfa_assemble": (i32, [vp, C.POINTER(HexGridDesc), C.POINTER(AssemblyIn), C.POINTER(AssemblyOut),
                             C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "edfa_update_accumulation": (i32, [vp, vp, vp, vp, vp, f64, C.POINTER(vp), vp]),
+    "edfa_face_fluxes": (i32, [vp, C.POINTER(HexGridDesc), vp, vp, vp, vp, vp, vp, vp, vp]),
+    "edfa_cfl": (i32, [vp, C.POINTER(HexGridDesc), vp, vp, vp, f64, f64, vp, vp, vp, C.POINTER(f64)]),
 }
 
 _lib = None

@@ -448,6 +448,82 @@ __global__ void k_accum_rhs(int n, const double* __restrict__ base, const double
     if (i < n) rhs[i] = base[i] + acc[i] * (p_prev ? p_prev[i] : 0.0) / dt;
 }
 
+// ---- after the solve (hx/assembly.py:334-387, hx/driver.py:67-71)
+__global__ void k_face_pressures(int nf, const int32_t* __restrict__ fidx, const double* __restrict__ fval,
+                                 const double* __restrict__ pi, double* __restrict__ out) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f < nf) out[f] = fidx[f] >= 0 ? pi[fidx[f]] : fval[f];
+}
+
+// one-sided fluxes q1 = rs p - Binv pi_local and strong-flux numerators lam = q1 + diag pi_local
+__global__ void k_cell_flux(int n, const int32_t* __restrict__ e2f, const double* __restrict__ pf,
+                            const double* __restrict__ p, const double* __restrict__ Bi,
+                            const double* __restrict__ rs, const double* __restrict__ dg, double* __restrict__ q1,
+                            double* __restrict__ lam) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    double pl[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) pl[j] = pf[e2f[6 * (int64_t)e + j]];
+    const double pe = p[e];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) s += Bi[(int64_t)(6 * i + j) * n + e] * pl[j];
+        const double q = rs[(int64_t)i * n + e] * pe - s;
+        q1[(int64_t)i * n + e] = q;
+        lam[(int64_t)i * n + e] = q + dg[(int64_t)i * n + e] * pl[i];
+    }
+}
+
+__global__ void k_face_flux(int nf, int n, const int32_t* __restrict__ f2e, const int32_t* __restrict__ floc,
+                            const double* __restrict__ q1, const double* __restrict__ lam,
+                            const double* __restrict__ dg, double* __restrict__ q) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= nf) return;
+    const int o = f2e[2 * f], nb = f2e[2 * f + 1], lo = floc[2 * f];
+    if (nb < 0) {
+        q[f] = q1[(int64_t)lo * n + o];
+        return;
+    }
+    const int ln = floc[2 * f + 1];
+    const double d_o = dg[(int64_t)lo * n + o], d_n = dg[(int64_t)ln * n + nb];
+    q[f] = (d_n * lam[(int64_t)lo * n + o] - d_o * lam[(int64_t)ln * n + nb]) / (d_o + d_n);
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(double* p, double v) {
+    if (!(v >= 0.0)) return;
+    atomicMax(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
+}
+
+// chi = outflow rate * dt / pore volume; max chi and max |p_new - p_old|
+__global__ void k_cfl(int n, const int32_t* __restrict__ e2f, const int32_t* __restrict__ f2e,
+                      const double* __restrict__ q, const double* __restrict__ vol, const double* __restrict__ phi,
+                      double phi_s, double dt, const double* __restrict__ pn, const double* __restrict__ po,
+                      double* __restrict__ chi, double* __restrict__ mx) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    double c = 0.0, dp = 0.0;
+    if (e < n) {
+        double rate = 0.0;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) {
+            const int f = e2f[6 * (int64_t)e + s];
+            const double o = (f2e[2 * f] == e ? 1.0 : -1.0) * q[f];
+            rate += o > 0.0 ? o : 0.0;
+        }
+        c = rate * dt / (vol[e] * (phi ? phi[e] : phi_s));
+        if (chi) chi[e] = c;
+        if (pn && po) dp = fabs(pn[e] - po[e]);
+    }
+    c = warp_max(c);
+    dp = warp_max(dp);
+    if ((threadIdx.x & 31) == 0) {
+        atomic_max_nonneg(mx, c);
+        atomic_max_nonneg(mx + 1, dp);
+    }
+}
+
 void alloc_rows(Ctx* c, Csr& M, int32_t rows, int32_t cols, const DevBuf<int32_t>& cnt) {
     M.n_rows = rows;
     M.n_cols = cols;
@@ -574,6 +650,42 @@ void update_accumulation(Ctx* c, const Csr& A_cc_steady, const double* acc, cons
         check_launch("k_accum_rhs");
     }
     csr_sub(c, A_cc_steady, D, 0.0, A_cc);
+}
+
+}  // namespace edfa
+
+namespace edfa {
+
+void face_fluxes(Ctx* c, const edfa_hex_grid& g, const int32_t* fidx, const double* fval, const double* Bi,
+                 const double* rs, const double* dg, const double* pi, const double* p, double* q) {
+    const int n = g.n_cells, nf = g.n_faces;
+    require(n > 0 && nf > 0 && g.elem_to_faces && g.face_to_elems && g.face_local && fidx && fval && Bi && rs &&
+                dg && pi && p && q,
+            EDFA_ERR_VALUE, "NULL grid, element operators or vectors");
+    DevBuf<double> pf(c, nf), q1(c, 6 * (size_t)n), lam(c, 6 * (size_t)n);
+    Prof pr(c, "asm_fluxes", 8.0 * (nf * 4 + n * 60));
+    k_face_pressures<<<ceil_div(nf, 256), 256, 0, c->stream>>>(nf, fidx, fval, pi, pf.p);
+    k_cell_flux<<<ceil_div(n, 128), 128, 0, c->stream>>>(n, g.elem_to_faces, pf.p, p, Bi, rs, dg, q1.p, lam.p);
+    k_face_flux<<<ceil_div(nf, 256), 256, 0, c->stream>>>(nf, n, g.face_to_elems, g.face_local, q1.p, lam.p, dg, q);
+    check_launch("face fluxes");
+}
+
+void cfl(Ctx* c, const edfa_hex_grid& g, const double* q, const double* vol, const double* phi, double phi_s,
+         double dt, const double* pn, const double* po, double* chi, double* out_host) {
+    const int n = g.n_cells;
+    require(n > 0 && g.elem_to_faces && g.face_to_elems && q && vol && out_host, EDFA_ERR_VALUE,
+            "NULL grid or vectors");
+    require(phi || phi_s > 0.0, EDFA_ERR_VALUE, "porosity must lie in (0, 1]");
+    double* mx = c->d_scalar_d + 4000;
+    EDFA_CUDA(cudaMemsetAsync(mx, 0, 2 * sizeof(double), c->stream));
+    {
+        Prof pr(c, "asm_cfl", 8.0 * (n * 10));
+        k_cfl<<<ceil_div(n, 256), 256, 0, c->stream>>>(n, g.elem_to_faces, g.face_to_elems, q, vol, phi, phi_s, dt,
+                                                       pn, po, chi, mx);
+        check_launch("k_cfl");
+    }
+    EDFA_CUDA(cudaMemcpyAsync(out_host, mx, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 }  // namespace edfa

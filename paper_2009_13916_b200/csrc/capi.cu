@@ -687,6 +687,24 @@ int edfa_assemble(edfa_ctx* ctx, const edfa_hex_grid* grid, const edfa_assembly_
     API_END
 }
 
+int edfa_face_fluxes(edfa_ctx* ctx, const edfa_hex_grid* grid, const int32_t* face_index, const double* face_value,
+                     const double* binv, const double* row_sums, const double* diag, const double* pi_reduced,
+                     const double* p, double* q_out) {
+    API_BEGIN
+    require(ctx && grid, EDFA_ERR_VALUE, "NULL argument");
+    face_fluxes(&ctx->c, *grid, face_index, face_value, binv, row_sums, diag, pi_reduced, p, q_out);
+    API_END
+}
+
+int edfa_cfl(edfa_ctx* ctx, const edfa_hex_grid* grid, const double* q, const double* elem_volume,
+             const double* porosity, double porosity_scalar, double dt, const double* p_new, const double* p_old,
+             double* chi_out, double* max_out) {
+    API_BEGIN
+    require(ctx && grid, EDFA_ERR_VALUE, "NULL argument");
+    cfl(&ctx->c, *grid, q, elem_volume, porosity, porosity_scalar, dt, p_new, p_old, chi_out, max_out);
+    API_END
+}
+
 int edfa_update_accumulation(edfa_ctx* ctx, const edfa_csr* A_cc_steady, const double* accumulation,
                              const double* rhs_c_base, const double* p_prev, double dt, edfa_csr** A_cc,
                              double* rhs_c) {

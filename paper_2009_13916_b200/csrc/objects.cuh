@@ -242,4 +242,8 @@ void assemble(Ctx* c, const edfa_hex_grid& g, const edfa_assembly_in& in, edfa_a
               Csr& A_fc, Csr& A_cf, Csr& A_cc);
 void update_accumulation(Ctx* c, const Csr& A_cc_steady, const double* acc, const double* rhs_c_base,
                          const double* p_prev, double dt, Csr& A_cc, double* rhs_c);
+void face_fluxes(Ctx* c, const edfa_hex_grid& g, const int32_t* fidx, const double* fval, const double* Bi,
+                 const double* rs, const double* dg, const double* pi, const double* p, double* q);
+void cfl(Ctx* c, const edfa_hex_grid& g, const double* q, const double* vol, const double* phi, double phi_s,
+         double dt, const double* pn, const double* po, double* chi, double* out_host);
 }  // namespace edfa

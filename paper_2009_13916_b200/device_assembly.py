@@ -41,9 +41,10 @@ class DeviceBlockSystem:
     dirichlet_values: np.ndarray
     dt: float
     grid: object
-    binv: torch.Tensor | None = None      # [36][n_cells] (SoA) when requested
+    binv: torch.Tensor | None = None      # [36][n_cells] (SoA)
     row_sums: torch.Tensor | None = None  # [6][n_cells]
     diag: torch.Tensor | None = None      # [6][n_cells]
+    dev: dict | None = None               # device grid arrays + per-face boundary values
 
     @property
     def A_ff(self) -> DeviceCsr:
@@ -103,7 +104,7 @@ def face_conditions(grid, bc):
 
 
 def assemble_device(grid, field, props, bc, dt: float, p_prev=None, source=None,
-                    element_ops: bool = False) -> DeviceBlockSystem:
+                    element_ops: bool = True) -> DeviceBlockSystem:
     """Block system for one step (``dt=math.inf``: steady) assembled on the
     device -- hexflow's ``assemble`` (hx/assembly.py:186-311)."""
     if not dt > 0:
@@ -146,8 +147,11 @@ def assemble_device(grid, field, props, bc, dt: float, p_prev=None, source=None,
     ds = DeviceSystem(A_ff, A_fc, A_cf, A_cc, rhs=torch.cat([rhs_f, rhs_c_base]),
                       topology_src=(e2f, f2e, fidx))
     ds.set_grid(grid.nx, grid.ny, grid.nz)
+    phi = np.broadcast_to(np.asarray(getattr(props, "porosity", 0.2), float), (n_e,))
+    dev = dict(coords=coords, e2n=e2n, e2f=e2f, f2e=f2e, floc=floc, area=area, bc_val=bc_val,
+               porosity=_dev(np.ascontiguousarray(phi), torch.float64), n_nodes=coords.shape[0])
     out_sys = DeviceBlockSystem(ds, A_cc, rhs_f, rhs_c_base, rhs_c_base, acc, vol, fidx, dfaces, dvals,
-                                math.inf, grid, *ops)
+                                math.inf, grid, *ops, dev=dev)
     if math.isinf(dt):
         return out_sys
     return update_accumulation_device(out_sys, dt, p_prev)
@@ -173,3 +177,82 @@ def update_accumulation_device(system: DeviceBlockSystem, dt: float, p_prev=None
     g = system.grid
     ds.set_grid(g.nx, g.ny, g.nz)
     return replace(system, system=ds, rhs_c=rhs_c, dt=dt)
+
+
+def _grid_desc(system: DeviceBlockSystem) -> L.HexGridDesc:
+    d = system.dev
+    return L.HexGridDesc(system.n_cells, system.face_index.numel(), d["n_nodes"],
+                         dptr(d["coords"]), dptr(d["e2n"]), dptr(d["e2f"]), dptr(d["f2e"]), dptr(d["floc"]),
+                         dptr(d["area"]))
+
+
+def recover_face_fluxes_device(system: DeviceBlockSystem, x) -> torch.Tensor:
+    """Per-face fluxes at the solution x = [pi; p], positive out of the owning
+    cell (hx/assembly.py:334-356), on the device."""
+    if system.binv is None or system.dev is None:
+        raise ValueError("the system was assembled without element operators")
+    nf = system.n_free_faces
+    x = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+    x = x.to(device="cuda", dtype=torch.float64).contiguous()
+    pi, p = x[:nf], x[nf:]
+    q = torch.empty(system.face_index.numel(), dtype=torch.float64, device="cuda")
+    g = _grid_desc(system)
+    L.check(L.lib().edfa_face_fluxes(ctx(), C.byref(g), dptr(system.face_index), dptr(system.dev["bc_val"]),
+                                     dptr(system.binv), dptr(system.row_sums), dptr(system.diag), dptr(pi),
+                                     dptr(p), dptr(q)))
+    return q
+
+
+def cfl_device(system: DeviceBlockSystem, q: torch.Tensor, dt: float, p_new=None, p_old=None):
+    """chi per cell (hx/driver.py:67-71) plus max chi and max |p_new - p_old|."""
+    chi = torch.empty(system.n_cells, dtype=torch.float64, device="cuda")
+    out = (C.c_double * 2)()
+    g = _grid_desc(system)
+    L.check(L.lib().edfa_cfl(ctx(), C.byref(g), dptr(q), dptr(system.elem_volume), dptr(system.dev["porosity"]),
+                             0.0, float(dt), None if p_new is None else dptr(p_new),
+                             None if p_old is None else dptr(p_old), dptr(chi), out))
+    return chi, out[0], out[1]
+
+
+def next_dt(dt: float, dt_max: float, dt_mult: float, dp_target: float, dp_max: float) -> float:
+    """TimestepController's rule (hx/driver.py:50-53)."""
+    ratio = dt_mult if dp_max <= 0 else min(dt_mult, dp_target / dp_max)
+    return min(dt * ratio, dt_max)
+
+
+def run_transient_device(grid, field, props, bc, *, p_init: float, dt0: float, dt_max: float, dt_mult: float,
+                         dp_target: float, n_step: int, precond: dict, tol: float = 1e-8, max_it: int = 2000,
+                         restart: int = 50):
+    """hx/driver.py:169-230 (``run_transient``) with every array on the device:
+    stage 1 once, per step update_accumulation + stage-2 refresh + GMRES, flux
+    recovery, CFL and the pressure-change step control.  Returns per-step
+    records (dt, iterations, relres, cfl_max, dp_max)."""
+    from .device import system_operator
+    from .krylov import gmres
+    from .precond import BlockLDUPreconditioner, DynamicConfig, patterns_for
+    n = grid.n_elems
+    p = torch.full((n,), float(p_init), dtype=torch.float64, device="cuda")
+    base = assemble_device(grid, field, props, bc, dt0, p)
+    opts = dict(precond)
+    kind = opts.pop("pattern", "static")
+    proto = opts.pop("prototype", "A")
+    n_add, n_ent = opts.pop("n_add", 1), opts.pop("n_ent", 4)
+    if kind == "dynamic":
+        pre = BlockLDUPreconditioner.build(base.system, dynamic=DynamicConfig(n_add, n_ent), **opts)
+    else:
+        pre = BlockLDUPreconditioner.build(base.system, patterns=patterns_for(base.system, kind, proto), **opts)
+    dt, steps = float(dt0), []
+    for step in range(n_step):
+        s = base if step == 0 else update_accumulation_device(base, dt, p)
+        if step:
+            pre.refresh(s.system)
+        x, rep = gmres(system_operator(s.system), pre, s.rhs(), tol=tol, restart=restart, max_it=max_it)
+        nf = s.n_free_faces
+        p_new = x[nf:]
+        q = recover_face_fluxes_device(s, x)
+        _, chi_max, dp_max = cfl_device(s, q, dt, p_new, p)
+        steps.append(dict(step=step + 1, dt=dt, n_it=rep.n_it, converged=rep.converged,
+                          relres=rep.final_relres, cfl_max=chi_max, dp_max=dp_max))
+        dt = next_dt(dt, dt_max, dt_mult, dp_target, dp_max)
+        p = p_new
+    return steps, x

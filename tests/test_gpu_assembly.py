@@ -167,3 +167,62 @@ def test_errors(dev):
                        g.face_area, g.elem_volume)
     with pytest.raises(ValueError, match="non-positive Jacobian"):
         dev.assemble_device(bad, fld, mesh.RockProps(), mesh.Boundaries(pressure_planes={"x-": 1.0}), math.inf)
+
+
+@pytest.mark.parametrize("name", ["config2_n6", "config3_n5"])
+def test_device_fluxes_and_cfl_match_reference(dev, name):
+    """recover_face_fluxes / cfl on the device against the reference's outputs
+    (tests/golden/flux_*.npz, made by the unmodified reference) and the
+    pinned oracle."""
+    from conftest import golden as _golden
+    from oracle import edfa_oracle as O
+    d = _golden("flux_" + name)
+    if name == "config2_n6":
+        g, fld, props, bc, _, _ = host_inputs(2, n=6)
+    else:
+        g, fld, props, bc, _, _ = host_inputs(3, n=5)
+    dt = float(d["dt"])
+    ds = dev.assemble_device(g, fld, props, bc, dt, d["p_prev"])
+    q = dev.recover_face_fluxes_device(ds, d["x"])
+    vec_close(q, d["q"], 1e-12)
+    nf = ds.n_free_faces
+    p_new = torch.from_numpy(d["x"][nf:]).cuda()
+    p_old = torch.from_numpy(np.ascontiguousarray(d["p_prev"])).cuda()
+    chi, chi_max, dp_max = dev.cfl_device(ds, q, dt, p_new, p_old)
+    chi_ref = O.cfl(g.elem_to_faces, g.face_to_elems, d["q"], g.elem_volume, 0.2, dt)
+    vec_close(chi, chi_ref, 1e-12)
+    assert chi_max == pytest.approx(float(chi_ref.max()), rel=1e-12)
+    assert dp_max == float(d["dp_max"])
+
+
+def test_device_transient_loop_matches_oracle(dev):
+    """hx/driver.py run_transient on the device (assembly, refresh, GMRES,
+    fluxes, CFL, pressure-change step control) against the same loop driven
+    by the oracle on the host."""
+    from oracle import edfa_oracle as O
+    g, fld, props, bc, _, _ = host_inputs(4, dims=(6, 10, 5))
+    kw = dict(p_init=140.0, dt0=0.1, dt_max=5.0, dt_mult=1.1, dp_target=5.0, n_step=4)
+    steps, _ = dev.run_transient_device(g, fld, props, bc, precond=dict(pattern="static", prototype="A",
+                                                                        no_fill=True), **kw)
+    p = np.full(g.n_elems, 140.0)
+    dt = 0.1
+    base = assembly.assemble(g, fld, props, bc, dt, p)
+    o1 = O.build_stage1(base.A_ff, base.A_fc, base.A_cf, sets=O.static_sets(g, base.face_index, "A"),
+                        no_fill=True)
+    for st in steps:
+        s = assembly.update_accumulation(base, dt, p)
+        o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
+        A, b = s.full_matrix(), s.rhs()
+        x, r = O.gmres(lambda v: A @ v, lambda v: O.apply(o1, o2, s.A_fc, s.A_cf, v), b, tol=1e-8, restart=50)
+        assert st["dt"] == pytest.approx(dt, rel=1e-12)
+        assert abs(st["n_it"] - r.n_it) <= 2 and st["converged"]
+        pi, pn = s.split(x)
+        pif = O.face_pressures(g.n_faces, s.free_faces, s.dirichlet_faces, s.dirichlet_values, pi)
+        q = O.recover_face_fluxes(g.elem_to_faces, g.face_to_elems, g.face_local, s.ops.Binv, s.ops.row_sums,
+                                  s.ops.diag, pif, pn)
+        chi = O.cfl(g.elem_to_faces, g.face_to_elems, q, g.elem_volume, 0.2, dt)
+        assert st["cfl_max"] == pytest.approx(float(chi.max()), rel=1e-6)
+        dp = float(np.abs(pn - p).max())
+        assert st["dp_max"] == pytest.approx(dp, rel=1e-6)
+        dt = O.next_dt(dt, 5.0, 1.1, 5.0, dp)
+        p = pn
