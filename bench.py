@@ -312,6 +312,7 @@ def run_edfa(args):
         # once, then per time step update_accumulation (A_cc + diag(acc/dt), rhs_c)
         # on the device, stage-2 refresh and GMRES from the previous pressure
         from paper_2009_13916_b200.device import DeviceCsr
+        from paper_2009_13916_b200.device_assembly import next_dt
         m = case.meta
         n_systems = int(m["n_steps"])
         acc_d = torch.from_numpy(np.ascontiguousarray(s.accumulation)).to(dev)
@@ -324,11 +325,11 @@ def run_edfa(args):
             system_dev = DeviceSystem(*blocks, rhs=b, host=s, topology_src=topo_src)
             pre = build_pre(case, system_dev)         # stage 1 + stage 2 of the first system
             dt, x, reps_seq = float(m["dt0"]), None, []
+            p_prev = torch.full((s.n_cells,), float(m["p_init"]), dtype=torch.float64, device=dev)
             for k in range(n_systems):
                 if k == 0:
                     sk = system_dev
                 else:
-                    p_prev = x[nf:]
                     rhs_c = torch.empty_like(rcb_d)
                     h = ctypes.c_void_p()
                     _lib.check(lib.edfa_update_accumulation(c, Acc_steady.handle, acc_d.data_ptr(),
@@ -340,7 +341,10 @@ def run_edfa(args):
                 x, rep = gmres(system_operator(sk), pre, sk.rhs(), tol=case.rtol, restart=case.restart,
                                max_it=case.max_it)
                 reps_seq.append(rep)
-                dt = min(dt * float(m["dt_mult"]), float(m["dt_max"]))
+                # TimestepController (hx/driver.py:50-53): dt * min(mult, dp_target / dp_max), capped
+                dp_max = float((x[nf:] - p_prev).abs().max())
+                dt = next_dt(dt, float(m["dt_max"]), float(m["dt_mult"]), float(m["dp_target"]), dp_max)
+                p_prev = x[nf:]
             rep.seq_iterations = [r.n_it for r in reps_seq]
             rep.seq_relres = max(r.final_relres for r in reps_seq)
             return x, rep, pre
@@ -426,10 +430,15 @@ def run_edfa(args):
         s_k = s_pin
         if n_systems > 1:   # the time-step sequence as a host application drives it
             from paper_2009_13916_b200 import assembly as host_asm
-            dt = float(case.meta["dt0"])
+            from paper_2009_13916_b200.device_assembly import next_dt
+            m = case.meta
+            dt, p_prev_h = float(m["dt0"]), np.full(s.n_cells, float(m["p_init"]))
             for q in range(1, n_systems):
-                dt = min(dt * float(case.meta["dt_mult"]), float(case.meta["dt_max"]))
-                s_k = host_asm.update_accumulation(s_pin, dt, x_h[s.n_free_faces:])   # host A_cc, rhs_c
+                p_new_h = x_h[s.n_free_faces:]
+                dt = next_dt(dt, float(m["dt_max"]), float(m["dt_mult"]), float(m["dp_target"]),
+                             float(np.abs(p_new_h - p_prev_h).max()))
+                p_prev_h = p_new_h
+                s_k = host_asm.update_accumulation(s_pin, dt, p_new_h)                # host A_cc, rhs_c
                 pre_h.refresh(s_k)                                                   # H2D of A_cc
                 x_h, rep_h = gmres(system_operator(pre_h.device_system), pre_h, s_k.rhs(), tol=case.rtol,
                                    restart=case.restart, max_it=case.max_it)
