@@ -81,8 +81,8 @@ class DeviceBlockSystem:
 def _dev(a, dtype) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device="cuda", dtype=dtype).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.dtype(str(dtype).split(".")[-1]))) \
-        .to("cuda", non_blocking=True)
+    a = np.require(np.asarray(a), dtype=np.dtype(str(dtype).split(".")[-1]), requirements=["C", "W"])
+    return torch.from_numpy(a).to("cuda", non_blocking=True)
 
 
 def face_conditions(grid, bc):
