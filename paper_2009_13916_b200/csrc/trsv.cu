@@ -10,6 +10,7 @@
 // entries its row depends on -- the solution vector is sentinel-initialised,
 // so the value is its own ready flag -- and publishes its own entry.
 #include <cub/cub.cuh>
+#include <climits>
 
 #include "dev_util.cuh"
 #include "edfa_internal.cuh"
@@ -436,6 +437,26 @@ __global__ void __launch_bounds__(256) k_trsv_wsf(const int* __restrict__ perm, 
         const int s = slot >> 5, rr = slot & 31;
         const int64_t b0 = sptr[s];
         const int w = (int)((sptr[s + 1] - b0) / 32);
+        // the dependency nearest to the row (for natural-order stencils the
+        // last one finished) is polled by one lane; the rest are read once it
+        // is present, so ~1 poll stream per row instead of one per entry
+        int near = INT_MAX, near_c = -1;
+        for (int k = lane; k < w; k += 32) {
+            const int cidx = __ldg(col + b0 + 32 * (int64_t)k + rr);
+            if (cidx >= 0 && abs(cidx - r) < near) { near = abs(cidx - r); near_c = cidx; }
+        }
+        int best = near;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+        const unsigned who = __ballot_sync(0xffffffffu, near == best && near_c >= 0);
+        if (who && lane == __ffs(who) - 1) {
+            long long spins = 0;
+            while (is_sentinel(ld_relaxed(x + near_c))) {
+                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); break; }
+                __nanosleep(20);
+            }
+        }
+        __syncwarp();
         double acc = 0.0;
         for (int k = lane; k < w; k += 32) {
             const int cidx = __ldg(col + b0 + 32 * (int64_t)k + rr);
