@@ -437,38 +437,69 @@ __global__ void __launch_bounds__(256) k_trsv_wsf(const int* __restrict__ perm, 
         const int s = slot >> 5, rr = slot & 31;
         const int64_t b0 = sptr[s];
         const int w = (int)((sptr[s + 1] - b0) / 32);
-        // the dependency nearest to the row (for natural-order stencils the
-        // last one finished) is polled by one lane; the rest are read once it
-        // is present, so ~1 poll stream per row instead of one per entry
-        int near = INT_MAX, near_c = -1;
-        for (int k = lane; k < w; k += 32) {
-            const int cidx = __ldg(col + b0 + 32 * (int64_t)k + rr);
-            if (cidx >= 0 && abs(cidx - r) < near) { near = abs(cidx - r); near_c = cidx; }
-        }
-        int best = near;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
-        const unsigned who = __ballot_sync(0xffffffffu, near == best && near_c >= 0);
-        if (who && lane == __ffs(who) - 1) {
-            long long spins = 0;
-            while (is_sentinel(ld_relaxed(x + near_c))) {
-                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); break; }
-                __nanosleep(20);
-            }
-        }
-        __syncwarp();
+        // pass 1: every lane loads its coefficients and the current values of
+        // its dependencies (most are final long before the row is taken); the
+        // missing dependency nearest to the row -- for natural-order stencils
+        // the last one to finish -- is polled by one lane, the others are
+        // re-read only if they were missing too
+        constexpr int PL = 4;                       // entries per lane held in registers
         double acc = 0.0;
-        for (int k = lane; k < w; k += 32) {
-            const int cidx = __ldg(col + b0 + 32 * (int64_t)k + rr);
-            if (cidx < 0) continue;
-            const double v = __ldg(val + b0 + 32 * (int64_t)k + rr);
-            double xv = ld_relaxed(x + cidx);
-            long long spins = 0;
-            while (is_sentinel(xv)) {
-                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv = 0.0; break; }
-                xv = ld_relaxed(x + cidx);
+        if (w <= 32 * PL) {
+            int cc[PL];
+            double vv[PL], xv[PL];
+            int near = INT_MAX, near_u = -1;
+#pragma unroll
+            for (int u = 0; u < PL; ++u) {
+                const int k = lane + 32 * u;
+                cc[u] = k < w ? __ldg(col + b0 + 32 * (int64_t)k + rr) : -1;
+                vv[u] = cc[u] >= 0 ? __ldg(val + b0 + 32 * (int64_t)k + rr) : 0.0;
             }
-            acc = fma(-v, xv, acc);
+#pragma unroll
+            for (int u = 0; u < PL; ++u) {
+                xv[u] = cc[u] >= 0 ? ld_relaxed(x + cc[u]) : 0.0;
+                if (cc[u] >= 0 && is_sentinel(xv[u]) && abs(cc[u] - r) < near) { near = abs(cc[u] - r); near_u = u; }
+            }
+            int best = near;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+            if (best != INT_MAX) {
+                const unsigned who = __ballot_sync(0xffffffffu, near == best);
+                if (lane == __ffs(who) - 1) {
+#pragma unroll
+                    for (int u = 0; u < PL; ++u)
+                        if (u == near_u) {
+                            long long spins = 0;
+                            while (is_sentinel(xv[u] = ld_relaxed(x + cc[u]))) {
+                                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv[u] = 0.0; break; }
+                                __nanosleep(20);
+                            }
+                        }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < PL; ++u) {
+                    long long spins = 0;
+                    while (cc[u] >= 0 && is_sentinel(xv[u])) {
+                        if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv[u] = 0.0; break; }
+                        xv[u] = ld_relaxed(x + cc[u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < PL; ++u) acc = fma(-vv[u], xv[u], acc);
+        } else {
+            for (int k = lane; k < w; k += 32) {
+                const int cidx = __ldg(col + b0 + 32 * (int64_t)k + rr);
+                if (cidx < 0) continue;
+                const double v = __ldg(val + b0 + 32 * (int64_t)k + rr);
+                double xk = ld_relaxed(x + cidx);
+                long long spins = 0;
+                while (is_sentinel(xk)) {
+                    if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xk = 0.0; break; }
+                    xk = ld_relaxed(x + cidx);
+                }
+                acc = fma(-v, xk, acc);
+            }
         }
         acc = warp_sum(acc);
         if (lane == 0) {
