@@ -545,16 +545,17 @@ __global__ void __launch_bounds__(256) k_trsv_tsf(const int* __restrict__ perm, 
             vv[u] = in ? __ldg(val + b0 + (int64_t)u * 32 + lane) : 0.0;
         }
         double acc = alpha * __ldg(b + r);
+        double xv[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) xv[u] = cc[u] >= 0 ? ld_relaxed(x + cc[u]) : 0.0;   // all in flight at once
 #pragma unroll
         for (int u = 0; u < K; ++u) {
-            if (cc[u] < 0) continue;
-            double xv = ld_relaxed(x + cc[u]);
             long long spins = 0;
-            while (is_sentinel(xv)) {
-                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv = 0.0; break; }
-                xv = ld_relaxed(x + cc[u]);
+            while (cc[u] >= 0 && is_sentinel(xv[u])) {
+                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv[u] = 0.0; break; }
+                xv[u] = ld_relaxed(x + cc[u]);
             }
-            acc = fma(-vv[u], xv, acc);
+            acc = fma(-vv[u], xv[u], acc);
         }
         const double xr = acc * dinv[s * 32 + lane];
         atomicAdd(reinterpret_cast<unsigned long long*>(x + r),
