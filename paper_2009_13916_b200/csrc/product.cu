@@ -162,7 +162,9 @@ __global__ void __launch_bounds__(256) k_product(ProdArgs a) {
             for (int i = lane; i < nH; i += 32) ss += tv[i] * tv[i];
             thr = a.tau * sqrt(warp_sum(ss));
         }
-        const long long o = MODE == FILL ? (long long)a.Hp[m] : MODE == PADDED ? (long long)m * a.cap : 0;
+        const long long o = MODE == FILL     ? (long long)a.Hp[m]
+                            : MODE == PADDED ? (long long)(a.rows ? it : m) * a.cap
+                                             : 0;
         int n = 0;
         for (int i0 = 0; i0 < nH; i0 += 32) {
             int i = i0 + lane;
@@ -204,6 +206,21 @@ __global__ void k_unpad(const int32_t* __restrict__ cnt, const int32_t* __restri
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= n) return;
     const int c = cnt[w], o = Hp[w];
+    const size_t src = (size_t)w * cap;
+    for (int i = lane; i < c; i += 32) {
+        Hi[o + i] = pi[src + i];
+        Hv[o + i] = pv[src + i];
+    }
+}
+
+// rows of a re-run list, padded by list position
+__global__ void k_unpad_list(const int32_t* __restrict__ rows, int nl, const int32_t* __restrict__ cnt,
+                             const int32_t* __restrict__ Hp, int cap, const int32_t* __restrict__ pi,
+                             const double* __restrict__ pv, int32_t* __restrict__ Hi, double* __restrict__ Hv) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= nl) return;
+    const int m = rows[w];
+    const int c = cnt[m], o = Hp[m];
     const size_t src = (size_t)w * cap;
     for (int i = lane; i < c; i += 32) {
         Hi[o + i] = pi[src + i];
@@ -254,16 +271,39 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
         launch_product<8, PADDED>(c, a);
         ovf_rows = read_overflow(c, ovf.p);
     }
-    DevBuf<int32_t> rows(c, std::max<size_t>(ovf_rows.size(), 1));
+    // rows longer than 128 entries: 1024-slot tables into a second padded
+    // buffer (by list position); rows beyond that: 4096-slot count + fill
+    constexpr int CAP2 = 512;
+    DevBuf<int32_t> rows1(c, std::max<size_t>(ovf_rows.size(), 1)), rows2(c, 1);
+    DevBuf<int32_t> pi2;
+    DevBuf<double> pv2;
+    std::vector<int32_t> ovf2;
     ProdArgs b = a;
-    if (!ovf_rows.empty()) {   // wide rows: count with 4096-slot tables
-        EDFA_CUDA(cudaMemcpyAsync(rows.p, ovf_rows.data(), sizeof(int) * ovf_rows.size(), cudaMemcpyHostToDevice,
+    if (!ovf_rows.empty()) {
+        EDFA_CUDA(cudaMemcpyAsync(rows1.p, ovf_rows.data(), sizeof(int) * ovf_rows.size(), cudaMemcpyHostToDevice,
                                   c->stream));
-        b.rows = rows.p;
+        pi2.reset(c, ovf_rows.size() * CAP2);
+        pv2.reset(c, ovf_rows.size() * CAP2);
+        b.rows = rows1.p;
         b.n_list = (int32_t)ovf_rows.size();
+        b.cap = CAP2;
+        b.Hi = pi2.p;
+        b.Hv = pv2.p;
         EDFA_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c->stream));
         Prof pr(c, "product_wide", 12.0 * (G.nnz + A.nnz + F.nnz) * b.n_list / std::max(n, 1));
-        launch_product<12, COUNT>(c, b);
+        launch_product<10, PADDED>(c, b);
+        ovf2 = read_overflow(c, ovf.p);
+    }
+    ProdArgs b3 = a;
+    if (!ovf2.empty()) {
+        rows2.reset(c, ovf2.size());
+        EDFA_CUDA(cudaMemcpyAsync(rows2.p, ovf2.data(), sizeof(int) * ovf2.size(), cudaMemcpyHostToDevice,
+                                  c->stream));
+        b3.rows = rows2.p;
+        b3.n_list = (int32_t)ovf2.size();
+        EDFA_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c->stream));
+        Prof pr(c, "product_wide", 12.0 * (G.nnz + A.nnz + F.nnz) * b3.n_list / std::max(n, 1));
+        launch_product<12, COUNT>(c, b3);
         require(read_overflow(c, ovf.p).empty(), EDFA_ERR_UNSUPPORTED, "H~ row exceeds 4096 distinct columns");
     }
     H.nnz = scan_counts(c, cnt.p, H.ptr.p, n);
@@ -276,12 +316,18 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
         check_launch("k_unpad");
     }
     if (!ovf_rows.empty()) {
-        b.Hp = H.ptr.p;
-        b.Hi = H.idx.p;
-        b.Hv = H.val.p;
+        const int nl = (int)ovf_rows.size();
+        k_unpad_list<<<ceil_div((int64_t)nl * 32, 256), 256, 0, c->stream>>>(rows1.p, nl, cnt.p, H.ptr.p, CAP2, pi2.p,
+                                                                            pv2.p, H.idx.p, H.val.p);
+        check_launch("k_unpad_list");
+    }
+    if (!ovf2.empty()) {
+        b3.Hp = H.ptr.p;
+        b3.Hi = H.idx.p;
+        b3.Hv = H.val.p;
         EDFA_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c->stream));
-        Prof pr(c, "product_wide", 12.0 * (G.nnz + A.nnz + F.nnz) * b.n_list / std::max(n, 1));
-        launch_product<12, FILL>(c, b);
+        Prof pr(c, "product_wide", 12.0 * (G.nnz + A.nnz + F.nnz) * b3.n_list / std::max(n, 1));
+        launch_product<12, FILL>(c, b3);
         require(read_overflow(c, ovf.p).empty(), EDFA_ERR_UNSUPPORTED, "H~ row exceeds 4096 distinct columns");
     }
 }
