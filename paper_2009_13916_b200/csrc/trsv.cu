@@ -594,7 +594,14 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
             EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_trsv_wsf, 256, 0));
             grid_sf = NUM_SMS_B200 * std::max(1, occ);
         }
-        if (p.max_w > 16 || getenv("EDFA_TRSV_WARP_ROWS")) {
+        // thread per row while rows fit 32 registers' worth of dependencies and
+        // levels are wide enough to fill the warps; warp per row otherwise
+        const bool wide_levels = (int64_t)p.n >= 1024ll * std::max(p.n_levels, 1);
+        if (p.max_w > 16 && p.max_w <= 32 && wide_levels && !getenv("EDFA_TRSV_WARP_ROWS")) {
+            k_trsv_tsf<32><<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p,
+                                                           p.n_slots / 32, p.ticket.p, b, alpha, x, add, out2, err);
+            check_launch("k_trsv_tsf");
+        } else if (p.max_w > 16 || getenv("EDFA_TRSV_WARP_ROWS")) {
             k_trsv_wsf<<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p,
                                                        p.n_slots, p.ticket.p, b, alpha, x, add, out2, err);
             check_launch("k_trsv_wsf");
