@@ -3,7 +3,8 @@
 //
 // Row-wise Gustavson, one warp per cell row m, two passes (count, fill):
 //   W_m = sum_{i in G_m, ascending} g_mi * A_ff[i, :]    (scipy csr_matmat order)
-//   H_m = sum_{k in W_m, ascending} W_mk * F~[k, :]
+//   H_m = sum_{k in W_m} W_mk * F~[k, :], k in reverse first-encounter order
+//         (the unsorted row order csr_matmat emits W in)
 // Both accumulators are shared-memory open-addressing tables; each
 // accumulation step adds the contributions of ONE source entry, whose target
 // columns are distinct, so lanes never collide and every sum is formed in a
@@ -20,16 +21,17 @@ constexpr int EMPTY = -1;
 
 __device__ __forceinline__ unsigned hslot(int key, int bits) { return ((unsigned)key * 2654435761u) >> (32 - bits); }
 
-// find-or-insert; returns slot or -1 when the table is full
-__device__ int h_insert(int* keys, int bits, int key) {
+// find-or-insert; returns slot or -1 when the table is full (*fresh: inserted now)
+__device__ int h_insert(int* keys, int bits, int key, bool* fresh = nullptr) {
     int mask = (1 << bits) - 1;
     unsigned s = hslot(key, bits);
     for (int t = 0; t <= mask; ++t) {
         int cur = keys[s];
-        if (cur == key) return (int)s;
+        if (cur == key) { if (fresh) *fresh = false; return (int)s; }
         if (cur == EMPTY) {
             int prev = atomicCAS(&keys[s], EMPTY, key);
-            if (prev == EMPTY || prev == key) return (int)s;
+            if (prev == EMPTY) { if (fresh) *fresh = true; return (int)s; }
+            if (prev == key) { if (fresh) *fresh = false; return (int)s; }
         }
         s = (s + 1) & mask;
     }
@@ -112,21 +114,44 @@ __global__ void __launch_bounds__(256) k_product(ProdArgs a) {
         for (int i = lane; i < T; i += 32) { tk[i] = EMPTY; tv[i] = 0.0; hk[i] = EMPTY; hv[i] = 0.0; }
         __syncwarp();
         bool full = false;
-        // ---- W = g_m A_ff
+        // ---- W = g_m A_ff; wk records the slots in first-encounter order
         int g0 = a.G.ptr[m], g1 = a.G.ptr[m + 1];
+        int nW = 0;
         for (int t = g0; t < g1; ++t) {
             int i = a.G.idx[t];
             double g = a.G.val[t];
-            for (int e = a.A.ptr[i] + lane; e < a.A.ptr[i + 1]; e += 32) {
-                int s = h_insert(tk, BITS, a.A.idx[e]);
-                if (s < 0) full = true;
-                else tv[s] = add_mul(tv[s], g, a.A.val[e]);
+            const int e0 = a.A.ptr[i], e1 = a.A.ptr[i + 1];
+            for (int eb = e0; eb < e1; eb += 32) {
+                const int e = eb + lane;
+                bool fresh = false;
+                int s = -1;
+                if (e < e1) {
+                    s = h_insert(tk, BITS, a.A.idx[e], &fresh);
+                    if (s < 0) full = true;
+                    else tv[s] = add_mul(tv[s], g, a.A.val[e]);
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+                if (fresh && nW + __popc(bal & ((1u << lane) - 1)) < T) wk[nW + __popc(bal & ((1u << lane) - 1))] = s;
+                nW += __popc(bal);
             }
             __syncwarp();
         }
-        full = __any_sync(0xffffffffu, full);
-        int nW = 0;
-        if (!full) nW = h_extract_sorted(tk, tv, BITS, wk, wv, lane);
+        full = __any_sync(0xffffffffu, full) || nW > T;
+        // scipy's csr_matmat emits a row's columns in REVERSE first-encounter
+        // order (linked-list head insertion), and (G A_ff) F walks W that way:
+        // H sums are formed in exactly the reference's order
+        if (!full) {
+            for (int q = lane; q < nW; q += 32) hk[q] = wk[q];
+            __syncwarp();
+            for (int q = lane; q < nW; q += 32) {
+                const int sl = hk[nW - 1 - q];
+                wk[q] = tk[sl];
+                wv[q] = tv[sl];
+            }
+            __syncwarp();
+            for (int q = lane; q < nW; q += 32) hk[q] = EMPTY;
+            __syncwarp();
+        }
         // ---- H = W F
         if (!full) {
             for (int t = 0; t < nW; ++t) {

@@ -556,3 +556,35 @@ def test_narrow_row_syncfree_solver_is_bitwise_level_solver(edfa, monkeypatch):
         pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, "static", "A"), no_fill=True)
         ys.append(pre.stage1.face_inner.apply(r))
     assert np.array_equal(ys[0], ys[1])
+
+
+@pytest.mark.parametrize("fname,tag", GOLD_NOFILL)
+def test_schur_parts_bit_identical_to_reference(edfa, fname, tag):
+    """H~ = (G~ A_ff) F~ sums in scipy's order (the first product's rows in
+    csr_matmat's reverse first-encounter order), so H~ and S~ = A_cc - H~ are
+    the reference's bit for bit, roundoff-level entries included."""
+    d = golden(fname)
+    s, pre = gpu_build(edfa, d, tag)
+    for part, name in ((pre.stage1.H, "H"), (pre.stage2.S, "S")):
+        R = g_csr(d, f"{tag}_{name}")
+        assert same_csr(part, R) and np.array_equal(part.data, R.data), name
+
+
+@pytest.mark.parametrize("idx,n", [(2, 16), (3, 7), (1, 12)])
+def test_schur_parts_bit_identical_to_oracle(edfa, idx, n):
+    from paper_2009_13916_b200 import configs
+    case = configs.make(idx, n=n)
+    s = case.system
+    if case.precond["pattern"] == "dynamic":
+        pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
+        o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, dynamic=(1, 4, None), no_fill=True)
+    else:
+        kind = case.precond["pattern"]
+        pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, kind, "A"), no_fill=True)
+        sets = O.static_sets(s.grid, s.face_index, "A") if kind == "static" else None
+        o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=sets, no_fill=True)
+    o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
+    for part, ref in ((pre.stage1.H, o1.H), (pre.stage2.S, o2.S), (pre.stage2.schur_inner.L, o2.schur_inner.L),
+                      (pre.stage2.schur_inner.U, o2.schur_inner.U)):
+        ref = ref.tocsr()
+        assert same_csr(part, ref) and np.array_equal(part.data, ref.data)
