@@ -579,11 +579,11 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
         run_tile(c, const_cast<TilePlan&>(p.tile), b, alpha, x, add, out2, name);
         return;
     }
-    static const bool force_sf = getenv("EDFA_TRSV_WSF") != nullptr;
     // wide rows, or levels narrow enough that a grid barrier per level costs
     // more than the rows: sync-free warp-per-row solve
-    const bool sf = p.max_w > 16 || (int64_t)p.n < 16384ll * std::max(p.n_levels, 1) || force_sf;
-    if (sf && x != b && !getenv("EDFA_TRSV_LEVELS")) {
+    // (measured on config 3's IC at 128^3, 16k rows per level: 1.95 ms vs 4.09 ms
+    // per solve pair for the level-synchronous kernel; at 64^3 1.03 vs 1.76 ms)
+    if (x != b && !getenv("EDFA_TRSV_LEVELS")) {
         fill_bits(c, x, p.n, SENTINEL_BITS);
         EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
         int* err = c->d_scalar_i + 52;
