@@ -954,7 +954,10 @@ __device__ __forceinline__ double flow_poll_g(const double* p) {
     }
     return ld_relaxed_d(p);
 }
-constexpr int FLOW_WARPS = 12;                      // compute warps (+1 loader)
+#ifndef FLOW_WARPS_N
+#define FLOW_WARPS_N 12
+#endif
+constexpr int FLOW_WARPS = FLOW_WARPS_N;            // compute warps (+1 loader)
 constexpr int FLOW_THREADS = (FLOW_WARPS + 1) * 32;
 __device__ __forceinline__ bool is_sent_hi(double v) {   // published values are never NaN-boxed like this
     return __double2hiint(v) == (int)(SENTINEL_BITS >> 32);
