@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(PIPE_THREADS) k_tile_pipe(TileSolve a) {
 __device__ __forceinline__ double ld_vol_s(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
 __device__ __forceinline__ void st_vol_s(double* p, double v) { *reinterpret_cast<volatile double*>(p) = v; }
 #ifndef FLOW_SLEEP_NS
-#define FLOW_SLEEP_NS 16
+#define FLOW_SLEEP_NS 0    // measured: no back-off is 1 % faster with 15 compute warps
 #endif
 __device__ __forceinline__ double poll_s(const double* p, int* err) {
     double v = ld_vol_s(p);
@@ -955,7 +955,7 @@ __device__ __forceinline__ double flow_poll_g(const double* p) {
     return ld_relaxed_d(p);
 }
 #ifndef FLOW_WARPS_N
-#define FLOW_WARPS_N 12
+#define FLOW_WARPS_N 15     // 15 + loader = 512 threads at 128 registers (measured: 12 -> 15 is 141 -> 134 us)
 #endif
 constexpr int FLOW_WARPS = FLOW_WARPS_N;            // compute warps (+1 loader)
 constexpr int FLOW_THREADS = (FLOW_WARPS + 1) * 32;
