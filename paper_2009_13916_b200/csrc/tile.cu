@@ -1249,9 +1249,11 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     const int n = D.n_rows;
     if (!dims || dims[0] <= 0 || (int64_t)dims[0] * dims[1] * dims[2] != n || n == 0) return false;
     Geo g{dims[0], dims[1], dims[2], 8, 8, 8, 0, 0, 0};
-    g.tx = std::min(8, g.nx);
-    g.ty = std::min(8, g.ny);
-    g.tz = std::min(8, g.nz);
+    int td[3] = {8, 8, 8};
+    if (const char* e = getenv("EDFA_TILE_DIM")) sscanf(e, "%d,%d,%d", &td[0], &td[1], &td[2]);   // A/B only
+    g.tx = std::min(td[0], g.nx);
+    g.ty = std::min(td[1], g.ny);
+    g.tz = std::min(td[2], g.nz);
     g.NX = ceil_div(g.nx, g.tx);
     g.NY = ceil_div(g.ny, g.ty);
     g.NZ = ceil_div(g.nz, g.tz);
