@@ -34,62 +34,8 @@ namespace edfa {
 namespace {
 
 constexpr double PIVOT_GUARD = 1e-12;   // hx/sparse.py:24-25
-constexpr int HBITS = 10;
-constexpr int HSZ = 1 << HBITS;         // working-row hash slots per warp
-constexpr int HMAX = HSZ * 3 / 4;       // load limit -> EDFA_ERR_UNSUPPORTED
 constexpr int EMPTY = -1, TOMB = -2;
 constexpr int ERR_OVERFLOW = 1, ERR_SPIN = 2;
-
-struct Table {
-    int* keys;      // [HSZ]
-    double* vals;   // [HSZ]
-    int* ckey;      // [cap] compacted U candidates
-    double* cval;   // [cap]
-    int* misc;      // [4]: inserted count
-};
-
-__host__ __device__ constexpr size_t warp_bytes(int cap) {
-    return ((size_t)HSZ * 12 + (size_t)cap * 12 + 16 + 15) & ~size_t(15);
-}
-
-__device__ __forceinline__ Table table_at(unsigned char* base, int cap) {
-    Table t;
-    t.vals = reinterpret_cast<double*>(base);
-    t.cval = t.vals + HSZ;
-    t.keys = reinterpret_cast<int*>(t.cval + cap);
-    t.ckey = t.keys + HSZ;
-    t.misc = t.ckey + cap;
-    return t;
-}
-
-__device__ __forceinline__ unsigned hslot(int j) { return ((unsigned)j * 2654435761u) >> (32 - HBITS); }
-
-// slot of key j, or -1
-__device__ __forceinline__ int hfind(const Table& t, int j) {
-    unsigned s = hslot(j);
-    for (int p = 0; p < HSZ; ++p, s = (s + 1) & (HSZ - 1)) {
-        const int k = t.keys[s];
-        if (k == j) return (int)s;
-        if (k == EMPTY) return -1;
-    }
-    return -1;
-}
-
-// slot of key j, inserting it when absent (*fresh = true); -1 when full.
-// Keys inserted concurrently by the lanes of one warp are distinct.
-__device__ __forceinline__ int hinsert(const Table& t, int j, bool* fresh) {
-    unsigned s = hslot(j);
-    for (int p = 0; p < HSZ; ++p, s = (s + 1) & (HSZ - 1)) {
-        int k = t.keys[s];
-        if (k == j) { *fresh = false; return (int)s; }
-        if (k == EMPTY) {
-            k = atomicCAS(t.keys + s, EMPTY, j);
-            if (k == EMPTY) { *fresh = true; return (int)s; }
-            if (k == j) { *fresh = false; return (int)s; }
-        }
-    }
-    return -1;
-}
 
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
 #pragma unroll
@@ -100,55 +46,7 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
     return v;
 }
 
-// next pivot: smallest live key in (last, lim); returns (key << 32 | slot) or ~0
-__device__ __forceinline__ unsigned long long next_pivot(const Table& t, int last, int lim, int lane) {
-    unsigned long long best = ~0ull;
-    for (int s = lane; s < HSZ; s += 32) {
-        const int k = t.keys[s];
-        if (k > last && k < lim) {
-            unsigned long long v = ((unsigned long long)(unsigned)k << 32) | (unsigned)s;
-            best = v < best ? v : best;
-        }
-    }
-    return warp_min_u64(best);
-}
-
-__device__ __forceinline__ void clear_table(const Table& t, int lane) {
-    for (int s = lane; s < HSZ; s += 32) t.keys[s] = EMPTY;
-    if (lane == 0) t.misc[0] = 0;
-    __syncwarp();
-}
-
-// Compact the row's live keys with key > i (and |v| >= tau) into ckey/cval and
-// write them sorted to out_col/out_val; returns the count (> cap: overflow).
-__device__ __forceinline__ int emit_sorted_upper(const Table& t, int i, double tau, int cap, int lane,
-                                                 int32_t* __restrict__ out_col, double* __restrict__ out_val) {
-    int m = 0;
-    for (int s0 = 0; s0 < HSZ; s0 += 32) {
-        const int s = s0 + lane;
-        const int k = t.keys[s];
-        const bool take = k > i && !(fabs(t.vals[s]) < tau);
-        const unsigned b = __ballot_sync(0xffffffffu, take);
-        const int pos = m + __popc(b & ((1u << lane) - 1));
-        if (take && pos < cap) {
-            t.ckey[pos] = k;
-            t.cval[pos] = t.vals[s];
-        }
-        m += __popc(b);
-    }
-    __syncwarp();
-    if (m > cap) return m;
-    for (int a = lane; a < m; a += 32) {
-        const int k = t.ckey[a];
-        int r = 0;
-        for (int b = 0; b < m; ++b) r += t.ckey[b] < k;
-        out_col[r] = k;
-        out_val[r] = t.cval[a];
-    }
-    return m;
-}
-
-// ---- ILU(tau): working table of 2^HB slots per warp, rows to a shared pool
+// ---- working row of ILU(tau) / IC(tau): open-addressing table of 2^HB slots per warp
 template <int HB>
 struct HTab {
     static constexpr int N = 1 << HB;
@@ -361,36 +259,40 @@ __global__ void __launch_bounds__(32) k_ict(int n, CsrV A, double sign, const do
                                             double* __restrict__ diag, int* __restrict__ Ccnt,
                                             int32_t* __restrict__ Crow, double* __restrict__ Cval, int* shifts,
                                             int* err) {
+    using T = HTab<10>;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
-    const Table t = table_at(smem, cap);
+    T t;
+    t.vals = reinterpret_cast<double*>(smem);
+    t.keys = reinterpret_cast<int*>(t.vals + T::N);
     int nshift = 0;
     for (int i = 0; i < n; ++i) {
-        clear_table(t, lane);
+        for (int q = lane; q < T::N; q += 32) t.keys[q] = EMPTY;
+        __syncwarp();
         const int lo = A.ptr[i], hi = A.ptr[i + 1];
         const double norm = scale[i];
         const double tau = fill_tol * norm;
-        bool bad = hi - lo > HMAX;
+        int live = hi - lo;
+        bool bad = live > T::MAX;
         double dii = 0.0;                       // row.get(i, 0.0)
         if (!bad) {
             for (int e = lo + lane; e < hi; e += 32) {
                 const int j = A.idx[e];
                 if (j < i) {
                     bool fresh;
-                    const int s = hinsert(t, j, &fresh);
+                    const int s = t.insert(j, &fresh);
                     t.vals[s] = sign * A.val[e];
                 } else if (j == i) {
                     dii = sign * A.val[e];
                 }
             }
             dii = warp_sum(dii);                 // at most one lane holds the diagonal
-            if (lane == 0) t.misc[0] = hi - lo;
         }
         __syncwarp();
         const int64_t o = (int64_t)i * cap;
         int nl = 0, last = -1;
         while (!bad) {
-            const unsigned long long best = next_pivot(t, last, i, lane);
+            const unsigned long long best = t.next_pivot(last, i, lane);
             if (best == ~0ull) break;
             const int k = (int)(best >> 32), s = (int)(best & 0xffffffffu);
             const double w = t.vals[s];
@@ -410,7 +312,7 @@ __global__ void __launch_bounds__(32) k_ict(int n, CsrV A, double sign, const do
                 if (j <= k || j >= i) continue;
                 const double ljk = Cval[ok + q];
                 bool fresh = false;
-                const int sj = hinsert(t, j, &fresh);
+                const int sj = t.insert(j, &fresh);
                 if (sj < 0) { bad = true; continue; }
                 if (fresh) {
                     t.vals[sj] = -__dmul_rn(lik, ljk);
@@ -419,19 +321,16 @@ __global__ void __launch_bounds__(32) k_ict(int n, CsrV A, double sign, const do
                     t.vals[sj] = sub_mul(t.vals[sj], lik, ljk);
                 }
             }
-            added = warp_sum(added);
-            bad = __any_sync(0xffffffffu, bad);
+            live += warp_sum(added);
+            bad = __any_sync(0xffffffffu, bad) || live > T::MAX;
             dii = sub_mul(dii, lik, lik);
-            if (lane == 0) {
-                if (nl < cap) {
-                    Lcol[o + nl] = k;
-                    Lval[o + nl] = lik;
-                }
-                t.misc[0] += added;
+            if (lane == 0 && nl < cap) {
+                Lcol[o + nl] = k;
+                Lval[o + nl] = lik;
             }
             ++nl;
             __syncwarp();
-            if (nl > cap || t.misc[0] > HMAX) bad = true;
+            if (nl > cap) bad = true;
         }
         double d = dii;
         if (bad) {
@@ -704,7 +603,7 @@ void ict_factor(Ctx* c, const Csr& A, double sign, double fill_tol, IcFactor& f)
         EDFA_CUDA(cudaMemsetAsync(cc.p, 0, sizeof(int) * n, c->stream));
         k_row_scale<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(A), sc.p);
         check_launch("k_row_scale");
-        const size_t smem = warp_bytes(cap);
+        const size_t smem = (size_t)HTab<10>::N * 12;
         EDFA_CUDA(cudaFuncSetAttribute(k_ict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         Prof pr(c, "ict_factor", 12.0 * A.nnz + 16.0 * n);
         k_ict<<<1, 32, smem, c->stream>>>(n, view(A), sign, sc.p, fill_tol, cap, capc, lc.p, lcol.p, lval.p, f.diag.p,
