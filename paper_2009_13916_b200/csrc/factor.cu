@@ -158,35 +158,18 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
     }
     __syncwarp();
     int nl = lower_bound(cols, 0, n, i);
-    // every pivot row is final (earlier level): fetch its pivot and
-    // U-row extent in parallel
+    // pattern-only work first (U-row extents, chunking, target slots): it
+    // needs no pivot values, so it overlaps the wait for the pivot rows and
+    // only the value loads and the elimination remain on the critical path
     for (int p = lane; p < nl; p += 32) {
-        int k = cols[p];
-        if (SF) {   // wait for pivot row k (its pivot is published last)
-            double d = ld_relaxed(udiag + k);
-            long long spins = 0;
-            while (is_sentinel(d)) {
-                if (++spins > SPIN_LIMIT) { atomicExch(err, 7); d = 1.0; break; }
-                __nanosleep(32);
-                d = ld_relaxed(udiag + k);
-            }
-            pdk[p] = d;
-        } else {
-            pdk[p] = __ldcg(udiag + k);
-        }
-        int u0 = __ldg(ustart + k);
+        const int k = cols[p];
+        const int u0 = __ldg(ustart + k);
         pu0[p] = u0;
         pcnt[p] = Sp[k + 1] - u0;
     }
-    if (SF) __threadfence();   // pivot rows' U entries are read after their pivots were seen
     __syncwarp();
-    if (dbg && lane == 0) {
-        long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        dbg[3 * (int64_t)i + 1] = t;
-    }
-    for (int p0 = 0; p0 < nl;) {
-        if (lane == 0) {   // chunk of pivots whose U entries fit the staging buffer
+    auto chunk = [&](int p0) {   // pivots [p0, misc[0]) whose U entries fit the staging buffer
+        if (lane == 0) {
             int acc = 0, p1 = p0;
             while (p1 < nl && (p1 == p0 || acc + pcnt[p1] <= ECAP)) {
                 poff[p1 - p0] = acc;
@@ -198,11 +181,13 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
             misc[1] = min(acc, ECAP);
         }
         __syncwarp();
+    };
+    // stage (target slot, global index of u_kj) of every U entry of a chunk
+    long long* eidx = reinterpret_cast<long long*>(eval);
+    auto stage_slots = [&](int p0) {
         const int p1 = misc[0], tot = misc[1];
-        // stage (target slot, u_kj) of every U entry of the chunk
         for (int f0 = 0; f0 < tot; f0 += 32 * SW) {
             int e[SW], q[SW];
-            double u[SW];
             int32_t j[SW];
 #pragma unroll
             for (int w = 0; w < SW; ++w) {
@@ -221,20 +206,58 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
             }
 #pragma unroll
             for (int w = 0; w < SW; ++w)
-                if (q[w] >= 0) {
-                    j[w] = __ldg(Si + e[w]);
-                    u[w] = __ldcg(LU + e[w]);
-                }
+                if (q[w] >= 0) j[w] = __ldg(Si + e[w]);
 #pragma unroll
             for (int w = 0; w < SW; ++w) {
                 int f = f0 + w * 32 + lane;
                 if (q[w] >= 0) {
                     eslot[f] = bsearch(cols, q[w] + 1, n, j[w]);
-                    eval[f] = u[w];
+                    eidx[f] = e[w];
                 }
             }
         }
         __syncwarp();
+    };
+    auto stage_values = [&]() {   // u_kj of the staged entries (pivot rows final)
+        const int tot = misc[1];
+        for (int f = lane; f < tot; f += 32) eval[f] = __ldcg(LU + eidx[f]);
+        __syncwarp();
+    };
+    if (nl > 0) {
+        chunk(0);
+        stage_slots(0);
+    }
+    // every pivot row is final (earlier level) or awaited here through its
+    // published pivot
+    for (int p = lane; p < nl; p += 32) {
+        int k = cols[p];
+        if (SF) {   // wait for pivot row k (its pivot is published last)
+            double d = ld_relaxed(udiag + k);
+            long long spins = 0;
+            while (is_sentinel(d)) {
+                if (++spins > SPIN_LIMIT) { atomicExch(err, 7); d = 1.0; break; }
+                __nanosleep(32);
+                d = ld_relaxed(udiag + k);
+            }
+            pdk[p] = d;
+        } else {
+            pdk[p] = __ldcg(udiag + k);
+        }
+    }
+    if (SF) __threadfence();   // pivot rows' U entries are read after their pivots were seen
+    __syncwarp();
+    if (dbg && lane == 0) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        dbg[3 * (int64_t)i + 1] = t;
+    }
+    for (int p0 = 0; p0 < nl;) {
+        if (p0 > 0) {   // later chunks (rows whose pivots' U parts exceed the buffer)
+            chunk(p0);
+            stage_slots(p0);
+        }
+        stage_values();
+        const int p1 = misc[0], tot = misc[1];
         // eliminate, pivots in increasing column order (reference IKJ order)
         for (int p = p0; p < p1; ++p) {
             double mult = __ddiv_rn(vals[p], pdk[p]);
@@ -242,8 +265,8 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
             if (lane == 0) vals[p] = mult;
             const int off = poff[p - p0], cnt = min(pcnt[p], tot - off);
             for (int f = lane; f < cnt; f += 32) {
-                int s = eslot[off + f];
-                if (s >= 0) vals[s] = sub_mul(vals[s], mult, eval[off + f]);
+                int sl = eslot[off + f];
+                if (sl >= 0) vals[sl] = sub_mul(vals[sl], mult, eval[off + f]);
             }
             __syncwarp();
         }
