@@ -322,8 +322,11 @@ __global__ void __launch_bounds__(RED_THREADS) k_dcgs2_coeffs(const double* __re
 // block-contiguous element ranges so the blocks sharing a range run together
 // and u, w come from L2 after the first group.  partial[r][0..63] = u-dots,
 // [64..127] = w-dots.
+#ifndef DOTS2_MINB
+#define DOTS2_MINB 1
+#endif
 template <bool VEC2>
-__global__ void __launch_bounds__(RED_THREADS) k_dots2(const double* __restrict__ V, int64_t ldv, int nv, int64_t n,
+__global__ void __launch_bounds__(RED_THREADS, DOTS2_MINB) k_dots2(const double* __restrict__ V, int64_t ldv, int nv, int64_t n,
                                                        int64_t range, double* __restrict__ partial, int pr,
                                                        unsigned* counter, int j, int m, double* __restrict__ H,
                                                        double* __restrict__ h1, double* __restrict__ coef,
