@@ -586,7 +586,7 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
     if (x != b && !getenv("EDFA_TRSV_LEVELS")) {
         fill_bits(c, x, p.n, SENTINEL_BITS);
         EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
-        int* err = c->d_scalar_i + 52;
+        int* err = c->d_scalar_i + 8;   // the solve error flag check_trsv_error reads
         Prof pr(c, name, 12.0 * p.n_dep + 8.0 * p.n + 16.0 * p.n + (out2 ? 16.0 * p.n : 0.0));
         static int grid_sf = 0;
         if (!grid_sf) {
