@@ -212,7 +212,10 @@ __global__ void __launch_bounds__(RED_THREADS, 3) k_multiaxpy(const double* __re
 //   c = Q_{j+1}^T A P q_j,  u_{j+1} = A P q_j - Q_{j+1} c    (one pass)
 // so each step reads the basis twice (dots, update) instead of CGS2's four
 // times; in exact arithmetic the columns equal CGS2's.
-constexpr int D2_GROUP = 8;
+#ifndef EDFA_D2_GROUP
+#define EDFA_D2_GROUP 8
+#endif
+constexpr int D2_GROUP = EDFA_D2_GROUP;
 #ifndef EDFA_DOTS2_WAVE
 #define EDFA_DOTS2_WAVE 2
 #endif
@@ -322,8 +325,10 @@ __global__ void __launch_bounds__(RED_THREADS) k_dcgs2_coeffs(const double* __re
 // block-contiguous element ranges so the blocks sharing a range run together
 // and u, w come from L2 after the first group.  partial[r][0..63] = u-dots,
 // [64..127] = w-dots.
+// 2 resident blocks per SM (<= 128 registers): the one-wave grid below assumes it
+// (157 registers at minBlocks 1 left half the grid in a second wave: 5.8 -> 4.6 ms/step)
 #ifndef DOTS2_MINB
-#define DOTS2_MINB 1
+#define DOTS2_MINB EDFA_DOTS2_WAVE
 #endif
 template <bool VEC2>
 __global__ void __launch_bounds__(RED_THREADS, DOTS2_MINB) k_dots2(const double* __restrict__ V, int64_t ldv, int nv, int64_t n,
