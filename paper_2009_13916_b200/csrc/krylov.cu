@@ -436,6 +436,135 @@ __global__ void __launch_bounds__(RED_THREADS, DOTS2_MINB) k_dots2(const double*
     dcgs2_coeffs_block(dot, j, m, H, h1, coef, hcol);
 }
 
+// TMA-pipelined variant of k_dots2 (EDFA_DOTS2_TMA): one block per SM streams its
+// element range in chunks of D2T_CH elements of all nv+1 vectors into shared
+// memory with cp.async.bulk (D2T_ST stages in flight, ~100 KB per SM, independent
+// of the register budget); warp k % 8 owns vector k's two dots.  Same partial
+// layout and last-block epilogue as k_dots2.  Needs ldv, range even, V 16-byte aligned.
+#ifndef EDFA_DOTS2_TMA
+#define EDFA_DOTS2_TMA 0
+#endif
+constexpr int D2T_CH = 128, D2T_ST = 3, D2T_MAXK = 8;
+__device__ __forceinline__ unsigned d2t_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(RED_THREADS, 1) k_dots2_tma(const double* __restrict__ V, int64_t ldv, int nv,
+                                                              int64_t n, int64_t range, double* __restrict__ partial,
+                                                              int pr, unsigned* counter, int j, int m,
+                                                              double* __restrict__ H, double* __restrict__ h1,
+                                                              double* __restrict__ coef, double* __restrict__ hcol) {
+    extern __shared__ __align__(128) double d2t_buf[];   // [D2T_ST][nv+1][D2T_CH]
+    __shared__ __align__(8) uint64_t full[D2T_ST];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nvec = nv + 1;   // V_0..V_{nv-1} (u = V_{nv-1}) and w = V_nv
+    const int64_t lo = (int64_t)blockIdx.x * range, hi = min(n, lo + range);
+    const int nch = hi > lo ? (int)((hi - lo + D2T_CH - 1) / D2T_CH) : 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < D2T_ST; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(d2t_saddr(&full[s])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int c) {   // thread 0: stage c % D2T_ST <- chunk c of every vector
+        const int s = c % D2T_ST;
+        const int64_t c0 = lo + (int64_t)c * D2T_CH;
+        const unsigned bytes = (unsigned)(min((int64_t)D2T_CH, hi - c0) * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(d2t_saddr(&full[s])),
+                     "r"(bytes * nvec) : "memory");
+        double* dst = d2t_buf + (size_t)s * nvec * D2T_CH;
+        for (int k = 0; k < nvec; ++k)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(d2t_saddr(dst + (size_t)k * D2T_CH)), "l"(V + (int64_t)k * ldv + c0), "r"(bytes),
+                         "r"(d2t_saddr(&full[s])) : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (int c = 0; c < min(nch, D2T_ST); ++c) issue(c);
+    double au[D2T_MAXK], aw[D2T_MAXK];
+#pragma unroll
+    for (int q = 0; q < D2T_MAXK; ++q) au[q] = aw[q] = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        const int s = c % D2T_ST;
+        const unsigned par = (unsigned)((c / D2T_ST) & 1);
+        asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                     "@!p bra WAIT_%=;\n\t}" ::"r"(d2t_saddr(&full[s])), "r"(par) : "memory");
+        const int cnt = (int)min((int64_t)D2T_CH, hi - (lo + (int64_t)c * D2T_CH));
+        const double* st = d2t_buf + (size_t)s * nvec * D2T_CH;
+        const double2* u2 = reinterpret_cast<const double2*>(st + (size_t)(nv - 1) * D2T_CH);
+        const double2* w2 = reinterpret_cast<const double2*>(st + (size_t)nv * D2T_CH);
+        double2 ue[D2T_CH / 64], we[D2T_CH / 64];
+#pragma unroll
+        for (int t = 0; t < D2T_CH / 64; ++t) {
+            const int e = lane + 32 * t;   // double2 index
+            const bool ok = 2 * e < cnt;
+            ue[t] = ok ? u2[e] : make_double2(0.0, 0.0);
+            we[t] = ok ? w2[e] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < D2T_MAXK; ++q) {
+            const int k = wid + 8 * q;
+            if (k < nv) {
+                const double2* v2 = reinterpret_cast<const double2*>(st + (size_t)k * D2T_CH);
+#pragma unroll
+                for (int t = 0; t < D2T_CH / 64; ++t) {
+                    const int e = lane + 32 * t;
+                    if (2 * e < cnt) {
+                        const double2 v = v2[e];
+                        au[q] = fma(v.y, ue[t].y, fma(v.x, ue[t].x, au[q]));
+                        aw[q] = fma(v.y, we[t].y, fma(v.x, we[t].x, aw[q]));
+                    }
+                }
+            }
+        }
+        __syncthreads();   // stage s consumed by every warp
+        if (threadIdx.x == 0 && c + D2T_ST < nch) issue(c + D2T_ST);
+    }
+#pragma unroll
+    for (int q = 0; q < D2T_MAXK; ++q) {
+        const int k = wid + 8 * q;
+        const double x = warp_sum(au[q]), y = warp_sum(aw[q]);
+        if (lane == 0 && k < nv) {
+            partial[(int64_t)k * pr + blockIdx.x] = x;
+            partial[(int64_t)(64 + k) * pr + blockIdx.x] = y;
+        }
+    }
+    // last block: fixed-order sum over ranges, then the step's coefficients
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // warp w sums the needed slots w, w+8, ... over the ranges (slot-major
+    // partials: lanes read consecutive ranges), fixed order: deterministic
+    __shared__ double dot[128];
+    {
+        const int nr = (int)(gridDim.x * gridDim.y), nw = RED_THREADS / 32;
+        for (int q = wid; q < 2 * nv; q += nw) {
+            const int slot = q < nv ? q : 64 + (q - nv);
+            const double* col = partial + (int64_t)slot * pr;
+            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+            int b = lane;
+            for (; b + 96 < nr; b += 128) {
+                acc0 += __ldcg(col + b);
+                acc1 += __ldcg(col + b + 32);
+                acc2 += __ldcg(col + b + 64);
+                acc3 += __ldcg(col + b + 96);
+            }
+            for (; b < nr; b += 32) acc0 += __ldcg(col + b);
+            const double t = warp_sum((acc0 + acc1) + (acc2 + acc3));
+            if (lane == 0) dot[slot] = t;
+        }
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    __syncthreads();
+    if (!coef) {   // dots only (slab-distributed solves reduce them across slabs first)
+        const int t = threadIdx.x;
+        if (t < 128) hcol[t] = (t < nv || (t >= 64 && t < 64 + nv)) ? dot[t] : 0.0;
+        return;
+    }
+    dcgs2_coeffs_block(dot, j, m, H, h1, coef, hcol);
+}
+
 // slot j  <- q_j     = coef[128] u - sum_k coef[k] V_k          (j >= 1)
 // slot j+1 <- u_{j+1} = coef[129] w + coef[130] u - sum_k coef[64+k] V_k
 template <bool VEC2>
@@ -590,7 +719,22 @@ struct Blas {
         {
             Prof pr(c, "gs_dots2", 8.0 * n * (nv + 1));
             dim3 grid(groups, (unsigned)ranges);
-            if (v2)
+            if (EDFA_DOTS2_TMA && v2 && nv <= 8 * D2T_MAXK) {
+                const int64_t rt = std::min<int64_t>(std::min<int64_t>(NUM_SMS_B200, part2_rows),
+                                                     (n + D2T_CH - 1) / D2T_CH);
+                int64_t rg = (n + rt - 1) / rt;
+                rg = (rg + 1) & ~int64_t(1);
+                const int64_t nr = (n + rg - 1) / rg;
+                const size_t smem = (size_t)D2T_ST * (nv + 1) * D2T_CH * sizeof(double);
+                static bool attr = false;
+                if (!attr) {
+                    EDFA_CUDA(cudaFuncSetAttribute(k_dots2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)((size_t)D2T_ST * 66 * D2T_CH * sizeof(double))));
+                    attr = true;
+                }
+                k_dots2_tma<<<(unsigned)nr, RED_THREADS, smem, c->stream>>>(V, n, nv, n, rg, part2, part2_rows, cnt,
+                                                                            j, m, H, h1, coef, hcol);
+            } else if (v2)
                 k_dots2<true><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, part2_rows, cnt, j, m, H,
                                                                   h1, coef, hcol);
             else
