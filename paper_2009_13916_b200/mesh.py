@@ -142,28 +142,54 @@ def _topology(nx, ny, nz):
     return e2n, e2f, f2e, floc
 
 
+_CHUNK = 1 << 20   # cells / faces per block of the geometry pass (bounded temporaries at 256^3)
+
+
 def geometry(node_coords, e2n, f2e, floc):
     """Cell volumes (2x2x2 Gauss) and owner-side bilinear face areas
-    (hx/grid.py:137-164).  Raises ValueError on an inverted cell."""
-    xyz = node_coords[e2n]
+    (hx/grid.py:137-164).  Raises ValueError on an inverted cell.
+
+    Same quadrature and accumulation order as the reference; per block of
+    cells, the Jacobian entries of all eight points come from three GEMMs with
+    contiguous (point, entry) rows, so a 256^3 grid takes seconds instead of
+    minutes (values agree to the last bits, inside the 1e-13 assembly
+    tolerance)."""
     pts, wts = gauss3()
-    vol = np.zeros(xyz.shape[0])
-    for p, w in zip(pts, wts):
-        J = np.einsum("enc,nb->ecb", xyz, shape_grad(p))
-        det = np.linalg.det(J)
-        if np.any(det <= 0):
-            raise ValueError(f"cell {int(np.flatnonzero(det <= 0)[0])} is inverted")
-        vol += w * det
-    fn = e2n[f2e[:, 0][:, None], FACE_CORNERS[floc[:, 0]]]
-    fc = node_coords[fn]
-    area = np.zeros(fc.shape[0])
+    dNT = np.concatenate([shape_grad(p) for p in pts], axis=1).T.copy()   # (8 points * 3, 8 nodes)
+    n_e = e2n.shape[0]
+    vol = np.zeros(n_e)
+    for c0 in range(0, n_e, _CHUNK):
+        c1 = min(c0 + _CHUNK, n_e)
+        nodes = e2n[c0:c1].T                                                 # (8, c)
+        J = [dNT @ node_coords[nodes, a] for a in range(3)]                 # J[a][3q + b] = dx_a/dxi_b at q
+        acc = np.zeros(c1 - c0)
+        for q, w in enumerate(wts):
+            (a0, a1, a2), (b0, b1, b2), (d0, d1, d2) = (J[a][3 * q:3 * q + 3] for a in range(3))
+            det = a0 * (b1 * d2 - b2 * d1) - a1 * (b0 * d2 - b2 * d0) + a2 * (b0 * d1 - b1 * d0)
+            if np.any(det <= 0):
+                raise ValueError(f"cell {c0 + int(np.flatnonzero(det <= 0)[0])} is inverted")
+            acc += w * det
+        vol[c0:c1] = acc
+    n_f = f2e.shape[0]
+    area = np.zeros(n_f)
+    dUV = []
     for v in (-_G, _G):
         for u in (-_G, _G):
-            du = np.array([-(1 - v), (1 - v), (1 + v), -(1 + v)]) / 4.0
-            dv = np.array([-(1 - u), -(1 + u), (1 + u), (1 - u)]) / 4.0
-            ru = np.einsum("fnc,n->fc", fc, du)
-            rv = np.einsum("fnc,n->fc", fc, dv)
-            area += np.linalg.norm(np.cross(ru, rv), axis=1)
+            dUV.append(np.array([-(1 - v), (1 - v), (1 + v), -(1 + v)]) / 4.0)
+            dUV.append(np.array([-(1 - u), -(1 + u), (1 + u), (1 - u)]) / 4.0)
+    dUVT = np.stack(dUV, axis=0)                                             # (8, 4 corners)
+    for c0 in range(0, n_f, _CHUNK):
+        c1 = min(c0 + _CHUNK, n_f)
+        fn = e2n[f2e[c0:c1, 0][:, None], FACE_CORNERS[floc[c0:c1, 0]]].T     # (4, c)
+        R = [dUVT @ node_coords[fn, a] for a in range(3)]                   # R[a][2q + (u|v)]
+        acc = np.zeros(c1 - c0)
+        for q in range(4):
+            (ux, vx), (uy, vy), (uz, vz) = (R[a][2 * q:2 * q + 2] for a in range(3))
+            cx = uy * vz - uz * vy
+            cy = uz * vx - ux * vz
+            cz = ux * vy - uy * vx
+            acc += np.sqrt(cx * cx + cy * cy + cz * cz)
+        area[c0:c1] = acc
     return vol, area
 
 
