@@ -119,6 +119,13 @@ int         edfa_abi_version(void);
 const char* edfa_last_error(void);
 int edfa_ctx_create(int device, void* cuda_stream, edfa_ctx** out);
 int edfa_ctx_set_stream(edfa_ctx* ctx, void* cuda_stream);
+/* Algorithm selections (defaults = production; alternatives for A/B tests):
+ * "ic_pair" (1) fused (L L^T)^-1 chain kernel, "fill_fusion" (1) ILU solves
+ * pre-fill each other's SENTINELs, "trsv_levels" (0) level-synchronous
+ * triangular solves, "ilu_levels" (0) level-synchronous ILU(0).  Seeded once
+ * from EDFA_OPT_<NAME> at context creation.  Unknown name -> EDFA_ERR_VALUE. */
+int edfa_ctx_set_option(edfa_ctx* ctx, const char* name, int value);
+int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value);
 int edfa_ctx_sync(edfa_ctx* ctx);
 int edfa_ctx_destroy(edfa_ctx* ctx);
 /* Per-kernel CUDA-event timing with algorithmic byte counts (roofline). */
@@ -238,6 +245,10 @@ int edfa_axpby(edfa_ctx* ctx, int64_t n, double a, const double* x, double b, do
  * (col_map must be increasing on the kept columns; device arrays). */
 int edfa_csr_submatrix(edfa_ctx* ctx, const edfa_csr* A, int32_t n_rows, const int32_t* rows,
                        const int32_t* col_map, int32_t n_cols, edfa_csr** out);
+/* filter_rows (hx/precond.py:138-157): out = A with the off-diagonal (or, with
+ * keep_diagonal = 0, all) entries |v| < tau * ||row||_2 and exact zeros
+ * dropped; A canonical, tau > 0. */
+int edfa_csr_filter(edfa_ctx* ctx, const edfa_csr* A, double tau, int keep_diagonal, edfa_csr** out);
 /* out = canonical(A - B) with the optional row filter (S~ = A_cc - H~,
  * hx/precond.py:264-271; filter_rows 138-157 when tau > 0). */
 int edfa_csr_sub(edfa_ctx* ctx, const edfa_csr* A, const edfa_csr* B, double tau, edfa_csr** out);

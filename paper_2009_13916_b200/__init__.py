@@ -17,9 +17,10 @@ _LAZY = {
     "Stage2": "precond", "build_stage1": "precond", "build_stage2": "precond",
     "compute_density": "precond", "grow_pattern_dynamic": "precond", "patterns_for": "precond",
     "solve_restricted_row": "precond", "InnerFactorization": "precond", "FILTRATION_MODES": "precond",
+    "filter_rows": "precond", "canonical": "sparse", "mm_write": "sparse", "mm_read": "sparse",
     "SolveReport": "krylov", "bicgstab": "krylov", "gmres": "krylov",
     "PatternSet": "patterns", "base_pattern": "patterns", "static_patterns": "patterns",
-    "DeviceCsr": "device", "DeviceSystem": "device", "system_operator": "device",
+    "DeviceCsr": "device", "DeviceSystem": "device", "system_operator": "device", "option": "device",
     "FactorizationError": "errors", "ConvergenceError": "errors",
 }
 

@@ -72,6 +72,8 @@ _SIGS = {
     "edfa_ctx_create": (i32, [i32, vp, C.POINTER(vp)]),
     "edfa_ctx_set_stream": (i32, [vp, vp]),
     "edfa_ctx_sync": (i32, [vp]),
+    "edfa_ctx_set_option": (i32, [vp, C.c_char_p, i32]),
+    "edfa_ctx_get_option": (i32, [vp, C.c_char_p, P_i32]),
     "edfa_ctx_destroy": (i32, [vp]),
     "edfa_ctx_profile": (i32, [vp, i32]),
     "edfa_ctx_profile_filter": (i32, [vp, C.c_char_p]),
@@ -107,6 +109,7 @@ _SIGS = {
     "edfa_axpby": (i32, [vp, i64, f64, vp, f64, vp]),
     "edfa_csr_submatrix": (i32, [vp, vp, i32, vp, vp, i32, C.POINTER(vp)]),
     "edfa_csr_sub": (i32, [vp, vp, vp, f64, C.POINTER(vp)]),
+    "edfa_csr_filter": (i32, [vp, vp, f64, i32, C.POINTER(vp)]),
     "edfa_factor_ic0": (i32, [vp, vp, f64, C.POINTER(vp)]),
     "edfa_factor_ilu0": (i32, [vp, vp, f64, i32, i32, i32, C.POINTER(vp)]),
     "edfa_factor_ic": (i32, [vp, vp, f64, i32, C.POINTER(vp)]),

@@ -327,7 +327,9 @@ int edfa_precond_apply(edfa_ctx* ctx, const edfa_system* sys, const edfa_stage1*
     API_BEGIN
     require(s1 != nullptr, EDFA_ERR_STATE, "stage 1 has not been built");
     require(s2 != nullptr, EDFA_ERR_STATE, "stage 2 has not been built; call refresh()");
+    ctx->c.trsv_err_poll();
     apply_entry(&ctx->c, sys, s1, s2, r, y);
+    ctx->c.trsv_err_post();
     API_END
 }
 
@@ -335,7 +337,9 @@ int edfa_inner_apply(edfa_ctx* ctx, const edfa_stage1* s1, const edfa_stage2* s2
                      double* y) {
     API_BEGIN
     require(which == 0 ? s1 != nullptr : s2 != nullptr, EDFA_ERR_STATE, "factorisation not built");
+    ctx->c.trsv_err_poll();
     inner_apply(&ctx->c, s1, s2, which, r, y);
+    ctx->c.trsv_err_post();
     API_END
 }
 
@@ -458,6 +462,22 @@ int edfa_csr_submatrix(edfa_ctx* ctx, const edfa_csr* A, int32_t n_rows, const i
     h->ctx = &ctx->c;
     try {
         csr_submatrix(&ctx->c, M(A), rows, n_rows, col_map, n_cols, h->own);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    *out = h;
+    API_END
+}
+
+int edfa_csr_filter(edfa_ctx* ctx, const edfa_csr* A, double tau, int keep_diagonal, edfa_csr** out) {
+    API_BEGIN
+    require(ctx && A && out, EDFA_ERR_VALUE, "NULL argument");
+    require(tau > 0.0, EDFA_ERR_VALUE, "tau must be > 0 (tau <= 0 leaves the matrix unchanged)");
+    auto* h = new edfa_csr();
+    h->ctx = &ctx->c;
+    try {
+        csr_filter(&ctx->c, M(A), tau, h->own, keep_diagonal != 0);
     } catch (...) {
         delete h;
         throw;
@@ -604,6 +624,7 @@ int edfa_factor_solve(edfa_ctx* ctx, const edfa_factor* f, const double* r, doub
     API_BEGIN
     require(ctx && f, EDFA_ERR_VALUE, "NULL argument");
     Ctx* c = &ctx->c;
+    c->trsv_err_poll();
     if (f->kind == 0) {
         // chain-structured factor: (L L^T)^-1 in one fused kernel (no shared state: safe for concurrent calls)
         if (!(f->ic.fwd.is_chain && f->ic.bwd.is_chain &&
@@ -617,6 +638,7 @@ int edfa_factor_solve(edfa_ctx* ctx, const edfa_factor* f, const double* r, doub
         run_plan(c, f->ilu.fwd, r, alpha, tmp.p, nullptr, nullptr, "trsv_ilu_L");
         run_plan(c, f->ilu.bwd, tmp.p, 1.0, y, nullptr, nullptr, "trsv_ilu_U");
     }
+    c->trsv_err_post();
     API_END
 }
 

@@ -226,26 +226,14 @@ __global__ void __launch_bounds__(256) k_chain_scan(const int64_t* __restrict__ 
 // then the mirrored backward scan (y_i = d_i(x_i - c_{i+1} y_{i+1})), with x
 // kept in registers (chains of at most 32*E rows).  Half the launches and no
 // HBM round trip for the intermediate vector.
-#ifndef PAIR_MINB
-#define PAIR_MINB 1
-#endif
 template <int E>
-__global__ void __launch_bounds__(256, PAIR_MINB) k_chain_pair(const int64_t* __restrict__ cptr, const int* __restrict__ rows,
+__global__ void __launch_bounds__(256) k_chain_pair(const int64_t* __restrict__ cptr, const int* __restrict__ rows,
                                                     const double* __restrict__ coef, const double* __restrict__ dinv,
                                                     int n_chains, const double* b, double alpha, double* x,
-                                                    const double* __restrict__ add, double* __restrict__ out2,
-                                                    const int32_t* __restrict__ fp, const int32_t* __restrict__ fi,
-                                                    const double* __restrict__ fv, const double* __restrict__ fx) {
+                                                    const double* __restrict__ add, double* __restrict__ out2) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= n_chains) return;
     const int64_t s = cptr[w], e = cptr[w + 1];
-    // right-hand side of row r: b[r], or (fused SpMV) M_r . fx in k_spmv_sell's FMA order
-    auto rhs = [&](int r) -> double {
-        if (!fp) return b[r];
-        double acc = 0.0;
-        for (int q = fp[r]; q < fp[r + 1]; ++q) acc = fma(fv[q], __ldg(fx + fi[q]), acc);
-        return acc;
-    };
     int r[E];
     double d[E], cf[E], xv[E];
 #pragma unroll
@@ -259,7 +247,7 @@ __global__ void __launch_bounds__(256, PAIR_MINB) k_chain_pair(const int64_t* __
     double al[E], be[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) {
-        if (r[j] >= 0) { al[j] = d[j] * (alpha * rhs(r[j])); be[j] = -cf[j] * d[j]; }
+        if (r[j] >= 0) { al[j] = d[j] * (alpha * b[r[j]]); be[j] = -cf[j] * d[j]; }
         else { al[j] = 0.0; be[j] = 1.0; }
     }
     double A = al[0], B = be[0];
@@ -426,20 +414,20 @@ void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, 
 }
 
 bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add,
-                    double* out2, const char* name, const Csr* fz, const double* fz_x) {
-    if (cp.n_chains == 0 || cp.max_len > 32 * 8) return false;
-    Prof pr(c, name, 12.0 * cp.n + 32.0 * cp.n + (out2 ? 16.0 * cp.n : 0.0) + (x ? 8.0 * cp.n : 0.0) +
-                         (fz ? 12.0 * fz->nnz + 8.0 * fz->n_cols : 0.0));
+                    double* out2, const char* name) {
+    if (cp.n_chains == 0 || cp.max_len > 32 * 16) return false;
+    Prof pr(c, name, 12.0 * cp.n + 32.0 * cp.n + (out2 ? 16.0 * cp.n : 0.0) + (x ? 8.0 * cp.n : 0.0));
     const unsigned grid = (unsigned)ceil_div((int64_t)cp.n_chains * 32, 256);
-    const int32_t* fp = fz ? fz->ptr.p : nullptr;
-    const int32_t* fi = fz ? fz->idx.p : nullptr;
-    const double* fv = fz ? fz->val.p : nullptr;
+    // rows per lane: chains of up to 32 E rows (256^3 face lines have 257 rows)
     if (cp.max_len <= 32 * 4)
         k_chain_pair<4><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha,
-                                                     x, add, out2, fp, fi, fv, fz_x);
-    else
+                                                     x, add, out2);
+    else if (cp.max_len <= 32 * 8)
         k_chain_pair<8><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha,
-                                                     x, add, out2, fp, fi, fv, fz_x);
+                                                     x, add, out2);
+    else
+        k_chain_pair<16><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b,
+                                                      alpha, x, add, out2);
     check_launch("k_chain_pair");
     return true;
 }

@@ -138,6 +138,41 @@ int set_error(int code, const std::string& msg) {
 }  // namespace edfa
 
 
+void Ctx::trsv_err_post() {
+    EDFA_CUDA(cudaMemcpyAsync(h_trsv_err, d_scalar_i + 8, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    EDFA_CUDA(cudaEventRecord(trsv_ev, stream));
+    trsv_pending = true;
+}
+
+static void raise_trsv(Ctx* c) {
+    *c->h_trsv_err = 0;
+    c->trsv_pending = false;
+    EDFA_CUDA(cudaMemsetAsync(c->d_scalar_i + 8, 0, sizeof(int), c->stream));
+    throw Error(EDFA_ERR_CUDA, "triangular solve exceeded its spin limit (dependency never published)");
+}
+
+void Ctx::trsv_err_poll() {
+    if (!trsv_pending) return;
+    const cudaError_t q = cudaEventQuery(trsv_ev);
+    if (q == cudaErrorNotReady) return;
+    EDFA_CUDA(q);
+    trsv_pending = false;
+    if (*h_trsv_err) raise_trsv(this);
+}
+
+void Ctx::trsv_err_check() {
+    EDFA_CUDA(cudaMemcpyAsync(h_trsv_err, d_scalar_i + 8, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    EDFA_CUDA(cudaStreamSynchronize(stream));
+    trsv_pending = false;
+    if (*h_trsv_err) raise_trsv(this);
+}
+
+void Ctx::trsv_err_reset() {
+    trsv_pending = false;
+    *h_trsv_err = 0;
+    EDFA_CUDA(cudaMemsetAsync(d_scalar_i + 8, 0, sizeof(int), stream));
+}
+
 extern "C" {
 
 int edfa_abi_version(void) { return EDFA_ABI_VERSION; }
@@ -151,10 +186,22 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
     auto* h = new edfa_ctx();
     h->c.device = device;
     h->c.stream = static_cast<cudaStream_t>(stream);
+    // algorithm selections: read from the environment once, here
+    auto env_opt = [](const char* name, int dflt) {
+        const char* e = getenv(name);
+        return e ? atoi(e) : dflt;
+    };
+    h->c.opt.ic_pair = env_opt("EDFA_OPT_IC_PAIR", 1);
+    h->c.opt.fill_fusion = env_opt("EDFA_OPT_FILL_FUSION", 1);
+    h->c.opt.trsv_levels = env_opt("EDFA_OPT_TRSV_LEVELS", 0);
+    h->c.opt.ilu_levels = env_opt("EDFA_OPT_ILU_LEVELS", 0);
     h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
     EDFA_CUDA(cudaMemsetAsync(h->c.d_scalar_i, 0, 64 * sizeof(int), h->c.stream));   // [60]: reduction ticket
     h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));
     EDFA_CUDA(cudaMallocHost(&h->c.h_pinned, 4096 * sizeof(double)));
+    EDFA_CUDA(cudaMallocHost(&h->c.h_trsv_err, sizeof(int)));
+    *h->c.h_trsv_err = 0;
+    EDFA_CUDA(cudaEventCreateWithFlags(&h->c.trsv_ev, cudaEventDisableTiming));
     *out = h;
     API_END
 }
@@ -171,9 +218,35 @@ int edfa_ctx_set_stream(edfa_ctx* ctx, void* stream) {
     API_END
 }
 
+int edfa_ctx_set_option(edfa_ctx* ctx, const char* name, int value) {
+    API_BEGIN
+    require(ctx && name, EDFA_ERR_VALUE, "ctx or name is NULL");
+    CtxOptions& o = ctx->c.opt;
+    const std::string n = name;
+    if (n == "ic_pair") o.ic_pair = value;
+    else if (n == "fill_fusion") o.fill_fusion = value;
+    else if (n == "trsv_levels") o.trsv_levels = value;
+    else if (n == "ilu_levels") o.ilu_levels = value;
+    else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
+    API_END
+}
+
+int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value) {
+    API_BEGIN
+    require(ctx && name && value, EDFA_ERR_VALUE, "ctx, name or value is NULL");
+    const CtxOptions& o = ctx->c.opt;
+    const std::string n = name;
+    if (n == "ic_pair") *value = o.ic_pair;
+    else if (n == "fill_fusion") *value = o.fill_fusion;
+    else if (n == "trsv_levels") *value = o.trsv_levels;
+    else if (n == "ilu_levels") *value = o.ilu_levels;
+    else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
+    API_END
+}
+
 int edfa_ctx_sync(edfa_ctx* ctx) {
     API_BEGIN
-    EDFA_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    ctx->c.trsv_err_check();   // synchronises; raises a solve that hit its spin limit
     API_END
 }
 
@@ -188,6 +261,8 @@ int edfa_ctx_destroy(edfa_ctx* ctx) {
     c.free(c.d_scalar_i);
     c.free(c.d_scalar_d);
     cudaFreeHost(c.h_pinned);
+    cudaFreeHost(c.h_trsv_err);
+    cudaEventDestroy(c.trsv_ev);
     cudaStreamSynchronize(c.stream);
     c.trim_cache();
     delete ctx;

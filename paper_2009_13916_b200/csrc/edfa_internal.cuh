@@ -59,9 +59,21 @@ struct ProfRec {
     double bytes;
 };
 
+// Algorithm selections of a context.  Defaults are the production choices;
+// the alternatives are kept because tests compare them against each other
+// (edfa_ctx_set_option; the EDFA_OPT_* environment variables seed them once
+// at context creation).
+struct CtxOptions {
+    int ic_pair = 1;        // fused (L L^T)^-1 chain kernel for chain-structured IC factors
+    int fill_fusion = 1;    // the two ILU tile solves pre-fill each other's SENTINELs
+    int trsv_levels = 0;    // level-synchronous triangular solves instead of the sync-free ones
+    int ilu_levels = 0;     // level-synchronous ILU(0) factorisation instead of the sync-free one
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    CtxOptions opt;
     int profiling = 0;
     std::string prof_prefix;   // only kernels whose name starts with it are timed
     int64_t launches = 0;
@@ -89,6 +101,16 @@ struct Ctx {
     void* cub_scratch(size_t bytes);
     cudaEvent_t get_event();
     void flush_profile();
+    // spin-limit flag of the sync-free triangular solves (d_scalar_i[8]):
+    // entry points that run solves post an async read-back; the next entry
+    // point (or edfa_ctx_sync) raises it once the copy has landed
+    int* h_trsv_err = nullptr;     // pinned
+    cudaEvent_t trsv_ev = nullptr;
+    bool trsv_pending = false;
+    void trsv_err_post();          // enqueue the flag's read-back (no host wait)
+    void trsv_err_poll();          // raise a landed flag (no host wait)
+    void trsv_err_check();         // synchronise, raise and clear
+    void trsv_err_reset();         // drop any stale flag before a new solve
 };
 
 // RAII guard for library-owned device allocations
@@ -228,7 +250,7 @@ void spmv_sell(Ctx* c, const Sell& A, const double* x, double* y, double alpha, 
 // S = A - H (row-wise sorted merge, exact zeros dropped, optional row filter)
 void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S);
 // row filter (filter_rows, precond.py:138-157): drop |v| < tau*||row||_2 off-diagonal
-void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out);
+void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out, bool keep_diag = true);
 void copy_csr(Ctx* c, const Csr& A, Csr& out);
 void fill(Ctx* c, double* p, int64_t n, double v);
 void fill_bits(Ctx* c, double* p, int64_t n, unsigned long long bits);

@@ -134,7 +134,7 @@ template <int RMAX, bool SF>
 __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, const int32_t* __restrict__ Si,
                                          const int32_t* __restrict__ ustart, double* __restrict__ LU,
                                          const double* __restrict__ scale, double* __restrict__ udiag, int* shifts,
-                                         int* err, unsigned char* base, int lane, long long* dbg = nullptr) {
+                                         int* err, unsigned char* base, int lane) {
     constexpr int ECAP = ilu0_ecap(RMAX);
     constexpr int SW = ECAP / 32 < 16 ? ECAP / 32 : 16;   // staged entries per lane per round trip
     double* vals = reinterpret_cast<double*>(base);
@@ -246,11 +246,6 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
     }
     if (SF) __threadfence();   // pivot rows' U entries are read after their pivots were seen
     __syncwarp();
-    if (dbg && lane == 0) {
-        long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        dbg[3 * (int64_t)i + 1] = t;
-    }
     for (int p0 = 0; p0 < nl;) {
         if (p0 > 0) {   // later chunks (rows whose pivots' U parts exceed the buffer)
             chunk(p0);
@@ -284,11 +279,6 @@ __device__ __forceinline__ void ilu0_row(int i, const int32_t* __restrict__ Sp, 
         __threadfence();
         __syncwarp();
         if (lane == 0) st_relaxed(udiag + i, publishable(piv));
-        if (dbg && lane == 0) {
-            long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            dbg[3 * (int64_t)i + 2] = t;
-        }
     } else if (lane == 0) {
         __stcg(udiag + i, piv);
     }
@@ -326,7 +316,7 @@ __global__ void __launch_bounds__(256) k_ilu0_sf(const int* __restrict__ ord, in
                                                  const int32_t* __restrict__ Sp, const int32_t* __restrict__ Si,
                                                  const int32_t* __restrict__ ustart, double* __restrict__ LU,
                                                  const double* __restrict__ scale, double* __restrict__ udiag,
-                                                 int* shifts, int* err, long long* dbg) {
+                                                 int* shifts, int* err) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* base = smem + (size_t)wid * ilu0_warp_smem(RMAX);
@@ -337,12 +327,7 @@ __global__ void __launch_bounds__(256) k_ilu0_sf(const int* __restrict__ ord, in
         if (s >= n_ord) break;
         const int i = ord[s];
         if (i < 0) continue;
-        if (dbg && lane == 0) {
-            long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            dbg[3 * (int64_t)i] = t;
-        }
-        ilu0_row<RMAX, true>(i, Sp, Si, ustart, LU, scale, udiag, shifts, err, base, lane, dbg);
+        ilu0_row<RMAX, true>(i, Sp, Si, ustart, LU, scale, udiag, shifts, err, base, lane);
     }
 }
 
@@ -554,7 +539,7 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         int hb = 0;
         EDFA_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         EDFA_CUDA(cudaStreamSynchronize(c->stream));
-        sync_free = hb == 0 && !getenv("EDFA_ILU_LEVELS");
+        sync_free = hb == 0 && !c->opt.ilu_levels;
     }
     Csr Lpart;
     auto level_plan = [&]() {
@@ -567,7 +552,7 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         level_plan();
         // rows in level order are topological too: run the sync-free kernel on
         // that order (no grid barrier per level) unless levels are requested
-        sync_free = !getenv("EDFA_ILU_LEVELS");
+        sync_free = !c->opt.ilu_levels;
     }
     PhaseTimer pt_fact(c, "ilu0.factor+plans");
     int maxr = n ? max_row_nnz(c, S) : 0;
@@ -594,14 +579,7 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         int* tk = c->d_scalar_i + 29;
         if (sync_free) EDFA_CUDA(cudaMemsetAsync(tk, 0, sizeof(int), c->stream));
         void* args[] = {&la, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
-        static const char* dbg_path = getenv("EDFA_ILU_DEBUG");
-        DevBuf<long long> dbgb;
-        long long* dbgp = nullptr;
-        if (dbg_path && sync_free) {
-            dbgb.reset(c, (size_t)3 * n);
-            dbgp = dbgb.p;
-        }
-        void* args_sf[] = {&op, &n_ord, &tk, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er, &dbgp};
+        void* args_sf[] = {&op, &n_ord, &tk, &Sp, &Si, &Us, &LUv, &scp, &ud, &sh, &er};
         auto launch = [&](auto kern, auto kern_sf, int rmax) {
             int threads = rmax >= 1024 ? 64 : rmax <= 64 ? 256 : 128;
             size_t smem = ilu0_warp_smem(rmax) * (threads / 32);
@@ -620,16 +598,6 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
         if (maxr <= 64) launch(k_ilu0<64>, k_ilu0_sf<64>, 64);
         else if (maxr <= 256) launch(k_ilu0<256>, k_ilu0_sf<256>, 256);
         else launch(k_ilu0<1024>, k_ilu0_sf<1024>, 1024);
-        if (dbgp) {
-            std::vector<long long> h((size_t)3 * n);
-            EDFA_CUDA(cudaMemcpyAsync(h.data(), dbgp, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-            EDFA_CUDA(cudaStreamSynchronize(c->stream));
-            FILE* fp = fopen(dbg_path, "wb");
-            if (fp) {
-                fwrite(h.data(), 8, h.size(), fp);
-                fclose(fp);
-            }
-        }
     }
     int err = 0;
     read_flags(c, flags, &f.shifts, &err);
@@ -644,15 +612,8 @@ void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
     Csr Lv, Uv;
     select_part(c, f.LU, 0, 1.0, true, Lv);
     select_part(c, f.LU, 1, 1.0, true, Uv);
-    // cell-grid factors: tile-DAG solves; otherwise level-synchronous plans
-    // cell-grid factors: pencil solves for axial stencils, tile-DAG solves for
-    // other grid-local stencils, otherwise level-ordered plans
-    if (dims && build_axial_plan(c, Lv, nullptr, true, false, dims, f.fwd.axial)) {
-        f.fwd.is_axial = true;
-        f.fwd.n = n;
-        f.fwd.n_dep = Lv.nnz;
-        f.fwd.n_levels = f.fwd.axial.nsteps;
-    } else if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
+    // cell-grid factors: tile-DAG solves; otherwise level-ordered plans
+    if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
         f.fwd.is_tile = true;
         f.fwd.n = n;
         f.fwd.n_dep = Lv.nnz;
@@ -661,12 +622,7 @@ void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
         if (!have_fwd_levels) build_plan(c, Lv, nullptr, true, false, f.fwd, /*allow_chain=*/false);
         plan_values(c, Lv, nullptr, f.fwd);
     }
-    if (dims && build_axial_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.axial)) {
-        f.bwd.is_axial = true;
-        f.bwd.n = n;
-        f.bwd.n_dep = Uv.nnz;
-        f.bwd.n_levels = f.bwd.axial.nsteps;
-    } else if (dims && build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile)) {
+    if (dims && build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile)) {
         f.bwd.is_tile = true;
         f.bwd.n = n;
         f.bwd.n_dep = Uv.nnz;

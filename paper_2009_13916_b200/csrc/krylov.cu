@@ -436,135 +436,6 @@ __global__ void __launch_bounds__(RED_THREADS, DOTS2_MINB) k_dots2(const double*
     dcgs2_coeffs_block(dot, j, m, H, h1, coef, hcol);
 }
 
-// TMA-pipelined variant of k_dots2 (EDFA_DOTS2_TMA): one block per SM streams its
-// element range in chunks of D2T_CH elements of all nv+1 vectors into shared
-// memory with cp.async.bulk (D2T_ST stages in flight, ~100 KB per SM, independent
-// of the register budget); warp k % 8 owns vector k's two dots.  Same partial
-// layout and last-block epilogue as k_dots2.  Needs ldv, range even, V 16-byte aligned.
-#ifndef EDFA_DOTS2_TMA
-#define EDFA_DOTS2_TMA 0
-#endif
-constexpr int D2T_CH = 128, D2T_ST = 3, D2T_MAXK = 8;
-__device__ __forceinline__ unsigned d2t_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__global__ void __launch_bounds__(RED_THREADS, 1) k_dots2_tma(const double* __restrict__ V, int64_t ldv, int nv,
-                                                              int64_t n, int64_t range, double* __restrict__ partial,
-                                                              int pr, unsigned* counter, int j, int m,
-                                                              double* __restrict__ H, double* __restrict__ h1,
-                                                              double* __restrict__ coef, double* __restrict__ hcol) {
-    extern __shared__ __align__(128) double d2t_buf[];   // [D2T_ST][nv+1][D2T_CH]
-    __shared__ __align__(8) uint64_t full[D2T_ST];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int nvec = nv + 1;   // V_0..V_{nv-1} (u = V_{nv-1}) and w = V_nv
-    const int64_t lo = (int64_t)blockIdx.x * range, hi = min(n, lo + range);
-    const int nch = hi > lo ? (int)((hi - lo + D2T_CH - 1) / D2T_CH) : 0;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < D2T_ST; ++s)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(d2t_saddr(&full[s])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    auto issue = [&](int c) {   // thread 0: stage c % D2T_ST <- chunk c of every vector
-        const int s = c % D2T_ST;
-        const int64_t c0 = lo + (int64_t)c * D2T_CH;
-        const unsigned bytes = (unsigned)(min((int64_t)D2T_CH, hi - c0) * 8);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(d2t_saddr(&full[s])),
-                     "r"(bytes * nvec) : "memory");
-        double* dst = d2t_buf + (size_t)s * nvec * D2T_CH;
-        for (int k = 0; k < nvec; ++k)
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                         ::"r"(d2t_saddr(dst + (size_t)k * D2T_CH)), "l"(V + (int64_t)k * ldv + c0), "r"(bytes),
-                         "r"(d2t_saddr(&full[s])) : "memory");
-    };
-    if (threadIdx.x == 0)
-        for (int c = 0; c < min(nch, D2T_ST); ++c) issue(c);
-    double au[D2T_MAXK], aw[D2T_MAXK];
-#pragma unroll
-    for (int q = 0; q < D2T_MAXK; ++q) au[q] = aw[q] = 0.0;
-    for (int c = 0; c < nch; ++c) {
-        const int s = c % D2T_ST;
-        const unsigned par = (unsigned)((c / D2T_ST) & 1);
-        asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-                     "@!p bra WAIT_%=;\n\t}" ::"r"(d2t_saddr(&full[s])), "r"(par) : "memory");
-        const int cnt = (int)min((int64_t)D2T_CH, hi - (lo + (int64_t)c * D2T_CH));
-        const double* st = d2t_buf + (size_t)s * nvec * D2T_CH;
-        const double2* u2 = reinterpret_cast<const double2*>(st + (size_t)(nv - 1) * D2T_CH);
-        const double2* w2 = reinterpret_cast<const double2*>(st + (size_t)nv * D2T_CH);
-        double2 ue[D2T_CH / 64], we[D2T_CH / 64];
-#pragma unroll
-        for (int t = 0; t < D2T_CH / 64; ++t) {
-            const int e = lane + 32 * t;   // double2 index
-            const bool ok = 2 * e < cnt;
-            ue[t] = ok ? u2[e] : make_double2(0.0, 0.0);
-            we[t] = ok ? w2[e] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int q = 0; q < D2T_MAXK; ++q) {
-            const int k = wid + 8 * q;
-            if (k < nv) {
-                const double2* v2 = reinterpret_cast<const double2*>(st + (size_t)k * D2T_CH);
-#pragma unroll
-                for (int t = 0; t < D2T_CH / 64; ++t) {
-                    const int e = lane + 32 * t;
-                    if (2 * e < cnt) {
-                        const double2 v = v2[e];
-                        au[q] = fma(v.y, ue[t].y, fma(v.x, ue[t].x, au[q]));
-                        aw[q] = fma(v.y, we[t].y, fma(v.x, we[t].x, aw[q]));
-                    }
-                }
-            }
-        }
-        __syncthreads();   // stage s consumed by every warp
-        if (threadIdx.x == 0 && c + D2T_ST < nch) issue(c + D2T_ST);
-    }
-#pragma unroll
-    for (int q = 0; q < D2T_MAXK; ++q) {
-        const int k = wid + 8 * q;
-        const double x = warp_sum(au[q]), y = warp_sum(aw[q]);
-        if (lane == 0 && k < nv) {
-            partial[(int64_t)k * pr + blockIdx.x] = x;
-            partial[(int64_t)(64 + k) * pr + blockIdx.x] = y;
-        }
-    }
-    // last block: fixed-order sum over ranges, then the step's coefficients
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    // warp w sums the needed slots w, w+8, ... over the ranges (slot-major
-    // partials: lanes read consecutive ranges), fixed order: deterministic
-    __shared__ double dot[128];
-    {
-        const int nr = (int)(gridDim.x * gridDim.y), nw = RED_THREADS / 32;
-        for (int q = wid; q < 2 * nv; q += nw) {
-            const int slot = q < nv ? q : 64 + (q - nv);
-            const double* col = partial + (int64_t)slot * pr;
-            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-            int b = lane;
-            for (; b + 96 < nr; b += 128) {
-                acc0 += __ldcg(col + b);
-                acc1 += __ldcg(col + b + 32);
-                acc2 += __ldcg(col + b + 64);
-                acc3 += __ldcg(col + b + 96);
-            }
-            for (; b < nr; b += 32) acc0 += __ldcg(col + b);
-            const double t = warp_sum((acc0 + acc1) + (acc2 + acc3));
-            if (lane == 0) dot[slot] = t;
-        }
-    }
-    if (threadIdx.x == 0) *counter = 0u;
-    __syncthreads();
-    if (!coef) {   // dots only (slab-distributed solves reduce them across slabs first)
-        const int t = threadIdx.x;
-        if (t < 128) hcol[t] = (t < nv || (t >= 64 && t < 64 + nv)) ? dot[t] : 0.0;
-        return;
-    }
-    dcgs2_coeffs_block(dot, j, m, H, h1, coef, hcol);
-}
-
 // slot j  <- q_j     = coef[128] u - sum_k coef[k] V_k          (j >= 1)
 // slot j+1 <- u_{j+1} = coef[129] w + coef[130] u - sum_k coef[64+k] V_k
 template <bool VEC2>
@@ -719,22 +590,7 @@ struct Blas {
         {
             Prof pr(c, "gs_dots2", 8.0 * n * (nv + 1));
             dim3 grid(groups, (unsigned)ranges);
-            if (EDFA_DOTS2_TMA && v2 && nv <= 8 * D2T_MAXK) {
-                const int64_t rt = std::min<int64_t>(std::min<int64_t>(NUM_SMS_B200, part2_rows),
-                                                     (n + D2T_CH - 1) / D2T_CH);
-                int64_t rg = (n + rt - 1) / rt;
-                rg = (rg + 1) & ~int64_t(1);
-                const int64_t nr = (n + rg - 1) / rg;
-                const size_t smem = (size_t)D2T_ST * (nv + 1) * D2T_CH * sizeof(double);
-                static bool attr = false;
-                if (!attr) {
-                    EDFA_CUDA(cudaFuncSetAttribute(k_dots2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)((size_t)D2T_ST * 66 * D2T_CH * sizeof(double))));
-                    attr = true;
-                }
-                k_dots2_tma<<<(unsigned)nr, RED_THREADS, smem, c->stream>>>(V, n, nv, n, rg, part2, part2_rows, cnt,
-                                                                            j, m, H, h1, coef, hcol);
-            } else if (v2)
+            if (v2)
                 k_dots2<true><<<grid, RED_THREADS, 0, c->stream>>>(V, n, nv, n, range, part2, part2_rows, cnt, j, m, H,
                                                                   h1, coef, hcol);
             else
@@ -831,54 +687,33 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     const IcFactor& ic = s1->ic;
     const IluFactor& il = s2->ilu;
     // (L L^T)^{-1}: one fused chain kernel when the factor is chain-structured
-    const bool pair = ic.fwd.is_chain && ic.bwd.is_chain && ic.fwd.chain.max_len <= 256 && !getenv("EDFA_NO_IC_PAIR");
+    const bool pair = ic.fwd.is_chain && ic.bwd.is_chain && c->opt.ic_pair;
     if (!pair || !run_chain_pair(c, ic.fwd.chain, r_f, -1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_pair")) {
         run_plan(c, ic.fwd, r_f, -1.0, ws.a_f.p, nullptr, nullptr, "trsv_ic_L");
         run_plan(c, ic.bwd, ws.a_f.p, 1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_LT");
     }
-    const char* tk = getenv("EDFA_TILE_KERNEL");
-    const bool flow = !tk || (tk[0] != 'l' && tk[0] != 'p');
-    const bool fuse = nc && il.fwd.is_tile && il.bwd.is_tile && flow && !getenv("EDFA_NO_FILL_FUSION");
-    // fused SpMVs (A_cf t_f in the L solve's gather, A_fc y_c in the second IC pair)
-    // are opt-in: measured 2 ms/step slower on config 2 than the separate SELL SpMVs
-    // (the gathers sit on the solves' critical paths)
-    static const bool fuse_mv = getenv("EDFA_FUSE_SPMV") != nullptr;
+    const bool fuse = nc && il.fwd.is_tile && il.bwd.is_tile && c->opt.fill_fusion;
     if (nc) {
-        if (fuse && !fuse_mv) {
-            EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
-            spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
+        EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
+        spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
+        if (fuse) {
+            // L writes c_c (SENTINEL since the last apply's U solve consumed it)
+            // and pre-fills y_c; U consumes c_c (resets it) and writes y_c
             run_tile_ex(c, const_cast<TilePlan&>(il.fwd.tile), ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L",
                         true, false, y_c);
             run_tile_ex(c, const_cast<TilePlan&>(il.bwd.tile), ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U",
                         true, true, nullptr);
-        } else if (fuse) {
-            // L: rhs r_c - A_cf t_f formed in its gather (fused SpMV), writes c_c
-            // (SENTINEL since the last apply's U solve read it) and pre-fills y_c;
-            // U consumes c_c (resets it) and writes y_c
-            run_tile_ex(c, const_cast<TilePlan&>(il.fwd.tile), r_c, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L",
-                        true, false, y_c, sys->A_cf, ws.t_f.p);
-            run_tile_ex(c, const_cast<TilePlan&>(il.bwd.tile), ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U",
-                        true, true, nullptr);
         } else {
-            EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
-            spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
             run_plan(c, il.fwd, ws.u_c.p, 1.0, ws.c_c.p, nullptr, nullptr, "trsv_ilu_L");
             run_plan(c, il.bwd, ws.c_c.p, 1.0, y_c, nullptr, nullptr, "trsv_ilu_U");
             if (il.fwd.is_tile) fill_bits(c, ws.c_c.p, nc, SENTINEL_BITS);   // restore the invariant
         }
-        if (!pair || !fuse_mv) spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
+        spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
     } else if (nf) {
         EDFA_CUDA(cudaMemsetAsync(ws.a_f.p, 0, sizeof(double) * nf, c->stream));
     }
     if (nf) {
-        // second pair: its right-hand side A_fc y_c is formed in the chain kernel (fused SpMV)
-        bool done = false;
-        if (pair) {
-            if (nc && fuse_mv) done = run_chain_pair(c, ic.fwd.chain, nullptr, 1.0, nullptr, ws.t_f.p, y_f,
-                                                     "trsv_ic_pair", sys->A_fc, y_c);
-            else done = run_chain_pair(c, ic.fwd.chain, ws.a_f.p, 1.0, nullptr, ws.t_f.p, y_f, "trsv_ic_pair");
-            if (!done && nc && fuse_mv) spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
-        }
+        const bool done = pair && run_chain_pair(c, ic.fwd.chain, ws.a_f.p, 1.0, nullptr, ws.t_f.p, y_f, "trsv_ic_pair");
         if (!done) {
             run_plan(c, ic.fwd, ws.a_f.p, 1.0, y_f, nullptr, nullptr, "trsv_ic_L");
             // b and out2 alias row-wise only (thread r reads b[r] before writing out2[r])
@@ -916,130 +751,6 @@ struct Operator {
     }
 };
 
-static void check_trsv_error(Ctx* c) {
-    int e = 0;
-    EDFA_CUDA(cudaMemcpyAsync(&e, c->d_scalar_i + 8, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    if (e) {
-        EDFA_CUDA(cudaMemsetAsync(c->d_scalar_i + 8, 0, sizeof(int), c->stream));
-        throw Error(EDFA_ERR_CUDA, "triangular solve exceeded its spin limit (dependency never published)");
-    }
-}
-
-static void gmres_cgs2(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b,
-                       double* x, double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap) {
-    // Arnoldi with classical Gram-Schmidt applied twice (CGS2): two fused
-    // multi-dot + multi-axpy(+norm) passes, normalisation by a device-side
-    // norm.  The host never waits inside a cycle for the step it just
-    // enqueued: it enqueues step j, then reads back step j-1's Hessenberg
-    // column (async copy + event), applies the Givens rotations and tests
-    // convergence.  When step j-1 converges, the already-enqueued step j is
-    // discarded (its vector is never used).
-    require(rtol > 0.0, EDFA_ERR_VALUE, "tol must be positive");
-    require(m >= 1 && m <= 62, EDFA_ERR_VALUE, "restart must be in [1, 62]");
-    require(max_it >= 0, EDFA_ERR_VALUE, "max_it must be >= 0");
-    const int64_t n = (int64_t)sys->A.n_rows;
-    Operator op{c, sys, s1, s2, {}, n};
-    Blas bl(c);
-    *rep = edfa_report{0, 0, 0, 0, INFINITY};
-    auto push_hist = [&](double v) {
-        if (hist && rep->n_hist < hist_cap) hist[rep->n_hist] = v;
-        rep->n_hist++;
-    };
-    double bnorm = std::sqrt(bl.dot(b, b, n));
-    if (bnorm == 0.0) {
-        EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
-        rep->converged = 1;
-        rep->final_relres = 0.0;
-        push_hist(0.0);
-        EDFA_CUDA(cudaStreamSynchronize(c->stream));
-        return;
-    }
-    // per-step device slots (parity j & 1): [0, 64) pass-1 coefficients,
-    // [64, 128) pass-2 coefficients, 128 / 129 norms^2 after pass 1 / 2
-    DevBuf<double> V(c, (size_t)(m + 1) * n), z(c, n), r(c, n), hd(c, 2 * 192 + 64);
-    double* hpin = c->h_pinned;   // 2 x 192 host slots + 64 for y
-    cudaEvent_t ev[2] = {c->get_event(), c->get_event()};
-    EDFA_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, c->stream));
-    EDFA_CUDA(cudaMemcpyAsync(r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
-    double beta = bnorm;
-    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
-    bool happy = false;
-    auto enqueue_step = [&](int j) {
-        double* vj = V.p + (int64_t)j * n;
-        double* w = V.p + (int64_t)(j + 1) * n;
-        double* h = hd.p + (j & 1) * 192;
-        op.P(vj, z.p);
-        op.A(z.p, w);
-        bl.multidot(V.p, n, j + 1, w, n, h);
-        bl.multiaxpy(V.p, n, j + 1, h, 1.0, w, w, n, h + 128);
-        bl.multidot(V.p, n, j + 1, w, n, h + 64);
-        bl.multiaxpy(V.p, n, j + 1, h + 64, 1.0, w, w, n, h + 129);
-        bl.normalize(n, h + 129, w);
-        EDFA_CUDA(cudaMemcpyAsync(hpin + (j & 1) * 192, h, sizeof(double) * 130, cudaMemcpyDeviceToHost,
-                                  c->stream));
-        EDFA_CUDA(cudaEventRecord(ev[j & 1], c->stream));
-    };
-    while (rep->n_it < max_it) {
-        bl.axpby(n, 1.0 / beta, r.p, 0.0, V.p);
-        std::fill(H.begin(), H.end(), 0.0);
-        std::fill(g.begin(), g.end(), 0.0);
-        g[0] = beta;
-        int k = 0;
-        int enq = 0;                       // steps enqueued in this cycle
-        const int budget = std::min(m, max_it - rep->n_it);
-        enqueue_step(enq++);
-        for (int j = 0; j < budget; ++j) {
-            if (enq < budget) enqueue_step(enq++);        // keep one step ahead
-            EDFA_CUDA(cudaEventSynchronize(ev[j & 1]));
-            const double* hp = hpin + (j & 1) * 192;
-            rep->n_it++;
-            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hp[i] + hp[64 + i];
-            const double wn = std::sqrt(std::max(hp[129], 0.0));
-            H[(size_t)(j + 1) * m + j] = wn;
-            for (int i = 0; i < j; ++i) {
-                double a = H[(size_t)i * m + j], bb = H[(size_t)(i + 1) * m + j];
-                H[(size_t)i * m + j] = cs[i] * a + sn[i] * bb;
-                H[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * bb;
-            }
-            double den = std::hypot(H[(size_t)j * m + j], H[(size_t)(j + 1) * m + j]);
-            if (den == 0.0) { cs[j] = 1.0; sn[j] = 0.0; }
-            else { cs[j] = H[(size_t)j * m + j] / den; sn[j] = H[(size_t)(j + 1) * m + j] / den; }
-            H[(size_t)j * m + j] = den;
-            H[(size_t)(j + 1) * m + j] = 0.0;
-            g[j + 1] = -sn[j] * g[j];
-            g[j] = cs[j] * g[j];
-            double est = std::fabs(g[j + 1]) / bnorm;
-            push_hist(est);
-            k = j + 1;
-            if (wn == 0.0) { happy = true; break; }
-            if (est <= rtol) break;
-        }
-        // a speculatively enqueued step may still be running: everything below
-        // is stream-ordered after it and reads only V_0..V_{k-1}
-        for (int i = k - 1; i >= 0; --i) {   // back substitution H y = g
-            double sacc = g[i];
-            for (int t = i + 1; t < k; ++t) sacc -= H[(size_t)i * m + t] * y[t];
-            y[i] = H[(size_t)i * m + i] != 0.0 ? sacc / H[(size_t)i * m + i] : 0.0;
-        }
-        for (int i = 0; i < k; ++i) hpin[384 + i] = y[i];
-        double* yd = hd.p + 2 * 192;
-        EDFA_CUDA(cudaMemcpyAsync(yd, hpin + 384, sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
-        bl.multiaxpy(V.p, n, k, yd, 1.0, nullptr, r.p, n, nullptr);   // r <- V y (scratch)
-        op.P(r.p, z.p);
-        bl.axpby(n, 1.0, z.p, 1.0, x);
-        op.A(x, r.p);
-        bl.axpby(n, 1.0, b, -1.0, r.p);                                   // r = b - A x
-        beta = std::sqrt(bl.dot(r.p, r.p, n));
-        check_trsv_error(c);
-        if (beta / bnorm <= rtol) { rep->converged = 1; break; }
-        if (happy || beta == 0.0) { rep->breakdown = 1; break; }
-    }
-    c->event_pool.push_back(ev[0]);
-    c->event_pool.push_back(ev[1]);
-    rep->final_relres = beta / bnorm;
-    if (rep->n_it == 0) push_hist(beta / bnorm);
-}
 
 void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* b, double* x,
            double rtol, int m, int max_it, edfa_report* rep, double* hist, int hist_cap) {
@@ -1051,13 +762,10 @@ void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_sta
     // Givens rotations and tests the estimate, so the GPU never idles between
     // steps.  Speculatively enqueued steps only touch slots above the ones the
     // solution update reads.  Convergence is confirmed on the true residual.
-    if (getenv("EDFA_GMRES_CGS2")) {
-        gmres_cgs2(c, sys, s1, s2, b, x, rtol, m, max_it, rep, hist, hist_cap);
-        return;
-    }
     require(rtol > 0.0, EDFA_ERR_VALUE, "tol must be positive");
     require(m >= 1 && m <= 62, EDFA_ERR_VALUE, "restart must be in [1, 62]");
     require(max_it >= 0, EDFA_ERR_VALUE, "max_it must be >= 0");
+    c->trsv_err_reset();   // a stale flag of an earlier call must not leak into this solve
     const int64_t n = (int64_t)sys->A.n_rows;
     Operator op{c, sys, s1, s2, {}, n};
     Blas bl(c);
@@ -1152,7 +860,7 @@ void gmres(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_sta
         op.A(x, r.p);
         bl.axpby(n, 1.0, b, -1.0, r.p);                                   // r = b - A x
         beta = std::sqrt(bl.dot(r.p, r.p, n));
-        check_trsv_error(c);
+        c->trsv_err_check();
         if (beta / bnorm <= rtol) { rep->converged = 1; break; }
         if (happy || beta == 0.0) { rep->breakdown = 1; break; }
     }
@@ -1166,6 +874,7 @@ void bicgstab(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_
               double* x, double rtol, int max_it, edfa_report* rep, double* hist, int hist_cap) {
     // operation-for-operation restatement of hx/krylov.py:40-115
     require(rtol > 0.0, EDFA_ERR_VALUE, "tol must be positive");
+    c->trsv_err_reset();
     const int64_t n = (int64_t)sys->A.n_rows;
     Operator op{c, sys, s1, s2, {}, n};
     Blas bl(c);
@@ -1238,7 +947,7 @@ void bicgstab(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_
     op.A(x, t.p);
     bl.axpby(n, 1.0, b, -1.0, t.p);
     rep->final_relres = std::sqrt(bl.dot(t.p, t.p, n)) / bnorm;
-    check_trsv_error(c);
+    c->trsv_err_check();
 }
 
 // exported to capi.cu

@@ -61,7 +61,7 @@ void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, doubl
 // the chains are too long for the fused kernel (caller runs the two solves)
 // fz (optional): b := fz x (a fused SpMV; rows of fz = rows of the factor), b itself is ignored
 bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add,
-                    double* out2, const char* name, const Csr* fz = nullptr, const double* fz_x = nullptr);
+                    double* out2, const char* name);
 void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, const double* scale, double* diag,
                int* shifts, double fill_tol = 0.0);
 
@@ -70,12 +70,12 @@ struct TilePlan {               // tile-DAG solves of cell-indexed factors (tile
     int32_t RC = 0, KD = 0, EC = 0, LC = 0;   // rows / early deps / externals / levels per tile
     int64_t n_dep = 0;
     bool unit = false;
-    DevBuf<int32_t> hdr, row_id, ext_id, up_cnt, up_ids, flags, ticket, order;
+    DevBuf<int32_t> hdr, row_id, ext_id, up_cnt, up_ids, order;   // up_*: tile DAG (schedule order)
+    DevBuf<unsigned> ticket;
     DevBuf<short> lev_ptr, dslot, eslot;     // critical / early dependency slots
     DevBuf<double> dcoef, ecoef, dinv;       // critical / early coefficients
     DevBuf<short> xlev_ptr;                  // externals first needed below level l: [0, xlev_ptr[l])
-    DevBuf<unsigned char> req;               // [LC][32]: upstream levels needed before loading level l
-    int32_t epoch = 0, ticket_base = 0;
+    unsigned ticket_base = 0;                // tickets wrap modulo 2^32
 };
 // dims = {nx, ny, nz} of the cell grid (rows = cells in natural order) or NULL
 bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
@@ -90,23 +90,7 @@ void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x,
                  const char* name, bool x_prefilled, bool consume_b, double* pre_sent, const Csr* fz = nullptr,
                  const double* fz_x = nullptr);
 
-struct AxialPlan {              // pencil solves of axial-stencil cell factors (axial.cu)
-    int32_t n = 0, R = 0, NJ = 0, NK = 0, nsteps = 0;
-    int32_t dims[3] = {0, 0, 0};
-    bool reverse = false;
-    int64_t n_dep = 0;
-    DevBuf<double> coef;        // [block][step][3R+1][64]
-    DevBuf<int32_t> order, ticket;
-    int32_t ticket_base = 0;
-};
-bool build_axial_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
-                      AxialPlan& p);
-void run_axial(Ctx* c, AxialPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
-               const char* name);
-
 struct TriPlan {
-    bool is_axial = false;
-    AxialPlan axial;
     bool is_chain = false;
     ChainPlan chain;
     bool is_tile = false;

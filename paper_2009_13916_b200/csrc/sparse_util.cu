@@ -187,7 +187,7 @@ __global__ void k_sub(CsrV A, CsrV H, double tau, int32_t* __restrict__ cnt, con
 }
 
 template <bool FILL>
-__global__ void k_filter(CsrV A, double tau, int32_t* __restrict__ cnt, const int32_t* __restrict__ Sp,
+__global__ void k_filter(CsrV A, double tau, bool keep_diag, int32_t* __restrict__ cnt, const int32_t* __restrict__ Sp,
                          int32_t* __restrict__ Si, double* __restrict__ Sv) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.n_rows) return;
@@ -199,7 +199,7 @@ __global__ void k_filter(CsrV A, double tau, int32_t* __restrict__ cnt, const in
     for (int p = a; p < a1; ++p) {
         double v = A.val[p];
         int col = A.idx[p];
-        if (v != 0.0 && (col == i || !(fabs(v) < thr))) {
+        if (v != 0.0 && ((keep_diag && col == i) || !(fabs(v) < thr))) {
             if (FILL) { Si[o + n] = col; Sv[o + n] = v; }
             ++n;
         }
@@ -383,7 +383,7 @@ void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S) {
     }
 }
 
-void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out) {
+void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out, bool keep_diag) {
     int n = A.n_rows;
     out.n_rows = n;
     out.n_cols = A.n_cols;
@@ -391,7 +391,7 @@ void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out) {
     DevBuf<int32_t> cnt(c, std::max(n, 1));
     if (n) {
         Prof pr(c, "filter_rows", 12.0 * A.nnz);
-        k_filter<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), tau, cnt.p, nullptr, nullptr, nullptr);
+        k_filter<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), tau, keep_diag, cnt.p, nullptr, nullptr, nullptr);
         check_launch("k_filter count");
     }
     out.nnz = scan_counts(c, cnt.p, out.ptr.p, n);
@@ -399,7 +399,7 @@ void csr_filter(Ctx* c, const Csr& A, double tau, Csr& out) {
     out.val.reset(c, out.nnz);
     if (n) {
         Prof pr(c, "filter_rows", 12.0 * (A.nnz + out.nnz));
-        k_filter<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), tau, nullptr, out.ptr.p, out.idx.p,
+        k_filter<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), tau, keep_diag, nullptr, out.ptr.p, out.idx.p,
                                                                out.val.p);
         check_launch("k_filter fill");
     }

@@ -4,22 +4,13 @@
 // into tx*ty*tz tiles; when every dependency of a row lies in its own tile or
 // in a tile that precedes it in natural tile order (true for the axial
 // stencils of base/static patterns on structured grids -- checked, otherwise
-// the caller falls back to the level-synchronous solver), the tiles form a
-// DAG of depth ~ NX+NY+NZ instead of the row DAG's nx+ny+nz.
+// the caller falls back to the level solvers), the tiles form a DAG.
 //
-// One persistent CTA per SM takes tiles in tile-level order from a ticket:
-//   1. stage the tile's plan (TMA bulk copies into shared memory) -- the plan
-//      is constant, so this overlaps the wait for upstream tiles;
-//   2. gather the tile's right-hand side, wait for the upstream tiles' epoch
-//      flags (one poller per upstream), gather the external dependencies;
-//   3. sweep the local levels.  The sweep is software-pipelined in two roles:
-//      "critical" lanes finish level k using only the dependencies on level
-//      k-1; "early" lanes fold every other dependency (earlier levels and
-//      externals, already final) of level k+1 into its partial sums.  Every
-//      lane's plan record for its next step is prefetched into registers, so
-//      a step's critical path is one shared-memory gather, a short FMA chain
-//      and a barrier;
-//   4. write the tile's solution to HBM and publish the tile's flag.
+// One persistent CTA per SM takes tiles in tile-level order from a ticket,
+// stages the tile's plan (TMA bulk copies into shared memory) and solves it
+// as a dataflow: every x slot (rows and externals) starts as the SENTINEL
+// pattern, so a stored value is its own ready flag -- no per-level barrier,
+// no per-tile flag (k_tile_flow below).
 //
 // Plan records are stored per level, column-major ([dep k][row r]) so the
 // lanes of a step read consecutive addresses.
@@ -39,8 +30,6 @@
 namespace edfa {
 namespace {
 
-constexpr int ROLE = 64;            // rows per level handled in one step
-constexpr int TILE_THREADS = 3 * ROLE;   // 2 warps critical (lane per row) + 4 warps early (2 lanes per row)
 constexpr int CK = 4;               // critical dependencies per row (axial stencils: <= 3)
 constexpr int EKMAX = 32;           // early dependencies per row
 
@@ -104,7 +93,6 @@ struct TileBuild {
     int MD;               // max dependencies of a row
     int* glev;            // local level of every row (written by the count pass)
     short* xlev_ptr;      // LC per tile: externals first needed below level l
-    unsigned char* req;   // LC*32 per tile: upstream progress needed to load externals < l+1
 };
 
 __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
@@ -181,8 +169,6 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
         for (int l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
         short* lp = b.lev_ptr + (size_t)t * b.LC;
         for (int l = 0; l <= nlev && l < b.LC; ++l) lp[l] = (short)cnt[l];
-        for (int l = 0; l < nlev; ++l)
-            if (cnt[l + 1] - cnt[l] > ROLE) atomicExch(b.err, 9);   // level wider than a role
         for (int r = 0; r < n; ++r) {
             int p = cnt[lev[r]]++;
             order[p] = r;
@@ -247,22 +233,18 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
         }
     }
     __syncthreads();
-    __shared__ int upl[32];   // compacted upstream list
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {   // compacted upstream list (tile DAG -> schedule order)
         int nu = 0;
         int* up = b.up_ids + (size_t)t * 32;
         for (int z = 0; z < 32; ++z)
-            if (ups[z] >= 0) { upl[nu] = ups[z]; up[nu++] = ups[z]; }
-        for (int z = nu; z < 32; ++z) upl[z] = -1;
+            if (ups[z] >= 0) up[nu++] = ups[z];
         b.up_cnt[t] = nu;
     }
     // externals ordered by the first local level that needs them (pipelined
     // loading); fn[q] = min level of a consumer row of ext[q]
     int* fn = misc + 8 + HS;                          // EC
     int* npos = fn + b.EC;                            // EC: id-sorted index -> need-sorted index
-    int* reqs = npos + b.EC;                          // LC*32
     for (int q = threadIdx.x; q < ne; q += blockDim.x) fn[q] = INT32_MAX;
-    for (int q = threadIdx.x; q < b.LC * 32; q += blockDim.x) reqs[q] = 0;
     __syncthreads();
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
         int row = cell[r];
@@ -294,24 +276,8 @@ __global__ void __launch_bounds__(256) k_tile_build(TileBuild b) {
         }
     for (int p = threadIdx.x; p < ne; p += blockDim.x) npos[srt[p] & 4095] = p;
     __syncthreads();
-    for (int q = threadIdx.x; q < ne; q += blockDim.x) {
-        b.ext_id[(size_t)t * b.EC + npos[q]] = ext[q];
-        const int u = g.tile_of(ext[q]);
-        int ui = 0;
-        while (ui < 31 && upl[ui] != u) ++ui;
-        const int need = b.glev[ext[q]] + 1;
-        if (need > 255) atomicExch(b.err, 12);
-        if (fn[q] < b.LC) atomicMax(&reqs[fn[q] * 32 + ui], need);
-    }
+    for (int q = threadIdx.x; q < ne; q += blockDim.x) b.ext_id[(size_t)t * b.EC + npos[q]] = ext[q];
     __syncthreads();
-    if (threadIdx.x < 32) {            // cumulative over levels, per upstream tile
-        int m = 0;
-        unsigned char* rq = b.req + (size_t)t * b.LC * 32;
-        for (int l = 0; l < b.LC; ++l) {
-            m = max(m, reqs[l * 32 + threadIdx.x]);
-            rq[l * 32 + threadIdx.x] = (unsigned char)m;
-        }
-    }
     if (threadIdx.x == 0) {            // xlev_ptr[l] = #externals with fn < l
         short* xl = b.xlev_ptr + (size_t)t * b.LC;
         int q = 0;
@@ -404,36 +370,23 @@ struct TileSolve {
     const short* es;
     const double* ec;
     const double* dinv;
-    const int* up_cnt;
-    const int* up_ids;
-    int* flags;
-    int* ticket;
-    int epoch;
-    int ticket_base;
+    unsigned* ticket;
+    unsigned ticket_base;  // tickets wrap modulo 2^32 (well defined for unsigned)
     const double* b;
     double alpha;
     double* x;
     const double* add;
     double* out2;
     int* err;
-    long long* dbg;
     const short* xlev_ptr;
-    const unsigned char* req;
-    int mode;             // EDFA_TILE_MODE experiment bits (diagnostics)
-    long long* dbg2;      // per-group timestamps (diagnostics): [tile][64][5]
-    double* b_sent;       // flow kernel: == b, whose tile rows are reset to SENTINEL once read (or NULL)
-    const int32_t* fz_ptr;   // flow kernel: fused right-hand side b - M x (CSR rows = this factor's rows) or NULL
+    double* b_sent;       // == b, whose tile rows are reset to SENTINEL once read (or NULL)
+    const int32_t* fz_ptr;   // fused right-hand side b - M x (CSR rows = this factor's rows) or NULL
     const int32_t* fz_idx;
     const double* fz_val;
     const double* fz_x;
-    double* pre_sent;     // flow kernel: another vector whose tile rows are set to SENTINEL (or NULL)
+    double* pre_sent;     // another vector whose tile rows are set to SENTINEL (or NULL)
 };
 
-__device__ __forceinline__ long long gtimer() {
-    long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 __device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned r16(unsigned b) { return (b + 15u) & ~15u; }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mbar) {
@@ -442,457 +395,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mbar)) : "memory");
 }
 
-// per-lane step record: the row, its dependencies (slot, coefficient)
-template <int K>
-struct Rec {
-    int p;             // sorted row slot, -1 if the lane is idle in this step
-    short s[K];
-    double c[K];
-    double d;          // 1/diag (critical role)
-};
-
-template <int K>
-__device__ __forceinline__ void rec_load(Rec<K>& rc, const short* lp, int nlev, int lv, int lane, const short* S,
-                                         const double* C, const double* di) {
-    rc.p = -1;
-    if (lv < 0 || lv >= nlev) return;
-    const int l0 = lp[lv], R = lp[lv + 1] - l0;
-    if (lane >= R) return;
-    rc.p = l0 + lane;
-    const short* sb = S + (size_t)l0 * K + lane;
-    const double* cb = C + (size_t)l0 * K + lane;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        rc.s[k] = sb[k * R];
-        rc.c[k] = cb[k * R];
-    }
-    rc.d = di[rc.p];
-}
-
-// early record split over a lane pair: lane li of row r takes deps li, li+2, ...
-template <int KH>
-__device__ __forceinline__ void rec_load_pair(Rec<KH>& rc, const short* lp, int nlev, int lv, int r, int li,
-                                              const short* S, const double* C) {
-    rc.p = -1;
-    if (lv < 0 || lv >= nlev) return;
-    const int l0 = lp[lv], R = lp[lv + 1] - l0;
-    if (r >= R) return;
-    rc.p = l0 + r;
-    const short* sb = S + (size_t)l0 * (2 * KH) + r + li * R;
-    const double* cb = C + (size_t)l0 * (2 * KH) + r + li * R;
-#pragma unroll
-    for (int k = 0; k < KH; ++k) {
-        rc.s[k] = sb[2 * k * R];
-        rc.c[k] = cb[2 * k * R];
-    }
-}
-
-template <int EK>
-__global__ void __launch_bounds__(TILE_THREADS) k_tile_solve(TileSolve a) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    // 16-byte aligned sections (capacities padded on the host, see tile_smem_bytes)
-    double* xs = reinterpret_cast<double*>(sm);                     // RC + EC + 2
-    double* cc = xs + a.RC + a.EC + 2;                              // RC*CK
-    double* ecf = cc + (size_t)a.RC * CK;                           // RC*EK
-    double* di = ecf + (size_t)a.RC * EK;                           // RC
-    int* rid = reinterpret_cast<int*>(di + a.RC);                   // RC
-    int* eid_s = rid + a.RC;                                        // EC (external row ids)
-    short* cs = reinterpret_cast<short*>(eid_s + a.EC);             // RC*CK
-    short* es = cs + (size_t)a.RC * CK;                             // RC*EK
-    short* lp = es + (size_t)a.RC * EK;                             // LC
-    __shared__ int s_tile, s_hdr[4];
-    __shared__ __align__(8) uint64_t mbar;
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&mbar)), "r"(1) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    unsigned phase = 0;
-    const bool crit = threadIdx.x < ROLE;
-    const int lane = crit ? threadIdx.x : (threadIdx.x - ROLE) >> 1;   // row within the step
-    const int li = (threadIdx.x - ROLE) & 1;                            // early: half of the deps
-    constexpr int KH = EK / 2;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            int k = atomicAdd(a.ticket, 1) - a.ticket_base;
-            int t = k < a.n_tiles ? a.order[k] : -1;
-            s_tile = t;
-            if (t >= 0) {
-                const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
-                s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z;
-                const unsigned n = h.x;
-                unsigned b_cs = r16(2u * n * CK), b_cc = r16(8u * n * CK), b_es = r16(2u * n * EK),
-                         b_ec = r16(8u * n * EK), b_di = r16(8u * n), b_ri = r16(4u * n), b_lp = r16(2u * (h.z + 1));
-                unsigned b_ei = r16(4u * h.y);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                             ::"r"(smem_addr(&mbar)), "r"(b_cs + b_cc + b_es + b_ec + b_di + b_ri + b_lp + b_ei)
-                             : "memory");
-                bulk_g2s(eid_s, a.ext_id + (size_t)t * a.EC, b_ei, &mbar);
-                bulk_g2s(cs, a.cs + (size_t)t * a.RC * CK, b_cs, &mbar);
-                bulk_g2s(cc, a.cc + (size_t)t * a.RC * CK, b_cc, &mbar);
-                bulk_g2s(es, a.es + (size_t)t * a.RC * EK, b_es, &mbar);
-                bulk_g2s(ecf, a.ec + (size_t)t * a.RC * EK, b_ec, &mbar);
-                bulk_g2s(di, a.dinv + (size_t)t * a.RC, b_di, &mbar);
-                bulk_g2s(rid, a.row_id + (size_t)t * a.RC, b_ri, &mbar);
-                bulk_g2s(lp, a.lev_ptr + (size_t)t * a.LC, b_lp, &mbar);
-            }
-        }
-        __syncthreads();
-        const int t = s_tile;
-        if (t < 0) break;
-        const int n = s_hdr[0], ne = s_hdr[1], nlev = s_hdr[2];
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 0] = gtimer();
-        {
-            unsigned done = 0;
-            while (!done)
-                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                             : "=r"(done) : "r"(smem_addr(&mbar)), "r"(phase) : "memory");
-            phase ^= 1u;
-        }
-        // right-hand side into the x slots (independent of upstream tiles)
-        for (int p0 = 0; p0 < n; p0 += 8 * TILE_THREADS) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                int p = p0 + u * TILE_THREADS + threadIdx.x;
-                v[u] = p < n ? __ldg(a.b + rid[p]) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                int p = p0 + u * TILE_THREADS + threadIdx.x;
-                if (p < n) xs[p] = a.alpha * v[u];
-            }
-        }
-        if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
-        // first step records (plan constants) before waiting
-        Rec<CK> rcr;
-        Rec<KH> rer;
-        if (crit) rec_load<CK>(rcr, lp, nlev, 0, lane, cs, cc, di);
-        else rec_load_pair<KH>(rer, lp, nlev, 0, lane, li, es, ecf);
-        // wait for upstream tiles (relaxed polls: no L1 invalidation per poll)
-        const int nu = a.up_cnt[t];
-        if (threadIdx.x < nu) {
-            const int* f = a.flags + a.up_ids[(size_t)t * 32 + threadIdx.x];
-            unsigned ns = 8;
-            long long spins = 0;
-            while (ld_relaxed_i(f) != a.epoch) {
-                __nanosleep(ns);
-                if (ns < 64) ns <<= 1;
-                if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
-            }
-            __threadfence();
-        }
-        __syncthreads();
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
-        {
-            const int* eid = eid_s;
-            for (int q0 = 0; q0 < ne; q0 += 8 * TILE_THREADS) {
-                int id[8];
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    int q = q0 + u * TILE_THREADS + threadIdx.x;
-                    id[u] = q < ne ? eid[q] : -1;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = id[u] >= 0 ? __ldcg(a.x + id[u]) : 0.0;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    int q = q0 + u * TILE_THREADS + threadIdx.x;
-                    if (q < ne) xs[a.RC + q] = v[u];
-                }
-            }
-        }
-        __syncthreads();
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 2] = gtimer();
-        const long long c_lev0 = clock64();
-        // pipelined level sweep: step k = critical(level k) || early(level k+1)
-        // step -1 only folds the early deps of level 0
-        // early half-sum of a lane pair; lane li == 0 folds it into the partial
-        auto early = [&]() {
-            double a2[2] = {0.0, 0.0};
-            if (rer.p >= 0) {
-#pragma unroll
-                for (int u = 0; u < KH; ++u) a2[u & 1] = fma(-rer.c[u], xs[rer.s[u]], a2[u & 1]);
-            }
-            double h = a2[0] + a2[1];
-            h += __shfl_xor_sync(0xffffffffu, h, 1);
-            if (rer.p >= 0 && li == 0) xs[rer.p] += h;
-        };
-        if (!crit) {
-            early();
-            rec_load_pair<KH>(rer, lp, nlev, 1, lane, li, es, ecf);
-        }
-        __syncthreads();
-        for (int k = 0; k < nlev; ++k) {
-            if (crit) {
-                if (rcr.p >= 0) {
-                    double x0 = xs[rcr.s[0]], x1 = xs[rcr.s[1]], x2 = xs[rcr.s[2]], x3 = xs[rcr.s[3]];
-                    double acc = xs[rcr.p];
-                    acc = fma(-rcr.c[0], x0, acc);
-                    acc = fma(-rcr.c[1], x1, acc);
-                    acc = fma(-rcr.c[2], x2, acc);
-                    acc = fma(-rcr.c[3], x3, acc);
-                    xs[rcr.p] = acc * rcr.d;
-                }
-                rec_load<CK>(rcr, lp, nlev, k + 1, lane, cs, cc, di);
-            } else {
-                early();
-                rec_load_pair<KH>(rer, lp, nlev, k + 2, lane, li, es, ecf);
-            }
-            __syncthreads();
-        }
-        const long long c_lev1 = clock64();
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 3] = gtimer();
-        for (int p = threadIdx.x; p < n; p += TILE_THREADS) {
-            int row = rid[p];
-            double v = xs[p];
-            __stcg(a.x + row, v);
-            if (a.out2) a.out2[row] = v + a.add[row];
-        }
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0)
-            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(a.flags + t), "r"(a.epoch) : "memory");
-        if (a.dbg && threadIdx.x == 0) {
-            a.dbg[t * 6 + 4] = gtimer();
-            a.dbg[t * 6 + 5] = (c_lev1 - c_lev0) / (nlev + 1);
-        }
-    }
-}
-
-
-// ---------------------------------------------------------------------------
-// Pipelined tile solve: a tile starts as soon as its first levels' external
-// dependencies exist instead of after its upstream tiles have finished.
-//   * compute warps (6): the pipelined level sweep of k_tile_solve; critical
-//     lanes also store every finished row to HBM (x is SENTINEL-filled before
-//     the launch, so a stored value is its own "ready" flag);
-//   * loader warp: polls the external values in need order (relaxed loads,
-//     sentinel = not produced yet) and copies them into shared memory,
-//     publishing how many local levels have all their externals.
-// A downstream tile therefore runs a few levels behind its upstream tiles (a
-// wavefront): the critical path is ~ the row DAG depth plus one L2 round
-// trip per tile boundary, with no flag, fence or publisher on the way.
-constexpr int PIPE_THREADS = TILE_THREADS + 32;
-constexpr int LOADER_WARP = TILE_THREADS / 32;
-
-__device__ __forceinline__ void bar_compute() { asm volatile("bar.sync 1, %0;" ::"n"(TILE_THREADS) : "memory"); }
-__device__ __forceinline__ int ld_acquire_cta(const int* p) {
-    int v;
-    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_cta(int* p, int v) {
-    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
-}
 __device__ __forceinline__ double ld_relaxed_d(const double* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return __longlong_as_double((long long)v);
 }
-
-template <int EK>
-__global__ void __launch_bounds__(PIPE_THREADS) k_tile_pipe(TileSolve a) {
-    extern __shared__ __align__(128) unsigned char sm[];
-    double* xs = reinterpret_cast<double*>(sm);                     // RC + EC + 2
-    double* cc = xs + a.RC + a.EC + 2;                              // RC*CK
-    double* ecf = cc + (size_t)a.RC * CK;                           // RC*EK
-    double* di = ecf + (size_t)a.RC * EK;                           // RC
-    int* rid = reinterpret_cast<int*>(di + a.RC);                   // RC
-    int* eid_s = rid + a.RC;                                        // EC (external row ids, need-sorted)
-    short* cs = reinterpret_cast<short*>(eid_s + a.EC);             // RC*CK
-    short* es = cs + (size_t)a.RC * CK;                             // RC*EK
-    short* lp = es + (size_t)a.RC * EK;                             // LC
-    short* xl = lp + a.LC;                                          // LC
-    __shared__ int s_tile, s_hdr[4], s_ready;
-    __shared__ __align__(8) uint64_t mbar;
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&mbar)), "r"(1) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    unsigned phase = 0;
-    const int warp = threadIdx.x >> 5, lane32 = threadIdx.x & 31;
-    const bool crit = threadIdx.x < ROLE;
-    const int lane = crit ? threadIdx.x : (threadIdx.x - ROLE) >> 1;
-    const int li = (threadIdx.x - ROLE) & 1;
-    constexpr int KH = EK / 2;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            int k = atomicAdd(a.ticket, 1) - a.ticket_base;
-            int t = k < a.n_tiles ? a.order[k] : -1;
-            s_tile = t;
-            s_ready = 0;
-            if (t >= 0) {
-                const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
-                s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z;
-                const unsigned n = h.x;
-                unsigned b_cs = r16(2u * n * CK), b_cc = r16(8u * n * CK), b_es = r16(2u * n * EK),
-                         b_ec = r16(8u * n * EK), b_di = r16(8u * n), b_ri = r16(4u * n), b_lp = r16(2u * (h.z + 1));
-                unsigned b_ei = r16(4u * h.y), b_xl = r16(2u * (h.z + 1));
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                             ::"r"(smem_addr(&mbar)),
-                             "r"(b_cs + b_cc + b_es + b_ec + b_di + b_ri + b_lp + b_ei + b_xl)
-                             : "memory");
-                bulk_g2s(eid_s, a.ext_id + (size_t)t * a.EC, b_ei, &mbar);
-                bulk_g2s(cs, a.cs + (size_t)t * a.RC * CK, b_cs, &mbar);
-                bulk_g2s(cc, a.cc + (size_t)t * a.RC * CK, b_cc, &mbar);
-                bulk_g2s(es, a.es + (size_t)t * a.RC * EK, b_es, &mbar);
-                bulk_g2s(ecf, a.ec + (size_t)t * a.RC * EK, b_ec, &mbar);
-                bulk_g2s(di, a.dinv + (size_t)t * a.RC, b_di, &mbar);
-                bulk_g2s(rid, a.row_id + (size_t)t * a.RC, b_ri, &mbar);
-                bulk_g2s(lp, a.lev_ptr + (size_t)t * a.LC, b_lp, &mbar);
-                bulk_g2s(xl, a.xlev_ptr + (size_t)t * a.LC, b_xl, &mbar);
-            }
-        }
-        __syncthreads();
-        const int t = s_tile;
-        if (t < 0) break;
-        const int n = s_hdr[0], ne = s_hdr[1], nlev = s_hdr[2];
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 0] = gtimer();
-        {
-            unsigned done = 0;
-            while (!done)
-                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                             : "=r"(done) : "r"(smem_addr(&mbar)), "r"(phase) : "memory");
-            phase ^= 1u;
-        }
-        for (int p0 = 0; p0 < n; p0 += 8 * PIPE_THREADS) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                int p = p0 + u * PIPE_THREADS + threadIdx.x;
-                v[u] = p < n ? __ldg(a.b + rid[p]) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                int p = p0 + u * PIPE_THREADS + threadIdx.x;
-                if (p < n) xs[p] = a.alpha * v[u];
-            }
-        }
-        if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
-        __syncthreads();
-        if (warp == LOADER_WARP) {
-            // ---- loader: externals in need order; q0 = first entry not yet seen.
-            // LW loads in flight per lane (one L2 round trip per LW*32 entries)
-            constexpr int LW = 16;
-            int q0 = 0, lv = 0;
-            long long spins = 0;
-            while (q0 < ne) {
-                const int qe = min(ne, q0 + LW * 32);
-                double v[LW];
-#pragma unroll
-                for (int u = 0; u < LW; ++u) {
-                    const int q = q0 + u * 32 + lane32;
-                    v[u] = q < qe ? ld_relaxed_d(a.x + eid_s[q]) : 0.0;
-                }
-                int adv = qe - q0;
-#pragma unroll
-                for (int u = 0; u < LW; ++u) {
-                    const int q = q0 + u * 32 + lane32;
-                    const bool ok = q >= qe || !is_sentinel(v[u]);
-                    if (q < qe && ok) xs[a.RC + q] = v[u];
-                    const unsigned miss = __ballot_sync(0xffffffffu, !ok);
-                    if (miss && adv == qe - q0) adv = u * 32 + __ffs(miss) - 1;
-                }
-                if (adv == 0) {
-                    __nanosleep(32);
-                    if (++spins > SPIN_LIMIT) { if (lane32 == 0) atomicExch(a.err, 7); break; }
-                    continue;
-                }
-                spins = 0;
-                q0 += adv;
-                while (lv < nlev && xl[lv + 1] <= q0) ++lv;   // levels [0, lv) have all externals
-                __syncwarp();
-                if (lane32 == 0) st_release_cta(&s_ready, lv);
-            }
-            if (lane32 == 0) st_release_cta(&s_ready, nlev);   // all loaded (or error path)
-        } else {
-            // ---- compute warps
-            auto wait_ready = [&](int m) {
-                if (threadIdx.x == 0) {
-                    m = min(m, nlev);
-                    long long spins = 0;
-                    if (a.mode & 1) {
-                        while (*(volatile int*)&s_ready < m)
-                            if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
-                        __threadfence_block();
-                    } else {
-                        while (ld_acquire_cta(&s_ready) < m)
-                            if (++spins > SPIN_LIMIT) { atomicExch(a.err, 7); break; }
-                    }
-                }
-            };
-            Rec<CK> rcr;
-            Rec<KH> rer;
-            int rrow = 0;
-            if (crit) {
-                rec_load<CK>(rcr, lp, nlev, 0, lane, cs, cc, di);
-                if (rcr.p >= 0) rrow = rid[rcr.p];
-            } else {
-                rec_load_pair<KH>(rer, lp, nlev, 0, lane, li, es, ecf);
-            }
-            wait_ready(1);
-            bar_compute();
-            if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
-            auto early = [&]() {
-                double a2[2] = {0.0, 0.0};
-                if (rer.p >= 0) {
-#pragma unroll
-                    for (int u = 0; u < KH; ++u) a2[u & 1] = fma(-rer.c[u], xs[rer.s[u]], a2[u & 1]);
-                }
-                double h = a2[0] + a2[1];
-                h += __shfl_xor_sync(0xffffffffu, h, 1);
-                if (rer.p >= 0 && li == 0) xs[rer.p] += h;
-            };
-            if (!crit) {
-                early();
-                rec_load_pair<KH>(rer, lp, nlev, 1, lane, li, es, ecf);
-            }
-            wait_ready(2);
-            bar_compute();
-            const long long c_lev0 = clock64();
-            for (int k = 0; k < nlev; ++k) {
-                if (crit) {
-                    if (rcr.p >= 0) {
-                        double x0 = xs[rcr.s[0]], x1 = xs[rcr.s[1]], x2 = xs[rcr.s[2]], x3 = xs[rcr.s[3]];
-                        double acc = xs[rcr.p];
-                        acc = fma(-rcr.c[0], x0, acc);
-                        acc = fma(-rcr.c[1], x1, acc);
-                        acc = fma(-rcr.c[2], x2, acc);
-                        acc = fma(-rcr.c[3], x3, acc);
-                        const double v = acc * rcr.d;
-                        xs[rcr.p] = v;
-                        if (!(a.mode & 2)) __stcg(a.x + rrow, publishable(v));
-                    }
-                    rec_load<CK>(rcr, lp, nlev, k + 1, lane, cs, cc, di);
-                    if (rcr.p >= 0) rrow = rid[rcr.p];
-                } else {
-                    early();
-                    rec_load_pair<KH>(rer, lp, nlev, k + 2, lane, li, es, ecf);
-                }
-                wait_ready(k + 3);
-                bar_compute();
-            }
-            const long long c_lev1 = clock64();
-            if (a.dbg && threadIdx.x == 0) {
-                a.dbg[t * 6 + 2] = gtimer();
-                a.dbg[t * 6 + 5] = (c_lev1 - c_lev0) / (nlev + 1);
-            }
-            if (a.out2)
-                for (int p = threadIdx.x; p < n; p += TILE_THREADS) {
-                    int row = rid[p];
-                    a.out2[row] = xs[p] + a.add[row];
-                }
-        }
-        __syncthreads();
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 3] = gtimer();
-    }
-}
-
 
 // ---------------------------------------------------------------------------
 // Dataflow tile solve: no per-level barrier.  Every x slot of the tile (its
@@ -909,55 +416,10 @@ __global__ void __launch_bounds__(PIPE_THREADS) k_tile_pipe(TileSolve a) {
 // starts as soon as its own externals exist.
 __device__ __forceinline__ double ld_vol_s(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
 __device__ __forceinline__ void st_vol_s(double* p, double v) { *reinterpret_cast<volatile double*>(p) = v; }
-#ifndef FLOW_SLEEP_NS
-#define FLOW_SLEEP_NS 0    // measured: no back-off is 1 % faster with 15 compute warps
-#endif
-__device__ __forceinline__ double poll_s(const double* p, int* err) {
-    double v = ld_vol_s(p);
-    if (is_sentinel(v)) {
-        long long spins = 0;
-        do {   // back off: spinning warps must not crowd the shared-memory pipe
-            if (++spins > SPIN_LIMIT) { atomicExch(err, 7); return 0.0; }
-            __nanosleep(FLOW_SLEEP_NS);
-            v = ld_vol_s(p);
-        } while (is_sentinel(v));
-    }
-    return v;
-}
-
-#ifndef FLOW_LW
-#define FLOW_LW 8          // loader: externals in flight per lane per polling round (8: 1 % faster than 16)
-#endif
-#ifndef FLOW_LSLEEP
-#define FLOW_LSLEEP 20     // loader back-off (ns) when nothing new arrived
-#endif
-#ifndef FLOW_LAHEAD
-#define FLOW_LAHEAD 64     // loader window: need-levels polled past the first missing external
-#endif
-#ifndef FLOW_LATE
-#define FLOW_LATE 0        // newest early deps per lane folded one by one (measured: 0 is best)
-#endif
-#ifndef FLOW_DIRECT
-#define FLOW_DIRECT 1      // compute lanes read missing externals from L2 themselves
-#endif
-#ifndef FLOW_STORE
-#define FLOW_STORE 5       // 0: st.global.cg, 1: st.relaxed.gpu, 2: st.cg + fence, 3: atom.exch, 4: st.release, 5: red.add at L2
-#endif
-#ifndef FLOW_POLL_CG
-#define FLOW_POLL_CG 0     // 1: poll with weak L2 loads (ld.global.cg) instead of ld.relaxed.gpu
-#endif
-__device__ __forceinline__ double flow_poll_g(const double* p) {
-    if (FLOW_POLL_CG) {
-        double v;
-        asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
-        return v;
-    }
-    return ld_relaxed_d(p);
-}
-#ifndef FLOW_WARPS_N
-#define FLOW_WARPS_N 15     // 15 + loader = 512 threads at 128 registers (measured: 12 -> 15 is 141 -> 134 us)
-#endif
-constexpr int FLOW_WARPS = FLOW_WARPS_N;            // compute warps (+1 loader)
+constexpr int FLOW_LW = 8;          // loader: externals in flight per lane per polling round (8: 1 % faster than 16)
+constexpr int FLOW_LSLEEP = 20;     // loader back-off (ns) when nothing new arrived
+constexpr int FLOW_LAHEAD = 64;     // loader window: need-levels polled past the first missing external
+constexpr int FLOW_WARPS = 15;      // compute warps (+1 loader) = 512 threads at 128 registers (12 -> 15: 141 -> 134 us)
 constexpr int FLOW_THREADS = (FLOW_WARPS + 1) * 32;
 __device__ __forceinline__ bool is_sent_hi(double v) {   // published values are never NaN-boxed like this
     return __double2hiint(v) == (int)(SENTINEL_BITS >> 32);
@@ -989,8 +451,8 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
     const double sent = __longlong_as_double((long long)SENTINEL_BITS);
     for (;;) {
         if (threadIdx.x == 0) {
-            int k = atomicAdd(a.ticket, 1) - a.ticket_base;
-            int t = k < a.n_tiles ? a.order[k] : -1;
+            const unsigned k = atomicAdd(a.ticket, 1u) - a.ticket_base;
+            const int t = k < (unsigned)a.n_tiles ? a.order[k] : -1;
             s_tile = t;
             if (t >= 0) {
                 const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
@@ -1018,7 +480,6 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
         const int t = s_tile;
         if (t < 0) break;
         const int n = s_hdr[0], ne = s_hdr[1], nlev = s_hdr[2];
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 0] = gtimer();
         for (int q = threadIdx.x; q < ne; q += FLOW_THREADS) xs[a.RC + q] = sent;
         {
             unsigned done = 0;
@@ -1062,7 +523,6 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
         }
         if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
         __syncthreads();
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 1] = gtimer();
         if (warp == FLOW_WARPS) {
             // externals in need order; q0 = first entry not yet present
             constexpr int LW = FLOW_LW;
@@ -1077,7 +537,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
 #pragma unroll
                 for (int u = 0; u < LW; ++u) {
                     const int q = q0 + u * 32 + lane;
-                    v[u] = q < qe ? flow_poll_g(a.x + eid_s[q]) : 0.0;
+                    v[u] = q < qe ? ld_relaxed_d(a.x + eid_s[q]) : 0.0;
                 }
                 int adv = qe - q0;
 #pragma unroll
@@ -1089,7 +549,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                     if (miss && adv == qe - q0) adv = u * 32 + __ffs(miss) - 1;
                 }
                 if (adv == 0) {
-                    if (FLOW_LSLEEP) __nanosleep(FLOW_LSLEEP);
+                    __nanosleep(FLOW_LSLEEP);
                     if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
                     continue;
                 }
@@ -1126,31 +586,27 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                         cs_[k] = act ? cs[(size_t)l0 * CK + k * R + r] : zs;
                         cc_[k] = act ? cc[(size_t)l0 * CK + k * R + r] : 0.0;
                     }
-                    long long c0 = a.dbg2 ? gtimer() : 0, c1 = 0, c2 = 0;
                     const double d = di[p];
                     const int row = rid[p];
                     const double bv = bsm[p];
-                    // early deps arrive oldest first (plan order): the older ones are
-                    // polled as one batch (one vote per round), the FLOW_LATE newest per
-                    // lane one at a time, so the fold runs up to the first missing one
+                    // early deps (older levels, externals) are polled as one batch,
+                    // one warp vote per round
                     double ev[KH];
 #pragma unroll
                     for (int u = 0; u < KH; ++u) ev[u] = ld_vol_s(xs + es_[u]);
-                    constexpr int NB = KH > FLOW_LATE ? KH - FLOW_LATE : 0;
                     auto fetch = [&](int u) -> double {   // an external the loader has not copied yet comes from L2
                         const int q = es_[u] - a.RC;
-                        return (FLOW_DIRECT && q >= 0 && q < ne) ? flow_poll_g(a.x + eid_s[q]) : ld_vol_s(xs + es_[u]);
+                        return (q >= 0 && q < ne) ? ld_relaxed_d(a.x + eid_s[q]) : ld_vol_s(xs + es_[u]);
                     };
                     {
                         bool miss = false;
 #pragma unroll
-                        for (int u = 0; u < NB; ++u) miss |= is_sent_hi(ev[u]);
+                        for (int u = 0; u < KH; ++u) miss |= is_sent_hi(ev[u]);
                         long long spins = 0;
                         while (__any_sync(0xffffffffu, miss)) {
-                            if (FLOW_SLEEP_NS) __nanosleep(FLOW_SLEEP_NS);
                             miss = false;
 #pragma unroll
-                            for (int u = 0; u < NB; ++u) {
+                            for (int u = 0; u < KH; ++u) {
                                 if (is_sent_hi(ev[u])) ev[u] = fetch(u);
                                 miss |= is_sent_hi(ev[u]);
                             }
@@ -1159,19 +615,9 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                     }
                     double h = 0.0;
 #pragma unroll
-                    for (int u = 0; u < NB; ++u) h = fma(-ec_[u], ev[u], h);
-#pragma unroll
-                    for (int u = NB; u < KH; ++u) {
-                        long long spins = 0;
-                        while (__any_sync(0xffffffffu, is_sent_hi(ev[u]))) {
-                            if (is_sent_hi(ev[u])) ev[u] = fetch(u);
-                            if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
-                        }
-                        h = fma(-ec_[u], ev[u], h);
-                    }
+                    for (int u = 0; u < KH; ++u) h = fma(-ec_[u], ev[u], h);
                     h += __shfl_xor_sync(0xffffffffu, h, 1);   // same sum on both lanes
                     double acc = bv + h;
-                    if (a.dbg2) c1 = gtimer();
                     double cv[CK];
 #pragma unroll
                     for (int k = 0; k < CK; ++k) cv[k] = ld_vol_s(xs + cs_[k]);
@@ -1190,43 +636,26 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                             if (++spins > SPIN_LIMIT) { if (lane == 0) atomicExch(a.err, 7); break; }
                         }
                     }
-                    if (a.dbg2) c2 = gtimer();
 #pragma unroll
                     for (int k = 0; k < CK; ++k) acc = fma(-cc_[k], cv[k], acc);
                     const double v = acc * d;
                     if (act && li == 0) {
                         st_vol_s(xs + p, v);
-                        if (FLOW_STORE == 1) {
-                            asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a.x + row), "d"(publishable(v)) : "memory");
-                        } else if (FLOW_STORE == 3) {   // performed at L2 (no write buffering in the SM)
-                            atomicExch(reinterpret_cast<unsigned long long*>(a.x + row),
-                                       (unsigned long long)__double_as_longlong(publishable(v)));
-                        } else if (FLOW_STORE == 5) {   // fire-and-forget reduction at L2: SENTINEL + (v - SENTINEL)
-                            atomicAdd(reinterpret_cast<unsigned long long*>(a.x + row),
-                                      (unsigned long long)__double_as_longlong(publishable(v)) - SENTINEL_BITS);
-                        } else if (FLOW_STORE == 4) {
-                            asm volatile("st.release.gpu.global.f64 [%0], %1;" ::"l"(a.x + row), "d"(publishable(v)) : "memory");
-                        } else {
-                            __stcg(a.x + row, publishable(v));
-                        }
-                        if (FLOW_STORE == 2) __threadfence();
+                        // fire-and-forget reduction at L2: SENTINEL + (v - SENTINEL)
+                        // (visible downstream ~0.5 us after issue; a plain store ~2 us)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(a.x + row),
+                                  (unsigned long long)__double_as_longlong(publishable(v)) - SENTINEL_BITS);
                     }
                     __syncwarp();
-                    if (a.dbg2 && lane == 0 && g < 64) {
-                        long long* q = a.dbg2 + ((size_t)t * 64 + g) * 5;
-                        q[0] = c0; q[1] = c1; q[2] = c2; q[3] = gtimer(); q[4] = lv;
-                    }
                 }
             }
         }
         __syncthreads();
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 2] = gtimer();
         if (a.out2)
             for (int p = threadIdx.x; p < n; p += FLOW_THREADS) {
                 int row = rid[p];
                 a.out2[row] = xs[p] + a.add[row];
             }
-        if (a.dbg && threadIdx.x == 0) a.dbg[t * 6 + 3] = gtimer();
     }
 }
 
@@ -1249,11 +678,9 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     const int n = D.n_rows;
     if (!dims || dims[0] <= 0 || (int64_t)dims[0] * dims[1] * dims[2] != n || n == 0) return false;
     Geo g{dims[0], dims[1], dims[2], 8, 8, 8, 0, 0, 0};
-    int td[3] = {8, 8, 8};
-    if (const char* e = getenv("EDFA_TILE_DIM")) sscanf(e, "%d,%d,%d", &td[0], &td[1], &td[2]);   // A/B only
-    g.tx = std::min(td[0], g.nx);
-    g.ty = std::min(td[1], g.ny);
-    g.tz = std::min(td[2], g.nz);
+    g.tx = std::min(8, g.nx);
+    g.ty = std::min(8, g.ny);
+    g.tz = std::min(8, g.nz);
     g.NX = ceil_div(g.nx, g.tx);
     g.NY = ceil_div(g.ny, g.ty);
     g.NZ = ceil_div(g.nz, g.tz);
@@ -1274,11 +701,10 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     if (tp.LC > tp.RC + 8) tp.LC = tp.RC + 8;
     tp.unit = unit;
     tp.n_dep = D.nnz;
-    if (tp.LC > 255) return false;                      // levels are stored as bytes in req
     DevBuf<int32_t> glev(c, n);
     int HS = 1;
     while (HS < 2 * tp.EC) HS <<= 1;
-    size_t bsm = sizeof(int) * (5 * tp.RC + 2 + tp.EC + 8 + HS + 2 * tp.EC + 32 * tp.LC);
+    size_t bsm = sizeof(int) * (5 * tp.RC + 2 + tp.EC + 8 + HS + 2 * tp.EC);
     bsm = std::max(bsm, sizeof(int) * 2 * tp.RC + sizeof(short) * (size_t)tp.RC * hf[1] + 64);
     if (bsm > 48 * 1024)
         EDFA_CUDA(cudaFuncSetAttribute(k_tile_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
@@ -1323,19 +749,14 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     tp.up_cnt.reset(c, nt);
     tp.up_ids.reset(c, (size_t)nt * 32);
     tp.xlev_ptr.reset(c, (size_t)nt * tp.LC);
-    tp.req.reset(c, (size_t)nt * tp.LC * 32);
-    tp.flags.reset(c, nt);
     tp.ticket.reset(c, 1);
-    EDFA_CUDA(cudaMemsetAsync(tp.flags.p, 0, sizeof(int) * nt, c->stream));
-    EDFA_CUDA(cudaMemsetAsync(tp.ticket.p, 0, sizeof(int), c->stream));
-    tp.epoch = 0;
+    EDFA_CUDA(cudaMemsetAsync(tp.ticket.p, 0, sizeof(unsigned), c->stream));
     tp.ticket_base = 0;
     TileBuild b{view(D), g, tp.RC, tp.KD, tp.EC, tp.LC, diag, unit, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
                 fl + 2, fl + 3, false, hf[1]};
     b.glev = glev.p;
     b.xlev_ptr = tp.xlev_ptr.p;
-    b.req = tp.req.p;
     {
         Prof pr(c, "tile_plan", 24.0 * D.nnz);
         k_tile_build<<<nt, 256, bsm, c->stream>>>(b);
@@ -1368,37 +789,28 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
 
 template <int EK>
 static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
-    // EDFA_TILE_KERNEL (A/B experiments only): legacy | pipe; default: dataflow
-    static const char* kv = getenv("EDFA_TILE_KERNEL");
-    static const int which = !kv ? 2 : (kv[0] == 'l' ? 0 : kv[0] == 'p' ? 1 : 2);
-    auto kern = which == 0 ? k_tile_solve<EK> : which == 1 ? k_tile_pipe<EK> : k_tile_flow<EK>;
-    const int threads = which == 0 ? TILE_THREADS : which == 1 ? PIPE_THREADS : FLOW_THREADS;
-    if (which == 2) smem = tile_flow_smem_bytes(tp);
-    // attribute + occupancy once per (kernel, smem): these are driver calls,
-    // kept off the per-solve path
+    // attribute + occupancy once per (device, smem): driver calls kept off the
+    // per-solve path
     static std::mutex mu;
-    static std::map<size_t, int> grids;
-    static size_t smem_set = 0;
+    static std::map<std::pair<int, size_t>, int> grids;
     int grid;
     {
         std::lock_guard<std::mutex> lk(mu);
-        auto it = grids.find(smem);
+        const auto key = std::make_pair(c->device, smem);
+        auto it = grids.find(key);
         if (it == grids.end()) {
-            if (smem > smem_set) {
-                EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                smem_set = smem;
-            }
+            EDFA_CUDA(cudaFuncSetAttribute(k_tile_flow<EK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             int occ = 0;
-            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-            static const int occ_cap = getenv("EDFA_TILE_OCC") ? atoi(getenv("EDFA_TILE_OCC")) : 2;
-            it = grids.emplace(smem, NUM_SMS_B200 * std::max(1, std::min(occ, occ_cap))).first;
+            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_flow<EK>, FLOW_THREADS, smem));
+            it = grids.emplace(key, NUM_SMS_B200 * std::max(1, std::min(occ, 2))).first;
         }
         grid = it->second;
     }
     a.ticket_base = tp.ticket_base;
-    tp.ticket_base += tp.n_tiles + grid;   // every CTA takes exactly one failing ticket
+    tp.ticket_base += (unsigned)(tp.n_tiles + grid);   // every CTA takes exactly one failing ticket
     void* args[] = {&a};
-    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(threads), args, smem, c->stream));
+    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)k_tile_flow<EK>, dim3(grid), dim3(FLOW_THREADS), args, smem,
+                                          c->stream));
 }
 
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
@@ -1409,56 +821,22 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
 void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
                  const char* name, bool x_prefilled, bool consume_b, double* pre_sent, const Csr* fz,
                  const double* fz_x) {
-    size_t smem = tile_smem_bytes(tp);
-    // EDFA_TILE_NOWAIT (profiling only): every upstream flag already matches,
-    // so tiles run without waiting -- isolates per-tile processing cost
-    static const bool nowait = getenv("EDFA_TILE_NOWAIT") != nullptr;
-    if (!nowait) tp.epoch += 1;
-    if (tp.epoch >= (1 << 22)) {   // progress words hold epoch << 8: restart the epoch sequence
-        EDFA_CUDA(cudaMemsetAsync(tp.flags.p, 0, sizeof(int) * tp.n_tiles, c->stream));
-        tp.epoch = 1;
-    }
     TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.LC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
-                tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.up_cnt.p, tp.up_ids.p,
-                tp.flags.p, tp.ticket.p, tp.epoch, 0, b, alpha, x, add, out2, c->d_scalar_i + 8, nullptr,
-                tp.xlev_ptr.p, tp.req.p, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-    static const int tile_mode = getenv("EDFA_TILE_MODE") ? atoi(getenv("EDFA_TILE_MODE")) : 0;
-    a.mode = tile_mode;
-    static const char* dbg_path = getenv("EDFA_TILE_DEBUG");
-    static const char* dbg2_path = getenv("EDFA_TILE_DEBUG2");
-    DevBuf<long long> dbg, dbg2;
-    if (dbg_path) {
-        dbg.reset(c, (size_t)tp.n_tiles * 6);
-        a.dbg = dbg.p;
-    }
-    a.dbg2 = nullptr;
-    if (dbg2_path) {
-        dbg2.reset(c, (size_t)tp.n_tiles * 64 * 5);
-        EDFA_CUDA(cudaMemsetAsync(dbg2.p, 0, sizeof(long long) * tp.n_tiles * 64 * 5, c->stream));
-        a.dbg2 = dbg2.p;
-    }
-    static const bool legacy = getenv("EDFA_TILE_KERNEL") && getenv("EDFA_TILE_KERNEL")[0] == 'l';
-    const bool flow = !getenv("EDFA_TILE_KERNEL") || (getenv("EDFA_TILE_KERNEL")[0] != 'l' &&
-                                                     getenv("EDFA_TILE_KERNEL")[0] != 'p');
-    if (flow) {
-        a.b_sent = consume_b ? const_cast<double*>(b) : nullptr;
-        a.pre_sent = pre_sent;
-        if (fz) {
-            require(!consume_b, EDFA_ERR_CUDA, "fused right-hand side and consumed b are exclusive");
-            a.fz_ptr = fz->ptr.p;
-            a.fz_idx = fz->idx.p;
-            a.fz_val = fz->val.p;
-            a.fz_x = fz_x;
-        }
-    } else {
-        require(!fz, EDFA_ERR_CUDA, "fused right-hand side needs the dataflow tile kernel");
-        x_prefilled = false;
-        if (consume_b) fill_bits(c, const_cast<double*>(b), tp.n, SENTINEL_BITS);
-        if (pre_sent) fill_bits(c, pre_sent, tp.n, SENTINEL_BITS);
+                tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.ticket.p, 0u, b, alpha, x,
+                add, out2, c->d_scalar_i + 8, tp.xlev_ptr.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.b_sent = consume_b ? const_cast<double*>(b) : nullptr;
+    a.pre_sent = pre_sent;
+    if (fz) {
+        require(!consume_b, EDFA_ERR_CUDA, "fused right-hand side and consumed b are exclusive");
+        a.fz_ptr = fz->ptr.p;
+        a.fz_idx = fz->idx.p;
+        a.fz_val = fz->val.p;
+        a.fz_x = fz_x;
     }
     // a row's value is its own ready flag
-    if (!legacy && !nowait && !x_prefilled) fill_bits(c, x, tp.n, SENTINEL_BITS);
+    if (!x_prefilled) fill_bits(c, x, tp.n, SENTINEL_BITS);
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
+    const size_t smem = tile_flow_smem_bytes(tp);
     switch (tp.KD) {
         case 4: launch_tile<4>(c, tp, a, smem); break;
         case 8: launch_tile<8>(c, tp, a, smem); break;
@@ -1466,32 +844,6 @@ void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x,
         case 16: launch_tile<16>(c, tp, a, smem); break;
         case 24: launch_tile<24>(c, tp, a, smem); break;
         default: launch_tile<32>(c, tp, a, smem); break;
-    }
-    if (dbg2_path) {
-        std::vector<long long> h((size_t)tp.n_tiles * 64 * 5);
-        EDFA_CUDA(cudaMemcpyAsync(h.data(), dbg2.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-        EDFA_CUDA(cudaStreamSynchronize(c->stream));
-        FILE* f = fopen(dbg2_path, "w");
-        if (f) {
-            for (int t = 0; t < tp.n_tiles; ++t)
-                for (int g = 0; g < 64; ++g) {
-                    const long long* q = &h[((size_t)t * 64 + g) * 5];
-                    if (q[0]) fprintf(f, "%d %d %lld %lld %lld %lld %lld\n", t, g, q[0], q[1], q[2], q[3], q[4]);
-                }
-            fclose(f);
-        }
-    }
-    if (dbg_path) {
-        std::vector<long long> h((size_t)tp.n_tiles * 6);
-        EDFA_CUDA(cudaMemcpyAsync(h.data(), dbg.p, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-        EDFA_CUDA(cudaStreamSynchronize(c->stream));
-        FILE* f = fopen(dbg_path, "w");
-        if (f) {
-            for (int t = 0; t < tp.n_tiles; ++t)
-                fprintf(f, "%d %lld %lld %lld %lld %lld %lld\n", t, h[t * 6], h[t * 6 + 1], h[t * 6 + 2], h[t * 6 + 3],
-                        h[t * 6 + 4], h[t * 6 + 5]);
-            fclose(f);
-        }
     }
 }
 

@@ -571,11 +571,7 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
         run_chain(c, p.chain, b, alpha, x, add, out2, name);
         return;
     }
-    if (p.is_axial) {
-        run_axial(c, const_cast<AxialPlan&>(p.axial), b, alpha, x, add, out2, name);
-        return;
-    }
-    if (p.is_tile) {   // epoch / ticket bookkeeping is per plan (serialised on the stream)
+    if (p.is_tile) {   // ticket bookkeeping is per plan (serialised on the stream)
         run_tile(c, const_cast<TilePlan&>(p.tile), b, alpha, x, add, out2, name);
         return;
     }
@@ -583,7 +579,7 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
     // more than the rows: sync-free warp-per-row solve
     // (measured on config 3's IC at 128^3, 16k rows per level: 1.95 ms vs 4.09 ms
     // per solve pair for the level-synchronous kernel; at 64^3 1.03 vs 1.76 ms)
-    if (x != b && !getenv("EDFA_TRSV_LEVELS")) {
+    if (x != b && !c->opt.trsv_levels) {
         fill_bits(c, x, p.n, SENTINEL_BITS);
         EDFA_CUDA(cudaMemsetAsync(p.ticket.p, 0, sizeof(int), c->stream));
         int* err = c->d_scalar_i + 8;   // the solve error flag check_trsv_error reads
@@ -597,11 +593,11 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
         // thread per row while rows fit 32 registers' worth of dependencies and
         // levels are wide enough to fill the warps; warp per row otherwise
         const bool wide_levels = (int64_t)p.n >= 1024ll * std::max(p.n_levels, 1);
-        if (p.max_w > 16 && p.max_w <= 32 && wide_levels && !getenv("EDFA_TRSV_WARP_ROWS")) {
+        if (p.max_w > 16 && p.max_w <= 32 && wide_levels) {
             k_trsv_tsf<32><<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p,
                                                            p.n_slots / 32, p.ticket.p, b, alpha, x, add, out2, err);
             check_launch("k_trsv_tsf");
-        } else if (p.max_w > 16 || getenv("EDFA_TRSV_WARP_ROWS")) {
+        } else if (p.max_w > 16) {
             k_trsv_wsf<<<grid_sf, 256, 0, c->stream>>>(p.perm.p, p.slice_ptr.p, p.col.p, p.val.p, p.dinv.p,
                                                        p.n_slots, p.ticket.p, b, alpha, x, add, out2, err);
             check_launch("k_trsv_wsf");

@@ -36,6 +36,26 @@ def ctx(device: int | None = None) -> C.c_void_p:
     return h
 
 
+class option:
+    """Context manager selecting one of libedfa's algorithm alternatives on the
+    current device's context (edfa_ctx_set_option; names in include/edfa.h),
+    restoring the previous value on exit -- the A/B switch the tests use."""
+
+    def __init__(self, name: str, value: int):
+        self.name, self.value = name.encode(), int(value)
+
+    def __enter__(self):
+        c = ctx()
+        old = C.c_int32()
+        L.check(L.lib().edfa_ctx_get_option(c, self.name, C.byref(old)))
+        self.old = old.value
+        L.check(L.lib().edfa_ctx_set_option(c, self.name, self.value))
+        return self
+
+    def __exit__(self, *exc):
+        L.check(L.lib().edfa_ctx_set_option(ctx(), self.name, self.old))
+
+
 def dptr(t: torch.Tensor) -> C.c_void_p:
     return C.c_void_p(t.data_ptr())
 

@@ -435,6 +435,9 @@ class CudaSlab:
                                         C.c_void_p(out.data_ptr()),
                                         None if norm2 is None else C.c_void_p(norm2.data_ptr())))
 
+    def sync(self):
+        L.check(self.lib.edfa_ctx_sync(self.ctx))
+
     def axpby(self, a, x, b, y):
         L.check(self.lib.edfa_axpby(self.ctx, y.numel(), a, C.c_void_p(x.data_ptr()), b,
                                     C.c_void_p(y.data_ptr())))
@@ -664,6 +667,8 @@ def slab_gmres(op: SlabOperator, bs, tol=1e-8, restart=50, max_it=2000):
         for p, r, b in zip(parts, rs, bs):
             p.axpby(1.0, b, -1.0, r)                              # r = b - A x
         beta = math.sqrt(global_dot(rs, rs))
+        for p in parts:        # once per restart cycle: a triangular solve that hit its spin limit raises
+            p.sync()
         if beta / bnorm <= tol:
             rep.converged = True
             break

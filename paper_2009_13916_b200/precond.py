@@ -107,7 +107,10 @@ class InnerFactorization:
         s1 = self._owner.handle if self.kind == "ic" else None
         s2 = self._owner.handle if self.kind == "ilu" else None
         L.check(L.lib().edfa_inner_apply(ctx(), s1, s2, 0 if self.kind == "ic" else 1, dptr(x), dptr(y)))
-        return y.cpu().numpy() if host else y
+        if host:   # the caller waits anyway: surface a solve that hit its spin limit here
+            L.check(L.lib().edfa_ctx_sync(ctx()))
+            return y.cpu().numpy()
+        return y
 
     __call__ = apply
 
@@ -302,7 +305,10 @@ class BlockLDUPreconditioner:
         y = torch.empty_like(x)
         L.check(L.lib().edfa_precond_apply(ctx(), ds.handle, self.stage1.handle, self.stage2.handle,
                                             dptr(x), dptr(y)))
-        return y.cpu().numpy() if host else y
+        if host:   # the caller waits anyway: surface a solve that hit its spin limit here
+            L.check(L.lib().edfa_ctx_sync(ctx()))
+            return y.cpu().numpy()
+        return y
 
     __call__ = apply
 
@@ -391,6 +397,16 @@ def grow_pattern_dynamic(A_ff, rhs_idx, rhs_val, cfg: DynamicConfig, A_csc=None)
 
 
 def filter_rows(M, tau: float, keep_diagonal: bool = True):
-    """Row filtration (hx/precond.py:138-157).  Exposed for API parity; inside
-    the build it is fused into the product / Schur-merge kernels."""
-    raise NotImplementedError("filter_rows runs fused inside build_stage1/build_stage2 on the GPU path")
+    """Drop row entries below tau times the row Euclidean norm; the diagonal
+    survives when keep_diagonal (hx/precond.py:138-157).  tau <= 0 returns M
+    itself.  Runs as libedfa's k_filter on the device; scipy input comes back
+    as canonical scipy CSR, device input (DeviceCsr) stays on the device."""
+    if tau <= 0:
+        return M
+    from .sparse import canonical
+    dev = isinstance(M, DeviceCsr)
+    A = M if dev else DeviceCsr.from_scipy(canonical(M))
+    h = C.c_void_p()
+    L.check(L.lib().edfa_csr_filter(ctx(), A.handle, float(tau), int(bool(keep_diagonal)), C.byref(h)))
+    out = DeviceCsr(h)
+    return out if dev else out.to_scipy()

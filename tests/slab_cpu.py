@@ -73,6 +73,9 @@ class CpuSlab:
         if norm2 is not None:
             norm2[0] = float(o @ o)
 
+    def sync(self):   # CPU arithmetic has no deferred solve errors
+        pass
+
     def axpby(self, a, x, b, y):
         y.copy_(a * x if b == 0.0 else a * x + b * y)
 

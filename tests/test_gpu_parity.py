@@ -21,6 +21,7 @@ import scipy.sparse as sp
 
 from conftest import GoldenSystem, g_csr, g_sets, golden, same_csr
 from oracle import edfa_oracle as O
+from paper_2009_13916_b200.device import option
 
 pytestmark = pytest.mark.gpu
 
@@ -401,33 +402,8 @@ def test_tile_solver_matches_level_solver(edfa, idx, n):
     assert np.abs(ys[0] - ys[1]).max() <= 1e-12 * np.abs(ys[1]).max()
 
 
-@pytest.mark.parametrize("idx,n", [(1, 12), (2, 10), (2, 19)])
-def test_axial_solver_matches_level_solver(edfa, idx, n, monkeypatch):
-    """The axial-stencil pencil solves (EDFA_AXIAL) and the level-synchronous
-    solves compute the same Schur triangular solutions (n = 19: blocks that
-    overhang the grid)."""
-    from paper_2009_13916_b200 import configs
-    case = configs.make(idx, n=n)
-    s = case.system
-    p = case.precond
-    ys = []
-    for hint in (True, False):
-        if hint:
-            monkeypatch.setenv("EDFA_AXIAL", "1")
-        else:
-            monkeypatch.delenv("EDFA_AXIAL", raising=False)
-        ds = edfa.DeviceSystem.from_host(s)
-        if not hint:
-            ds.set_grid(0, 0, 0)
-        pats = edfa.patterns_for(s, p["pattern"], p.get("prototype", "A"))
-        pre = edfa.BlockLDUPreconditioner.build(ds, patterns=pats, no_fill=True)
-        r = np.random.default_rng(5).standard_normal(s.n_unknowns)
-        ys.append(pre.apply(r))
-    assert np.abs(ys[0] - ys[1]).max() <= 1e-12 * np.abs(ys[1]).max()
-
-
 @pytest.mark.parametrize("idx,n", [(1, 12), (2, 16)])
-def test_ic_pair_matches_separate_solves(edfa, idx, n, monkeypatch):
+def test_ic_pair_matches_separate_solves(edfa, idx, n):
     """The fused (L L^T)^-1 chain kernel equals the two separate chain solves."""
     from paper_2009_13916_b200 import configs
     case = configs.make(idx, n=n)
@@ -438,8 +414,8 @@ def test_ic_pair_matches_separate_solves(edfa, idx, n, monkeypatch):
     pre = edfa.BlockLDUPreconditioner.build(ds, patterns=pats, no_fill=True)
     r = np.random.default_rng(7).standard_normal(s.n_unknowns)
     y_pair = pre.apply(r)
-    monkeypatch.setenv("EDFA_NO_IC_PAIR", "1")
-    y_sep = pre.apply(r)
+    with option("ic_pair", 0):
+        y_sep = pre.apply(r)
     assert np.abs(y_pair - y_sep).max() <= 1e-11 * np.abs(y_sep).max()
 
 
@@ -506,43 +482,42 @@ def test_config4_transient_refresh_matches_oracle(edfa):
 
 
 @pytest.mark.parametrize("idx,n,dyn", [(3, 7, True), (3, 6, False)])
-def test_wide_row_syncfree_solver_matches_level_solver(edfa, idx, n, dyn, monkeypatch):
+def test_wide_row_syncfree_solver_matches_level_solver(edfa, idx, n, dyn):
     """Schur factors with wide rows (dynamic / distorted patterns) use the
     warp-per-row sync-free solve; it computes the level solver's triangular
     solutions (up to the order of the row sums)."""
     from paper_2009_13916_b200 import configs
     s = configs.make(idx, n=n).system
     ys = []
-    for env in (None, "1"):
-        if env:
-            monkeypatch.setenv("EDFA_TRSV_LEVELS", env)
-        if dyn:
-            pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
-        else:
-            pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, "static", "C"), no_fill=True)
-        r = np.random.default_rng(11).standard_normal(s.n_unknowns)
-        ys.append((pre.apply(r), pre.stage2.schur_inner.apply(r[s.n_free_faces:])))
+    for lv in (0, 1):
+        with option("trsv_levels", lv):
+            if dyn:
+                pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
+            else:
+                pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, "static", "C"),
+                                                        no_fill=True)
+            r = np.random.default_rng(11).standard_normal(s.n_unknowns)
+            ys.append((pre.apply(r), pre.stage2.schur_inner.apply(r[s.n_free_faces:])))
     for a, b in zip(ys[0], ys[1]):
         assert np.abs(a - b).max() <= 1e-11 * np.abs(b).max()
 
 
-def test_syncfree_ilu0_on_level_order_is_bitwise_level_synchronous(edfa, monkeypatch):
+def test_syncfree_ilu0_on_level_order_is_bitwise_level_synchronous(edfa):
     """Stencils whose wavefront order is not topological (dynamic patterns on
     distorted grids) factor sync-free in level order; the factors equal the
     level-synchronous kernel's bit for bit (same operations per row)."""
     from paper_2009_13916_b200 import configs
     s = configs.make(3, n=6).system
     out = []
-    for env in (None, "1"):
-        if env:
-            monkeypatch.setenv("EDFA_ILU_LEVELS", env)
-        pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
-        out.append((pre.stage2.schur_inner.L, pre.stage2.schur_inner.U))
+    for lv in (0, 1):
+        with option("ilu_levels", lv):
+            pre = edfa.BlockLDUPreconditioner.build(s, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
+            out.append((pre.stage2.schur_inner.L, pre.stage2.schur_inner.U))
     for a, b in zip(out[0], out[1]):
         assert same_csr(a, b) and np.array_equal(a.data, b.data)
 
 
-def test_narrow_row_syncfree_solver_is_bitwise_level_solver(edfa, monkeypatch):
+def test_narrow_row_syncfree_solver_is_bitwise_level_solver(edfa):
     """Level plans with narrow rows (IC of -A_ff on a distorted grid) run the
     thread-per-row sync-free solve: same arithmetic order as the
     level-synchronous kernel, so the solutions agree bit for bit."""
@@ -550,11 +525,10 @@ def test_narrow_row_syncfree_solver_is_bitwise_level_solver(edfa, monkeypatch):
     s = configs.make(3, n=7).system
     r = np.random.default_rng(5).standard_normal(s.n_free_faces)
     ys = []
-    for env in (None, "1"):
-        if env:
-            monkeypatch.setenv("EDFA_TRSV_LEVELS", env)
-        pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, "static", "A"), no_fill=True)
-        ys.append(pre.stage1.face_inner.apply(r))
+    for lv in (0, 1):
+        with option("trsv_levels", lv):
+            pre = edfa.BlockLDUPreconditioner.build(s, patterns=edfa.patterns_for(s, "static", "A"), no_fill=True)
+            ys.append(pre.stage1.face_inner.apply(r))
     assert np.array_equal(ys[0], ys[1])
 
 

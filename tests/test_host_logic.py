@@ -38,3 +38,28 @@ def test_face_conditions_rejects_interior_flux():
 @pytest.mark.parametrize("dt,dp", [(0.1, 0.0), (0.1, 1.0), (0.1, 50.0), (4.9, 0.01), (1.0, 5.0)])
 def test_step_controller_matches_oracle(dt, dp):
     assert next_dt(dt, 5.0, 1.1, 5.0, dp) == O.next_dt(dt, 5.0, 1.1, 5.0, dp)
+
+
+def test_matrix_market_roundtrip(tmp_path):
+    """mm_write / mm_read (hx/sparse.py:302-317): 17 significant digits make
+    the round trip exact; vectors come back as n x 1 canonical CSR."""
+    import scipy.sparse as sp
+
+    from paper_2009_13916_b200.sparse import canonical, mm_read, mm_write
+    rng = np.random.default_rng(0)
+    A = canonical(sp.random(40, 30, density=0.1, random_state=1, format="csr"))
+    A.data = rng.standard_normal(A.nnz) * 10.0 ** rng.uniform(-12, 12, A.nnz)
+    mm_write(A, tmp_path / "A.mtx")
+    B = mm_read(tmp_path / "A.mtx")
+    assert B.shape == A.shape and np.array_equal(B.indptr, A.indptr) and np.array_equal(B.indices, A.indices)
+    assert np.array_equal(B.data, A.data)
+    v = rng.standard_normal(17)
+    mm_write(v, tmp_path / "v.mtx")
+    w = mm_read(tmp_path / "v.mtx")
+    assert w.shape == (17, 1) and np.array_equal(w.toarray().ravel(), v)
+    S = canonical(A[:30, :30] + A[:30, :30].T)
+    mm_write(S, tmp_path / "S.mtx", symmetric=True)
+    assert abs(mm_read(tmp_path / "S.mtx") - S).max() == 0.0
+    (tmp_path / "bad.mtx").write_text("not a matrix market file\n")
+    with pytest.raises(Exception):
+        mm_read(tmp_path / "bad.mtx")
