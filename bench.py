@@ -1,28 +1,29 @@
 #!/usr/bin/env python
 """EDFA setup + GMRES(50) solve throughput on B200 (BASELINE.json metric).
 
-One step = the hot path over one system: static-pattern generation, stage 1
+One step = the hot path over one system: system creation from the resident
+blocks (merged A, SELL copies, grid topology), restriction patterns, stage 1
 (restricted row solves, G~/F~, H~ = G~ A_ff F~, IC(0) of -A_ff), stage 2
 (S~ = A_cc - H~, ILU(0)) and right-preconditioned GMRES(50) to rtol 1e-8 from
-x0 = 0.  Workload: BASELINE config 2 (64^3 hex grid, lognormal anisotropic K,
-static prototype A, IC(0)/ILU(0)), synthetic seeded inputs (SPE10 is not in
-this container).  ``value`` = N_dof * steps / device time with the blocks, rhs
-and grid index arrays resident in HBM (the step derives everything else:
-merged A, SELL copies, topology, patterns, stage 1/2, GMRES); ``e2e`` = the
-same through the drop-in API from page-locked host scipy blocks (H2D of the
-blocks, rhs and grid arrays, D2H of x inside the timed region).
+x0 = 0 (hx/driver.py:108-142's stage timers: t_stage1, t_stage2, t_solve).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl edfa|reference] [--slabs P]
+Workload at N = 1: BASELINE config 5 -- 256^3 hex grid (16.8M cells, 67.2M
+DOF), config-2 lognormal anisotropic K, static prototype A, IC(0)/ILU(0) --
+the largest single-GPU configuration, assembled on the device from seeded
+synthetic inputs (SPE10 is not in this container).  ``value`` = N_dof *
+steps / device time with the blocks, rhs and grid index arrays resident in
+HBM; ``e2e`` = the same through the drop-in API from page-locked host scipy
+blocks (H2D of the blocks, rhs and grid arrays, D2H of x inside the timed
+region).  Config 2 (64^3) is measured too and reported under ``config2``.
 
-N = 1: the single-device solver on config 2.  N > 1 (torchrun, one process
-per GPU): weak scaling over z-slabs -- an n x n x (n N) grid of the config-2
-generator, one n^3 slab per GPU, block-Jacobi inner factors per slab, halo
-exchange and Krylov allreduces over NCCL (parallel.py).  ``--slabs P`` on one
-GPU runs P slabs in one process (the same per-slab device work, local halos).
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl edfa|reference]
+                    [--config C] [--n n] [--slabs P]
 
-``--impl reference`` times the CPU restatement of the reference algorithm
-(oracle/, the reference is pure Python and cannot travel to the GPU box) on a
-bounded sample of the same workload and prints the same JSON line.
+N > 1 (torchrun, one process per GPU): z-slab partitioned solve
+(parallel.py), see run_slabs.  ``--impl reference`` times the CPU
+restatement of the reference algorithm (oracle/, the reference is pure
+Python and cannot travel to the GPU box): one full measured config-2 run
+with the reference's stage timers, extrapolated per DOF to the bench config.
 """
 
 from __future__ import annotations
@@ -36,25 +37,29 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "EDFA setup+GMRES solve throughput per system (config 2)"
-METRIC_OF = lambda k: METRIC.replace("config 2", f"config {k}")  # noqa: E731
+METRIC = "EDFA setup+GMRES solve throughput per system"
 UNIT = "MDOF/s"
-
-
 DEFAULT_N = {1: 16, 2: 64, 3: 128, 4: None, 5: 256}
+# GMRES(50) iterations of config 5 at 256^3 on the GPU (profiles/r02_bench_config5.json);
+# the CPU arm's extrapolation uses it (the MGS oracle matched the GPU count at 64^3: 84 = 84)
+CONFIG5_ITERS = 381
 
 
-def make_case(args):
+def metric_of(k):
+    return f"{METRIC} (config {k})"
+
+
+def make_case(config, n, host=True):
     from paper_2009_13916_b200 import configs
-    if args.config == 4:
-        return configs.config4() if args.n is None else configs.config4(nx=args.n, ny=args.n, nz=args.n)
-    return configs.make(args.config, n=args.n or DEFAULT_N[args.config])
+    mk = configs.make if host else configs.inputs_only
+    if config == 4:
+        return mk(4) if n is None else mk(4, nx=n, ny=n, nz=n)
+    return mk(config, n=n or DEFAULT_N[config])
 
 
 INNER = {}   # --drop-tol / --fill override the config's inner-solve options
@@ -68,14 +73,28 @@ def inner_opts(case):
     return o
 
 
-def build_pre(case, ds):
-    """Preconditioner of a BASELINE config through the drop-in API."""
-    from paper_2009_13916_b200.precond import BlockLDUPreconditioner, DynamicConfig, patterns_for
-    p = case.precond
+def stage1_of(case, ds):
+    """Stage 1 of a BASELINE config through the drop-in API."""
+    from paper_2009_13916_b200.precond import DynamicConfig, build_stage1, patterns_for
+    p, o = case.precond, inner_opts(case)
     if p["pattern"] == "dynamic":
-        return BlockLDUPreconditioner.build(ds, dynamic=DynamicConfig(p["n_add"], p["n_ent"]), **inner_opts(case))
-    pats = patterns_for(ds, p["pattern"], p.get("prototype", "A"))
-    return BlockLDUPreconditioner.build(ds, patterns=pats, **inner_opts(case))
+        return build_stage1(ds, dynamic=DynamicConfig(p["n_add"], p["n_ent"]), face_drop_tol=o["face_drop_tol"],
+                            no_fill=o["no_fill"])
+    return build_stage1(ds, patterns=patterns_for(ds, p["pattern"], p.get("prototype", "A")),
+                        face_drop_tol=o["face_drop_tol"], no_fill=o["no_fill"])
+
+
+def precond_of(case, ds, s1):
+    from paper_2009_13916_b200.precond import BlockLDUPreconditioner
+    o = inner_opts(case)
+    pre = BlockLDUPreconditioner(ds, s1, settings=dict(tau_filt=0.0, filtration="none",
+                                                       schur_drop_tol=o["schur_drop_tol"], no_fill=o["no_fill"]))
+    pre.refresh(ds)
+    return pre
+
+
+def build_pre(case, ds):
+    return precond_of(case, ds, stage1_of(case, ds))
 
 
 def inner_tag(case):
@@ -92,9 +111,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="edfa", choices=["edfa", "reference"])
     ap.add_argument("--n", type=int, default=None, help="grid cells per side (default: the config's size)")
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
-                    help="BASELINE config (2 = the headline workload; others for evidence runs)")
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE config (5 = the headline: largest single-GPU workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config2", action="store_true", help="skip the extra config-2 leg")
     ap.add_argument("--drop-tol", type=float, default=0.0,
                     help="face_drop_tol = schur_drop_tol (evidence runs of the threshold inner solves)")
     ap.add_argument("--fill", action="store_true", help="no_fill=False (threshold factorisations with fill)")
@@ -104,6 +124,8 @@ def parse():
     ap.add_argument("--slabs", type=int, default=0,
                     help="z-slab partitioned solver with this many slabs per process (default: 1 slab per "
                          "GPU when N > 1, the single-device solver when N = 1)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong (one global grid cut into N slabs) or weak (n^3 per GPU, grown along z)")
     return ap.parse_args()
 
 
@@ -167,358 +189,384 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
-def cpu_baseline(n_full: int, n_iters_full: int, sample_n: int = 20, gmres_iters: int = 8):
-    """Time the oracle restatement of the reference on a bounded sample and
-    extrapolate to the full workload: stage 1 and stage 2 are
-    per-row independent work -> per-DOF rates from a sample_n^3 instance of the
-    same generator; GMRES -> per-iteration-per-DOF rate from ``gmres_iters``
-    iterations on that instance, scaled by the GPU's iteration count."""
-    import numpy as np
+def n_dof_config2(n, nz=None):
+    """Free faces + cells of the config-2/5 generator on an n x n x nz box
+    (x faces minus the two Dirichlet x planes, plus y and z faces)."""
+    nz = nz or n
+    return (n + 1) * n * nz - 2 * n * nz + n * (n + 1) * nz + n * n * (nz + 1) + n * n * nz
 
+
+def oracle_run(n: int, max_it: int = 2000):
+    """One full CPU run of the reference algorithm (oracle/ restatement, the
+    reference is pure Python + scipy) on the config-2 generator at n^3 with
+    hexflow's stage timers (hx/driver.py:110-140): stage 1 with n_workers=1
+    (SURVEY.md §8(d)), stage 2, GMRES(50) to 1e-8.  Input generation is not
+    timed."""
     from oracle import edfa_oracle as O
     from paper_2009_13916_b200 import configs
-    case = configs.config2(n=sample_n)
-    s = case.system
-    N = s.n_unknowns
+    s = configs.config2(n=n).system
     A = s.full_matrix()
-    workers = max(1, os.cpu_count() or 1)
+    b = s.rhs()
     t0 = time.perf_counter()
     sets = O.static_sets(s.grid, s.face_index, "A")
-    o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=sets, no_fill=True, n_workers=workers)
+    o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=sets, no_fill=True, n_workers=1)
     t1 = time.perf_counter()
     o2 = O.build_stage2(s.A_cc, o1, no_fill=True)
     t2 = time.perf_counter()
-    O.gmres(lambda v: A @ v, lambda r: O.apply(o1, o2, s.A_fc, s.A_cf, r), s.rhs(), tol=1e-30,
-            restart=50, max_it=1)                   # one-time scipy solver initialisation
-    t2g = time.perf_counter()
-    _, rep = O.gmres(lambda v: A @ v, lambda r: O.apply(o1, o2, s.A_fc, s.A_cf, r), s.rhs(), tol=1e-30,
-                     restart=50, max_it=gmres_iters)
+    _, rep = O.gmres(lambda v: A @ v, lambda r: O.apply(o1, o2, s.A_fc, s.A_cf, r), b, tol=1e-8, restart=50,
+                     max_it=max_it)
     t3 = time.perf_counter()
-    it_time = (t3 - t2g) / max(rep.n_it, 1)
-    N_full = None
-    per_dof_setup = (t2 - t0) / N
-    per_dof_iter = it_time / N
-    return dict(per_dof_setup=per_dof_setup, per_dof_iter=per_dof_iter, sample_N=N,
-                sample=f"oracle port on the config-2 generator at {sample_n}^3 (N={N}): full stage 1 (per-cell "
-                       f"loop over {workers} processes, as the reference's n_workers fan-out) + stage 2 and "
-                       f"{rep.n_it} GMRES(50) iterations (scipy, single-threaded); extrapolated per DOF to "
-                       f"{n_full}^3 with {n_iters_full} iterations",
-                cores=workers,
-                t_stage1=t1 - t0, t_stage2=t2 - t1, t_iter=it_time, _np=np)
+    N = s.n_unknowns
+    return dict(n=n, n_dof=N, t_stage1=t1 - t0, t_stage2=t2 - t1, t_solve=t3 - t2, iterations=rep.n_it,
+                converged=bool(rep.converged), final_relres=rep.final_relres,
+                mdof_s=N / (t3 - t0) / 1e6, setup_mdof_s=N / (t2 - t0) / 1e6, solve_mdof_s=N / (t3 - t2) / 1e6)
 
 
-def extrapolate(cb, N_full, iters):
-    t = N_full * cb["per_dof_setup"] + iters * N_full * cb["per_dof_iter"]
+def extrapolate(run, N_full, iters_full):
+    """Per-DOF setup cost and per-DOF-per-iteration solve cost of a measured
+    run, scaled to N_full DOF and iters_full GMRES iterations (stage-1 rows
+    are independent, the factorisation and the Krylov work are linear in N)."""
+    per_dof_setup = (run["t_stage1"] + run["t_stage2"]) / run["n_dof"]
+    per_dof_iter = run["t_solve"] / max(run["iterations"], 1) / run["n_dof"]
+    t = N_full * per_dof_setup + iters_full * N_full * per_dof_iter
     return N_full / t / 1e6
+
+
+def cpu_baseline(N_full, iters_full, n_sample=32):
+    """The GPU line's cpu_baseline: a bounded (~15 s) full oracle run on the
+    same generator at n_sample^3, one core, extrapolated to the workload."""
+    run = oracle_run(n_sample)
+    return {"value": extrapolate(run, N_full, iters_full), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": (f"oracle port (CPU restatement of hexflow's EDFA + GMRES(50)) on the config-2 generator at "
+                       f"{n_sample}^3 (N={run['n_dof']}): stage 1 (n_workers=1) {run['t_stage1']:.2f} s, "
+                       f"stage 2 {run['t_stage2']:.2f} s, GMRES {run['iterations']} it {run['t_solve']:.2f} s "
+                       f"(measured); extrapolated per DOF to N={N_full} with {iters_full} iterations"),
+            "measured_sample": run}
 
 
 # ---------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference's CPU algorithm on the box's host cores (no GPU).  The
+    headline ``value`` extrapolates one full, measured config-2 run (64^3,
+    stage timers, n_workers=1 as SURVEY.md §8(d)) per DOF to the bench config
+    (config 5: 67.2M DOF, CONFIG5_ITERS iterations) -- a 256^3 CPU run would
+    take ~10 hours; ``measured_config2`` is that run itself.  The W + K steps
+    are bounded 24^3 samples (~5 s each) whose extrapolations show the spread."""
     rank, world, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    from paper_2009_13916_b200 import configs  # noqa: F401
-    n_full = args.n or 64
-    # iteration count of the full workload: the oracle's own GMRES count is
-    # not affordable at 64^3 per step; use the survey-measured 87 (SURVEY.md
-    # §6.2, oracle restatement, config-2 shape) unless a smaller grid is asked
-    iters = 87
-    N_full = free_faces_config2(n_full) + n_full ** 3
-    vals = []
-    cb = None
+    cfg = args.config
+    n = args.n or DEFAULT_N[cfg]
+    if cfg in (2, 5):
+        N_full = n_dof_config2(n)
+        iters = CONFIG5_ITERS if (cfg == 5 and n == 256) else None
+    else:
+        raise SystemExit("--impl reference covers the config-2/5 generator")
+    full = oracle_run(64)
+    if iters is None:
+        iters = full["iterations"] if n == 64 else int(round(full["iterations"] * n / 64))
+    samples = []
     for k in range(max(args.warmup, 0) + args.steps):
-        cb = cpu_baseline(n_full, iters, sample_n=16, gmres_iters=5)
+        r = oracle_run(24)
         if k >= args.warmup:
-            vals.append(extrapolate(cb, N_full, iters))
-    v = statistics.mean(vals)
+            samples.append(extrapolate(r, N_full, iters))
+    v = extrapolate(full, N_full, iters) if not (cfg == 2 and n == 64) else full["mdof_s"]
+    workload = f"config{cfg}-{n}^3-staticA-IC0ILU0-gmres50"
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": metric_of(cfg), "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": N_full / (v * 1e6) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded config-2 generator)",
-        "config": {"workload": f"config2-{n_full}^3-staticA-IC0ILU0-gmres50", "n_dof": N_full,
-                   "rtol": 1e-8, "restart": 50, "l2": "inputs larger than L2"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "port", "sample": cb["sample"]},
+        "data": f"synthetic (seeded config-{cfg} generator)",
+        "config": {"workload": workload, "n_dof": N_full, "rtol": 1e-8, "restart": 50,
+                   "gmres_iterations_assumed": iters, "l2": "inputs larger than L2"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": (f"full measured oracle run on the config-2 generator at 64^3 (N={full['n_dof']}, "
+                                    f"stage timers, n_workers=1, {full['iterations']} GMRES iterations), "
+                                    + ("the bench workload itself" if (cfg == 2 and n == 64) else
+                                       f"extrapolated per DOF to N={N_full} with {iters} iterations"))},
+        "measured_config2": full,
+        "step_samples_extrapolated": samples,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def free_faces_config2(n):
-    # x-faces minus the two Dirichlet x-planes, plus y and z faces
-    return (n + 1) * n * n - 2 * n * n + 2 * n * (n + 1) * n
+# ---------------------------------------------------------------- algorithmic bytes (SURVEY.md §8(d))
+def csr_b(nnz, rows):
+    return 12.0 * nnz + 4.0 * (rows + 1)
+
+
+def spmv_b(nnz, rows, cols):
+    return csr_b(nnz, rows) + 8.0 * cols + 8.0 * rows
+
+
+def trsv_b(nnz, n):
+    return csr_b(nnz, n) + 16.0 * n
+
+
+def algorithmic_bytes(ds, pre, n_it, m):
+    """Setup bytes and total solve bytes of one step."""
+    i1, i2 = pre.stage1.info, pre.stage2.info
+    nf, ne = ds.n_free_faces, ds.n_cells
+    N = nf + ne
+    nnz = {k: getattr(ds, k).nnz for k in ("A_ff", "A_fc", "A_cf", "A_cc")}
+    q = 4.0 * i1.nnz_Q + 4.0 * (ne + 1)
+    setup = (csr_b(nnz["A_ff"], nf) + csr_b(nnz["A_cf"], ne) + csr_b(nnz["A_fc"], ne) + csr_b(nnz["A_cc"], ne) + q
+             + csr_b(i1.nnz_G, ne) + csr_b(i1.nnz_FT, ne) + csr_b(i1.nnz_H, ne) + csr_b(i1.nnz_L, nf)
+             + csr_b(i1.nnz_H, ne) + csr_b(i2.nnz_S, ne) + csr_b(i2.nnz_L, ne) + csr_b(i2.nnz_U, ne))
+    nnz_A = sum(nnz.values())
+    apply_b = (2 * (2 * trsv_b(i1.nnz_L, nf)) + spmv_b(nnz["A_cf"], ne, nf) + spmv_b(nnz["A_fc"], nf, ne)
+               + trsv_b(i2.nnz_L, ne) + trsv_b(i2.nnz_U, ne) + 8.0 * (3 * nf + 2 * ne))
+    spmv_A = spmv_b(nnz_A, N, N)
+    solve = 0.0
+    done, cycles = 0, 0
+    while done < n_it:
+        k = min(m, n_it - done)
+        solve += sum(spmv_A + apply_b + 8.0 * N * (2 * j + 5) for j in range(k))
+        solve += apply_b + 8.0 * N * (m + 2) + spmv_A + 16.0 * N     # restart: update + true residual
+        done += k
+        cycles += 1
+    return setup, solve
+
+
+def peak_hbm():
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        peaks = {}
+    if peaks.get("hbm_gbs"):
+        return float(peaks["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst)"
+    return 6650.0, "fallback 6650 GB/s (B200_PROFILING.md)"
 
 
 # ---------------------------------------------------------------- EDFA arm
+def profile_report(lib, c, reset=1):
+    import ctypes
+    n = lib.edfa_ctx_profile_report(c, None, 0, 0)
+    buf = ctypes.create_string_buffer(int(n))
+    lib.edfa_ctx_profile_report(c, buf, n, reset)
+    return json.loads(buf.value.decode())
+
+
+def device_inputs(case):
+    """Assemble the config on the device (device_assembly.assemble_device,
+    hx/assembly.py:186-333) -- the resident inputs of the timed region."""
+    import torch
+
+    from paper_2009_13916_b200 import device_assembly as DA
+    t = time.perf_counter()
+    dsys = DA.assemble_device(*case.meta["inputs"], element_ops=False)
+    torch.cuda.synchronize()
+    return dsys, time.perf_counter() - t
+
+
+def timed_steps(case, dsys, steps, warmup, lib, c, flush, clk=None):
+    """W untimed + K timed steps on the resident blocks; per-phase CUDA events
+    (stage 1, stage 2, solve) inside each step.  Returns per-step records and
+    the last step's objects."""
+    import torch
+
+    from paper_2009_13916_b200.device import DeviceSystem, system_operator
+    from paper_2009_13916_b200.krylov import gmres
+    g = case.meta["inputs"][0]
+    base = dsys.system
+    blocks = (base.A_ff, base.A_fc, base.A_cf, base.A_cc)
+    b = base.rhs()
+
+    def step():
+        ds = DeviceSystem(*blocks, rhs=b, topology_src=dsys.topology_inputs)
+        ds.set_grid(g.nx, g.ny, g.nz)
+        s1 = stage1_of(case, ds)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        pre = precond_of(case, ds, s1)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e2.record()
+        x, rep = gmres(system_operator(ds), pre, b, tol=case.rtol, restart=case.restart, max_it=case.max_it)
+        return ds, pre, x, rep, e1, e2
+
+    recs, last = [], None
+    ds = pre = x = rep = None
+    for w in range(warmup + steps):
+        timed = w >= warmup
+        if timed:
+            flush.fill_(1.0)                        # evict L2 between steps
+        torch.cuda.synchronize()
+        e0, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        last = ds = pre = x = rep = None             # one preconditioner alive at a time (256^3 memory)
+        e0.record()
+        ds, pre, x, rep, e1, e2 = step()
+        e3.record()
+        torch.cuda.synchronize()
+        if timed:
+            recs.append(dict(ms=e0.elapsed_time(e3), stage1_ms=e0.elapsed_time(e1), stage2_ms=e1.elapsed_time(e2),
+                             solve_ms=e2.elapsed_time(e3), n_it=rep.n_it, relres=rep.final_relres,
+                             converged=rep.converged))
+        last = (ds, pre, x, rep)
+    return recs, last
+
+
 def run_edfa(args):
+    import ctypes
+
     import numpy as np
     import torch
 
     rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    from paper_2009_13916_b200 import _lib, configs
-    from paper_2009_13916_b200.device import DeviceSystem, ctx, system_operator
+    from paper_2009_13916_b200 import _lib
+    from paper_2009_13916_b200.device import DeviceSystem, ctx, pinned_copy, system_operator
     from paper_2009_13916_b200.krylov import gmres
-    from paper_2009_13916_b200.precond import BlockLDUPreconditioner, patterns_for
 
     lib = _lib.lib()
-    diag = []
-    if os.environ.get("EDFA_BENCH_DIAG"):      # slow-call tracer (diagnostics only)
-        for _name in _lib._SIGS:
-            _fn = getattr(lib, _name)
-
-            def _w(*a, _fn=_fn, _name=_name):
-                t = time.perf_counter()
-                r = _fn(*a)
-                dt = time.perf_counter() - t
-                if dt > 0.03:
-                    diag.append((_name, round(dt * 1e3, 1)))
-                return r
-            setattr(lib, _name, _w)
-    case = make_case(args)
-    if args.n is None:
-        args.n = DEFAULT_N[args.config] or 0
-    s = case.system
-    N = s.n_unknowns
-    # resident inputs: the four blocks, the rhs and the grid's index arrays;
-    # every step derives everything else on the device (merged A, SELL
-    # copies, topology, patterns, stage 1/2, GMRES)
-    from paper_2009_13916_b200.device import DeviceCsr
-    blocks = tuple(DeviceCsr.from_scipy(getattr(s, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc"))
-    topo_src = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-                     for a in (s.grid.elem_to_faces, s.grid.face_to_elems, s.face_index))
-    b_dev = torch.from_numpy(s.rhs()).to(dev)
+    cfg = args.config
+    if cfg == 4:
+        raise SystemExit("config 4 (time-step sequence): use tools/converge_sweep.py / tests for evidence runs")
+    n = args.n or DEFAULT_N[cfg]
+    case = make_case(cfg, n, host=False)
+    dsys, t_asm = device_inputs(case)
+    N = dsys.n_unknowns
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
-    import ctypes
-
-    from paper_2009_13916_b200 import _lib
     c = ctx()
 
-    def step(_unused, b):
-        system_dev = DeviceSystem(*blocks, rhs=b, host=s, topology_src=topo_src)
-        pre = build_pre(case, system_dev)
-        x, rep = gmres(system_operator(system_dev), pre, b, tol=case.rtol, restart=case.restart,
-                       max_it=case.max_it)
-        return x, rep, pre
-
-    n_systems = 1
-    if args.config == 4 and not args.single_system:
-        # BASELINE config 4: one step = the 10-system time-step sequence -- stage 1
-        # once, then per time step update_accumulation (A_cc + diag(acc/dt), rhs_c)
-        # on the device, stage-2 refresh and GMRES from the previous pressure
-        from paper_2009_13916_b200.device import DeviceCsr
-        from paper_2009_13916_b200.device_assembly import next_dt
-        m = case.meta
-        n_systems = int(m["n_steps"])
-        acc_d = torch.from_numpy(np.ascontiguousarray(s.accumulation)).to(dev)
-        rcb_d = torch.from_numpy(np.ascontiguousarray(s.rhs_c_base)).to(dev)
-        rhs_f_d = torch.from_numpy(np.ascontiguousarray(s.rhs_f)).to(dev)
-        Acc_steady = DeviceCsr.from_scipy(s.A_cc_steady)
-        nf = s.n_free_faces
-
-        def step(_unused, b):
-            system_dev = DeviceSystem(*blocks, rhs=b, host=s, topology_src=topo_src)
-            pre = build_pre(case, system_dev)         # stage 1 + stage 2 of the first system
-            dt, x, reps_seq = float(m["dt0"]), None, []
-            p_prev = torch.full((s.n_cells,), float(m["p_init"]), dtype=torch.float64, device=dev)
-            for k in range(n_systems):
-                if k == 0:
-                    sk = system_dev
-                else:
-                    rhs_c = torch.empty_like(rcb_d)
-                    h = ctypes.c_void_p()
-                    _lib.check(lib.edfa_update_accumulation(c, Acc_steady.handle, acc_d.data_ptr(),
-                                                            rcb_d.data_ptr(), p_prev.data_ptr(), dt,
-                                                            ctypes.byref(h), rhs_c.data_ptr()))
-                    sk = DeviceSystem(blocks[0], blocks[1], blocks[2], DeviceCsr(h),
-                                      rhs=torch.cat([rhs_f_d, rhs_c]), host=s, topology_src=topo_src)
-                    pre.refresh(sk)                   # stage 2 only; stage 1 reused
-                x, rep = gmres(system_operator(sk), pre, sk.rhs(), tol=case.rtol, restart=case.restart,
-                               max_it=case.max_it)
-                reps_seq.append(rep)
-                # TimestepController (hx/driver.py:50-53): dt * min(mult, dp_target / dp_max), capped
-                dp_max = float((x[nf:] - p_prev).abs().max())
-                dt = next_dt(dt, float(m["dt_max"]), float(m["dt_mult"]), float(m["dp_target"]), dp_max)
-                p_prev = x[nf:]
-            rep.seq_iterations = [r.n_it for r in reps_seq]
-            rep.seq_relres = max(r.final_relres for r in reps_seq)
-            return x, rep, pre
-
-    def report(c, reset=1):
-        n = lib.edfa_ctx_profile_report(c, None, 0, 0)
-        buf = ctypes.create_string_buffer(int(n))
-        lib.edfa_ctx_profile_report(c, buf, n, reset)
-        return json.loads(buf.value.decode())
-
-    c = ctx()
-    for w in range(args.warmup):
-        last = w == args.warmup - 1
-        if last:   # full per-kernel event profile of one (untimed) step: shares + dominant kernel
-            lib.edfa_ctx_profile_filter(c, b"")
-            lib.edfa_ctx_profile(c, 1)
-            report(c)
-        x = rep = pre = None              # one preconditioner alive at a time (256^3 memory)
-        x, rep, pre = step(None, b_dev)
-        if last:
-            prof_full = report(c)
-            lib.edfa_ctx_profile(c, 0)
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    # ---- profile of one (untimed) warm-up step: kernel shares, dominant kernel
+    lib.edfa_ctx_profile_filter(c, b"")
+    lib.edfa_ctx_profile(c, 1)
+    profile_report(lib, c)
+    _, last = timed_steps(case, dsys, 0, 1, lib, c, flush)
+    prof_full = profile_report(lib, c)
+    lib.edfa_ctx_profile(c, 0)
+    last = None
     dom_name = max(prof_full.items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
 
     # ---- device-resident timed region; CUDA events bracket every launch of
     # the dominant kernel only (cheap enough not to perturb the step)
     lib.edfa_ctx_profile_filter(c, dom_name.encode())
     lib.edfa_ctx_profile(c, 1)
-    report(c)
+    profile_report(lib, c)
     launches0 = lib.edfa_ctx_launch_count(c)
-    times = []
-    reps = []
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            flush.fill_(1.0)                        # evict L2 between steps
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            x = rep = pre = None
-            e0.record()
-            x, rep, pre = step(None, b_dev)
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-            reps.append(rep)
-            if diag:
-                print("diag step", len(times), times[-1], diag, file=sys.stderr, flush=True)
-                diag.clear()
+        recs, last = timed_steps(case, dsys, args.steps, max(args.warmup - 1, 0), lib, c, flush)
     launches = lib.edfa_ctx_launch_count(c) - launches0
-    prof = report(c)
+    prof = profile_report(lib, c)
     lib.edfa_ctx_profile(c, 0)
     lib.edfa_ctx_profile_filter(c, b"")
     clocks = clk.summary()
-    t_total_ms = sum(times)
-    if world > 1:
-        tt = torch.tensor([t_total_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_total_ms = float(tt.item())
-    value = world * N * n_systems * args.steps / (t_total_ms / 1e3) / 1e6
-
-    n_it_last, relres_last = reps[-1].n_it, reps[-1].final_relres
-    seq_its = getattr(reps[-1], "seq_iterations", None)
-    seq_rel = getattr(reps[-1], "seq_relres", None)
-    del x, rep, pre, reps                 # release the timed step's preconditioner before the e2e leg
+    t_total_ms = sum(r["ms"] for r in recs)
+    value = N * args.steps / (t_total_ms / 1e3) / 1e6
+    ds, pre, x, rep = last
+    setup_b, solve_b = algorithmic_bytes(ds, pre, rep.n_it, case.restart)
+    peak, peak_src = peak_hbm()
+    med = {k: statistics.median(r[k] for r in recs) for k in ("ms", "stage1_ms", "stage2_ms", "solve_ms")}
+    setup_ms = med["stage1_ms"] + med["stage2_ms"]
+    phases = {
+        "stage1_ms": med["stage1_ms"], "stage2_ms": med["stage2_ms"], "solve_ms": med["solve_ms"],
+        "setup_mdof_s": N / (setup_ms / 1e3) / 1e6, "solve_mdof_s": N / (med["solve_ms"] / 1e3) / 1e6,
+        "ms_per_iteration": med["solve_ms"] / max(rep.n_it, 1),
+        "setup_algorithmic_bytes": setup_b, "solve_algorithmic_bytes": solve_b,
+        "setup_hbm_frac": setup_b / (setup_ms / 1e3) / 1e9 / peak,
+        "solve_hbm_frac": solve_b / (med["solve_ms"] / 1e3) / 1e9 / peak,
+        "note": "phase fractions = SURVEY.md 8(d) algorithmic bytes / phase time / HBM peak; the setup phase "
+                "includes system creation (merged A, SELL copies, topology) in stage 1",
+    }
+    del pre, x, ds
+    last = None
+    lib.edfa_ctx_trim(c)                     # hand the library's cached blocks back before the e2e leg
 
     # ---- end-to-end through the public API from host scipy blocks
-    e2e_times = []
-    from paper_2009_13916_b200.device import pinned_copy
-    s_pin = pinned_copy(s)              # the host application's page-locked staging of the inputs
-    h2d = sum(getattr(s, n).data.nbytes + getattr(s, n).indices.nbytes + getattr(s, n).indptr.nbytes
-              for n in ("A_ff", "A_fc", "A_cf", "A_cc")) + s.rhs().nbytes
-    h2d += 4 * (12 * s.n_cells + s.face_index.size)      # cell->face map, neighbours, face index
+    s_host = dsys.to_host()
+    s_pin = pinned_copy(s_host)              # the host application's page-locked staging of the inputs
+    h2d = sum(getattr(s_host, k).data.nbytes + getattr(s_host, k).indices.nbytes + getattr(s_host, k).indptr.nbytes
+              for k in ("A_ff", "A_fc", "A_cf", "A_cc")) + s_host.rhs().nbytes
+    h2d += 4 * (12 * s_host.n_cells + s_host.face_index.size)      # cell->face map, neighbours, face index
     d2h = N * 8
-    for k in range(max(1, min(args.steps, 3))):
+    e2e_times = []
+    x_h = None
+    for _ in range(max(1, min(args.steps, 2))):
+        x_h = None
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ds_h = DeviceSystem.from_host(s_pin)                  # H2D of the four blocks, rhs, topology
         pre_h = build_pre(case, ds_h)                          # patterns from the device topology
         x_h, rep_h = gmres(system_operator(ds_h), pre_h, s_pin.rhs(), tol=case.rtol, restart=case.restart,
                            max_it=case.max_it)                # x returned to host (D2H)
-        s_k = s_pin
-        if n_systems > 1:   # the time-step sequence as a host application drives it
-            from paper_2009_13916_b200 import assembly as host_asm
-            from paper_2009_13916_b200.device_assembly import next_dt
-            m = case.meta
-            dt, p_prev_h = float(m["dt0"]), np.full(s.n_cells, float(m["p_init"]))
-            for q in range(1, n_systems):
-                p_new_h = x_h[s.n_free_faces:]
-                dt = next_dt(dt, float(m["dt_max"]), float(m["dt_mult"]), float(m["dp_target"]),
-                             float(np.abs(p_new_h - p_prev_h).max()))
-                p_prev_h = p_new_h
-                s_k = host_asm.update_accumulation(s_pin, dt, p_new_h)                # host A_cc, rhs_c
-                pre_h.refresh(s_k)                                                   # H2D of A_cc
-                x_h, rep_h = gmres(system_operator(pre_h.device_system), pre_h, s_k.rhs(), tol=case.rtol,
-                                   restart=case.restart, max_it=case.max_it)
         e2e_times.append(time.perf_counter() - t0)
         del ds_h, pre_h
-    if n_systems > 1:
-        h2d += (n_systems - 1) * (12 * s.A_cc.nnz + 4 * (s.n_cells + 1) + 8 * N)
-        d2h *= n_systems
-    e2e_val = world * N * n_systems / statistics.median(e2e_times) / 1e6
-    relres_host = float(np.linalg.norm(s_k.rhs() - s_k.full_matrix() @ x_h) / np.linalg.norm(s_k.rhs()))
+    e2e_val = N / statistics.median(e2e_times) / 1e6
+    A_h = s_host.full_matrix()
+    relres_host = float(np.linalg.norm(s_host.rhs() - A_h @ x_h) / np.linalg.norm(s_host.rhs()))
+    del A_h, s_pin
 
-    # ---- roofline of the dominant kernel
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs")
-    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs, burst)" if peak else "fallback 6650 GB/s (B200_PROFILING.md)"
-    peak = peak or 6650.0
-    dom = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", {"ms": 0, "bytes": 0, "launches": 1})
-    dname, d = dom
+    # ---- roofline of the dominant kernel (live CUDA events over the timed region)
+    dname, d = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", {"ms": 0, "bytes": 0,
+                                                                                  "launches": 1})
     per_launch_ms = d["ms"] / max(d["launches"], 1)
     per_launch_bytes = d["bytes"] / max(d["launches"], 1)
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
     traffic = None
     try:
-        nc = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
-        traffic = nc.get(dname)
+        traffic = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text()).get(f"config{cfg}", {}).get(dname)
     except Exception:
         pass
-    step_ms = t_total_ms / args.steps
     tot_full = max(sum(p["ms"] for p in prof_full.values()), 1e-9)
-    shares = {k: round(v["ms"] / tot_full, 4) for k, v in sorted(prof_full.items(), key=lambda kv: -kv[1]["ms"])[:8]}
-    kernel_ms_per_step = tot_full
-
+    shares = {k: round(v["ms"] / tot_full, 4) for k, v in sorted(prof_full.items(), key=lambda kv: -kv[1]["ms"])[:10]}
+    g = case.meta["inputs"][0]
     line = {
-        "metric": METRIC_OF(args.config), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": ("synthetic (seeded config-2 generator: 64^3, lnK~N(0,2), kz/kx=0.1)" if args.config == 2
-                 else f"synthetic (seeded generator of BASELINE config {args.config}: {case.name})"),
-        "config": {"workload": (f"config2-{args.n}^3-staticA-{inner_tag(case)}-gmres50" if args.config == 2
-                                else f"{case.name}-{inner_tag(case)}-gmres50"), "n_dof": N,
-                   "n_free_faces": s.n_free_faces, "n_cells": s.n_cells, "rtol": case.rtol,
-                   "restart": case.restart, "gmres_iterations": n_it_last,
-                   "final_true_relres": relres_last, "host_check_relres": relres_host,
-                   **({"systems_per_step": n_systems, "sequence_iterations": seq_its,
-                       "sequence_max_relres": seq_rel} if n_systems > 1 else {}),
-                   "parallelism": "single", "step_ms": [round(t, 3) for t in times],
-                   "l2": "inputs larger than L2 and a 256 MiB L2 flush between steps"},
+        "data": f"synthetic (seeded generator of BASELINE config {cfg}: {case.name}), assembled on the device",
+        "config": {"workload": f"{case.name}-{inner_tag(case)}-gmres50", "grid": [g.nx, g.ny, g.nz], "n_dof": N,
+                   "n_free_faces": dsys.n_free_faces, "n_cells": dsys.n_cells, "rtol": case.rtol,
+                   "restart": case.restart, "gmres_iterations": rep.n_it, "final_true_relres": rep.final_relres,
+                   "host_check_relres": relres_host, "parallelism": "single",
+                   "step_ms": [round(r["ms"], 3) for r in recs],
+                   "l2": "inputs larger than L2 and a 256 MiB L2 flush between steps",
+                   "input_assembly_s": t_asm},
+        "phases": phases,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "seconds_per_step": statistics.median(e2e_times)},
+                "seconds_per_step": statistics.median(e2e_times),
+                "note": "host blocks page-locked once before the timed region (pinned_copy); the copies are timed"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "launches_per_step": d["launches"] / args.steps,
-                     "step_share_of_kernel_time": shares, "kernel_ms_per_step": kernel_ms_per_step,
-                     "shares_from": "per-kernel CUDA events of the last warm-up step (same workload)"},
+                     "step_share_of_kernel_time": shares, "kernel_ms_per_step": tot_full,
+                     "shares_from": "per-kernel CUDA events of one untimed warm-up step (same workload)"},
         "clocks": clocks,
     }
-    if rank == 0 and "inputs" in case.meta:
-        line["assembly"] = assembly_leg(case, c, lib, report, N)
-    if args.profile_json and rank == 0:
+    if args.profile_json:
         pathlib.Path(args.profile_json).write_text(json.dumps({"timed_region": prof, "warmup_step": prof_full},
                                                               indent=1))
-    if rank == 0 and not args.no_cpu_baseline and args.config == 2:
-        cb = cpu_baseline(args.n, n_it_last)
-        v = extrapolate(cb, N, n_it_last)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": "port",
-                                "sample": cb["sample"]}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.barrier()
-        torch.distributed.destroy_process_group()
+    lib.edfa_ctx_trim(c)
+    line["assembly"] = assembly_leg(case, c, lib, N)
+    if cfg != 2 and not args.no_config2:
+        line["config2"] = config2_leg(lib, c, flush)
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(N, rep.n_it)
+    print(json.dumps(line), flush=True)
 
 
-def assembly_leg(case, c, lib, report, N):
+def config2_leg(lib, c, flush, steps=5, warmup=2):
+    """BASELINE config 2 (64^3) on the same path: the previous headline, kept
+    for comparison across rounds."""
+    case = make_case(2, 64, host=False)
+    dsys, _ = device_inputs(case)
+    recs, last = timed_steps(case, dsys, steps, warmup, lib, c, flush)
+    N = dsys.n_unknowns
+    t = sum(r["ms"] for r in recs)
+    return {"workload": f"{case.name}-{inner_tag(case)}-gmres50", "value": N * steps / (t / 1e3) / 1e6,
+            "unit": UNIT, "ms_per_step": t / steps, "gmres_iterations": last[3].n_it,
+            "final_true_relres": last[3].final_relres,
+            "stage1_ms": statistics.median(r["stage1_ms"] for r in recs),
+            "stage2_ms": statistics.median(r["stage2_ms"] for r in recs),
+            "solve_ms": statistics.median(r["solve_ms"] for r in recs)}
+
+
+def assembly_leg(case, c, lib, N):
     """The device assembly of the same system (the
     producer of the path's blocks): hexflow's assemble through
     device_assembly.assemble_device -- grid arrays and tensors uploaded from
@@ -531,7 +579,7 @@ def assembly_leg(case, c, lib, report, N):
     torch.cuda.synchronize()
     lib.edfa_ctx_profile_filter(c, b"asm_")
     lib.edfa_ctx_profile(c, 1)
-    report(c)
+    profile_report(lib, c)
     ts = []
     for _ in range(3):
         torch.cuda.synchronize()
@@ -540,7 +588,7 @@ def assembly_leg(case, c, lib, report, N):
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
         del d
-    prof = report(c)
+    prof = profile_report(lib, c)
     lib.edfa_ctx_profile(c, 0)
     lib.edfa_ctx_profile_filter(c, b"")
     kms = sum(v["ms"] for v in prof.values()) / 3

@@ -127,6 +127,9 @@ int edfa_ctx_set_stream(edfa_ctx* ctx, void* cuda_stream);
 int edfa_ctx_set_option(edfa_ctx* ctx, const char* name, int value);
 int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value);
 int edfa_ctx_sync(edfa_ctx* ctx);
+/* Return the context's cached (freed, stream-ordered) device blocks to the
+ * driver -- synchronises the stream. */
+int edfa_ctx_trim(edfa_ctx* ctx);
 int edfa_ctx_destroy(edfa_ctx* ctx);
 /* Per-kernel CUDA-event timing with algorithmic byte counts (roofline). */
 int edfa_ctx_profile(edfa_ctx* ctx, int enable);

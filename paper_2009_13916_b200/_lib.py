@@ -72,6 +72,7 @@ _SIGS = {
     "edfa_ctx_create": (i32, [i32, vp, C.POINTER(vp)]),
     "edfa_ctx_set_stream": (i32, [vp, vp]),
     "edfa_ctx_sync": (i32, [vp]),
+    "edfa_ctx_trim": (i32, [vp]),
     "edfa_ctx_set_option": (i32, [vp, C.c_char_p, i32]),
     "edfa_ctx_get_option": (i32, [vp, C.c_char_p, P_i32]),
     "edfa_ctx_destroy": (i32, [vp]),

@@ -43,12 +43,29 @@ class CaseSpec:
     meta: dict = field(default_factory=dict)
 
 
+HOST_ASSEMBLY = True   # False: configs carry only their inputs (system=None); see inputs_only()
+
+
 def _assemble(g, fld, props, bc, dt, p_prev):
     """Host assembly plus the inputs it was built from (kept so the device
     assembly, device_assembly.assemble_device, can rebuild the same system)."""
+    if not HOST_ASSEMBLY:
+        return None, dict(inputs=(g, fld, props, bc, dt, p_prev), host_assembly_s=None)
     t = time.perf_counter()
     s = assembly.assemble(g, fld, props, bc, dt=dt, p_prev=p_prev)
     return s, dict(inputs=(g, fld, props, bc, dt, p_prev), host_assembly_s=time.perf_counter() - t)
+
+
+def inputs_only(idx: int, **kw) -> CaseSpec:
+    """The config's grid, field, properties and boundary conditions without the
+    host assembly (``case.system`` is None): large grids are assembled on the
+    device (device_assembly.assemble_device(*case.meta["inputs"]))."""
+    global HOST_ASSEMBLY
+    HOST_ASSEMBLY = False
+    try:
+        return make(idx, **kw)
+    finally:
+        HOST_ASSEMBLY = True
 
 
 def _inner():
@@ -104,11 +121,11 @@ def config3(n=128, seed=SEEDS[3]):
                     dict(pattern="dynamic", n_add=1, n_ent=4, **_inner()), meta=meta)
 
 
-def channelised_field(nx, ny, nz, seed, sigma=2.5, kv_kh=0.1, n_channel_layers=None):
+def channelised_field(nx, ny, nz, seed, sigma=2.5, kv_kh=0.1, n_channel_layers=None, layer_sd=1.5):
     """Layered log-normal background plus high-K sinuous channels in the top
     layers (k x 1e3 inside y0 + a sin(2 pi x / lambda + phi) bands)."""
     rng = np.random.default_rng(seed)
-    mu = rng.normal(0.0, 1.5, size=nz)
+    mu = rng.normal(0.0, layer_sd, size=nz)
     lnk = mu[:, None, None] + rng.normal(0.0, sigma, size=(nz, ny, nx))
     top = n_channel_layers if n_channel_layers is not None else max(1, nz // 2)
     x = np.arange(nx)[None, :]
@@ -126,9 +143,9 @@ def channelised_field(nx, ny, nz, seed, sigma=2.5, kv_kh=0.1, n_channel_layers=N
     return mesh.Conductivity.diagonal(k, k, kv_kh * k)
 
 
-def config4(nx=60, ny=220, nz=85, seed=SEEDS[4], dt=0.1):
+def config4(nx=60, ny=220, nz=85, seed=SEEDS[4], dt=0.1, sigma=2.5, layer_sd=1.5):
     g = mesh.box_grid(nx, ny, nz, 6.1, 3.05, 0.61)
-    fld = channelised_field(nx, ny, nz, seed)
+    fld = channelised_field(nx, ny, nz, seed, sigma=sigma, layer_sd=layer_sd)
     bc = mesh.Boundaries(wells=[(0, 0, 200.0), (nx - 1, 0, 200.0),
                                 (0, ny - 1, 200.0), (nx - 1, ny - 1, 200.0),
                                 (nx // 2, ny // 2, 100.0)])

@@ -144,18 +144,28 @@ struct I64 {
     __host__ __device__ int64_t operator()(int v) const { return (int64_t)v; }
 };
 
-// contiguous (chain-major) layout for the scan solver
-__global__ void k_chain_fill_contig(CsrV D, const int* __restrict__ succ, const int* __restrict__ heads, int n_chains,
-                                    const int64_t* __restrict__ cptr, int* __restrict__ rows, double* __restrict__ coef,
-                                    double* __restrict__ dinv, const double* __restrict__ diag, bool unit) {
+// lane-interleaved layout for the warp solvers: chain t's k-th row at
+// t*32E + (k % E)*32 + k / E, so lane l owns the consecutive segment
+// [l*E, l*E + E) and a warp-wide load of step j is one coalesced line
+__global__ void k_chain_fill_il(CsrV D, const int* __restrict__ succ, const int* __restrict__ heads, int n_chains,
+                                int E, int* __restrict__ rows, double* __restrict__ coef, double* __restrict__ dinv,
+                                const double* __restrict__ diag, bool unit) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_chains) return;
-    int64_t p = cptr[t];
-    for (int r = heads[t]; r >= 0; r = succ[r], ++p) {
+    const int64_t base = (int64_t)t * 32 * E;
+    int k = 0;
+    for (int r = heads[t]; r >= 0; r = succ[r], ++k) {
+        const int64_t p = base + (k % E) * 32 + k / E;
         rows[p] = r;
         int e = D.ptr[r];
         coef[p] = (D.ptr[r + 1] > e && D.val) ? D.val[e] : 0.0;
         dinv[p] = (unit || !diag) ? 1.0 : 1.0 / diag[r];
+    }
+    for (; k < 32 * E; ++k) {
+        const int64_t p = base + (k % E) * 32 + k / E;
+        rows[p] = -1;
+        coef[p] = 0.0;
+        dinv[p] = 0.0;
     }
 }
 
@@ -164,59 +174,52 @@ __global__ void k_chain_fill_contig(CsrV D, const int* __restrict__ succ, const 
 // a warp scan composes across lanes, then every lane replays its segment.
 // Depth log2(32) + E instead of the chain length.
 template <int E>
-__global__ void __launch_bounds__(256) k_chain_scan(const int64_t* __restrict__ cptr, const int* __restrict__ rows,
-                                                    const double* __restrict__ coef, const double* __restrict__ dinv,
-                                                    int n_chains, const double* __restrict__ b, double alpha,
+__global__ void __launch_bounds__(256) k_chain_scan(const int* __restrict__ rows, const double* __restrict__ coef,
+                                                    const double* __restrict__ dinv, int n_chains,
+                                                    const double* __restrict__ b, double alpha,
                                                     double* __restrict__ x, const double* __restrict__ add,
                                                     double* __restrict__ out2) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= n_chains) return;
-    const int64_t s = cptr[w], e = cptr[w + 1];
-    double xin = 0.0;
-    for (int64_t c0 = s; c0 < e; c0 += 32 * E) {
-        int r[E];
-        double al[E], be[E];
+    const int64_t base = (int64_t)w * 32 * E + lane;
+    int r[E];
+    double al[E], be[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-            int64_t q = c0 + lane * E + j;
-            r[j] = q < e ? rows[q] : -1;
-            double d = q < e ? dinv[q] : 0.0, cf = q < e ? coef[q] : 0.0;
-            al[j] = d;
-            be[j] = -cf * d;
-        }
+    for (int j = 0; j < E; ++j) {
+        r[j] = rows[base + 32 * j];
+        const double d = dinv[base + 32 * j], cf = coef[base + 32 * j];
+        al[j] = d;
+        be[j] = -cf * d;
+    }
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-            if (r[j] >= 0) al[j] = al[j] * (alpha * b[r[j]]);
-            else { al[j] = 0.0; be[j] = 1.0; }
-        }
-        double A = al[0], B = be[0];
+    for (int j = 0; j < E; ++j) {
+        if (r[j] >= 0) al[j] = al[j] * (alpha * b[r[j]]);
+        else { al[j] = 0.0; be[j] = 1.0; }
+    }
+    double A = al[0], B = be[0];
 #pragma unroll
-        for (int j = 1; j < E; ++j) {
-            A = fma(be[j], A, al[j]);
-            B = be[j] * B;
-        }
+    for (int j = 1; j < E; ++j) {
+        A = fma(be[j], A, al[j]);
+        B = be[j] * B;
+    }
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            double Ap = __shfl_up_sync(0xffffffffu, A, off), Bp = __shfl_up_sync(0xffffffffu, B, off);
-            if (lane >= off) {
-                A = fma(B, Ap, A);
-                B = B * Bp;
-            }
+    for (int off = 1; off < 32; off <<= 1) {
+        double Ap = __shfl_up_sync(0xffffffffu, A, off), Bp = __shfl_up_sync(0xffffffffu, B, off);
+        if (lane >= off) {
+            A = fma(B, Ap, A);
+            B = B * Bp;
         }
-        double Ae = __shfl_up_sync(0xffffffffu, A, 1), Be = __shfl_up_sync(0xffffffffu, B, 1);
-        if (lane == 0) { Ae = 0.0; Be = 1.0; }
-        double xl = fma(Be, xin, Ae);
+    }
+    double xl = __shfl_up_sync(0xffffffffu, A, 1);
+    if (lane == 0) xl = 0.0;
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-            double v = fma(be[j], xl, al[j]);
-            if (r[j] >= 0) {
-                x[r[j]] = v;
-                if (out2) out2[r[j]] = v + add[r[j]];
-            }
-            xl = v;
+    for (int j = 0; j < E; ++j) {
+        double v = fma(be[j], xl, al[j]);
+        if (r[j] >= 0) {
+            x[r[j]] = v;
+            if (out2) out2[r[j]] = v + add[r[j]];
         }
-        double A31 = __shfl_sync(0xffffffffu, A, 31), B31 = __shfl_sync(0xffffffffu, B, 31);
-        xin = fma(B31, xin, A31);
+        xl = v;
     }
 }
 
@@ -227,21 +230,20 @@ __global__ void __launch_bounds__(256) k_chain_scan(const int64_t* __restrict__ 
 // kept in registers (chains of at most 32*E rows).  Half the launches and no
 // HBM round trip for the intermediate vector.
 template <int E>
-__global__ void __launch_bounds__(256) k_chain_pair(const int64_t* __restrict__ cptr, const int* __restrict__ rows,
+__global__ void __launch_bounds__(256, E <= 8 ? 2 : 1) k_chain_pair(const int* __restrict__ rows,
                                                     const double* __restrict__ coef, const double* __restrict__ dinv,
                                                     int n_chains, const double* b, double alpha, double* x,
                                                     const double* __restrict__ add, double* __restrict__ out2) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= n_chains) return;
-    const int64_t s = cptr[w], e = cptr[w + 1];
+    const int64_t base = (int64_t)w * 32 * E + lane;
     int r[E];
     double d[E], cf[E], xv[E];
 #pragma unroll
-    for (int j = 0; j < E; ++j) {
-        const int64_t q = s + lane * E + j;
-        r[j] = q < e ? rows[q] : -1;
-        d[j] = q < e ? dinv[q] : 0.0;
-        cf[j] = q < e ? coef[q] : 0.0;
+    for (int j = 0; j < E; ++j) {   // coalesced: step j of all 32 lanes is one line
+        r[j] = rows[base + 32 * j];
+        d[j] = dinv[base + 32 * j];
+        cf[j] = coef[base + 32 * j];
     }
     // forward: x_i = al_i + be_i x_{i-1}
     double al[E], be[E];
@@ -358,31 +360,24 @@ bool build_chain(Ctx* c, const Csr& deps, const double* diag, bool unit, ChainPl
     cp.dinv.reset(c, std::max<int64_t>(total, 1));
     cp.heads = std::move(heads_s);
     cp.succ = std::move(succ);
-    cp.cptr.reset(c, (size_t)nc + 1);
-    {
-        size_t bytes = 0;
-        cub::TransformInputIterator<int64_t, I64, const int*> it(lens_s.p, I64());
-        cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, cp.cptr.p, nc, c->stream);
-        EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(bytes), bytes, it, cp.cptr.p, nc, c->stream));
-        int64_t nn = n;
-        EDFA_CUDA(cudaMemcpyAsync(cp.cptr.p + nc, &nn, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
-        EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    }
-    cp.crow.reset(c, n);
-    cp.ccoef.reset(c, n);
-    cp.cdinv.reset(c, n);
-    {   // longest chain (decides whether the fused L, L^T kernel applies)
+    {   // longest chain -> segment length E of the warp solvers (lane-interleaved layout)
         int* mx = c->d_scalar_i + 34;
         EDFA_CUDA(cudaMemsetAsync(mx, 0, sizeof(int), c->stream));
         k_max_int<<<ceil_div(nc, 256), 256, 0, c->stream>>>(lens_s.p, nc, mx);
         EDFA_CUDA(cudaMemcpyAsync(&cp.max_len, mx, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         EDFA_CUDA(cudaStreamSynchronize(c->stream));
     }
+    cp.E = chain_segment(cp.max_len);
+    if (cp.E == 0) return false;   // chains longer than 512 rows: level plans instead
+    const int64_t il = (int64_t)nc * 32 * cp.E;
+    cp.crow.reset(c, il);
+    cp.ccoef.reset(c, il);
+    cp.cdinv.reset(c, il);
     Prof pr(c, "chain_plan", 24.0 * total);
     k_chain_fill<<<ceil_div(nc, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, nc, cp.gbase.p,
                                                            cp.rows.p, cp.coef.p, cp.dinv.p, diag, unit);
-    k_chain_fill_contig<<<ceil_div(nc, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, nc, cp.cptr.p,
-                                                                  cp.crow.p, cp.ccoef.p, cp.cdinv.p, diag, unit);
+    k_chain_fill_il<<<ceil_div(nc, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, nc, cp.E, cp.crow.p,
+                                                              cp.ccoef.p, cp.cdinv.p, diag, unit);
     check_launch("k_chain_fill");
     return true;
 }
@@ -392,16 +387,36 @@ void chain_values(Ctx* c, const Csr& deps, const double* diag, ChainPlan& cp) {
     k_chain_fill<<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p, cp.n_chains,
                                                                     cp.gbase.p, cp.rows.p, cp.coef.p, cp.dinv.p,
                                                                     diag, cp.unit);
-    k_chain_fill_contig<<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(
-        view(deps), cp.succ.p, cp.heads.p, cp.n_chains, cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, diag, cp.unit);
+    k_chain_fill_il<<<ceil_div(cp.n_chains, 128), 128, 0, c->stream>>>(view(deps), cp.succ.p, cp.heads.p,
+                                                                       cp.n_chains, cp.E, cp.crow.p, cp.ccoef.p,
+                                                                       cp.cdinv.p, diag, cp.unit);
     check_launch("k_chain_fill");
+}
+
+#define EDFA_CHAIN_E(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(12) X(16)
+
+int chain_segment(int max_len) {
+    const int need = std::max(1, ceil_div(max_len, 32));
+#define EDFA_E_PICK(e) if (need <= e) return e;
+    EDFA_CHAIN_E(EDFA_E_PICK)
+#undef EDFA_E_PICK
+    return 0;
 }
 
 void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add, double* out2,
                const char* name) {
     Prof pr(c, name, 12.0 * cp.n + 24.0 * cp.n + (out2 ? 16.0 * cp.n : 0.0));
-    k_chain_scan<4><<<ceil_div((int64_t)cp.n_chains * 32, 256), 256, 0, c->stream>>>(
-        cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha, x, add, out2);
+    const unsigned grid = (unsigned)ceil_div((int64_t)cp.n_chains * 32, 256);
+    switch (cp.E) {
+#define EDFA_E_CASE(e)                                                                                     \
+    case e:                                                                                                \
+        k_chain_scan<e><<<grid, 256, 0, c->stream>>>(cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha, x, \
+                                                     add, out2);                                           \
+        break;
+        EDFA_CHAIN_E(EDFA_E_CASE)
+#undef EDFA_E_CASE
+        default: throw Error(EDFA_ERR_CUDA, "chain plan without a segment length");
+    }
     check_launch("k_chain_scan");
 }
 
@@ -415,19 +430,19 @@ void chain_ic0(Ctx* c, const ChainPlan& cp, const Csr& Lpat, const double* aii, 
 
 bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add,
                     double* out2, const char* name) {
-    if (cp.n_chains == 0 || cp.max_len > 32 * 16) return false;
+    if (cp.n_chains == 0 || cp.E == 0) return false;
     Prof pr(c, name, 12.0 * cp.n + 32.0 * cp.n + (out2 ? 16.0 * cp.n : 0.0) + (x ? 8.0 * cp.n : 0.0));
     const unsigned grid = (unsigned)ceil_div((int64_t)cp.n_chains * 32, 256);
-    // rows per lane: chains of up to 32 E rows (256^3 face lines have 257 rows)
-    if (cp.max_len <= 32 * 4)
-        k_chain_pair<4><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha,
-                                                     x, add, out2);
-    else if (cp.max_len <= 32 * 8)
-        k_chain_pair<8><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha,
-                                                     x, add, out2);
-    else
-        k_chain_pair<16><<<grid, 256, 0, c->stream>>>(cp.cptr.p, cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b,
-                                                      alpha, x, add, out2);
+    switch (cp.E) {
+#define EDFA_E_CASE(e)                                                                                     \
+    case e:                                                                                                \
+        k_chain_pair<e><<<grid, 256, 0, c->stream>>>(cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha, x, \
+                                                     add, out2);                                           \
+        break;
+        EDFA_CHAIN_E(EDFA_E_CASE)
+#undef EDFA_E_CASE
+        default: return false;
+    }
     check_launch("k_chain_pair");
     return true;
 }

@@ -244,6 +244,13 @@ int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value) {
     API_END
 }
 
+int edfa_ctx_trim(edfa_ctx* ctx) {
+    API_BEGIN
+    require(ctx, EDFA_ERR_VALUE, "ctx is NULL");
+    ctx->c.trim_cache();
+    API_END
+}
+
 int edfa_ctx_sync(edfa_ctx* ctx) {
     API_BEGIN
     ctx->c.trsv_err_check();   // synchronises; raises a solve that hit its spin limit

@@ -49,10 +49,11 @@ struct ChainPlan {              // disjoint-path DAGs (chain.cu)
     DevBuf<int32_t> rows;       // SELL-32 over chains: row of step k of chain t
     DevBuf<double> coef, dinv;  // dependency coefficient / inverse diagonal per step
     DevBuf<int32_t> heads, succ;
-    DevBuf<int64_t> cptr;       // chain-major layout for the warp-scan solver
-    DevBuf<int32_t> crow;
+    int32_t E = 0;              // segment length per lane of the warp solvers (max_len <= 32 E)
+    DevBuf<int32_t> crow;       // lane-interleaved: chain t, step k at t*32E + (k%E)*32 + k/E
     DevBuf<double> ccoef, cdinv;
 };
+int chain_segment(int max_len);   // smallest instantiated E with 32 E >= max_len (0: too long)
 bool build_chain(Ctx* c, const Csr& deps, const double* diag, bool unit, ChainPlan& cp);
 void chain_values(Ctx* c, const Csr& deps, const double* diag, ChainPlan& cp);
 void run_chain(Ctx* c, const ChainPlan& cp, const double* b, double alpha, double* x, const double* add, double* out2,

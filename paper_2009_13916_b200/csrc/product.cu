@@ -10,6 +10,9 @@
 // columns are distinct, so lanes never collide and every sum is formed in a
 // fixed order (deterministic, bit-reproducible across runs).  Products are
 // not contracted into FMAs, as in the reference's compiled sparsetools.
+#include <mutex>
+#include <set>
+
 #include "dev_util.cuh"
 #include "edfa_internal.cuh"
 #include "objects.cuh"
@@ -209,6 +212,220 @@ __global__ void __launch_bounds__(256) k_product(ProdArgs a) {
     }
 }
 
+// ---- first tier: the same accumulation, operands prefetched.
+// k_product walks G_m entry by entry and W_m entry by entry, and every step
+// started with dependent global loads (row pointer, then the row) -- ~60
+// serialised L2/HBM round trips per row.  Here the warp first loads G_m's
+// entries and the row pointers they need in one round, then every A_ff entry
+// the row will touch (flattened, all loads in flight) into shared memory, and
+// the same for the F~ rows of W_m; the hash accumulation then runs from
+// shared memory in exactly k_product's order (bit-identical results).  Rows
+// that exceed the tier's capacities go to the overflow list (k_product).
+constexpr int PF_BITS = 7, PF_T = 1 << PF_BITS, PF_CAPG = 32, PF_CAPF = 512, PF_CAP = 64;
+constexpr size_t PF_WARP_BYTES = (size_t)PF_T * 12 * 3 + PF_CAPG * (8 + 4 + 4) + (PF_CAPG + 1) * 4 +
+                                 (PF_T + 1) * 4 + (size_t)PF_CAPF * 12;
+
+__device__ __forceinline__ int seg_of(const int* off, int n, int p) {   // last t with off[t] <= p
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (off[mid] <= p) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256) k_product_pf(ProdArgs a) {
+    constexpr int T = PF_T;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warps = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem + (size_t)wid * PF_WARP_BYTES;
+    double* tv = reinterpret_cast<double*>(base);
+    double* wv = tv + T;
+    double* hv = wv + T;
+    double* gv = hv + T;                                 // PF_CAPG
+    double* fval = gv + PF_CAPG;                         // PF_CAPF
+    int* tk = reinterpret_cast<int*>(fval + PF_CAPF);
+    int* wk = tk + T;
+    int* hk = wk + T;
+    int* ga0 = hk + T;                                   // PF_CAPG
+    int* goff = ga0 + PF_CAPG;                           // PF_CAPG + 1
+    int* wo = goff + PF_CAPG + 1;                        // T + 1
+    int* fcol = wo + T + 1;                              // PF_CAPF
+    for (int m = blockIdx.x * warps + wid; m < a.n_rows; m += gridDim.x * warps) {
+        for (int i = lane; i < T; i += 32) { tk[i] = EMPTY; tv[i] = 0.0; hk[i] = EMPTY; hv[i] = 0.0; }
+        const int g0 = a.G.ptr[m], nG = a.G.ptr[m + 1] - g0;
+        bool full = nG > PF_CAPG;
+        // ---- G_m entries and the A_ff row extents they select (one round trip each)
+        int len = 0;
+        if (!full && lane < nG) {
+            const int i = a.G.idx[g0 + lane];
+            gv[lane] = a.G.val[g0 + lane];
+            const int e0 = a.A.ptr[i];
+            ga0[lane] = e0;
+            len = a.A.ptr[i + 1] - e0;
+        }
+        int inc = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const int P = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane < nG) goff[lane] = inc - len;
+        if (lane == 0) goff[min(nG, PF_CAPG)] = P;
+        full = full || P > PF_CAPF;
+        __syncwarp();
+        // ---- every A_ff entry of the row's W, flattened, loads in flight
+        if (!full)
+            for (int p = lane; p < P; p += 32) {
+                const int t = seg_of(goff, nG, p);
+                const int e = ga0[t] + (p - goff[t]);
+                fcol[p] = a.A.idx[e];
+                fval[p] = a.A.val[e];
+            }
+        __syncwarp();
+        // ---- W = g_m A_ff from shared memory, k_product's order
+        int nW = 0;
+        if (!full) {
+            for (int t = 0; t < nG; ++t) {
+                const double g = gv[t];
+                const int e0 = goff[t], e1 = goff[t + 1];
+                for (int eb = e0; eb < e1; eb += 32) {
+                    const int e = eb + lane;
+                    bool fresh = false;
+                    int sl = -1;
+                    if (e < e1) {
+                        sl = h_insert(tk, PF_BITS, fcol[e], &fresh);
+                        if (sl < 0) full = true;
+                        else tv[sl] = add_mul(tv[sl], g, fval[e]);
+                    }
+                    const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+                    const int pos = nW + __popc(bal & ((1u << lane) - 1));
+                    if (fresh && pos < T) wk[pos] = sl;
+                    nW += __popc(bal);
+                }
+                __syncwarp();
+            }
+            full = __any_sync(0xffffffffu, full) || nW > T;
+        }
+        if (!full) {   // reverse first-encounter order (scipy csr_matmat's emission order)
+            for (int q = lane; q < nW; q += 32) hk[q] = wk[q];
+            __syncwarp();
+            for (int q = lane; q < nW; q += 32) {
+                const int sl = hk[nW - 1 - q];
+                wk[q] = tk[sl];
+                wv[q] = tv[sl];
+            }
+            __syncwarp();
+            for (int q = lane; q < nW; q += 32) hk[q] = EMPTY;
+            __syncwarp();
+        }
+        // ---- F~ rows of W's entries: extents, then every entry, flattened
+        int P2 = 0;
+        if (!full) {
+            int run = 0;
+            for (int q0 = 0; q0 < nW; q0 += 32) {
+                const int q = q0 + lane;
+                int l2 = 0;
+                if (q < nW && wv[q] != 0.0) {            // scipy drops exact-zero sums of W
+                    const int k = wk[q];
+                    const int f0 = a.F.ptr[k];
+                    tk[q] = f0;                           // tk is free after the W extraction
+                    l2 = a.F.ptr[k + 1] - f0;
+                }
+                int inc2 = l2;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc2, o);
+                    if (lane >= o) inc2 += v;
+                }
+                if (q < nW) wo[q] = run + inc2 - l2;
+                run += __shfl_sync(0xffffffffu, inc2, 31);
+            }
+            if (lane == 0) wo[nW] = run;
+            P2 = run;
+            full = P2 > PF_CAPF;
+            __syncwarp();
+            if (!full)
+                for (int p = lane; p < P2; p += 32) {
+                    const int q = seg_of(wo, nW, p);
+                    const int e = tk[q] + (p - wo[q]);
+                    fcol[p] = a.F.idx[e];
+                    fval[p] = a.F.val[e];
+                }
+            __syncwarp();
+        }
+        // ---- H = W F from shared memory, k_product's order
+        if (!full) {
+            for (int q = 0; q < nW; ++q) {
+                const double w = wv[q];
+                const int e0 = wo[q], e1 = wo[q + 1];    // empty for zero sums
+                for (int e = e0 + lane; e < e1; e += 32) {
+                    const int sl = h_insert(hk, PF_BITS, fcol[e]);
+                    if (sl < 0) full = true;
+                    else hv[sl] = add_mul(hv[sl], w, fval[e]);
+                }
+                __syncwarp();
+            }
+            full = __any_sync(0xffffffffu, full);
+        }
+        int nH = 0;
+        if (!full) {
+            nH = h_extract_sorted(hk, hv, PF_BITS, tk, tv, lane);   // sorted H row in (tk, tv)
+            if (nH > PF_CAP) full = true;
+        }
+        if (full) {
+            if (lane == 0) {
+                a.cnt[m] = 0;
+                const int p = atomicAdd(a.overflow, 1);
+                a.overflow[1 + p] = m;
+            }
+            __syncwarp();
+            continue;
+        }
+        double thr = 0.0;
+        if (a.tau > 0.0) {
+            double ss = 0.0;
+            for (int i = lane; i < nH; i += 32) ss += tv[i] * tv[i];
+            thr = a.tau * sqrt(warp_sum(ss));
+        }
+        const long long o = (long long)m * PF_CAP;
+        int n = 0;
+        for (int i0 = 0; i0 < nH; i0 += 32) {
+            const int i = i0 + lane;
+            const double v = i < nH ? tv[i] : 0.0;
+            const int col = i < nH ? tk[i] : -1;
+            const bool keep = i < nH && v != 0.0 && (col == m || !(fabs(v) < thr));
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const long long p = o + n + __popc(bal & ((1u << lane) - 1));
+                a.Hi[p] = col;
+                a.Hv[p] = v;
+            }
+            n += __popc(bal);
+        }
+        if (lane == 0) a.cnt[m] = n;
+        __syncwarp();
+    }
+}
+
+void launch_product_pf(Ctx* c, const ProdArgs& a) {
+    constexpr int warps = 8;
+    const size_t sm = PF_WARP_BYTES * warps;
+    static std::mutex mu;
+    static std::set<int> done;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (done.insert(c->device).second)
+            EDFA_CUDA(cudaFuncSetAttribute(k_product_pf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
+    const int per_sm = std::max(1, (int)((227 * 1024) / sm));
+    const int blocks = std::max(1, std::min(ceil_div(a.n_rows, warps), NUM_SMS_B200 * per_sm * 8));
+    k_product_pf<<<blocks, warps * 32, sm, c->stream>>>(a);
+    check_launch("k_product_pf");
+}
+
 template <int BITS, int MODE>
 void launch_product(Ctx* c, const ProdArgs& a) {
     constexpr int T = 1 << BITS;
@@ -282,7 +499,7 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
     a.tau = post_tau;
     a.cnt = cnt.p;
     a.overflow = ovf.p;
-    constexpr int CAP = 128;
+    constexpr int CAP = PF_CAP;
     a.cap = CAP;
     DevBuf<int32_t> pi(c, (size_t)std::max(n, 1) * CAP);
     DevBuf<double> pv(c, (size_t)std::max(n, 1) * CAP);
@@ -290,13 +507,13 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
     a.Hv = pv.p;
     std::vector<int32_t> ovf_rows;
     if (n) {
-        // single pass into the padded buffer (256-slot tables)
+        // single pass into the padded buffer (prefetching tier, 128-slot tables)
         Prof pr(c, "product", 12.0 * (G.nnz + A.nnz + F.nnz) + 12.0 * G.n_rows * 35);
         EDFA_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int), c->stream));
-        launch_product<8, PADDED>(c, a);
+        launch_product_pf(c, a);
         ovf_rows = read_overflow(c, ovf.p);
     }
-    // rows longer than 128 entries: 1024-slot tables into a second padded
+    // rows beyond the first tier: 1024-slot tables into a second padded
     // buffer (by list position); rows beyond that: 4096-slot count + fill
     constexpr int CAP2 = 512;
     DevBuf<int32_t> rows1(c, std::max<size_t>(ovf_rows.size(), 1)), rows2(c, 1);

@@ -15,6 +15,9 @@
 //           dropped, hx/sparse.py:28-34).
 #include <cub/cub.cuh>
 
+#include <mutex>
+#include <set>
+
 #include "dev_util.cuh"
 #include "edfa_internal.cuh"
 #include "objects.cuh"
@@ -316,6 +319,170 @@ __global__ void __launch_bounds__(128) k_setup_rows(RowArgs a) {
     }
 }
 
+// ---- static / base patterns: register-resident Cholesky (s <= 32)
+//
+// L = 8, 16 or 32 lanes per row (32 / L rows per warp).  Lane i of a row's
+// segment owns row i of M = -A_ff[Q,Q] in registers (a[0..SMAX)); the
+// factorisation is right-looking with the column entries l_jk broadcast by
+// segment shuffles, so the only shared-memory traffic is the gather (a
+// scatter of A_ff's rows into a per-row scratch tile) and the columns of L
+// read by the backward substitution.  No __syncwarp per column.
+template <int SMAX>
+struct RegRow {
+    static constexpr int L = SMAX <= 8 ? 8 : (SMAX <= 16 ? 16 : 32);   // lanes per row
+    static constexpr int RPW = 32 / L;                                  // rows per warp
+    static constexpr int LD = SMAX + 1;
+    static constexpr size_t BYTES = sizeof(double) * (SMAX * LD + 2 * SMAX) + sizeof(int) * SMAX;
+};
+
+template <int SMAX>
+__global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
+    using R = RegRow<SMAX>;
+    constexpr int L = R::L, RPW = R::RPW, LD = R::LD;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, seg = lane / L, li = lane % L;
+    const int wid = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    const unsigned segmask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (seg * L));
+    unsigned char* base = smem + (size_t)(wid * RPW + seg) * R::BYTES;
+    double* M = reinterpret_cast<double*>(base);
+    double* bg = M + SMAX * LD;
+    double* bf = bg + SMAX;
+    int* q = reinterpret_cast<int*>(bf + SMAX);
+    const int n_groups = (a.n_rows + RPW - 1) / RPW;
+    for (int grp = blockIdx.x * warps + wid; grp < n_groups; grp += gridDim.x * warps) {
+        const int m = grp * RPW + seg;
+        const bool row_ok = m < a.n_rows;
+        int s = 0, q0 = 0;
+        if (row_ok) {
+            q0 = a.q_ptr[m];
+            s = a.q_ptr[m + 1] - q0;
+        }
+        int s_w = s;                                   // warp-uniform loop bound
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s_w = max(s_w, __shfl_xor_sync(0xffffffffu, s_w, o));
+        // ---- gather: q, the scratch tile, the two right-hand sides
+        if (li < s) q[li] = a.q_idx[q0 + li];
+        for (int t = li; t < s * LD; t += L) M[t] = 0.0;
+        if (li < SMAX) { bg[li] = 0.0; bf[li] = 0.0; }
+        __syncwarp();
+        if (li < s) {
+            const int row = q[li];
+            const int e0 = a.A.ptr[row], e1 = a.A.ptr[row + 1];
+            for (int e = e0; e < e1; ++e) {
+                const int j = bsearch(q, 0, s, a.A.idx[e]);
+                if (j >= 0) M[li * LD + j] = -a.A.val[e];
+            }
+        }
+        if (row_ok) {
+            for (int e = a.Acf.ptr[m] + li; e < a.Acf.ptr[m + 1]; e += L) {
+                const int j = bsearch(q, 0, s, a.Acf.idx[e]);
+                if (j >= 0) bg[j] = a.Acf.val[e];
+            }
+            for (int e = a.AfcT.ptr[m] + li; e < a.AfcT.ptr[m + 1]; e += L) {
+                const int j = bsearch(q, 0, s, a.AfcT.idx[e]);
+                if (j >= 0) bf[j] = a.AfcT.val[e];
+            }
+        }
+        __syncwarp();
+        double r[SMAX];
+#pragma unroll
+        for (int j = 0; j < SMAX; ++j) r[j] = (li < s && j < s) ? M[li * LD + j] : 0.0;
+        double yg = li < s ? bg[li] : 0.0, yf = li < s ? bf[li] : 0.0;
+        // ---- right-looking Cholesky, lane i holds row i (lower part)
+        double inv_self = 0.0;
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < SMAX; ++k) {
+            if (k >= s_w) break;
+            const double dkk = __shfl_sync(0xffffffffu, r[k], seg * L + k);
+            if (k < s && !(dkk > 0.0)) bad = true;
+            const double lkk = sqrt(dkk), ik = 1.0 / lkk;
+            if (li > k) r[k] *= ik;
+            if (li == k) { r[k] = lkk; inv_self = ik; }
+#pragma unroll
+            for (int j = k + 1; j < SMAX; ++j) {
+                if (j >= s_w) break;
+                const double ljk = __shfl_sync(0xffffffffu, r[k], seg * L + j);
+                if (li >= j) r[j] = fma(-r[k], ljk, r[j]);
+            }
+        }
+        bad = bad && row_ok;
+        if (__any_sync(0xffffffffu, bad)) {
+            if (bad && li == 0) report(a.err, ERR_FACT, m);
+            continue;                                  // the build raises; values are not used
+        }
+        // ---- forward substitution L y = b (both right-hand sides)
+#pragma unroll
+        for (int k = 0; k < SMAX; ++k) {
+            if (k >= s_w) break;
+            if (li == k) { yg *= inv_self; yf *= inv_self; }
+            const double vg = __shfl_sync(0xffffffffu, yg, seg * L + k);
+            const double vf = __shfl_sync(0xffffffffu, yf, seg * L + k);
+            if (li > k) { yg = fma(-r[k], vg, yg); yf = fma(-r[k], vf, yf); }
+        }
+        // ---- backward substitution L^T x = y: columns of L from the scratch tile
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < SMAX; ++j)
+            if (li < s && j < li) M[li * LD + j] = r[j];
+        __syncwarp();
+        for (int k = s_w - 1; k >= 0; --k) {
+            if (li == k) { yg *= inv_self; yf *= inv_self; }
+            const double vg = __shfl_sync(0xffffffffu, yg, seg * L + k);
+            const double vf = __shfl_sync(0xffffffffu, yf, seg * L + k);
+            if (li < k && k < s) {
+                const double l = M[k * LD + li];
+                yg = fma(-l, vg, yg);
+                yf = fma(-l, vf, yf);
+            }
+        }
+        // ---- pre-filter (hx/precond.py:160-165), slot-layout output, nonzero counts
+        if (a.pre_tau > 0.0) {
+            double sg = li < s ? yg * yg : 0.0, sf = li < s ? yf * yf : 0.0;
+#pragma unroll
+            for (int o = L / 2; o > 0; o >>= 1) {
+                sg += __shfl_xor_sync(0xffffffffu, sg, o);
+                sf += __shfl_xor_sync(0xffffffffu, sf, o);
+            }
+            const double tg = a.pre_tau * sqrt(sg), tf = a.pre_tau * sqrt(sf);
+            if (fabs(yg) < tg) yg = 0.0;
+            if (fabs(yf) < tf) yf = 0.0;
+        }
+        const bool live = row_ok && li < s;
+        if (live) {
+            const int o = a.slot_ptr[m];
+            a.out_g[o + li] = yg;
+            a.out_f[o + li] = yf;
+        }
+        const unsigned bgm = __ballot_sync(0xffffffffu, live && yg != 0.0) & segmask;
+        const unsigned bfm = __ballot_sync(0xffffffffu, live && yf != 0.0) & segmask;
+        if (row_ok && li == 0) {
+            a.out_gcnt[m] = __popc(bgm);
+            a.out_fcnt[m] = __popc(bfm);
+        }
+        __syncwarp();
+    }
+}
+
+template <int SMAX>
+void launch_rows_reg(Ctx* c, const RowArgs& a) {
+    using R = RegRow<SMAX>;
+    constexpr int warps = 4;
+    const size_t sm = R::BYTES * R::RPW * warps;
+    auto kern = k_setup_rows_reg<SMAX>;
+    static std::mutex mu;
+    static std::set<int> done;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (done.insert(c->device).second)
+            EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    }
+    const int groups = ceil_div(a.n_rows, R::RPW);
+    const int blocks = std::max(1, std::min(ceil_div(groups, warps), NUM_SMS_B200 * 64));
+    kern<<<blocks, warps * 32, sm, c->stream>>>(a);
+    check_launch("k_setup_rows_reg");
+}
+
 // compaction of slot-layout values into canonical CSR rows (zeros dropped)
 __global__ void k_compact(int32_t n_rows, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ qsize,
                           const int32_t* __restrict__ qidx, const double* __restrict__ v,
@@ -475,8 +642,10 @@ void setup_rows(Ctx* c, const SetupInput& in, SetupOutput& out) {
     {
         Prof pr(c, dyn ? "setup_rows_dynamic" : "setup_rows_static", bytes);
         if (!dyn) {
-            if (smax_need <= 16) launch_rows<16, 0, false>(c, a);
-            else if (smax_need <= 32) launch_rows<32, 0, false>(c, a);
+            if (smax_need <= 8) launch_rows_reg<8>(c, a);
+            else if (smax_need <= 16) launch_rows_reg<16>(c, a);
+            else if (smax_need <= 24) launch_rows_reg<24>(c, a);
+            else if (smax_need <= 32) launch_rows_reg<32>(c, a);
             else if (smax_need <= 64) launch_rows<64, 0, false>(c, a);
             else launch_rows<128, 0, false>(c, a);
         } else {

@@ -791,15 +791,23 @@ template <int EK>
 static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
     // attribute + occupancy once per (device, smem): driver calls kept off the
     // per-solve path
+    // the dynamic shared-memory attribute only ever grows (a smaller value set
+    // for one plan must not invalidate the grid sized for another)
     static std::mutex mu;
     static std::map<std::pair<int, size_t>, int> grids;
+    static std::map<int, size_t> smem_set;   // per device
     int grid;
     {
         std::lock_guard<std::mutex> lk(mu);
         const auto key = std::make_pair(c->device, smem);
         auto it = grids.find(key);
         if (it == grids.end()) {
-            EDFA_CUDA(cudaFuncSetAttribute(k_tile_flow<EK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            size_t& cur = smem_set[c->device];
+            if (smem > cur) {
+                EDFA_CUDA(cudaFuncSetAttribute(k_tile_flow<EK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem));
+                cur = smem;
+            }
             int occ = 0;
             EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_flow<EK>, FLOW_THREADS, smem));
             it = grids.emplace(key, NUM_SMS_B200 * std::max(1, std::min(occ, 2))).first;

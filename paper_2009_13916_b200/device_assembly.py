@@ -77,6 +77,29 @@ class DeviceBlockSystem:
     def rhs(self) -> torch.Tensor:
         return self.system.rhs()
 
+    @property
+    def topology_inputs(self):
+        """(elem_to_faces, face_to_elems, face_index) on the device: what a
+        DeviceSystem derives the grid topology from (edfa_grid_topology)."""
+        return self.dev["e2f"], self.dev["f2e"], self.face_index
+
+    def to_host(self):
+        """The same step as a host ``BlockSystem`` (scipy CSR blocks, numpy
+        vectors; element operators not copied) -- what a host application
+        holds and hands to the drop-in API."""
+        from . import assembly
+        n_free = self.n_free_faces
+        fidx = self.face_index.cpu().numpy().astype(np.int64)
+        free = np.flatnonzero(fidx >= 0)
+        assert free.size == n_free
+        return assembly.BlockSystem(
+            A_ff=self.A_ff.to_scipy(), A_fc=self.A_fc.to_scipy(), A_cf=self.A_cf.to_scipy(),
+            A_cc=self.A_cc.to_scipy(), rhs_f=self.rhs_f.cpu().numpy(), rhs_c=self.rhs_c.cpu().numpy(),
+            dt=self.dt, free_faces=free, face_index=fidx, dirichlet_faces=self.dirichlet_faces,
+            dirichlet_values=self.dirichlet_values, A_cc_steady=self.A_cc_steady.to_scipy(),
+            accumulation=self.accumulation.cpu().numpy(), rhs_c_base=self.rhs_c_base.cpu().numpy(),
+            ops=None, grid=self.grid)
+
 
 def _dev(a, dtype) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
