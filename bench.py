@@ -604,12 +604,33 @@ def assembly_leg(case, c, lib, N):
 
 
 # ---------------------------------------------------------------- slab-partitioned arm (N > 1)
-def run_slabs(args):
-    """Weak scaling over z-slabs (BASELINE config 5 method):
-    the global grid is n x n x (n * slabs), one n^3 slab per GPU, block-Jacobi
-    inner factors per slab, halo exchange + allreduce over NCCL."""
-    import ctypes
+def slab_layouts_local(cfg, n, nz, parts, mine, halo):
+    """Every slab this process holds, built from its own sub-box only
+    (configs.slab_case assembled on the device, parallel.build_slab_layout):
+    no process ever holds the global system (host memory O(slab))."""
+    import torch
 
+    from paper_2009_13916_b200 import configs, parallel
+    from paper_2009_13916_b200 import device_assembly as DA
+    lays = []
+    for r in mine:
+        k0, k1 = parallel.slab_bounds(nz, parts)[r]
+        s0, s1 = max(0, k0 - halo - 1), min(nz, k1 + halo + 1)
+        case = configs.slab_case(cfg, n, s0, s1, nz=nz, host=False)
+        dsys = DA.assemble_device(*case.meta["inputs"], element_ops=False)
+        sub = dsys.to_host()
+        del dsys
+        torch.cuda.synchronize()
+        lays.append(parallel.build_slab_layout(sub, s0, nz, parts, r, halo))
+    return lays
+
+
+def run_slabs(args):
+    """z-slab partitioned solve: one slab per GPU (or
+    ``--slabs P`` slabs in one process), block-Jacobi inner factors per slab,
+    halo exchanges over NCCL P2P, one all-reduce per Arnoldi step.
+    --scaling strong: BASELINE config 5's 256^3 grid cut into N slabs;
+    --scaling weak: n^3 per GPU (default 128^3) stacked along z."""
     import numpy as np
     import torch
 
@@ -621,21 +642,31 @@ def run_slabs(args):
         dist.init_process_group("nccl", device_id=dev)
     per_proc = max(args.slabs, 1)
     parts = world * per_proc
-    from paper_2009_13916_b200 import _lib, configs, parallel
+    from paper_2009_13916_b200 import _lib, parallel
     from paper_2009_13916_b200.device import ctx
     lib = _lib.lib()
-    diag = []
-    args.n = args.n or 64
-    case = configs.config2(n=args.n, nz=args.n * parts)
-    s = case.system
-    N = s.n_unknowns
+    cfg = args.config if args.config in (1, 2, 5) else 5
+    if args.scaling == "weak":
+        n = args.n or 128
+        nz = n * parts
+    else:
+        n = args.n or DEFAULT_N[cfg]
+        nz = n
+    rtol, restart, max_it = 1e-8, 50, 2000
     mine = [rank * per_proc + k for k in range(per_proc)]
-    halo = parallel.halo_layers("static", "A")
-    lays = parallel.build_layouts(s, parts, halo=halo, ranks=mine)
+    halo = parallel.halo_layers("static" if cfg != 1 else "base", "A")
+    t0 = time.perf_counter()
+    my_lays = slab_layouts_local(cfg, n, nz, parts, mine, halo)
+    t_layout = time.perf_counter() - t0
+    # global N from the per-slab owned counts
+    n_own = torch.tensor([float(sum(l.n_own for l in my_lays))], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(n_own)
+    N = int(n_own.item())
     comm = (parallel.TorchComm([q // per_proc for q in range(parts)]) if world > 1
             else parallel.LocalComm(parts))
-    my_lays = [lays[q] for q in mine]
-    solver = parallel.SlabSolver(my_lays, comm, kind="static", prototype="A")
+    kind = "base" if cfg == 1 else "static"
+    solver = parallel.SlabSolver(my_lays, comm, kind=kind, prototype="A")
     if world > 1:
         t = torch.zeros(1, device=dev)
         torch.distributed.all_reduce(t)                # communicator up before the first P2P
@@ -643,13 +674,7 @@ def run_slabs(args):
 
     def step():
         solver.build()
-        return solver.solve(tol=case.rtol, restart=case.restart, max_it=case.max_it)
-
-    def report(c, reset=1):
-        n = lib.edfa_ctx_profile_report(c, None, 0, 0)
-        buf = ctypes.create_string_buffer(int(n))
-        lib.edfa_ctx_profile_report(c, buf, n, reset)
-        return json.loads(buf.value.decode())
+        return solver.solve(tol=rtol, restart=restart, max_it=max_it)
 
     c = ctx()
     prof_full = {}
@@ -658,18 +683,20 @@ def run_slabs(args):
         if last:
             lib.edfa_ctx_profile_filter(c, b"")
             lib.edfa_ctx_profile(c, 1)
-            report(c)
+            profile_report(lib, c)
         xs, rep = step()
         if last:
-            prof_full = report(c)
+            prof_full = profile_report(lib, c)
             lib.edfa_ctx_profile(c, 0)
     torch.cuda.synchronize()
     dom_name = max(prof_full.items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
     lib.edfa_ctx_profile_filter(c, dom_name.encode())
     lib.edfa_ctx_profile(c, 1)
-    report(c)
+    profile_report(lib, c)
     launches0 = lib.edfa_ctx_launch_count(c)
     times, reps = [], []
+    solver.op.timer.enabled = True
+    solver.op.timer.collect()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1.0)
@@ -683,32 +710,20 @@ def run_slabs(args):
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             reps.append(rep)
-            if diag:
-                print("diag step", len(times), times[-1], diag, file=sys.stderr, flush=True)
-                diag.clear()
+    comm_ms = solver.op.timer.collect()
+    solver.op.timer.enabled = False
     launches = lib.edfa_ctx_launch_count(c) - launches0
-    prof = report(c)
+    prof = profile_report(lib, c)
     lib.edfa_ctx_profile(c, 0)
     lib.edfa_ctx_profile_filter(c, b"")
     clocks = clk.summary()
     t_total_ms = sum(times)
+    comm_share = (comm_ms["halo"] + comm_ms["allreduce"]) / max(t_total_ms, 1e-9)
     if world > 1:
-        tt = torch.tensor([t_total_ms], device=dev, dtype=torch.float64)
+        tt = torch.tensor([t_total_ms, comm_share], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_total_ms = float(tt.item())
+        t_total_ms, comm_share = float(tt[0].item()), float(tt[1].item())
     value = N * args.steps / (t_total_ms / 1e3) / 1e6
-    # true residual of the assembled global solution on the host (rank 0 gathers)
-    x_loc = [x.cpu().numpy() for x in xs]
-    relres_host = None
-    if world > 1:
-        gathered = [None] * world
-        torch.distributed.all_gather_object(gathered, x_loc)
-        x_all = [v for g in gathered for v in g]
-    else:
-        x_all = x_loc
-    if rank == 0:
-        x = parallel.scatter_solution(lays, x_all, s.n_free_faces, s.n_cells)
-        relres_host = float(np.linalg.norm(s.rhs() - s.full_matrix() @ x) / np.linalg.norm(s.rhs()))
 
     # ---- end to end from host blocks: H2D of the slab's local blocks, build, solve, D2H of x
     e2e_times = []
@@ -719,14 +734,15 @@ def run_slabs(args):
         h2d += sum(m.data.nbytes + m.indices.nbytes + m.indptr.nbytes for m in mats) + b["rhs"].nbytes
         h2d += sum(a.nbytes for a in b["ext_topology"])
     d2h = sum(l.n_own for l in my_lays) * 8
-    for _ in range(max(1, min(args.steps, 3))):
+    del solver
+    for _ in range(max(1, min(args.steps, 2))):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
         t0 = time.perf_counter()
-        sv = parallel.SlabSolver(my_lays, comm, kind="static", prototype="A")
+        sv = parallel.SlabSolver(my_lays, comm, kind=kind, prototype="A")
         sv.build()
-        xs_h, _ = sv.solve(tol=case.rtol, restart=case.restart, max_it=case.max_it)
+        xs_h, _ = sv.solve(tol=rtol, restart=restart, max_it=max_it)
         _ = [x.cpu().numpy() for x in xs_h]
         dt = time.perf_counter() - t0
         if world > 1:
@@ -737,36 +753,37 @@ def run_slabs(args):
         del sv
     e2e_val = N / statistics.median(e2e_times) / 1e6
 
-    peaks = {}
-    try:
-        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
-    except Exception:
-        pass
-    peak = peaks.get("hbm_gbs") or 6650.0
+    peak, peak_src = peak_hbm()
     dname, d = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", {"ms": 0, "bytes": 0,
-                                                                                    "launches": 1})
+                                                                                  "launches": 1})
     per_launch_ms = d["ms"] / max(d["launches"], 1)
     per_launch_bytes = d["bytes"] / max(d["launches"], 1)
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
     tot_full = max(sum(p["ms"] for p in prof_full.values()), 1e-9)
     shares = {k: round(v["ms"] / tot_full, 4) for k, v in sorted(prof_full.items(), key=lambda kv: -kv[1]["ms"])[:8]}
+    scaling = "weak" if args.scaling == "weak" else "strong"
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic (seeded config-2 generator stacked along z: {args.n}x{args.n}x{args.n * parts})",
-        "config": {"workload": f"config2-{args.n}^3-per-slab-z{parts}-staticA-IC0ILU0-gmres50",
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded config-{cfg} generator, {n}x{n}x{nz}); every rank assembles only its own "
+                f"extended slab on the device",
+        "config": {"workload": f"config{cfg}-{n}x{n}x{nz}-zslab{parts}-staticA-IC0ILU0-gmres50",
                    "n_dof": N, "slabs": parts, "slabs_per_gpu": per_proc, "halo_layers": halo,
                    "gmres_iterations": reps[-1].n_it, "final_true_relres": reps[-1].final_relres,
-                   "host_check_relres": relres_host, "parallelism": f"zslab{parts}",
+                   "parallelism": f"zslab{parts}", "layout_build_s": t_layout,
                    "inner_factors": "block-Jacobi per slab (IC(0) of -A_ff, ILU(0) of S~)",
                    "l2": "inputs larger than L2 and a 256 MiB L2 flush between steps"},
+        "comm": {"halo_ms_per_step": comm_ms["halo"] / args.steps,
+                 "allreduce_ms_per_step": comm_ms["allreduce"] / args.steps,
+                 "share_of_step": comm_share,
+                 "calls_per_step": (comm_ms["halo_calls"] + comm_ms["allreduce_calls"]) / args.steps,
+                 "note": "CUDA events around the NCCL halo exchanges and all-reduces (max over ranks)"},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "seconds_per_step": statistics.median(e2e_times)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs, burst)",
+                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "step_share_of_kernel_time": shares},
         "clocks": clocks,

@@ -168,6 +168,38 @@ def config5(n=256, seed=SEEDS[5]):
     return c
 
 
+def slab_case(idx: int, n: int, s0: int, s1: int, nz: int | None = None, host: bool = True) -> CaseSpec:
+    """The cell layers [s0, s1) of config ``idx``'s n x n x nz grid (default
+    nz = n) as a case of their own: same spacing, node coordinates, field
+    values (the global seeded draws, sliced) and boundary conditions (x
+    planes), so every row whose cells lie inside the slab equals the full
+    system's row.  Used by the multi-GPU partition: a rank assembles only its
+    extended slab.  Configs 1, 2 and 5 (regular boxes, x-plane Dirichlet)."""
+    nz = nz or n
+    if idx not in (1, 2, 5):
+        raise ValueError("slab_case covers the box configs 1, 2 and 5")
+    if not 0 <= s0 < s1 <= nz:
+        raise ValueError("slab layers out of range")
+    nxy = n * n
+    if idx == 1:
+        h = 1.0 / n
+        g = mesh.box_grid(n, n, s1 - s0, h, h, h, z0_layer=s0)
+        fld = mesh.Conductivity.homogeneous(g.n_elems, 1.0)
+        precond = dict(pattern="base", **_inner())
+    else:
+        h = 1000.0 / n
+        g = mesh.box_grid(n, n, s1 - s0, h, h, h, z0_layer=s0)
+        rng = np.random.default_rng(SEEDS[idx])
+        k = np.exp(rng.normal(0.0, 2.0, size=nxy * nz))[s0 * nxy:s1 * nxy]
+        fld = mesh.Conductivity.diagonal(k, k, 0.1 * k)
+        precond = dict(pattern="static", prototype="A", **_inner())
+    bc = mesh.Boundaries(pressure_planes={"x-": 1.0, "x+": 0.0})
+    inputs = (g, fld, mesh.RockProps(gamma=1.0), bc, 1.0, np.zeros(g.n_elems))
+    s, meta = _assemble(*inputs) if host else (None, dict(inputs=inputs, host_assembly_s=None))
+    meta.update(slab=(s0, s1), nz_global=nz)
+    return CaseSpec(f"config{idx}-{n}x{n}x{nz}-layers{s0}-{s1}", s, precond, meta=meta)
+
+
 def make(idx: int, **kw) -> CaseSpec:
     return {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}[idx](**kw)
 

@@ -195,6 +195,7 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
     h->c.opt.fill_fusion = env_opt("EDFA_OPT_FILL_FUSION", 1);
     h->c.opt.trsv_levels = env_opt("EDFA_OPT_TRSV_LEVELS", 0);
     h->c.opt.ilu_levels = env_opt("EDFA_OPT_ILU_LEVELS", 0);
+    h->c.opt.tile_direct = env_opt("EDFA_OPT_TILE_DIRECT", -1);
     h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
     EDFA_CUDA(cudaMemsetAsync(h->c.d_scalar_i, 0, 64 * sizeof(int), h->c.stream));   // [60]: reduction ticket
     h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));
@@ -227,6 +228,7 @@ int edfa_ctx_set_option(edfa_ctx* ctx, const char* name, int value) {
     else if (n == "fill_fusion") o.fill_fusion = value;
     else if (n == "trsv_levels") o.trsv_levels = value;
     else if (n == "ilu_levels") o.ilu_levels = value;
+    else if (n == "tile_direct") o.tile_direct = value;
     else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
     API_END
 }
@@ -240,6 +242,7 @@ int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value) {
     else if (n == "fill_fusion") *value = o.fill_fusion;
     else if (n == "trsv_levels") *value = o.trsv_levels;
     else if (n == "ilu_levels") *value = o.ilu_levels;
+    else if (n == "tile_direct") *value = o.tile_direct;
     else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
     API_END
 }

@@ -68,6 +68,7 @@ struct CtxOptions {
     int fill_fusion = 1;    // the two ILU tile solves pre-fill each other's SENTINELs
     int trsv_levels = 0;    // level-synchronous triangular solves instead of the sync-free ones
     int ilu_levels = 0;     // level-synchronous ILU(0) factorisation instead of the sync-free one
+    int tile_direct = -1;   // ILU tile solves: -1 by wavefront width, 0 staged plan (15 warps), 1 direct (7 warps)
 };
 
 struct Ctx {

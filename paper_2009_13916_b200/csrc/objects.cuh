@@ -86,10 +86,8 @@ void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, co
 // x_prefilled: x already holds SENTINEL; consume_b: b's rows are reset to
 // SENTINEL once read; pre_sent: a vector set to SENTINEL row by row (the next
 // solve's output) -- lets consecutive solves skip their fill kernels
-// fz (optional): the right-hand side becomes b - fz x (a fused SpMV; rows of fz = rows of the factor)
 void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
-                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent, const Csr* fz = nullptr,
-                 const double* fz_x = nullptr);
+                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent);
 
 struct TriPlan {
     bool is_chain = false;

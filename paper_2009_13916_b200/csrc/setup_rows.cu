@@ -365,12 +365,22 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
         for (int t = li; t < s * LD; t += L) M[t] = 0.0;
         if (li < SMAX) { bg[li] = 0.0; bf[li] = 0.0; }
         __syncwarp();
-        if (li < s) {
+        if (li < s) {   // the row's entries are loaded in batches of 12 (all in flight), then placed
             const int row = q[li];
             const int e0 = a.A.ptr[row], e1 = a.A.ptr[row + 1];
-            for (int e = e0; e < e1; ++e) {
-                const int j = bsearch(q, 0, s, a.A.idx[e]);
-                if (j >= 0) M[li * LD + j] = -a.A.val[e];
+            for (int eb = e0; eb < e1; eb += 12) {
+                int ci[12];
+                double cv[12];
+#pragma unroll
+                for (int u = 0; u < 12; ++u) {
+                    ci[u] = eb + u < e1 ? a.A.idx[eb + u] : -1;
+                    cv[u] = eb + u < e1 ? a.A.val[eb + u] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 12; ++u) {
+                    const int j = ci[u] >= 0 ? bsearch(q, 0, s, ci[u]) : -1;
+                    if (j >= 0) M[li * LD + j] = -cv[u];
+                }
             }
         }
         if (row_ok) {

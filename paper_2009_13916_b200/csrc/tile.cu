@@ -380,10 +380,6 @@ struct TileSolve {
     int* err;
     const short* xlev_ptr;
     double* b_sent;       // == b, whose tile rows are reset to SENTINEL once read (or NULL)
-    const int32_t* fz_ptr;   // fused right-hand side b - M x (CSR rows = this factor's rows) or NULL
-    const int32_t* fz_idx;
-    const double* fz_val;
-    const double* fz_x;
     double* pre_sent;     // another vector whose tile rows are set to SENTINEL (or NULL)
 };
 
@@ -419,25 +415,38 @@ __device__ __forceinline__ void st_vol_s(double* p, double v) { *reinterpret_cas
 constexpr int FLOW_LW = 8;          // loader: externals in flight per lane per polling round (8: 1 % faster than 16)
 constexpr int FLOW_LSLEEP = 20;     // loader back-off (ns) when nothing new arrived
 constexpr int FLOW_LAHEAD = 64;     // loader window: need-levels polled past the first missing external
-constexpr int FLOW_WARPS = 15;      // compute warps (+1 loader) = 512 threads at 128 registers (12 -> 15: 141 -> 134 us)
-constexpr int FLOW_THREADS = (FLOW_WARPS + 1) * 32;
+// Two shapes of the kernel:
+//  * narrow wavefronts (few tiles per level, e.g. 64^3): W = 15 compute warps
+//    + the loader (512 threads at 128 registers, one CTA per SM) with the whole
+//    plan staged in shared memory -- the latency of the level chain dominates
+//    (12 -> 15 warps: 141 -> 134 us per solve at 64^3);
+//  * wide wavefronts (thousands of ready tiles, e.g. 256^3): W = 7 (256
+//    threads) and DIRECT early records -- read from global memory (L2-warmed
+//    by a bulk prefetch when the tile starts) instead of staged, so the CTA
+//    needs ~60 KB of shared memory and two tiles are in flight per SM: the
+//    solve is bound by tile throughput, not by the critical path.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ bool is_sent_hi(double v) {   // published values are never NaN-boxed like this
     return __double2hiint(v) == (int)(SENTINEL_BITS >> 32);
 }
 
-template <int EK>
-__global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
+template <int EK, int W, bool DIRECT>
+__global__ void __launch_bounds__((W + 1) * 32, DIRECT ? 2 : 1) k_tile_flow(TileSolve a) {
+    constexpr int FLOW_THREADS = (W + 1) * 32;
+    constexpr int SEK = DIRECT ? 0 : EK;                            // early records staged in smem
     extern __shared__ __align__(128) unsigned char sm[];
     double* xs = reinterpret_cast<double*>(sm);                     // RC + EC + 2
     double* bsm = xs + a.RC + a.EC + 2;                             // RC (right-hand side)
     double* cc = bsm + a.RC;                                        // RC*CK
-    double* ecf = cc + (size_t)a.RC * CK;                           // RC*EK
-    double* di = ecf + (size_t)a.RC * EK;                           // RC
+    double* ecf = cc + (size_t)a.RC * CK;                           // RC*SEK
+    double* di = ecf + (size_t)a.RC * SEK;                          // RC
     int* rid = reinterpret_cast<int*>(di + a.RC);                   // RC
     int* eid_s = rid + a.RC;                                        // EC (external row ids, need-sorted)
     short* cs = reinterpret_cast<short*>(eid_s + a.EC);             // RC*CK
-    short* es = cs + (size_t)a.RC * CK;                             // RC*EK
-    short* lp = es + (size_t)a.RC * EK;                             // LC
+    short* es = cs + (size_t)a.RC * CK;                             // RC*SEK
+    short* lp = es + (size_t)a.RC * SEK;                            // LC
     short* xl = lp + a.LC;                                          // LC: externals needed below level l
     __shared__ int s_tile, s_hdr[4];
     __shared__ __align__(8) uint64_t mbar;
@@ -458,8 +467,13 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                 const int4 h = *reinterpret_cast<const int4*>(a.hdr + (size_t)t * 4);
                 s_hdr[0] = h.x; s_hdr[1] = h.y; s_hdr[2] = h.z;
                 const unsigned n = h.x;
-                unsigned b_cs = r16(2u * n * CK), b_cc = r16(8u * n * CK), b_es = r16(2u * n * EK),
-                         b_ec = r16(8u * n * EK), b_di = r16(8u * n), b_ri = r16(4u * n), b_lp = r16(2u * (h.z + 1));
+                unsigned b_cs = r16(2u * n * CK), b_cc = r16(8u * n * CK), b_es = DIRECT ? 0u : r16(2u * n * EK),
+                         b_ec = DIRECT ? 0u : r16(8u * n * EK), b_di = r16(8u * n), b_ri = r16(4u * n),
+                         b_lp = r16(2u * (h.z + 1));
+                if (DIRECT) {   // the early records are read per group: warm L2 with them now
+                    bulk_prefetch_l2(a.es + (size_t)t * a.RC * EK, r16(2u * n * EK));
+                    bulk_prefetch_l2(a.ec + (size_t)t * a.RC * EK, r16(8u * n * EK));
+                }
                 unsigned b_ei = r16(4u * h.y), b_xl = r16(2u * (h.z + 1));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
@@ -469,8 +483,10 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                 bulk_g2s(eid_s, a.ext_id + (size_t)t * a.EC, b_ei, &mbar);
                 bulk_g2s(cs, a.cs + (size_t)t * a.RC * CK, b_cs, &mbar);
                 bulk_g2s(cc, a.cc + (size_t)t * a.RC * CK, b_cc, &mbar);
-                bulk_g2s(es, a.es + (size_t)t * a.RC * EK, b_es, &mbar);
-                bulk_g2s(ecf, a.ec + (size_t)t * a.RC * EK, b_ec, &mbar);
+                if (!DIRECT) {
+                    bulk_g2s(es, a.es + (size_t)t * a.RC * EK, b_es, &mbar);
+                    bulk_g2s(ecf, a.ec + (size_t)t * a.RC * EK, b_ec, &mbar);
+                }
                 bulk_g2s(di, a.dinv + (size_t)t * a.RC, b_di, &mbar);
                 bulk_g2s(rid, a.row_id + (size_t)t * a.RC, b_ri, &mbar);
                 bulk_g2s(lp, a.lev_ptr + (size_t)t * a.LC, b_lp, &mbar);
@@ -495,19 +511,6 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
                 int p = p0 + u * FLOW_THREADS + threadIdx.x;
                 v[u] = p < n ? __ldg(a.b + rid[p]) : 0.0;
             }
-            if (a.fz_ptr) {   // fused SpMV: b_row - M_row . x (same FMA order as k_spmv_sell)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    int p = p0 + u * FLOW_THREADS + threadIdx.x;
-                    if (p < n) {
-                        const int row = rid[p];
-                        double acc = 0.0;
-                        for (int e = a.fz_ptr[row]; e < a.fz_ptr[row + 1]; ++e)
-                            acc = fma(a.fz_val[e], __ldg(a.fz_x + a.fz_idx[e]), acc);
-                        v[u] = fma(1.0, v[u], -acc);
-                    }
-                }
-            }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 int p = p0 + u * FLOW_THREADS + threadIdx.x;
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
         }
         if (threadIdx.x < 2) xs[a.RC + a.EC + threadIdx.x] = 0.0;   // ZSLOT (+pad)
         __syncthreads();
-        if (warp == FLOW_WARPS) {
+        if (warp == W) {
             // externals in need order; q0 = first entry not yet present
             constexpr int LW = FLOW_LW;
             // the polling window stops FLOW_LAHEAD need-levels past the first
@@ -568,18 +571,20 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
             for (int lv = 0; lv < nlev; ++lv) {
                 const int l0 = lp[lv], R = lp[lv + 1] - l0;
                 for (int r0 = 0; r0 < R; r0 += 16, ++g) {
-                    if (g % FLOW_WARPS != warp) continue;
+                    if (g % W != warp) continue;
                     const int r = r0 + (lane >> 1);
                     const bool act = r < R;
                     const int p = l0 + (act ? r : 0);
                     const short zs = (short)(a.RC + a.EC);
                     short es_[KH], cs_[CK];
                     double ec_[KH], cc_[CK];
+                    const short* esb = DIRECT ? a.es + (size_t)t * a.RC * EK : es;
+                    const double* ecb = DIRECT ? a.ec + (size_t)t * a.RC * EK : ecf;
 #pragma unroll
                     for (int u = 0; u < KH; ++u) {
                         const int k = 2 * u + li;
-                        es_[u] = act ? es[(size_t)l0 * EK + k * R + r] : zs;
-                        ec_[u] = act ? ecf[(size_t)l0 * EK + k * R + r] : 0.0;
+                        es_[u] = act ? esb[(size_t)l0 * EK + k * R + r] : zs;
+                        ec_[u] = act ? ecb[(size_t)l0 * EK + k * R + r] : 0.0;
                     }
 #pragma unroll
                     for (int k = 0; k < CK; ++k) {
@@ -661,16 +666,18 @@ __global__ void __launch_bounds__(FLOW_THREADS) k_tile_flow(TileSolve a) {
 
 }  // namespace
 
-// smem: xs[RC+EC+2] cc[RC*CK] ec[RC*EK] di[RC] rid[RC] cs[RC*CK] es[RC*EK] lp[LC]
-size_t tile_smem_bytes(const TilePlan& tp) {
-    size_t rc = tp.RC, ek = tp.KD, ec = tp.EC, lc = tp.LC;
-    size_t bytes = 8 * (rc + ec + 2) + 8 * rc * CK + 8 * rc * ek + 8 * rc + 4 * rc + 4 * ec + 2 * rc * CK +
-                   2 * rc * ek + 2 * lc + 2 * lc;
+// smem: xs[RC+EC+2] b[RC] cc[RC*CK] ec[RC*EK] di[RC] rid[RC] eid[EC] cs[RC*CK] es[RC*EK] lp[LC] xl[LC]
+// (ec / es absent with direct early records)
+size_t tile_flow_smem_bytes(const TilePlan& tp, bool direct) {
+    size_t rc = tp.RC, ek = direct ? 0 : tp.KD, ec = tp.EC, lc = tp.LC;
+    size_t bytes = 8 * (rc + ec + 2) + 8 * rc + 8 * rc * CK + 8 * rc * ek + 8 * rc + 4 * rc + 4 * ec +
+                   2 * rc * CK + 2 * rc * ek + 2 * lc + 2 * lc;
     return (bytes + 127) & ~size_t(127);
 }
 
-size_t tile_flow_smem_bytes(const TilePlan& tp) {
-    return (tile_smem_bytes(tp) + 8 * (size_t)tp.RC + 127) & ~size_t(127);
+// wide wavefronts: enough tiles per tile level to keep two CTAs per SM busy
+static bool tile_direct(const TilePlan& tp) {
+    return tp.n_tile_levels > 0 && tp.n_tiles / tp.n_tile_levels >= 2 * NUM_SMS_B200 / 8 && tp.n_tiles >= 4096;
 }
 
 bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool reverse, const int* dims,
@@ -735,8 +742,7 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
             if (me <= w) { tp.KD = w; break; }
         if (!tp.KD) return false;
     }
-    size_t smem = tile_flow_smem_bytes(tp);
-    if (smem > 220 * 1024) return false;
+    if (tile_flow_smem_bytes(tp, false) > 220 * 1024) return false;
     tp.hdr.reset(c, (size_t)nt * 4);
     tp.lev_ptr.reset(c, (size_t)nt * tp.LC);
     tp.row_id.reset(c, (size_t)nt * tp.RC);
@@ -787,10 +793,11 @@ bool build_tile_plan(Ctx* c, const Csr& D, const double* diag, bool unit, bool r
     return true;
 }
 
-template <int EK>
-static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
-    // attribute + occupancy once per (device, smem): driver calls kept off the
-    // per-solve path
+template <int EK, int W, bool DIRECT>
+static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a) {
+    const size_t smem = tile_flow_smem_bytes(tp, DIRECT);
+    auto kern = k_tile_flow<EK, W, DIRECT>;
+    constexpr int threads = (W + 1) * 32;
     // the dynamic shared-memory attribute only ever grows (a smaller value set
     // for one plan must not invalidate the grid sized for another)
     static std::mutex mu;
@@ -804,12 +811,11 @@ static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
         if (it == grids.end()) {
             size_t& cur = smem_set[c->device];
             if (smem > cur) {
-                EDFA_CUDA(cudaFuncSetAttribute(k_tile_flow<EK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem));
+                EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 cur = smem;
             }
             int occ = 0;
-            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_flow<EK>, FLOW_THREADS, smem));
+            EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
             it = grids.emplace(key, NUM_SMS_B200 * std::max(1, std::min(occ, 2))).first;
         }
         grid = it->second;
@@ -817,41 +823,38 @@ static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a, size_t smem) {
     a.ticket_base = tp.ticket_base;
     tp.ticket_base += (unsigned)(tp.n_tiles + grid);   // every CTA takes exactly one failing ticket
     void* args[] = {&a};
-    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)k_tile_flow<EK>, dim3(grid), dim3(FLOW_THREADS), args, smem,
-                                          c->stream));
+    EDFA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(threads), args, smem, c->stream));
+}
+
+template <int EK>
+static void launch_tile_shape(Ctx* c, TilePlan& tp, TileSolve& a) {
+    const bool direct = c->opt.tile_direct < 0 ? tile_direct(tp) : c->opt.tile_direct != 0;
+    if (direct) launch_tile<EK, 7, true>(c, tp, a);
+    else launch_tile<EK, 15, false>(c, tp, a);
 }
 
 void run_tile(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name) {
-    run_tile_ex(c, tp, b, alpha, x, add, out2, name, false, false, nullptr, nullptr, nullptr);
+    run_tile_ex(c, tp, b, alpha, x, add, out2, name, false, false, nullptr);
 }
 
 void run_tile_ex(Ctx* c, TilePlan& tp, const double* b, double alpha, double* x, const double* add, double* out2,
-                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent, const Csr* fz,
-                 const double* fz_x) {
+                 const char* name, bool x_prefilled, bool consume_b, double* pre_sent) {
     TileSolve a{tp.n_tiles, tp.RC, tp.KD, tp.EC, tp.LC, tp.order.p, tp.hdr.p, tp.lev_ptr.p, tp.row_id.p,
                 tp.ext_id.p, tp.dslot.p, tp.dcoef.p, tp.eslot.p, tp.ecoef.p, tp.dinv.p, tp.ticket.p, 0u, b, alpha, x,
-                add, out2, c->d_scalar_i + 8, tp.xlev_ptr.p, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+                add, out2, c->d_scalar_i + 8, tp.xlev_ptr.p, nullptr, nullptr};
     a.b_sent = consume_b ? const_cast<double*>(b) : nullptr;
     a.pre_sent = pre_sent;
-    if (fz) {
-        require(!consume_b, EDFA_ERR_CUDA, "fused right-hand side and consumed b are exclusive");
-        a.fz_ptr = fz->ptr.p;
-        a.fz_idx = fz->idx.p;
-        a.fz_val = fz->val.p;
-        a.fz_x = fz_x;
-    }
     // a row's value is its own ready flag
     if (!x_prefilled) fill_bits(c, x, tp.n, SENTINEL_BITS);
     Prof pr(c, name, 12.0 * tp.n_dep + 24.0 * tp.n + (out2 ? 16.0 * tp.n : 0.0));
-    const size_t smem = tile_flow_smem_bytes(tp);
     switch (tp.KD) {
-        case 4: launch_tile<4>(c, tp, a, smem); break;
-        case 8: launch_tile<8>(c, tp, a, smem); break;
-        case 12: launch_tile<12>(c, tp, a, smem); break;
-        case 16: launch_tile<16>(c, tp, a, smem); break;
-        case 24: launch_tile<24>(c, tp, a, smem); break;
-        default: launch_tile<32>(c, tp, a, smem); break;
+        case 4: launch_tile_shape<4>(c, tp, a); break;
+        case 8: launch_tile_shape<8>(c, tp, a); break;
+        case 12: launch_tile_shape<12>(c, tp, a); break;
+        case 16: launch_tile_shape<16>(c, tp, a); break;
+        case 24: launch_tile_shape<24>(c, tp, a); break;
+        default: launch_tile_shape<32>(c, tp, a); break;
     }
 }
 

@@ -193,15 +193,19 @@ def geometry(node_coords, e2n, f2e, floc):
     return vol, area
 
 
-def box_grid(nx, ny, nz, dx, dy, dz) -> HexGrid:
-    """Regular nx*ny*nz box with spacings dx, dy, dz (hx/grid.py:68-134)."""
+def box_grid(nx, ny, nz, dx, dy, dz, z0_layer: int = 0) -> HexGrid:
+    """Regular nx*ny*nz box with spacings dx, dy, dz (hx/grid.py:68-134).
+
+    ``z0_layer`` > 0 builds the cell layers [z0, z0 + nz) of a taller box
+    (a z-slab of the multi-GPU partition): node z = (k + z0) dz exactly as
+    in the full box, so the slab's geometry is the full box's bit for bit."""
     if min(nx, ny, nz) < 1 or min(dx, dy, dz) <= 0:
         raise ValueError("grid dimensions must be >= 1 and spacings > 0")
     nx, ny, nz = int(nx), int(ny), int(nz)
     n = np.arange((nx + 1) * (ny + 1) * (nz + 1))
     coords = np.stack([(n % (nx + 1)) * dx,
                        ((n // (nx + 1)) % (ny + 1)) * dy,
-                       (n // ((nx + 1) * (ny + 1))) * dz], axis=1).astype(float)
+                       (n // ((nx + 1) * (ny + 1)) + int(z0_layer)) * dz], axis=1).astype(float)
     e2n, e2f, f2e, floc = _topology(nx, ny, nz)
     vol, area = geometry(coords, e2n, f2e, floc)
     return HexGrid(nx, ny, nz, coords, e2n, e2f, f2e, floc, area, vol)

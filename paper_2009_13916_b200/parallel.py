@@ -224,6 +224,105 @@ def _local_blocks(system, A, lay, nf, f2e, free, nxy):
     b["rhs"] = np.concatenate([system.rhs_f[lay.own_faces], system.rhs_c[lay.own_cells]])
 
 
+def _sub_face_keys(nx, ny, nz, s0, nzs):
+    """Global face ids and owner cell layers of the faces of the sub-box of
+    cell layers [s0, s0 + nzs) (hx/grid.py:97-129 numbering: families x, y, z,
+    each k-slowest; a face is owned by its lower-indexed cell)."""
+    nxf, nyf = (nx + 1) * ny * nzs, nx * (ny + 1) * nzs
+    NXF, NYF = (nx + 1) * ny * nz, nx * (ny + 1) * nz
+    f = np.arange(nxf)
+    i, j, k = f % (nx + 1), (f // (nx + 1)) % ny, f // ((nx + 1) * ny)
+    gx, lx = i + (nx + 1) * (j + ny * (k + s0)), k + s0
+    f = np.arange(nyf)
+    i, j, k = f % nx, (f // nx) % (ny + 1), f // (nx * (ny + 1))
+    gy, ly = NXF + i + nx * (j + (ny + 1) * (k + s0)), k + s0
+    f = np.arange(nx * ny * (nzs + 1))
+    i, j, kp = f % nx, (f // nx) % ny, f // (nx * ny)
+    gz, lz = NXF + NYF + i + nx * (j + ny * (kp + s0)), np.maximum(kp + s0 - 1, 0)
+    return np.concatenate([gx, gy, gz]), np.concatenate([lx, ly, lz])
+
+
+def build_slab_layout(sub, s0: int, nz: int, parts: int, rank: int, halo: int) -> SlabLayout:
+    """The layout of slab ``rank`` built from its own sub-box only -- no
+    global system on any process (host memory O(slab)).
+
+    ``sub`` is the BlockSystem of the cell layers [s0, s1) with s0 = max(0,
+    e0 - 1), s1 = min(nz, e1 + 1) around the extended slab [e0, e1) =
+    [k0 - halo, k1 + halo) (configs.slab_case): every row whose cells lie in
+    layers [s0 + 1, s1 - 2] equals the global row.  Entries are matched
+    across ranks by global ids (cells i + nx(j + ny k), faces by
+    _sub_face_keys); halo lists are ordered by (owner slab, global id), the
+    order build_layouts uses, so the local blocks are the global ones."""
+    grid = sub.grid
+    nx, ny, nzs = grid.nx, grid.ny, grid.nz
+    s1 = s0 + nzs
+    nxy = nx * ny
+    bounds = slab_bounds(nz, parts)
+    k0, k1 = bounds[rank]
+    e0, e1 = max(0, k0 - halo), min(nz, k1 + halo)
+    if not (s0 <= max(e0 - 1, 0) and min(e1 + 1, nz) <= s1):
+        raise ValueError("the sub-box does not cover the extended slab plus one layer")
+    layer_part = np.empty(nz, dtype=np.int64)
+    for r, (a, b) in enumerate(bounds):
+        layer_part[a:b] = r
+    free = np.asarray(sub.free_faces)
+    nf = free.size
+    gface, lface = _sub_face_keys(nx, ny, nz, s0, nzs)
+    fkey, flay = gface[free], lface[free]
+    face_part = layer_part[flay]
+    n_c = sub.n_cells
+    clay = np.arange(n_c) // nxy + s0
+    ckey = np.arange(n_c) + s0 * nxy
+    cell_part = layer_part[clay]
+    A = _canon(sub.full_matrix())
+    own_f = np.flatnonzero(face_part == rank)
+    own_c = np.flatnonzero(cell_part == rank)
+    rows = np.concatenate([own_f, nf + own_c])
+    cols = np.unique(A[rows].indices)
+    hf = cols[cols < nf]
+    hf = hf[face_part[hf] != rank]
+    hc = cols[cols >= nf] - nf
+    hc = hc[cell_part[hc] != rank]
+
+    def ordered(ids, owner, key):
+        o = np.lexsort((key[ids], owner[ids]))
+        ids = ids[o]
+        recv = {}
+        for q in np.unique(owner[ids]):
+            w = np.flatnonzero(owner[ids] == q)
+            recv[int(q)] = (int(w[0]), int(w[-1]) + 1)
+        return ids, recv
+
+    hf, recv_f = ordered(hf, face_part, fkey)
+    hc, recv_c = ordered(hc, cell_part, ckey)
+    lay = SlabLayout(rank, parts, k0 - s0, k1 - s0, e0 - s0, e1 - s0, (nx, ny, nzs), own_f, own_c, hf, hc,
+                     recv_f, recv_c)
+    lay.global_bounds = (k0, k1, e0, e1, s0, s1)
+    lay.face_keys, lay.cell_keys = fkey, ckey
+    # what each other slab needs from this one: this slab's entries among the
+    # columns of that slab's complete rows in the sub-box (sorted by global id)
+    lo = s0 + 1 if s0 > 0 else 0
+    hi = s1 - 2 if s1 < nz else nz - 1
+    complete_f = (flay >= lo) & (flay <= hi)
+    complete_c = (clay >= lo) & (clay <= hi)
+    for q in sorted(set(face_part[complete_f].tolist()) | set(cell_part[complete_c].tolist())):
+        if q == rank:
+            continue
+        qrows = np.concatenate([np.flatnonzero(complete_f & (face_part == q)),
+                                nf + np.flatnonzero(complete_c & (cell_part == q))])
+        qc = np.unique(A[qrows].indices)
+        sf = qc[(qc < nf)]
+        sf = sf[face_part[sf] == rank]
+        sc = qc[qc >= nf] - nf
+        sc = sc[cell_part[sc] == rank]
+        if sf.size:
+            lay.send_faces[q] = np.searchsorted(own_f, sf[np.argsort(fkey[sf], kind="stable")])
+        if sc.size:
+            lay.send_cells[q] = np.searchsorted(own_c, sc[np.argsort(ckey[sc], kind="stable")])
+    _local_blocks(sub, A, lay, nf, np.asarray(grid.face_to_elems), free, nxy)
+    return lay
+
+
 def scatter_solution(layouts, xs, n_free_faces, n_cells):
     """Global solution from the per-slab local vectors (host)."""
     x = np.empty(n_free_faces + n_cells)
@@ -509,6 +608,40 @@ class CudaSlab:
 # ---------------------------------------------------------------------------
 # distributed operator + GMRES
 
+class CommTimer:
+    """CUDA events around the communication calls of a distributed solve
+    (halo exchanges, all-reduces) on the current stream: device time spent
+    inside NCCL, reported as a share of the step (bench.py)."""
+
+    def __init__(self):
+        self.pairs = {"halo": [], "allreduce": []}
+        self.enabled = False
+
+    def __call__(self, kind):
+        timer = self
+
+        class _Span:
+            def __enter__(self_):
+                if timer.enabled:
+                    self_.e0 = torch.cuda.Event(enable_timing=True)
+                    self_.e0.record()
+
+            def __exit__(self_, *exc):
+                if timer.enabled:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record()
+                    timer.pairs[kind].append((self_.e0, e1))
+        return _Span()
+
+    def collect(self, reset=True):
+        torch.cuda.synchronize()
+        out = {k: sum(a.elapsed_time(b) for a, b in v) for k, v in self.pairs.items()}
+        out.update({f"{k}_calls": len(v) for k, v in self.pairs.items()})
+        if reset:
+            self.pairs = {k: [] for k in self.pairs}
+        return out
+
+
 class SlabOperator:
     """The block operator and the EDFA preconditioner over a set of slabs."""
 
@@ -516,6 +649,7 @@ class SlabOperator:
         self.parts = parts
         self.comm = comm
         self.halo = HaloExchange(parts, comm)
+        self.timer = CommTimer()
 
     def _own_views(self, vecs, kind):
         out = []
@@ -528,21 +662,24 @@ class SlabOperator:
         """zext[:n_own] = P^-1 r per part (two halo exchanges)."""
         for p, r in zip(self.parts, rs):
             p.apply_faces(r)
-        self.halo.run("f", [p.tf_ext[:p.layout.n_faces] for p in self.parts],
-                      [p.tf_ext[p.layout.n_faces:] for p in self.parts])
+        with self.timer("halo"):
+            self.halo.run("f", [p.tf_ext[:p.layout.n_faces] for p in self.parts],
+                          [p.tf_ext[p.layout.n_faces:] for p in self.parts])
         for p, r in zip(self.parts, rs):
             p.apply_cells(r)
-        self.halo.run("c", [p.yc_ext[:p.layout.n_cells] for p in self.parts],
-                      [p.yc_ext[p.layout.n_cells:] for p in self.parts])
+        with self.timer("halo"):
+            self.halo.run("c", [p.yc_ext[:p.layout.n_cells] for p in self.parts],
+                          [p.yc_ext[p.layout.n_cells:] for p in self.parts])
         for p in self.parts:
             p.apply_finish(p.zext[:p.layout.n_own])
 
     def matvec_zext(self, ws):
         """w = A zext per part (exchanges the halo of zext's own part)."""
-        self.halo.run("f", [p.zext[:p.layout.n_faces] for p in self.parts],
-                      [p.zext[p.layout.n_own:p.layout.n_own + p.layout.halo_faces.size] for p in self.parts])
-        self.halo.run("c", [p.zext[p.layout.n_faces:p.layout.n_own] for p in self.parts],
-                      [p.zext[p.layout.n_own + p.layout.halo_faces.size:] for p in self.parts])
+        with self.timer("halo"):
+            self.halo.run("f", [p.zext[:p.layout.n_faces] for p in self.parts],
+                          [p.zext[p.layout.n_own:p.layout.n_own + p.layout.halo_faces.size] for p in self.parts])
+            self.halo.run("c", [p.zext[p.layout.n_faces:p.layout.n_own] for p in self.parts],
+                          [p.zext[p.layout.n_own + p.layout.halo_faces.size:] for p in self.parts])
         for p, w in zip(self.parts, ws):
             p.spmv_ext(w)
 
@@ -552,7 +689,8 @@ class SlabOperator:
             t = partials[0].clone()
             for q in partials[1:]:
                 t += q.to(t.device)
-        self.comm.allreduce_(t)
+        with self.timer("allreduce"):
+            self.comm.allreduce_(t)
         return t
 
 

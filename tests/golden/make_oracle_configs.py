@@ -1,0 +1,72 @@
+"""Parity fixtures of BASELINE configs 3 and 4 from the pinned CPU oracle.
+
+    python tests/golden/make_oracle_configs.py [c3_24 c3_32 c4]
+
+Runs the oracle port (tests/test_oracle_golden.py pins it to the reference)
+with each config's bench options (configs.py) on the same seeded generator at
+CPU-feasible sizes -- config 3 at 24^3 and 32^3, config 4 (first system of
+the time-step sequence) at 20 x 73 x 28 -- and stores what the GPU parity
+tests gate: GMRES(50) iterations, residual history, true relative residual,
+nnz of H~ and S~, the restriction sets and G~/F~ rows of 512 seeded cells, and
+a subsample of the solution with its norm.
+"""
+
+import pathlib
+import sys
+import time
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent.parent))
+
+from oracle import edfa_oracle as O                     # noqa: E402
+from paper_2009_13916_b200 import configs                # noqa: E402
+
+CASES = {
+    "c3_24": lambda: configs.config3(n=24),
+    "c3_32": lambda: configs.config3(n=32),
+    "c4": lambda: configs.config4(nx=20, ny=73, nz=28),
+}
+
+
+def run(name):
+    case = CASES[name]()
+    s = case.system
+    p = case.precond
+    A, b = s.full_matrix(), s.rhs()
+    face_nf = p.get("face_no_fill", p.get("no_fill", True))
+    schur_nf = p.get("schur_no_fill", p.get("no_fill", True))
+    t0 = time.perf_counter()
+    kw = dict(face_drop_tol=p.get("face_drop_tol", 0.0), no_fill=face_nf, n_workers=8)
+    if p["pattern"] == "dynamic":
+        o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, dynamic=(p["n_add"], p["n_ent"], None), **kw)
+    else:
+        o1 = O.build_stage1(s.A_ff, s.A_fc, s.A_cf, sets=O.static_sets(s.grid, s.face_index, p["prototype"]), **kw)
+    t1 = time.perf_counter()
+    o2 = O.build_stage2(s.A_cc, o1, schur_drop_tol=p.get("schur_drop_tol", 0.0), no_fill=schur_nf)
+    t2 = time.perf_counter()
+    x, r = O.gmres(lambda v: A @ v, lambda v: O.apply(o1, o2, s.A_fc, s.A_cf, v), b, tol=case.rtol,
+                   restart=case.restart, max_it=case.max_it)
+    t3 = time.perf_counter()
+    rows = np.sort(np.random.default_rng(7).choice(s.n_cells, size=min(512, s.n_cells), replace=False))
+    G, FT = o1.G.tocsr(), o1.F.T.tocsr()
+    sets = [np.asarray(o1.sets[m], dtype=np.int64) for m in rows]
+    out = dict(n_it=r.n_it, converged=r.converged, hist=np.array(r.relres_history), final_relres=r.final_relres,
+               x_sub=x[::37], x_norm=np.linalg.norm(x), nnz_H=o1.H.nnz, nnz_S=o2.S.nnz, rows=rows,
+               set_ptr=np.cumsum([0] + [len(q) for q in sets]), set_idx=np.concatenate(sets),
+               G_ptr=np.cumsum([0] + [G.indptr[m + 1] - G.indptr[m] for m in rows]),
+               G_idx=np.concatenate([G.indices[G.indptr[m]:G.indptr[m + 1]] for m in rows]),
+               G_val=np.concatenate([G.data[G.indptr[m]:G.indptr[m + 1]] for m in rows]),
+               F_ptr=np.cumsum([0] + [FT.indptr[m + 1] - FT.indptr[m] for m in rows]),
+               F_idx=np.concatenate([FT.indices[FT.indptr[m]:FT.indptr[m + 1]] for m in rows]),
+               F_val=np.concatenate([FT.data[FT.indptr[m]:FT.indptr[m + 1]] for m in rows]),
+               seconds=np.array([t1 - t0, t2 - t1, t3 - t2]))
+    np.savez_compressed(HERE / f"oracle_{name}.npz", **out)
+    print(name, case.name, "its", r.n_it, "converged", r.converged, "relres", r.final_relres,
+          "s1/s2/solve s", [round(v, 1) for v in out["seconds"]], flush=True)
+
+
+if __name__ == "__main__":
+    for name in (sys.argv[1:] or list(CASES)):
+        run(name)

@@ -589,3 +589,27 @@ def test_config2_full_size_matches_oracle(edfa):
     x = x.cpu().numpy() if hasattr(x, "cpu") else x
     assert abs(np.linalg.norm(x) - float(d["x_norm"])) <= 1e-7 * float(d["x_norm"])
     assert np.abs(x[::97] - d["x_sub"]).max() <= 1e-7 * np.abs(d["x_sub"]).max()
+
+
+@pytest.mark.parametrize("idx,n", [(2, 24), (1, 16)])
+def test_direct_tile_solve_equals_staged(edfa, idx, n):
+    """The wide-wavefront shape of the ILU tile solve (7 warps, early records
+    read from L2) performs the same operations as the staged shape: identical
+    triangular solutions."""
+    from paper_2009_13916_b200 import configs
+    case = configs.make(idx, n=n)
+    s = case.system
+    p = case.precond
+    ds = edfa.DeviceSystem.from_host(s)
+    if p["pattern"] == "dynamic":
+        pre = edfa.BlockLDUPreconditioner.build(ds, dynamic=edfa.DynamicConfig(p["n_add"], p["n_ent"]), no_fill=True)
+    else:
+        pre = edfa.BlockLDUPreconditioner.build(ds, patterns=edfa.patterns_for(ds, p["pattern"], p.get("prototype", "A")),
+                                                no_fill=True)
+    r = np.random.default_rng(13).standard_normal(s.n_unknowns)
+    ys = []
+    for direct in (0, 1):
+        with option("tile_direct", direct):
+            ys.append((pre.apply(r), pre.stage2.schur_inner.apply(r[s.n_free_faces:])))
+    for a, b in zip(ys[0], ys[1]):
+        assert np.array_equal(a, b)

@@ -177,3 +177,46 @@ def test_slab_bounds_errors():
     with pytest.raises(ValueError):
         parallel.slab_bounds(4, 5)
     assert parallel.slab_bounds(8, 3) == [(0, 2), (2, 5), (5, 8)]
+
+
+@pytest.mark.parametrize("parts,n,nz", [(2, 5, 10), (3, 6, 12), (4, 4, 16)])
+def test_slab_layout_from_sub_box_equals_global_layout(parts, n, nz):
+    """A rank that assembles only its own sub-box (configs.slab_case) gets the
+    same owned rows, halo lists, send lists and local blocks as the layout
+    cut from the global system (entries matched by global ids).  Patterns
+    are exact; values agree to 1e-13 (numpy's batched element kernels round
+    differently in the last bit for a different number of cells; the device
+    assembly is per cell and bit-identical)."""
+
+    def same(a, b):
+        return (a.shape == b.shape and np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+                and np.abs(a.data - b.data).max(initial=0.0) <= 1e-13 * np.abs(b.data).max(initial=1.0))
+    s = configs.config2(n=n, nz=nz).system
+    halo = parallel.halo_layers("static", "A")
+    glays = parallel.build_layouts(s, parts, halo=halo)
+    gkey_f, _ = parallel._sub_face_keys(n, n, nz, 0, nz)
+    free_key = gkey_f[s.free_faces]
+    for r in range(parts):
+        k0, k1 = parallel.slab_bounds(nz, parts)[r]
+        s0, s1 = max(0, k0 - halo - 1), min(nz, k1 + halo + 1)
+        sub = configs.slab_case(2, n, s0, s1, nz=nz).system
+        lay = parallel.build_slab_layout(sub, s0, nz, parts, r, halo)
+        g = glays[r]
+        assert np.array_equal(lay.face_keys[lay.own_faces], free_key[g.own_faces])
+        assert np.array_equal(lay.cell_keys[lay.own_cells], g.own_cells)
+        assert np.array_equal(lay.face_keys[lay.halo_faces], free_key[g.halo_faces])
+        assert np.array_equal(lay.cell_keys[lay.halo_cells], g.halo_cells)
+        assert lay.recv_faces == g.recv_faces and lay.recv_cells == g.recv_cells
+        assert lay.send_faces.keys() == g.send_faces.keys() and lay.send_cells.keys() == g.send_cells.keys()
+        for q in g.send_faces:
+            assert np.array_equal(lay.send_faces[q], g.send_faces[q])
+        for q in g.send_cells:
+            assert np.array_equal(lay.send_cells[q], g.send_cells[q])
+        for name in ("A_loc", "A_cf_loc", "A_fc_loc", "A_ff_own", "A_cc_own"):
+            assert same(lay.blocks[name], g.blocks[name]), name
+        for name in ("A_ff", "A_fc", "A_cf", "A_cc"):
+            assert same(lay.blocks["ext"][name], g.blocks["ext"][name]), name
+        for a, b in zip(lay.blocks["ext_topology"], g.blocks["ext_topology"]):
+            assert np.array_equal(a, b)
+        rb = g.blocks["rhs"]
+        assert np.abs(lay.blocks["rhs"] - rb).max() <= 1e-13 * max(np.abs(rb).max(), 1.0)
