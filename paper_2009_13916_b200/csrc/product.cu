@@ -513,6 +513,10 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
         launch_product_pf(c, a);
         ovf_rows = read_overflow(c, ovf.p);
     }
+    // first-tier counts (0 for the rows re-run below): what k_unpad copies from
+    // the first padded buffer -- the re-runs overwrite cnt with their own counts
+    DevBuf<int32_t> cnt1(c, std::max(n, 1));
+    if (n) EDFA_CUDA(cudaMemcpyAsync(cnt1.p, cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
     // rows beyond the first tier: 1024-slot tables into a second padded
     // buffer (by list position); rows beyond that: 4096-slot count + fill
     constexpr int CAP2 = 512;
@@ -536,6 +540,11 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
         launch_product<10, PADDED>(c, b);
         ovf2 = read_overflow(c, ovf.p);
     }
+    DevBuf<int32_t> cnt2;   // second-tier counts (0 for the rows the third tier re-runs)
+    if (!ovf2.empty()) {
+        cnt2.reset(c, std::max(n, 1));
+        EDFA_CUDA(cudaMemcpyAsync(cnt2.p, cnt.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+    }
     ProdArgs b3 = a;
     if (!ovf2.empty()) {
         rows2.reset(c, ovf2.size());
@@ -553,14 +562,15 @@ void triple_product(Ctx* c, const Csr& G, const Csr& A, const Csr& F, double pos
     H.val.reset(c, H.nnz);
     if (n) {
         Prof pr(c, "product_unpad", 24.0 * H.nnz + 8.0 * n);
-        k_unpad<<<ceil_div((int64_t)n * 32, 256), 256, 0, c->stream>>>(cnt.p, H.ptr.p, n, CAP, pi.p, pv.p, H.idx.p,
+        k_unpad<<<ceil_div((int64_t)n * 32, 256), 256, 0, c->stream>>>(cnt1.p, H.ptr.p, n, CAP, pi.p, pv.p, H.idx.p,
                                                                       H.val.p);
         check_launch("k_unpad");
     }
     if (!ovf_rows.empty()) {
         const int nl = (int)ovf_rows.size();
-        k_unpad_list<<<ceil_div((int64_t)nl * 32, 256), 256, 0, c->stream>>>(rows1.p, nl, cnt.p, H.ptr.p, CAP2, pi2.p,
-                                                                            pv2.p, H.idx.p, H.val.p);
+        k_unpad_list<<<ceil_div((int64_t)nl * 32, 256), 256, 0, c->stream>>>(rows1.p, nl, ovf2.empty() ? cnt.p : cnt2.p,
+                                                                            H.ptr.p, CAP2, pi2.p, pv2.p, H.idx.p,
+                                                                            H.val.p);
         check_launch("k_unpad_list");
     }
     if (!ovf2.empty()) {

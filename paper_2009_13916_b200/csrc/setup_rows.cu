@@ -365,21 +365,23 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
         for (int t = li; t < s * LD; t += L) M[t] = 0.0;
         if (li < SMAX) { bg[li] = 0.0; bf[li] = 0.0; }
         __syncwarp();
-        if (li < s) {   // the row's entries are loaded in batches of 12 (all in flight), then placed
+        if (li < s) {   // the row's entries are loaded in batches of 12 (all in flight), then
+                        // merged with the sorted set (both ascending: one forward walk, no search)
             const int row = q[li];
             const int e0 = a.A.ptr[row], e1 = a.A.ptr[row + 1];
+            int j = 0;
             for (int eb = e0; eb < e1; eb += 12) {
                 int ci[12];
                 double cv[12];
 #pragma unroll
                 for (int u = 0; u < 12; ++u) {
-                    ci[u] = eb + u < e1 ? a.A.idx[eb + u] : -1;
+                    ci[u] = eb + u < e1 ? a.A.idx[eb + u] : INT32_MAX;
                     cv[u] = eb + u < e1 ? a.A.val[eb + u] : 0.0;
                 }
 #pragma unroll
                 for (int u = 0; u < 12; ++u) {
-                    const int j = ci[u] >= 0 ? bsearch(q, 0, s, ci[u]) : -1;
-                    if (j >= 0) M[li * LD + j] = -cv[u];
+                    while (j < s && q[j] < ci[u]) ++j;
+                    if (j < s && q[j] == ci[u]) M[li * LD + j] = -cv[u];
                 }
             }
         }
@@ -398,9 +400,13 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
 #pragma unroll
         for (int j = 0; j < SMAX; ++j) r[j] = (li < s && j < s) ? M[li * LD + j] : 0.0;
         double yg = li < s ? bg[li] : 0.0, yf = li < s ? bf[li] : 0.0;
-        // ---- right-looking Cholesky, lane i holds row i (lower part)
+        // ---- right-looking Cholesky, lane i holds row i (lower part); column k
+        // of L goes through a shared-memory line (broadcast reads) instead of
+        // one shuffle pair per entry
         double inv_self = 0.0;
         bool bad = false;
+        double* colk = bg;                             // bg / bf are in registers now: reuse as the line
+        __syncwarp();
 #pragma unroll
         for (int k = 0; k < SMAX; ++k) {
             if (k >= s_w) break;
@@ -409,12 +415,14 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
             const double lkk = sqrt(dkk), ik = 1.0 / lkk;
             if (li > k) r[k] *= ik;
             if (li == k) { r[k] = lkk; inv_self = ik; }
+            if (li < SMAX) colk[li] = r[k];
+            __syncwarp();
 #pragma unroll
             for (int j = k + 1; j < SMAX; ++j) {
                 if (j >= s_w) break;
-                const double ljk = __shfl_sync(0xffffffffu, r[k], seg * L + j);
-                if (li >= j) r[j] = fma(-r[k], ljk, r[j]);
+                if (li >= j) r[j] = fma(-r[k], colk[j], r[j]);
             }
+            __syncwarp();
         }
         bad = bad && row_ok;
         if (__any_sync(0xffffffffu, bad)) {

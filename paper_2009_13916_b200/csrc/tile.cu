@@ -816,7 +816,7 @@ static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a) {
             }
             int occ = 0;
             EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
-            it = grids.emplace(key, NUM_SMS_B200 * std::max(1, std::min(occ, 2))).first;
+            it = grids.emplace(key, NUM_SMS_B200 * std::max(1, std::min(occ, DIRECT ? 4 : 2))).first;
         }
         grid = it->second;
     }
@@ -828,8 +828,9 @@ static void launch_tile(Ctx* c, TilePlan& tp, TileSolve& a) {
 
 template <int EK>
 static void launch_tile_shape(Ctx* c, TilePlan& tp, TileSolve& a) {
-    const bool direct = c->opt.tile_direct < 0 ? tile_direct(tp) : c->opt.tile_direct != 0;
-    if (direct) launch_tile<EK, 7, true>(c, tp, a);
+    const int mode = c->opt.tile_direct < 0 ? (tile_direct(tp) ? 1 : 0) : c->opt.tile_direct;
+    if (mode == 2) launch_tile<EK, 5, true>(c, tp, a);        // three CTAs per SM
+    else if (mode == 1) launch_tile<EK, 7, true>(c, tp, a);
     else launch_tile<EK, 15, false>(c, tp, a);
 }
 

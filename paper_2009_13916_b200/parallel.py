@@ -387,27 +387,37 @@ class HaloExchange:
 
     def run(self, kind: str, src, dst) -> None:
         """kind 'f' or 'c'; src[i] own-entry vector, dst[i] halo vector of parts[i]."""
-        send_attr = "send_faces" if kind == "f" else "send_cells"
-        recv_attr = "recv_faces" if kind == "f" else "recv_cells"
+        self.run_many([(kind, src, dst)])
+
+    def run_many(self, jobs) -> None:
+        """Several exchanges [(kind, src, dst), ...] in ONE batch of P2P
+        operations (one NCCL group launch instead of one per kind)."""
         rank_of = self.comm.rank_of_part
         remote_s, remote_r = [], []
-        bufs = {}
-        for p, s in zip(self.parts, src):
-            for q in sorted(getattr(p.layout, send_attr)):
-                bufs[(p.layout.rank, q)] = p.gather(s, kind, q)
-        for p, d in zip(self.parts, dst):
-            for q, (a, b) in sorted(getattr(p.layout, recv_attr).items()):
-                if q in self.by_slab:
-                    d[a:b].copy_(bufs[(q, p.layout.rank)])
-                else:
-                    remote_r.append((rank_of[q], d[a:b]))
-        for (src_slab, q), buf in sorted(bufs.items()):
-            if q not in self.by_slab:
-                remote_s.append((rank_of[q], buf))
-        if remote_s or remote_r:
-            # matched in order: sends sorted by (source slab, target slab),
-            # receives by (local slab, source slab) -- the same sequence on
-            # both ends of every process pair
+        sends = {}
+        for ji, (kind, src, dst) in enumerate(jobs):
+            send_attr = "send_faces" if kind == "f" else "send_cells"
+            recv_attr = "recv_faces" if kind == "f" else "recv_cells"
+            bufs = {}
+            for p, s in zip(self.parts, src):
+                for q in sorted(getattr(p.layout, send_attr)):
+                    bufs[(p.layout.rank, q)] = p.gather(s, kind, q)
+            for p, d in zip(self.parts, dst):
+                for q, (a, b) in sorted(getattr(p.layout, recv_attr).items()):
+                    if q in self.by_slab:
+                        d[a:b].copy_(bufs[(q, p.layout.rank)])
+                    else:
+                        remote_r.append(((p.layout.rank, q, ji), rank_of[q], d[a:b]))
+            for (src_slab, q), buf in bufs.items():
+                if q not in self.by_slab:
+                    sends[(src_slab, q, ji)] = (rank_of[q], buf)
+        if sends or remote_r:
+            # matched in order on both ends of every process pair: sends sorted
+            # by (source slab, target slab, job), receives by (local slab,
+            # source slab, job) -- z-slabs of one process are contiguous, so a
+            # process pair shares one slab boundary
+            remote_s = [sends[k] for k in sorted(sends)]
+            remote_r = [(peer, t) for _, peer, t in sorted(remote_r, key=lambda e: e[0])]
             self.comm.p2p(remote_s, remote_r)
 
 
@@ -676,10 +686,11 @@ class SlabOperator:
     def matvec_zext(self, ws):
         """w = A zext per part (exchanges the halo of zext's own part)."""
         with self.timer("halo"):
-            self.halo.run("f", [p.zext[:p.layout.n_faces] for p in self.parts],
-                          [p.zext[p.layout.n_own:p.layout.n_own + p.layout.halo_faces.size] for p in self.parts])
-            self.halo.run("c", [p.zext[p.layout.n_faces:p.layout.n_own] for p in self.parts],
-                          [p.zext[p.layout.n_own + p.layout.halo_faces.size:] for p in self.parts])
+            self.halo.run_many([
+                ("f", [p.zext[:p.layout.n_faces] for p in self.parts],
+                 [p.zext[p.layout.n_own:p.layout.n_own + p.layout.halo_faces.size] for p in self.parts]),
+                ("c", [p.zext[p.layout.n_faces:p.layout.n_own] for p in self.parts],
+                 [p.zext[p.layout.n_own + p.layout.halo_faces.size:] for p in self.parts])])
         for p, w in zip(self.parts, ws):
             p.spmv_ext(w)
 
