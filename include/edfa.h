@@ -307,6 +307,9 @@ int edfa_multiaxpy(edfa_ctx* ctx, int64_t n, int32_t nvec, const double* V, int6
                    const double* h_dev, double hscale, const double* w_in, double* out,
                    double* norm2_dev);
 /* out[i] = x[idx[i]]  (halo send buffers). */
+/* y[rows[r]] = (A x)[r] for r < rows of A: the halo-dependent (boundary) rows of
+ * a slab's SpMV, computed after the halo exchange that the interior rows overlap. */
+int edfa_spmv_rows(edfa_ctx* ctx, const edfa_csr* A, const int32_t* rows, const double* x, double* y);
 int edfa_gather(edfa_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* out);
 
 /* ---- RT0 MHFE / FV assembly --------------------------

@@ -125,6 +125,7 @@ _SIGS = {
     "edfa_multidot": (i32, [vp, i64, i32, vp, i64, vp, vp]),
     "edfa_multiaxpy": (i32, [vp, i64, i32, vp, i64, vp, f64, vp, vp, vp]),
     "edfa_gather": (i32, [vp, i64, vp, vp, vp]),
+    "edfa_spmv_rows": (i32, [vp, vp, vp, vp, vp]),
     "edfa_assemble": (i32, [vp, C.POINTER(HexGridDesc), C.POINTER(AssemblyIn), C.POINTER(AssemblyOut),
                             C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "edfa_update_accumulation": (i32, [vp, vp, vp, vp, vp, f64, C.POINTER(vp), vp]),

@@ -681,6 +681,13 @@ int edfa_multiaxpy(edfa_ctx* ctx, int64_t n, int32_t nvec, const double* V, int6
     API_END
 }
 
+int edfa_spmv_rows(edfa_ctx* ctx, const edfa_csr* A, const int32_t* rows, const double* x, double* y) {
+    API_BEGIN
+    require(ctx && A, EDFA_ERR_VALUE, "NULL argument");
+    spmv_rows(&ctx->c, M(A), rows, x, y);
+    API_END
+}
+
 int edfa_gather(edfa_ctx* ctx, int64_t n, const int32_t* idx, const double* x, double* out) {
     API_BEGIN
     gather(&ctx->c, n, idx, x, out);

@@ -216,6 +216,8 @@ void multiaxpy_entry(Ctx* c, int64_t n, int nvec, const double* V, int64_t ldv, 
 void csr_submatrix(Ctx* c, const Csr& A, const int32_t* rows, int32_t n_out, const int32_t* cmap, int32_t n_cols,
                    Csr& out);
 void gather(Ctx* c, int64_t n, const int32_t* idx, const double* x, double* out);
+// y[rows[r]] = (A x)[r], A compact (the boundary rows of a slab SpMV)
+void spmv_rows(Ctx* c, const Csr& A, const int32_t* rows, const double* x, double* y);
 void axpby_entry(Ctx* c, int64_t n, double a, const double* x, double b, double* y);
 void dcgs2_dots_entry(Ctx* c, int64_t n, int j, const double* V, int64_t ldv, double* dots_out);
 void dcgs2_coeffs_entry(Ctx* c, int j, int m, const double* dots, double* H, double* h1, double* coef, double* hcol);

@@ -235,6 +235,36 @@ __device__ __forceinline__ int seg_of(const int* off, int n, int p) {   // last 
     return lo;
 }
 
+// One chunk of 32 consecutive contributions (lane order = flattened order p)
+// added into a hash accumulator with exactly the sequential semantics:
+// lanes holding the same key form a match group whose leader (lowest lane)
+// inserts, and the group's adds run in lane order, so every sum is formed in
+// increasing p (bit-identical to one entry at a time).  Returns the slot and
+// whether the leader inserted the key now (first encounter).
+__device__ __forceinline__ int chunk_accumulate(int* keys, double* vals, int bits, bool act, int key, double v,
+                                                int lane, bool* fresh_out, bool* full) {
+    const unsigned am = __ballot_sync(0xffffffffu, act);
+    const unsigned grp = __match_any_sync(0xffffffffu, act ? key : INT32_MIN);
+    const int leader = __ffs(grp) - 1;
+    bool fresh = false;
+    int sl = -1;
+    if (act && lane == leader) {
+        sl = h_insert(keys, bits, key, &fresh);
+        if (sl < 0) *full = true;
+    }
+    sl = __shfl_sync(0xffffffffu, sl, leader);
+    const int rank = __popc(grp & am & ((1u << lane) - 1));
+    int rmax = act ? rank : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    for (int r = 0; r <= rmax; ++r) {
+        if (act && sl >= 0 && rank == r) vals[sl] = __dadd_rn(vals[sl], v);
+        __syncwarp();
+    }
+    *fresh_out = fresh;
+    return sl;
+}
+
 __global__ void __launch_bounds__(256) k_product_pf(ProdArgs a) {
     constexpr int T = PF_T;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -278,33 +308,25 @@ __global__ void __launch_bounds__(256) k_product_pf(ProdArgs a) {
         __syncwarp();
         // ---- every A_ff entry of the row's W, flattened, loads in flight
         if (!full)
-            for (int p = lane; p < P; p += 32) {
+            for (int p = lane; p < P; p += 32) {   // products formed here: acc + (g * a), no contraction
                 const int t = seg_of(goff, nG, p);
                 const int e = ga0[t] + (p - goff[t]);
                 fcol[p] = a.A.idx[e];
-                fval[p] = a.A.val[e];
+                fval[p] = __dmul_rn(gv[t], a.A.val[e]);
             }
         __syncwarp();
         // ---- W = g_m A_ff from shared memory, k_product's order
         int nW = 0;
         if (!full) {
-            for (int t = 0; t < nG; ++t) {
-                const double g = gv[t];
-                const int e0 = goff[t], e1 = goff[t + 1];
-                for (int eb = e0; eb < e1; eb += 32) {
-                    const int e = eb + lane;
-                    bool fresh = false;
-                    int sl = -1;
-                    if (e < e1) {
-                        sl = h_insert(tk, PF_BITS, fcol[e], &fresh);
-                        if (sl < 0) full = true;
-                        else tv[sl] = add_mul(tv[sl], g, fval[e]);
-                    }
-                    const unsigned bal = __ballot_sync(0xffffffffu, fresh);
-                    const int pos = nW + __popc(bal & ((1u << lane) - 1));
-                    if (fresh && pos < T) wk[pos] = sl;
-                    nW += __popc(bal);
-                }
+            for (int pb = 0; pb < P; pb += 32) {   // 32 contributions per step, in p order
+                const int e = pb + lane;
+                bool fresh = false;
+                const int sl = chunk_accumulate(tk, tv, PF_BITS, e < P, e < P ? fcol[e] : 0, e < P ? fval[e] : 0.0,
+                                                lane, &fresh, &full);
+                const unsigned bal = __ballot_sync(0xffffffffu, fresh);
+                const int pos = nW + __popc(bal & ((1u << lane) - 1));
+                if (fresh && pos < T) wk[pos] = sl;
+                nW += __popc(bal);
                 __syncwarp();
             }
             full = __any_sync(0xffffffffu, full) || nW > T;
@@ -352,20 +374,17 @@ __global__ void __launch_bounds__(256) k_product_pf(ProdArgs a) {
                     const int q = seg_of(wo, nW, p);
                     const int e = tk[q] + (p - wo[q]);
                     fcol[p] = a.F.idx[e];
-                    fval[p] = a.F.val[e];
+                    fval[p] = __dmul_rn(wv[q], a.F.val[e]);
                 }
             __syncwarp();
         }
         // ---- H = W F from shared memory, k_product's order
         if (!full) {
-            for (int q = 0; q < nW; ++q) {
-                const double w = wv[q];
-                const int e0 = wo[q], e1 = wo[q + 1];    // empty for zero sums
-                for (int e = e0 + lane; e < e1; e += 32) {
-                    const int sl = h_insert(hk, PF_BITS, fcol[e]);
-                    if (sl < 0) full = true;
-                    else hv[sl] = add_mul(hv[sl], w, fval[e]);
-                }
+            for (int pb = 0; pb < P2; pb += 32) {  // zero sums of W contribute nothing (empty ranges)
+                const int e = pb + lane;
+                bool fresh = false;
+                chunk_accumulate(hk, hv, PF_BITS, e < P2, e < P2 ? fcol[e] : 0, e < P2 ? fval[e] : 0.0, lane, &fresh,
+                                 &full);
                 __syncwarp();
             }
             full = __any_sync(0xffffffffu, full);

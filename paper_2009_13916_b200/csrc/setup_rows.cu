@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(128) k_setup_rows(RowArgs a) {
 // read by the backward substitution.  No __syncwarp per column.
 template <int SMAX>
 struct RegRow {
-    static constexpr int L = SMAX <= 8 ? 8 : (SMAX <= 16 ? 16 : 32);   // lanes per row
+    static constexpr int L = SMAX <= 8 ? 8 : (SMAX <= 16 ? 16 : 32);   // lanes per row (>= SMAX)
     static constexpr int RPW = 32 / L;                                  // rows per warp
     static constexpr int LD = SMAX + 1;
     static constexpr size_t BYTES = sizeof(double) * (SMAX * LD + 2 * SMAX) + sizeof(int) * SMAX;
@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
         // ---- gather: q, the scratch tile, the two right-hand sides
         if (li < s) q[li] = a.q_idx[q0 + li];
         for (int t = li; t < s * LD; t += L) M[t] = 0.0;
+        (void)s_w;
         if (li < SMAX) { bg[li] = 0.0; bf[li] = 0.0; }
         __syncwarp();
         if (li < s) {   // the row's entries are loaded in batches of 12 (all in flight), then
@@ -396,32 +397,30 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
             }
         }
         __syncwarp();
+        // the s x s block padded to SMAX with an identity: every loop below is
+        // straight-line code over the compile-time size (padded unknowns solve to 0)
         double r[SMAX];
 #pragma unroll
-        for (int j = 0; j < SMAX; ++j) r[j] = (li < s && j < s) ? M[li * LD + j] : 0.0;
+        for (int j = 0; j < SMAX; ++j) r[j] = (li < s && j < s) ? M[li * LD + j] : (j == li ? 1.0 : 0.0);
         double yg = li < s ? bg[li] : 0.0, yf = li < s ? bf[li] : 0.0;
-        // ---- right-looking Cholesky, lane i holds row i (lower part); column k
-        // of L goes through a shared-memory line (broadcast reads) instead of
-        // one shuffle pair per entry
+        // ---- right-looking Cholesky, lane i holds row i; column k of L goes
+        // through a shared-memory line (broadcast reads).  Lanes update their
+        // whole row (the upper part is never read), so no per-entry predicates.
         double inv_self = 0.0;
         bool bad = false;
         double* colk = bg;                             // bg / bf are in registers now: reuse as the line
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < SMAX; ++k) {
-            if (k >= s_w) break;
             const double dkk = __shfl_sync(0xffffffffu, r[k], seg * L + k);
-            if (k < s && !(dkk > 0.0)) bad = true;
-            const double lkk = sqrt(dkk), ik = 1.0 / lkk;
+            bad |= !(dkk > 0.0);
+            const double ik = rsqrt(dkk), lkk = dkk * ik;
             if (li > k) r[k] *= ik;
             if (li == k) { r[k] = lkk; inv_self = ik; }
-            if (li < SMAX) colk[li] = r[k];
+            colk[li] = r[k];
             __syncwarp();
 #pragma unroll
-            for (int j = k + 1; j < SMAX; ++j) {
-                if (j >= s_w) break;
-                if (li >= j) r[j] = fma(-r[k], colk[j], r[j]);
-            }
+            for (int j = k + 1; j < SMAX; ++j) r[j] = fma(-r[k], colk[j], r[j]);
             __syncwarp();
         }
         bad = bad && row_ok;
@@ -432,23 +431,22 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
         // ---- forward substitution L y = b (both right-hand sides)
 #pragma unroll
         for (int k = 0; k < SMAX; ++k) {
-            if (k >= s_w) break;
             if (li == k) { yg *= inv_self; yf *= inv_self; }
             const double vg = __shfl_sync(0xffffffffu, yg, seg * L + k);
             const double vf = __shfl_sync(0xffffffffu, yf, seg * L + k);
             if (li > k) { yg = fma(-r[k], vg, yg); yf = fma(-r[k], vf, yf); }
         }
         // ---- backward substitution L^T x = y: columns of L from the scratch tile
-        __syncwarp();
 #pragma unroll
         for (int j = 0; j < SMAX; ++j)
-            if (li < s && j < li) M[li * LD + j] = r[j];
+            if (j < li) M[li * LD + j] = r[j];
         __syncwarp();
-        for (int k = s_w - 1; k >= 0; --k) {
+#pragma unroll
+        for (int k = SMAX - 1; k >= 0; --k) {
             if (li == k) { yg *= inv_self; yf *= inv_self; }
             const double vg = __shfl_sync(0xffffffffu, yg, seg * L + k);
             const double vf = __shfl_sync(0xffffffffu, yf, seg * L + k);
-            if (li < k && k < s) {
+            if (li < k) {
                 const double l = M[k * LD + li];
                 yg = fma(-l, vg, yg);
                 yf = fma(-l, vf, yf);
@@ -660,8 +658,11 @@ void setup_rows(Ctx* c, const SetupInput& in, SetupOutput& out) {
     {
         Prof pr(c, dyn ? "setup_rows_dynamic" : "setup_rows_static", bytes);
         if (!dyn) {
+            // the smallest register-row size >= the largest set (prototype A: 18, B/E: 24, base: 6-12)
             if (smax_need <= 8) launch_rows_reg<8>(c, a);
+            else if (smax_need <= 12) launch_rows_reg<12>(c, a);
             else if (smax_need <= 16) launch_rows_reg<16>(c, a);
+            else if (smax_need <= 18) launch_rows_reg<18>(c, a);
             else if (smax_need <= 24) launch_rows_reg<24>(c, a);
             else if (smax_need <= 32) launch_rows_reg<32>(c, a);
             else if (smax_need <= 64) launch_rows<64, 0, false>(c, a);

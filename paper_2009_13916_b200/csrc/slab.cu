@@ -52,7 +52,24 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ idx, const doubl
         out[i] = x[idx[i]];
 }
 
+// y[rows[r]] = (A x)[r] for a compact CSR A (boundary rows of a slab's SpMV)
+__global__ void k_spmv_rows(CsrV A, const int32_t* __restrict__ rows, const double* __restrict__ x,
+                            double* __restrict__ y) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= A.n_rows) return;
+    double acc = 0.0;
+    for (int e = A.ptr[r]; e < A.ptr[r + 1]; ++e) acc = fma(A.val[e], x[A.idx[e]], acc);
+    y[rows[r]] = acc;
+}
+
 }  // namespace
+
+void spmv_rows(Ctx* c, const Csr& A, const int32_t* rows, const double* x, double* y) {
+    if (A.n_rows <= 0) return;
+    Prof pr(c, "spmv_rows", 12.0 * A.nnz + 12.0 * A.n_rows + 8.0 * A.nnz);
+    k_spmv_rows<<<ceil_div(A.n_rows, 128), 128, 0, c->stream>>>(view(A), rows, x, y);
+    check_launch("k_spmv_rows");
+}
 
 void csr_submatrix(Ctx* c, const Csr& A, const int32_t* rows, int32_t n_out, const int32_t* cmap, int32_t n_cols,
                    Csr& out) {

@@ -323,6 +323,23 @@ def build_slab_layout(sub, s0: int, nz: int, parts: int, rank: int, halo: int) -
     return lay
 
 
+def split_boundary_rows(A_loc, n_own):
+    """(interior, boundary rows, boundary block) of a slab's local matrix:
+    interior = A_loc with the rows that reference halo columns emptied (it
+    writes 0 there), boundary = those rows compacted.  The interior SpMV runs
+    while the halo exchange is in flight; the boundary rows follow it."""
+    A = sp.csr_matrix(A_loc)
+    touches = np.zeros(A.shape[0], dtype=bool)
+    if A.nnz:
+        row_of = np.repeat(np.arange(A.shape[0]), np.diff(A.indptr))
+        touches[row_of[A.indices >= n_own]] = True
+    rows = np.flatnonzero(touches)
+    keep = np.repeat(~touches, np.diff(A.indptr))
+    A_int = sp.csr_matrix((A.data[keep], A.indices[keep],
+                           np.concatenate([[0], np.cumsum(np.diff(A.indptr) * ~touches)])), shape=A.shape)
+    return A_int, rows, A[rows]
+
+
 def scatter_solution(layouts, xs, n_free_faces, n_cells):
     """Global solution from the per-slab local vectors (host)."""
     x = np.empty(n_free_faces + n_cells)
@@ -352,6 +369,14 @@ class LocalComm:
         if sends or recvs:
             raise RuntimeError("LocalComm has no remote peers")
 
+    def p2p_start(self, sends, recvs):
+        self.p2p(sends, recvs)
+        return []
+
+    @staticmethod
+    def p2p_wait(works) -> None:
+        return None
+
 
 class TorchComm:
     """torch.distributed process group (NCCL on GPUs, gloo on CPU); one or
@@ -367,14 +392,21 @@ class TorchComm:
     def allreduce_(self, t: torch.Tensor) -> None:
         self.dist.all_reduce(t, group=self.group)
 
-    def p2p(self, sends, recvs) -> None:
-        """sends/recvs: lists of (peer process, tensor); matched in order."""
+    def p2p_start(self, sends, recvs):
+        """Issue the P2P operations (one NCCL group); returns the pending works."""
         d = self.dist
         ops = [d.P2POp(d.isend, t, peer, self.group) for peer, t in sends]
         ops += [d.P2POp(d.irecv, t, peer, self.group) for peer, t in recvs]
-        if ops:
-            for req in d.batch_isend_irecv(ops):
-                req.wait()
+        return d.batch_isend_irecv(ops) if ops else []
+
+    @staticmethod
+    def p2p_wait(works) -> None:
+        for req in works:        # stream-ordered: the compute stream waits for NCCL's
+            req.wait()
+
+    def p2p(self, sends, recvs) -> None:
+        """sends/recvs: lists of (peer process, tensor); matched in order."""
+        self.p2p_wait(self.p2p_start(sends, recvs))
 
 
 class HaloExchange:
@@ -392,6 +424,11 @@ class HaloExchange:
     def run_many(self, jobs) -> None:
         """Several exchanges [(kind, src, dst), ...] in ONE batch of P2P
         operations (one NCCL group launch instead of one per kind)."""
+        self.comm.p2p_wait(self.start_many(jobs))
+
+    def start_many(self, jobs):
+        """run_many without the final wait: returns the pending works (local
+        copies are done; the remote halves are in flight on NCCL's stream)."""
         rank_of = self.comm.rank_of_part
         remote_s, remote_r = [], []
         sends = {}
@@ -418,7 +455,8 @@ class HaloExchange:
             # process pair shares one slab boundary
             remote_s = [sends[k] for k in sorted(sends)]
             remote_r = [(peer, t) for _, peer, t in sorted(remote_r, key=lambda e: e[0])]
-            self.comm.p2p(remote_s, remote_r)
+            return self.comm.p2p_start(remote_s, remote_r)
+        return []
 
 
 # ---------------------------------------------------------------------------
@@ -440,6 +478,8 @@ class CudaSlab:
         dev = torch.device("cuda", torch.cuda.current_device())
         i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)  # noqa: E731
         self.A_loc = DeviceCsr.from_scipy(b["A_loc"])
+        A_int, brows, A_bnd = split_boundary_rows(b["A_loc"], layout.n_own)
+        self.A_int, self.A_bnd = DeviceCsr.from_scipy(A_int), DeviceCsr.from_scipy(A_bnd)
         self.A_cf_loc = DeviceCsr.from_scipy(b["A_cf_loc"])
         self.A_fc_loc = DeviceCsr.from_scipy(b["A_fc_loc"])
         self.A_ff_own = DeviceCsr.from_scipy(b["A_ff_own"])
@@ -451,6 +491,7 @@ class CudaSlab:
         cm = np.full(layout.ext_cells.size, -1, dtype=np.int32)
         cm[b["own_cells_in_ext"]] = np.arange(layout.n_cells, dtype=np.int32)
         self.cell_map = i32(cm)
+        self.brows = i32(brows)
         self.send = {("f", q): i32(v) for q, v in layout.send_faces.items()}
         self.send.update({("c", q): i32(v) for q, v in layout.send_cells.items()})
         self.rhs = torch.from_numpy(b["rhs"]).to(dev)
@@ -583,6 +624,17 @@ class CudaSlab:
         L.check(self.lib.edfa_spmv(self.ctx, self.A_loc.handle, C.c_void_p(self.zext.data_ptr()),
                                    C.c_void_p(y.data_ptr()), 1.0, 0.0))
 
+    def spmv_interior(self, y):
+        """y = A_loc zext on the rows without halo columns (0 on the others)."""
+        L.check(self.lib.edfa_spmv(self.ctx, self.A_int.handle, C.c_void_p(self.zext.data_ptr()),
+                                   C.c_void_p(y.data_ptr()), 1.0, 0.0))
+
+    def spmv_boundary(self, y):
+        """The rows that read halo values, after the exchange."""
+        if self.brows.numel():
+            L.check(self.lib.edfa_spmv_rows(self.ctx, self.A_bnd.handle, C.c_void_p(self.brows.data_ptr()),
+                                            C.c_void_p(self.zext.data_ptr()), C.c_void_p(y.data_ptr())))
+
     def apply_faces(self, r):
         """t_f = -(L L^T)^-1 r_f into tf_ext[:nfo]."""
         nfo = self.layout.n_faces
@@ -686,13 +738,17 @@ class SlabOperator:
     def matvec_zext(self, ws):
         """w = A zext per part (exchanges the halo of zext's own part)."""
         with self.timer("halo"):
-            self.halo.run_many([
+            works = self.halo.start_many([
                 ("f", [p.zext[:p.layout.n_faces] for p in self.parts],
                  [p.zext[p.layout.n_own:p.layout.n_own + p.layout.halo_faces.size] for p in self.parts]),
                 ("c", [p.zext[p.layout.n_faces:p.layout.n_own] for p in self.parts],
                  [p.zext[p.layout.n_own + p.layout.halo_faces.size:] for p in self.parts])])
-        for p, w in zip(self.parts, ws):
-            p.spmv_ext(w)
+        for p, w in zip(self.parts, ws):          # interior rows overlap the exchange
+            p.spmv_interior(w)
+        with self.timer("halo"):
+            self.comm.p2p_wait(works)
+        for p, w in zip(self.parts, ws):          # rows that read halo values
+            p.spmv_boundary(w)
 
     def allsum(self, partials):
         t = partials[0]

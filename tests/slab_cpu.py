@@ -136,6 +136,17 @@ class CpuSlab:
     def spmv_ext(self, y):
         y.copy_(torch.from_numpy(self.A_loc @ self.zext.numpy()))
 
+    def spmv_interior(self, y):
+        from paper_2009_13916_b200.parallel import split_boundary_rows
+        if not hasattr(self, "_split"):
+            self._split = split_boundary_rows(self.A_loc, self.layout.n_own)
+        y.copy_(torch.from_numpy(self._split[0] @ self.zext.numpy()))
+
+    def spmv_boundary(self, y):
+        _, rows, A_b = self._split
+        if rows.size:
+            y[torch.from_numpy(rows)] = torch.from_numpy(A_b @ self.zext.numpy())
+
     def apply_faces(self, r):
         nfo = self.layout.n_faces
         self.tf_ext[:nfo] = torch.from_numpy(-self.ic.apply(r[:nfo].numpy()))
