@@ -196,6 +196,7 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
     h->c.opt.trsv_levels = env_opt("EDFA_OPT_TRSV_LEVELS", 0);
     h->c.opt.ilu_levels = env_opt("EDFA_OPT_ILU_LEVELS", 0);
     h->c.opt.tile_direct = env_opt("EDFA_OPT_TILE_DIRECT", -1);
+    h->c.opt.ilu_wf = env_opt("EDFA_OPT_ILU_WF", 0);
     h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
     EDFA_CUDA(cudaMemsetAsync(h->c.d_scalar_i, 0, 64 * sizeof(int), h->c.stream));   // [60]: reduction ticket
     h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));
@@ -229,6 +230,7 @@ int edfa_ctx_set_option(edfa_ctx* ctx, const char* name, int value) {
     else if (n == "trsv_levels") o.trsv_levels = value;
     else if (n == "ilu_levels") o.ilu_levels = value;
     else if (n == "tile_direct") o.tile_direct = value;
+    else if (n == "ilu_wf") o.ilu_wf = value;
     else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
     API_END
 }
@@ -243,6 +245,7 @@ int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value) {
     else if (n == "trsv_levels") *value = o.trsv_levels;
     else if (n == "ilu_levels") *value = o.ilu_levels;
     else if (n == "tile_direct") *value = o.tile_direct;
+    else if (n == "ilu_wf") *value = o.ilu_wf;
     else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
     API_END
 }

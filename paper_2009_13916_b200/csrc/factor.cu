@@ -435,6 +435,7 @@ int coop_grid(K kern, int threads, size_t smem, int cap = 2) {
 }  // namespace
 
 void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels);
+bool use_wf_layout(Ctx* c, int n, const int* dims);
 
 void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f, bool no_fill) {
     require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
@@ -520,7 +521,7 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
                       (int64_t)dims[0] * dims[1] * dims[2] == n;
     bool sync_free = false;
     DevBuf<int> ord;
-    if (grid) {
+    if (grid && !use_wf_layout(c, n, dims)) {
         PhaseTimer pt(c, "ilu0.wavefront_order");
         int* bad = c->d_scalar_i + 28;
         EDFA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
@@ -605,6 +606,15 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
     ilu_plans(c, f, dims, have_levels);
 }
 
+// the wavefront-packed layout pays when levels are wide: decided from the grid
+// shape before any plan exists (levels of an axial stencil = nx+ny+nz-2), and
+// re-checked against the real level count in ilu_plans
+bool use_wf_layout(Ctx* c, int n, const int* dims) {
+    if (c->opt.ilu_wf >= 0) return c->opt.ilu_wf == 1 && n > 0;
+    if (!dims || dims[0] <= 0) return false;
+    return (int64_t)n >= 8192ll * (dims[0] + dims[1] + dims[2]);
+}
+
 // triangular-solve plans of an ILU factor (f.LU strict parts + f.udiag);
 // have_fwd_levels: f.fwd already holds the level plan of L's pattern
 void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
@@ -612,6 +622,18 @@ void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
     Csr Lv, Uv;
     select_part(c, f.LU, 0, 1.0, true, Lv);
     select_part(c, f.LU, 1, 1.0, true, Uv);
+    // wide dependency levels (e.g. 256^3: 766 levels of up to 49k rows): both
+    // solves wavefront-packed on the slot layout of L's level plan
+    if (use_wf_layout(c, n, dims)) {
+        if (!have_fwd_levels) build_plan(c, Lv, nullptr, true, false, f.fwd, /*allow_chain=*/false);
+        if ((int64_t)n >= (c->opt.ilu_wf == 1 ? 0 : 4096ll * f.fwd.n_levels)) {
+            plan_values(c, Lv, nullptr, f.fwd);
+            if (build_wf_plans(c, Lv, Uv, f.udiag.p, f.fwd, f.bwd)) return;
+            build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
+            return;
+        }
+        have_fwd_levels = true;
+    }
     // cell-grid factors: tile-DAG solves; otherwise level-ordered plans
     if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
         f.fwd.is_tile = true;

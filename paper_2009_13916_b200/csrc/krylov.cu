@@ -666,6 +666,7 @@ struct Blas {
 // ---------------------------------------------------------------- apply
 struct ApplyWS {
     DevBuf<double> a_f, t_f, u_c, c_c;
+    DevBuf<double> u_s, c_s, y_s;   // slot-order cell vectors of the wavefront-packed ILU solves
 };
 
 static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2,
@@ -675,7 +676,16 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
         ws.a_f.reset(c, nf);
         ws.t_f.reset(c, nf);
     }
-    if (!ws.u_c.p && nc) {
+    const IluFactor& il = s2->ilu;
+    const bool wf = nc && il.fwd.is_wf && il.bwd.is_wf;
+    if (wf && !ws.u_s.p) {
+        const int ns = il.fwd.n_slots;
+        ws.u_s.reset(c, ns);
+        ws.c_s.reset(c, ns);
+        ws.y_s.reset(c, ns);
+        fill_bits(c, ws.c_s.p, ns, SENTINEL_BITS);   // kept SENTINEL between applies (U resets what it reads)
+    }
+    if (!wf && !ws.u_c.p && nc) {
         ws.u_c.reset(c, nc);
         ws.c_c.reset(c, nc);
         fill_bits(c, ws.c_c.p, nc, SENTINEL_BITS);   // kept SENTINEL between applies (tile path)
@@ -685,7 +695,6 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     double* y_f = y;
     double* y_c = y + nf;
     const IcFactor& ic = s1->ic;
-    const IluFactor& il = s2->ilu;
     // (L L^T)^{-1}: one fused chain kernel when the factor is chain-structured
     const bool pair = ic.fwd.is_chain && ic.bwd.is_chain && c->opt.ic_pair;
     if (!pair || !run_chain_pair(c, ic.fwd.chain, r_f, -1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_pair")) {
@@ -693,7 +702,18 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
         run_plan(c, ic.bwd, ws.a_f.p, 1.0, ws.t_f.p, nullptr, nullptr, "trsv_ic_LT");
     }
     const bool fuse = nc && il.fwd.is_tile && il.bwd.is_tile && c->opt.fill_fusion;
-    if (nc) {
+    if (wf) {
+        // cell block in the factor's slot order: u_s = r_c - A_cf t_f gathered by the
+        // row-permuted A_cf, L and U on slots, y_c scattered by the U solve, A_fc
+        // with slot columns
+        wf_system_copies(c, sys, il.fwd, s2->wfsys);
+        wf_spmv_acf(c, sys, il.fwd, s2->wfsys, ws.t_f.p, r_c, ws.u_s.p);
+        run_wf(c, il.fwd, ws.u_s.p, true, 1.0, ws.c_s.p, false, nullptr, nullptr, nullptr, nullptr, ws.y_s.p,
+               "trsv_ilu_L");
+        run_wf(c, il.bwd, ws.c_s.p, true, 1.0, ws.y_s.p, false, y_c, nullptr, nullptr, ws.c_s.p, nullptr,
+               "trsv_ilu_U");
+        spmv_sell_cols(c, sys->sAfc, s2->wfsys.afc_col.p, ws.y_s.p, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
+    } else if (nc) {
         EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
         spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
         if (fuse) {

@@ -112,6 +112,21 @@ struct TriPlan {
     // [done[0..n_levels), ticket, finished]; self-resetting at kernel end
     DevBuf<int32_t> sync;
     DevBuf<int32_t> ticket;     // unused (kept for ABI of older plans)
+    // wavefront-packed solves (wf.cu): col holds dependency SLOTS, vectors live in slot order
+    bool is_wf = false, wf_reverse = false;
+    const int32_t* wf_perm = nullptr;   // the shared slot -> row map (the forward plan's perm)
+    int32_t wf_slices = 0;
+    DevBuf<int32_t> wf_pos;             // row -> slot (forward plan only)
+    DevBuf<unsigned> wf_ticket;
+    unsigned wf_ticket_base = 0;        // tickets wrap modulo 2^32
+};
+// system blocks on a factor's slot layout (built on the first apply with that system)
+struct WfSystem {
+    const void* sys = nullptr;
+    DevBuf<int64_t> acf_sptr;           // A_cf with rows = slots (SELL-32)
+    DevBuf<int32_t> acf_col;
+    DevBuf<double> acf_val;
+    DevBuf<int32_t> afc_col;            // A_fc's SELL columns -> slots
 };
 // deps: row i -> (j, coef) with x_i = (alpha*b_i - sum coef*x_j) * dinv_i;
 // reverse = deps point to higher rows (backward substitution).  diag may be
@@ -119,6 +134,16 @@ struct TriPlan {
 void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& plan,
                 bool allow_chain = true);
 void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& plan);
+// SELL-32 storage of deps' rows on a given slot layout (perm: slot -> row, -1 pad)
+void sell_on_layout(Ctx* c, const int32_t* perm, int n_slices, const Csr& deps, const double* diag, bool unit,
+                    DevBuf<int64_t>& slice_ptr, DevBuf<int32_t>& col, DevBuf<double>& val, DevBuf<double>& dinv,
+                    int64_t& n_stored, int32_t& max_w);
+// wavefront-packed L / U solves on one slot layout (wf.cu)
+bool build_wf_plans(Ctx* c, const Csr& Lv, const Csr& Uv, const double* udiag, TriPlan& fwd, TriPlan& bwd);
+void run_wf(Ctx* c, const TriPlan& p, const double* b, bool b_slots, double alpha, double* xs, bool fill_xs,
+            double* x_nat, const double* add, double* out2, double* b_sent, double* pre_sent, const char* name);
+void run_wf_natural(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add,
+                    double* out2, const char* name);
 // x = solve(b * alpha); if (add) out2 = x + add (fused epilogue)
 void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x, const double* add, double* out2,
               const char* name);
@@ -185,6 +210,7 @@ struct edfa_stage2 {
     edfa::Ctx* ctx;
     edfa::Csr S;
     edfa::IluFactor ilu;
+    mutable edfa::WfSystem wfsys;   // slot-layout copies of A_cf / A_fc (wavefront-packed solves)
     edfa_csr views[3];
 };
 
@@ -202,6 +228,9 @@ void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynam
 void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, int filt, double schur_drop_tol,
                   int no_fill, edfa_stage2* s2);
 void ensure_transposes(Ctx* c, edfa_system* sys, bool need_AffT);
+void wf_system_copies(Ctx* c, const edfa_system* sys, const TriPlan& fwd, WfSystem& ws);
+void wf_spmv_acf(Ctx* c, const edfa_system* sys, const TriPlan& fwd, const WfSystem& ws, const double* t_f,
+                 const double* r_c, double* u_s);
 void apply_entry(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* r,
                  double* y);
 void inner_apply(Ctx* c, const edfa_stage1* s1, const edfa_stage2* s2, int which, const double* r, double* y);

@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
             const double ik = rsqrt(dkk), lkk = dkk * ik;
             if (li > k) r[k] *= ik;
             if (li == k) { r[k] = lkk; inv_self = ik; }
-            colk[li] = r[k];
+            if (li < SMAX) colk[li] = r[k];
             __syncwarp();
 #pragma unroll
             for (int j = k + 1; j < SMAX; ++j) r[j] = fma(-r[k], colk[j], r[j]);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
         // ---- backward substitution L^T x = y: columns of L from the scratch tile
 #pragma unroll
         for (int j = 0; j < SMAX; ++j)
-            if (j < li) M[li * LD + j] = r[j];
+            if (j < li && li < SMAX) M[li * LD + j] = r[j];
         __syncwarp();
 #pragma unroll
         for (int k = SMAX - 1; k >= 0; --k) {

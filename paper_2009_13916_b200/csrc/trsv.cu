@@ -367,35 +367,42 @@ void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool rev
     check_launch("k_slice_level");
     p.sync.reset(c, (size_t)nl + 2);
     EDFA_CUDA(cudaMemsetAsync(p.sync.p, 0, sizeof(int) * (nl + 2), c->stream));
+    sell_on_layout(c, p.perm.p, n_slices, deps, diag, unit, p.slice_ptr, p.col, p.val, p.dinv, p.n_stored, p.max_w);
+}
+
+// SELL-32 storage of deps' rows on a given slot layout (perm: slot -> row, -1 pad)
+void sell_on_layout(Ctx* c, const int32_t* perm, int n_slices, const Csr& deps, const double* diag, bool unit,
+                    DevBuf<int64_t>& slice_ptr, DevBuf<int32_t>& col, DevBuf<double>& val, DevBuf<double>& dinv,
+                    int64_t& n_stored, int32_t& max_w) {
+    const int64_t slots = (int64_t)n_slices * 32;
     DevBuf<int64_t> wb(c, (size_t)n_slices + 1);
-    k_slice_width<<<ceil_div((int64_t)n_slices * 32, 256), 256, 0, c->stream>>>(p.perm.p, n_slices, deps.ptr.p,
-                                                                               wb.p);
+    k_slice_width<<<ceil_div((int64_t)n_slices * 32, 256), 256, 0, c->stream>>>(perm, n_slices, deps.ptr.p, wb.p);
     check_launch("k_slice_width");
-    p.slice_ptr.reset(c, (size_t)n_slices + 1);
+    slice_ptr.reset(c, (size_t)n_slices + 1);
     {
         size_t b2 = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, b2, wb.p, p.slice_ptr.p, n_slices + 1, c->stream);
+        cub::DeviceScan::ExclusiveSum(nullptr, b2, wb.p, slice_ptr.p, n_slices + 1, c->stream);
         EDFA_CUDA(cudaMemsetAsync(wb.p + n_slices, 0, sizeof(int64_t), c->stream));
-        EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(b2), b2, wb.p, p.slice_ptr.p, n_slices + 1, c->stream));
+        EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(b2), b2, wb.p, slice_ptr.p, n_slices + 1, c->stream));
     }
     int64_t stored = 0;
     int* mw = c->d_scalar_i + 19;
     EDFA_CUDA(cudaMemsetAsync(mw, 0, sizeof(int), c->stream));
-    k_max_width<<<ceil_div(n_slices, 256), 256, 0, c->stream>>>(p.slice_ptr.p, n_slices, mw);
+    k_max_width<<<ceil_div(n_slices, 256), 256, 0, c->stream>>>(slice_ptr.p, n_slices, mw);
     check_launch("k_max_width");
     int hmw = 0;
-    EDFA_CUDA(cudaMemcpyAsync(&stored, p.slice_ptr.p + n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(&stored, slice_ptr.p + n_slices, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaMemcpyAsync(&hmw, mw, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    p.n_stored = stored;
-    p.max_w = hmw;
-    p.col.reset(c, std::max<int64_t>(stored, 1));
-    p.val.reset(c, std::max<int64_t>(stored, 1));
-    p.dinv.reset(c, std::max<int64_t>(slots, 1));
+    n_stored = stored;
+    max_w = hmw;
+    col.reset(c, std::max<int64_t>(stored, 1));
+    val.reset(c, std::max<int64_t>(stored, 1));
+    dinv.reset(c, std::max<int64_t>(slots, 1));
     Prof pr(c, "trsv_plan", 12.0 * stored + 8.0 * slots);
     k_fill_sell<<<ceil_div((int64_t)n_slices * 32, 256), 256, 0, c->stream>>>(
-        p.perm.p, n_slices, view(deps), p.slice_ptr.p, p.col.p, deps.val.p ? p.val.p : nullptr, diag, unit,
-        diag || unit ? p.dinv.p : nullptr);
+        perm, n_slices, view(deps), slice_ptr.p, col.p, deps.val.p ? val.p : nullptr, diag, unit,
+        diag || unit ? dinv.p : nullptr);
     check_launch("k_fill_sell");
 }
 
@@ -535,7 +542,7 @@ __global__ void __launch_bounds__(256) k_trsv_tsf(const int* __restrict__ perm, 
         const int r = perm[s * 32 + lane];
         const int64_t b0 = sptr[s];
         const int w = (int)((sptr[s + 1] - b0) / 32);
-        if (r < 0) continue;
+        const bool act = r >= 0;   // pad lanes run along (their records hold no dependencies)
         int cc[K];
         double vv[K];
 #pragma unroll
@@ -544,19 +551,39 @@ __global__ void __launch_bounds__(256) k_trsv_tsf(const int* __restrict__ perm, 
             cc[u] = in ? __ldg(col + b0 + (int64_t)u * 32 + lane) : -1;
             vv[u] = in ? __ldg(val + b0 + (int64_t)u * 32 + lane) : 0.0;
         }
-        double acc = alpha * __ldg(b + r);
+        double acc = act ? alpha * __ldg(b + r) : 0.0;
         double xv[K];
 #pragma unroll
         for (int u = 0; u < K; ++u) xv[u] = cc[u] >= 0 ? ld_relaxed(x + cc[u]) : 0.0;   // all in flight at once
+        // missing dependencies are re-read as one batch per round (all loads in
+        // flight, one warp vote): polling them one after the other left every
+        // stale value to be re-read in sequence after the last arrival
+        {
+            bool miss = false;
 #pragma unroll
-        for (int u = 0; u < K; ++u) {
+            for (int u = 0; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
             long long spins = 0;
-            while (cc[u] >= 0 && is_sentinel(xv[u])) {
-                if (++spins > SPIN_LIMIT) { atomicExch(err, 3); xv[u] = 0.0; break; }
-                xv[u] = ld_relaxed(x + cc[u]);
+            while (__any_sync(0xffffffffu, miss)) {
+#pragma unroll
+                for (int u = 0; u < K; ++u)
+                    if (cc[u] >= 0 && is_sentinel(xv[u])) xv[u] = ld_relaxed(x + cc[u]);
+                miss = false;
+#pragma unroll
+                for (int u = 0; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
+                if (++spins > SPIN_LIMIT) {
+                    if (miss) {
+                        atomicExch(err, 3);
+#pragma unroll
+                        for (int u = 0; u < K; ++u)
+                            if (is_sentinel(xv[u])) xv[u] = 0.0;
+                    }
+                    break;
+                }
             }
-            acc = fma(-vv[u], xv[u], acc);
         }
+#pragma unroll
+        for (int u = 0; u < K; ++u) acc = fma(-vv[u], xv[u], acc);
+        if (!act) continue;
         const double xr = acc * dinv[s * 32 + lane];
         atomicAdd(reinterpret_cast<unsigned long long*>(x + r),
                   (unsigned long long)__double_as_longlong(publishable(xr)) - SENTINEL_BITS);
@@ -569,6 +596,10 @@ void run_plan(Ctx* c, const TriPlan& p, const double* b, double alpha, double* x
     if (p.n == 0) return;
     if (p.is_chain) {
         run_chain(c, p.chain, b, alpha, x, add, out2, name);
+        return;
+    }
+    if (p.is_wf) {
+        run_wf_natural(c, p, b, alpha, x, add, out2, name);
         return;
     }
     if (p.is_tile) {   // ticket bookkeeping is per plan (serialised on the stream)

@@ -1,7 +1,7 @@
 #!/bin/bash
 # round 2 g: full GPU suite, smoke, default bench (config 5), launch list, step anatomy, dynamic-setup ncu (config 3)
 mkdir -p gpurun_out
-TAG=r02g
+TAG=${1:-r02g}
 bash tools/r02_check.sh $TAG
 EDFA_PHASE_TIMING=1 timeout 600 python tools/step_breakdown.py 5 256 2 > gpurun_out/${TAG}_step_breakdown.log 2>&1
 echo "breakdown rc=$?"; tail -4 gpurun_out/${TAG}_step_breakdown.log
