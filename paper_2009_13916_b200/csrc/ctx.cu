@@ -196,7 +196,7 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
     h->c.opt.trsv_levels = env_opt("EDFA_OPT_TRSV_LEVELS", 0);
     h->c.opt.ilu_levels = env_opt("EDFA_OPT_ILU_LEVELS", 0);
     h->c.opt.tile_direct = env_opt("EDFA_OPT_TILE_DIRECT", -1);
-    h->c.opt.ilu_wf = env_opt("EDFA_OPT_ILU_WF", 0);
+    h->c.opt.ilu_wf = env_opt("EDFA_OPT_ILU_WF", -1);
     h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
     EDFA_CUDA(cudaMemsetAsync(h->c.d_scalar_i, 0, 64 * sizeof(int), h->c.stream));   // [60]: reduction ticket
     h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));

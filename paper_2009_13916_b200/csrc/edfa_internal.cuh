@@ -69,7 +69,7 @@ struct CtxOptions {
     int trsv_levels = 0;    // level-synchronous triangular solves instead of the sync-free ones
     int ilu_levels = 0;     // level-synchronous ILU(0) factorisation instead of the sync-free one
     int tile_direct = -1;   // ILU tile solves: -1 by wavefront width, 0 staged plan (15 warps), 1 direct (7 warps)
-    int ilu_wf = 0;         // ILU solves wavefront-packed on one slot layout: -1 by level width, 0 never, 1 always
+    int ilu_wf = -1;        // ILU solves wavefront-packed on one slot layout: -1 by level width, 0 never, 1 always
 };
 
 struct Ctx {
@@ -249,8 +249,6 @@ void spmv(Ctx* c, const CsrV& A, int64_t nnz, const double* x, double* y, double
           const char* name = "spmv");
 void build_sell(Ctx* c, const Csr& A, Sell& S);
 void spmv_sell(Ctx* c, const Sell& A, const double* x, double* y, double alpha, double beta, const char* name);
-void spmv_sell_cols(Ctx* c, const Sell& A, const int32_t* cols, const double* x, double* y, double alpha, double beta,
-                    const char* name);
 // S = A - H (row-wise sorted merge, exact zeros dropped, optional row filter)
 void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S);
 // row filter (filter_rows, precond.py:138-157): drop |v| < tau*||row||_2 off-diagonal

@@ -339,14 +339,15 @@ __global__ void k_grid_keys(int n, int nx, int ny, int* __restrict__ key, int* _
     row[e] = e;
 }
 // the order is topological iff every strictly-lower entry has key <= the row's
-__global__ void k_grid_order_check(CsrV A, int nx, int ny, int* __restrict__ bad) {
+__global__ void k_grid_order_check(CsrV A, int nx, int ny, int* __restrict__ bad, bool strict = false) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.n_rows) return;
     const int ki = i % nx + (i / nx) % ny + i / (nx * ny);
     for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) {
         const int j = A.idx[e];
         if (j >= i) break;
-        if (j % nx + (j / nx) % ny + j / (nx * ny) > ki) { atomicExch(bad, 1); return; }
+        const int kj = j % nx + (j / nx) % ny + j / (nx * ny);
+        if (strict ? kj >= ki : kj > ki) { atomicExch(bad, 1); return; }
     }
 }
 
@@ -546,6 +547,24 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
     auto level_plan = [&]() {
         PhaseTimer pt(c, "ilu0.level_plan");
         select_part(c, S, 0, 1.0, false, Lpart);
+        if (grid) {
+            // axial stencils: every lower entry lies on an earlier plane i+j+k, so the
+            // planes are a valid layering (no sync-free level computation)
+            int* bad = c->d_scalar_i + 28;
+            EDFA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+            k_grid_order_check<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(S), dims[0], dims[1], bad, true);
+            DevBuf<int> key(c, n), row(c, n);
+            k_grid_keys<<<ceil_div(n, 256), 256, 0, c->stream>>>(n, dims[0], dims[1], key.p, row.p);
+            check_launch("k_grid_keys");
+            int hb = 0;
+            EDFA_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            EDFA_CUDA(cudaStreamSynchronize(c->stream));
+            if (!hb) {
+                build_plan(c, Lpart, nullptr, true, false, f.fwd, /*allow_chain=*/false, key.p,
+                           dims[0] + dims[1] + dims[2] - 2);
+                return;
+            }
+        }
         build_plan(c, Lpart, nullptr, true, false, f.fwd, /*allow_chain=*/false);
     };
     const bool have_levels = !sync_free;
@@ -608,11 +627,14 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
 
 // the wavefront-packed layout pays when levels are wide: decided from the grid
 // shape before any plan exists (levels of an axial stencil = nx+ny+nz-2), and
-// re-checked against the real level count in ilu_plans
+// re-checked against the real level count in ilu_plans.  Measured (config 5
+// generator, per solve): the wf solve costs ~2.1-2.5 us per level (382 / 574 / 766
+// levels at 128^3 / 192^3 / 256^3: 0.80 / 1.23 / 1.89 ms), the tile-DAG solve
+// streams at ~1.75 TB/s (0.40 / 0.98 / 2.23 ms): crossover at ~16k rows per level.
 bool use_wf_layout(Ctx* c, int n, const int* dims) {
     if (c->opt.ilu_wf >= 0) return c->opt.ilu_wf == 1 && n > 0;
     if (!dims || dims[0] <= 0) return false;
-    return (int64_t)n >= 8192ll * (dims[0] + dims[1] + dims[2]);
+    return (int64_t)n >= 16384ll * (dims[0] + dims[1] + dims[2]);
 }
 
 // triangular-solve plans of an ILU factor (f.LU strict parts + f.udiag);
@@ -626,7 +648,7 @@ void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
     // solves wavefront-packed on the slot layout of L's level plan
     if (use_wf_layout(c, n, dims)) {
         if (!have_fwd_levels) build_plan(c, Lv, nullptr, true, false, f.fwd, /*allow_chain=*/false);
-        if ((int64_t)n >= (c->opt.ilu_wf == 1 ? 0 : 4096ll * f.fwd.n_levels)) {
+        if ((int64_t)n >= (c->opt.ilu_wf == 1 ? 0 : 16384ll * f.fwd.n_levels)) {
             plan_values(c, Lv, nullptr, f.fwd);
             if (build_wf_plans(c, Lv, Uv, f.udiag.p, f.fwd, f.bwd)) return;
             build_plan(c, Uv, f.udiag.p, false, true, f.bwd);

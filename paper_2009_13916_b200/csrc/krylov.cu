@@ -666,7 +666,7 @@ struct Blas {
 // ---------------------------------------------------------------- apply
 struct ApplyWS {
     DevBuf<double> a_f, t_f, u_c, c_c;
-    DevBuf<double> u_s, c_s, y_s;   // slot-order cell vectors of the wavefront-packed ILU solves
+    DevBuf<double> c_s, y_s;        // slot-order cell vectors of the wavefront-packed ILU solves
 };
 
 static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2,
@@ -678,9 +678,9 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     }
     const IluFactor& il = s2->ilu;
     const bool wf = nc && il.fwd.is_wf && il.bwd.is_wf;
-    if (wf && !ws.u_s.p) {
+    if (wf && !ws.c_s.p) {
         const int ns = il.fwd.n_slots;
-        ws.u_s.reset(c, ns);
+        ws.u_c.reset(c, nc);
         ws.c_s.reset(c, ns);
         ws.y_s.reset(c, ns);
         fill_bits(c, ws.c_s.p, ns, SENTINEL_BITS);   // kept SENTINEL between applies (U resets what it reads)
@@ -703,16 +703,15 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
     }
     const bool fuse = nc && il.fwd.is_tile && il.bwd.is_tile && c->opt.fill_fusion;
     if (wf) {
-        // cell block in the factor's slot order: u_s = r_c - A_cf t_f gathered by the
-        // row-permuted A_cf, L and U on slots, y_c scattered by the U solve, A_fc
-        // with slot columns
-        wf_system_copies(c, sys, il.fwd, s2->wfsys);
-        wf_spmv_acf(c, sys, il.fwd, s2->wfsys, ws.t_f.p, r_c, ws.u_s.p);
-        run_wf(c, il.fwd, ws.u_s.p, true, 1.0, ws.c_s.p, false, nullptr, nullptr, nullptr, nullptr, ws.y_s.p,
+        // L gathers its right-hand side by row, both solves keep their vectors in the
+        // factor's slot order (c_s, y_s), U scatters y_c back to natural order
+        EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
+        spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");
+        run_wf(c, il.fwd, ws.u_c.p, false, 1.0, ws.c_s.p, false, nullptr, nullptr, nullptr, nullptr, ws.y_s.p,
                "trsv_ilu_L");
         run_wf(c, il.bwd, ws.c_s.p, true, 1.0, ws.y_s.p, false, y_c, nullptr, nullptr, ws.c_s.p, nullptr,
                "trsv_ilu_U");
-        spmv_sell_cols(c, sys->sAfc, s2->wfsys.afc_col.p, ws.y_s.p, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
+        spmv_sell(c, sys->sAfc, y_c, ws.a_f.p, 1.0, 0.0, "spmv_Afc");
     } else if (nc) {
         EDFA_CUDA(cudaMemcpyAsync(ws.u_c.p, r_c, sizeof(double) * nc, cudaMemcpyDeviceToDevice, c->stream));
         spmv_sell(c, sys->sAcf, ws.t_f.p, ws.u_c.p, -1.0, 1.0, "spmv_Acf");

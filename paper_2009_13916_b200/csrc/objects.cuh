@@ -120,19 +120,13 @@ struct TriPlan {
     DevBuf<unsigned> wf_ticket;
     unsigned wf_ticket_base = 0;        // tickets wrap modulo 2^32
 };
-// system blocks on a factor's slot layout (built on the first apply with that system)
-struct WfSystem {
-    const void* sys = nullptr;
-    DevBuf<int64_t> acf_sptr;           // A_cf with rows = slots (SELL-32)
-    DevBuf<int32_t> acf_col;
-    DevBuf<double> acf_val;
-    DevBuf<int32_t> afc_col;            // A_fc's SELL columns -> slots
-};
 // deps: row i -> (j, coef) with x_i = (alpha*b_i - sum coef*x_j) * dinv_i;
 // reverse = deps point to higher rows (backward substitution).  diag may be
 // NULL (values loaded later with plan_values).
+// given_level (optional): a layering of the rows computed by the caller (every
+// dependency in a strictly earlier layer), given_levels layers
 void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& plan,
-                bool allow_chain = true);
+                bool allow_chain = true, const int32_t* given_level = nullptr, int given_levels = 0);
 void plan_values(Ctx* c, const Csr& deps, const double* diag, TriPlan& plan);
 // SELL-32 storage of deps' rows on a given slot layout (perm: slot -> row, -1 pad)
 void sell_on_layout(Ctx* c, const int32_t* perm, int n_slices, const Csr& deps, const double* diag, bool unit,
@@ -210,7 +204,6 @@ struct edfa_stage2 {
     edfa::Ctx* ctx;
     edfa::Csr S;
     edfa::IluFactor ilu;
-    mutable edfa::WfSystem wfsys;   // slot-layout copies of A_cf / A_fc (wavefront-packed solves)
     edfa_csr views[3];
 };
 
@@ -228,9 +221,6 @@ void stage1_build(Ctx* c, edfa_system* sys, const Csr* pattern, const edfa_dynam
 void stage2_build(Ctx* c, const Csr& A_cc, const edfa_stage1* s1, double tau, int filt, double schur_drop_tol,
                   int no_fill, edfa_stage2* s2);
 void ensure_transposes(Ctx* c, edfa_system* sys, bool need_AffT);
-void wf_system_copies(Ctx* c, const edfa_system* sys, const TriPlan& fwd, WfSystem& ws);
-void wf_spmv_acf(Ctx* c, const edfa_system* sys, const TriPlan& fwd, const WfSystem& ws, const double* t_f,
-                 const double* r_c, double* u_s);
 void apply_entry(Ctx* c, const edfa_system* sys, const edfa_stage1* s1, const edfa_stage2* s2, const double* r,
                  double* y);
 void inner_apply(Ctx* c, const edfa_stage1* s1, const edfa_stage2* s2, int which, const double* r, double* y);

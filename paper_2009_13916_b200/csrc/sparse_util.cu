@@ -359,16 +359,6 @@ void spmv_sell(Ctx* c, const Sell& A, const double* x, double* y, double alpha, 
     check_launch("k_spmv_sell");
 }
 
-// same operator with another column array (columns renumbered, e.g. onto a factor's slot layout)
-void spmv_sell_cols(Ctx* c, const Sell& A, const int32_t* cols, const double* x, double* y, double alpha, double beta,
-                    const char* name) {
-    if (A.n_rows == 0) return;
-    Prof pr(c, name, 12.0 * A.nnz + 4.0 * (A.n_rows + 1) + 8.0 * A.n_cols + 8.0 * A.n_rows * (beta != 0.0 ? 2 : 1));
-    k_spmv_sell<<<ceil_div(A.n_rows, 256), 256, 0, c->stream>>>(A.n_rows, A.slice_ptr.p, cols, A.val.p, x, y, alpha,
-                                                               beta);
-    check_launch("k_spmv_sell");
-}
-
 void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S) {
     require(A.n_rows == H.n_rows && A.n_cols == H.n_cols, EDFA_ERR_VALUE, "A_cc and H shapes differ");
     int n = A.n_rows;

@@ -302,7 +302,8 @@ __global__ void k_slice_level(const int* __restrict__ pstart, int nl, int* __res
 }  // namespace
 
 // Build the level-ordered SELL plan for deps (pattern and, optionally, values).
-void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& p, bool allow_chain) {
+void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool reverse, TriPlan& p, bool allow_chain,
+                const int32_t* given_level, int given_levels) {
     const int n = deps.n_rows;
     p.n = n;
     p.unit = unit;
@@ -323,21 +324,29 @@ void build_plan(Ctx* c, const Csr& deps, const double* diag, bool unit, bool rev
         EDFA_CUDA(cudaMemsetAsync(p.slice_ptr.p, 0, sizeof(int64_t), c->stream));
         return;
     }
-    DevBuf<int> level(c, n), rows(c, n), skeys(c, n), srows(c, n);
-    int* scal = c->d_scalar_i + 16;   // [ticket, max_level, err]
-    EDFA_CUDA(cudaMemsetAsync(scal, 0, 3 * sizeof(int), c->stream));
-    {
-        Prof pr(c, "trsv_levels", 4.0 * deps.nnz + 8.0 * n);
-        k_fill_int<<<ceil_div(n, 256), 256, 0, c->stream>>>(level.p, n, LEVEL_UNSET);
-        k_levels<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(deps), reverse, level.p, scal, scal + 1, scal + 2);
-        check_launch("k_levels");
+    DevBuf<int> level_own, rows(c, n), skeys(c, n), srows(c, n);
+    const int* level_p = given_level;
+    int nl = given_levels;
+    if (!given_level) {
+        level_own.reset(c, n);
+        int* scal = c->d_scalar_i + 16;   // [ticket, max_level, err]
+        EDFA_CUDA(cudaMemsetAsync(scal, 0, 3 * sizeof(int), c->stream));
+        {
+            Prof pr(c, "trsv_levels", 4.0 * deps.nnz + 8.0 * n);
+            k_fill_int<<<ceil_div(n, 256), 256, 0, c->stream>>>(level_own.p, n, LEVEL_UNSET);
+            k_levels<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(deps), reverse, level_own.p, scal, scal + 1,
+                                                               scal + 2);
+            check_launch("k_levels");
+        }
+        int hs[3];
+        EDFA_CUDA(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
+        EDFA_CUDA(cudaStreamSynchronize(c->stream));
+        require(hs[2] == 0, EDFA_ERR_CUDA, "level computation did not converge (dependency cycle?)");
+        nl = hs[1] + 1;
+        level_p = level_own.p;
     }
-    int hs[3];
-    EDFA_CUDA(cudaMemcpyAsync(hs, scal, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
-    EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    require(hs[2] == 0, EDFA_ERR_CUDA, "level computation did not converge (dependency cycle?)");
-    int nl = hs[1] + 1;
     p.n_levels = nl;
+    struct { const int* p; } level{level_p};
     // sort rows by level (stable: natural order inside a level)
     k_iota_i<<<ceil_div(n, 256), 256, 0, c->stream>>>(rows.p, n);
     int bits = 1;

@@ -4,8 +4,8 @@
 //
 // Both solves run on ONE slot layout: rows sorted by the dependency level of
 // L (natural order inside a level), every level padded to whole warps.  The
-// right-hand side, the intermediate and the solution live in slot order, and
-// the SELL-32 coefficient records store dependency SLOTS, so
+// intermediate and the solution live in slot order, and the SELL-32
+// coefficient records store dependency SLOTS, so
 //   * the plan is streamed once, fully coalesced;
 //   * the rows of a level that sit next to each other in a slice depend on
 //     rows that sit next to each other in an earlier level (axial stencils),
@@ -47,12 +47,6 @@ __global__ void k_wf_remap(int32_t* __restrict__ col, int64_t n, const int32_t* 
         if (c >= 0) col[q] = pos[c];
     }
 }
-__global__ void k_wf_remap_to(const int32_t* __restrict__ col, int64_t n, const int32_t* __restrict__ pos,
-                              int32_t* __restrict__ out) {
-    int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (; q < n; q += (int64_t)gridDim.x * blockDim.x) out[q] = pos[col[q]];
-}
-
 struct WfArgs {
     const int32_t* perm;
     const int64_t* sptr;
@@ -159,24 +153,6 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
     }
 }
 
-// y[slot] = g[perm[slot]] - (A x)[slot]   (A stored on the slot layout; pad slots -> 0)
-__global__ void __launch_bounds__(256) k_spmv_slots(int n_slots, const int64_t* __restrict__ sp,
-                                                    const int32_t* __restrict__ col, const double* __restrict__ val,
-                                                    const double* __restrict__ x, const int32_t* __restrict__ perm,
-                                                    const double* __restrict__ g, double* __restrict__ y) {
-    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= n_slots) return;
-    const int s = slot >> 5, lane = slot & 31;
-    const int r = perm[slot];
-    const int64_t e = sp[s + 1];
-    double acc = 0.0;
-    for (int64_t q = sp[s] + lane; q < e; q += 32) {
-        const int c = col[q];
-        if (c >= 0) acc = fma(val[q], __ldg(x + c), acc);
-    }
-    y[slot] = r >= 0 ? __ldg(g + r) - acc : 0.0;
-}
-
 template <int K>
 void launch_wf(Ctx* c, const TriPlan& p, WfArgs& a) {
     static int grid = 0;
@@ -265,33 +241,6 @@ void run_wf_natural(Ctx* c, const TriPlan& p, const double* b, double alpha, dou
                     double* out2, const char* name) {
     DevBuf<double> xs(c, p.n_slots);
     run_wf(c, p, b, false, alpha, xs.p, true, x, add, out2, nullptr, nullptr, name);
-}
-
-// system blocks on the slot layout: A_cf with rows = slots, A_fc's SELL columns -> slots
-void wf_system_copies(Ctx* c, const edfa_system* sys, const TriPlan& fwd, WfSystem& ws) {
-    if (ws.sys == sys) return;
-    const int n_slices = fwd.wf_slices;
-    DevBuf<double> dinv_unused;
-    int64_t stored = 0;
-    int32_t mw = 0;
-    sell_on_layout(c, fwd.wf_perm, n_slices, *sys->A_cf, nullptr, false, ws.acf_sptr, ws.acf_col, ws.acf_val,
-                   dinv_unused, stored, mw);
-    ws.afc_col.reset(c, std::max<int64_t>(sys->sAfc.stored, 1));
-    if (sys->sAfc.stored)
-        k_wf_remap_to<<<std::min<int64_t>(ceil_div(sys->sAfc.stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
-            sys->sAfc.col.p, sys->sAfc.stored, fwd.wf_pos.p, ws.afc_col.p);
-    check_launch("k_wf_remap_to");
-    ws.sys = sys;
-}
-
-// u_s[slot] = r_c[perm[slot]] - (A_cf t_f)[perm[slot]]
-void wf_spmv_acf(Ctx* c, const edfa_system* sys, const TriPlan& fwd, const WfSystem& ws, const double* t_f,
-                 const double* r_c, double* u_s) {
-    const Sell& A = sys->sAcf;
-    Prof pr(c, "spmv_Acf", 12.0 * A.nnz + 4.0 * (A.n_rows + 1) + 8.0 * A.n_cols + 16.0 * A.n_rows);
-    k_spmv_slots<<<ceil_div(fwd.n_slots, 256), 256, 0, c->stream>>>(fwd.n_slots, ws.acf_sptr.p, ws.acf_col.p,
-                                                                    ws.acf_val.p, t_f, fwd.wf_perm, r_c, u_s);
-    check_launch("k_spmv_slots");
 }
 
 }  // namespace edfa
