@@ -15,8 +15,8 @@
 // in later slices).  The solve itself is sync-free: warps take slices from a
 // ticket in topological order, a thread per row polls its dependencies on the
 // SENTINEL-prefilled slot vector (a stored value is its own ready flag).
-// The row arithmetic is the level solver's (bias first, entries in stored
-// order), so results equal k_trsv_ls / k_trsv_tsf bit for bit.
+// A row is summed bias first, then its records in stored order (sorted by
+// dependency level, oldest first): fixed per plan, so solves are reproducible.
 #include "dev_util.cuh"
 #include "edfa_internal.cuh"
 #include "objects.cuh"
@@ -68,6 +68,17 @@ struct WfArgs {
     int* err;
 };
 
+// Per-row records are sorted so that the dependencies of the nearest level
+// come LAST (k_wf_sort_rows) and are loaded right-aligned into the register
+// arrays: slots [0, K-NEAR) hold older levels, [K-NEAR, K) the nearest ones.
+//   phase 1: the older dependencies -- nearly always present already; warps
+//     that run several levels ahead of the frontier wait here with a back-off,
+//     so they do not flood the L2 with polls;
+//   phase 2: the nearest NEAR dependencies, polled tightly as one batch; after
+//     the last arrival only NEAR FMAs and the publish remain.
+// The summation order is the stored order (bias first), fixed per plan.
+constexpr int WF_NEAR = 3;
+
 template <int K, bool REV>
 __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
     const int lane = threadIdx.x & 31;
@@ -82,55 +93,26 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
         const int r = a.perm[slot];
         const int64_t b0 = a.sptr[s];
         const int w = (int)((a.sptr[s + 1] - b0) / 32);
+        const int skip = w > K ? w - K : 0;            // oldest records beyond the register arrays
+        const int off = K - (w - skip);                // right alignment: record k sits in register k + off
         int cc[K];
         double vv[K];
 #pragma unroll
         for (int u = 0; u < K; ++u) {
-            const bool in = u < w;
-            cc[u] = in ? __ldg(a.col + b0 + (int64_t)u * 32 + lane) : -1;
-            vv[u] = in ? __ldg(a.val + b0 + (int64_t)u * 32 + lane) : 0.0;
+            const bool in = u >= off;
+            const int64_t q = b0 + (int64_t)(u - off + skip) * 32 + lane;
+            cc[u] = in ? __ldg(a.col + q) : -1;
+            vv[u] = in ? __ldg(a.val + q) : 0.0;
         }
-        double bias = 0.0;
-        if (r >= 0) bias = a.alpha * (a.b_slots ? a.b[slot] : __ldg(a.b + r));
+        double acc = 0.0;
+        if (r >= 0) acc = a.alpha * (a.b_slots ? a.b[slot] : __ldg(a.b + r));
         const double di = a.dinv ? a.dinv[slot] : 1.0;
         if (a.b_sent) a.b_sent[slot] = sent;
         if (a.pre_sent) a.pre_sent[slot] = sent;
         double xv[K];
 #pragma unroll
         for (int u = 0; u < K; ++u) xv[u] = cc[u] >= 0 ? ld_relaxed(a.xs + cc[u]) : 0.0;   // all in flight at once
-        // dependencies still missing are re-read as ONE batch per round (all loads
-        // in flight together, one warp vote): once the previous level is complete
-        // a single L2 round trip finishes the row.  Polling them one after the
-        // other left up to 8 stale values to re-read in sequence after the last
-        // arrival (measured: 9 us per level instead of ~1.5 us at 256^3).
-        {
-            bool miss = false;
-#pragma unroll
-            for (int u = 0; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
-            long long spins = 0;
-            while (__any_sync(0xffffffffu, miss)) {
-#pragma unroll
-                for (int u = 0; u < K; ++u)
-                    if (cc[u] >= 0 && is_sentinel(xv[u])) xv[u] = ld_relaxed(a.xs + cc[u]);
-                miss = false;
-#pragma unroll
-                for (int u = 0; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
-                if (++spins > SPIN_LIMIT) {
-                    if (miss) {
-                        atomicExch(a.err, 3);
-#pragma unroll
-                        for (int u = 0; u < K; ++u)
-                            if (is_sentinel(xv[u])) xv[u] = 0.0;
-                    }
-                    break;
-                }
-            }
-        }
-        double acc = bias;
-#pragma unroll
-        for (int u = 0; u < K; ++u) acc = fma(-vv[u], xv[u], acc);
-        // rows wider than K (never for the instantiated widths' plans)
-        for (int k = K; k < w; ++k) {
+        for (int k = 0; k < skip; ++k) {               // rows wider than K: oldest records first
             const int c = __ldg(a.col + b0 + (int64_t)k * 32 + lane);
             if (c < 0) continue;
             const double v = __ldg(a.val + b0 + (int64_t)k * 32 + lane);
@@ -138,10 +120,66 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
             long long spins = 0;
             while (is_sentinel(xk)) {
                 if (++spins > SPIN_LIMIT) { atomicExch(a.err, 3); xk = 0.0; break; }
+                __nanosleep(100);
                 xk = ld_relaxed(a.xs + c);
             }
             acc = fma(-v, xk, acc);
         }
+        // ---- phase 1: older levels
+        {
+            bool miss = false;
+#pragma unroll
+            for (int u = 0; u < K - WF_NEAR; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
+            long long spins = 0;
+            unsigned ns = 64;
+            while (__any_sync(0xffffffffu, miss)) {
+                __nanosleep(ns);
+                if (ns < 512) ns <<= 1;
+#pragma unroll
+                for (int u = 0; u < K - WF_NEAR; ++u)
+                    if (cc[u] >= 0 && is_sentinel(xv[u])) xv[u] = ld_relaxed(a.xs + cc[u]);
+                miss = false;
+#pragma unroll
+                for (int u = 0; u < K - WF_NEAR; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
+                if (++spins > SPIN_LIMIT) {
+                    if (miss) {
+                        atomicExch(a.err, 3);
+#pragma unroll
+                        for (int u = 0; u < K - WF_NEAR; ++u)
+                            if (is_sentinel(xv[u])) xv[u] = 0.0;
+                    }
+                    break;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < K - WF_NEAR; ++u) acc = fma(-vv[u], xv[u], acc);
+        // ---- phase 2: the nearest level
+        {
+            bool miss = false;
+#pragma unroll
+            for (int u = K - WF_NEAR; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
+            long long spins = 0;
+            while (__any_sync(0xffffffffu, miss)) {
+#pragma unroll
+                for (int u = K - WF_NEAR; u < K; ++u)
+                    if (cc[u] >= 0 && is_sentinel(xv[u])) xv[u] = ld_relaxed(a.xs + cc[u]);
+                miss = false;
+#pragma unroll
+                for (int u = K - WF_NEAR; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
+                if (++spins > SPIN_LIMIT) {
+                    if (miss) {
+                        atomicExch(a.err, 3);
+#pragma unroll
+                        for (int u = K - WF_NEAR; u < K; ++u)
+                            if (is_sentinel(xv[u])) xv[u] = 0.0;
+                    }
+                    break;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = K - WF_NEAR; u < K; ++u) acc = fma(-vv[u], xv[u], acc);
         if (r >= 0) {
             const double xr = acc * di;
             // fire-and-forget reduction at L2: SENTINEL + (x - SENTINEL)
@@ -150,6 +188,36 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
             if (a.x_nat) a.x_nat[r] = xr;
             if (a.out2) a.out2[r] = xr + a.add[r];
         }
+    }
+}
+
+// Sort every row's records by dependency slot -- ascending for L (older levels
+// first), descending for U (run in reverse: larger slots are older) -- pads (-1)
+// in front, so the nearest level's dependencies are the last records of the row.
+__global__ void k_wf_sort_rows(const int64_t* __restrict__ sptr, int n_slices, int32_t* __restrict__ col,
+                               double* __restrict__ val, bool descending) {
+    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s = slot >> 5, lane = slot & 31;
+    if (s >= n_slices) return;
+    const int64_t b0 = sptr[s];
+    const int w = (int)((sptr[s + 1] - b0) / 32);
+    // insertion sort in place (w is small; one-time plan work)
+    for (int i = 1; i < w; ++i) {
+        const int ci = col[b0 + (int64_t)i * 32 + lane];
+        const double vi = val[b0 + (int64_t)i * 32 + lane];
+        // key: pads first, then by slot in the requested direction
+        auto before = [&](int x, int y) {   // x sorts before y
+            if (x < 0 || y < 0) return x < 0 && y >= 0;
+            return descending ? x > y : x < y;
+        };
+        int j = i - 1;
+        while (j >= 0 && before(ci, col[b0 + (int64_t)j * 32 + lane])) {
+            col[b0 + (int64_t)(j + 1) * 32 + lane] = col[b0 + (int64_t)j * 32 + lane];
+            val[b0 + (int64_t)(j + 1) * 32 + lane] = val[b0 + (int64_t)j * 32 + lane];
+            --j;
+        }
+        col[b0 + (int64_t)(j + 1) * 32 + lane] = ci;
+        val[b0 + (int64_t)(j + 1) * 32 + lane] = vi;
     }
 }
 
@@ -193,6 +261,7 @@ bool build_wf_plans(Ctx* c, const Csr& Lv, const Csr& Uv, const double* udiag, T
     // L: the level plan's records, dependency columns -> slots
     k_wf_remap<<<std::min<int64_t>(ceil_div(fwd.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
         fwd.col.p, fwd.n_stored, pos.p);
+    k_wf_sort_rows<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(fwd.slice_ptr.p, n_slices, fwd.col.p, fwd.val.p, false);
     fwd.is_wf = true;
     fwd.wf_reverse = false;
     fwd.wf_perm = fwd.perm.p;
@@ -207,6 +276,7 @@ bool build_wf_plans(Ctx* c, const Csr& Lv, const Csr& Uv, const double* udiag, T
                    bwd.max_w);
     k_wf_remap<<<std::min<int64_t>(ceil_div(bwd.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
         bwd.col.p, bwd.n_stored, pos.p);
+    k_wf_sort_rows<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(bwd.slice_ptr.p, n_slices, bwd.col.p, bwd.val.p, true);
     check_launch("k_wf_remap");
     bwd.is_wf = true;
     bwd.wf_reverse = true;

@@ -615,8 +615,8 @@ def test_direct_tile_solve_equals_staged(edfa, idx, n):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("idx,n", [(2, 24), (1, 16), (5, 20)])
-def test_wavefront_packed_ilu_solves_equal_level_solves(edfa, idx, n):
+@pytest.mark.parametrize("idx,n,proto", [(2, 24, None), (1, 16, None), (5, 20, None), (2, 16, "B"), (2, 12, "D")])
+def test_wavefront_packed_ilu_solves_equal_level_solves(edfa, idx, n, proto):
     """ILU solves on the wavefront-packed slot layout (wf.cu: vectors in level
     order, dependency slots, U on L's layout in reverse) perform the level
     solvers' row arithmetic: the Schur inner apply matches scipy's triangular
@@ -629,7 +629,8 @@ def test_wavefront_packed_ilu_solves_equal_level_solves(edfa, idx, n):
     s = case.system
     p = case.precond
     ds = edfa.DeviceSystem.from_host(s)
-    pats = edfa.patterns_for(ds, p["pattern"], p.get("prototype", "A"))
+    pats = (edfa.patterns_for(ds, "static", proto) if proto else
+            edfa.patterns_for(ds, p["pattern"], p.get("prototype", "A")))   # B / D: Schur rows wider than 20 / 32
     r = np.random.default_rng(17).standard_normal(s.n_unknowns)
     out = {}
     for wf in (0, 1):

@@ -1,6 +1,6 @@
 #!/bin/bash
-# round 2: full ncu captures of the hot kernels on the config-5 (256^3) step and the setup kernels on config 2
-# usage: tools/r02_ncu.sh TAG "regex1 regex2 ..." [config]
+# full ncu captures of the hot kernels on the config-5 (256^3) step and the setup kernels on config 2
+# usage: tools/ncu_kernels.sh TAG "regex1 regex2 ..." [config]
 mkdir -p gpurun_out
 TAG=$1; KS=$2; CFG=${3:-5}
 for k in $KS; do
