@@ -45,9 +45,9 @@ sys.path.insert(0, str(ROOT))
 METRIC = "EDFA setup+GMRES solve throughput per system"
 UNIT = "MDOF/s"
 DEFAULT_N = {1: 16, 2: 64, 3: 128, 4: None, 5: 256}
-# GMRES(50) iterations of config 5 at 256^3 on the GPU (profiles/r02_bench_config5.json);
+# GMRES(50) iterations of config 5 at 256^3 on the GPU (profiles/r02n_bench.json);
 # the CPU arm's extrapolation uses it (the MGS oracle matched the GPU count at 64^3: 84 = 84)
-CONFIG5_ITERS = 381
+CONFIG5_ITERS = 382
 
 
 def metric_of(k):
@@ -291,6 +291,20 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def kernel_groups(prof):
+    """Profile records by kernel: the forward and backward ILU solves are one
+    kernel (k_wf / k_tile_flow run in the two directions), every other record
+    is one kernel."""
+    out = {}
+    for k, v in prof.items():
+        g = "trsv_ilu" if k.startswith("trsv_ilu") else k
+        o = out.setdefault(g, {"ms": 0.0, "bytes": 0.0, "launches": 0})
+        o["ms"] += v["ms"]
+        o["bytes"] += v["bytes"]
+        o["launches"] += v["launches"]
+    return out
+
+
 # ---------------------------------------------------------------- algorithmic bytes (SURVEY.md §8(d))
 def csr_b(nnz, rows):
     return 12.0 * nnz + 4.0 * (rows + 1)
@@ -439,7 +453,7 @@ def run_edfa(args):
     prof_full = profile_report(lib, c)
     lib.edfa_ctx_profile(c, 0)
     last = None
-    dom_name = max(prof_full.items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
+    dom_name = max(kernel_groups(prof_full).items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
 
     # ---- device-resident timed region; CUDA events bracket every launch of
     # the dominant kernel only (cheap enough not to perturb the step)
@@ -500,8 +514,8 @@ def run_edfa(args):
     del A_h, s_pin
 
     # ---- roofline of the dominant kernel (live CUDA events over the timed region)
-    dname, d = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else ("none", {"ms": 0, "bytes": 0,
-                                                                                  "launches": 1})
+    dname, d = max(kernel_groups(prof).items(), key=lambda kv: kv[1]["ms"]) if prof else (
+        "none", {"ms": 0, "bytes": 0, "launches": 1})
     per_launch_ms = d["ms"] / max(d["launches"], 1)
     per_launch_bytes = d["bytes"] / max(d["launches"], 1)
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else 0.0
@@ -512,6 +526,11 @@ def run_edfa(args):
         pass
     tot_full = max(sum(p["ms"] for p in prof_full.values()), 1e-9)
     shares = {k: round(v["ms"] / tot_full, 4) for k, v in sorted(prof_full.items(), key=lambda kv: -kv[1]["ms"])[:10]}
+    # the same figures for the six largest kernels of the step (warm-up step's events)
+    top = [{"kernel": k, "ms_per_step": round(v["ms"], 3), "launches": v["launches"],
+            "achieved": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 else 0.0,
+            "frac": round(v["bytes"] / (v["ms"] / 1e3) / 1e9 / peak, 4) if v["ms"] > 0 else 0.0}
+           for k, v in sorted(kernel_groups(prof_full).items(), key=lambda kv: -kv[1]["ms"])[:6]]
     g = case.meta["inputs"][0]
     line = {
         "metric": metric_of(cfg), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -536,6 +555,7 @@ def run_edfa(args):
                      "launches_per_step": d["launches"] / args.steps,
                      "step_share_of_kernel_time": shares, "kernel_ms_per_step": tot_full,
                      "shares_from": "per-kernel CUDA events of one untimed warm-up step (same workload)"},
+        "roofline_top": top,
         "clocks": clocks,
     }
     if args.profile_json:
@@ -689,7 +709,7 @@ def run_slabs(args):
             prof_full = profile_report(lib, c)
             lib.edfa_ctx_profile(c, 0)
     torch.cuda.synchronize()
-    dom_name = max(prof_full.items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
+    dom_name = max(kernel_groups(prof_full).items(), key=lambda kv: kv[1]["ms"])[0] if prof_full else ""
     lib.edfa_ctx_profile_filter(c, dom_name.encode())
     lib.edfa_ctx_profile(c, 1)
     profile_report(lib, c)

@@ -1,6 +1,6 @@
 """Summarise an ncu launch list (gpu__time_duration + dram bytes per launch).
 
-    python tools/ncu_summary.py LAUNCHES.csv OUT_SUMMARY.txt [OUT_TRAFFIC.json] [header line]
+    python tools/ncu_summary.py LAUNCHES.csv OUT_SUMMARY.txt [OUT_TRAFFIC.json] [header line] [config key]
 
 Writes per-kernel launch counts, summed time, step share and DRAM bytes per
 launch; the optional JSON maps the bench's profiler names of the dominant
@@ -13,15 +13,15 @@ import re
 import sys
 
 # bench profiler name -> ncu kernel name prefix
-PROFILER_NAMES = {"trsv_ilu_L": "k_tile_flow", "trsv_ilu_U": "k_tile_flow", "gs_dots2": "k_dots2",
-                  "gs_axpy2": "k_axpy2", "spmv_A": "k_spmv", "trsv_ic_L": "k_chain_scan",
-                  "trsv_ic_LT": "k_chain_scan"}
+PROFILER_NAMES = {"trsv_ilu": ("k_wf", "k_tile_flow"), "gs_dots2": ("k_dots2",), "gs_axpy2": ("k_axpy2",),
+                  "spmv_A": ("k_spmv_sell",), "trsv_ic_pair": ("k_chain_pair",)}
 
 
 def main():
     src, out = sys.argv[1], sys.argv[2]
     traffic_out = sys.argv[3] if len(sys.argv) > 3 else None
     header = sys.argv[4] if len(sys.argv) > 4 else ""
+    cfg_key = sys.argv[5] if len(sys.argv) > 5 else "config5"
     rows = list(csv.reader(open(src)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
@@ -54,12 +54,19 @@ def main():
                     f"{(b / t if t else 0):8.1f}\n")
     if traffic_out:
         tr = {}
-        for prof, kern in PROFILER_NAMES.items():
-            hit = [(n, b) for k, (n, t, b) in agg.items() if k.startswith(kern)]
+        for prof, kerns in PROFILER_NAMES.items():
+            hit = [(n, b) for k, (n, t, b) in agg.items() if k in kerns]
             if hit:
                 n = sum(x[0] for x in hit)
                 tr[prof] = sum(x[1] for x in hit) / n
-        json.dump(tr, open(traffic_out, "w"), indent=1)
+        try:
+            allcfg = json.load(open(traffic_out))
+            if not all(isinstance(v, dict) for v in allcfg.values()):
+                allcfg = {}
+        except Exception:
+            allcfg = {}
+        allcfg[cfg_key] = tr
+        json.dump(allcfg, open(traffic_out, "w"), indent=1)
     print(open(out).read())
 
 
