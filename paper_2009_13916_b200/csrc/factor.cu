@@ -628,13 +628,14 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
 // the wavefront-packed layout pays when levels are wide: decided from the grid
 // shape before any plan exists (levels of an axial stencil = nx+ny+nz-2), and
 // re-checked against the real level count in ilu_plans.  Measured (config 5
-// generator, per solve): the wf solve costs ~2.1-2.5 us per level (382 / 574 / 766
-// levels at 128^3 / 192^3 / 256^3: 0.80 / 1.23 / 1.89 ms), the tile-DAG solve
-// streams at ~1.75 TB/s (0.40 / 0.98 / 2.23 ms): crossover at ~16k rows per level.
+// generator, per solve): the wf solve costs ~1.1 us per level while levels are
+// narrow and turns bandwidth-bound when they are wide (382 / 574 / 766 levels at
+// 128^3 / 192^3 / 256^3: 0.42 / 0.73 / 1.51 ms), the tile-DAG solve streams at
+// ~1.75 TB/s (0.40 / 0.98 / 2.23 ms): crossover at ~6k rows per level.
 bool use_wf_layout(Ctx* c, int n, const int* dims) {
     if (c->opt.ilu_wf >= 0) return c->opt.ilu_wf == 1 && n > 0;
     if (!dims || dims[0] <= 0) return false;
-    return (int64_t)n >= 16384ll * (dims[0] + dims[1] + dims[2]);
+    return (int64_t)n >= 6144ll * (dims[0] + dims[1] + dims[2]);
 }
 
 // triangular-solve plans of an ILU factor (f.LU strict parts + f.udiag);
@@ -648,7 +649,7 @@ void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
     // solves wavefront-packed on the slot layout of L's level plan
     if (use_wf_layout(c, n, dims)) {
         if (!have_fwd_levels) build_plan(c, Lv, nullptr, true, false, f.fwd, /*allow_chain=*/false);
-        if ((int64_t)n >= (c->opt.ilu_wf == 1 ? 0 : 16384ll * f.fwd.n_levels)) {
+        if ((int64_t)n >= (c->opt.ilu_wf == 1 ? 0 : 6144ll * f.fwd.n_levels)) {
             plan_values(c, Lv, nullptr, f.fwd);
             if (build_wf_plans(c, Lv, Uv, f.udiag.p, f.fwd, f.bwd)) return;
             build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
