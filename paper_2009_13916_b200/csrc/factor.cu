@@ -645,36 +645,45 @@ void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
     Csr Lv, Uv;
     select_part(c, f.LU, 0, 1.0, true, Lv);
     select_part(c, f.LU, 1, 1.0, true, Uv);
-    // wide dependency levels (e.g. 256^3: 766 levels of up to 49k rows): both
-    // solves wavefront-packed on the slot layout of L's level plan
-    if (use_wf_layout(c, n, dims)) {
+    // 1. wide dependency levels on a cell grid (e.g. 256^3: 766 levels of up to 49k
+    //    rows): both solves wavefront-packed on the slot layout of L's level plan;
+    // 2. otherwise cell-grid factors with an axial stencil: tile-DAG solves;
+    // 3. otherwise (general factors, e.g. dynamic patterns on distorted grids:
+    //    thousands of narrow levels): wavefront-packed again -- its hand-off per
+    //    level is the cheapest of the level-ordered solvers.
+    const bool wf_allowed = c->opt.ilu_wf != 0 && !c->opt.trsv_levels;
+    bool want_wf = wf_allowed && use_wf_layout(c, n, dims);
+    auto fwd_levels = [&]() {
         if (!have_fwd_levels) build_plan(c, Lv, nullptr, true, false, f.fwd, /*allow_chain=*/false);
-        if ((int64_t)n >= (c->opt.ilu_wf == 1 ? 0 : 6144ll * f.fwd.n_levels)) {
-            plan_values(c, Lv, nullptr, f.fwd);
-            if (build_wf_plans(c, Lv, Uv, f.udiag.p, f.fwd, f.bwd)) return;
-            build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
-            return;
-        }
         have_fwd_levels = true;
+    };
+    if (want_wf && c->opt.ilu_wf != 1) {
+        fwd_levels();
+        want_wf = (int64_t)n >= 6144ll * f.fwd.n_levels;
     }
-    // cell-grid factors: tile-DAG solves; otherwise level-ordered plans
-    if (dims && build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile)) {
+    bool fwd_tile = false, bwd_tile = false;
+    if (!want_wf && dims) {
+        fwd_tile = build_tile_plan(c, Lv, nullptr, true, false, dims, f.fwd.tile);
+        bwd_tile = build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile);
+    }
+    if (fwd_tile) {
         f.fwd.is_tile = true;
         f.fwd.n = n;
         f.fwd.n_dep = Lv.nnz;
         f.fwd.n_levels = f.fwd.tile.n_tile_levels;
     } else {
-        if (!have_fwd_levels) build_plan(c, Lv, nullptr, true, false, f.fwd, /*allow_chain=*/false);
+        fwd_levels();
         plan_values(c, Lv, nullptr, f.fwd);
     }
-    if (dims && build_tile_plan(c, Uv, f.udiag.p, false, true, dims, f.bwd.tile)) {
+    if (bwd_tile) {
         f.bwd.is_tile = true;
         f.bwd.n = n;
         f.bwd.n_dep = Uv.nnz;
         f.bwd.n_levels = f.bwd.tile.n_tile_levels;
-    } else {
-        build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
+        return;
     }
+    if (!fwd_tile && wf_allowed && n > 0 && build_wf_plans(c, Lv, Uv, f.udiag.p, f.fwd, f.bwd)) return;
+    build_plan(c, Uv, f.udiag.p, false, true, f.bwd);
 }
 
 void ic_export(Ctx* c, IcFactor& f) {

@@ -677,7 +677,7 @@ static void precond_apply(Ctx* c, const edfa_system* sys, const edfa_stage1* s1,
         ws.t_f.reset(c, nf);
     }
     const IluFactor& il = s2->ilu;
-    const bool wf = nc && il.fwd.is_wf && il.bwd.is_wf;
+    const bool wf = nc && il.fwd.is_wf && il.bwd.is_wf && il.bwd.wf_shared;   // else: natural hand-over (run_plan)
     if (wf && !ws.c_s.p) {
         const int ns = il.fwd.n_slots;
         ws.u_c.reset(c, nc);

@@ -114,6 +114,7 @@ struct TriPlan {
     DevBuf<int32_t> ticket;     // unused (kept for ABI of older plans)
     // wavefront-packed solves (wf.cu): col holds dependency SLOTS, vectors live in slot order
     bool is_wf = false, wf_reverse = false;
+    bool wf_shared = false;             // a backward plan on the forward plan's slot layout
     const int32_t* wf_perm = nullptr;   // the shared slot -> row map (the forward plan's perm)
     int32_t wf_slices = 0;
     DevBuf<int32_t> wf_pos;             // row -> slot (forward plan only)

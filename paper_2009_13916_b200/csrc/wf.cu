@@ -78,8 +78,46 @@ struct WfArgs {
 //     the last arrival only NEAR FMAs and the publish remain.
 // The summation order is the stored order (bias first), fixed per plan.
 constexpr int WF_NEAR = 3;
+constexpr int WF_CHUNK = 16;   // records per batch of the older part of rows wider than the register window
 
-template <int K, bool REV>
+// batch poll of missing values (SENTINEL) among x[U0..U1): re-read all of them
+// per round, one warp vote; back_off: sleep between rounds (warps far ahead of
+// the frontier)
+template <int N, int U0, int U1, bool BACKOFF>
+__device__ __forceinline__ void wf_poll(const int (&cc)[N], double (&xv)[N], const double* xs, int* err) {
+    bool miss = false;
+#pragma unroll
+    for (int u = U0; u < U1; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
+    long long spins = 0;
+    unsigned ns = 64;
+    while (__any_sync(0xffffffffu, miss)) {
+        if (BACKOFF) {
+            __nanosleep(ns);
+            if (ns < 512) ns <<= 1;
+        }
+#pragma unroll
+        for (int u = U0; u < U1; ++u)
+            if (cc[u] >= 0 && is_sentinel(xv[u])) xv[u] = ld_relaxed(xs + cc[u]);
+        miss = false;
+#pragma unroll
+        for (int u = U0; u < U1; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
+        if (++spins > SPIN_LIMIT) {
+            if (miss) {
+                atomicExch(err, 3);
+#pragma unroll
+                for (int u = U0; u < U1; ++u)
+                    if (is_sentinel(xv[u])) xv[u] = 0.0;
+            }
+            break;
+        }
+    }
+}
+
+// WIDE: rows may hold more than K records (general factors, e.g. the Schur
+// ILU of dynamic patterns on distorted grids: ~110 dependencies per row);
+// the records in front of the last K are streamed in batches of WF_CHUNK
+// (they belong to old levels and are nearly always present).
+template <int K, bool REV, bool WIDE>
 __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
     const int lane = threadIdx.x & 31;
     const double sent = __longlong_as_double((long long)SENTINEL_BITS);
@@ -93,8 +131,31 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
         const int r = a.perm[slot];
         const int64_t b0 = a.sptr[s];
         const int w = (int)((a.sptr[s + 1] - b0) / 32);
-        const int skip = w > K ? w - K : 0;            // oldest records beyond the register arrays
-        const int off = K - (w - skip);                // right alignment: record k sits in register k + off
+        const int skip = (WIDE && w > K) ? w - K : 0;  // oldest records beyond the register window
+        const int off = K - (w - skip);                // right alignment: record k sits in register k - skip + off
+        double acc = 0.0;
+        if (r >= 0) acc = a.alpha * (a.b_slots ? a.b[slot] : __ldg(a.b + r));
+        const double di = a.dinv ? a.dinv[slot] : 1.0;
+        if (a.b_sent) a.b_sent[slot] = sent;
+        if (a.pre_sent) a.pre_sent[slot] = sent;
+        if (WIDE) {
+            for (int k0 = 0; k0 < skip; k0 += WF_CHUNK) {
+                int c[WF_CHUNK];
+                double v[WF_CHUNK], x[WF_CHUNK];
+#pragma unroll
+                for (int u = 0; u < WF_CHUNK; ++u) {
+                    const bool in = k0 + u < skip;
+                    const int64_t q = b0 + (int64_t)(k0 + u) * 32 + lane;
+                    c[u] = in ? __ldg(a.col + q) : -1;
+                    v[u] = in ? __ldg(a.val + q) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < WF_CHUNK; ++u) x[u] = c[u] >= 0 ? ld_relaxed(a.xs + c[u]) : 0.0;
+                wf_poll<WF_CHUNK, 0, WF_CHUNK, true>(c, x, a.xs, a.err);
+#pragma unroll
+                for (int u = 0; u < WF_CHUNK; ++u) acc = fma(-v[u], x[u], acc);
+            }
+        }
         int cc[K];
         double vv[K];
 #pragma unroll
@@ -104,80 +165,15 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
             cc[u] = in ? __ldg(a.col + q) : -1;
             vv[u] = in ? __ldg(a.val + q) : 0.0;
         }
-        double acc = 0.0;
-        if (r >= 0) acc = a.alpha * (a.b_slots ? a.b[slot] : __ldg(a.b + r));
-        const double di = a.dinv ? a.dinv[slot] : 1.0;
-        if (a.b_sent) a.b_sent[slot] = sent;
-        if (a.pre_sent) a.pre_sent[slot] = sent;
         double xv[K];
 #pragma unroll
         for (int u = 0; u < K; ++u) xv[u] = cc[u] >= 0 ? ld_relaxed(a.xs + cc[u]) : 0.0;   // all in flight at once
-        for (int k = 0; k < skip; ++k) {               // rows wider than K: oldest records first
-            const int c = __ldg(a.col + b0 + (int64_t)k * 32 + lane);
-            if (c < 0) continue;
-            const double v = __ldg(a.val + b0 + (int64_t)k * 32 + lane);
-            double xk = ld_relaxed(a.xs + c);
-            long long spins = 0;
-            while (is_sentinel(xk)) {
-                if (++spins > SPIN_LIMIT) { atomicExch(a.err, 3); xk = 0.0; break; }
-                __nanosleep(100);
-                xk = ld_relaxed(a.xs + c);
-            }
-            acc = fma(-v, xk, acc);
-        }
         // ---- phase 1: older levels
-        {
-            bool miss = false;
-#pragma unroll
-            for (int u = 0; u < K - WF_NEAR; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
-            long long spins = 0;
-            unsigned ns = 64;
-            while (__any_sync(0xffffffffu, miss)) {
-                __nanosleep(ns);
-                if (ns < 512) ns <<= 1;
-#pragma unroll
-                for (int u = 0; u < K - WF_NEAR; ++u)
-                    if (cc[u] >= 0 && is_sentinel(xv[u])) xv[u] = ld_relaxed(a.xs + cc[u]);
-                miss = false;
-#pragma unroll
-                for (int u = 0; u < K - WF_NEAR; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
-                if (++spins > SPIN_LIMIT) {
-                    if (miss) {
-                        atomicExch(a.err, 3);
-#pragma unroll
-                        for (int u = 0; u < K - WF_NEAR; ++u)
-                            if (is_sentinel(xv[u])) xv[u] = 0.0;
-                    }
-                    break;
-                }
-            }
-        }
+        wf_poll<K, 0, K - WF_NEAR, true>(cc, xv, a.xs, a.err);
 #pragma unroll
         for (int u = 0; u < K - WF_NEAR; ++u) acc = fma(-vv[u], xv[u], acc);
         // ---- phase 2: the nearest level
-        {
-            bool miss = false;
-#pragma unroll
-            for (int u = K - WF_NEAR; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
-            long long spins = 0;
-            while (__any_sync(0xffffffffu, miss)) {
-#pragma unroll
-                for (int u = K - WF_NEAR; u < K; ++u)
-                    if (cc[u] >= 0 && is_sentinel(xv[u])) xv[u] = ld_relaxed(a.xs + cc[u]);
-                miss = false;
-#pragma unroll
-                for (int u = K - WF_NEAR; u < K; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
-                if (++spins > SPIN_LIMIT) {
-                    if (miss) {
-                        atomicExch(a.err, 3);
-#pragma unroll
-                        for (int u = K - WF_NEAR; u < K; ++u)
-                            if (is_sentinel(xv[u])) xv[u] = 0.0;
-                    }
-                    break;
-                }
-            }
-        }
+        wf_poll<K, K - WF_NEAR, K, false>(cc, xv, a.xs, a.err);
 #pragma unroll
         for (int u = K - WF_NEAR; u < K; ++u) acc = fma(-vv[u], xv[u], acc);
         if (r >= 0) {
@@ -221,11 +217,11 @@ __global__ void k_wf_sort_rows(const int64_t* __restrict__ sptr, int n_slices, i
     }
 }
 
-template <int K>
+template <int K, bool WIDE>
 void launch_wf(Ctx* c, const TriPlan& p, WfArgs& a) {
     static int grid = 0;
-    auto kf = k_wf<K, false>;
-    auto kr = k_wf<K, true>;
+    auto kf = k_wf<K, false, WIDE>;
+    auto kr = k_wf<K, true, WIDE>;
     if (!grid) {
         int occ = 0;
         EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, 256, 0));
@@ -241,32 +237,53 @@ void launch_wf(Ctx* c, const TriPlan& p, WfArgs& a) {
 
 }  // namespace
 
+// A level plan (natural dependency columns, values loaded) becomes a
+// wavefront-packed plan on its own slot layout: columns -> slots, records
+// sorted oldest level first, slices run in plan order.
+static void wf_from_level_plan(Ctx* c, TriPlan& p) {
+    const int n_slots = p.n_slots, n_slices = n_slots / 32;
+    p.wf_pos.reset(c, std::max(p.n, 1));
+    k_wf_pos<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(p.perm.p, n_slots, p.wf_pos.p);
+    if (p.n_stored > 0)
+        k_wf_remap<<<std::min<int64_t>(ceil_div(p.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
+            p.col.p, p.n_stored, p.wf_pos.p);
+    k_wf_sort_rows<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(p.slice_ptr.p, n_slices, p.col.p, p.val.p, false);
+    check_launch("k_wf_sort_rows");
+    p.is_wf = true;
+    p.wf_reverse = false;
+    p.wf_shared = false;
+    p.wf_perm = p.perm.p;
+    p.wf_slices = n_slices;
+    p.wf_ticket.reset(c, 1);
+    EDFA_CUDA(cudaMemsetAsync(p.wf_ticket.p, 0, sizeof(unsigned), c->stream));
+    p.wf_ticket_base = 0;
+}
+
 // Turn the level plan of L (fwd, built by build_plan on Lv's pattern, values
-// loaded) and U's rows into the shared slot layout.  false: U does not fit
-// L's level order (nothing is modified).
+// loaded) and U's rows into wavefront-packed plans.  When every dependency of
+// U lies in a later slice of L's layout (structurally symmetric factors) U
+// shares that layout and runs its slices in reverse, so the intermediate
+// vector never leaves slot order; otherwise U gets the layout of its own
+// level plan and the two solves hand over in natural order.
 bool build_wf_plans(Ctx* c, const Csr& Lv, const Csr& Uv, const double* udiag, TriPlan& fwd, TriPlan& bwd) {
     const int n = Lv.n_rows;
     if (n == 0 || fwd.n_slots == 0 || fwd.is_chain) return false;
     const int n_slots = fwd.n_slots, n_slices = n_slots / 32;
-    DevBuf<int32_t> pos(c, n);
-    k_wf_pos<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(fwd.perm.p, n_slots, pos.p);
+    wf_from_level_plan(c, fwd);
     int* bad = c->d_scalar_i + 30;
     EDFA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
-    k_wf_check<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(Uv), pos.p, true, bad);
+    k_wf_check<<<ceil_div(n, 256), 256, 0, c->stream>>>(view(Uv), fwd.wf_pos.p, true, bad);
     check_launch("k_wf_check");
     int hb = 0;
     EDFA_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     EDFA_CUDA(cudaStreamSynchronize(c->stream));
-    if (hb) return false;
-    // L: the level plan's records, dependency columns -> slots
-    k_wf_remap<<<std::min<int64_t>(ceil_div(fwd.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
-        fwd.col.p, fwd.n_stored, pos.p);
-    k_wf_sort_rows<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(fwd.slice_ptr.p, n_slices, fwd.col.p, fwd.val.p, false);
-    fwd.is_wf = true;
-    fwd.wf_reverse = false;
-    fwd.wf_perm = fwd.perm.p;
-    fwd.wf_slices = n_slices;
-    // U on the same slots
+    if (hb) {   // U on the layout of its own (reverse) level plan
+        build_plan(c, Uv, udiag, false, true, bwd, /*allow_chain=*/false);
+        if (bwd.n_slots == 0) return true;
+        wf_from_level_plan(c, bwd);
+        return true;
+    }
+    // U on L's slots
     bwd.n = n;
     bwd.unit = false;
     bwd.n_dep = Uv.nnz;
@@ -274,20 +291,19 @@ bool build_wf_plans(Ctx* c, const Csr& Lv, const Csr& Uv, const double* udiag, T
     bwd.n_levels = fwd.n_levels;
     sell_on_layout(c, fwd.perm.p, n_slices, Uv, udiag, false, bwd.slice_ptr, bwd.col, bwd.val, bwd.dinv, bwd.n_stored,
                    bwd.max_w);
-    k_wf_remap<<<std::min<int64_t>(ceil_div(bwd.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
-        bwd.col.p, bwd.n_stored, pos.p);
+    if (bwd.n_stored > 0)
+        k_wf_remap<<<std::min<int64_t>(ceil_div(bwd.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
+            bwd.col.p, bwd.n_stored, fwd.wf_pos.p);
     k_wf_sort_rows<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(bwd.slice_ptr.p, n_slices, bwd.col.p, bwd.val.p, true);
     check_launch("k_wf_remap");
     bwd.is_wf = true;
     bwd.wf_reverse = true;
+    bwd.wf_shared = true;
     bwd.wf_perm = fwd.perm.p;
     bwd.wf_slices = n_slices;
-    for (TriPlan* p : {&fwd, &bwd}) {
-        p->wf_ticket.reset(c, 1);
-        EDFA_CUDA(cudaMemsetAsync(p->wf_ticket.p, 0, sizeof(unsigned), c->stream));
-        p->wf_ticket_base = 0;
-    }
-    fwd.wf_pos = std::move(pos);
+    bwd.wf_ticket.reset(c, 1);
+    EDFA_CUDA(cudaMemsetAsync(bwd.wf_ticket.p, 0, sizeof(unsigned), c->stream));
+    bwd.wf_ticket_base = 0;
     return true;
 }
 
@@ -300,10 +316,10 @@ void run_wf(Ctx* c, const TriPlan& p, const double* b, bool b_slots, double alph
     WfArgs a{p.wf_perm, p.slice_ptr.p, p.col.p, p.val.p, p.unit ? nullptr : p.dinv.p, p.wf_slices,
              p.wf_ticket.p, 0u, b, b_slots ? 1 : 0, alpha, xs, x_nat, add, out2, b_sent, pre_sent, c->d_scalar_i + 8};
     Prof pr(c, name, 12.0 * p.n_dep + 24.0 * p.n + (out2 ? 16.0 * p.n : 0.0));
-    if (p.max_w <= 8) launch_wf<8>(c, p, a);
-    else if (p.max_w <= 12) launch_wf<12>(c, p, a);
-    else if (p.max_w <= 20) launch_wf<20>(c, p, a);
-    else launch_wf<32>(c, p, a);
+    if (p.max_w <= 8) launch_wf<8, false>(c, p, a);
+    else if (p.max_w <= 12) launch_wf<12, false>(c, p, a);
+    else if (p.max_w <= 20) launch_wf<20, false>(c, p, a);
+    else launch_wf<16, true>(c, p, a);
 }
 
 // natural-order entry (run_plan): gathers b, scatters x through a slot-order scratch
