@@ -438,6 +438,16 @@ int coop_grid(K kern, int threads, size_t smem, int cap = 2) {
 void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels);
 bool use_wf_layout(Ctx* c, int n, const int* dims);
 
+// backward plan of an IC factor whose forward plan holds L's values: chains
+// and level plans as before; non-chain factors (distorted grids) get the
+// wavefront-packed solves, L^T on L's slot layout
+static void ic_backward_plan(Ctx* c, IcFactor& f, const Csr& LT) {
+    if (!f.fwd.is_chain && f.n > 0 && c->opt.ilu_wf != 0 && !c->opt.trsv_levels &&
+        build_wf_plans(c, f.Lpat, LT, f.diag.p, f.fwd, f.bwd))
+        return;
+    build_plan(c, LT, f.diag.p, false, true, f.bwd);
+}
+
 void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f, bool no_fill) {
     require(drop_tol >= 0.0, EDFA_ERR_VALUE, "fill_tol must be >= 0");
     const int n = A_ff.n_rows;
@@ -460,7 +470,7 @@ void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f, bool no_f
         plan_values(c, f.Lpat, f.diag.p, f.fwd);
         Csr LT;
         transpose(c, f.Lpat, LT);
-        build_plan(c, LT, f.diag.p, false, true, f.bwd);
+        ic_backward_plan(c, f, LT);
         return;
     }
     int* flags = c->d_scalar_i + 24;   // [shifts, err]
@@ -493,7 +503,7 @@ void ic0_factor(Ctx* c, const Csr& A_ff, double drop_tol, IcFactor& f, bool no_f
     plan_values(c, f.Lpat, f.diag.p, f.fwd);
     Csr LT;
     transpose(c, f.Lpat, LT);
-    build_plan(c, LT, f.diag.p, false, true, f.bwd);
+    ic_backward_plan(c, f, LT);
 }
 
 void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int* dims, bool no_fill) {

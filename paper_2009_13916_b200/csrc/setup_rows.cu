@@ -669,7 +669,10 @@ void setup_rows(Ctx* c, const SetupInput& in, SetupOutput& out) {
             else launch_rows<128, 0, false>(c, a);
         } else {
             require(cand_need <= 4096, EDFA_ERR_UNSUPPORTED, "dynamic candidate support exceeds 4096 entries");
+            // shared memory per warp sets the residency: <64, 1024> fits one 4-warp block per
+            // SM (6 % warps active in ncu, profiles/r02h), <32, 1024> two
             if (smax_need <= 32 && cand_need <= 512) launch_rows<32, 512, true>(c, a);
+            else if (smax_need <= 32 && cand_need <= 1024) launch_rows<32, 1024, true>(c, a);
             else if (smax_need <= 64 && cand_need <= 1024) launch_rows<64, 1024, true>(c, a);
             else if (smax_need <= 64) launch_rows<64, 4096, true>(c, a);
             else launch_rows<128, 4096, true>(c, a);

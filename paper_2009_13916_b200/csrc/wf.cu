@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
         const int skip = (WIDE && w > K) ? w - K : 0;  // oldest records beyond the register window
         const int off = K - (w - skip);                // right alignment: record k sits in register k - skip + off
         double acc = 0.0;
-        if (r >= 0) acc = a.alpha * (a.b_slots ? a.b[slot] : __ldg(a.b + r));
+        if (r >= 0) acc = a.alpha * (a.b_slots ? a.b[slot] : a.b[r]);   // b may alias out2 row-wise: plain load
         const double di = a.dinv ? a.dinv[slot] : 1.0;
         if (a.b_sent) a.b_sent[slot] = sent;
         if (a.pre_sent) a.pre_sent[slot] = sent;
