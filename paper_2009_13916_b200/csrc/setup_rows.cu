@@ -53,14 +53,19 @@ __device__ void report(int* err, int code, int row) {
     atomicMin(err + 1, row);
 }
 
-__device__ void gather_M(const CsrV& A, const int* q, int s, double* M, int ld, int lane) {
-    for (int t = lane; t < s * ld; t += 32) M[t] = 0.0;
+// The s x s block is kept as its lower triangle, packed by rows (entry (i, j),
+// j <= i, at i(i+1)/2 + j): half the shared memory of a padded square tile, so
+// more warps are resident per SM (the dynamic kernel is latency-bound).
+__device__ __forceinline__ int tri(int i, int j) { return ((i * (i + 1)) >> 1) + j; }
+
+__device__ void gather_M(const CsrV& A, const int* q, int s, double* M, int lane) {
+    for (int t = lane; t < tri(s, 0); t += 32) M[t] = 0.0;
     __syncwarp();
     for (int i = lane; i < s; i += 32) {
         int row = q[i];
         for (int e = A.ptr[row]; e < A.ptr[row + 1]; ++e) {
-            int j = bsearch(q, 0, s, A.idx[e]);
-            if (j >= 0) M[i * ld + j] = -A.val[e];
+            int j = bsearch(q, 0, i + 1, A.idx[e]);   // lower triangle only
+            if (j >= 0) M[tri(i, j)] = -A.val[e];
         }
     }
     __syncwarp();
@@ -76,21 +81,21 @@ __device__ void gather_rhs(const CsrV& R, int m, const int* q, int s, double* b,
     __syncwarp();
 }
 
-// in-place lower Cholesky of the s x s block; false on a non-positive pivot
-__device__ bool cholesky(double* M, int s, int ld, int lane) {
+// in-place lower Cholesky of the packed s x s block; false on a non-positive pivot
+__device__ bool cholesky(double* M, int s, int lane) {
     for (int k = 0; k < s; ++k) {
-        double d = M[k * ld + k];
+        double d = M[tri(k, k)];
         if (!(d > 0.0)) return false;
         double l = sqrt(d);
         double il = 1.0 / l;
         __syncwarp();
-        for (int i = k + 1 + lane; i < s; i += 32) M[i * ld + k] *= il;
-        if (lane == 0) M[k * ld + k] = l;
+        for (int i = k + 1 + lane; i < s; i += 32) M[tri(i, k)] *= il;
+        if (lane == 0) M[tri(k, k)] = l;
         __syncwarp();
         for (int i = k + 1 + lane; i < s; i += 32) {
-            double lik = M[i * ld + k];
-            double* Mi = M + i * ld;
-            for (int j = k + 1; j <= i; ++j) Mi[j] = fma(-lik, M[j * ld + k], Mi[j]);
+            double lik = M[tri(i, k)];
+            double* Mi = M + tri(i, 0);
+            for (int j = k + 1; j <= i; ++j) Mi[j] = fma(-lik, M[tri(j, k)], Mi[j]);
         }
         __syncwarp();
     }
@@ -98,14 +103,14 @@ __device__ bool cholesky(double* M, int s, int ld, int lane) {
 }
 
 template <int NRHS>
-__device__ void chol_solve(const double* M, int s, int ld, double* b1, double* b2, int lane) {
+__device__ void chol_solve(const double* M, int s, double* b1, double* b2, int lane) {
     for (int k = 0; k < s; ++k) {
         __syncwarp();
-        double il = 1.0 / M[k * ld + k];
+        double il = 1.0 / M[tri(k, k)];
         double y1 = b1[k] * il, y2 = NRHS > 1 ? b2[k] * il : 0.0;
         __syncwarp();
         for (int i = k + 1 + lane; i < s; i += 32) {
-            double l = M[i * ld + k];
+            double l = M[tri(i, k)];
             b1[i] = fma(-l, y1, b1[i]);
             if (NRHS > 1) b2[i] = fma(-l, y2, b2[i]);
         }
@@ -116,11 +121,11 @@ __device__ void chol_solve(const double* M, int s, int ld, double* b1, double* b
     }
     for (int k = s - 1; k >= 0; --k) {
         __syncwarp();
-        double il = 1.0 / M[k * ld + k];
+        double il = 1.0 / M[tri(k, k)];
         double x1 = b1[k] * il, x2 = NRHS > 1 ? b2[k] * il : 0.0;
         __syncwarp();
         for (int i = lane; i < k; i += 32) {
-            double l = M[k * ld + i];
+            double l = M[tri(k, i)];
             b1[i] = fma(-l, x1, b1[i]);
             if (NRHS > 1) b2[i] = fma(-l, x2, b2[i]);
         }
@@ -163,16 +168,16 @@ __device__ void warp_sort(int* a, int n, int lane) {
 }
 
 template <int SMAX, int CMAX, bool DYN>
-__global__ void __launch_bounds__(128) k_setup_rows(RowArgs a) {
-    constexpr int LD = SMAX + 1;
+__global__ void __launch_bounds__(256) k_setup_rows(RowArgs a) {
+    constexpr int MSZ = SMAX * (SMAX + 1) / 2;   // packed lower triangle
     extern __shared__ __align__(16) unsigned char smem[];
     const int warps = blockDim.x >> 5;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr size_t per_warp = sizeof(double) * (SMAX * LD + 2 * SMAX + (DYN ? CMAX : 0)) +
+    constexpr size_t per_warp = sizeof(double) * (MSZ + 2 * SMAX + (DYN ? CMAX : 0)) +
                                 sizeof(int) * (SMAX + (DYN ? CMAX + 8 : 0));
     unsigned char* base = smem + per_warp * wid;
     double* M = reinterpret_cast<double*>(base);
-    double* bg = M + SMAX * LD;
+    double* bg = M + MSZ;
     double* bf = bg + SMAX;
     double* rv = bf + SMAX;                                   // CMAX (dynamic)
     int* q = reinterpret_cast<int*>(rv + (DYN ? CMAX : 0));   // SMAX
@@ -193,15 +198,15 @@ __global__ void __launch_bounds__(128) k_setup_rows(RowArgs a) {
             for (int i = lane; i < s; i += 32) q[i] = a.Acf.idx[r0 + i];   // canonical rows: sorted, unique
         }
         __syncwarp();
-        gather_M(a.A, q, s, M, LD, lane);
+        gather_M(a.A, q, s, M, lane);
         gather_rhs(a.Acf, m, q, s, bg, lane);
         if (!DYN) gather_rhs(a.AfcT, m, q, s, bf, lane);
-        bool ok = cholesky(M, s, LD, lane);
+        bool ok = cholesky(M, s, lane);
         if (!ok) { if (lane == 0) report(a.err, ERR_FACT, m); continue; }
         if (!DYN) {
-            chol_solve<2>(M, s, LD, bg, bf, lane);
+            chol_solve<2>(M, s, bg, bf, lane);
         } else {
-            chol_solve<1>(M, s, LD, bg, nullptr, lane);
+            chol_solve<1>(M, s, bg, nullptr, lane);
             int added = 0, sweeps = 0;
             bool failed = false;
             while (added < a.n_ent && sweeps < a.sweep_limit) {
@@ -285,15 +290,15 @@ __global__ void __launch_bounds__(128) k_setup_rows(RowArgs a) {
                 __syncwarp();
                 s += picked;
                 added += picked;
-                gather_M(a.A, q, s, M, LD, lane);
+                gather_M(a.A, q, s, M, lane);
                 gather_rhs(a.Acf, m, q, s, bg, lane);
-                if (!cholesky(M, s, LD, lane)) { failed = true; if (lane == 0) report(a.err, ERR_FACT, m); break; }
-                chol_solve<1>(M, s, LD, bg, nullptr, lane);
+                if (!cholesky(M, s, lane)) { failed = true; if (lane == 0) report(a.err, ERR_FACT, m); break; }
+                chol_solve<1>(M, s, bg, nullptr, lane);
                 (void)best_r;
             }
             if (failed) continue;
             gather_rhs(a.AfcT, m, q, s, bf, lane);
-            chol_solve<1>(M, s, LD, bf, nullptr, lane);
+            chol_solve<1>(M, s, bf, nullptr, lane);
         }
         prefilter(bg, s, a.pre_tau, lane);
         prefilter(bf, s, a.pre_tau, lane);
@@ -581,14 +586,14 @@ __global__ void k_static_pattern(int32_t n_cells, const int32_t* __restrict__ e2
 }
 
 size_t warp_smem(int smax, int cmax, bool dyn) {
-    return sizeof(double) * (smax * (smax + 1) + 2 * smax + (dyn ? cmax : 0)) +
+    return sizeof(double) * (smax * (smax + 1) / 2 + 2 * smax + (dyn ? cmax : 0)) +
            sizeof(int) * (smax + (dyn ? cmax + 8 : 0));
 }
 
 template <int SMAX, int CMAX, bool DYN>
 void launch_rows(Ctx* c, const RowArgs& a) {
     size_t pw = warp_smem(SMAX, CMAX, DYN);
-    int warps = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / pw));
+    int warps = (int)std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / pw));
     size_t sm = pw * warps;
     auto kern = k_setup_rows<SMAX, CMAX, DYN>;
     EDFA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -653,6 +658,9 @@ void setup_rows(Ctx* c, const SetupInput& in, SetupOutput& out) {
     if (n == 0) return;
     int amax = dyn ? max_row_nnz(c, *in.A) : 0;
     int cand_need = dyn ? smax_need * std::max(amax, in.AT ? max_row_nnz(c, *in.AT) : amax) + max_row_nnz(c, *in.Acf) : 0;
+    if (PhaseTimer::enabled())
+        fprintf(stderr, "[edfa phase] setup_rows: dyn=%d smax_need=%d amax=%d cand_need=%d n_add=%d n_ent=%d\n", (int)dyn,
+                smax_need, amax, cand_need, (int)in.n_add, (int)in.n_ent);
     double bytes = 12.0 * in.Acf->nnz + 12.0 * in.AfcT->nnz + 16.0 * out.n_slots + 8.0 * n +
                    (dyn ? 0.0 : 4.0 * out.n_slots) + 12.0 * (double)out.n_slots * 3.0;
     {
