@@ -243,6 +243,7 @@ void launch_wf(Ctx* c, const TriPlan& p, WfArgs& a) {
 static void wf_from_level_plan(Ctx* c, TriPlan& p) {
     const int n_slots = p.n_slots, n_slices = n_slots / 32;
     p.wf_pos.reset(c, std::max(p.n, 1));
+    Prof pr(c, "wf_plan", 40.0 * p.n_stored + 8.0 * p.n);
     k_wf_pos<<<ceil_div(n_slots, 256), 256, 0, c->stream>>>(p.perm.p, n_slots, p.wf_pos.p);
     if (p.n_stored > 0)
         k_wf_remap<<<std::min<int64_t>(ceil_div(p.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
@@ -291,6 +292,7 @@ bool build_wf_plans(Ctx* c, const Csr& Lv, const Csr& Uv, const double* udiag, T
     bwd.n_levels = fwd.n_levels;
     sell_on_layout(c, fwd.perm.p, n_slices, Uv, udiag, false, bwd.slice_ptr, bwd.col, bwd.val, bwd.dinv, bwd.n_stored,
                    bwd.max_w);
+    Prof pr(c, "wf_plan", 40.0 * bwd.n_stored);
     if (bwd.n_stored > 0)
         k_wf_remap<<<std::min<int64_t>(ceil_div(bwd.n_stored, 256), NUM_SMS_B200 * 16), 256, 0, c->stream>>>(
             bwd.col.p, bwd.n_stored, fwd.wf_pos.p);
