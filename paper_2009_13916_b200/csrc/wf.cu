@@ -117,6 +117,8 @@ __device__ __forceinline__ void wf_poll(const int (&cc)[N], double (&xv)[N], con
 // ILU of dynamic patterns on distorted grids: ~110 dependencies per row);
 // the records in front of the last K are streamed in batches of WF_CHUNK
 // (they belong to old levels and are nearly always present).
+// (two blocks per SM: three force the K = 20 window into 80 registers with 168 bytes of spills and are slower,
+// 697 / 714 us vs 577 / 653 us per solve at 256^3)
 template <int K, bool REV, bool WIDE>
 __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
     const int lane = threadIdx.x & 31;
