@@ -216,6 +216,7 @@ struct Csr {
 struct Sell {
     int32_t n_rows = 0, n_cols = 0;
     int64_t nnz = 0, stored = 0;
+    int32_t uniform_w = 0;       // > 0: every slice stores exactly this many entries per row
     DevBuf<int64_t> slice_ptr;   // n_slices + 1
     DevBuf<int32_t> col;
     DevBuf<double> val;

@@ -147,6 +147,43 @@ __global__ void __launch_bounds__(256) k_spmv_sell(int n, const int64_t* __restr
     y[r] = (beta == 0.0) ? alpha * acc : fma(beta, y[r], alpha * acc);
 }
 
+// uniform slice width W (every slice stores exactly W entries per row, e.g. A_fc:
+// two cells per face): the slice offset is arithmetic, so the column / value
+// loads do not wait for a slice-pointer load, and all W loads are in flight
+template <int W>
+__global__ void __launch_bounds__(256) k_spmv_ell(int n, const int32_t* __restrict__ col,
+                                                  const double* __restrict__ val, const double* __restrict__ x,
+                                                  double* __restrict__ y, double alpha, double beta) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int64_t b = (int64_t)(r >> 5) * (32 * W) + (r & 31);
+    int c[W];
+    double v[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        c[k] = col[b + 32 * k];
+        v[k] = val[b + 32 * k];
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc = fma(v[k], __ldg(x + c[k]), acc);   // same order as k_spmv_sell
+    y[r] = (beta == 0.0) ? alpha * acc : fma(beta, y[r], alpha * acc);
+}
+
+// w[s] = 32 * (entries per row of slice s): widest slice and the sum of the widths
+__global__ void k_sell_max_width(const int64_t* __restrict__ w, int ns, int* __restrict__ out,
+                                 unsigned long long* __restrict__ sum) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < ns) {
+        atomicMax(out, (int)(w[s] / 32));
+        atomicAdd(sum, (unsigned long long)(w[s] / 32));
+    }
+}
+__global__ void k_sell_set_width(int64_t* __restrict__ w, int ns, int64_t v) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < ns) w[s] = v;
+}
+
 // S = A - H, thread per row, two passes (count / fill); tau > 0 -> filter_rows
 template <bool FILL>
 __global__ void k_sub(CsrV A, CsrV H, double tau, int32_t* __restrict__ cnt, const int32_t* __restrict__ Sp,
@@ -337,6 +374,22 @@ void build_sell(Ctx* c, const Csr& A, Sell& S) {
         k_sell_width<<<ceil_div((int64_t)ns * 32, 256), 256, 0, c->stream>>>(A.ptr.p, n, w.p);
         check_launch("k_sell_width");
     }
+    // narrow matrices whose slices are (almost) all as wide as the widest are stored with
+    // ONE width (the few narrower slices padded): the SpMV then needs no slice pointers
+    int* mw = c->d_scalar_i + 46;   // [max width, sum of widths (entries per row, 64-bit)]
+    int h_mw = 0;
+    unsigned long long h_sum = 0;
+    EDFA_CUDA(cudaMemsetAsync(mw, 0, 4 * sizeof(int), c->stream));
+    if (ns) k_sell_max_width<<<ceil_div(ns, 256), 256, 0, c->stream>>>(w.p, ns, mw,
+                                                                       reinterpret_cast<unsigned long long*>(mw + 2));
+    EDFA_CUDA(cudaMemcpyAsync(&h_mw, mw, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaMemcpyAsync(&h_sum, mw + 2, sizeof(h_sum), cudaMemcpyDeviceToHost, c->stream));
+    EDFA_CUDA(cudaStreamSynchronize(c->stream));
+    S.uniform_w = 0;
+    if (ns > 0 && (h_mw == 2 || h_mw == 6) && (double)ns * h_mw <= 1.05 * (double)h_sum) {
+        S.uniform_w = h_mw;
+        k_sell_set_width<<<ceil_div(ns, 256), 256, 0, c->stream>>>(w.p, ns, (int64_t)h_mw * 32);
+    }
     size_t bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, bytes, w.p, S.slice_ptr.p, ns + 1, c->stream);
     EDFA_CUDA(cub::DeviceScan::ExclusiveSum(c->cub_scratch(bytes), bytes, w.p, S.slice_ptr.p, ns + 1, c->stream));
@@ -354,8 +407,11 @@ void build_sell(Ctx* c, const Csr& A, Sell& S) {
 void spmv_sell(Ctx* c, const Sell& A, const double* x, double* y, double alpha, double beta, const char* name) {
     if (A.n_rows == 0) return;
     Prof pr(c, name, 12.0 * A.nnz + 4.0 * (A.n_rows + 1) + 8.0 * A.n_cols + 8.0 * A.n_rows * (beta != 0.0 ? 2 : 1));
-    k_spmv_sell<<<ceil_div(A.n_rows, 256), 256, 0, c->stream>>>(A.n_rows, A.slice_ptr.p, A.col.p, A.val.p, x, y,
-                                                               alpha, beta);
+    const int g = ceil_div(A.n_rows, 256);
+    if (A.uniform_w == 2) k_spmv_ell<2><<<g, 256, 0, c->stream>>>(A.n_rows, A.col.p, A.val.p, x, y, alpha, beta);
+    else if (A.uniform_w == 6) k_spmv_ell<6><<<g, 256, 0, c->stream>>>(A.n_rows, A.col.p, A.val.p, x, y, alpha, beta);
+    else
+        k_spmv_sell<<<g, 256, 0, c->stream>>>(A.n_rows, A.slice_ptr.p, A.col.p, A.val.p, x, y, alpha, beta);
     check_launch("k_spmv_sell");
 }
 
