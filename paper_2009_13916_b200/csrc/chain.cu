@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256) k_chain_scan(const int* __restrict__ rows
 // kept in registers (chains of at most 32*E rows).  Half the launches and no
 // HBM round trip for the intermediate vector.
 template <int E>
-__global__ void __launch_bounds__(256, E <= 8 ? 2 : 1) k_chain_pair(const int* __restrict__ rows,
+__global__ void __launch_bounds__(128, E <= 9 ? 5 : 2) k_chain_pair(const int* __restrict__ rows,
                                                     const double* __restrict__ coef, const double* __restrict__ dinv,
                                                     int n_chains, const double* b, double alpha, double* x,
                                                     const double* __restrict__ add, double* __restrict__ out2) {
@@ -432,11 +432,12 @@ bool run_chain_pair(Ctx* c, const ChainPlan& cp, const double* b, double alpha, 
                     double* out2, const char* name) {
     if (cp.n_chains == 0 || cp.E == 0) return false;
     Prof pr(c, name, 12.0 * cp.n + 32.0 * cp.n + (out2 ? 16.0 * cp.n : 0.0) + (x ? 8.0 * cp.n : 0.0));
-    const unsigned grid = (unsigned)ceil_div((int64_t)cp.n_chains * 32, 256);
+    // 128-thread blocks: five resident per SM at <= 102 registers (20 warps instead of 16)
+    const unsigned grid = (unsigned)ceil_div((int64_t)cp.n_chains * 32, 128);
     switch (cp.E) {
 #define EDFA_E_CASE(e)                                                                                     \
     case e:                                                                                                \
-        k_chain_pair<e><<<grid, 256, 0, c->stream>>>(cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha, x, \
+        k_chain_pair<e><<<grid, 128, 0, c->stream>>>(cp.crow.p, cp.ccoef.p, cp.cdinv.p, cp.n_chains, b, alpha, x, \
                                                      add, out2);                                           \
         break;
         EDFA_CHAIN_E(EDFA_E_CASE)
