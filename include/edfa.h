@@ -125,7 +125,9 @@ int edfa_ctx_set_stream(edfa_ctx* ctx, void* cuda_stream);
  * triangular solves, "ilu_levels" (0) level-synchronous ILU(0), "tile_direct" (-1)
  * ILU tile solves with early records read from L2 (1) / staged (0) / chosen
  * by wavefront width (-1), "ilu_wf" (-1) ILU solves wavefront-packed on one
- * slot layout (1) / tile-DAG or level plans (0) / chosen by level width (-1).  Seeded once
+ * slot layout (1) / tile-DAG or level plans (0) / chosen by level width (-1),
+ * "wf_prefetch" (1) wavefront-packed solves prefetch the next slice's records
+ * into shared memory by bulk copies (0: records loaded to registers per slice).  Seeded once
  * from EDFA_OPT_<NAME> at context creation.  Unknown name -> EDFA_ERR_VALUE. */
 int edfa_ctx_set_option(edfa_ctx* ctx, const char* name, int value);
 int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value);

@@ -18,7 +18,19 @@ void slow_log(double ms, const char* what, const char* file, int line) {
 }
 
 namespace {
-constexpr size_t CACHE_LIMIT = size_t(48) << 30;   // trim when the idle cache exceeds this
+// The idle cache is trimmed only when it outgrows 70 % of the device memory (at
+// least 48 GiB): a time-step loop that frees one preconditioner and builds the
+// next of the same shape then reuses every block instead of paying cudaFree +
+// cudaMalloc per system (256^3: ~0.3 s per system).  An allocation that fails
+// still hands the whole cache back and retries (alloc).
+size_t cache_limit() {
+    static const size_t v = [] {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); tot = 0; }
+        return std::max(size_t(48) << 30, tot / 10 * 7);
+    }();
+    return v;
+}
 
 size_t round_block(size_t bytes) {
     if (bytes <= (size_t(1) << 20)) return (bytes + 511) & ~size_t(511);
@@ -79,7 +91,7 @@ void Ctx::free(void* p) {
         if (it == block_size.end()) return;   // not ours
         free_blocks.emplace(it->second, p);   // reusable in stream order
         cached_bytes += it->second;
-        trim = cached_bytes > CACHE_LIMIT;
+        trim = cached_bytes > cache_limit();
     }
     if (trim) trim_cache();
 }
@@ -197,6 +209,7 @@ int edfa_ctx_create(int device, void* stream, edfa_ctx** out) {
     h->c.opt.ilu_levels = env_opt("EDFA_OPT_ILU_LEVELS", 0);
     h->c.opt.tile_direct = env_opt("EDFA_OPT_TILE_DIRECT", -1);
     h->c.opt.ilu_wf = env_opt("EDFA_OPT_ILU_WF", -1);
+    h->c.opt.wf_prefetch = env_opt("EDFA_OPT_WF_PREFETCH", 1);
     h->c.d_scalar_i = static_cast<int*>(h->c.alloc(64 * sizeof(int)));
     EDFA_CUDA(cudaMemsetAsync(h->c.d_scalar_i, 0, 64 * sizeof(int), h->c.stream));   // [60]: reduction ticket
     h->c.d_scalar_d = static_cast<double*>(h->c.alloc(4096 * sizeof(double)));
@@ -231,6 +244,7 @@ int edfa_ctx_set_option(edfa_ctx* ctx, const char* name, int value) {
     else if (n == "ilu_levels") o.ilu_levels = value;
     else if (n == "tile_direct") o.tile_direct = value;
     else if (n == "ilu_wf") o.ilu_wf = value;
+    else if (n == "wf_prefetch") o.wf_prefetch = value;
     else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
     API_END
 }
@@ -246,6 +260,7 @@ int edfa_ctx_get_option(edfa_ctx* ctx, const char* name, int* value) {
     else if (n == "ilu_levels") *value = o.ilu_levels;
     else if (n == "tile_direct") *value = o.tile_direct;
     else if (n == "ilu_wf") *value = o.ilu_wf;
+    else if (n == "wf_prefetch") *value = o.wf_prefetch;
     else throw Error(EDFA_ERR_VALUE, "unknown option '" + n + "'");
     API_END
 }

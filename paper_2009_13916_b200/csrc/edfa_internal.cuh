@@ -70,6 +70,7 @@ struct CtxOptions {
     int ilu_levels = 0;     // level-synchronous ILU(0) factorisation instead of the sync-free one
     int tile_direct = -1;   // ILU tile solves: -1 by wavefront width, 0 staged plan (15 warps), 1 direct (7 warps)
     int ilu_wf = -1;        // ILU solves wavefront-packed on one slot layout: -1 by level width, 0 never, 1 always
+    int wf_prefetch = 1;    // wavefront-packed solves prefetch the next slice's records into shared memory (k_wf_pf)
 };
 
 struct Ctx {

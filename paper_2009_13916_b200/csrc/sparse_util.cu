@@ -28,10 +28,13 @@ __global__ void k_fill_bits(unsigned long long* p, int64_t n, unsigned long long
     for (; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
+// G lanes per row (chosen from the mean row length: short rows keep their lanes busy)
+template <int G>
 __global__ void k_row_of(const int32_t* __restrict__ ptr, int32_t n, int32_t* __restrict__ row_of) {
-    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int w = (int)(t / G), lane = (int)(t % G);
     if (w >= n) return;
-    for (int e = ptr[w] + lane; e < ptr[w + 1]; e += 32) row_of[e] = w;
+    for (int e = ptr[w] + lane; e < ptr[w + 1]; e += G) row_of[e] = w;
 }
 __global__ void k_iota(int32_t* p, int64_t n) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -60,9 +63,11 @@ __global__ void k_merge_ptr(const int32_t* A, const int32_t* B, const int32_t* C
         M[i] = A[nA] + B[nA] + C[k] + D[k];
     }
 }
+template <int G>   // lanes per row
 __global__ void k_merge_fill(CsrV A, CsrV B, CsrV C, CsrV D, const int32_t* __restrict__ Mp,
                              int32_t* __restrict__ Mi, double* __restrict__ Mv) {
-    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int w = (int)(t / G), lane = (int)(t % G);
     int n = A.n_rows + C.n_rows;
     if (w >= n) return;
     const CsrV& L = w < A.n_rows ? A : C;
@@ -71,12 +76,12 @@ __global__ void k_merge_fill(CsrV A, CsrV B, CsrV C, CsrV D, const int32_t* __re
     int off = A.n_cols;
     int o = Mp[w];
     int l0 = L.ptr[r], l1 = L.ptr[r + 1], r0 = R.ptr[r], r1 = R.ptr[r + 1];
-    for (int e = l0 + lane; e < l1; e += 32) {
+    for (int e = l0 + lane; e < l1; e += G) {
         Mi[o + e - l0] = L.idx[e];
         Mv[o + e - l0] = L.val[e];
     }
     o += l1 - l0;
-    for (int e = r0 + lane; e < r1; e += 32) {
+    for (int e = r0 + lane; e < r1; e += G) {
         Mi[o + e - r0] = R.idx[e] + off;
         Mv[o + e - r0] = R.val[e];
     }
@@ -223,6 +228,119 @@ __global__ void k_sub(CsrV A, CsrV H, double tau, int32_t* __restrict__ cnt, con
     if (!FILL) cnt[i] = n;
 }
 
+// S = A - H without a row filter (tau = 0: only exact zeros are dropped), eight
+// lanes per row.  Every entry of the union finds its own output position:
+// an H entry ranks by its index in H plus the A-only entries left of it, an
+// A-only entry by the H entries left of it plus the A-only ones before it; the
+// kept entries are compacted through a per-row bit mask in shared memory.
+// Rows the fast path does not cover (more than 8 entries in A's row, more than
+// SUB_MAX entries in the union) are merged serially by the group's first lane.
+constexpr int SUB_G = 8;
+constexpr int SUB_MAX = 128;
+__device__ __forceinline__ int sub_lower_bound(const int32_t* __restrict__ idx, int lo, int hi, int col) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (idx[mid] < col) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+template <bool FILL>
+__global__ void __launch_bounds__(256) k_sub_rows8(CsrV A, CsrV H, int32_t* __restrict__ cnt,
+                                                   const int32_t* __restrict__ Sp, int32_t* __restrict__ Si,
+                                                   double* __restrict__ Sv) {
+    __shared__ unsigned mask_s[256 / SUB_G][SUB_MAX / 32];
+    const int g = threadIdx.x % SUB_G, grp = threadIdx.x / SUB_G;
+    const int gshift = (threadIdx.x & 31) / SUB_G * SUB_G;
+    const int i = blockIdx.x * (256 / SUB_G) + grp;
+    const bool live = i < A.n_rows;
+    int a0 = 0, a1 = 0, h0 = 0, h1 = 0;
+    if (live) { a0 = A.ptr[i]; a1 = A.ptr[i + 1]; h0 = H.ptr[i]; h1 = H.ptr[i + 1]; }
+    const int nA = a1 - a0, nH = h1 - h0;
+    const bool fast = nA <= SUB_G && nA + nH <= SUB_MAX;
+    unsigned* mask = mask_s[grp];
+    if (g < SUB_MAX / 32) mask[g] = 0u;
+    // A's row: one entry per lane
+    int colA = 0, lbH = 0;
+    bool a_only = false;
+    double vA = 0.0;
+    if (fast && g < nA) {
+        colA = A.idx[a0 + g];
+        lbH = sub_lower_bound(H.idx, h0, h1, colA);
+        a_only = !(lbH < h1 && H.idx[lbH] == colA);
+        vA = A.val[a0 + g];
+    }
+    const unsigned onlyA = (__ballot_sync(0xffffffffu, a_only) >> gshift) & ((1u << SUB_G) - 1u);
+    __syncwarp();
+    if (fast) {
+        if (g < nA && a_only && vA != 0.0) {
+            const int u = (lbH - h0) + __popc(onlyA & ((1u << g) - 1u));
+            atomicOr(&mask[u >> 5], 1u << (u & 31));
+        }
+        for (int q = h0 + g; q < h1; q += SUB_G) {
+            const int col = H.idx[q];
+            const int lb = sub_lower_bound(A.idx, a0, a1, col);
+            const bool hit = lb < a1 && A.idx[lb] == col;
+            const double v = (hit ? A.val[lb] : 0.0) - H.val[q];
+            if (v != 0.0) {
+                const int u = (q - h0) + __popc(onlyA & ((1u << (lb - a0)) - 1u));
+                atomicOr(&mask[u >> 5], 1u << (u & 31));
+            }
+        }
+    }
+    __syncwarp();
+    if (fast) {
+        auto kept_before = [&](int u) {
+            int n = 0;
+            for (int w = 0; w < (u >> 5); ++w) n += __popc(mask[w]);
+            return n + __popc(mask[u >> 5] & ((1u << (u & 31)) - 1u));
+        };
+        if (!FILL) {
+            if (live && g == 0) {
+                int n = 0;
+#pragma unroll
+                for (int w = 0; w < SUB_MAX / 32; ++w) n += __popc(mask[w]);
+                cnt[i] = n;
+            }
+        } else {
+            const int o = live ? Sp[i] : 0;
+            if (g < nA && a_only && vA != 0.0) {
+                const int u = (lbH - h0) + __popc(onlyA & ((1u << g) - 1u));
+                const int d = o + kept_before(u);
+                Si[d] = colA;
+                Sv[d] = vA;
+            }
+            for (int q = h0 + g; q < h1; q += SUB_G) {
+                const int col = H.idx[q];
+                const int lb = sub_lower_bound(A.idx, a0, a1, col);
+                const bool hit = lb < a1 && A.idx[lb] == col;
+                const double v = (hit ? A.val[lb] : 0.0) - H.val[q];
+                if (v != 0.0) {
+                    const int u = (q - h0) + __popc(onlyA & ((1u << (lb - a0)) - 1u));
+                    const int d = o + kept_before(u);
+                    Si[d] = col;
+                    Sv[d] = v;
+                }
+            }
+        }
+    } else if (live && g == 0) {   // serial merge of an oversized row
+        int o = FILL ? Sp[i] : 0, n = 0, p = a0, q = h0;
+        while (p < a1 || q < h1) {
+            const int ca = p < a1 ? A.idx[p] : INT32_MAX, ch = q < h1 ? H.idx[q] : INT32_MAX;
+            double v;
+            int col;
+            if (ca == ch) { col = ca; v = A.val[p++] - H.val[q++]; }
+            else if (ca < ch) { col = ca; v = A.val[p++]; }
+            else { col = ch; v = 0.0 - H.val[q++]; }
+            if (v != 0.0) {
+                if (FILL) { Si[o + n] = col; Sv[o + n] = v; }
+                ++n;
+            }
+        }
+        if (!FILL) cnt[i] = n;
+    }
+}
+
 template <bool FILL>
 __global__ void k_filter(CsrV A, double tau, bool keep_diag, int32_t* __restrict__ cnt, const int32_t* __restrict__ Sp,
                          int32_t* __restrict__ Si, double* __restrict__ Sv) {
@@ -301,7 +419,13 @@ void transpose(Ctx* c, const Csr& A, Csr& AT) {
     DevBuf<int32_t> row_of(c, A.nnz), ids(c, A.nnz), keys_out(c, A.nnz), order(c, A.nnz);
     {
         Prof pr(c, "transpose", 24.0 * A.nnz + 8.0 * A.n_rows);
-        k_row_of<<<ceil_div((int64_t)A.n_rows * 32, 256), 256, 0, c->stream>>>(A.ptr.p, A.n_rows, row_of.p);
+        const int64_t mean = A.nnz / std::max(A.n_rows, 1);
+        if (mean <= 4)
+            k_row_of<4><<<ceil_div((int64_t)A.n_rows * 4, 256), 256, 0, c->stream>>>(A.ptr.p, A.n_rows, row_of.p);
+        else if (mean <= 16)
+            k_row_of<8><<<ceil_div((int64_t)A.n_rows * 8, 256), 256, 0, c->stream>>>(A.ptr.p, A.n_rows, row_of.p);
+        else
+            k_row_of<32><<<ceil_div((int64_t)A.n_rows * 32, 256), 256, 0, c->stream>>>(A.ptr.p, A.n_rows, row_of.p);
         k_iota<<<ceil_div(A.nnz, 256), 256, 0, c->stream>>>(ids.p, A.nnz);
         k_col_hist<<<ceil_div(A.nnz, 256), 256, 0, c->stream>>>(A.idx.p, A.nnz, cnt.p);
         check_launch("transpose prep");
@@ -336,8 +460,12 @@ void block_merge(Ctx* c, const Csr& A, const Csr& B, const Csr& C, const Csr& D,
     Prof pr(c, "block_merge", 24.0 * M.nnz);
     k_merge_ptr<<<ceil_div(M.n_rows + 1, 256), 256, 0, c->stream>>>(A.ptr.p, B.ptr.p, C.ptr.p, D.ptr.p, A.n_rows,
                                                                    C.n_rows, M.ptr.p);
-    k_merge_fill<<<ceil_div((int64_t)M.n_rows * 32, 256), 256, 0, c->stream>>>(view(A), view(B), view(C), view(D),
-                                                                              M.ptr.p, M.idx.p, M.val.p);
+    if (M.nnz <= 16ll * M.n_rows)
+        k_merge_fill<8><<<ceil_div((int64_t)M.n_rows * 8, 256), 256, 0, c->stream>>>(view(A), view(B), view(C), view(D),
+                                                                                    M.ptr.p, M.idx.p, M.val.p);
+    else
+        k_merge_fill<32><<<ceil_div((int64_t)M.n_rows * 32, 256), 256, 0, c->stream>>>(
+            view(A), view(B), view(C), view(D), M.ptr.p, M.idx.p, M.val.p);
     check_launch("block_merge");
 }
 
@@ -424,8 +552,12 @@ void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S) {
     DevBuf<int32_t> cnt(c, std::max(n, 1));
     if (n) {
         Prof pr(c, "schur_sub", 12.0 * (A.nnz + H.nnz) + 8.0 * n);
-        k_sub<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), view(H), tau, cnt.p, nullptr, nullptr,
-                                                             nullptr);
+        if (tau > 0.0)
+            k_sub<false><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), view(H), tau, cnt.p, nullptr, nullptr,
+                                                                 nullptr);
+        else
+            k_sub_rows8<false><<<ceil_div(n, 256 / SUB_G), 256, 0, c->stream>>>(view(A), view(H), cnt.p, nullptr,
+                                                                               nullptr, nullptr);
         check_launch("k_sub count");
     }
     S.nnz = scan_counts(c, cnt.p, S.ptr.p, n);
@@ -433,8 +565,12 @@ void csr_sub(Ctx* c, const Csr& A, const Csr& H, double tau, Csr& S) {
     S.val.reset(c, S.nnz);
     if (n) {
         Prof pr(c, "schur_sub", 12.0 * (A.nnz + H.nnz + S.nnz) + 8.0 * n);
-        k_sub<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), view(H), tau, nullptr, S.ptr.p, S.idx.p,
-                                                            S.val.p);
+        if (tau > 0.0)
+            k_sub<true><<<ceil_div(n, 128), 128, 0, c->stream>>>(view(A), view(H), tau, nullptr, S.ptr.p, S.idx.p,
+                                                                S.val.p);
+        else
+            k_sub_rows8<true><<<ceil_div(n, 256 / SUB_G), 256, 0, c->stream>>>(view(A), view(H), nullptr, S.ptr.p,
+                                                                              S.idx.p, S.val.p);
         check_launch("k_sub fill");
     }
 }

@@ -189,6 +189,134 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
     }
 }
 
+// Prefetching shape of k_wf (rows of at most K records): a warp holds three
+// slices at a time --
+//   A: being solved; its columns sit in registers, its coefficients in shared memory;
+//   B: the next ticket; its records are on their way into the warp's shared-memory
+//      stage by two bulk copies (cp.async.bulk, one mbarrier per stage), its
+//      right-hand side and diagonal are in flight to registers;
+//   C: the ticket after that; its slice pointer and row index are in flight;
+// so the DRAM latency of a slice's plan (slice pointer -> records) is paid while the
+// previous slice polls its dependencies instead of in front of every slice.
+// Tickets are still handed out in topological order and a warp solves its slices
+// in ticket order, so the lowest unfinished slice is always some warp's A: no deadlock.
+// Per warp: one column stage (read into registers as soon as it lands, then free
+// for B) and two coefficient stages.  Summation order as in k_wf.
+__device__ __forceinline__ unsigned wf_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+constexpr int WF_PF_WARPS = 8;
+constexpr size_t wf_pf_warp_bytes(int K) { return (size_t)K * 32 * (4 + 2 * 8); }
+constexpr size_t wf_pf_smem(int K) { return WF_PF_WARPS * wf_pf_warp_bytes(K) + WF_PF_WARPS * 2 * sizeof(uint64_t); }
+
+template <int K, bool REV>
+__global__ void __launch_bounds__(WF_PF_WARPS * 32, 2) k_wf_pf(WfArgs a) {
+    extern __shared__ __align__(128) unsigned char wf_smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double* vbuf = reinterpret_cast<double*>(wf_smem) + (size_t)wid * 2 * K * 32;            // [2][K*32]
+    int32_t* cbuf = reinterpret_cast<int32_t*>(wf_smem + WF_PF_WARPS * (size_t)2 * K * 32 * 8) + (size_t)wid * K * 32;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(wf_smem + WF_PF_WARPS * wf_pf_warp_bytes(K)) + wid * 2;
+    const double sent = __longlong_as_double((long long)SENTINEL_BITS);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wf_saddr(&bar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(wf_saddr(&bar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    bool more = true;   // tickets left (a warp stops at its first failing ticket)
+    auto take = [&]() -> int {
+        if (!more) return -1;
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(a.ticket, 1u) - a.ticket_base;
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= (unsigned)a.n_slices) { more = false; return -1; }
+        return REV ? a.n_slices - 1 - (int)t : (int)t;
+    };
+    // lane 0: records of slice (b0, w) -> column stage and coefficient stage st
+    auto issue = [&](int64_t b0, int w, int st) {
+        if (lane == 0 && w > 0) {
+            const unsigned mb = wf_saddr(&bar[st]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"((unsigned)w * 32u * 12u)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(wf_saddr(cbuf)), "l"(a.col + b0), "r"((unsigned)w * 128u), "r"(mb) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(wf_saddr(vbuf + (size_t)st * K * 32)), "l"(a.val + b0), "r"((unsigned)w * 256u), "r"(mb)
+                         : "memory");
+        }
+    };
+    // stage C of a slice: pointer pair and row index (loads stay in flight until used)
+    int sA = take(), sB = -1, sC = -1;
+    int64_t b0A = 0, b0B = 0, b0C = 0;
+    int wA = 0, wB = 0, wC = 0, rA = -1, rB = -1, rC = -1;
+    double biasA = 0.0, biasB = 0.0, diA = 1.0, diB = 1.0;
+    auto stage_c = [&](int s, int64_t& b0, int& w, int& r) {
+        if (s < 0) return;
+        b0 = a.sptr[s];
+        w = (int)((a.sptr[s + 1] - b0) / 32);
+        r = a.perm[s * 32 + lane];
+    };
+    auto stage_b = [&](int s, int r, double& bias, double& di) {
+        if (s < 0) return;
+        const int slot = s * 32 + lane;
+        bias = r >= 0 ? (a.b_slots ? a.b[slot] : a.b[r]) : 0.0;   // b may alias out2 / b_sent row-wise: plain load
+        di = a.dinv ? a.dinv[slot] : 1.0;
+    };
+    stage_c(sA, b0A, wA, rA);
+    stage_b(sA, rA, biasA, diA);
+    issue(b0A, wA, 0);
+    sB = take();
+    stage_c(sB, b0B, wB, rB);
+    unsigned phase = 0;   // bit st: parity of the next completion of bar[st]
+    int st = 0;
+    while (sA >= 0) {
+        const int slot = sA * 32 + lane;
+        const int off = K - wA;   // right alignment: record k sits in register k + off
+        int cc[K];
+        if (wA > 0) {
+            asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                         "@!p bra WAIT_%=;\n\t}" ::"r"(wf_saddr(&bar[st])), "r"((phase >> st) & 1u) : "memory");
+            phase ^= 1u << st;
+        }
+#pragma unroll
+        for (int u = 0; u < K; ++u) cc[u] = u >= off ? cbuf[(u - off) * 32 + lane] : -1;
+        double xv[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) xv[u] = cc[u] >= 0 ? ld_relaxed(a.xs + cc[u]) : 0.0;   // all in flight at once
+        __syncwarp();   // the column stage is free again
+        // B's records into the other stage, B's scalars and C's pointers into registers
+        issue(b0B, wB, st ^ 1);
+        stage_b(sB, rB, biasB, diB);
+        sC = take();
+        stage_c(sC, b0C, wC, rC);
+        if (a.b_sent) a.b_sent[slot] = sent;
+        if (a.pre_sent) a.pre_sent[slot] = sent;
+        const double* vv = vbuf + (size_t)st * K * 32 + lane;
+        double acc = rA >= 0 ? a.alpha * biasA : 0.0;
+        // ---- phase 1: older levels
+        wf_poll<K, 0, K - WF_NEAR, true>(cc, xv, a.xs, a.err);
+#pragma unroll
+        for (int u = 0; u < K - WF_NEAR; ++u)
+            if (u >= off) acc = fma(-vv[(u - off) * 32], xv[u], acc);
+        // ---- phase 2: the nearest level
+        wf_poll<K, K - WF_NEAR, K, false>(cc, xv, a.xs, a.err);
+#pragma unroll
+        for (int u = K - WF_NEAR; u < K; ++u)
+            if (u >= off) acc = fma(-vv[(u - off) * 32], xv[u], acc);
+        if (rA >= 0) {
+            const double xr = acc * diA;
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.xs + slot),
+                      (unsigned long long)__double_as_longlong(publishable(xr)) - SENTINEL_BITS);
+            if (a.x_nat) a.x_nat[rA] = xr;
+            if (a.out2) a.out2[rA] = xr + a.add[rA];
+        }
+        __syncwarp();   // every lane is done with coefficient stage st before it is refilled
+        sA = sB; b0A = b0B; wA = wB; rA = rB; biasA = biasB; diA = diB;
+        sB = sC; b0B = b0C; wB = wC; rB = rC;
+        sC = -1;
+        st ^= 1;
+    }
+}
+
 // Sort every row's records by dependency slot -- ascending for L (older levels
 // first), descending for U (run in reverse: larger slots are older) -- pads (-1)
 // in front, so the nearest level's dependencies are the last records of the row.
@@ -217,6 +345,28 @@ __global__ void k_wf_sort_rows(const int64_t* __restrict__ sptr, int n_slices, i
         col[b0 + (int64_t)(j + 1) * 32 + lane] = ci;
         val[b0 + (int64_t)(j + 1) * 32 + lane] = vi;
     }
+}
+
+template <int K>
+void launch_wf_pf(Ctx* c, const TriPlan& p, WfArgs& a) {
+    static int grid = 0;
+    auto kf = k_wf_pf<K, false>;
+    auto kr = k_wf_pf<K, true>;
+    const size_t smem = wf_pf_smem(K);
+    // per launch: the attribute is per device and the call costs ~1 us against a ~1 ms solve
+    EDFA_CUDA(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EDFA_CUDA(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (!grid) {
+        int occ = 0;
+        EDFA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kf, WF_PF_WARPS * 32, smem));
+        grid = NUM_SMS_B200 * std::max(1, occ);
+    }
+    unsigned& base = const_cast<unsigned&>(p.wf_ticket_base);
+    a.ticket_base = base;
+    base += (unsigned)(a.n_slices + grid * WF_PF_WARPS);   // every warp takes exactly one failing ticket
+    if (p.wf_reverse) kr<<<grid, WF_PF_WARPS * 32, smem, c->stream>>>(a);
+    else kf<<<grid, WF_PF_WARPS * 32, smem, c->stream>>>(a);
+    check_launch("k_wf_pf");
 }
 
 template <int K, bool WIDE>
@@ -320,7 +470,11 @@ void run_wf(Ctx* c, const TriPlan& p, const double* b, bool b_slots, double alph
     WfArgs a{p.wf_perm, p.slice_ptr.p, p.col.p, p.val.p, p.unit ? nullptr : p.dinv.p, p.wf_slices,
              p.wf_ticket.p, 0u, b, b_slots ? 1 : 0, alpha, xs, x_nat, add, out2, b_sent, pre_sent, c->d_scalar_i + 8};
     Prof pr(c, name, 12.0 * p.n_dep + 24.0 * p.n + (out2 ? 16.0 * p.n : 0.0));
-    if (p.max_w <= 8) launch_wf<8, false>(c, p, a);
+    if (c->opt.wf_prefetch && p.max_w <= 20) {
+        if (p.max_w <= 8) launch_wf_pf<8>(c, p, a);
+        else if (p.max_w <= 12) launch_wf_pf<12>(c, p, a);
+        else launch_wf_pf<20>(c, p, a);
+    } else if (p.max_w <= 8) launch_wf<8, false>(c, p, a);
     else if (p.max_w <= 12) launch_wf<12, false>(c, p, a);
     else if (p.max_w <= 20) launch_wf<20, false>(c, p, a);
     else launch_wf<16, true>(c, p, a);

@@ -185,8 +185,7 @@ class DeviceSystem:
         if isinstance(system, DeviceSystem):
             return system
         blocks = [DeviceCsr.from_scipy(getattr(system, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc")]
-        rhs = system.rhs() if hasattr(system, "rhs") else None
-        ds = cls(*blocks, rhs=rhs, host=system)
+        ds = cls(*blocks, rhs=_upload_rhs(system), host=system)
         ds._src = {n: id(getattr(system, n)) for n in ("A_ff", "A_fc", "A_cf", "A_cc")}
         return ds
 
@@ -199,8 +198,7 @@ class DeviceSystem:
                                     for n in ("A_ff", "A_fc", "A_cf")):
             return DeviceSystem.from_host(system)
         A_cc = self.A_cc if id(system.A_cc) == self._src.get("A_cc") else DeviceCsr.from_scipy(system.A_cc)
-        rhs = system.rhs() if hasattr(system, "rhs") else None
-        ds = DeviceSystem(self.A_ff, self.A_fc, self.A_cf, A_cc, rhs=rhs, host=system)
+        ds = DeviceSystem(self.A_ff, self.A_fc, self.A_cf, A_cc, rhs=_upload_rhs(system), host=system)
         ds._src = dict(self._src, A_cc=id(system.A_cc))
         return ds
 
@@ -237,6 +235,30 @@ class DeviceSystem:
             except Exception:   # pragma: no cover
                 pass
             self.handle = None
+
+
+def _upload_rhs(system):
+    """Device right-hand side [rhs_f; rhs_c] (hx/assembly.py:172-173) uploaded
+    part by part: no concatenated host copy, DMA when the parts are page-locked."""
+    if hasattr(system, "rhs_f") and hasattr(system, "rhs_c"):
+        parts = [np.ascontiguousarray(np.asarray(getattr(system, n), dtype=np.float64)) for n in ("rhs_f", "rhs_c")]
+        out = torch.empty(sum(p.size for p in parts), dtype=torch.float64, device="cuda")
+        o = 0
+        for p in parts:
+            out[o:o + p.size].copy_(torch.from_numpy(p), non_blocking=True)
+            o += p.size
+        return out
+    return system.rhs() if hasattr(system, "rhs") else None
+
+
+def to_host_vector(x: torch.Tensor) -> np.ndarray:
+    """Device vector -> numpy through a page-locked block of torch's caching
+    host allocator (DMA at full rate; the block is reused by the next call
+    once the returned array is released)."""
+    h = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    h.copy_(x, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
 
 
 def _upload_index(a) -> torch.Tensor:

@@ -26,7 +26,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from .device import DeviceSystem, SystemOperator, as_device_vector, ctx, dptr
+from .device import DeviceSystem, SystemOperator, as_device_vector, ctx, dptr, to_host_vector
 
 
 @dataclass
@@ -90,7 +90,7 @@ def _run_fused(which, ops, b, tol, restart, max_it):
                                   C.byref(rep), hist.ctypes.data_as(C.c_void_p), cap))
     r = SolveReport(n_it=rep.n_it, converged=bool(rep.converged), breakdown=bool(rep.breakdown),
                     relres_history=hist[:min(rep.n_hist, cap)].tolist(), final_relres=rep.final_relres)
-    return (x.cpu().numpy() if host else x), r
+    return (to_host_vector(x) if host else x), r
 
 
 class _Vec:

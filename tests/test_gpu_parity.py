@@ -668,3 +668,31 @@ def test_wavefront_packed_ilu_solves_equal_level_solves(edfa, idx, n, proto):
     ref = spla.spsolve_triangular(sp.csr_matrix(f2.U), spla.spsolve_triangular(sp.csr_matrix(f2.L), rc, lower=True),
                                   lower=False)
     assert np.abs(out[1][1] - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("idx,n", [(2, 24), (1, 16), (5, 20), (3, 8)])
+def test_prefetching_wavefront_solve_is_bitwise_the_register_one(edfa, idx, n):
+    """k_wf_pf (next slice's records prefetched into shared memory by bulk
+    copies, three slices in flight per warp) sums every row in k_wf's order:
+    apply, Schur inner apply and repeated applies are bit-identical."""
+    from paper_2009_13916_b200 import configs
+    case = configs.make(idx, n=n)
+    s = case.system
+    p = case.precond
+    ds = edfa.DeviceSystem.from_host(s)
+    r = np.random.default_rng(23).standard_normal(s.n_unknowns)
+    out = {}
+    with option("ilu_wf", 1):
+        if p["pattern"] == "dynamic":       # Schur rows wider than the register window: k_wf's streaming shape
+            pre = edfa.BlockLDUPreconditioner.build(ds, dynamic=edfa.DynamicConfig(1, 4), no_fill=True)
+        else:
+            pre = edfa.BlockLDUPreconditioner.build(
+                ds, patterns=edfa.patterns_for(ds, p["pattern"], p.get("prototype", "A")), no_fill=True)
+        for pf in (0, 1):
+            with option("wf_prefetch", pf):
+                y = pre.apply(r)
+                y2 = pre.apply(r)
+                assert np.array_equal(y, y2)
+                out[pf] = (y, pre.stage2.schur_inner.apply(r[s.n_free_faces:]))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
