@@ -77,23 +77,32 @@ struct WfArgs {
 //   phase 2: the nearest NEAR dependencies, polled tightly as one batch; after
 //     the last arrival only NEAR FMAs and the publish remain.
 // The summation order is the stored order (bias first), fixed per plan.
-constexpr int WF_NEAR = 3;
+#ifndef EDFA_WF_NEAR
+#define EDFA_WF_NEAR 3
+#endif
+constexpr int WF_NEAR = EDFA_WF_NEAR;
+#ifndef EDFA_WF_SLEEP0
+#define EDFA_WF_SLEEP0 64
+#endif
+#ifndef EDFA_WF_SLEEP_MAX
+#define EDFA_WF_SLEEP_MAX 512
+#endif
 constexpr int WF_CHUNK = 16;   // records per batch of the older part of rows wider than the register window
 
 // batch poll of missing values (SENTINEL) among x[U0..U1): re-read all of them
 // per round, one warp vote; back_off: sleep between rounds (warps far ahead of
 // the frontier)
-template <int N, int U0, int U1, bool BACKOFF>
+template <int N, int U0, int U1, bool BACKOFF, unsigned SLEEP0 = EDFA_WF_SLEEP0, unsigned SLEEP_MAX = EDFA_WF_SLEEP_MAX>
 __device__ __forceinline__ void wf_poll(const int (&cc)[N], double (&xv)[N], const double* xs, int* err) {
     bool miss = false;
 #pragma unroll
     for (int u = U0; u < U1; ++u) miss |= cc[u] >= 0 && is_sentinel(xv[u]);
     long long spins = 0;
-    unsigned ns = 64;
+    unsigned ns = SLEEP0;
     while (__any_sync(0xffffffffu, miss)) {
         if (BACKOFF) {
             __nanosleep(ns);
-            if (ns < 512) ns <<= 1;
+            if (ns < SLEEP_MAX) ns <<= 1;
         }
 #pragma unroll
         for (int u = U0; u < U1; ++u)
@@ -203,12 +212,25 @@ __global__ void __launch_bounds__(256, 2) k_wf(WfArgs a) {
 // Per warp: one column stage (read into registers as soon as it lands, then free
 // for B) and two coefficient stages.  Summation order as in k_wf.
 __device__ __forceinline__ unsigned wf_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-constexpr int WF_PF_WARPS = 8;
+// back-off of the prefetching shape's phase 1 (A/B at 256^3: 64..512 ns 502/512 ms per step for L/U, 8..32 ns 479/490)
+#ifndef EDFA_WF_PF_SLEEP0
+#define EDFA_WF_PF_SLEEP0 8
+#endif
+#ifndef EDFA_WF_PF_SLEEP_MAX
+#define EDFA_WF_PF_SLEEP_MAX 32
+#endif
+#ifndef EDFA_WF_PF_WARPS
+#define EDFA_WF_PF_WARPS 8
+#endif
+#ifndef EDFA_WF_PF_BLOCKS
+#define EDFA_WF_PF_BLOCKS 2
+#endif
+constexpr int WF_PF_WARPS = EDFA_WF_PF_WARPS;
 constexpr size_t wf_pf_warp_bytes(int K) { return (size_t)K * 32 * (4 + 2 * 8); }
 constexpr size_t wf_pf_smem(int K) { return WF_PF_WARPS * wf_pf_warp_bytes(K) + WF_PF_WARPS * 2 * sizeof(uint64_t); }
 
 template <int K, bool REV>
-__global__ void __launch_bounds__(WF_PF_WARPS * 32, 2) k_wf_pf(WfArgs a) {
+__global__ void __launch_bounds__(WF_PF_WARPS * 32, EDFA_WF_PF_BLOCKS) k_wf_pf(WfArgs a) {
     extern __shared__ __align__(128) unsigned char wf_smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     double* vbuf = reinterpret_cast<double*>(wf_smem) + (size_t)wid * 2 * K * 32;            // [2][K*32]
@@ -293,22 +315,27 @@ __global__ void __launch_bounds__(WF_PF_WARPS * 32, 2) k_wf_pf(WfArgs a) {
         const double* vv = vbuf + (size_t)st * K * 32 + lane;
         double acc = rA >= 0 ? a.alpha * biasA : 0.0;
         // ---- phase 1: older levels
-        wf_poll<K, 0, K - WF_NEAR, true>(cc, xv, a.xs, a.err);
+        wf_poll<K, 0, K - WF_NEAR, true, EDFA_WF_PF_SLEEP0, EDFA_WF_PF_SLEEP_MAX>(cc, xv, a.xs, a.err);
 #pragma unroll
         for (int u = 0; u < K - WF_NEAR; ++u)
             if (u >= off) acc = fma(-vv[(u - off) * 32], xv[u], acc);
         // ---- phase 2: the nearest level
+        auto publish = [&](double sum) {
+            if (rA >= 0) {
+                const double xr = sum * diA;
+                // fire-and-forget reduction at L2: SENTINEL + (x - SENTINEL)
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.xs + slot),
+                          (unsigned long long)__double_as_longlong(publishable(xr)) - SENTINEL_BITS);
+                if (a.x_nat) a.x_nat[rA] = xr;
+                if (a.out2) a.out2[rA] = xr + a.add[rA];
+            }
+        };
+        // (publishing per lane, without the warp vote, measured slower: 495 / 508 vs 479 / 490 ms per step)
         wf_poll<K, K - WF_NEAR, K, false>(cc, xv, a.xs, a.err);
 #pragma unroll
         for (int u = K - WF_NEAR; u < K; ++u)
             if (u >= off) acc = fma(-vv[(u - off) * 32], xv[u], acc);
-        if (rA >= 0) {
-            const double xr = acc * diA;
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.xs + slot),
-                      (unsigned long long)__double_as_longlong(publishable(xr)) - SENTINEL_BITS);
-            if (a.x_nat) a.x_nat[rA] = xr;
-            if (a.out2) a.out2[rA] = xr + a.add[rA];
-        }
+        publish(acc);
         __syncwarp();   // every lane is done with coefficient stage st before it is refilled
         sA = sB; b0A = b0B; wA = wB; rA = rB; biasA = biasB; diA = diB;
         sB = sC; b0B = b0C; wB = wC; rB = rC;
