@@ -12,6 +12,8 @@ for cfg in 1 2; do
 done
 timeout 1500 python bench.py --config 3 --steps 1 --warmup 1 --no-cpu-baseline --profile-json gpurun_out/${TAG}_profile_c3.json > gpurun_out/${TAG}_bench_c3.log 2>&1
 echo "config 3 rc=$? $(tail -1 gpurun_out/${TAG}_bench_c3.log | cut -c1-300)"
+timeout 900 python bench.py --config 4 --no-cpu-baseline > gpurun_out/${TAG}_bench_c4.log 2>&1
+echo "config 4 rc=$? $(tail -1 gpurun_out/${TAG}_bench_c4.log | cut -c1-300)"
 timeout 900 python bench.py --config 2 --slabs 2 --steps 3 --warmup 2 > gpurun_out/${TAG}_slabs2_c2.log 2>&1
 echo "slabs2 c2 rc=$? $(tail -1 gpurun_out/${TAG}_slabs2_c2.log | cut -c1-300)"
 timeout 900 python bench.py --config 5 --slabs 2 --scaling weak --n 96 --steps 2 --warmup 2 > gpurun_out/${TAG}_slabs2_weak96.log 2>&1
@@ -19,7 +21,7 @@ echo "slabs2 weak rc=$? $(tail -1 gpurun_out/${TAG}_slabs2_weak96.log | cut -c1-
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 16000 --csv \
   --log-file gpurun_out/${TAG}_ncu_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config2 > gpurun_out/${TAG}_ncu_list.log 2>&1
 echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:^k_wf$' -s 40 -c 2 \
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:^k_wf_pf$' -s 40 -c 2 \
     -o gpurun_out/${TAG}_k_wf_c5 -f python bench.py --config 5 --steps 1 --warmup 1 --no-cpu-baseline --no-config2 \
     > gpurun_out/${TAG}_k_wf_c5.log 2>&1
 echo "ncu k_wf rc=$?"
