@@ -12,7 +12,7 @@ import json
 try:
     p=json.load(open("gpurun_out/${tag}_$v.json"))["warmup_step"]
     d=json.loads(open("gpurun_out/${tag}_$v.log").read().strip().splitlines()[-1])
-    print("$v", "step", round(d["ms_per_step"],1), {k:round(x["ms"],1) for k,x in p.items() if k.startswith("trsv_il") or k=="trsv_ic_pair"}, d["clocks"]["sm_mhz"])
+    print("$v", "step", round(d["ms_per_step"],1), {k:round(x["ms"],1) for k,x in p.items() if k.startswith("trsv_il") or k in ("trsv_ic_pair","ilu0_factor","product","setup_rows_static")}, d["clocks"]["sm_mhz"])
 except Exception as e:
     print("$v", "failed", e)
 P

@@ -13,7 +13,7 @@ import re
 import sys
 
 # bench profiler name -> ncu kernel name prefix
-PROFILER_NAMES = {"trsv_ilu": ("k_wf", "k_tile_flow"), "gs_dots2": ("k_dots2",), "gs_axpy2": ("k_axpy2",),
+PROFILER_NAMES = {"trsv_ilu": ("k_wf_pf", "k_wf", "k_tile_flow"), "gs_dots2": ("k_dots2",), "gs_axpy2": ("k_axpy2",),
                   "spmv_A": ("k_spmv_sell",), "trsv_ic_pair": ("k_chain_pair",)}
 
 
