@@ -115,7 +115,13 @@ __global__ void __launch_bounds__(256) k_ic0(LevelArgs la, const int32_t* __rest
 // strictly lower part holds the multipliers and its strictly upper part U;
 // pivots go to udiag.
 // staged U entries per pivot chunk (the elimination chunks longer pivot sets)
-__host__ __device__ constexpr int ilu0_ecap(int rmax) { return rmax <= 64 ? 512 : 1024; }
+// (rows of at most 40 entries -- static patterns on regular grids: 37 -- stage at most 18 x 19 U entries: the
+// smaller working set and 64 registers let four blocks share an SM instead of two)
+__host__ __device__ constexpr int ilu0_ecap(int rmax) { return rmax <= 40 ? 352 : rmax <= 64 ? 512 : 1024; }
+#ifndef EDFA_ILU0_MINB
+#define EDFA_ILU0_MINB 4
+#endif
+__host__ __device__ constexpr int ilu0_min_blocks(int rmax) { return rmax <= 40 ? EDFA_ILU0_MINB : 1; }
 __host__ __device__ constexpr size_t ilu0_warp_smem(int rmax) {
     return ((size_t)(3 * rmax + ilu0_ecap(rmax)) * 8 + (size_t)(4 * rmax + 1 + ilu0_ecap(rmax) + 2) * 4 + 15) &
            ~size_t(15);
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(256) k_ilu0(LevelArgs la, const int32_t* __res
 // running warps -- no grid barrier, no level plan, a row starts as soon as its
 // own pivot rows are final
 template <int RMAX>
-__global__ void __launch_bounds__(256) k_ilu0_sf(const int* __restrict__ ord, int n_ord, int* ticket,
+__global__ void __launch_bounds__(256, ilu0_min_blocks(RMAX)) k_ilu0_sf(const int* __restrict__ ord, int n_ord, int* ticket,
                                                  const int32_t* __restrict__ Sp, const int32_t* __restrict__ Si,
                                                  const int32_t* __restrict__ ustart, double* __restrict__ LU,
                                                  const double* __restrict__ scale, double* __restrict__ udiag,
@@ -625,7 +631,8 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
                 EDFA_CUDA(cudaLaunchCooperativeKernel(k, dim3(grid), dim3(threads), args, smem, c->stream));
             }
         };
-        if (maxr <= 64) launch(k_ilu0<64>, k_ilu0_sf<64>, 64);
+        if (maxr <= 40) launch(k_ilu0<40>, k_ilu0_sf<40>, 40);
+        else if (maxr <= 64) launch(k_ilu0<64>, k_ilu0_sf<64>, 64);
         else if (maxr <= 256) launch(k_ilu0<256>, k_ilu0_sf<256>, 256);
         else launch(k_ilu0<1024>, k_ilu0_sf<1024>, 1024);
     }

@@ -221,7 +221,10 @@ __global__ void __launch_bounds__(256) k_product(ProdArgs a) {
 // the same for the F~ rows of W_m; the hash accumulation then runs from
 // shared memory in exactly k_product's order (bit-identical results).  Rows
 // that exceed the tier's capacities go to the overflow list (k_product).
-constexpr int PF_BITS = 7, PF_T = 1 << PF_BITS, PF_CAPG = 32, PF_CAPF = 512, PF_CAP = 64;
+#ifndef EDFA_PF_CAPF
+#define EDFA_PF_CAPF 512
+#endif
+constexpr int PF_BITS = 7, PF_T = 1 << PF_BITS, PF_CAPG = 32, PF_CAPF = EDFA_PF_CAPF, PF_CAP = 64;
 constexpr size_t PF_WARP_BYTES = (size_t)PF_T * 12 * 3 + PF_CAPG * (8 + 4 + 4) + (PF_CAPG + 1) * 4 +
                                  (PF_T + 1) * 4 + (size_t)PF_CAPF * 12;
 

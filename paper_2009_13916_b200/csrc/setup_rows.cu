@@ -340,8 +340,11 @@ struct RegRow {
     static constexpr size_t BYTES = sizeof(double) * (SMAX * LD + 2 * SMAX) + sizeof(int) * SMAX;
 };
 
+// blocks per SM: the static prototype-A rows (s = 18) run at 64 registers, eight blocks = 32 warps per SM
+// (config 5, 256^3: 72 -> 64 ms; six blocks 68 ms); wider rows keep their ~100 registers
+constexpr int rows_reg_min_blocks(int smax) { return smax == 18 ? 8 : 0; }   // 0: unspecified (the other instances keep their allocation)
 template <int SMAX>
-__global__ void __launch_bounds__(128) k_setup_rows_reg(RowArgs a) {
+__global__ void __launch_bounds__(128, rows_reg_min_blocks(SMAX)) k_setup_rows_reg(RowArgs a) {
     using R = RegRow<SMAX>;
     constexpr int L = R::L, RPW = R::RPW, LD = R::LD;
     extern __shared__ __align__(16) unsigned char smem[];

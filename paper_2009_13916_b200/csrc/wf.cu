@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(WF_PF_WARPS * 32, EDFA_WF_PF_BLOCKS) k_wf_pf(W
             }
         };
         // (publishing per lane, without the warp vote, measured slower: 495 / 508 vs 479 / 490 ms per step)
+        // (two staggered probes in flight per poll round measured slower too: 498 / 508 ms)
         wf_poll<K, K - WF_NEAR, K, false>(cc, xv, a.xs, a.err);
 #pragma unroll
         for (int u = K - WF_NEAR; u < K; ++u)
