@@ -221,8 +221,10 @@ __global__ void __launch_bounds__(256) k_product(ProdArgs a) {
 // the same for the F~ rows of W_m; the hash accumulation then runs from
 // shared memory in exactly k_product's order (bit-identical results).  Rows
 // that exceed the tier's capacities go to the overflow list (k_product).
+// staged F~ / A_ff entries per cell: 288 keeps a warp's working set at 9.2 KB, so three blocks (24 warps)
+// share an SM instead of two (config 5: 123 -> 90 ms; cells with more products take the next tier)
 #ifndef EDFA_PF_CAPF
-#define EDFA_PF_CAPF 512
+#define EDFA_PF_CAPF 288
 #endif
 constexpr int PF_BITS = 7, PF_T = 1 << PF_BITS, PF_CAPG = 32, PF_CAPF = EDFA_PF_CAPF, PF_CAP = 64;
 constexpr size_t PF_WARP_BYTES = (size_t)PF_T * 12 * 3 + PF_CAPG * (8 + 4 + 4) + (PF_CAPG + 1) * 4 +
