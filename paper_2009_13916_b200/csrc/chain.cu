@@ -229,8 +229,11 @@ __global__ void __launch_bounds__(256) k_chain_scan(const int* __restrict__ rows
 // then the mirrored backward scan (y_i = d_i(x_i - c_{i+1} y_{i+1})), with x
 // kept in registers (chains of at most 32*E rows).  Half the launches and no
 // HBM round trip for the intermediate vector.
+#ifndef EDFA_CHAIN_PAIR_MINB
+#define EDFA_CHAIN_PAIR_MINB 5
+#endif
 template <int E>
-__global__ void __launch_bounds__(128, E <= 9 ? 5 : 2) k_chain_pair(const int* __restrict__ rows,
+__global__ void __launch_bounds__(128, E <= 9 ? EDFA_CHAIN_PAIR_MINB : 2) k_chain_pair(const int* __restrict__ rows,
                                                     const double* __restrict__ coef, const double* __restrict__ dinv,
                                                     int n_chains, const double* b, double alpha, double* x,
                                                     const double* __restrict__ add, double* __restrict__ out2) {
