@@ -648,11 +648,14 @@ void ilu0_factor(Ctx* c, const Csr& S, double drop_tol, IluFactor& f, const int*
 // generator, per solve): the wf solve costs ~1.1 us per level while levels are
 // narrow and turns bandwidth-bound when they are wide (382 / 574 / 766 levels at
 // 128^3 / 192^3 / 256^3: 0.42 / 0.73 / 1.51 ms), the tile-DAG solve streams at
-// ~1.75 TB/s (0.40 / 0.98 / 2.23 ms): crossover at ~6k rows per level.
+// ~1.75 TB/s (0.40 / 0.98 / 2.23 ms).  With the prefetching shape (k_wf_pf) the wf solve takes 0.26 / 0.35 ms at
+// 96^3 / 128^3 against the tile solver's 0.235 / 0.40 ms, and its plan builds faster (stage 2 at 128^3: 17 vs 28 ms):
+// crossover at ~4k rows per level (96^3: 3.1k, 128^3: 5.5k).
+constexpr int64_t WF_MIN_ROWS_PER_LEVEL = 4096;
 bool use_wf_layout(Ctx* c, int n, const int* dims) {
     if (c->opt.ilu_wf >= 0) return c->opt.ilu_wf == 1 && n > 0;
     if (!dims || dims[0] <= 0) return false;
-    return (int64_t)n >= 6144ll * (dims[0] + dims[1] + dims[2]);
+    return (int64_t)n >= WF_MIN_ROWS_PER_LEVEL * (dims[0] + dims[1] + dims[2]);
 }
 
 // triangular-solve plans of an ILU factor (f.LU strict parts + f.udiag);
@@ -676,7 +679,7 @@ void ilu_plans(Ctx* c, IluFactor& f, const int* dims, bool have_fwd_levels) {
     };
     if (want_wf && c->opt.ilu_wf != 1) {
         fwd_levels();
-        want_wf = (int64_t)n >= 6144ll * f.fwd.n_levels;
+        want_wf = (int64_t)n >= WF_MIN_ROWS_PER_LEVEL * f.fwd.n_levels;
     }
     bool fwd_tile = false, bwd_tile = false;
     if (!want_wf && dims) {
